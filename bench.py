@@ -1,0 +1,408 @@
+"""Benchmark: sampled-MTTKRP nonzeros/s and ALS rounds/s of the leverage-sampled ALS hot
+path on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--sampler sts]
+    python bench.py --impl reference ...     # reference CPU implementation (oracle port)
+
+A step is one ALS round (N mode solves: sample -> weights -> sketched Gram -> sampled
+MTTKRP -> update -> renormalise -> rebuild) over the synthetic tensor of the named
+config, all inputs resident in HBM.  `value` = sampled nonzeros iterated by the MTTKRP
+(with sample multiplicity -- the reference's csr.nnz and the paper's "nonzeros iterated",
+PAPER.md:1527-1529) per second of round time, summed over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "sampled-MTTKRP nnz/s"
+UNIT = "nnz/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--sampler", default="sts", choices=["sts", "arls-lev"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-samples", type=int, default=0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def start(self):
+        def run():
+            q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "--query-gpu=" + q, "--format=csv,noheader,nounits",
+                                          "-i", str(self.index)], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._th = threading.Thread(target=run, daemon=True)
+        self._th.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=6)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ workload
+def make_tensor(cfg_name, seed, dev):
+    """Synthetic tensor of the named config on `dev` (torch tensors), reference
+    load-balancing permutation applied (ref tensor.py:207-210)."""
+    import torch
+    from paper_2210_05105_b200 import rng, synth
+    c = synth.CONFIGS[cfg_name]
+    if c["kind"] == "planted":
+        idx, vals = synth.planted_c1(seed=seed)
+        return c, torch.as_tensor(idx, device=dev), torch.as_tensor(vals, device=dev)
+    idx, vals = synth.zipf_tensor(c["dims"], c["nnz"], c["s"], seed=seed, values=c["values"],
+                                  sigma=c.get("sigma", 1.0), device=dev)
+    idx, _ = synth.permute(idx, c["dims"], seed,
+                           lambda j, d: rng.permutation(rng.stream_key(seed, rng.TENSOR_PERM, j), d))
+    return c, idx, vals
+
+
+def peaks():
+    p = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def flush_l2(buf):
+    buf.add_(1.0)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    from paper_2210_05105_b200 import _lib
+    from paper_2210_05105_b200.engine import (Cluster, LocalComm, RankState, make_local_cluster)
+    from paper_2210_05105_b200.grid import optimal_grid
+    from paper_2210_05105_b200.linalg import init_factors
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    _lib.load()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    t_setup = time.perf_counter()
+    c, idx, vals = make_tensor(args.config, args.seed, dev)
+    dims, R, J = c["dims"], c["R"], c["J"]
+    N = len(dims)
+    nnz = int(idx.shape[0])
+    if world > 1:
+        from paper_2210_05105_b200.dist import make_spmd_cluster
+        cl = make_spmd_cluster(dims, idx, vals, R, J, args.sampler, args.seed)
+    else:
+        cl = make_local_cluster(dims, idx, vals, R, J, args.sampler, args.seed)
+    del idx, vals
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    me = cl.ranks[0]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev).view(torch.float64)  # 256 MB > L2
+
+    # per-step events: whole round, and the sampled-MTTKRP calls inside it
+    mt_events = []
+    orig = me.mttkrp
+
+    def timed_mttkrp(k):
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        out = orig(k)
+        e.record()
+        mt_events.append((s, e))
+        return out
+    me.mttkrp = timed_mttkrp
+
+    rnd = 0
+    for _ in range(args.warmup):
+        rnd += 1
+        cl.round(rnd)
+    torch.cuda.synchronize()
+    mt_events.clear()
+    stats0 = me.stats.clone()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local_rank)
+    clocks.start()
+    step_ms = []
+    for _ in range(args.steps):
+        flush_l2(flush)
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        rnd += 1
+        s.record()
+        cl.round(rnd, check=False)
+        e.record()
+        e.synchronize()
+        step_ms.append(s.elapsed_time(e))
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    cl.check("in timed rounds")
+    st = (me.stats - stats0).cpu().numpy().astype(np.int64)
+    mt_ms = sum(a.elapsed_time(b) for a, b in mt_events)
+    t_total = sum(step_ms) / 1e3
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t_total, float(st[3]), float(st[2])], dtype=torch.float64, device=dev)
+        gathered = [torch.zeros_like(tt) for _ in range(world)]
+        dist.all_gather(gathered, tt)
+        t_total = max(float(g[0]) for g in gathered)
+        nnz_m = sum(float(g[1]) for g in gathered)
+        nnz_d = sum(float(g[2]) for g in gathered)
+    else:
+        nnz_m, nnz_d = float(st[3]), float(st[2])
+    K = args.steps
+    value = nnz_m / t_total
+    hbm, peak_kind = peaks()
+    # algorithmic bytes of the sampled MTTKRP:
+    #   12 nnz_d + 16 S_d + 8R S_ne + 8R rows_hit  per solve, summed over the timed solves
+    B = 12.0 * st[2] + 16.0 * st[0] + 8.0 * R * st[1] + 8.0 * R * st[4]
+    n_launch = len(mt_events)
+    achieved = (B / (mt_ms / 1e3)) / 1e9 if mt_ms > 0 else 0.0
+    e2e = measure_e2e(cl, args, rnd) if world == 1 else None
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": sum(step_ms) / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "%s %s R=%d J=%d dims=%s nnz=%d" % (args.config, args.sampler, R, J,
+                                                                 "x".join(map(str, dims)), nnz),
+                   "sampler": args.sampler, "rank": R, "samples_J": J, "modes": N,
+                   "parallelism": "as%d" % world, "l2": "256 MB flush between timed rounds "
+                   "(outside the round events); stores %.1f GB > L2" % (
+                       sum(s.bytes() for s in me.stores) / 1e9),
+                   "setup_s": round(setup_s, 1)},
+        "rounds_per_s": K / t_total,
+        "distinct_nnz_per_s": nnz_d / t_total,
+        "sampled_nnz_per_round": nnz_m / K,
+        "distinct_nnz_per_round": nnz_d / K,
+        "roofline": {"kernel": "rcp_sampled_mttkrp (dedup+lookup+transpose+segmented SpMM)",
+                     "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": B / max(n_launch, 1),
+                     "avg_launch_ms": mt_ms / max(n_launch, 1), "launches": n_launch,
+                     "share_of_step": mt_ms / max(sum(step_ms), 1e-9)},
+        "clocks": clk,
+        "gpu_launches": None,
+    }
+    if e2e is not None:
+        out["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline(args, cl, c)
+        except Exception as ex:  # reported, never fatal
+            out["cpu_baseline"] = {"value": None, "error": repr(ex)[:200]}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def measure_e2e(cl, args, rnd, steps=None):
+    """Same metric through the public host-buffer API: each step uploads the factor
+    matrices from pinned host memory, rebuilds the sampler state, runs the round and
+    reads the updated factors and sigma back (AlsSession.step_host)."""
+    import torch
+    from paper_2210_05105_b200.als import AlsSession
+    sess = AlsSession(cl)
+    host_in = sess.pinned_factors()
+    host_out = sess.pinned_factors()
+    steps = steps or max(2, args.steps)
+    me = cl.ranks[0]
+    sess.step_host(host_in, host_out, rnd + 1)
+    torch.cuda.synchronize()
+    st0 = me.stats.clone()
+    t0 = time.perf_counter()
+    for s in range(steps):
+        sess.step_host(host_in, host_out, rnd + 2 + s)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    st = (me.stats - st0).cpu().numpy()
+    return {"value": float(st[3]) / dt, "unit": UNIT,
+            "h2d_bytes_per_step": int(sum(h.numel() * 8 for h in host_in)),
+            "d2h_bytes_per_step": int(sum(h.numel() * 8 for h in host_out) + 8 * me.R),
+            "steps": steps, "ms_per_step": dt / steps * 1e3}
+
+
+# ------------------------------------------------------------------ CPU arms
+def cpu_baseline(args, cl, c, samples=None):
+    """Oracle port (numpy, oracle/) timed on this host on a bounded sample of the same
+    workload: one mode-k solve's gather + downsampled MTTKRP (the dominant CPU phase)
+    for the first `samples` draws of a real device batch of the last solved mode."""
+    import torch
+    from oracle import randcp_oracle as O
+    me = cl.ranks[0]
+    k = me.N - 1
+    samples = samples or args.cpu_samples or (2048 if c["J"] >= 2048 else c["J"])
+    st = me.stores[k]
+    # host copy of the mode-k store in the oracle's own layout (built untimed)
+    t0 = time.perf_counter()
+    ostore = oracle_store_from_device(st)
+    build_s = time.perf_counter() - t0
+    X = me.X.T.contiguous().cpu().numpy()[:samples]
+    H = me.H.cpu().numpy()[:samples]
+    w = me.w.cpu().numpy()[:samples]
+    workers = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    csr = O.sampled_csr(ostore, X, k)
+    out = O.sketched_mttkrp(csr, H, w, workers=workers)
+    dt = time.perf_counter() - t0
+    del out
+    return {"value": csr.nnz / dt, "unit": UNIT, "cores": workers, "kind": "port",
+            "sample": "oracle gather_sampled_nonzeros_to_csr + downsampled_mttkrp, mode %d of %s, "
+                      "first %d of J=%d samples of a device STS/ARLS batch; %d nnz iterated in %.2f s "
+                      "(store conversion %.1f s untimed)" % (k, args.config, samples, c["J"], csr.nnz,
+                                                             dt, build_s)}
+
+
+class _HostStore:
+    """Oracle-shaped view (skeys/col_order/idx-rows/vals) of a device store."""
+
+
+def oracle_store_from_device(st):
+    keys = st.keys.cpu().numpy()
+    colptr = st.colptr.cpu().numpy()
+    rows = st.rows.cpu().numpy().astype(np.int64) + st.row_lo
+    vals = st.vals.cpu().numpy()
+    s = _HostStore()
+    s.j = st.mode
+    s.dims = st.dims
+    s.lo = st.row_lo
+    s.hi = st.row_hi
+    s.skeys = np.repeat(keys, np.diff(colptr))
+    s.col_order = np.arange(vals.size, dtype=np.int64)
+    s.idx = np.zeros((vals.size, len(st.dims)), dtype=np.int64)
+    s.idx[:, st.mode] = rows
+    s.vals = vals
+    s.n_rows = st.row_hi - st.row_lo
+    s.find = lambda q: (np.searchsorted(s.skeys, q, side="left"),
+                        np.searchsorted(s.skeys, q, side="right"))
+    return s
+
+
+def run_reference(args):
+    """`--impl reference`: the reference's own algorithm on host cores (oracle port,
+    numpy), same config/metric; each step = one bounded solve sample."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    from oracle import randcp_oracle as O
+    from paper_2210_05105_b200 import synth
+    c = synth.CONFIGS[args.config]
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    c, idx, vals = make_tensor(args.config, args.seed, dev)   # input generation only
+    idx = idx.cpu().numpy()
+    vals = vals.cpu().numpy()
+    dims, R, J = c["dims"], c["R"], c["J"]
+    N = len(dims)
+    k = N - 1
+    samples = args.cpu_samples or min(J, 2048)
+    workers = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    store = O.Store(dims, idx, vals, k)
+    factors, _ = O.init_factors(dims, R, args.seed)
+    blocks = [[U] for U in factors]
+    grams = [O.gram_blocks(b) for b in blocks]
+    if args.sampler == "sts":
+        trees = [O.tree_build(blocks[j], [0]) for j in range(N)]
+    else:
+        levs = [O.lev_build(blocks[j], [0]) for j in range(N)]
+    setup = time.perf_counter() - t0
+    total_nnz, total_t = 0, 0.0
+    for step in range(args.warmup + args.steps):
+        ts = time.perf_counter()
+        if args.sampler == "sts":
+            cp = O.sym_pinv(O.hadamard_chain(grams, skip=k))
+            b = O.tree_sample(trees, k, samples, cp, grams, blocks, args.seed, step + 1)
+        else:
+            b = O.lev_sample(levs, k, samples, factors, args.seed, step + 1)
+        w = O.weights_for(b.prob, samples)
+        csr = O.sampled_csr(store, b.X, k)
+        out = O.sketched_mttkrp(csr, b.H, w, workers=workers)
+        Hw = b.H * w[:, None]
+        newU = out @ O.sym_pinv(Hw.T @ Hw)
+        dt = time.perf_counter() - ts
+        if step >= args.warmup:
+            total_nnz += csr.nnz
+            total_t += dt
+        del newU
+    value = total_nnz / total_t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "%s %s R=%d J=%d dims=%s" % (args.config, args.sampler, R, J,
+                                                               "x".join(map(str, dims))),
+                       "sampler": args.sampler, "rank": R, "samples_J": J,
+                       "parallelism": "host"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                             "sample": "one mode-%d solve per step restricted to the first %d of "
+                                       "J=%d samples (sampler + gather + downsampled MTTKRP + "
+                                       "solve); setup %.0f s untimed" % (k, samples, J, setup)},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

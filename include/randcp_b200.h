@@ -1,0 +1,217 @@
+/*
+ * randcp_b200.h -- C ABI of the B200-native leverage-score-sampled ALS hot path.
+ *
+ * The reference (`randcp`, pure Python/numpy, /root/reference/pkg/src/randcp) has no
+ * FFI: its boundary is the Python API called by schedules.py / als.py.  Each entry point
+ * below replaces one piece of arithmetic behind that API; the comment on each cites the
+ * reference function (file:line) it implements.  The Python package
+ * `paper_2210_05105_b200` binds these with ctypes and keeps the reference's names,
+ * signatures and exceptions.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no torch types.  All `d_*` pointers are device
+ *     pointers (cudaMalloc / torch CUDA allocations), `h_*` pointers are host memory.
+ *   - `stream` is a cudaStream_t passed as void*; every device call is stream-ordered and
+ *     asynchronous.  Nothing allocates: workspaces are caller-provided and sized by the
+ *     matching *_ws_bytes() query.
+ *   - Matrices are row-major fp64.  Sample index matrices are stored mode-major
+ *     (X[m*J + s] = mode-m row of sample s; the reference's X is (J, N), i.e. transposed).
+ *   - Return value: RCP_OK or a launch/argument error.  Data-dependent errors (zero-mass
+ *     walk, zero sampling probability, asymmetric Gram, non-finite factor) are raised on
+ *     the device into `d_status` (one int32, bitwise OR of RCP_ST_* flags) and surfaced
+ *     by the host after its next synchronisation, mapped to the reference exceptions:
+ *       RCP_ST_DEGENERATE -> DegenerateWalkError   (ref samplers.py:34-35)
+ *       RCP_ST_ZERO_PROB  -> ValueError            (ref samplers.py:93-94)
+ *       RCP_ST_ASYMMETRIC -> ValueError            (ref linalg.py:92-95)
+ *       RCP_ST_ZERO_MASS  -> ValueError            (ref samplers.py:142-143,167-168)
+ *       RCP_ST_NONFINITE  -> FloatingPointError    (ref als.py:202-204)
+ */
+#ifndef RANDCP_B200_H
+#define RANDCP_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RCP_OK 0
+#define RCP_ERR_ARG 1
+#define RCP_ERR_CUDA 2
+
+#define RCP_ST_DEGENERATE 1
+#define RCP_ST_ZERO_PROB 2
+#define RCP_ST_ASYMMETRIC 4
+#define RCP_ST_ZERO_MASS 8
+#define RCP_ST_NONFINITE 16
+#define RCP_ST_CAPACITY 32
+
+#define RCP_MAX_RANK 128
+
+/* ---------------------------------------------------------------- version / errors */
+const char *rcp_version(void);
+const char *rcp_last_error(void);
+/* Number of SMs of the current device (0 without a device). */
+int rcp_device_sms(void);
+
+/* ------------------------------------------------------------------- random streams
+ * Reference: rng.stream(seed, purpose, *context) builds
+ *   Generator(Philox(SeedSequence(entropy=seed, spawn_key=(purpose,)+context)))
+ * (ref rng.py:26-32).  These reproduce numpy 2.x's SeedSequence key derivation,
+ * Philox4x64-10 stream, Generator.random() and Generator.permutation() bit for bit. */
+
+/* key_out[2] = SeedSequence(seed, spawn_key=(purpose, ctx...)).generate_state(2, uint64). */
+int rcp_stream_key(uint64_t seed, uint64_t purpose, const uint64_t *h_ctx, int n_ctx,
+                   uint64_t *h_key_out);
+/* Host: draws [first, first+n) of Generator.random() on that key. */
+int rcp_uniform_host(const uint64_t *h_key, int64_t first, int64_t n, double *h_out);
+/* Host: Generator.permutation(n) (arange + Fisher-Yates with masked-rejection
+ * random_interval on buffered uint32 draws).  Used for the CP-ARLS-LEV SHUFFLE stream
+ * (ref samplers.py:183). */
+int rcp_permutation_host(const uint64_t *h_key, int64_t n, int64_t *h_out);
+/* Device: d_out[i] = draw (first+i) of Generator.random(). */
+int rcp_uniform(uint64_t key0, uint64_t key1, int64_t first, int64_t n, double *d_out,
+                void *stream);
+
+/* ------------------------------------------------------------- small dense algebra */
+/* G = sum_rows (s_r u_r)(s_r u_r)^T for U (n x R); d_scale may be NULL (s_r = 1).
+ * Deterministic (fixed CTA partition + ordered reduction).
+ * Ref: gram() linalg.py:64-70; sketched Gram (H.w)^T(H.w) schedules.py:104-109. */
+size_t rcp_gram_ws_bytes(int64_t n, int R);
+int rcp_gram(const double *d_U, const double *d_scale, int64_t n, int R, double *d_G,
+             void *d_ws, void *stream);
+
+/* Moore-Penrose inverse of a symmetric PSD R x R matrix with eigenvalue cutoff
+ * rel_cutoff * lambda_max (ref pseudo_inverse linalg.py:85-104): symmetry check
+ * (RCP_ST_ASYMMETRIC), then a Cholesky inverse when its Frobenius condition bound
+ * proves every eigenvalue is above the cutoff, else a parallel cyclic Jacobi
+ * eigendecomposition with the reference's cutoff rule.  One CTA.
+ * If n_chain > 0, the input is first formed as the Hadamard product of the n_chain
+ * R x R matrices d_in[m*R*R] skipping index `skip` (ref hadamard_gram_chain
+ * linalg.py:73-82); d_chain_out (nullable) receives that product. */
+int rcp_pinv(const double *d_in, int n_chain, int skip, int R, double rel_cutoff,
+             double *d_chain_out, double *d_out, int *d_status, void *stream);
+
+/* U_out (n x R) = M (n x R) @ B (R x R); also accumulates per-column sums of squares of
+ * U_out into d_colsq (R, caller-zeroed, via ordered per-CTA partials in d_ws) and flags
+ * non-finite entries (RCP_ST_NONFINITE).  Ref: _postprocess schedules.py:124-128 and
+ * the finite check als.py:202-204. */
+size_t rcp_update_ws_bytes(int64_t n, int R);
+int rcp_update(const double *d_M, int64_t n, int R, const double *d_B, double *d_U_out,
+               double *d_colsq, void *d_ws, int *d_status, void *stream);
+/* sigma = sqrt(colsq); U /= (sigma > 0 ? sigma : 1) in place (ref _renormalize
+ * als.py:129-138). */
+int rcp_renormalize(double *d_U, int64_t n, int R, const double *d_colsq, double *d_sigma,
+                    void *stream);
+
+/* ------------------------------------------------------------ CP-ARLS-LEV sampler
+ * Ref: arls_lev_build samplers.py:122-135, arls_lev_sample samplers.py:148-191. */
+/* d_lev[q] = max(u_q Gp u_q^T, 0); d_dist = d_lev / C (C = sum, ordered), d_cdf =
+ * inclusive scan of d_dist normalised by its last element (numpy choice semantics);
+ * d_mass[0] = C. */
+size_t rcp_arls_build_ws_bytes(int64_t n, int R);
+int rcp_arls_build(const double *d_U, int64_t n, int R, const double *d_Gp, double *d_dist,
+                   double *d_cdf, double *d_mass, void *d_ws, void *stream);
+/* q draws from one rank's distribution with stream key (LOCAL_DRAW): row = row_lo +
+ * searchsorted(cdf, u, 'right'); prob = (C_p / W) * dist[row].  Writes into
+ * d_rows_out/d_prob_out at [offset, offset+q).  d_total_mass (nullable, device scalar):
+ * RCP_ST_ZERO_MASS is raised when it is <= 0 (ref samplers.py:166-168).
+ * d_urow_out (nullable): also copies the drawn factor rows U[row - row_lo] (q x R). */
+int rcp_arls_draw(const double *d_cdf, const double *d_dist, int64_t n, int64_t row_lo,
+                  double mass_ratio, const double *d_total_mass, uint64_t key0, uint64_t key1,
+                  int64_t q, int64_t offset, int64_t *d_rows_out, double *d_prob_out,
+                  const double *d_U, int R, double *d_urow_out, int *d_status, void *stream);
+/* Apply the SHUFFLE permutation and fold mode i into the batch:
+ * X_i[s] = rows[perm[s]], pmp_i[s] = prob[perm[s]], H[s,:] (*)= row(perm[s]) where
+ * row(t) = d_urows[t,:] when d_urows != NULL, else U[rows[t] - u_row_lo, :].
+ * d_perm may be NULL (identity).  `first` != 0 assigns H instead of multiplying. */
+int rcp_batch_fold(const int64_t *d_perm, const int64_t *d_rows, const double *d_prob,
+                   int64_t J, const double *d_U, int64_t u_row_lo, const double *d_urows,
+                   int R, int first, int64_t *d_Xi, double *d_pmp_i, double *d_H,
+                   void *stream);
+
+/* ------------------------------------------------------------------ STS-CP sampler
+ * Ref: sts_build samplers.py:224-288, sts_sample samplers.py:379-468.
+ * Device layout: complete binary tree over leaf blocks of `leaf` consecutive rows; level
+ * l holds 2^l node Grams, each packed upper-triangular (R(R+1)/2 doubles, row-major);
+ * node (l, v) lives at offset ((1<<l) - 1 + v) * R(R+1)/2.  depth = ceil(log2(n_leaves)). */
+int rcp_sts_depth(int64_t n, int leaf);
+size_t rcp_sts_tree_doubles(int64_t n, int leaf, int R);
+/* Conditioning matrix of constant mode i in a mode-k solve:
+ * M = chain_pinv (.) prod_{m>i, m!=k} G_m, left fold in mode order (ref samplers.py:412-415).
+ * d_grams: N stacked R x R Grams. */
+int rcp_sts_cond(const double *d_chain_pinv, const double *d_grams, int N, int i, int k, int R,
+                 double *d_M, void *stream);
+/* Shared (rank-level) levels of the walk for P > 1 (ref samplers.py:423-451): node Grams
+ * of the padded rank tree, full R x R each, level-major (level l at offset (2^l-1)*R*R);
+ * leaf_rank[2^depth] maps tree leaves to ranks (-1 = padding).  Writes owner rank, the
+ * rescaled residual and the product of step probabilities; RCP_ST_DEGENERATE on a
+ * zero-mass node or a branch into an empty padded subtree. */
+int rcp_sts_rank_walk(const double *d_node_grams, int depth, int P, const int32_t *d_leaf_rank,
+                      const double *d_M, const double *d_H, int64_t J, int R, uint64_t key0,
+                      uint64_t key1, const double *d_override, int32_t *d_owner,
+                      double *d_r_out, double *d_pmp_i, int *d_status, void *stream);
+int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
+                  void *stream);
+/* Walk J samples down the tree of one factor block (rows global [row_lo, row_lo+n)).
+ * M = conditioning matrix (R x R, full) for this mode (ref samplers.py:412-415).
+ * Uniforms: d_override (J doubles, nullable) else WALK_UNIFORM draws of key (key0,key1).
+ * d_sel (nullable): only samples s with d_sel[s] == sel_value walk (multi-rank owner).
+ * Outputs: d_Xi[s] (global row), d_pmp_i[s] *= step probabilities (caller initialises to
+ * the probability so far, 1 for single-rank), d_resid[s]; H[s,:] *= U[row].
+ * d_rin (nullable) supplies starting residuals instead of fresh uniforms. */
+int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
+                 int64_t row_lo, const double *d_M, const double *d_H_in, int64_t J,
+                 uint64_t key0, uint64_t key1, const double *d_override, const double *d_rin,
+                 const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi, double *d_pmp_i,
+                 double *d_resid, double *d_urow_out, int *d_status, void *stream);
+/* H[s,:] *= d_urow[s,:] for all s (fold walked rows into the running Hadamard rows). */
+int rcp_hadamard_rows(double *d_H, const double *d_urow, int64_t J, int R, int init_ones,
+                      void *stream);
+/* Sample weights w = 1/sqrt(J * prod_m pmp[m]) (ref sample_weights samplers.py:89-96),
+ * also writes prob = prod_m pmp[m] (ref samplers.py:466); RCP_ST_ZERO_PROB if prob<=0. */
+int rcp_weights(const double *d_pmp, int N, int64_t J, double *d_prob, double *d_w,
+                int *d_status, void *stream);
+
+/* ------------------------------------------------------------- sampled MTTKRP
+ * Per-mode sorted store (ref Matricization matricization.py:67-128), device layout:
+ *   keys[n_cols]     int64  distinct column keys (off-mode mixed-radix, ascending)
+ *   colptr[n_cols+1] int64  nonzeros of column c at [colptr[c], colptr[c+1])
+ *   rows[nnz]        int32  local row (global row - row_lo), ascending within a column
+ *   vals[nnz]        fp64
+ * Downsampled MTTKRP of one mode solve (ref gather_sampled_nonzeros_to_csr
+ * mttkrp.py:131-155 + downsampled_mttkrp mttkrp.py:158-189, fused):
+ *   out[i,:] = sum_s w_s^2 * T(i, col(s)) * H[s,:]
+ * Samples with equal column keys are merged (count * w^2, identical H rows), then the
+ * distinct fibers are looked up, transposed to row order and segment-reduced.
+ * d_stats (int64[8], accumulated): [0] distinct samples, [1] distinct samples with >=1
+ * local nonzero, [2] gathered nonzeros (distinct fibers), [3] gathered nonzeros with
+ * multiplicity (the reference's csr.nnz), [4] output rows hit; [5..7] reserved. */
+size_t rcp_mttkrp_ws_bytes(int64_t J, int64_t store_nnz, int64_t n_rows, int R);
+int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n_cols,
+                       const int32_t *d_rows, const double *d_vals, int64_t n_rows,
+                       const int64_t *d_X, int N, int64_t J, int k, const int64_t *h_strides,
+                       const double *d_H, const double *d_w, int R, double *d_out,
+                       int64_t *d_stats, void *d_ws, size_t ws_bytes, int *d_status,
+                       void *stream);
+/* Reference-shaped CSR gather with multiplicity (drop-in for
+ * gather_sampled_nonzeros_to_csr): d_counts[s] = fiber length of sample s, and, when
+ * d_pos_out != NULL, expanded (row, sample, value) triples in sample order (row-sorting
+ * is done by the caller). */
+int rcp_fiber_lookup(const int64_t *d_keys, int64_t n_cols, const int64_t *d_colptr,
+                     const int64_t *d_X, int N, int64_t J, int k, const int64_t *h_strides,
+                     int64_t *d_lo, int64_t *d_counts, void *stream);
+int rcp_fiber_expand(const int64_t *d_lo, const int64_t *d_off, int64_t J,
+                     const int32_t *d_rows, const double *d_vals, int64_t *d_row_out,
+                     int64_t *d_col_out, double *d_val_out, void *stream);
+/* CSR SpMM: out[i,:] = sum_{e in row i} val[e] * scale[col[e]] * H[col[e],:]
+ * (drop-in for downsampled_mttkrp with scale = w^2; ref mttkrp.py:158-189). */
+int rcp_csr_spmm(const int64_t *d_row_ptr, int64_t n_rows, const int64_t *d_col,
+                 const double *d_val, const double *d_H, const double *d_scale, int R,
+                 double *d_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RANDCP_B200_H */

@@ -1,0 +1,580 @@
+// Small dense fp64 algebra on the hot path: Gram matrices, the R x R pseudo-inverse,
+// the factor update GEMM with its column norms, renormalisation, sample weights.
+// Ref: linalg.py:64-111, schedules.py:104-128, samplers.py:89-96, als.py:129-138.
+#include "common.cuh"
+
+using namespace rcp;
+
+namespace {
+
+int g_sms = 0;
+int sm_count() {
+  if (!g_sms) {
+    g_sms = rcp_device_sms();
+    if (!g_sms) g_sms = 148;
+  }
+  return g_sms;
+}
+
+// ------------------------------------------------------------------------------ Gram
+constexpr int kGramRows = 32;      // rows staged per tile
+constexpr int kGramThreads = 256;
+constexpr int kGramMaxPairs = 3;   // (R/4)(R/4+1)/2 <= 3*256 for R <= 128
+
+int gram_grid(int64_t n) {
+  int64_t tiles = ceil_div(n, kGramRows);
+  int64_t g = 2LL * sm_count();
+  if (tiles < g) g = tiles;
+  return (int)(g < 1 ? 1 : g);
+}
+
+__global__ void __launch_bounds__(kGramThreads)
+gram_partial_kernel(const double *__restrict__ U, const double *__restrict__ scale, int64_t n,
+                    int R, double *__restrict__ part) {
+  extern __shared__ double sh[];
+  const int nT = (R + 3) / 4;
+  const int RP = nT * 4;
+  double *tile = sh;  // kGramRows x RP
+  const int npairs = nT * (nT + 1) / 2;
+  int pa[kGramMaxPairs], pb[kGramMaxPairs];
+  double acc[kGramMaxPairs][4][4];
+#pragma unroll
+  for (int p = 0; p < kGramMaxPairs; ++p) {
+    int id = threadIdx.x + p * kGramThreads;
+    pa[p] = -1;
+    pb[p] = -1;
+    if (id < npairs) {  // decode upper-triangular tile pair (ta <= tb)
+      int ta = 0, rem = id;
+      while (rem >= nT - ta) {
+        rem -= nT - ta;
+        ++ta;
+      }
+      pa[p] = ta;
+      pb[p] = ta + rem;
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[p][x][y] = 0.0;
+  }
+  const int64_t ntiles = ceil_div(n, kGramRows);
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t r0 = t * kGramRows;
+    __syncthreads();
+    for (int e = threadIdx.x; e < kGramRows * RP; e += blockDim.x) {
+      int rr = e / RP, c = e % RP;
+      int64_t row = r0 + rr;
+      double v = 0.0;
+      if (row < n && c < R) {
+        v = U[row * R + c];
+        if (scale) v *= scale[row];
+      }
+      tile[e] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < kGramMaxPairs; ++p) {
+      if (pa[p] < 0) continue;
+      const int a0 = pa[p] * 4, b0 = pb[p] * 4;
+      for (int rr = 0; rr < kGramRows; ++rr) {
+        const double *row = tile + rr * RP;
+        double av[4], bv[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          av[x] = row[a0 + x];
+          bv[x] = row[b0 + x];
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[p][x][y] = fma(av[x], bv[y], acc[p][x][y]);
+      }
+    }
+  }
+  double *out = part + (int64_t)blockIdx.x * R * R;
+#pragma unroll
+  for (int p = 0; p < kGramMaxPairs; ++p) {
+    if (pa[p] < 0) continue;
+    const int a0 = pa[p] * 4, b0 = pb[p] * 4;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        int a = a0 + x, b = b0 + y;
+        if (a < R && b < R) {
+          out[a * R + b] = acc[p][x][y];
+          out[b * R + a] = acc[p][x][y];
+        }
+      }
+  }
+}
+
+__global__ void sum_partials_kernel(const double *__restrict__ part, int nparts, int64_t len,
+                                    double *__restrict__ out) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= len) return;
+  double s = 0.0;
+  for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * len + e];
+  out[e] = s;
+}
+
+// --------------------------------------------------------------------------- pinv
+constexpr int kPinvThreads = 512;
+
+__device__ double block_reduce(double v, double *red, bool is_max) {
+  // all threads participate; result broadcast
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmax(v, w) : v + w;
+  }
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    int nw = blockDim.x >> 5;
+    v = lane < nw ? red[lane] : (is_max ? -1.0 / 0.0 : 0.0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = is_max ? fmax(v, w) : v + w;
+    }
+    if (lane == 0) red[32] = v;
+  }
+  __syncthreads();
+  double r = red[32];
+  __syncthreads();
+  return r;
+}
+
+// Load (chain of) input into A (stride LD), symmetric check; returns false if asymmetric.
+__device__ void load_input(const double *in, int n_chain, int skip, int R, int LD, double *A,
+                           double *chain_out) {
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    double v;
+    if (n_chain <= 0) {
+      v = in[e];
+    } else {
+      bool have = false;
+      v = 0.0;
+      for (int m = 0; m < n_chain; ++m) {
+        if (m == skip) continue;
+        double g = in[(int64_t)m * R * R + e];
+        v = have ? v * g : g;
+        have = true;
+      }
+    }
+    A[(e / R) * LD + (e % R)] = v;
+    if (chain_out) chain_out[e] = v;
+  }
+}
+
+__global__ void __launch_bounds__(kPinvThreads)
+pinv_kernel(const double *__restrict__ in, int n_chain, int skip, int R, double cutoff,
+            double *__restrict__ chain_out, double *__restrict__ out, int *status) {
+  extern __shared__ double sh[];
+  const int LD = R + 1;
+  double *A = sh;                       // R x LD
+  double *red = A + R * LD;             // 33
+  double *diag = red + 40;              // R (eigenvalues)
+  double *cs = diag + R + 1;            // R/2+1 cosines
+  double *sn = cs + (R / 2 + 2);        // sines
+  int *pr = reinterpret_cast<int *>(sn + (R / 2 + 2));  // pairs (2*(R/2+1))
+  __shared__ int flag;
+
+  load_input(in, n_chain, skip, R, LD, A, chain_out);
+  __syncthreads();
+  // symmetry check on the raw input (ref linalg.py:92-95)
+  double mx = 0.0, asym = 0.0;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    int a = e / R, b = e % R;
+    mx = fmax(mx, fabs(A[a * LD + b]));
+    asym = fmax(asym, fabs(A[a * LD + b] - A[b * LD + a]));
+  }
+  mx = block_reduce(mx, red, true);
+  asym = block_reduce(asym, red, true);
+  if (asym > 1e-8 * fmax(mx, 1.0)) {
+    if (threadIdx.x == 0) raise_status(status, RCP_ST_ASYMMETRIC);
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) out[e] = 0.0;
+    return;
+  }
+  // symmetrise: S = (G + G^T)/2 (upper triangle computed once, mirrored)
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    int a = e / R, b = e % R;
+    if (a < b) {
+      double s = 0.5 * (A[a * LD + b] + A[b * LD + a]);
+      A[a * LD + b] = s;
+      A[b * LD + a] = s;
+    }
+  }
+  __syncthreads();
+  double fro = 0.0;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    double v = A[(e / R) * LD + (e % R)];
+    fro += v * v;
+  }
+  fro = sqrt(block_reduce(fro, red, false));
+
+  // ---- fast path: in-place Gauss-Jordan inverse (no pivoting; valid for SPD) ----
+  if (threadIdx.x == 0) flag = (fro > 0.0) ? 1 : 0;
+  __syncthreads();
+  for (int k = 0; k < R && flag; ++k) {
+    const double pk = A[k * LD + k];
+    if (!(pk > 0.0)) {  // not positive definite (or NaN): fall back
+      __syncthreads();
+      if (threadIdx.x == 0) flag = 0;
+      __syncthreads();
+      break;
+    }
+    for (int j = threadIdx.x; j < R; j += blockDim.x)
+      if (j != k) A[k * LD + j] /= pk;
+    __syncthreads();
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      int i = e / R, j = e % R;
+      if (i != k && j != k) A[i * LD + j] -= A[i * LD + k] * A[k * LD + j];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < R; i += blockDim.x) {
+      if (i != k) A[i * LD + k] = -A[i * LD + k] / pk;
+    }
+    if (threadIdx.x == 0) A[k * LD + k] = 1.0 / pk;
+    __syncthreads();
+  }
+  if (flag) {
+    double ifro = 0.0;
+    bool finite = true;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      double v = A[(e / R) * LD + (e % R)];
+      ifro += v * v;
+      if (!isfinite(v)) finite = false;
+    }
+    double bad = block_reduce(finite ? 0.0 : 1.0, red, true);
+    ifro = sqrt(block_reduce(ifro, red, false));
+    // kappa_2 <= ||S||_F ||S^-1||_F ; below 1e8 every eigenvalue clears 1e-10 * lambda_max
+    if (bad == 0.0 && fro * ifro < 1e8 && cutoff <= 1e-9) {
+      for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+        int a = e / R, b = e % R;
+        out[e] = 0.5 * (A[a * LD + b] + A[b * LD + a]);
+      }
+      return;
+    }
+  }
+  // ---- robust path: parallel cyclic Jacobi eigendecomposition, reference cutoff ----
+  __syncthreads();
+  load_input(in, n_chain, skip, R, LD, A, nullptr);
+  __syncthreads();
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    int a = e / R, b = e % R;
+    if (a < b) {
+      double s = 0.5 * (A[a * LD + b] + A[b * LD + a]);
+      A[a * LD + b] = s;
+      A[b * LD + a] = s;
+    }
+  }
+  double *Vt = out;  // eigenvectors as rows, kept in global scratch
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Vt[e] = (e / R == e % R) ? 1.0 : 0.0;
+  __syncthreads();
+  const int m = (R + 1) & ~1;  // even count with a dummy index R when R is odd
+  const int half = m / 2;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    double off = 0.0, dg = 0.0;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      int a = e / R, b = e % R;
+      double v = A[a * LD + b];
+      if (a != b) off += v * v; else dg += v * v;
+    }
+    off = block_reduce(off, red, false);
+    dg = block_reduce(dg, red, false);
+    if (off <= 1e-32 * dg || off == 0.0) break;
+    for (int step = 0; step < m - 1; ++step) {
+      // round-robin pairing: slot 0 fixed, others rotate by `step`
+      for (int i = threadIdx.x; i < half; i += blockDim.x) {
+        int s1 = i, s2 = m - 1 - i;
+        auto who = [&](int slot) { return slot == 0 ? 0 : 1 + (slot - 1 + step) % (m - 1); };
+        int p = who(s1), q = who(s2);
+        if (p > q) { int t = p; p = q; q = t; }
+        double c = 1.0, s = 0.0;
+        if (q < R) {
+          double apq = A[p * LD + q];
+          if (apq != 0.0) {
+            double th = (A[q * LD + q] - A[p * LD + p]) / (2.0 * apq);
+            double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+          }
+        }
+        cs[i] = c;
+        sn[i] = s;
+        pr[2 * i] = p;
+        pr[2 * i + 1] = q;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < half * R; e += blockDim.x) {  // rows: A <- J^T A ; Vt
+        int i = e / R, j = e % R;
+        int p = pr[2 * i], q = pr[2 * i + 1];
+        if (q >= R || sn[i] == 0.0) continue;
+        double c = cs[i], s = sn[i];
+        double ap = A[p * LD + j], aq = A[q * LD + j];
+        A[p * LD + j] = c * ap - s * aq;
+        A[q * LD + j] = s * ap + c * aq;
+        double vp = Vt[p * R + j], vq = Vt[q * R + j];
+        Vt[p * R + j] = c * vp - s * vq;
+        Vt[q * R + j] = s * vp + c * vq;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < half * R; e += blockDim.x) {  // cols: A <- A J
+        int i = e / R, j = e % R;
+        int p = pr[2 * i], q = pr[2 * i + 1];
+        if (q >= R || sn[i] == 0.0) continue;
+        double c = cs[i], s = sn[i];
+        double ap = A[j * LD + p], aq = A[j * LD + q];
+        A[j * LD + p] = c * ap - s * aq;
+        A[j * LD + q] = s * ap + c * aq;
+      }
+      __syncthreads();
+    }
+  }
+  for (int a = threadIdx.x; a < R; a += blockDim.x) diag[a] = A[a * LD + a];
+  __syncthreads();
+  double lmax = -1.0 / 0.0;
+  for (int a = threadIdx.x; a < R; a += blockDim.x) lmax = fmax(lmax, diag[a]);
+  lmax = block_reduce(lmax, red, true);
+  // reuse A for Vt (global -> shared) before overwriting `out`
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) A[(e / R) * LD + (e % R)] = Vt[e];
+  __syncthreads();
+  for (int a = threadIdx.x; a < R; a += blockDim.x) {
+    double w = diag[a];
+    diag[a] = (lmax > 0.0 && w > cutoff * lmax) ? 1.0 / (w > 0.0 ? w : 1.0) : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    int a = e / R, b = e % R;
+    double s = 0.0;
+    for (int t = 0; t < R; ++t) s += A[t * LD + a] * diag[t] * A[t * LD + b];
+    out[e] = s;
+  }
+}
+
+// ------------------------------------------------------------------- update GEMM
+constexpr int kUpdThreads = 256;
+
+template <int RPL>
+__global__ void __launch_bounds__(kUpdThreads)
+update_kernel(const double *__restrict__ M, int64_t n, int R, const double *__restrict__ B,
+              double *__restrict__ U, double *__restrict__ part, int *status) {
+  extern __shared__ double sh[];
+  double *Bs = sh;  // R x R
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Bs[e] = B[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double sq[RPL];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < RPL; ++j) sq[j] = 0.0;
+  for (int64_t row = (int64_t)blockIdx.x * nw + wid; row < n; row += (int64_t)gridDim.x * nw) {
+    double mv[RPL], acc[RPL];
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+      int c = lane + 32 * j;
+      mv[j] = c < R ? M[row * R + c] : 0.0;
+      acc[j] = 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+      const int amax = min(32, R - 32 * j);
+      for (int t = 0; t < amax; ++t) {
+        double ma = __shfl_sync(0xffffffffu, mv[j], t);
+        const double *brow = Bs + (32 * j + t) * R;
+#pragma unroll
+        for (int jj = 0; jj < RPL; ++jj) {
+          int c = lane + 32 * jj;
+          if (c < R) acc[jj] = fma(ma, brow[c], acc[jj]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+      int c = lane + 32 * j;
+      if (c < R) {
+        U[row * R + c] = acc[j];
+        sq[j] += acc[j] * acc[j];
+        if (!isfinite(acc[j])) bad = true;
+      }
+    }
+  }
+  if (bad) raise_status(status, RCP_ST_NONFINITE);
+  // per-CTA column partials in fixed warp order (deterministic)
+  __syncthreads();
+  double *wsq = sh;  // reuse: nw x R
+#pragma unroll
+  for (int j = 0; j < RPL; ++j) {
+    int c = lane + 32 * j;
+    if (c < R) wsq[wid * R + c] = sq[j];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < R; c += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += wsq[w * R + c];
+    part[(int64_t)blockIdx.x * R + c] = s;
+  }
+}
+
+__global__ void renorm_kernel(double *__restrict__ U, int64_t n, int R,
+                              const double *__restrict__ colsq, double *__restrict__ sigma) {
+  extern __shared__ double nrm[];
+  for (int c = threadIdx.x; c < R; c += blockDim.x) {
+    double s = sqrt(colsq[c]);
+    nrm[c] = s > 0.0 ? s : 1.0;
+    if (blockIdx.x == 0 && sigma) sigma[c] = s;
+  }
+  __syncthreads();
+  int64_t tot = n * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x)
+    U[e] /= nrm[e % R];
+}
+
+__global__ void weights_kernel(const double *__restrict__ pmp, int N, int64_t J,
+                               double *__restrict__ prob, double *__restrict__ w, int *status) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= J) return;
+  double p = pmp[s];
+  for (int m = 1; m < N; ++m) p *= pmp[(int64_t)m * J + s];
+  if (prob) prob[s] = p;
+  if (!(p > 0.0)) raise_status(status, RCP_ST_ZERO_PROB);
+  w[s] = 1.0 / sqrt((double)J * p);
+}
+
+__global__ void hadamard_rows_kernel(double *__restrict__ H, const double *__restrict__ urow,
+                                     int64_t tot, int init) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x)
+    H[e] = init ? urow[e] : H[e] * urow[e];
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t rcp_gram_ws_bytes(int64_t n, int R) {
+  return (size_t)gram_grid(n) * R * R * sizeof(double);
+}
+
+int rcp_gram(const double *d_U, const double *d_scale, int64_t n, int R, double *d_G,
+             void *d_ws, void *stream) {
+  if (R < 1 || R > RCP_MAX_RANK || n < 0 || !d_G || (n > 0 && (!d_U || !d_ws)))
+    return RCP_ERR_ARG;
+  cudaStream_t st = RCP_STREAM(stream);
+  if (n == 0) {
+    RCP_CUDA_TRY(cudaMemsetAsync(d_G, 0, sizeof(double) * R * R, st));
+    return RCP_OK;
+  }
+  const int grid = gram_grid(n);
+  const int RP = ((R + 3) / 4) * 4;
+  size_t smem = sizeof(double) * kGramRows * RP;
+  gram_partial_kernel<<<grid, kGramThreads, smem, st>>>(d_U, d_scale, n, R, (double *)d_ws);
+  RCP_LAUNCH_CHECK("gram_partial");
+  int64_t len = (int64_t)R * R;
+  sum_partials_kernel<<<(unsigned)ceil_div(len, 256), 256, 0, st>>>((double *)d_ws, grid, len,
+                                                                     d_G);
+  RCP_LAUNCH_CHECK("gram_reduce");
+  return RCP_OK;
+}
+
+int rcp_pinv(const double *d_in, int n_chain, int skip, int R, double rel_cutoff,
+             double *d_chain_out, double *d_out, int *d_status, void *stream) {
+  if (R < 1 || R > RCP_MAX_RANK || !d_in || !d_out) return RCP_ERR_ARG;
+  size_t smem = sizeof(double) * ((size_t)R * (R + 1) + 40 + (R + 1) + 2 * (R / 2 + 2)) +
+                sizeof(int) * (2 * (R / 2 + 2)) + 64;
+  static bool attr = false;
+  if (!attr) {
+    RCP_CUDA_TRY(cudaFuncSetAttribute(pinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+    attr = true;
+  }
+  pinv_kernel<<<1, kPinvThreads, smem, RCP_STREAM(stream)>>>(d_in, n_chain, skip, R, rel_cutoff,
+                                                            d_chain_out, d_out, d_status);
+  RCP_LAUNCH_CHECK("pinv");
+  return RCP_OK;
+}
+
+size_t rcp_update_ws_bytes(int64_t n, int R) {
+  (void)n;
+  return (size_t)4 * sm_count() * R * sizeof(double);
+}
+
+int rcp_update(const double *d_M, int64_t n, int R, const double *d_B, double *d_U_out,
+               double *d_colsq, void *d_ws, int *d_status, void *stream) {
+  if (R < 1 || R > RCP_MAX_RANK || n < 0 || !d_B || !d_colsq || (n > 0 && (!d_M || !d_U_out)))
+    return RCP_ERR_ARG;
+  cudaStream_t st = RCP_STREAM(stream);
+  if (n == 0) {
+    RCP_CUDA_TRY(cudaMemsetAsync(d_colsq, 0, sizeof(double) * R, st));
+    return RCP_OK;
+  }
+  const int nw = kUpdThreads / 32;
+  int64_t want = ceil_div(n, nw);
+  int grid = (int)(want < 4LL * sm_count() ? want : 4LL * sm_count());
+  size_t smem = sizeof(double) * (size_t)((R * R > nw * R) ? R * R : nw * R);
+  static bool attr = false;
+  if (!attr) {
+    RCP_CUDA_TRY(cudaFuncSetAttribute(update_kernel<1>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
+    RCP_CUDA_TRY(cudaFuncSetAttribute(update_kernel<2>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
+    RCP_CUDA_TRY(cudaFuncSetAttribute(update_kernel<3>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
+    RCP_CUDA_TRY(cudaFuncSetAttribute(update_kernel<4>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
+    attr = true;
+  }
+  double *part = (double *)d_ws;
+  switch ((R + 31) / 32) {
+    case 1: update_kernel<1><<<grid, kUpdThreads, smem, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+    case 2: update_kernel<2><<<grid, kUpdThreads, smem, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+    case 3: update_kernel<3><<<grid, kUpdThreads, smem, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+    default: update_kernel<4><<<grid, kUpdThreads, smem, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+  }
+  RCP_LAUNCH_CHECK("update");
+  sum_partials_kernel<<<(unsigned)ceil_div(R, 128), 128, 0, st>>>(part, grid, R, d_colsq);
+  RCP_LAUNCH_CHECK("update_colsq");
+  return RCP_OK;
+}
+
+int rcp_renormalize(double *d_U, int64_t n, int R, const double *d_colsq, double *d_sigma,
+                    void *stream) {
+  if (R < 1 || R > RCP_MAX_RANK || n < 0 || !d_colsq) return RCP_ERR_ARG;
+  int64_t tot = n * R;
+  int64_t blocks = ceil_div(tot > 0 ? tot : 1, 256);
+  if (blocks > 8LL * sm_count()) blocks = 8LL * sm_count();
+  renorm_kernel<<<(unsigned)blocks, 256, sizeof(double) * R, RCP_STREAM(stream)>>>(d_U, n, R,
+                                                                                  d_colsq, d_sigma);
+  RCP_LAUNCH_CHECK("renormalize");
+  return RCP_OK;
+}
+
+int rcp_weights(const double *d_pmp, int N, int64_t J, double *d_prob, double *d_w,
+                int *d_status, void *stream) {
+  if (N < 1 || J < 0 || (J > 0 && (!d_pmp || !d_w))) return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  weights_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, RCP_STREAM(stream)>>>(d_pmp, N, J, d_prob,
+                                                                             d_w, d_status);
+  RCP_LAUNCH_CHECK("weights");
+  return RCP_OK;
+}
+
+int rcp_hadamard_rows(double *d_H, const double *d_urow, int64_t J, int R, int init_ones,
+                      void *stream) {
+  if (J < 0 || R < 1) return RCP_ERR_ARG;
+  int64_t tot = J * R;
+  if (tot == 0) return RCP_OK;
+  int64_t blocks = ceil_div(tot, 256);
+  if (blocks > 8LL * sm_count()) blocks = 8LL * sm_count();
+  hadamard_rows_kernel<<<(unsigned)blocks, 256, 0, RCP_STREAM(stream)>>>(d_H, d_urow, tot,
+                                                                         init_ones);
+  RCP_LAUNCH_CHECK("hadamard_rows");
+  return RCP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,642 @@
+// Sampled (downsampled) MTTKRP for one mode solve, device-resident and free of host
+// synchronisation (all sizes stay on the device, so a whole ALS round can be captured in
+// a CUDA graph).  Ref: gather_sampled_nonzeros_to_csr mttkrp.py:131-155 and
+// downsampled_mttkrp mttkrp.py:158-189 (with _row_blocks/_accumulate_rows :31-62).
+//
+// Pipeline (per solve, per rank):
+//  1. column key of every sample; hash-dedup -> distinct fibers d with multiplicity c_d
+//     and representative sample (smallest id);                       [dedup]
+//  2. binary search of each distinct key in the mode's sorted store -> [lo_d, lo_d+len_d);
+//     scaled KRP row Hs_d = c_d w^2 H[rep_d,:];                      [lookup]
+//  3. exclusive scan of len_d -> gathered-entry offsets;            [scan]
+//  4. row histogram of the gathered entries (CTA-private in shared memory when the
+//     block's row count fits, one global atomic per (CTA,row));   [row count + scan]
+//  5. scatter entries (fiber id, value) into row order (the "sparse transpose" the
+//     paper uses instead of atomics);            [scatter]
+//  6. warp-per-chunk segmented reduction out[i,:] = sum val * Hs_d, plain stores for rows
+//     owned by one warp, fp64 red.add only for rows split across chunks.   [spmm]
+#include <limits.h>
+
+#include "common.cuh"
+#include "scan.cuh"
+
+using namespace rcp;
+
+namespace {
+
+int sm_count() {
+  static int s = 0;
+  if (!s) {
+    s = rcp_device_sms();
+    if (!s) s = 148;
+  }
+  return s;
+}
+
+constexpr int kMaxModes = 8;
+constexpr int kPrivRows = 40960;   // CTA-private row histogram limit (int32 in smem)
+constexpr int kTileE = 2048;       // entries per traversal tile
+constexpr int kMinRange = 8192;    // min entries per CTA in the histogram/scatter passes
+constexpr int kSpmmChunk = 256;    // entries per warp in the segmented reduction
+
+struct Strides {
+  int64_t s[kMaxModes];
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ int64_t sample_key(const int64_t *__restrict__ X, int N, int64_t J,
+                                              int k, const Strides &st, int64_t s) {
+  int64_t key = 0;
+  for (int m = 0; m < N; ++m)
+    if (m != k) key += X[(int64_t)m * J + s] * st.s[m];
+  return key;
+}
+
+__device__ __forceinline__ int64_t lower_bound_i64(const int64_t *__restrict__ a, int64_t n,
+                                                   int64_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// largest i in [0, n) with a[i] <= x  (a nondecreasing, a[0] <= x)
+__device__ __forceinline__ int64_t floor_index(const int64_t *__restrict__ a, int64_t n, int64_t x) {
+  int64_t lo = 0, hi = n;
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------------------- dedup
+__global__ void hash_insert_kernel(const int64_t *__restrict__ X, int N, int64_t J, int k,
+                                   Strides st, int64_t tmask, unsigned long long *tkey,
+                                   int32_t *tcnt, int32_t *trep) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= J) return;
+  const int64_t key = sample_key(X, N, J, k, st, s);
+  uint64_t h = mix64((uint64_t)key) & (uint64_t)tmask;
+  while (true) {
+    unsigned long long prev = atomicCAS(&tkey[h], ~0ull, (unsigned long long)key);
+    if (prev == ~0ull || prev == (unsigned long long)key) {
+      atomicAdd(&tcnt[h], 1);
+      atomicMin(&trep[h], (int32_t)s);
+      return;
+    }
+    h = (h + 1) & (uint64_t)tmask;
+  }
+}
+
+__global__ void compact_count_kernel(const int32_t *__restrict__ tcnt, int64_t T,
+                                     int64_t *__restrict__ bcnt) {
+  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
+  int f = (i < T && tcnt[i] > 0) ? 1 : 0;
+  f = __syncthreads_count(f);
+  if (threadIdx.x == 0) bcnt[blockIdx.x] = f;
+}
+
+__global__ void compact_write_kernel(const unsigned long long *__restrict__ tkey,
+                                     const int32_t *__restrict__ tcnt,
+                                     const int32_t *__restrict__ trep, int64_t T,
+                                     const int64_t *__restrict__ bcnt, int nb,
+                                     int64_t *__restrict__ dkey, int32_t *__restrict__ dcnt,
+                                     int32_t *__restrict__ drep, int64_t *__restrict__ S) {
+  __shared__ int64_t base;
+  __shared__ int wsum[32];
+  if (threadIdx.x == 0) {
+    int64_t b = 0, tot = 0;
+    for (int j = 0; j < nb; ++j) {
+      if (j < (int)blockIdx.x) b += bcnt[j];
+      tot += bcnt[j];
+    }
+    base = b;
+    if (blockIdx.x == 0) S[0] = tot;
+  }
+  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
+  const int f = (i < T && tcnt[i] > 0) ? 1 : 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, f);
+  const int pre = __popc(bal & ((1u << lane) - 1u));
+  if (lane == 0) wsum[wid] = __popc(bal);
+  __syncthreads();
+  int woff = 0;
+  for (int w = 0; w < wid; ++w) woff += wsum[w];
+  if (f) {
+    const int64_t o = base + woff + pre;
+    dkey[o] = (int64_t)tkey[i];
+    dcnt[o] = tcnt[i];
+    drep[o] = trep[i];
+  }
+}
+
+// ------------------------------------------------------------------------ lookup
+__global__ void lookup_kernel(const int64_t *__restrict__ keys, int64_t n_cols,
+                              const int64_t *__restrict__ colptr, const int64_t *__restrict__ dkey,
+                              const int32_t *__restrict__ dcnt, const int32_t *__restrict__ drep,
+                              const int64_t *__restrict__ S, const double *__restrict__ H,
+                              const double *__restrict__ w, int R, int64_t *__restrict__ dlo,
+                              int64_t *__restrict__ dlen, double *__restrict__ Hs,
+                              int64_t *__restrict__ stats) {
+  const int lane = threadIdx.x & 31;
+  const int64_t d = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nS = S[0];
+  if (d >= nS) return;
+  int64_t lo = 0, len = 0;
+  if (lane == 0) {
+    const int64_t key = dkey[d];
+    int64_t c = lower_bound_i64(keys, n_cols, key);
+    if (c < n_cols && keys[c] == key) {
+      lo = colptr[c];
+      len = colptr[c + 1] - lo;
+    }
+    dlo[d] = lo;
+    dlen[d] = len;
+    if (len > 0) {
+      atomicAdd((unsigned long long *)&stats[1], 1ull);
+      atomicAdd((unsigned long long *)&stats[3], (unsigned long long)(len * (int64_t)dcnt[d]));
+    }
+  }
+  const int32_t rep = drep[d];
+  const double ws = w[rep];
+  const double sc = (double)dcnt[d] * (ws * ws);
+  for (int c = lane; c < R; c += 32) Hs[d * R + c] = sc * H[(int64_t)rep * R + c];
+}
+
+__global__ void finalize_counts_kernel(const int64_t *__restrict__ S,
+                                       const int64_t *__restrict__ doff, int64_t *__restrict__ nnz,
+                                       int64_t *__restrict__ stats) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const int64_t s = S[0];
+    const int64_t t = doff[s];
+    nnz[0] = t;
+    stats[0] += s;
+    stats[2] += t;
+  }
+}
+
+__global__ void rows_hit_kernel(const int64_t *__restrict__ rcnt, int64_t n_rows,
+                                int64_t *__restrict__ stats) {
+  int64_t c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += rcnt[i] > 0 ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)&stats[4], (unsigned long long)c);
+}
+
+// ------------------------------------------------------------ entry traversal
+// The gathered entries e in [0, nnz) are the concatenation of the distinct fibers; entry e
+// of fiber d sits at store position lo_d + (e - off_d).  A tile of kTileE consecutive
+// entries stages the needed slice of the fiber offsets in shared memory.
+struct TileFibers {
+  int64_t d0;   // first fiber of the tile
+  int nwin;     // window length (offsets d0 .. d0+nwin-1 staged)
+};
+
+__device__ TileFibers stage_tile(const int64_t *__restrict__ doff, int64_t S, int64_t t0,
+                                 int64_t t1, int64_t *win) {
+  __shared__ int64_t sd0, sd1;
+  if (threadIdx.x == 0) {
+    sd0 = floor_index(doff, S + 1, t0);
+    sd1 = floor_index(doff, S + 1, t1 - 1);
+  }
+  __syncthreads();
+  const int64_t d0 = sd0, d1 = sd1;
+  const int nwin = (int)(d1 - d0 + 2);
+  for (int i = threadIdx.x; i < nwin; i += blockDim.x) win[i] = doff[d0 + i];
+  __syncthreads();
+  TileFibers tf;
+  tf.d0 = d0;
+  tf.nwin = nwin;
+  return tf;
+}
+
+__device__ __forceinline__ int64_t fiber_of(const int64_t *win, int nwin, int64_t e) {
+  int lo = 0, hi = nwin - 1;  // win[lo] <= e < win[hi]
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (win[mid] <= e) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void cta_range(int64_t nnz, int64_t &r0, int64_t &r1) {
+  int64_t per = ceil_div(nnz, (int64_t)gridDim.x);
+  if (per < kMinRange) per = kMinRange;
+  per = ceil_div(per, kTileE) * kTileE;
+  r0 = (int64_t)blockIdx.x * per;
+  r1 = r0 + per;
+  if (r1 > nnz) r1 = nnz;
+}
+
+__global__ void __launch_bounds__(256)
+row_count_kernel(const int64_t *__restrict__ doff, const int64_t *__restrict__ Sp,
+                 const int64_t *__restrict__ nnzp, const int64_t *__restrict__ dlo,
+                 const int32_t *__restrict__ rows, int64_t n_rows, int priv,
+                 int64_t *__restrict__ rcnt) {
+  extern __shared__ int64_t sm[];
+  int64_t *win = sm;                                      // kTileE + 2
+  int32_t *hist = reinterpret_cast<int32_t *>(sm + kTileE + 2);
+  const int64_t nnz = nnzp[0], S = Sp[0];
+  int64_t r0, r1;
+  cta_range(nnz, r0, r1);
+  if (r0 >= r1) return;
+  if (priv) {
+    for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) hist[i] = 0;
+  }
+  for (int64_t t0 = r0; t0 < r1; t0 += kTileE) {
+    const int64_t t1 = min(t0 + kTileE, r1);
+    __syncthreads();
+    TileFibers tf = stage_tile(doff, S, t0, t1, win);
+    for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
+      const int64_t j = fiber_of(win, tf.nwin, e);
+      const int32_t row = rows[dlo[tf.d0 + j] + (e - win[j])];
+      if (priv) atomicAdd(&hist[row], 1);
+      else atomicAdd((unsigned long long *)&rcnt[row], 1ull);
+    }
+  }
+  if (priv) {
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x)
+      if (hist[i]) atomicAdd((unsigned long long *)&rcnt[i], (unsigned long long)hist[i]);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+scatter_kernel(const int64_t *__restrict__ doff, const int64_t *__restrict__ Sp,
+               const int64_t *__restrict__ nnzp, const int64_t *__restrict__ dlo,
+               const int32_t *__restrict__ rows, const double *__restrict__ vals, int64_t n_rows,
+               int priv, const int64_t *__restrict__ rptr, int64_t *__restrict__ rcur,
+               int32_t *__restrict__ ed, double *__restrict__ ev, int64_t cap, int *status) {
+  extern __shared__ int64_t sm[];
+  int64_t *win = sm;
+  int32_t *hist = reinterpret_cast<int32_t *>(sm + kTileE + 2);
+  const int64_t nnz = nnzp[0], S = Sp[0];
+  int64_t r0, r1;
+  cta_range(nnz, r0, r1);
+  if (r0 >= r1) return;
+  if (priv) {
+    // pass A: CTA-local counts; reserve one contiguous run per (CTA, row)
+    for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) hist[i] = 0;
+    for (int64_t t0 = r0; t0 < r1; t0 += kTileE) {
+      const int64_t t1 = min(t0 + kTileE, r1);
+      __syncthreads();
+      TileFibers tf = stage_tile(doff, S, t0, t1, win);
+      for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
+        const int64_t j = fiber_of(win, tf.nwin, e);
+        atomicAdd(&hist[rows[dlo[tf.d0 + j] + (e - win[j])]], 1);
+      }
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) {
+      const int32_t c = hist[i];
+      if (c) hist[i] = (int32_t)atomicAdd((unsigned long long *)&rcur[i], (unsigned long long)c);
+    }
+  }
+  for (int64_t t0 = r0; t0 < r1; t0 += kTileE) {
+    const int64_t t1 = min(t0 + kTileE, r1);
+    __syncthreads();
+    TileFibers tf = stage_tile(doff, S, t0, t1, win);
+    for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
+      const int64_t j = fiber_of(win, tf.nwin, e);
+      const int64_t pos = dlo[tf.d0 + j] + (e - win[j]);
+      const int32_t row = rows[pos];
+      int64_t slot;
+      if (priv) slot = atomicAdd(&hist[row], 1);
+      else slot = (int64_t)atomicAdd((unsigned long long *)&rcur[row], 1ull);
+      const int64_t o = rptr[row] + slot;
+      if (o >= cap) {
+        raise_status(status, RCP_ST_CAPACITY);
+        continue;
+      }
+      ed[o] = (int32_t)(tf.d0 + j);
+      ev[o] = vals[pos];
+    }
+  }
+}
+
+// ------------------------------------------------------------ segmented SpMM
+// One warp per chunk of kSpmmChunk row-sorted entries; lanes own output columns.
+template <int RPL, typename ColT>
+__global__ void __launch_bounds__(256)
+spmm_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__restrict__ nnzp,
+            int64_t nnz_host, const ColT *__restrict__ col, const double *__restrict__ val,
+            const double *__restrict__ Hs, const double *__restrict__ scale, int R,
+            double *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nnz = nnzp ? nnzp[0] : nnz_host;
+  const int64_t nchunks = ceil_div(nnz, kSpmmChunk);
+  for (int64_t ch = warp0; ch < nchunks; ch += nwarps) {
+    const int64_t c0 = ch * kSpmmChunk;
+    const int64_t c1 = min(c0 + kSpmmChunk, nnz);
+    int64_t row = floor_index(rptr, n_rows + 1, c0);
+    int64_t e = c0;
+    while (e < c1) {
+      const int64_t rs = rptr[row], re = rptr[row + 1];
+      const int64_t stop = min(re, c1);
+      if (stop > e) {
+        double acc[RPL];
+#pragma unroll
+        for (int j = 0; j < RPL; ++j) acc[j] = 0.0;
+        int64_t x = e;
+        for (; x + 2 <= stop; x += 2) {
+          const int64_t d0 = (int64_t)col[x], d1 = (int64_t)col[x + 1];
+          double v0 = val[x], v1 = val[x + 1];
+          if (scale) {
+            v0 *= scale[d0];
+            v1 *= scale[d1];
+          }
+#pragma unroll
+          for (int j = 0; j < RPL; ++j) {
+            const int c = lane + 32 * j;
+            if (c < R) {
+              acc[j] = fma(v0, Hs[d0 * R + c], acc[j]);
+              acc[j] = fma(v1, Hs[d1 * R + c], acc[j]);
+            }
+          }
+        }
+        for (; x < stop; ++x) {
+          const int64_t d0 = (int64_t)col[x];
+          double v0 = val[x];
+          if (scale) v0 *= scale[d0];
+#pragma unroll
+          for (int j = 0; j < RPL; ++j) {
+            const int c = lane + 32 * j;
+            if (c < R) acc[j] = fma(v0, Hs[d0 * R + c], acc[j]);
+          }
+        }
+        const bool whole = (rs >= c0) && (re <= c1);
+#pragma unroll
+        for (int j = 0; j < RPL; ++j) {
+          const int c = lane + 32 * j;
+          if (c < R) {
+            if (whole) out[row * R + c] = acc[j];
+            else atomicAdd(&out[row * R + c], acc[j]);
+          }
+        }
+        e = stop;
+      }
+      ++row;
+    }
+  }
+}
+
+template <typename ColT>
+int launch_spmm(const int64_t *rptr, int64_t n_rows, const int64_t *nnzp, int64_t nnz_host,
+                const ColT *col, const double *val, const double *Hs, const double *scale, int R,
+                double *out, cudaStream_t st) {
+  int64_t chunks_host = nnzp ? -1 : ceil_div(nnz_host, kSpmmChunk);
+  int64_t blocks = 8LL * sm_count();
+  if (chunks_host >= 0) {
+    int64_t need = ceil_div(chunks_host, 8);
+    if (need < blocks) blocks = need;
+    if (blocks < 1) return RCP_OK;
+  }
+  switch ((R + 31) / 32) {
+    case 1: spmm_kernel<1, ColT><<<(unsigned)blocks, 256, 0, st>>>(rptr, n_rows, nnzp, nnz_host, col, val, Hs, scale, R, out); break;
+    case 2: spmm_kernel<2, ColT><<<(unsigned)blocks, 256, 0, st>>>(rptr, n_rows, nnzp, nnz_host, col, val, Hs, scale, R, out); break;
+    case 3: spmm_kernel<3, ColT><<<(unsigned)blocks, 256, 0, st>>>(rptr, n_rows, nnzp, nnz_host, col, val, Hs, scale, R, out); break;
+    default: spmm_kernel<4, ColT><<<(unsigned)blocks, 256, 0, st>>>(rptr, n_rows, nnzp, nnz_host, col, val, Hs, scale, R, out); break;
+  }
+  RCP_LAUNCH_CHECK("spmm");
+  return RCP_OK;
+}
+
+// ------------------------------------------------------------ drop-in CSR helpers
+__global__ void fiber_lookup_kernel(const int64_t *__restrict__ keys, int64_t n_cols,
+                                    const int64_t *__restrict__ colptr,
+                                    const int64_t *__restrict__ X, int N, int64_t J, int k,
+                                    Strides st, int64_t *__restrict__ lo,
+                                    int64_t *__restrict__ cnt) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= J) return;
+  const int64_t key = sample_key(X, N, J, k, st, s);
+  const int64_t c = lower_bound_i64(keys, n_cols, key);
+  int64_t a = 0, b = 0;
+  if (c < n_cols && keys[c] == key) {
+    a = colptr[c];
+    b = colptr[c + 1];
+  }
+  lo[s] = a;
+  cnt[s] = b - a;
+}
+
+__global__ void fiber_expand_kernel(const int64_t *__restrict__ lo, const int64_t *__restrict__ off,
+                                    int64_t J, const int32_t *__restrict__ rows,
+                                    const double *__restrict__ vals, int64_t *__restrict__ ro,
+                                    int64_t *__restrict__ co, double *__restrict__ vo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (s >= J) return;
+  const int64_t a = lo[s], o = off[s], len = off[s + 1] - off[s];
+  for (int64_t t = lane; t < len; t += 32) {
+    ro[o + t] = rows[a + t];
+    co[o + t] = s;
+    vo[o + t] = vals[a + t];
+  }
+}
+
+// ------------------------------------------------------------ workspace layout
+struct Ws {
+  size_t off[32];
+  int n = 0;
+  size_t total = 0;
+  size_t add(size_t bytes) {
+    size_t o = (total + 255) & ~(size_t)255;
+    total = o + bytes;
+    off[n++] = o;
+    return o;
+  }
+};
+
+struct MttkrpLayout {
+  int64_t T;
+  size_t o_tkey, o_tcnt, o_trep, o_bcnt, o_dkey, o_dcnt, o_drep, o_dlo, o_dlen, o_doff, o_Hs,
+      o_scan, o_rcnt, o_rptr, o_ed, o_ev, o_S, o_nnz;
+  size_t total;
+  MttkrpLayout(int64_t J, int64_t cap, int64_t n_rows, int R) {
+    T = 1024;
+    while (T < 2 * J) T <<= 1;
+    Ws w;
+    o_tkey = w.add(sizeof(int64_t) * T);
+    o_tcnt = w.add(sizeof(int32_t) * T);
+    o_trep = w.add(sizeof(int32_t) * T);
+    o_bcnt = w.add(sizeof(int64_t) * (T / 1024));
+    o_dkey = w.add(sizeof(int64_t) * (J + 1));
+    o_dcnt = w.add(sizeof(int32_t) * (J + 1));
+    o_drep = w.add(sizeof(int32_t) * (J + 1));
+    o_dlo = w.add(sizeof(int64_t) * (J + 1));
+    o_dlen = w.add(sizeof(int64_t) * (J + 1));
+    o_doff = w.add(sizeof(int64_t) * (J + 2));
+    o_Hs = w.add(sizeof(double) * (size_t)(J + 1) * R);
+    int64_t sc = J + 1 > n_rows + 1 ? J + 1 : n_rows + 1;
+    o_scan = w.add(scan_ws_bytes(sc));
+    o_rcnt = w.add(sizeof(int64_t) * (n_rows + 1));
+    o_rptr = w.add(sizeof(int64_t) * (n_rows + 2));
+    o_ed = w.add(sizeof(int32_t) * (cap + 1));
+    o_ev = w.add(sizeof(double) * (cap + 1));
+    o_S = w.add(sizeof(int64_t) * 4);
+    o_nnz = w.add(sizeof(int64_t) * 4);
+    total = w.total + 256;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+size_t rcp_mttkrp_ws_bytes(int64_t J, int64_t store_nnz, int64_t n_rows, int R) {
+  MttkrpLayout L(J, store_nnz, n_rows, R);
+  return L.total;
+}
+
+int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n_cols,
+                       const int32_t *d_rows, const double *d_vals, int64_t n_rows,
+                       const int64_t *d_X, int N, int64_t J, int k, const int64_t *h_strides,
+                       const double *d_H, const double *d_w, int R, double *d_out,
+                       int64_t *d_stats, void *d_ws, size_t ws_bytes, int *d_status,
+                       void *stream) {
+  if (N < 2 || N > kMaxModes || k < 0 || k >= N || R < 1 || R > RCP_MAX_RANK || J < 0 ||
+      n_rows < 0 || n_cols < 0 || !h_strides || !d_stats)
+    return RCP_ERR_ARG;
+  cudaStream_t st = RCP_STREAM(stream);
+  if (n_rows > 0) RCP_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(double) * n_rows * R, st));
+  if (J == 0 || n_rows == 0 || n_cols == 0) return RCP_OK;
+  if (!d_keys || !d_colptr || !d_rows || !d_vals || !d_X || !d_H || !d_w || !d_out || !d_ws)
+    return RCP_ERR_ARG;
+  // store_nnz (capacity of the entry arrays) is implied by ws_bytes
+  int64_t cap = 0;
+  {
+    // find the largest capacity that fits ws_bytes (layout is monotone in cap)
+    MttkrpLayout base(J, 0, n_rows, R);
+    if (ws_bytes < base.total) return RCP_ERR_ARG;
+    cap = (int64_t)((ws_bytes - base.total) / (sizeof(int32_t) + sizeof(double)));
+  }
+  MttkrpLayout L(J, cap, n_rows, R);
+  while (L.total > ws_bytes && cap > 0) {
+    cap -= 64;
+    L = MttkrpLayout(J, cap, n_rows, R);
+  }
+  char *w = (char *)d_ws;
+  auto P = [&](size_t o) { return (void *)(w + o); };
+  unsigned long long *tkey = (unsigned long long *)P(L.o_tkey);
+  int32_t *tcnt = (int32_t *)P(L.o_tcnt), *trep = (int32_t *)P(L.o_trep);
+  int64_t *bcnt = (int64_t *)P(L.o_bcnt);
+  int64_t *dkey = (int64_t *)P(L.o_dkey);
+  int32_t *dcnt = (int32_t *)P(L.o_dcnt), *drep = (int32_t *)P(L.o_drep);
+  int64_t *dlo = (int64_t *)P(L.o_dlo), *dlen = (int64_t *)P(L.o_dlen), *doff = (int64_t *)P(L.o_doff);
+  double *Hs = (double *)P(L.o_Hs);
+  void *scan_ws = P(L.o_scan);
+  int64_t *rcnt = (int64_t *)P(L.o_rcnt), *rptr = (int64_t *)P(L.o_rptr);
+  int32_t *ed = (int32_t *)P(L.o_ed);
+  double *ev = (double *)P(L.o_ev);
+  int64_t *S = (int64_t *)P(L.o_S), *nnz = (int64_t *)P(L.o_nnz);
+
+  Strides sd;
+  for (int m = 0; m < kMaxModes; ++m) sd.s[m] = m < N ? h_strides[m] : 0;
+
+  // 1. dedup
+  RCP_CUDA_TRY(cudaMemsetAsync(tkey, 0xff, sizeof(int64_t) * L.T, st));
+  RCP_CUDA_TRY(cudaMemsetAsync(tcnt, 0, sizeof(int32_t) * L.T, st));
+  RCP_CUDA_TRY(cudaMemsetAsync(trep, 0x7f, sizeof(int32_t) * L.T, st));
+  hash_insert_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(d_X, N, J, k, sd, L.T - 1, tkey,
+                                                                 tcnt, trep);
+  RCP_LAUNCH_CHECK("hash_insert");
+  const int nb = (int)(L.T / 1024);
+  compact_count_kernel<<<nb, 1024, 0, st>>>(tcnt, L.T, bcnt);
+  RCP_LAUNCH_CHECK("compact_count");
+  compact_write_kernel<<<nb, 1024, 0, st>>>(tkey, tcnt, trep, L.T, bcnt, nb, dkey, dcnt, drep, S);
+  RCP_LAUNCH_CHECK("compact_write");
+  // 2. lookup + scaled KRP rows
+  lookup_kernel<<<(unsigned)ceil_div(J * 32, 256), 256, 0, st>>>(
+      d_keys, n_cols, d_colptr, dkey, dcnt, drep, S, d_H, d_w, R, dlo, dlen, Hs, d_stats);
+  RCP_LAUNCH_CHECK("lookup");
+  // 3. fiber offsets
+  int rc = scan_i64_exclusive(dlen, doff, J, S, scan_ws, st);
+  if (rc) return rc;
+  finalize_counts_kernel<<<1, 32, 0, st>>>(S, doff, nnz, d_stats);
+  RCP_LAUNCH_CHECK("finalize_counts");
+  // 4. row histogram -> row pointers
+  const int priv = n_rows <= kPrivRows ? 1 : 0;
+  size_t smem = sizeof(int64_t) * (kTileE + 2) + (priv ? sizeof(int32_t) * n_rows : 0);
+  static bool attr = false;
+  if (!attr) {
+    RCP_CUDA_TRY(cudaFuncSetAttribute(row_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RCP_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  const int grid = 2 * sm_count();
+  RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
+  row_count_kernel<<<grid, 256, smem, st>>>(doff, S, nnz, dlo, d_rows, n_rows, priv, rcnt);
+  RCP_LAUNCH_CHECK("row_count");
+  rc = scan_i64_exclusive(rcnt, rptr, n_rows, nullptr, scan_ws, st);
+  if (rc) return rc;
+  {
+    int64_t b = ceil_div(n_rows, 256);
+    if (b > 4LL * sm_count()) b = 4LL * sm_count();
+    rows_hit_kernel<<<(unsigned)b, 256, 0, st>>>(rcnt, n_rows, d_stats);
+    RCP_LAUNCH_CHECK("rows_hit");
+  }
+  // 5. scatter into row order (rcnt reused as per-row cursor)
+  RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
+  scatter_kernel<<<grid, 256, smem, st>>>(doff, S, nnz, dlo, d_rows, d_vals, n_rows, priv, rptr,
+                                          rcnt, ed, ev, cap, d_status);
+  RCP_LAUNCH_CHECK("scatter");
+  // 6. segmented reduction
+  return launch_spmm<int32_t>(rptr, n_rows, nnz, 0, ed, ev, Hs, nullptr, R, d_out, st);
+}
+
+int rcp_fiber_lookup(const int64_t *d_keys, int64_t n_cols, const int64_t *d_colptr,
+                     const int64_t *d_X, int N, int64_t J, int k, const int64_t *h_strides,
+                     int64_t *d_lo, int64_t *d_counts, void *stream) {
+  if (N < 2 || N > kMaxModes || k < 0 || k >= N || J < 0 || !h_strides) return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  if (!d_X || !d_lo || !d_counts || (n_cols > 0 && (!d_keys || !d_colptr))) return RCP_ERR_ARG;
+  Strides sd;
+  for (int m = 0; m < kMaxModes; ++m) sd.s[m] = m < N ? h_strides[m] : 0;
+  fiber_lookup_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, RCP_STREAM(stream)>>>(
+      d_keys, n_cols, d_colptr, d_X, N, J, k, sd, d_lo, d_counts);
+  RCP_LAUNCH_CHECK("fiber_lookup");
+  return RCP_OK;
+}
+
+int rcp_fiber_expand(const int64_t *d_lo, const int64_t *d_off, int64_t J, const int32_t *d_rows,
+                     const double *d_vals, int64_t *d_row_out, int64_t *d_col_out,
+                     double *d_val_out, void *stream) {
+  if (J < 0) return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  if (!d_lo || !d_off || !d_row_out || !d_col_out || !d_val_out) return RCP_ERR_ARG;
+  fiber_expand_kernel<<<(unsigned)ceil_div(J * 32, 256), 256, 0, RCP_STREAM(stream)>>>(
+      d_lo, d_off, J, d_rows, d_vals, d_row_out, d_col_out, d_val_out);
+  RCP_LAUNCH_CHECK("fiber_expand");
+  return RCP_OK;
+}
+
+int rcp_csr_spmm(const int64_t *d_row_ptr, int64_t n_rows, const int64_t *d_col,
+                 const double *d_val, const double *d_H, const double *d_scale, int R,
+                 double *d_out, void *stream) {
+  if (n_rows < 0 || R < 1 || R > RCP_MAX_RANK || !d_row_ptr) return RCP_ERR_ARG;
+  cudaStream_t st = RCP_STREAM(stream);
+  if (n_rows == 0) return RCP_OK;
+  RCP_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(double) * n_rows * R, st));
+  int64_t nnz = 0;
+  RCP_CUDA_TRY(cudaMemcpyAsync(&nnz, d_row_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  RCP_CUDA_TRY(cudaStreamSynchronize(st));
+  if (nnz == 0) return RCP_OK;
+  return launch_spmm<int64_t>(d_row_ptr, n_rows, nullptr, nnz, d_col, d_val, d_H, d_scale, R,
+                              d_out, st);
+}
+
+}  // extern "C"

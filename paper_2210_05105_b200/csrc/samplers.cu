@@ -1,0 +1,599 @@
+// Leverage-score samplers on the device.
+//  * CP-ARLS-LEV (ref samplers.py:104-191): per-row leverage u G+ u^T, ordered mass,
+//    normalised cdf, inverse-CDF draws on Philox LOCAL_DRAW streams, SHUFFLE fold.
+//  * STS-CP (ref samplers.py:194-468): a complete binary tree of packed node Grams over
+//    leaf blocks of consecutive rows; one warp walks one sample, evaluating the two child
+//    masses h^T (G (.) M) h per level as a dot product of the node Gram with the
+//    sample's precomputed packed P = (h h^T) (.) M, then an inverse-CDF over the leaf's
+//    rows.  In exact arithmetic this is the reference's inverse CDF of r over rows in
+//    global order (the reference itself is leaf-size and rank-count invariant).
+#include <float.h>
+
+#include "common.cuh"
+#include "scan.cuh"
+
+using namespace rcp;
+
+namespace {
+
+int sm_count() {
+  static int s = 0;
+  if (!s) {
+    s = rcp_device_sms();
+    if (!s) s = 148;
+  }
+  return s;
+}
+
+// ------------------------------------------------------------------ ARLS leverage
+template <int RPL>
+__global__ void __launch_bounds__(256)
+leverage_kernel(const double *__restrict__ U, int64_t n, int R, const double *__restrict__ Gp,
+                double *__restrict__ lev, double *__restrict__ part) {
+  extern __shared__ double sh[];
+  double *G = sh;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) G[e] = Gp[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double local = 0.0;
+  for (int64_t row = (int64_t)blockIdx.x * nw + wid; row < n; row += (int64_t)gridDim.x * nw) {
+    double u[RPL], y[RPL];
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+      int c = lane + 32 * j;
+      u[j] = c < R ? U[row * R + c] : 0.0;
+      y[j] = 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+      const int amax = min(32, R - 32 * j);
+      for (int t = 0; t < amax; ++t) {
+        double ua = __shfl_sync(0xffffffffu, u[j], t);
+        const double *grow = G + (32 * j + t) * R;
+#pragma unroll
+        for (int jj = 0; jj < RPL; ++jj) {
+          int c = lane + 32 * jj;
+          if (c < R) y[jj] = fma(ua, grow[c], y[jj]);
+        }
+      }
+    }
+    double d = 0.0;
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) d += u[j] * y[j];
+    d = warp_sum(d);
+    d = d > 0.0 ? d : 0.0;
+    if (lane == 0) {
+      lev[row] = d;
+      local += d;
+    }
+  }
+  __syncthreads();
+  if (lane == 0) sh[wid] = local;  // reuse (G no longer needed)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += sh[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+__global__ void mass_kernel(const double *__restrict__ part, int nparts, double *mass) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += part[p];
+    mass[0] = s;
+  }
+}
+
+__global__ void normalize_kernel(double *__restrict__ dist, int64_t n, const double *mass) {
+  const double C = mass[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (C > 0.0) dist[i] = dist[i] / C;
+}
+
+__global__ void cdf_div_kernel(double *__restrict__ cdf, int64_t n) {
+  const double last = cdf[n - 1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    cdf[i] = cdf[i] / last;
+}
+
+__global__ void arls_draw_kernel(const double *__restrict__ cdf, const double *__restrict__ dist,
+                                 int64_t n, int64_t row_lo, double ratio, const double *tmass,
+                                 uint64_t k0, uint64_t k1, int64_t q, int64_t offset,
+                                 int64_t *__restrict__ rows, double *__restrict__ prob,
+                                 const double *__restrict__ U, int R, double *__restrict__ urow,
+                                 int *status) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= q) return;
+  if (tmass && !(tmass[0] > 0.0)) {
+    if (t == 0) raise_status(status, RCP_ST_ZERO_MASS);
+    rows[offset + t] = row_lo;
+    prob[offset + t] = 0.0;
+    return;
+  }
+  const double u = u64_to_unit(philox_word(k0, k1, (uint64_t)t));
+  // searchsorted(cdf, u, side='right'): number of entries <= u
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (cdf[mid] <= u) lo = mid + 1; else hi = mid;
+  }
+  if (lo > n - 1) lo = n - 1;
+  rows[offset + t] = row_lo + lo;
+  prob[offset + t] = ratio * dist[lo];
+  if (urow)
+    for (int c = 0; c < R; ++c) urow[(offset + t) * R + c] = U[lo * R + c];
+}
+
+__global__ void batch_fold_kernel(const int64_t *__restrict__ perm, const int64_t *__restrict__ rows,
+                                  const double *__restrict__ prob, int64_t J,
+                                  const double *__restrict__ U, int64_t u_lo,
+                                  const double *__restrict__ urows, int R, int first,
+                                  int64_t *__restrict__ Xi, double *__restrict__ pmp,
+                                  double *__restrict__ H) {
+  // one warp per sample: coalesced H row update
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (s >= J) return;
+  const int64_t t = perm ? perm[s] : s;
+  const int64_t x = rows[t];
+  if (lane == 0) {
+    Xi[s] = x;
+    pmp[s] = prob[t];
+  }
+  const double *src = urows ? urows + t * R : U + (x - u_lo) * R;
+  for (int c = lane; c < R; c += 32) H[s * R + c] = first ? src[c] : H[s * R + c] * src[c];
+}
+
+// --------------------------------------------------------------------- STS build
+__global__ void sts_leaf_kernel(const double *__restrict__ U, int64_t n, int R, int leaf,
+                                int64_t nleaves, double *__restrict__ level) {
+  extern __shared__ double rows[];  // leaf x R
+  const int Rt = R * (R + 1) / 2;
+  for (int64_t v = blockIdx.x; v < nleaves; v += gridDim.x) {
+    const int64_t r0 = v * leaf;
+    const int nr = (int)min((int64_t)leaf, n - r0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * R; e += blockDim.x) rows[e] = U[r0 * R + e];
+    __syncthreads();
+    double *out = level + v * Rt;
+    for (int e = threadIdx.x; e < Rt; e += blockDim.x) {
+      // decode packed (a, b)
+      int a = 0, rem = e;
+      while (rem >= R - a) {
+        rem -= R - a;
+        ++a;
+      }
+      const int b = a + rem;
+      double s = 0.0;
+      for (int q = 0; q < nr; ++q) s = fma(rows[q * R + a], rows[q * R + b], s);
+      out[e] = s;
+    }
+  }
+}
+
+__global__ void sts_zero_kernel(double *__restrict__ p, int64_t len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0.0;
+}
+
+__global__ void sts_level_kernel(const double *__restrict__ child, double *__restrict__ parent,
+                                 int64_t nodes, int Rt) {
+  const int64_t tot = nodes * Rt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / Rt, e = i % Rt;
+    parent[i] = child[(2 * v) * Rt + e] + child[(2 * v + 1) * Rt + e];
+  }
+}
+
+// ---------------------------------------------------------------------- STS walk
+constexpr int kMaxLeaf = 64;
+
+struct WalkSmem {
+  static size_t bytes(int R, int warps, int leaf) {
+    const int Rt = R * (R + 1) / 2;
+    return sizeof(double) * ((size_t)Rt + (size_t)warps * (Rt + 2 * R + leaf + 2)) +
+           sizeof(uint16_t) * (size_t)Rt + 64;
+  }
+};
+
+__global__ void sts_walk_kernel(const double *__restrict__ tree, const double *__restrict__ U,
+                                int64_t n, int R, int leaf, int depth, int64_t row_lo,
+                                const double *__restrict__ Mfull, const double *__restrict__ Hin,
+                                int64_t J, uint64_t k0, uint64_t k1,
+                                const double *__restrict__ override_u,
+                                const double *__restrict__ rin, const int32_t *__restrict__ sel,
+                                int32_t selv, int64_t *__restrict__ Xi, double *__restrict__ pmp,
+                                double *__restrict__ resid, double *__restrict__ urow,
+                                int *status) {
+  extern __shared__ double sh[];
+  const int Rt = R * (R + 1) / 2;
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double *Mp = sh;                                       // Rt: packed M, off-diagonals x2
+  double *wbase = Mp + Rt;
+  double *P = wbase + (size_t)wid * (Rt + 2 * R + leaf + 2);  // per-warp packed P
+  double *hv = P + Rt;                                   // R
+  double *uv = hv + R;                                   // R
+  double *mass = uv + R;                                 // leaf (+2)
+  uint16_t *pairs = reinterpret_cast<uint16_t *>(wbase + (size_t)warps * (Rt + 2 * R + leaf + 2));
+
+  for (int e = threadIdx.x; e < Rt; e += blockDim.x) {
+    int a = 0, rem = e;
+    while (rem >= R - a) {
+      rem -= R - a;
+      ++a;
+    }
+    const int b = a + rem;
+    pairs[e] = (uint16_t)(a | (b << 8));
+    const double m = Mfull[a * R + b];
+    Mp[e] = (a == b) ? m : 2.0 * m;
+  }
+  __syncthreads();
+
+  const double tiny = DBL_MIN;
+  for (int64_t s = (int64_t)blockIdx.x * warps + wid; s < J; s += (int64_t)gridDim.x * warps) {
+    if (sel && sel[s] != selv) continue;
+    double r;
+    if (override_u) r = override_u[s];
+    else if (rin) r = rin[s];
+    else r = u64_to_unit(philox_word(k0, k1, (uint64_t)s));
+    for (int c = lane; c < R; c += 32) hv[c] = Hin ? Hin[s * R + c] : 1.0;
+    __syncwarp();
+    for (int e = lane; e < Rt; e += 32) {
+      const uint16_t ab = pairs[e];
+      P[e] = hv[ab & 0xff] * hv[ab >> 8] * Mp[e];
+    }
+    __syncwarp();
+    double prob = 1.0;
+    int64_t v = 0;
+    bool bad = false;
+    for (int lev = 0; lev < depth; ++lev) {
+      const double *GL = tree + ((1LL << (lev + 1)) - 1 + 2 * v) * (int64_t)Rt;
+      const double *GR = GL + Rt;
+      double qL = 0.0, qR = 0.0;
+      for (int e = lane; e < Rt; e += 32) {
+        const double p = P[e];
+        qL = fma(__ldg(GL + e), p, qL);
+        qR = fma(__ldg(GR + e), p, qR);
+      }
+      qL = warp_sum(qL);
+      qR = warp_sum(qR);
+      qL = qL > 0.0 ? qL : 0.0;
+      qR = qR > 0.0 ? qR : 0.0;
+      const double tot = qL + qR;
+      if (!(tot > 0.0)) {
+        bad = true;
+        break;
+      }
+      double T = qL / tot;
+      T = fmin(fmax(T, 0.0), 1.0);
+      const bool right = r >= T;
+      prob *= right ? (1.0 - T) : T;
+      r = right ? (r - T) / fmax(1.0 - T, tiny) : r / fmax(T, tiny);
+      r = fmin(fmax(r, 0.0), one_below());
+      v = 2 * v + (right ? 1 : 0);
+    }
+    if (bad) {
+      if (lane == 0) {
+        raise_status(status, RCP_ST_DEGENERATE);
+        Xi[s] = -1;
+      }
+      continue;
+    }
+    // leaf block: row masses (u (.) h)^T M (u (.) h) = sum_e u_a u_b P_e
+    const int64_t r0 = v * leaf;
+    const int nr = (int)min((int64_t)leaf, n - r0);
+    if (nr <= 0) {
+      if (lane == 0) {
+        raise_status(status, RCP_ST_DEGENERATE);
+        Xi[s] = -1;
+      }
+      continue;
+    }
+    for (int q = 0; q < nr; ++q) {
+      for (int c = lane; c < R; c += 32) uv[c] = U[(r0 + q) * R + c];
+      __syncwarp();
+      double m = 0.0;
+      for (int e = lane; e < Rt; e += 32) {
+        const uint16_t ab = pairs[e];
+        m = fma(uv[ab & 0xff] * uv[ab >> 8], P[e], m);
+      }
+      m = warp_sum(m);
+      if (lane == 0) mass[q] = m > 0.0 ? m : 0.0;
+      __syncwarp();
+    }
+    // inverse CDF over the leaf rows (ref _inverse_cdf samplers.py:291-310)
+    int choice = 0;
+    double picked = 0.0, total = 0.0, rout = 0.0;
+    if (lane == 0) {
+      for (int q = 0; q < nr; ++q) total += mass[q];
+      if (!(total > 0.0)) {
+        bad = true;
+      } else {
+        const double target = r * total;
+        double cdf = 0.0;
+        int cnt = 0;
+        double cdf_at = 0.0;
+        for (int q = 0; q < nr; ++q) {
+          cdf += mass[q];
+          if (cdf <= target) ++cnt;
+        }
+        choice = cnt < nr - 1 ? cnt : nr - 1;
+        cdf = 0.0;
+        for (int q = 0; q <= choice; ++q) cdf += mass[q];
+        cdf_at = cdf;
+        picked = mass[choice];
+        const double before = cdf_at - picked;
+        rout = picked > 0.0 ? (target - before) / picked : 0.0;
+        rout = fmin(fmax(rout, 0.0), one_below());
+      }
+    }
+    bad = __shfl_sync(0xffffffffu, bad ? 1 : 0, 0) != 0;
+    if (bad) {
+      if (lane == 0) {
+        raise_status(status, RCP_ST_DEGENERATE);
+        Xi[s] = -1;
+      }
+      continue;
+    }
+    choice = __shfl_sync(0xffffffffu, choice, 0);
+    const int64_t row = r0 + choice;
+    if (lane == 0) {
+      Xi[s] = row_lo + row;
+      pmp[s] *= prob * (picked / total);
+      if (resid) resid[s] = rout;
+    }
+    for (int c = lane; c < R; c += 32) urow[s * R + c] = U[row * R + c];
+    __syncwarp();
+  }
+}
+
+__global__ void sts_cond_kernel(const double *__restrict__ cp, const double *__restrict__ grams,
+                                int N, int i, int k, int R, double *__restrict__ M) {
+  const int RR = R * R;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < RR; e += gridDim.x * blockDim.x) {
+    double m = cp[e];
+    for (int t = i + 1; t < N; ++t)
+      if (t != k) m = m * grams[(int64_t)t * RR + e];
+    M[e] = m;
+  }
+}
+
+// One warp per sample over the (small) padded rank tree (ref samplers.py:423-451).
+__global__ void sts_rank_walk_kernel(const double *__restrict__ ng, int depth, int P,
+                                     const int32_t *__restrict__ leaf_rank,
+                                     const double *__restrict__ M, const double *__restrict__ H,
+                                     int64_t J, int R, uint64_t k0, uint64_t k1,
+                                     const double *__restrict__ ov, int32_t *__restrict__ owner,
+                                     double *__restrict__ rout, double *__restrict__ pmp,
+                                     int *status) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (s >= J) return;
+  double r = ov ? ov[s] : u64_to_unit(philox_word(k0, k1, (uint64_t)s));
+  const double tiny = DBL_MIN;
+  double prob = 1.0;
+  int64_t v = 0;
+  const int RR = R * R;
+  for (int lev = 0; lev < depth; ++lev) {
+    const double *Gv = ng + ((1LL << lev) - 1 + v) * (int64_t)RR;
+    const double *Gl = ng + ((1LL << (lev + 1)) - 1 + 2 * v) * (int64_t)RR;
+    double den = 0.0, num = 0.0;
+    for (int e = lane; e < RR; e += 32) {
+      const int a = e / R, b = e % R;
+      const double hm = H[s * R + a] * H[s * R + b] * M[e];
+      den = fma(Gv[e], hm, den);
+      num = fma(Gl[e], hm, num);
+    }
+    den = warp_sum(den);
+    num = warp_sum(num);
+    if (!(den > 0.0)) {
+      if (lane == 0) raise_status(status, RCP_ST_DEGENERATE);
+      return;
+    }
+    double T = (num > 0.0 ? num : 0.0) / den;
+    T = fmin(fmax(T, 0.0), 1.0);
+    const bool right = r >= T;
+    prob *= right ? (1.0 - T) : T;
+    r = right ? (r - T) / fmax(1.0 - T, tiny) : r / fmax(T, tiny);
+    r = fmin(fmax(r, 0.0), one_below());
+    v = 2 * v + (right ? 1 : 0);
+    const int64_t width = 1LL << (depth - 1 - lev);
+    const int64_t lo = v * width;
+    const int64_t nreal = min((v + 1) * width, (int64_t)P) - lo;
+    if (nreal <= 0) {
+      if (lane == 0) raise_status(status, RCP_ST_DEGENERATE);
+      return;
+    }
+  }
+  if (lane == 0) {
+    owner[s] = depth ? leaf_rank[v] : leaf_rank[0];
+    rout[s] = r;
+    pmp[s] = prob;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t rcp_arls_build_ws_bytes(int64_t n, int R) {
+  (void)R;
+  return (size_t)4 * sm_count() * sizeof(double) + scan_ws_bytes(n) + 64;
+}
+
+int rcp_arls_build(const double *d_U, int64_t n, int R, const double *d_Gp, double *d_dist,
+                   double *d_cdf, double *d_mass, void *d_ws, void *stream) {
+  if (R < 1 || R > RCP_MAX_RANK || n < 0 || !d_Gp || !d_mass || (n > 0 && (!d_U || !d_dist || !d_cdf || !d_ws)))
+    return RCP_ERR_ARG;
+  cudaStream_t st = RCP_STREAM(stream);
+  if (n == 0) {
+    RCP_CUDA_TRY(cudaMemsetAsync(d_mass, 0, sizeof(double), st));
+    return RCP_OK;
+  }
+  int64_t want = ceil_div(n, 8);
+  int grid = (int)(want < 4LL * sm_count() ? want : 4LL * sm_count());
+  double *part = (double *)d_ws;
+  void *scan_ws = (char *)d_ws + (size_t)4 * sm_count() * sizeof(double);
+  size_t smem = sizeof(double) * R * R;
+  static bool attr = false;
+  if (!attr) {
+    RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
+    RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
+    RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
+    RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
+    attr = true;
+  }
+  switch ((R + 31) / 32) {
+    case 1: leverage_kernel<1><<<grid, 256, smem, st>>>(d_U, n, R, d_Gp, d_dist, part); break;
+    case 2: leverage_kernel<2><<<grid, 256, smem, st>>>(d_U, n, R, d_Gp, d_dist, part); break;
+    case 3: leverage_kernel<3><<<grid, 256, smem, st>>>(d_U, n, R, d_Gp, d_dist, part); break;
+    default: leverage_kernel<4><<<grid, 256, smem, st>>>(d_U, n, R, d_Gp, d_dist, part); break;
+  }
+  RCP_LAUNCH_CHECK("leverage");
+  mass_kernel<<<1, 32, 0, st>>>(part, grid, d_mass);
+  RCP_LAUNCH_CHECK("leverage_mass");
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > 8LL * sm_count()) blocks = 8LL * sm_count();
+  normalize_kernel<<<(unsigned)blocks, 256, 0, st>>>(d_dist, n, d_mass);
+  RCP_LAUNCH_CHECK("leverage_normalize");
+  int rc = scan_f64_inclusive(d_dist, d_cdf, n, scan_ws, st);
+  if (rc) return rc;
+  cdf_div_kernel<<<(unsigned)blocks, 256, 0, st>>>(d_cdf, n);
+  RCP_LAUNCH_CHECK("cdf_normalize");
+  return RCP_OK;
+}
+
+int rcp_arls_draw(const double *d_cdf, const double *d_dist, int64_t n, int64_t row_lo,
+                  double mass_ratio, const double *d_total_mass, uint64_t key0, uint64_t key1,
+                  int64_t q, int64_t offset, int64_t *d_rows_out, double *d_prob_out,
+                  const double *d_U, int R, double *d_urow_out, int *d_status, void *stream) {
+  if (q < 0 || n < 1 || !d_cdf || !d_dist || !d_rows_out || !d_prob_out) return RCP_ERR_ARG;
+  if (d_urow_out && (!d_U || R < 1)) return RCP_ERR_ARG;
+  if (q == 0) return RCP_OK;
+  arls_draw_kernel<<<(unsigned)ceil_div(q, 256), 256, 0, RCP_STREAM(stream)>>>(
+      d_cdf, d_dist, n, row_lo, mass_ratio, d_total_mass, key0, key1, q, offset, d_rows_out,
+      d_prob_out, d_U, R, d_urow_out, d_status);
+  RCP_LAUNCH_CHECK("arls_draw");
+  return RCP_OK;
+}
+
+int rcp_batch_fold(const int64_t *d_perm, const int64_t *d_rows, const double *d_prob, int64_t J,
+                   const double *d_U, int64_t u_row_lo, const double *d_urows, int R, int first,
+                   int64_t *d_Xi, double *d_pmp_i, double *d_H, void *stream) {
+  if (J < 0 || R < 1 || (J > 0 && (!d_rows || !d_prob || !d_Xi || !d_pmp_i || !d_H)))
+    return RCP_ERR_ARG;
+  if (!d_urows && !d_U && J > 0) return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  batch_fold_kernel<<<(unsigned)ceil_div(J * 32, 256), 256, 0, RCP_STREAM(stream)>>>(
+      d_perm, d_rows, d_prob, J, d_U, u_row_lo, d_urows, R, first, d_Xi, d_pmp_i, d_H);
+  RCP_LAUNCH_CHECK("batch_fold");
+  return RCP_OK;
+}
+
+int rcp_sts_depth(int64_t n, int leaf) {
+  if (n <= 0 || leaf < 1) return 0;
+  int64_t nl = ceil_div(n, leaf);
+  int d = 0;
+  while ((1LL << d) < nl) ++d;
+  return d;
+}
+
+size_t rcp_sts_tree_doubles(int64_t n, int leaf, int R) {
+  if (n <= 0) return 0;
+  int d = rcp_sts_depth(n, leaf);
+  return (size_t)((2LL << d) - 1) * (size_t)(R * (R + 1) / 2);
+}
+
+int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree, void *stream) {
+  if (R < 1 || R > RCP_MAX_RANK || leaf < 1 || leaf > kMaxLeaf || n < 0) return RCP_ERR_ARG;
+  if (n == 0) return RCP_OK;
+  if (!d_U || !d_tree) return RCP_ERR_ARG;
+  cudaStream_t st = RCP_STREAM(stream);
+  const int Rt = R * (R + 1) / 2;
+  const int depth = rcp_sts_depth(n, leaf);
+  const int64_t nleaves = ceil_div(n, leaf);
+  const int64_t width = 1LL << depth;
+  double *lvl = d_tree + (width - 1) * (int64_t)Rt;
+  int64_t g = nleaves < 16LL * sm_count() ? nleaves : 16LL * sm_count();
+  sts_leaf_kernel<<<(unsigned)g, 128, sizeof(double) * leaf * R, st>>>(d_U, n, R, leaf, nleaves,
+                                                                      lvl);
+  RCP_LAUNCH_CHECK("sts_leaf");
+  if (width > nleaves) {
+    int64_t len = (width - nleaves) * Rt;
+    int64_t b = ceil_div(len, 256);
+    if (b > 8LL * sm_count()) b = 8LL * sm_count();
+    sts_zero_kernel<<<(unsigned)b, 256, 0, st>>>(lvl + nleaves * Rt, len);
+    RCP_LAUNCH_CHECK("sts_pad");
+  }
+  for (int lev = depth - 1; lev >= 0; --lev) {
+    const int64_t nodes = 1LL << lev;
+    double *parent = d_tree + (nodes - 1) * (int64_t)Rt;
+    double *child = d_tree + (2 * nodes - 1) * (int64_t)Rt;
+    int64_t b = ceil_div(nodes * Rt, 256);
+    if (b > 8LL * sm_count()) b = 8LL * sm_count();
+    sts_level_kernel<<<(unsigned)b, 256, 0, st>>>(child, parent, nodes, Rt);
+    RCP_LAUNCH_CHECK("sts_level");
+  }
+  return RCP_OK;
+}
+
+int rcp_sts_cond(const double *d_chain_pinv, const double *d_grams, int N, int i, int k, int R,
+                 double *d_M, void *stream) {
+  if (R < 1 || R > RCP_MAX_RANK || N < 2 || !d_chain_pinv || !d_grams || !d_M) return RCP_ERR_ARG;
+  sts_cond_kernel<<<(unsigned)ceil_div(R * R, 256), 256, 0, RCP_STREAM(stream)>>>(
+      d_chain_pinv, d_grams, N, i, k, R, d_M);
+  RCP_LAUNCH_CHECK("sts_cond");
+  return RCP_OK;
+}
+
+int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
+                 int64_t row_lo, const double *d_M, const double *d_H_in, int64_t J,
+                 uint64_t key0, uint64_t key1, const double *d_override, const double *d_rin,
+                 const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi, double *d_pmp_i,
+                 double *d_resid, double *d_urow_out, int *d_status, void *stream) {
+  if (R < 1 || R > RCP_MAX_RANK || leaf < 1 || leaf > kMaxLeaf || J < 0 || n < 0) return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  if (n == 0 || !d_tree || !d_U || !d_M || !d_Xi || !d_pmp_i || !d_urow_out) return RCP_ERR_ARG;
+  const int depth = rcp_sts_depth(n, leaf);
+  int warps = 8;
+  const size_t cap = 200 * 1024;
+  while (warps > 1 && WalkSmem::bytes(R, warps, leaf) > cap) --warps;
+  size_t smem = WalkSmem::bytes(R, warps, leaf);
+  if (smem > 220 * 1024) return RCP_ERR_ARG;
+  static bool attr = false;
+  if (!attr) {
+    RCP_CUDA_TRY(cudaFuncSetAttribute(sts_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      220 * 1024));
+    attr = true;
+  }
+  int64_t want = ceil_div(J, warps);
+  int64_t grid = want < 8LL * sm_count() ? want : 8LL * sm_count();
+  sts_walk_kernel<<<(unsigned)grid, warps * 32, smem, RCP_STREAM(stream)>>>(
+      d_tree, d_U, n, R, leaf, depth, row_lo, d_M, d_H_in, J, key0, key1, d_override, d_rin, d_sel,
+      sel_value, d_Xi, d_pmp_i, d_resid, d_urow_out, d_status);
+  RCP_LAUNCH_CHECK("sts_walk");
+  return RCP_OK;
+}
+
+int rcp_sts_rank_walk(const double *d_node_grams, int depth, int P, const int32_t *d_leaf_rank,
+                      const double *d_M, const double *d_H, int64_t J, int R, uint64_t key0,
+                      uint64_t key1, const double *d_override, int32_t *d_owner, double *d_r_out,
+                      double *d_pmp_i, int *d_status, void *stream) {
+  if (J < 0 || R < 1 || depth < 0 || P < 1 || !d_leaf_rank || !d_owner || !d_r_out || !d_pmp_i)
+    return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  if (depth > 0 && (!d_node_grams || !d_M || !d_H)) return RCP_ERR_ARG;
+  sts_rank_walk_kernel<<<(unsigned)ceil_div(J * 32, 256), 256, 0, RCP_STREAM(stream)>>>(
+      d_node_grams, depth, P, d_leaf_rank, d_M, d_H, J, R, key0, key1, d_override, d_owner,
+      d_r_out, d_pmp_i, d_status);
+  RCP_LAUNCH_CHECK("sts_rank_walk");
+  return RCP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,478 @@
+"""Device-resident accumulator-stationary sketched ALS (the hot path, B200-native).
+
+One `RankState` per GPU rank holds that rank's factor row blocks, per-mode sorted
+nonzero stores, sampler structures and batch buffers -- all in HBM.  The round is written
+bulk-synchronously over a list of rank states and a communicator:
+
+* SPMD (`dist.TorchComm`, one process per GPU, NCCL): the list holds one rank state;
+* simulation (`LocalComm`, one process, P virtual ranks): the list holds all P states and
+  collectives are list operations -- the reference's own execution model (ref grid.py:1-20),
+  used to check CP-ARLS-LEV parity at P > 1 on a single GPU.
+
+Schedule of one mode-k solve (ref schedules.py:227-258, als.py:196-208):
+  sampling  -> STS walk (rank-level levels replicated, local tree per owner) or CP-ARLS-LEV
+               draws, then the sampled-row all-gather (J (N-1) (R+2) / R words)
+  weights   -> w = 1/sqrt(J p)
+  Gs        -> (H.w)^T (H.w), pinv           (replicated, no collective)
+  mttkrp    -> local sampled MTTKRP into the stationary row block (no collective)
+  update    -> U_k = M Gs^+, column sums of squares (R-word reduction), renormalise
+  rebuild   -> per-rank block Gram (R x R all-gather), tree / leverage rebuild
+"""
+
+from __future__ import annotations
+
+import math
+import time
+
+import numpy as np
+
+from . import rng
+from .device import torch
+from .grid import ProcessorGrid, optimal_grid
+from .ops import ops_for
+from .store import build_store
+
+PHASES = ("sampling", "gather", "mttkrp", "reduction", "postprocess", "rebuild")
+
+
+def default_leaf(n, R, budget_bytes=4 << 30):
+    """Rows per tree leaf: 16, doubled until the padded tree fits the budget (<= 64)."""
+    Rt = R * (R + 1) // 2
+    L = 16
+    while L < 64:
+        nl = max(1, math.ceil(n / L))
+        nodes = 2 * (1 << max(0, math.ceil(math.log2(nl)))) - 1
+        if nodes * Rt * 8 <= budget_bytes:
+            break
+        L *= 2
+    return L
+
+
+class LocalComm:
+    """P virtual ranks in one process (list collectives, rank order)."""
+
+    def __init__(self, P):
+        self.P = int(P)
+        self.ranks = list(range(self.P))
+
+    def all_gather(self, local):            # local: list (one per local rank) of tensors
+        return list(local)
+
+    def all_gather_v(self, local, counts):  # counts known to all ranks
+        return list(local)
+
+    def all_gather_obj(self, local):
+        return list(local)
+
+    def barrier(self):
+        pass
+
+
+class RankState:
+    def __init__(self, rank, grid: ProcessorGrid, dev, dims, R, J, sampler, seed, leaf=None):
+        t = torch()
+        self.t = t
+        self.rank = int(rank)
+        self.grid = grid
+        self.P = grid.P
+        self.dev = dev
+        self.dims = tuple(int(d) for d in dims)
+        self.N = len(self.dims)
+        self.R, self.J = int(R), int(J)
+        self.sampler = sampler
+        self.seed = int(seed)
+        self.ops = ops_for(dev)
+        N, R, J = self.N, self.R, self.J
+        self.lo = [grid.block_range(j, rank)[0] for j in range(N)]
+        self.n = [grid.block_range(j, rank)[1] - self.lo[j] for j in range(N)]
+        self.leaf_cfg = leaf
+        self.leaf = [None] * N
+        f64 = dict(dtype=t.float64, device=dev)
+        self.U = [t.zeros((self.n[j], R), **f64) for j in range(N)]
+        self.grams = t.zeros((N, R, R), **f64)
+        self.block_grams = [None] * N          # (P, R, R) per mode (P > 1)
+        self.trees = [None] * N
+        self.rank_tree = [None] * N            # (node_grams, leaf_rank, depth) per mode
+        self.dist = [None] * N
+        self.cdf = [None] * N
+        self.mass = [t.zeros(1, **f64) for _ in range(N)]
+        self.C_host = [None] * N               # P rank masses per mode (ARLS)
+        self.stores = [None] * N
+        self.X = t.full((N, J), -1, dtype=t.int64, device=dev)
+        self.pmp = t.ones((N, J), **f64)
+        self.prob = t.ones(J, **f64)
+        self.w = t.ones(J, **f64)
+        self.resid = t.zeros(J, **f64)
+        self.H = t.ones((J, R), **f64)
+        self.urow = t.zeros((J, R), **f64)
+        self.owner = t.zeros(J, dtype=t.int32, device=dev)
+        self.rtop = t.zeros(J, **f64)
+        self.rows_tmp = t.zeros(J, dtype=t.int64, device=dev)
+        self.prob_tmp = t.zeros(J, **f64)
+        self.urow_tmp = t.zeros((J, R), **f64) if self.P > 1 else None
+        self.perm = t.zeros(J, dtype=t.int64, device=dev)
+        self.chain_pinv = t.zeros((R, R), **f64)
+        self.M = t.zeros((R, R), **f64)
+        self.Gs = t.zeros((R, R), **f64)
+        self.Gsp = t.zeros((R, R), **f64)
+        self.Gp = t.zeros((R, R), **f64)
+        self.colsq = t.zeros(R, **f64)
+        self.sigma = t.ones(R, **f64)
+        self.Mout = t.zeros((max(self.n) if N else 0, R), **f64)
+        self.stats = t.zeros(8, dtype=t.int64, device=dev)
+        self.block_gram_buf = t.zeros((R, R), **f64)
+
+    # -------------------------------------------------------------- set-up
+    def load_factor_blocks(self, full_factors):
+        """full_factors: list of host (I_j x R) arrays; keep this rank's block."""
+        t = self.t
+        for j in range(self.N):
+            blk = np.ascontiguousarray(full_factors[j][self.lo[j]:self.lo[j] + self.n[j]],
+                                       dtype=np.float64)
+            self.U[j].copy_(t.from_numpy(blk))
+
+    def build_stores(self, idx, vals):
+        """idx/vals: device COO of the whole tensor (or a superset); keeps, per mode, the
+        nonzeros whose mode-j row lies in this rank's block (ref matricization.py:187-198)."""
+        for j in range(self.N):
+            rows = idx[:, j]
+            sel = (rows >= self.lo[j]) & (rows < self.lo[j] + self.n[j])
+            if self.P == 1:
+                self.stores[j] = build_store(self.dims, idx, vals, j, self.lo[j], self.lo[j] + self.n[j])
+            else:
+                self.stores[j] = build_store(self.dims, idx[sel], vals[sel], j, self.lo[j],
+                                             self.lo[j] + self.n[j])
+
+    def leaf_of(self, j):
+        if self.leaf[j] is None:
+            if self.leaf_cfg is not None:
+                self.leaf[j] = int(max(1, min(64, int(self.leaf_cfg))))
+            else:
+                self.leaf[j] = default_leaf(max(self.n[j], 1), self.R)
+        return self.leaf[j]
+
+    # ------------------------------------------------------------- rebuild
+    def block_gram(self, k):
+        return self.ops.gram(self.U[k], out=self.block_gram_buf)
+
+    def set_gram(self, k, blocks):
+        """blocks: list of P (R x R) tensors in rank order -> ordered sum (ref grid.py:295-297)."""
+        g = blocks[0].clone()
+        for b in blocks[1:]:
+            g += b
+        self.grams[k].copy_(g)
+        if self.P > 1:
+            self.block_grams[k] = torch().stack([b for b in blocks])
+
+    def build_tree(self, k):
+        if self.n[k] > 0:
+            self.trees[k] = self.ops.sts_build(self.U[k], self.leaf_of(k), self.trees[k])
+        if self.P > 1:
+            self._build_rank_tree(k)
+
+    def _build_rank_tree(self, k):
+        """Padded complete tree over ranks in global row order (ref samplers.py:239-275)."""
+        t = self.t
+        P, R = self.P, self.R
+        depth = int(math.ceil(math.log2(P))) if P > 1 else 0
+        width = 1 << depth
+        order = self.grid.row_order(k)
+        leaf_rank = np.full(width, -1, dtype=np.int32)
+        leaf_rank[:P] = order
+        leaves = t.zeros((width, R, R), dtype=t.float64, device=self.dev)
+        leaves[:P] = self.block_grams[k][t.as_tensor(order, device=self.dev)]
+        levels = [None] * (depth + 1)
+        levels[depth] = leaves
+        for lev in range(depth - 1, -1, -1):
+            levels[lev] = levels[lev + 1].reshape(-1, 2, R, R).sum(dim=1)
+        node_grams = t.cat([lv.reshape(-1) for lv in levels]).contiguous()
+        self.rank_tree[k] = (node_grams, t.as_tensor(leaf_rank, device=self.dev), depth)
+
+    def arls_local(self, k):
+        """Local leverage distribution of mode k given the replicated Gram (ref
+        samplers.py:122-135); returns the device mass scalar."""
+        ops = self.ops
+        ops.pinv(self.grams[k], out=self.Gp)
+        n = self.n[k]
+        if self.dist[k] is None or self.dist[k].shape[0] != n:
+            self.dist[k] = self.t.zeros(n, dtype=self.t.float64, device=self.dev)
+            self.cdf[k] = self.t.zeros(n, dtype=self.t.float64, device=self.dev)
+        if n > 0:
+            ops.arls_build(self.U[k], self.Gp, self.dist[k], self.cdf[k], self.mass[k])
+        else:
+            self.mass[k].zero_()
+        return self.mass[k]
+
+    # ------------------------------------------------------------ sampling
+    def chain(self, k):
+        self.ops.pinv(self.grams, n_chain=self.N, skip=k, out=self.chain_pinv)
+
+    def sts_mode(self, i, k, rnd, first, override=None):
+        """Walk all samples for constant mode i; this rank completes the samples whose
+        leaf lies in its block (all of them when P == 1)."""
+        ops = self.ops
+        ops.sts_cond(self.chain_pinv, self.grams, i, k, self.M)
+        key = rng.stream_key(self.seed, rng.WALK_UNIFORM, rnd, k, i)
+        H_in = None if first else self.H
+        if self.P > 1:
+            node_grams, leaf_rank, depth = self.rank_tree[i]
+            ops.sts_rank_walk(node_grams, depth, self.P, leaf_rank, self.M, self.H if not first else self._ones_H(),
+                              self.J, key, override, self.owner, self.rtop, self.pmp[i])
+            sel, rin = self.owner, self.rtop
+        else:
+            self.pmp[i].fill_(1.0)
+            sel, rin = None, None
+        if self.n[i] > 0:
+            ops.sts_walk(self.trees[i], self.U[i], self.leaf_of(i), self.lo[i], self.M, H_in,
+                         self.J, key, override if self.P == 1 else None, rin, sel, self.rank,
+                         self.X[i], self.pmp[i], self.resid, self.urow)
+
+    def _ones_H(self):
+        if not hasattr(self, "_H1"):
+            self._H1 = self.t.ones((self.J, self.R), dtype=self.t.float64, device=self.dev)
+        return self._H1
+
+    def fold_urow(self, first):
+        self.ops.hadamard_rows(self.H, self.urow, init=first)
+
+    def arls_draw(self, i, k, rnd, quota, W):
+        """This rank's quota of draws for constant mode i (ref samplers.py:169-181);
+        staged in rows_tmp/prob_tmp (and urow_tmp when P > 1)."""
+        q = int(quota[self.rank]) if self.P > 1 else self.J
+        if q == 0:
+            return 0
+        key = rng.stream_key(self.seed, rng.LOCAL_DRAW, rnd, k, i, self.rank)
+        if self.P > 1:
+            ratio = float(self.C_host[i][self.rank]) / W
+            tmass = None
+        else:
+            ratio = 1.0
+            tmass = self.mass[i]
+        self.ops.arls_draw(self.cdf[i], self.dist[i], self.lo[i], ratio, tmass, key, q, 0,
+                           self.rows_tmp, self.prob_tmp,
+                           U=self.U[i] if self.P > 1 else None,
+                           urow_out=self.urow_tmp if self.P > 1 else None)
+        return q
+
+    def arls_fold(self, i, k, rnd, first, rows, probs, urows):
+        key = rng.stream_key(self.seed, rng.SHUFFLE, rnd, k, i)
+        perm = rng.permutation(key, self.J)
+        self.perm.copy_(self.t.from_numpy(perm), non_blocking=False)
+        self.ops.batch_fold(self.perm, rows, probs, self.U[i] if urows is None else None,
+                            self.lo[i], urows, first, self.X[i], self.pmp[i], self.H)
+
+    # --------------------------------------------------------------- solve
+    def weights(self):
+        self.ops.weights(self.pmp, self.prob, self.w)
+
+    def sketched_system(self):
+        """Gs = (H.w)^T (H.w) and its pseudo-inverse (ref schedules.py:104-109, :258)."""
+        self.ops.gram(self.H, scale=self.w, out=self.Gs)
+        self.ops.pinv(self.Gs, out=self.Gsp)
+
+    def mttkrp(self, k):
+        n = self.n[k]
+        out = self.Mout[:n]
+        if n > 0:
+            st = self.stores[k]
+            self.ops.sampled_mttkrp(st, self.X, k, self.H, self.w, out, self.stats,
+                                    cap=st.capacity(self.J))
+        return out
+
+    def update(self, k):
+        n = self.n[k]
+        if n > 0:
+            self.ops.update(self.Mout[:n], self.Gsp, self.U[k], self.colsq)
+        else:
+            self.colsq.zero_()
+        return self.colsq
+
+    def renormalize(self, k, colsq_total):
+        self.colsq.copy_(colsq_total)
+        if self.n[k] > 0:
+            self.ops.renormalize(self.U[k], self.colsq, self.sigma)
+        else:
+            self.sigma.copy_(self.t.sqrt(self.colsq))
+
+
+class Cluster:
+    """Bulk-synchronous driver over the rank states of this process."""
+
+    def __init__(self, ranks, comm, sampler, J, seed):
+        self.ranks = ranks
+        self.comm = comm
+        self.sampler = sampler
+        self.J = int(J)
+        self.seed = int(seed)
+        self.N = ranks[0].N
+        self.P = ranks[0].P
+        self.timings = {p: 0.0 for p in PHASES}
+        self.timed = False
+
+    def _tick(self, phase, t0):
+        if not self.timed:
+            return t0
+        torch().cuda.synchronize()
+        t1 = time.perf_counter()
+        self.timings[phase] += t1 - t0
+        return t1
+
+    # ------------------------------------------------------------ rebuild
+    def rebuild(self, k):
+        """(ref als.py:114-126)"""
+        blocks = self.comm.all_gather([r.block_gram(k) for r in self.ranks])
+        for r in self.ranks:
+            r.set_gram(k, [b for b in blocks])
+        if self.sampler == "sts":
+            for r in self.ranks:
+                r.build_tree(k)
+        else:
+            masses = [r.arls_local(k) for r in self.ranks]
+            if self.P > 1:
+                allm = self.comm.all_gather(masses)
+                C = np.array([float(m.item()) for m in allm])
+                for r in self.ranks:
+                    r.C_host[k] = C
+
+    # ------------------------------------------------------------ sampling
+    def sample(self, k, rnd, override=None):
+        N = self.N
+        for r in self.ranks:
+            r.X[k].fill_(-1)
+            r.pmp[k].fill_(1.0)
+        if self.sampler == "sts":
+            for r in self.ranks:
+                r.chain(k)
+            first = True
+            for i in range(N):
+                if i == k:
+                    continue
+                ov = None
+                if override is not None:
+                    ov = override[i]
+                for r in self.ranks:
+                    r.sts_mode(i, k, rnd, first, override=ov)
+                if self.P > 1:
+                    self._exchange_walk(i)
+                for r in self.ranks:
+                    r.fold_urow(first)
+                first = False
+        else:
+            first = True
+            for i in range(N):
+                if i == k:
+                    continue
+                quota, W = self._arls_quota(i, k, rnd)
+                for r in self.ranks:
+                    r.arls_draw(i, k, rnd, quota, W)
+                if self.P > 1:
+                    counts = [int(q) for q in quota]
+                    rows = self.comm.all_gather_v([r.rows_tmp for r in self.ranks], counts)
+                    probs = self.comm.all_gather_v([r.prob_tmp for r in self.ranks], counts)
+                    urs = self.comm.all_gather_v([r.urow_tmp for r in self.ranks], counts)
+                    t = torch()
+                    cat_rows = t.cat([rows[p][:counts[p]] for p in range(self.P)])
+                    cat_probs = t.cat([probs[p][:counts[p]] for p in range(self.P)])
+                    cat_urows = t.cat([urs[p][:counts[p]] for p in range(self.P)]).contiguous()
+                    for r in self.ranks:
+                        r.arls_fold(i, k, rnd, first, cat_rows.to(r.dev), cat_probs.to(r.dev),
+                                    cat_urows.to(r.dev))
+                else:
+                    for r in self.ranks:
+                        r.arls_fold(i, k, rnd, first, r.rows_tmp, r.prob_tmp, None)
+                first = False
+        for r in self.ranks:
+            r.weights()
+
+    def _arls_quota(self, i, k, rnd):
+        """Consistent multinomial split of J over rank masses (ref samplers.py:138-145);
+        trivial at P = 1 (zero-mass is raised on the device)."""
+        if self.P == 1:
+            return np.array([self.J]), 1.0
+        C = self.ranks[0].C_host[i]
+        W = float(C.sum())
+        if W <= 0.0:
+            raise ValueError("mode %d has zero total leverage mass" % i)
+        gen = rng.stream(self.seed, rng.MULTINOMIAL, rnd, k, i)
+        return gen.multinomial(self.J, C / W), W
+
+    def _exchange_walk(self, i):
+        """After the local walks, every rank holds the finished samples it owns; gather
+        (row, step probability, residual, factor row) to all ranks in rank order
+        (ref schedules.py:239-247: R+2 words per sample per constant mode)."""
+        t = torch()
+        P = self.P
+        owner = self.ranks[0].owner
+        counts = t.bincount(owner.long(), minlength=P).cpu().tolist()
+        packs = []
+        for r in self.ranks:
+            mine = (r.owner == r.rank).nonzero().squeeze(1)
+            pk = t.cat([r.X[i][mine].to(t.float64).unsqueeze(1), r.pmp[i][mine].unsqueeze(1),
+                        r.resid[mine].unsqueeze(1), r.urow[mine]], dim=1).contiguous()
+            packs.append(pk)
+        got = self.comm.all_gather_v(packs, counts)
+        for r in self.ranks:
+            for q in range(P):
+                sel = (r.owner == q).nonzero().squeeze(1)
+                if sel.numel() == 0:
+                    continue
+                blk = got[q][:counts[q]].to(r.dev)
+                r.X[i][sel] = blk[:, 0].to(t.int64)
+                r.pmp[i][sel] = blk[:, 1]
+                r.resid[sel] = blk[:, 2]
+                r.urow[sel] = blk[:, 3:]
+
+    # -------------------------------------------------------------- solve
+    def solve(self, k, rnd, override=None, injected=None):
+        t0 = time.perf_counter()
+        if injected is None:
+            self.sample(k, rnd, override=override)
+        else:
+            for r in self.ranks:
+                injected(r)
+        t0 = self._tick("sampling", t0)
+        for r in self.ranks:
+            r.sketched_system()
+            r.mttkrp(k)
+        t0 = self._tick("mttkrp", t0)
+        parts = self.comm.all_gather([r.update(k) for r in self.ranks])
+        tot = parts[0].clone()
+        for p in parts[1:]:
+            tot += p.to(tot.device)
+        for r in self.ranks:
+            r.renormalize(k, tot.to(r.dev))
+        t0 = self._tick("postprocess", t0)
+        self.rebuild(k)
+        self._tick("rebuild", t0)
+
+    def check(self, where=""):
+        for r in self.ranks:
+            r.ops.status.check(where)
+
+    def round(self, rnd, check=True):
+        for k in range(self.N):
+            self.solve(k, rnd)
+            if check:
+                self.check("after round %d mode %d solve" % (rnd, k))
+
+
+def make_local_cluster(dims, idx, vals, R, J, sampler, seed, P=1, grid_dims=None, leaf=None,
+                       factors=None, trial=0):
+    """Single-process cluster (P virtual ranks on the current device).  idx/vals are CUDA
+    tensors; factors default to the reference initialisation (ref als.py:99-105)."""
+    from .device import require_cuda
+    dev = require_cuda()
+    grid = ProcessorGrid(dims, grid_dims) if grid_dims is not None else optimal_grid(dims, P)
+    if factors is None:
+        from .linalg import init_factors
+        factors, _ = init_factors(dims, R, seed, trial)
+    ranks = []
+    for p in range(grid.P):
+        r = RankState(p, grid, dev, dims, R, J, sampler, seed, leaf=leaf)
+        r.load_factor_blocks(factors)
+        r.build_stores(idx, vals)
+        ranks.append(r)
+    cl = Cluster(ranks, LocalComm(grid.P), sampler, J, seed)
+    for j in range(len(dims)):
+        cl.rebuild(j)
+    return cl

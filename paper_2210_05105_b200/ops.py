@@ -1,0 +1,169 @@
+"""Typed wrappers over the C ABI taking torch CUDA tensors (stream = torch's current
+stream).  One `Ops` object per device owns the status word and reusable workspaces."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .device import Status, ptr, stream_handle, torch
+
+CUTOFF = 1e-10   # ref linalg.py:16
+
+
+class Ops:
+    def __init__(self, dev):
+        self.dev = dev
+        self.status = Status(dev)
+        self._ws = {}
+        self.lib = _lib.lib()
+
+    # ------------------------------------------------------------------ workspace
+    def ws(self, name, nbytes):
+        t = torch()
+        nbytes = max(int(nbytes), 256)
+        buf = self._ws.get(name)
+        if buf is None or buf.numel() < nbytes:
+            buf = t.empty(nbytes, dtype=t.uint8, device=self.dev)
+            self._ws[name] = buf
+        return buf
+
+    def _c(self, name, *args):
+        rc = getattr(self.lib, name)(*args)
+        if rc != _lib.OK:
+            _lib.check(rc, name)
+
+    # ------------------------------------------------------------------- dense
+    def gram(self, U, scale=None, out=None):
+        t = torch()
+        n, R = U.shape
+        if out is None:
+            out = t.empty((R, R), dtype=t.float64, device=self.dev)
+        w = self.ws("gram", self.lib.rcp_gram_ws_bytes(n, R))
+        self._c("rcp_gram", ptr(U), ptr(scale), n, R, ptr(out), ptr(w), stream_handle())
+        return out
+
+    def pinv(self, G, n_chain=0, skip=-1, cutoff=CUTOFF, out=None, chain_out=None):
+        t = torch()
+        R = G.shape[-1]
+        if out is None:
+            out = t.empty((R, R), dtype=t.float64, device=self.dev)
+        self._c("rcp_pinv", ptr(G), int(n_chain), int(skip), int(R), float(cutoff),
+                ptr(chain_out), ptr(out), self.status.ptr, stream_handle())
+        return out
+
+    def update(self, M, B, out, colsq):
+        n, R = M.shape
+        w = self.ws("update", self.lib.rcp_update_ws_bytes(n, R))
+        self._c("rcp_update", ptr(M), n, R, ptr(B), ptr(out), ptr(colsq), ptr(w),
+                self.status.ptr, stream_handle())
+
+    def renormalize(self, U, colsq, sigma):
+        n, R = U.shape
+        self._c("rcp_renormalize", ptr(U), n, R, ptr(colsq), ptr(sigma), stream_handle())
+
+    def weights(self, pmp, prob, w):
+        N, J = pmp.shape
+        self._c("rcp_weights", ptr(pmp), N, J, ptr(prob), ptr(w), self.status.ptr,
+                stream_handle())
+
+    def hadamard_rows(self, H, urow, init):
+        J, R = H.shape
+        self._c("rcp_hadamard_rows", ptr(H), ptr(urow), J, R, 1 if init else 0, stream_handle())
+
+    # -------------------------------------------------------------------- ARLS
+    def arls_build(self, U, Gp, dist, cdf, mass):
+        n, R = U.shape
+        w = self.ws("arls", self.lib.rcp_arls_build_ws_bytes(n, R))
+        self._c("rcp_arls_build", ptr(U), n, R, ptr(Gp), ptr(dist), ptr(cdf), ptr(mass), ptr(w),
+                stream_handle())
+
+    def arls_draw(self, cdf, dist, row_lo, ratio, total_mass, key, q, offset, rows_out,
+                  prob_out, U=None, urow_out=None):
+        n = cdf.shape[0]
+        R = U.shape[1] if U is not None else 0
+        self._c("rcp_arls_draw", ptr(cdf), ptr(dist), n, int(row_lo), float(ratio),
+                ptr(total_mass), key[0], key[1], int(q), int(offset), ptr(rows_out),
+                ptr(prob_out), ptr(U), R, ptr(urow_out), self.status.ptr, stream_handle())
+
+    def batch_fold(self, perm, rows, prob, U, u_row_lo, urows, first, Xi, pmp_i, H):
+        J, R = H.shape
+        self._c("rcp_batch_fold", ptr(perm), ptr(rows), ptr(prob), J, ptr(U), int(u_row_lo),
+                ptr(urows), R, 1 if first else 0, ptr(Xi), ptr(pmp_i), ptr(H), stream_handle())
+
+    # --------------------------------------------------------------------- STS
+    def sts_depth(self, n, leaf):
+        return int(self.lib.rcp_sts_depth(int(n), int(leaf)))
+
+    def sts_build(self, U, leaf, tree=None):
+        t = torch()
+        n, R = U.shape
+        nd = int(self.lib.rcp_sts_tree_doubles(n, int(leaf), R))
+        if tree is None or tree.numel() < nd:
+            tree = t.empty(max(nd, 1), dtype=t.float64, device=self.dev)
+        self._c("rcp_sts_build", ptr(U), n, R, int(leaf), ptr(tree), stream_handle())
+        return tree
+
+    def sts_cond(self, chain_pinv, grams, i, k, out):
+        N, R = grams.shape[0], grams.shape[1]
+        self._c("rcp_sts_cond", ptr(chain_pinv), ptr(grams), N, int(i), int(k), R, ptr(out),
+                stream_handle())
+
+    def sts_walk(self, tree, U, leaf, row_lo, M, H_in, J, key, override, rin, sel, sel_value,
+                 Xi, pmp_i, resid, urow):
+        n, R = U.shape
+        self._c("rcp_sts_walk", ptr(tree), ptr(U), n, R, int(leaf), int(row_lo), ptr(M),
+                ptr(H_in), int(J), key[0], key[1], ptr(override), ptr(rin), ptr(sel),
+                int(sel_value), ptr(Xi), ptr(pmp_i), ptr(resid), ptr(urow), self.status.ptr,
+                stream_handle())
+
+    def sts_rank_walk(self, node_grams, depth, P, leaf_rank, M, H, J, key, override, owner,
+                      r_out, pmp_i):
+        R = M.shape[0]
+        self._c("rcp_sts_rank_walk", ptr(node_grams), int(depth), int(P), ptr(leaf_rank),
+                ptr(M), ptr(H), int(J), R, key[0], key[1], ptr(override), ptr(owner),
+                ptr(r_out), ptr(pmp_i), self.status.ptr, stream_handle())
+
+    # ------------------------------------------------------------------ MTTKRP
+    def mttkrp_ws(self, J, cap, n_rows, R):
+        return self.ws("mttkrp", self.lib.rcp_mttkrp_ws_bytes(int(J), int(cap), int(n_rows), int(R)))
+
+    def sampled_mttkrp(self, store, X, k, H, w, out, stats, cap=None):
+        N, J = X.shape
+        R = H.shape[1]
+        cap = store.nnz if cap is None else cap
+        ws = self.mttkrp_ws(J, cap, store.n_rows, R)
+        strides = np.ascontiguousarray(store.strides, dtype=np.int64)
+        self._c("rcp_sampled_mttkrp", ptr(store.keys), ptr(store.colptr), store.n_cols,
+                ptr(store.rows), ptr(store.vals), store.n_rows, ptr(X), N, J, int(k),
+                strides.ctypes.data, ptr(H), ptr(w), R, ptr(out), ptr(stats), ptr(ws),
+                ws.numel(), self.status.ptr, stream_handle())
+
+    def fiber_lookup(self, store, X, k, lo, counts):
+        N, J = X.shape
+        strides = np.ascontiguousarray(store.strides, dtype=np.int64)
+        self._c("rcp_fiber_lookup", ptr(store.keys), store.n_cols, ptr(store.colptr), ptr(X), N,
+                J, int(k), strides.ctypes.data, ptr(lo), ptr(counts), stream_handle())
+
+    def fiber_expand(self, lo, off, store, row_out, col_out, val_out):
+        J = lo.shape[0]
+        self._c("rcp_fiber_expand", ptr(lo), ptr(off), J, ptr(store.rows), ptr(store.vals),
+                ptr(row_out), ptr(col_out), ptr(val_out), stream_handle())
+
+    def csr_spmm(self, row_ptr, col, val, H, scale, out):
+        n_rows = row_ptr.shape[0] - 1
+        R = H.shape[1]
+        self._c("rcp_csr_spmm", ptr(row_ptr), n_rows, ptr(col), ptr(val), ptr(H), ptr(scale), R,
+                ptr(out), stream_handle())
+
+
+_OPS = {}
+
+
+def ops_for(dev) -> Ops:
+    key = str(dev)
+    o = _OPS.get(key)
+    if o is None:
+        o = Ops(dev)
+        _OPS[key] = o
+    return o

@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+reference's golden vectors.  Bars (BASELINE.json north star): sampled indices and sampled
+nonzero sets bit-exact; MTTKRP outputs and factors within 1e-9 relative (fp64); fit
+after a fixed number of rounds within 1e-6."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import cuda_ok, golden
+from oracle import randcp_oracle as O
+from paper_2210_05105_b200 import synth
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+REL = 1e-9
+
+
+def rel_err(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    scale = max(np.abs(b).max(), 1e-300) if b.size else 1.0
+    return float(np.abs(a - b).max() / scale) if a.size else 0.0
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2210_05105_b200 as P
+    return P
+
+
+# ------------------------------------------------------------------------ rng
+def test_device_uniforms_match_reference(pkg):
+    import torch
+    from paper_2210_05105_b200 import _lib, rng
+    g = golden("rng.npz")
+    for row, draws in zip(g["ctx"], g["draws"]):
+        seed, purpose, n = int(row[0]), int(row[1]), int(row[2])
+        k = rng.stream_key(seed, purpose, *[int(v) for v in row[3:3 + n]])
+        out = torch.empty(13, dtype=torch.float64, device="cuda")
+        _lib.call("rcp_uniform", k[0], k[1], 0, 13, out.data_ptr(),
+                  torch.cuda.current_stream().cuda_stream)
+        assert np.array_equal(out.cpu().numpy(), draws)
+
+
+# ---------------------------------------------------------------------- dense
+@pytest.mark.parametrize("R", [1, 3, 8, 25, 50, 75, 100, 128])
+def test_gram_and_pinv_full_rank(pkg, R):
+    gen = np.random.default_rng(R)
+    U = gen.standard_normal((5 * R + 37, R))
+    G = pkg.gram(U)
+    assert rel_err(G, U.T @ U) < 1e-13
+    Gp = pkg.pseudo_inverse(G)
+    assert rel_err(Gp, O.sym_pinv(U.T @ U)) < 1e-9
+
+
+@pytest.mark.parametrize("R,rank", [(6, 3), (25, 10), (50, 49), (3, 0)])
+def test_pinv_rank_deficient_uses_cutoff(pkg, R, rank):
+    gen = np.random.default_rng(7)
+    B = gen.standard_normal((R, rank)) if rank else np.zeros((R, 1))
+    G = B @ B.T
+    assert rel_err(pkg.pseudo_inverse(G), O.sym_pinv(G)) < 1e-8
+
+
+def test_pinv_rejects_asymmetric(pkg):
+    G = np.eye(4)
+    G[0, 1] = 1e-3
+    with pytest.raises(ValueError):
+        pkg.pseudo_inverse(G)
+
+
+def test_hadamard_chain(pkg):
+    gen = np.random.default_rng(3)
+    grams = [gen.standard_normal((5, 5)) for _ in range(4)]
+    for skip in (None, 0, 2, 3):
+        assert np.array_equal(pkg.hadamard_gram_chain(grams, skip), O.hadamard_chain(grams, skip))
+
+
+# ------------------------------------------------------------------- samplers
+def _blocks(P, factors, g):
+    return [P.FactorBlocks.from_global(U, g, j) for j, U in enumerate(factors)]
+
+
+@pytest.mark.parametrize("gd", [(1, 1, 1), (2, 2, 1), (4, 2, 1)])
+def test_samplers_match_reference_golden(pkg, gd):
+    g0 = golden("samplers.npz")
+    dims = tuple(int(d) for d in g0["dims"])
+    factors = [g0["U%d" % j] for j in range(3)]
+    g = pkg.ProcessorGrid(dims, gd)
+    blocks = _blocks(pkg, factors, g)
+    grams = [pkg.gram(b) for b in blocks]
+    trees = [pkg.sts_build(b, grid=g) for b in blocks]
+    states = [pkg.arls_lev_build(b) for b in blocks]
+    tag = "x".join(map(str, gd))
+    for k in range(3):
+        cp = pkg.pseudo_inverse(pkg.hadamard_gram_chain(grams, skip=k))
+        b = pkg.sts_sample(trees, k, 512, cp, grams, blocks, seed=17, round_id=2, grid=g)
+        assert np.array_equal(b.X, g0["sts_%s_k%d_X" % (tag, k)])
+        assert rel_err(b.prob, g0["sts_%s_k%d_prob" % (tag, k)]) < 1e-12
+        assert rel_err(b.H, g0["sts_%s_k%d_H" % (tag, k)]) < 1e-14
+        a = pkg.arls_lev_sample(states, k, 512, factors, seed=19, round_id=3)
+        assert np.array_equal(a.X, g0["arls_%s_k%d_X" % (tag, k)])
+        assert rel_err(a.prob, g0["arls_%s_k%d_prob" % (tag, k)]) < 1e-12
+        w = pkg.sample_weights(a)
+        assert rel_err(w, g0["arls_%s_k%d_w" % (tag, k)]) < 1e-12
+
+
+def test_steered_walk_matches_reference(pkg):
+    g0 = golden("walk.npz")
+    factors = [g0["U%d" % j] for j in range(3)]
+    dims = tuple(U.shape[0] for U in factors)
+    g = pkg.ProcessorGrid(dims, (1, 1, 1))
+    blocks = _blocks(pkg, factors, g)
+    grams = [pkg.gram(b) for b in blocks]
+    k = int(g0["k"])
+    for leaf in (1, 2, 3, None):
+        trees = [pkg.sts_build(b, grid=g, leaf_block_size=leaf) for b in blocks]
+        cp = pkg.pseudo_inverse(pkg.hadamard_gram_chain(grams, skip=k))
+        b = pkg.sts_sample(trees, k, g0["override"].shape[0], cp, grams, blocks, seed=0,
+                           uniform_override=g0["override"])
+        assert np.array_equal(b.X, g0["X"]), leaf
+        assert rel_err(b.prob, g0["prob"]) < 1e-12
+
+
+def test_sts_distribution_matches_exact_leverage(pkg):
+    gen = np.random.default_rng(14)
+    dims = (4, 4, 3)
+    factors = [gen.standard_normal((d, 2)) for d in dims]
+    g = pkg.ProcessorGrid(dims, (1, 1, 1))
+    blocks = _blocks(pkg, factors, g)
+    grams = [pkg.gram(b) for b in blocks]
+    trees = [pkg.sts_build(b, grid=g) for b in blocks]
+    cp = pkg.pseudo_inverse(pkg.hadamard_gram_chain(grams, skip=2))
+    J = 50000
+    b = pkg.sts_sample(trees, 2, J, cp, grams, blocks, seed=15, grid=g)
+    ref = O.leverage_probs(factors, skip=2)
+    keys = b.X[:, 0] + 4 * b.X[:, 1]
+    emp = np.bincount(keys, minlength=16) / J
+    assert 0.5 * np.abs(emp - ref).sum() < 0.02
+    assert np.abs(b.prob - ref[keys]).max() < 1e-12
+
+
+def test_degenerate_and_zero_mass_errors(pkg):
+    factors = [np.zeros((4, 2)), np.ones((4, 2)), np.ones((3, 2))]
+    g = pkg.ProcessorGrid((4, 4, 3), (1, 1, 1))
+    blocks = _blocks(pkg, factors, g)
+    grams = [pkg.gram(b) for b in blocks]
+    trees = [pkg.sts_build(b, grid=g) for b in blocks]
+    cp = pkg.pseudo_inverse(pkg.hadamard_gram_chain(grams, skip=2))
+    with pytest.raises(pkg.DegenerateWalkError):
+        pkg.sts_sample(trees, 2, 4, cp, grams, blocks, seed=20, grid=g)
+    zf = [np.zeros((4, 2)) for _ in range(3)]
+    st = [pkg.arls_lev_build(b) for b in _blocks(pkg, zf, pkg.ProcessorGrid((4, 4, 4), (1, 1, 1)))]
+    with pytest.raises(ValueError):
+        pkg.arls_lev_sample(st, 2, 8, zf, seed=0)
+    # zero samples
+    assert pkg.arls_lev_sample(st, 1, 0, zf, seed=0).J == 0
+
+
+def test_local_leaf_search_segments(pkg):
+    gen = np.random.default_rng(21)
+    W = gen.standard_normal((8, 3))
+    offs = np.array([0, 4, 8])
+    B = gen.standard_normal((3, 3))
+    cond = B @ B.T
+    h = gen.standard_normal(3)
+    m = np.array([(W[q] * h) @ cond @ (W[q] * h) for q in range(8)])
+    edges = np.cumsum(m) / m.sum()
+    for r in (np.arange(400) + 0.5) / 400:
+        got = pkg.local_sts_leaf_search(h, W, None, offs, cond, r)
+        assert got == min(int(np.searchsorted(edges, r, side="right")), 7)
+
+
+# --------------------------------------------------------------------- mttkrp
+def test_gather_csr_and_downsampled_match_reference(pkg):
+    g0 = golden("mttkrp.npz")
+    t = pkg.SparseTensorCOO((9, 8, 7), g0["idx"], g0["vals"])
+    for k in range(3):
+        m = pkg.matricize(t, k)
+        csr = pkg.gather_sampled_nonzeros_to_csr(m, g0["X%d" % k], k)
+        assert np.array_equal(csr.row_ptr, g0["rp%d" % k])
+        assert np.array_equal(csr.col_idx, g0["ci%d" % k])
+        assert np.array_equal(csr.vals, g0["cv%d" % k])
+        out = pkg.downsampled_mttkrp(csr, g0["H%d" % k], g0["w%d" % k])
+        assert rel_err(out, g0["out%d" % k]) < 1e-13
+
+
+def test_fused_sampled_mttkrp_matches_oracle(pkg):
+    import torch
+    from paper_2210_05105_b200.ops import ops_for
+    from paper_2210_05105_b200.store import build_store
+    dims = (40, 35, 30)
+    idx, vals = synth.small_random(dims, 6000, seed=2)
+    gen = np.random.default_rng(4)
+    R = 37
+    factors = [gen.standard_normal((d, R)) for d in dims]
+    dev = torch.device("cuda")
+    ops = ops_for(dev)
+    for k in range(3):
+        st = build_store(dims, torch.as_tensor(idx, device=dev), torch.as_tensor(vals, device=dev), k)
+        J = 3000
+        X = np.stack([gen.integers(0, d, J) for d in dims], 1).astype(np.int64)
+        X[:, k] = -1
+        X[100:400] = X[0]                      # heavy duplication
+        H = np.ones((J, R))
+        for i in range(3):
+            if i != k:
+                H *= factors[i][X[:, i]]
+        w = gen.random(J) + 0.5
+        w[100:400] = w[0]
+        ref = O.sketched_mttkrp(O.sampled_csr(O.Store(dims, idx, vals, k), X, k), H, w)
+        out = torch.empty((dims[k], R), dtype=torch.float64, device=dev)
+        stats = torch.zeros(8, dtype=torch.int64, device=dev)
+        ops.sampled_mttkrp(st, torch.as_tensor(np.ascontiguousarray(X.T), device=dev), k,
+                           torch.as_tensor(H, device=dev), torch.as_tensor(w, device=dev), out,
+                           stats, cap=st.capacity(J))
+        ops.status.check()
+        got = out.cpu().numpy()
+        assert rel_err(got, ref) < 1e-12, k
+        csr = O.sampled_csr(O.Store(dims, idx, vals, k), X, k)
+        s = stats.cpu().numpy()
+        assert s[3] == csr.nnz                       # gathered nnz with multiplicity
+        assert np.array_equal(got == 0, ref == 0)    # untouched rows exactly zero
+
+
+# ------------------------------------------------------------------- full ALS
+@pytest.fixture(scope="module")
+def c1():
+    return synth.planted_c1(seed=0)
+
+
+@pytest.mark.parametrize("sampler,P", [("sts", 1), ("sts", 4), ("arls-lev", 1),
+                                       ("arls-lev", 2), ("arls-lev", 4)])
+def test_c1_als_matches_reference(pkg, c1, sampler, P):
+    g0 = golden("als_c1.npz")
+    idx, vals = c1
+    t = pkg.SparseTensorCOO((2000, 1500, 1000), idx, vals)
+    cfg = pkg.AlsConfig(rank=8, rounds=10, sampler=sampler, samples=4096,
+                        schedule="accumulator-stationary", procs=P, seed=3, fit_every=1,
+                        record_samples=True, permute=False)
+    res = pkg.run_als(cfg, tensor=t)
+    tag = "%s_p%d" % (sampler.replace("-", ""), P)
+    hashes = [sha(X) for X in res.sample_log]
+    ref_hashes = [str(h) for h in g0[tag + "_hash"]]
+    mism = [i for i, (a, b) in enumerate(zip(hashes, ref_hashes)) if a != b]
+    assert not mism, "sample batches differ at solves %s" % mism
+    for j in range(3):
+        assert rel_err(res.factors[j], g0[tag + "_U%d" % j]) < REL, j
+    assert rel_err(res.sigma, g0[tag + "_sigma"]) < REL
+    fits = np.array([f for _, f in res.fit_history])
+    assert np.abs(fits - g0[tag + "_fits"]).max() < 1e-6
+
+
+def test_drop_in_solve_matches_oracle(pkg):
+    """solve_mode_accumulator_stationary through the drop-in API (host buffers)."""
+    dims = (30, 25, 20)
+    idx, vals = synth.small_random(dims, 2500, seed=8)
+    t = pkg.SparseTensorCOO(dims, idx, vals)
+    for sampler, P in (("sts", 1), ("arls-lev", 2)):
+        g = pkg.optimal_grid(dims, P)
+        part = pkg.partition_to_grid(t, g, "accumulator-stationary")
+        full, _ = pkg.init_factors(dims, 5, 4)
+        fbs = [pkg.FactorBlocks.from_global(U, g, j) for j, U in enumerate(full)]
+        grams = [pkg.gram(b) for b in fbs]
+        ctx = pkg.SolveContext(g, "accumulator-stationary", sampler, 400, fbs, grams, part, None, 4)
+        ctx.round_id = 1
+        if sampler == "sts":
+            ctx.trees = [pkg.sts_build(b, grid=g) for b in fbs]
+        else:
+            ctx.arls_states = [pkg.arls_lev_build(b) for b in fbs]
+        st = O.AsState(dims, idx, vals, 5, sampler, 400, seed=4, P=P)
+        st.rnd = 1
+        bo = st.solve(0)
+        b = pkg.solve_mode_accumulator_stationary(ctx, 0)
+        assert np.array_equal(b.X, bo.X)
+        for p in range(g.P):
+            assert rel_err(ctx.factors[0].blocks[p], st.blocks[0][p]) < REL
