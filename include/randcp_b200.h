@@ -189,6 +189,10 @@ int rcp_weights(const double *d_pmp, int N, int64_t J, double *d_prob, double *d
  * local nonzero, [2] gathered nonzeros (distinct fibers), [3] gathered nonzeros with
  * multiplicity (the reference's csr.nnz), [4] output rows hit; [5..7] reserved. */
 size_t rcp_mttkrp_ws_bytes(int64_t J, int64_t store_nnz, int64_t n_rows, int R);
+/* Byte offsets of the internal arrays inside a workspace of ws_bytes (introspection for
+ * tests): dkey, dcnt, drep, dlo, dlen, doff, Hs, rcnt, rptr, ed, ev, S, nnz, then the
+ * entry capacity; 14 int64 written to h_out. */
+int rcp_mttkrp_layout(int64_t J, int64_t n_rows, int R, size_t ws_bytes, int64_t *h_out);
 int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n_cols,
                        const int32_t *d_rows, const double *d_vals, int64_t n_rows,
                        const int64_t *d_X, int N, int64_t J, int k, const int64_t *h_strides,

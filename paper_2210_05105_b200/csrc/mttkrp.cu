@@ -78,18 +78,29 @@ __device__ __forceinline__ int64_t floor_index(const int64_t *__restrict__ a, in
 }
 
 // ------------------------------------------------------------------------- dedup
+// Samples with equal column keys are merged.  Their KRP rows are equal (H is a function
+// of the index tuple); their weights are equal for sampler output (w depends on the
+// tuple's probability only), in which case the merged weight is count * w^2 exactly.
+// Unequal weights (e.g. an injected batch) fall back to the sum of w^2.
 __global__ void hash_insert_kernel(const int64_t *__restrict__ X, int N, int64_t J, int k,
-                                   Strides st, int64_t tmask, unsigned long long *tkey,
-                                   int32_t *tcnt, int32_t *trep) {
+                                   Strides st, int64_t tmask, const double *__restrict__ w,
+                                   unsigned long long *tkey, int32_t *tcnt, int32_t *trep,
+                                   unsigned long long *twmin, unsigned long long *twmax,
+                                   double *twsum) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= J) return;
   const int64_t key = sample_key(X, N, J, k, st, s);
+  const double w2 = w[s] * w[s];
+  const unsigned long long wb = (unsigned long long)__double_as_longlong(w2);  // w2 >= 0
   uint64_t h = mix64((uint64_t)key) & (uint64_t)tmask;
   while (true) {
     unsigned long long prev = atomicCAS(&tkey[h], ~0ull, (unsigned long long)key);
     if (prev == ~0ull || prev == (unsigned long long)key) {
       atomicAdd(&tcnt[h], 1);
       atomicMin(&trep[h], (int32_t)s);
+      atomicMin(&twmin[h], wb);
+      atomicMax(&twmax[h], wb);
+      atomicAdd(&twsum[h], w2);
       return;
     }
     h = (h + 1) & (uint64_t)tmask;
@@ -106,10 +117,14 @@ __global__ void compact_count_kernel(const int32_t *__restrict__ tcnt, int64_t T
 
 __global__ void compact_write_kernel(const unsigned long long *__restrict__ tkey,
                                      const int32_t *__restrict__ tcnt,
-                                     const int32_t *__restrict__ trep, int64_t T,
+                                     const int32_t *__restrict__ trep,
+                                     const unsigned long long *__restrict__ twmin,
+                                     const unsigned long long *__restrict__ twmax,
+                                     const double *__restrict__ twsum, int64_t T,
                                      const int64_t *__restrict__ bcnt, int nb,
                                      int64_t *__restrict__ dkey, int32_t *__restrict__ dcnt,
-                                     int32_t *__restrict__ drep, int64_t *__restrict__ S) {
+                                     int32_t *__restrict__ drep, double *__restrict__ dsc,
+                                     int64_t *__restrict__ S) {
   __shared__ int64_t base;
   __shared__ int wsum[32];
   if (threadIdx.x == 0) {
@@ -135,6 +150,8 @@ __global__ void compact_write_kernel(const unsigned long long *__restrict__ tkey
     dkey[o] = (int64_t)tkey[i];
     dcnt[o] = tcnt[i];
     drep[o] = trep[i];
+    dsc[o] = twmin[i] == twmax[i] ? (double)tcnt[i] * __longlong_as_double((long long)twmin[i])
+                                  : twsum[i];
   }
 }
 
@@ -143,7 +160,7 @@ __global__ void lookup_kernel(const int64_t *__restrict__ keys, int64_t n_cols,
                               const int64_t *__restrict__ colptr, const int64_t *__restrict__ dkey,
                               const int32_t *__restrict__ dcnt, const int32_t *__restrict__ drep,
                               const int64_t *__restrict__ S, const double *__restrict__ H,
-                              const double *__restrict__ w, int R, int64_t *__restrict__ dlo,
+                              const double *__restrict__ dsc, int R, int64_t *__restrict__ dlo,
                               int64_t *__restrict__ dlen, double *__restrict__ Hs,
                               int64_t *__restrict__ stats) {
   const int lane = threadIdx.x & 31;
@@ -166,8 +183,7 @@ __global__ void lookup_kernel(const int64_t *__restrict__ keys, int64_t n_cols,
     }
   }
   const int32_t rep = drep[d];
-  const double ws = w[rep];
-  const double sc = (double)dcnt[d] * (ws * ws);
+  const double sc = dsc[d];
   for (int c = lane; c < R; c += 32) Hs[d * R + c] = sc * H[(int64_t)rep * R + c];
 }
 
@@ -197,10 +213,14 @@ __global__ void rows_hit_kernel(const int64_t *__restrict__ rcnt, int64_t n_rows
 // ------------------------------------------------------------ entry traversal
 // The gathered entries e in [0, nnz) are the concatenation of the distinct fibers; entry e
 // of fiber d sits at store position lo_d + (e - off_d).  A tile of kTileE consecutive
-// entries stages the needed slice of the fiber offsets in shared memory.
+// entries stages the needed slice of the fiber offsets in shared memory (or, when empty
+// fibers make the slice longer than the window, searches it in global memory).
+constexpr int kWinCap = 4096;
+
 struct TileFibers {
-  int64_t d0;   // first fiber of the tile
-  int nwin;     // window length (offsets d0 .. d0+nwin-1 staged)
+  int64_t d0;            // first fiber of the tile
+  int64_t nwin;          // offsets d0 .. d0+nwin-1 cover the tile
+  const int64_t *off;    // -> those offsets (shared window or global)
 };
 
 __device__ TileFibers stage_tile(const int64_t *__restrict__ doff, int64_t S, int64_t t0,
@@ -212,20 +232,24 @@ __device__ TileFibers stage_tile(const int64_t *__restrict__ doff, int64_t S, in
   }
   __syncthreads();
   const int64_t d0 = sd0, d1 = sd1;
-  const int nwin = (int)(d1 - d0 + 2);
-  for (int i = threadIdx.x; i < nwin; i += blockDim.x) win[i] = doff[d0 + i];
-  __syncthreads();
   TileFibers tf;
   tf.d0 = d0;
-  tf.nwin = nwin;
+  tf.nwin = d1 - d0 + 2;
+  if (tf.nwin <= kWinCap) {
+    for (int64_t i = threadIdx.x; i < tf.nwin; i += blockDim.x) win[i] = doff[d0 + i];
+    tf.off = win;
+  } else {
+    tf.off = doff + d0;
+  }
+  __syncthreads();
   return tf;
 }
 
-__device__ __forceinline__ int64_t fiber_of(const int64_t *win, int nwin, int64_t e) {
-  int lo = 0, hi = nwin - 1;  // win[lo] <= e < win[hi]
+__device__ __forceinline__ int64_t fiber_of(const int64_t *off, int64_t nwin, int64_t e) {
+  int64_t lo = 0, hi = nwin - 1;  // off[lo] <= e < off[hi]
   while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (win[mid] <= e) lo = mid; else hi = mid;
+    int64_t mid = (lo + hi) >> 1;
+    if (off[mid] <= e) lo = mid; else hi = mid;
   }
   return lo;
 }
@@ -245,8 +269,8 @@ row_count_kernel(const int64_t *__restrict__ doff, const int64_t *__restrict__ S
                  const int32_t *__restrict__ rows, int64_t n_rows, int priv,
                  int64_t *__restrict__ rcnt) {
   extern __shared__ int64_t sm[];
-  int64_t *win = sm;                                      // kTileE + 2
-  int32_t *hist = reinterpret_cast<int32_t *>(sm + kTileE + 2);
+  int64_t *win = sm;                                      // kWinCap + 2
+  int32_t *hist = reinterpret_cast<int32_t *>(sm + kWinCap + 2);
   const int64_t nnz = nnzp[0], S = Sp[0];
   int64_t r0, r1;
   cta_range(nnz, r0, r1);
@@ -259,8 +283,8 @@ row_count_kernel(const int64_t *__restrict__ doff, const int64_t *__restrict__ S
     __syncthreads();
     TileFibers tf = stage_tile(doff, S, t0, t1, win);
     for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
-      const int64_t j = fiber_of(win, tf.nwin, e);
-      const int32_t row = rows[dlo[tf.d0 + j] + (e - win[j])];
+      const int64_t j = fiber_of(tf.off, tf.nwin, e);
+      const int32_t row = rows[dlo[tf.d0 + j] + (e - tf.off[j])];
       if (priv) atomicAdd(&hist[row], 1);
       else atomicAdd((unsigned long long *)&rcnt[row], 1ull);
     }
@@ -280,7 +304,7 @@ scatter_kernel(const int64_t *__restrict__ doff, const int64_t *__restrict__ Sp,
                int32_t *__restrict__ ed, double *__restrict__ ev, int64_t cap, int *status) {
   extern __shared__ int64_t sm[];
   int64_t *win = sm;
-  int32_t *hist = reinterpret_cast<int32_t *>(sm + kTileE + 2);
+  int32_t *hist = reinterpret_cast<int32_t *>(sm + kWinCap + 2);
   const int64_t nnz = nnzp[0], S = Sp[0];
   int64_t r0, r1;
   cta_range(nnz, r0, r1);
@@ -293,8 +317,8 @@ scatter_kernel(const int64_t *__restrict__ doff, const int64_t *__restrict__ Sp,
       __syncthreads();
       TileFibers tf = stage_tile(doff, S, t0, t1, win);
       for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
-        const int64_t j = fiber_of(win, tf.nwin, e);
-        atomicAdd(&hist[rows[dlo[tf.d0 + j] + (e - win[j])]], 1);
+        const int64_t j = fiber_of(tf.off, tf.nwin, e);
+        atomicAdd(&hist[rows[dlo[tf.d0 + j] + (e - tf.off[j])]], 1);
       }
     }
     __syncthreads();
@@ -308,8 +332,8 @@ scatter_kernel(const int64_t *__restrict__ doff, const int64_t *__restrict__ Sp,
     __syncthreads();
     TileFibers tf = stage_tile(doff, S, t0, t1, win);
     for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
-      const int64_t j = fiber_of(win, tf.nwin, e);
-      const int64_t pos = dlo[tf.d0 + j] + (e - win[j]);
+      const int64_t j = fiber_of(tf.off, tf.nwin, e);
+      const int64_t pos = dlo[tf.d0 + j] + (e - tf.off[j]);
       const int32_t row = rows[pos];
       int64_t slot;
       if (priv) slot = atomicAdd(&hist[row], 1);
@@ -463,8 +487,8 @@ struct Ws {
 
 struct MttkrpLayout {
   int64_t T;
-  size_t o_tkey, o_tcnt, o_trep, o_bcnt, o_dkey, o_dcnt, o_drep, o_dlo, o_dlen, o_doff, o_Hs,
-      o_scan, o_rcnt, o_rptr, o_ed, o_ev, o_S, o_nnz;
+  size_t o_tkey, o_tcnt, o_trep, o_twmin, o_twmax, o_twsum, o_dsc, o_bcnt, o_dkey, o_dcnt,
+      o_drep, o_dlo, o_dlen, o_doff, o_Hs, o_scan, o_rcnt, o_rptr, o_ed, o_ev, o_S, o_nnz;
   size_t total;
   MttkrpLayout(int64_t J, int64_t cap, int64_t n_rows, int R) {
     T = 1024;
@@ -473,6 +497,10 @@ struct MttkrpLayout {
     o_tkey = w.add(sizeof(int64_t) * T);
     o_tcnt = w.add(sizeof(int32_t) * T);
     o_trep = w.add(sizeof(int32_t) * T);
+    o_twmin = w.add(sizeof(int64_t) * T);
+    o_twmax = w.add(sizeof(int64_t) * T);
+    o_twsum = w.add(sizeof(double) * T);
+    o_dsc = w.add(sizeof(double) * (J + 1));
     o_bcnt = w.add(sizeof(int64_t) * (T / 1024));
     o_dkey = w.add(sizeof(int64_t) * (J + 1));
     o_dcnt = w.add(sizeof(int32_t) * (J + 1));
@@ -502,6 +530,31 @@ size_t rcp_mttkrp_ws_bytes(int64_t J, int64_t store_nnz, int64_t n_rows, int R) 
   return L.total;
 }
 
+// Entry capacity implied by a workspace size (the layout is monotone in it).
+static int64_t mttkrp_cap(int64_t J, int64_t n_rows, int R, size_t ws_bytes) {
+  MttkrpLayout base(J, 0, n_rows, R);
+  if (ws_bytes < base.total) return -1;
+  int64_t cap = (int64_t)((ws_bytes - base.total) / (sizeof(int32_t) + sizeof(double)));
+  MttkrpLayout L(J, cap, n_rows, R);
+  while (L.total > ws_bytes && cap > 0) {
+    cap -= 64;
+    L = MttkrpLayout(J, cap, n_rows, R);
+  }
+  return cap;
+}
+
+int rcp_mttkrp_layout(int64_t J, int64_t n_rows, int R, size_t ws_bytes, int64_t *h_out) {
+  if (!h_out) return RCP_ERR_ARG;
+  int64_t cap = mttkrp_cap(J, n_rows, R, ws_bytes);
+  if (cap < 0) return RCP_ERR_ARG;
+  MttkrpLayout L(J, cap, n_rows, R);
+  const size_t o[] = {L.o_dkey, L.o_dcnt, L.o_drep, L.o_dlo, L.o_dlen, L.o_doff, L.o_Hs,
+                      L.o_rcnt, L.o_rptr, L.o_ed, L.o_ev, L.o_S, L.o_nnz};
+  for (int i = 0; i < 13; ++i) h_out[i] = (int64_t)o[i];
+  h_out[13] = cap;
+  return RCP_OK;
+}
+
 int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n_cols,
                        const int32_t *d_rows, const double *d_vals, int64_t n_rows,
                        const int64_t *d_X, int N, int64_t J, int k, const int64_t *h_strides,
@@ -516,19 +569,10 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   if (J == 0 || n_rows == 0 || n_cols == 0) return RCP_OK;
   if (!d_keys || !d_colptr || !d_rows || !d_vals || !d_X || !d_H || !d_w || !d_out || !d_ws)
     return RCP_ERR_ARG;
-  // store_nnz (capacity of the entry arrays) is implied by ws_bytes
-  int64_t cap = 0;
-  {
-    // find the largest capacity that fits ws_bytes (layout is monotone in cap)
-    MttkrpLayout base(J, 0, n_rows, R);
-    if (ws_bytes < base.total) return RCP_ERR_ARG;
-    cap = (int64_t)((ws_bytes - base.total) / (sizeof(int32_t) + sizeof(double)));
-  }
+  // the capacity of the entry arrays is implied by ws_bytes
+  const int64_t cap = mttkrp_cap(J, n_rows, R, ws_bytes);
+  if (cap < 0) return RCP_ERR_ARG;
   MttkrpLayout L(J, cap, n_rows, R);
-  while (L.total > ws_bytes && cap > 0) {
-    cap -= 64;
-    L = MttkrpLayout(J, cap, n_rows, R);
-  }
   char *w = (char *)d_ws;
   auto P = [&](size_t o) { return (void *)(w + o); };
   unsigned long long *tkey = (unsigned long long *)P(L.o_tkey);
@@ -551,17 +595,24 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   RCP_CUDA_TRY(cudaMemsetAsync(tkey, 0xff, sizeof(int64_t) * L.T, st));
   RCP_CUDA_TRY(cudaMemsetAsync(tcnt, 0, sizeof(int32_t) * L.T, st));
   RCP_CUDA_TRY(cudaMemsetAsync(trep, 0x7f, sizeof(int32_t) * L.T, st));
-  hash_insert_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(d_X, N, J, k, sd, L.T - 1, tkey,
-                                                                 tcnt, trep);
+  unsigned long long *twmin = (unsigned long long *)P(L.o_twmin);
+  unsigned long long *twmax = (unsigned long long *)P(L.o_twmax);
+  double *twsum = (double *)P(L.o_twsum), *dsc = (double *)P(L.o_dsc);
+  RCP_CUDA_TRY(cudaMemsetAsync(twmin, 0xff, sizeof(int64_t) * L.T, st));
+  RCP_CUDA_TRY(cudaMemsetAsync(twmax, 0, sizeof(int64_t) * L.T, st));
+  RCP_CUDA_TRY(cudaMemsetAsync(twsum, 0, sizeof(double) * L.T, st));
+  hash_insert_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(
+      d_X, N, J, k, sd, L.T - 1, d_w, tkey, tcnt, trep, twmin, twmax, twsum);
   RCP_LAUNCH_CHECK("hash_insert");
   const int nb = (int)(L.T / 1024);
   compact_count_kernel<<<nb, 1024, 0, st>>>(tcnt, L.T, bcnt);
   RCP_LAUNCH_CHECK("compact_count");
-  compact_write_kernel<<<nb, 1024, 0, st>>>(tkey, tcnt, trep, L.T, bcnt, nb, dkey, dcnt, drep, S);
+  compact_write_kernel<<<nb, 1024, 0, st>>>(tkey, tcnt, trep, twmin, twmax, twsum, L.T, bcnt, nb,
+                                            dkey, dcnt, drep, dsc, S);
   RCP_LAUNCH_CHECK("compact_write");
   // 2. lookup + scaled KRP rows
   lookup_kernel<<<(unsigned)ceil_div(J * 32, 256), 256, 0, st>>>(
-      d_keys, n_cols, d_colptr, dkey, dcnt, drep, S, d_H, d_w, R, dlo, dlen, Hs, d_stats);
+      d_keys, n_cols, d_colptr, dkey, dcnt, drep, S, d_H, dsc, R, dlo, dlen, Hs, d_stats);
   RCP_LAUNCH_CHECK("lookup");
   // 3. fiber offsets
   int rc = scan_i64_exclusive(dlen, doff, J, S, scan_ws, st);
@@ -570,7 +621,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   RCP_LAUNCH_CHECK("finalize_counts");
   // 4. row histogram -> row pointers
   const int priv = n_rows <= kPrivRows ? 1 : 0;
-  size_t smem = sizeof(int64_t) * (kTileE + 2) + (priv ? sizeof(int32_t) * n_rows : 0);
+  size_t smem = sizeof(int64_t) * (kWinCap + 2) + (priv ? sizeof(int32_t) * n_rows : 0);
   static bool attr = false;
   if (!attr) {
     RCP_CUDA_TRY(cudaFuncSetAttribute(row_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
