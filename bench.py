@@ -175,6 +175,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks = Clocks(local_rank)
     clocks.start()
+    lib = _lib.lib()
+    launches0 = lib.rcp_launch_count()
     step_ms = []
     for _ in range(args.steps):
         flush_l2(flush)
@@ -188,7 +190,17 @@ def run_ours(args):
         step_ms.append(s.elapsed_time(e))
     torch.cuda.synchronize()
     clk = clocks.stop()
+    launches = lib.rcp_launch_count() - launches0
     cl.check("in timed rounds")
+    # one extra (untimed) round with device phase markers for the breakdown
+    cl.phase_events = []
+    me.mttkrp = orig
+    rnd += 1
+    cl.round(rnd, check=False)
+    torch.cuda.synchronize()
+    phases = {k: round(v, 4) for k, v in cl.phase_breakdown().items()}
+    cl.phase_events = None
+    me.mttkrp = timed_mttkrp
     st = (me.stats - stats0).cpu().numpy().astype(np.int64)
     mt_ms = sum(a.elapsed_time(b) for a, b in mt_events)
     t_total = sum(step_ms) / 1e3
@@ -233,7 +245,8 @@ def run_ours(args):
                      "avg_launch_ms": mt_ms / max(n_launch, 1), "launches": n_launch,
                      "share_of_step": mt_ms / max(sum(step_ms), 1e-9)},
         "clocks": clk,
-        "gpu_launches": None,
+        "gpu_launches": int(launches),
+        "phases_ms_per_round": phases,
     }
     if e2e is not None:
         out["e2e"] = e2e

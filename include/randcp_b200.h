@@ -54,6 +54,8 @@ const char *rcp_version(void);
 const char *rcp_last_error(void);
 /* Number of SMs of the current device (0 without a device). */
 int rcp_device_sms(void);
+/* Number of kernels this library has launched in the process (all entry points). */
+int64_t rcp_launch_count(void);
 
 /* ------------------------------------------------------------------- random streams
  * Reference: rng.stream(seed, purpose, *context) builds

@@ -32,6 +32,7 @@ _SIGS = {
     "rcp_version": (C.c_char_p, []),
     "rcp_last_error": (C.c_char_p, []),
     "rcp_device_sms": (_i32, []),
+    "rcp_launch_count": (_i64, []),
     "rcp_stream_key": (_i32, [_u64, _u64, _vp, _i32, _vp]),
     "rcp_uniform_host": (_i32, [_vp, _i64, _i64, _vp]),
     "rcp_permutation_host": (_i32, [_vp, _i64, _vp]),

@@ -13,7 +13,10 @@ static thread_local std::string g_err;
 
 void set_error(const char *msg) { g_err = msg ? msg : ""; }
 
+static unsigned long long g_launches = 0;
+
 int check_launch(const char *what) {
+  ++g_launches;  // every kernel launch site calls this once
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -62,6 +65,7 @@ extern "C" {
 
 const char *rcp_version(void) { return "randcp_b200 0.1.0 (sm_100a)"; }
 const char *rcp_last_error(void) { return rcp::g_err.c_str(); }
+int64_t rcp_launch_count(void) { return (int64_t)rcp::g_launches; }
 
 int rcp_device_sms(void) {
   int dev = 0, n = 0;

@@ -308,6 +308,7 @@ class Cluster:
         self.P = ranks[0].P
         self.timings = {p: 0.0 for p in PHASES}
         self.timed = False
+        self.phase_events = None
 
     def _tick(self, phase, t0):
         if not self.timed:
@@ -423,18 +424,31 @@ class Cluster:
                 r.urow[sel] = blk[:, 3:]
 
     # -------------------------------------------------------------- solve
+    def _ev(self, phase):
+        """Device-side phase marker (CUDA event on the current stream) when profiling."""
+        if self.phase_events is None:
+            return
+        e = torch().cuda.Event(enable_timing=True)
+        e.record()
+        self.phase_events.append((phase, e))
+
     def solve(self, k, rnd, override=None, injected=None):
         t0 = time.perf_counter()
+        self._ev("sampling")
         if injected is None:
             self.sample(k, rnd, override=override)
         else:
             for r in self.ranks:
                 injected(r)
         t0 = self._tick("sampling", t0)
+        self._ev("gram+pinv")
         for r in self.ranks:
             r.sketched_system()
+        self._ev("mttkrp")
+        for r in self.ranks:
             r.mttkrp(k)
         t0 = self._tick("mttkrp", t0)
+        self._ev("update")
         parts = self.comm.all_gather([r.update(k) for r in self.ranks])
         tot = parts[0].clone()
         for p in parts[1:]:
@@ -442,8 +456,20 @@ class Cluster:
         for r in self.ranks:
             r.renormalize(k, tot.to(r.dev))
         t0 = self._tick("postprocess", t0)
+        self._ev("rebuild")
         self.rebuild(k)
         self._tick("rebuild", t0)
+        self._ev("end")
+
+    def phase_breakdown(self):
+        """ms per phase from the recorded events (after synchronisation)."""
+        out = {}
+        ev = self.phase_events or []
+        for (name, a), (_, b) in zip(ev, ev[1:]):
+            if name == "end":
+                continue
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return out
 
     def check(self, where=""):
         for r in self.ranks:
