@@ -46,6 +46,7 @@ extern "C" {
 #define RCP_ST_ZERO_MASS 8
 #define RCP_ST_NONFINITE 16
 #define RCP_ST_CAPACITY 32
+#define RCP_ST_TIMEOUT 64
 
 #define RCP_MAX_RANK 128
 
@@ -158,16 +159,28 @@ int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
                   void *stream);
 /* Walk J samples down the tree of one factor block (rows global [row_lo, row_lo+n)).
  * M = conditioning matrix (R x R, full) for this mode (ref samplers.py:412-415).
- * Uniforms: d_override (J doubles, nullable) else WALK_UNIFORM draws of key (key0,key1).
- * d_sel (nullable): only samples s with d_sel[s] == sel_value walk (multi-rank owner).
- * Outputs: d_Xi[s] (global row), d_pmp_i[s] *= step probabilities (caller initialises to
- * the probability so far, 1 for single-rank), d_resid[s]; H[s,:] *= U[row].
- * d_rin (nullable) supplies starting residuals instead of fresh uniforms. */
+ * d_H_in: running Hadamard rows (J x R), NULL = all ones (first constant mode).
+ * d_hkey (nullable): per-sample key of the indices already sampled in earlier modes;
+ * samples with equal keys must have equal H rows.  Samples are grouped by (key, r) and
+ * each group descends as runs, so node masses are evaluated once per distinct
+ * (H row, node).  Uniforms: d_override (J doubles) or d_rin (residuals after the
+ * rank-level levels) else WALK_UNIFORM draws of key (key0,key1).
+ * d_sel (nullable): only samples s with d_sel[s] == sel_value walk (multi-rank owner);
+ * their d_pmp_i[s] holds the probability so far and is multiplied, otherwise it is set.
+ * Outputs per walked sample: d_Xi[s] (global row), d_pmp_i[s], d_resid[s] (nullable),
+ * d_urow_out[s,:] = the chosen factor row.  d_ws: rcp_sts_walk_ws_bytes(J, n, leaf). */
+size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf);
 int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
-                 int64_t row_lo, const double *d_M, const double *d_H_in, int64_t J,
-                 uint64_t key0, uint64_t key1, const double *d_override, const double *d_rin,
-                 const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi, double *d_pmp_i,
-                 double *d_resid, double *d_urow_out, int *d_status, void *stream);
+                 int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
+                 int64_t J, uint64_t key0, uint64_t key1, const double *d_override,
+                 const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
+                 double *d_pmp_i, double *d_resid, double *d_urow_out, void *d_ws,
+                 size_t ws_bytes, int *d_status, void *stream);
+/* d_out[s] = sum_m X[m*J + s] * strides[m] over modes with nonzero stride (mixed-radix
+ * key of a subset of a sample's indices; ref matricization.py:41-54 for the MTTKRP
+ * column key, and the STS walk's grouping key). */
+int rcp_row_keys(const int64_t *d_X, int N, int64_t J, const int64_t *h_strides,
+                 int64_t *d_out, void *stream);
 /* H[s,:] *= d_urow[s,:] for all s (fold walked rows into the running Hadamard rows). */
 int rcp_hadamard_rows(double *d_H, const double *d_urow, int64_t J, int R, int init_ones,
                       void *stream);

@@ -19,6 +19,7 @@ ST_ASYMMETRIC = 4
 ST_ZERO_MASS = 8
 ST_NONFINITE = 16
 ST_CAPACITY = 32
+ST_TIMEOUT = 64
 
 _vp = C.c_void_p
 _i64 = C.c_int64
@@ -55,8 +56,10 @@ _SIGS = {
     "rcp_sts_rank_walk": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _i64, _i32, _u64, _u64, _vp,
                                  _vp, _vp, _vp, _vp, _vp]),
     "rcp_sts_build": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp]),
-    "rcp_sts_walk": (_i32, [_vp, _vp, _i64, _i32, _i32, _i64, _vp, _vp, _i64, _u64, _u64, _vp,
-                            _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "rcp_sts_walk_ws_bytes": (_sz, [_i64, _i64, _i32]),
+    "rcp_sts_walk": (_i32, [_vp, _vp, _i64, _i32, _i32, _i64, _vp, _vp, _vp, _i64, _u64, _u64,
+                            _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
+    "rcp_row_keys": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp]),
     "rcp_hadamard_rows": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp]),
     "rcp_weights": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp, _vp]),
     "rcp_mttkrp_ws_bytes": (_sz, [_i64, _i64, _i64, _i32]),

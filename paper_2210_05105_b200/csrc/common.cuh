@@ -81,6 +81,11 @@ __host__ __device__ __forceinline__ double u64_to_unit(uint64_t x) {
 // Largest double below 1 (ref samplers.py:31 _ONE_BELOW).
 __host__ __device__ __forceinline__ double one_below() { return 0x1.fffffffffffffp-1; }
 
+// Per-mode strides passed by value to kernels (N <= 8 modes).
+struct Strides8 {
+  int64_t s[8];
+};
+
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) {
   return (a + b - 1) / b;
 }

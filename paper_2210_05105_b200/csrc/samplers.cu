@@ -190,169 +190,6 @@ __global__ void sts_level_kernel(const double *__restrict__ child, double *__res
   }
 }
 
-// ---------------------------------------------------------------------- STS walk
-constexpr int kMaxLeaf = 64;
-
-struct WalkSmem {
-  static size_t bytes(int R, int warps, int leaf) {
-    const int Rt = R * (R + 1) / 2;
-    return sizeof(double) * ((size_t)Rt + (size_t)warps * (Rt + 2 * R + leaf + 2)) +
-           sizeof(uint16_t) * (size_t)Rt + 64;
-  }
-};
-
-__global__ void sts_walk_kernel(const double *__restrict__ tree, const double *__restrict__ U,
-                                int64_t n, int R, int leaf, int depth, int64_t row_lo,
-                                const double *__restrict__ Mfull, const double *__restrict__ Hin,
-                                int64_t J, uint64_t k0, uint64_t k1,
-                                const double *__restrict__ override_u,
-                                const double *__restrict__ rin, const int32_t *__restrict__ sel,
-                                int32_t selv, int64_t *__restrict__ Xi, double *__restrict__ pmp,
-                                double *__restrict__ resid, double *__restrict__ urow,
-                                int *status) {
-  extern __shared__ double sh[];
-  const int Rt = R * (R + 1) / 2;
-  const int warps = blockDim.x >> 5;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double *Mp = sh;                                       // Rt: packed M, off-diagonals x2
-  double *wbase = Mp + Rt;
-  double *P = wbase + (size_t)wid * (Rt + 2 * R + leaf + 2);  // per-warp packed P
-  double *hv = P + Rt;                                   // R
-  double *uv = hv + R;                                   // R
-  double *mass = uv + R;                                 // leaf (+2)
-  uint16_t *pairs = reinterpret_cast<uint16_t *>(wbase + (size_t)warps * (Rt + 2 * R + leaf + 2));
-
-  for (int e = threadIdx.x; e < Rt; e += blockDim.x) {
-    int a = 0, rem = e;
-    while (rem >= R - a) {
-      rem -= R - a;
-      ++a;
-    }
-    const int b = a + rem;
-    pairs[e] = (uint16_t)(a | (b << 8));
-    const double m = Mfull[a * R + b];
-    Mp[e] = (a == b) ? m : 2.0 * m;
-  }
-  __syncthreads();
-
-  const double tiny = DBL_MIN;
-  for (int64_t s = (int64_t)blockIdx.x * warps + wid; s < J; s += (int64_t)gridDim.x * warps) {
-    if (sel && sel[s] != selv) continue;
-    double r;
-    if (override_u) r = override_u[s];
-    else if (rin) r = rin[s];
-    else r = u64_to_unit(philox_word(k0, k1, (uint64_t)s));
-    for (int c = lane; c < R; c += 32) hv[c] = Hin ? Hin[s * R + c] : 1.0;
-    __syncwarp();
-    for (int e = lane; e < Rt; e += 32) {
-      const uint16_t ab = pairs[e];
-      P[e] = hv[ab & 0xff] * hv[ab >> 8] * Mp[e];
-    }
-    __syncwarp();
-    double prob = 1.0;
-    int64_t v = 0;
-    bool bad = false;
-    for (int lev = 0; lev < depth; ++lev) {
-      const double *GL = tree + ((1LL << (lev + 1)) - 1 + 2 * v) * (int64_t)Rt;
-      const double *GR = GL + Rt;
-      double qL = 0.0, qR = 0.0;
-      for (int e = lane; e < Rt; e += 32) {
-        const double p = P[e];
-        qL = fma(__ldg(GL + e), p, qL);
-        qR = fma(__ldg(GR + e), p, qR);
-      }
-      qL = warp_sum(qL);
-      qR = warp_sum(qR);
-      qL = qL > 0.0 ? qL : 0.0;
-      qR = qR > 0.0 ? qR : 0.0;
-      const double tot = qL + qR;
-      if (!(tot > 0.0)) {
-        bad = true;
-        break;
-      }
-      double T = qL / tot;
-      T = fmin(fmax(T, 0.0), 1.0);
-      const bool right = r >= T;
-      prob *= right ? (1.0 - T) : T;
-      r = right ? (r - T) / fmax(1.0 - T, tiny) : r / fmax(T, tiny);
-      r = fmin(fmax(r, 0.0), one_below());
-      v = 2 * v + (right ? 1 : 0);
-    }
-    if (bad) {
-      if (lane == 0) {
-        raise_status(status, RCP_ST_DEGENERATE);
-        Xi[s] = -1;
-      }
-      continue;
-    }
-    // leaf block: row masses (u (.) h)^T M (u (.) h) = sum_e u_a u_b P_e
-    const int64_t r0 = v * leaf;
-    const int nr = (int)min((int64_t)leaf, n - r0);
-    if (nr <= 0) {
-      if (lane == 0) {
-        raise_status(status, RCP_ST_DEGENERATE);
-        Xi[s] = -1;
-      }
-      continue;
-    }
-    for (int q = 0; q < nr; ++q) {
-      for (int c = lane; c < R; c += 32) uv[c] = U[(r0 + q) * R + c];
-      __syncwarp();
-      double m = 0.0;
-      for (int e = lane; e < Rt; e += 32) {
-        const uint16_t ab = pairs[e];
-        m = fma(uv[ab & 0xff] * uv[ab >> 8], P[e], m);
-      }
-      m = warp_sum(m);
-      if (lane == 0) mass[q] = m > 0.0 ? m : 0.0;
-      __syncwarp();
-    }
-    // inverse CDF over the leaf rows (ref _inverse_cdf samplers.py:291-310)
-    int choice = 0;
-    double picked = 0.0, total = 0.0, rout = 0.0;
-    if (lane == 0) {
-      for (int q = 0; q < nr; ++q) total += mass[q];
-      if (!(total > 0.0)) {
-        bad = true;
-      } else {
-        const double target = r * total;
-        double cdf = 0.0;
-        int cnt = 0;
-        double cdf_at = 0.0;
-        for (int q = 0; q < nr; ++q) {
-          cdf += mass[q];
-          if (cdf <= target) ++cnt;
-        }
-        choice = cnt < nr - 1 ? cnt : nr - 1;
-        cdf = 0.0;
-        for (int q = 0; q <= choice; ++q) cdf += mass[q];
-        cdf_at = cdf;
-        picked = mass[choice];
-        const double before = cdf_at - picked;
-        rout = picked > 0.0 ? (target - before) / picked : 0.0;
-        rout = fmin(fmax(rout, 0.0), one_below());
-      }
-    }
-    bad = __shfl_sync(0xffffffffu, bad ? 1 : 0, 0) != 0;
-    if (bad) {
-      if (lane == 0) {
-        raise_status(status, RCP_ST_DEGENERATE);
-        Xi[s] = -1;
-      }
-      continue;
-    }
-    choice = __shfl_sync(0xffffffffu, choice, 0);
-    const int64_t row = r0 + choice;
-    if (lane == 0) {
-      Xi[s] = row_lo + row;
-      pmp[s] *= prob * (picked / total);
-      if (resid) resid[s] = rout;
-    }
-    for (int c = lane; c < R; c += 32) urow[s * R + c] = U[row * R + c];
-    __syncwarp();
-  }
-}
-
 __global__ void sts_cond_kernel(const double *__restrict__ cp, const double *__restrict__ grams,
                                 int N, int i, int k, int R, double *__restrict__ M) {
   const int RR = R * R;
@@ -511,7 +348,7 @@ size_t rcp_sts_tree_doubles(int64_t n, int leaf, int R) {
 }
 
 int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree, void *stream) {
-  if (R < 1 || R > RCP_MAX_RANK || leaf < 1 || leaf > kMaxLeaf || n < 0) return RCP_ERR_ARG;
+  if (R < 1 || R > RCP_MAX_RANK || leaf < 1 || leaf > 64 || n < 0) return RCP_ERR_ARG;
   if (n == 0) return RCP_OK;
   if (!d_U || !d_tree) return RCP_ERR_ARG;
   cudaStream_t st = RCP_STREAM(stream);
@@ -549,35 +386,6 @@ int rcp_sts_cond(const double *d_chain_pinv, const double *d_grams, int N, int i
   sts_cond_kernel<<<(unsigned)ceil_div(R * R, 256), 256, 0, RCP_STREAM(stream)>>>(
       d_chain_pinv, d_grams, N, i, k, R, d_M);
   RCP_LAUNCH_CHECK("sts_cond");
-  return RCP_OK;
-}
-
-int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
-                 int64_t row_lo, const double *d_M, const double *d_H_in, int64_t J,
-                 uint64_t key0, uint64_t key1, const double *d_override, const double *d_rin,
-                 const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi, double *d_pmp_i,
-                 double *d_resid, double *d_urow_out, int *d_status, void *stream) {
-  if (R < 1 || R > RCP_MAX_RANK || leaf < 1 || leaf > kMaxLeaf || J < 0 || n < 0) return RCP_ERR_ARG;
-  if (J == 0) return RCP_OK;
-  if (n == 0 || !d_tree || !d_U || !d_M || !d_Xi || !d_pmp_i || !d_urow_out) return RCP_ERR_ARG;
-  const int depth = rcp_sts_depth(n, leaf);
-  int warps = 8;
-  const size_t cap = 200 * 1024;
-  while (warps > 1 && WalkSmem::bytes(R, warps, leaf) > cap) --warps;
-  size_t smem = WalkSmem::bytes(R, warps, leaf);
-  if (smem > 220 * 1024) return RCP_ERR_ARG;
-  static bool attr = false;
-  if (!attr) {
-    RCP_CUDA_TRY(cudaFuncSetAttribute(sts_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      220 * 1024));
-    attr = true;
-  }
-  int64_t want = ceil_div(J, warps);
-  int64_t grid = want < 8LL * sm_count() ? want : 8LL * sm_count();
-  sts_walk_kernel<<<(unsigned)grid, warps * 32, smem, RCP_STREAM(stream)>>>(
-      d_tree, d_U, n, R, leaf, depth, row_lo, d_M, d_H_in, J, key0, key1, d_override, d_rin, d_sel,
-      sel_value, d_Xi, d_pmp_i, d_resid, d_urow_out, d_status);
-  RCP_LAUNCH_CHECK("sts_walk");
   return RCP_OK;
 }
 

@@ -1,0 +1,442 @@
+// STS-CP tree walk, run-grouped (ref sts_sample samplers.py:379-468; _inverse_cdf :291-310).
+//
+// Every sample of constant mode i descends the per-block binary tree of packed node Grams:
+// at a node with children (L, R) it computes the child masses q = h^T (G_child (.) M) h,
+// goes right iff r >= T = qL / (qL + qR), multiplies its probability by T or 1-T and
+// rescales r exactly as the reference does; at a leaf block it inverts the CDF of its
+// rows' masses (u (.) h)^T M (u (.) h).
+//
+// Samples whose running Hadamard rows h are equal (equal indices in the already-sampled
+// modes) see identical node masses.  Sorting the samples by (key of those indices, r)
+// makes each such group contiguous and ordered by r; at every node the left-goers are a
+// prefix of the group.  A group at a node is a *run* [lo, hi) of the sorted array: its
+// masses are computed once, the run splits into a left and a right run, and the walk is a
+// parallel breadth of run splits driven by a device work queue (persistent warps).  The
+// arithmetic per sample is the same as a per-sample walk; the work is proportional to the
+// number of distinct (h, node) pairs instead of samples x levels.
+#include <cub/device/device_radix_sort.cuh>
+#include <float.h>
+
+#include "common.cuh"
+
+using namespace rcp;
+
+namespace {
+
+int sm_count() {
+  static int s = 0;
+  if (!s) {
+    s = rcp_device_sms();
+    if (!s) s = 148;
+  }
+  return s;
+}
+
+constexpr int kMaxLeaf = 64;
+constexpr int kWalkWarps = 8;
+
+struct Run {
+  int32_t lo, hi;    // sorted positions
+  int32_t level;     // tree level of `node`
+  int32_t node;      // node index within its level
+};
+
+struct WalkWs {
+  size_t o_key, o_key2, o_r, o_r2, o_idx, o_idx2, o_prob, o_runs, o_ready, o_ctl, o_cub, total;
+  size_t cub_bytes;
+  WalkWs(int64_t J, int depth) {
+    cub_bytes = 0;
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b1, (const double *)nullptr, (double *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, (int)J);
+    cub::DeviceRadixSort::SortPairs(nullptr, b2, (const int64_t *)nullptr, (int64_t *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, (int)J);
+    cub_bytes = b1 > b2 ? b1 : b2;
+    size_t t = 0;
+    auto add = [&](size_t bytes) {
+      size_t o = (t + 255) & ~(size_t)255;
+      t = o + bytes;
+      return o;
+    };
+    const int64_t nruns = J * (int64_t)(depth + 2) + 16;
+    o_key = add(8 * J);
+    o_key2 = add(8 * J);
+    o_r = add(8 * J);
+    o_r2 = add(8 * J);
+    o_idx = add(4 * J);
+    o_idx2 = add(4 * J);
+    o_prob = add(8 * J);
+    o_runs = add(sizeof(Run) * nruns);
+    o_ready = add(4 * nruns);
+    o_ctl = add(64);
+    o_cub = add(cub_bytes + 256);
+    total = t + 256;
+  }
+};
+
+// control words: [0] queue tail, [1] queue head, [2] samples finished, [3] participants
+__device__ __forceinline__ int ld_volatile(const int *p) { return *(volatile const int *)p; }
+
+__global__ void walk_prepare_kernel(const int64_t *__restrict__ hkey_in, int64_t J, uint64_t k0,
+                                    uint64_t k1, const double *__restrict__ ov,
+                                    const double *__restrict__ rin, const int32_t *__restrict__ sel,
+                                    int32_t selv, int64_t *__restrict__ key, double *__restrict__ r,
+                                    int32_t *__restrict__ idx) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= J) return;
+  double u;
+  if (ov) u = ov[s];
+  else if (rin) u = rin[s];
+  else u = u64_to_unit(philox_word(k0, k1, (uint64_t)s));
+  const bool mine = !sel || sel[s] == selv;
+  r[s] = u;
+  key[s] = mine ? (hkey_in ? hkey_in[s] : 0) : INT64_MAX;
+  idx[s] = (int32_t)s;
+}
+
+__global__ void walk_gather_kernel(const int64_t *__restrict__ key_in, const int32_t *__restrict__ idx,
+                                   int64_t J, int64_t *__restrict__ key_out) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s < J) key_out[s] = key_in[idx[s]];
+}
+
+// Seed one root run per distinct key; count participants; init per-sample probability.
+__global__ void walk_seed_kernel(const int64_t *__restrict__ key, const int32_t *__restrict__ idx,
+                                 int64_t J, const double *__restrict__ pmp_in,
+                                 double *__restrict__ prob, Run *runs, int *ready, int *ctl) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= J) return;
+  const int64_t k = key[s];
+  prob[s] = pmp_in ? pmp_in[idx[s]] : 1.0;
+  if (k == INT64_MAX) return;
+  atomicAdd(&ctl[3], 1);
+  if (s > 0 && key[s - 1] == k) return;
+  // run end: first position with a larger key
+  int64_t lo = s + 1, hi = J;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (key[mid] <= k) lo = mid + 1; else hi = mid;
+  }
+  const int t = atomicAdd(&ctl[0], 1);
+  Run rr;
+  rr.lo = (int32_t)s;
+  rr.hi = (int32_t)lo;
+  rr.level = 0;
+  rr.node = 0;
+  runs[t] = rr;
+  ready[t] = 1;
+}
+
+__device__ __forceinline__ void push_run(Run *runs, int *ready, int *ctl, int32_t lo, int32_t hi,
+                                         int32_t level, int32_t node) {
+  const int t = atomicAdd(&ctl[0], 1);
+  Run rr;
+  rr.lo = lo;
+  rr.hi = hi;
+  rr.level = level;
+  rr.node = node;
+  runs[t] = rr;
+  __threadfence();
+  atomicExch(&ready[t], 1);
+}
+
+__global__ void row_keys_kernel(const int64_t *__restrict__ X, int N, int64_t J, Strides8 st,
+                                int64_t *__restrict__ out) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= J) return;
+  int64_t k = 0;
+  for (int m = 0; m < N; ++m)
+    if (st.s[m]) k += X[(int64_t)m * J + s] * st.s[m];
+  out[s] = k;
+}
+
+__global__ void __launch_bounds__(kWalkWarps * 32)
+walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, int64_t n, int R,
+                 int leaf, int depth, int64_t row_lo, const double *__restrict__ Mfull,
+                 const double *__restrict__ H, const int32_t *__restrict__ idx,
+                 double *__restrict__ r, double *__restrict__ prob, Run *runs, int *ready, int *ctl,
+                 int64_t cap_runs, int64_t *__restrict__ Xi, double *__restrict__ pmp,
+                 double *__restrict__ resid, double *__restrict__ urow, int *status) {
+  extern __shared__ double sh[];
+  const int Rt = R * (R + 1) / 2;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double *Mp = sh;                                              // Rt, off-diagonals x2
+  double *P = Mp + Rt + (size_t)wid * (Rt + R + kMaxLeaf + 2);  // per warp: Rt
+  double *uv = P + Rt;                                          // R
+  double *mass = uv + R;                                        // leaf
+  uint16_t *pairs = reinterpret_cast<uint16_t *>(Mp + Rt + (size_t)nw * (Rt + R + kMaxLeaf + 2));
+  for (int e = threadIdx.x; e < Rt; e += blockDim.x) {
+    int a = 0, rem = e;
+    while (rem >= R - a) {
+      rem -= R - a;
+      ++a;
+    }
+    const int b = a + rem;
+    pairs[e] = (uint16_t)(a | (b << 8));
+    const double m = Mfull[a * R + b];
+    Mp[e] = (a == b) ? m : 2.0 * m;
+  }
+  __syncthreads();
+  const double tiny = DBL_MIN;
+  const int total = ld_volatile(&ctl[3]);
+
+  while (true) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&ctl[1], 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    // wait for run t to be published, or for every participant to finish
+    bool quit = false;
+    uint64_t t_start = 0;
+    if (lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    while (true) {
+      int rd = 0, dn = 0;
+      if (lane == 0) {
+        rd = t < cap_runs ? ld_volatile(&ready[t]) : 0;
+        dn = ld_volatile(&ctl[2]);
+      }
+      rd = __shfl_sync(0xffffffffu, rd, 0);
+      dn = __shfl_sync(0xffffffffu, dn, 0);
+      if (rd) break;
+      if (dn >= total) {
+        quit = true;
+        break;
+      }
+      // watchdog: a queue that never drains is a bug -- fail loudly instead of hanging
+      int expired = 0;
+      if (lane == 0) {
+        uint64_t now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        expired = (now - t_start) > 4000000000ull;
+      }
+      if (__shfl_sync(0xffffffffu, expired, 0)) {
+        if (lane == 0) raise_status(status, RCP_ST_TIMEOUT);
+        quit = true;
+        break;
+      }
+      __nanosleep(200);
+    }
+    if (quit) break;
+    __threadfence();
+    const Run run = runs[t];
+    const int32_t lo = run.lo, hi = run.hi;
+    // P = (h h^T) (.) M' of the run's common Hadamard row
+    const int32_t s0 = idx[lo];
+    for (int e = lane; e < Rt; e += 32) {
+      const uint16_t ab = pairs[e];
+      const double ha = H ? H[(int64_t)s0 * R + (ab & 0xff)] : 1.0;
+      const double hb = H ? H[(int64_t)s0 * R + (ab >> 8)] : 1.0;
+      P[e] = ha * hb * Mp[e];
+    }
+    __syncwarp();
+    if (run.level < depth) {
+      const int64_t v = run.node;
+      const double *GL = tree + ((1LL << (run.level + 1)) - 1 + 2 * v) * (int64_t)Rt;
+      const double *GR = GL + Rt;
+      double qL = 0.0, qR = 0.0;
+      for (int e = lane; e < Rt; e += 32) {
+        const double p = P[e];
+        qL = fma(__ldg(GL + e), p, qL);
+        qR = fma(__ldg(GR + e), p, qR);
+      }
+      qL = warp_sum(qL);
+      qR = warp_sum(qR);
+      qL = qL > 0.0 ? qL : 0.0;
+      qR = qR > 0.0 ? qR : 0.0;
+      const double tot = qL + qR;
+      if (!(tot > 0.0)) {
+        for (int32_t s = lo + lane; s < hi; s += 32) Xi[idx[s]] = -1;
+        if (lane == 0) {
+          raise_status(status, RCP_ST_DEGENERATE);
+          __threadfence();
+          atomicAdd(&ctl[2], hi - lo);
+        }
+        continue;
+      }
+      double T = qL / tot;
+      T = fmin(fmax(T, 0.0), 1.0);
+      // left-goers (r < T) form a prefix of the r-sorted run
+      int32_t nl = 0;
+      if (lane == 0) {
+        int32_t a = lo, b = hi;
+        while (a < b) {
+          int32_t mid = (a + b) >> 1;
+          if (r[mid] < T) a = mid + 1; else b = mid;
+        }
+        nl = a - lo;
+      }
+      nl = __shfl_sync(0xffffffffu, nl, 0);
+      const double den_l = fmax(T, tiny), den_r = fmax(1.0 - T, tiny);
+      for (int32_t s = lo + lane; s < hi; s += 32) {
+        const double x = r[s];
+        const bool right = x >= T;
+        double y = right ? (x - T) / den_r : x / den_l;
+        r[s] = fmin(fmax(y, 0.0), one_below());
+        prob[s] *= right ? (1.0 - T) : T;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        if (nl > 0) push_run(runs, ready, ctl, lo, lo + nl, run.level + 1, (int32_t)(2 * v));
+        if (hi - lo - nl > 0) push_run(runs, ready, ctl, lo + nl, hi, run.level + 1, (int32_t)(2 * v + 1));
+      }
+      continue;
+    }
+    // ---- leaf block: masses of its rows, then each sample's inverse CDF
+    const int64_t r0 = (int64_t)run.node * leaf;
+    const int nr = (int)min((int64_t)leaf, n - r0);
+    bool bad = nr <= 0;
+    double total_m = 0.0;
+    if (!bad) {
+      for (int q = 0; q < nr; ++q) {
+        for (int c = lane; c < R; c += 32) uv[c] = U[(r0 + q) * R + c];
+        __syncwarp();
+        double m = 0.0;
+        for (int e = lane; e < Rt; e += 32) {
+          const uint16_t ab = pairs[e];
+          m = fma(uv[ab & 0xff] * uv[ab >> 8], P[e], m);
+        }
+        m = warp_sum(m);
+        if (lane == 0) mass[q] = m > 0.0 ? m : 0.0;
+        __syncwarp();
+      }
+      if (lane == 0)
+        for (int q = 0; q < nr; ++q) total_m += mass[q];
+      total_m = __shfl_sync(0xffffffffu, total_m, 0);
+      bad = !(total_m > 0.0);
+    }
+    if (bad) {
+      for (int32_t s = lo + lane; s < hi; s += 32) Xi[idx[s]] = -1;
+      if (lane == 0) {
+        raise_status(status, RCP_ST_DEGENERATE);
+        __threadfence();
+        atomicAdd(&ctl[2], hi - lo);
+      }
+      continue;
+    }
+    for (int32_t s = lo + lane; s < hi; s += 32) {
+      const double target = r[s] * total_m;
+      double cdf = 0.0;
+      int cnt = 0;
+      for (int q = 0; q < nr; ++q) {
+        cdf += mass[q];
+        if (cdf <= target) ++cnt;
+      }
+      const int choice = cnt < nr - 1 ? cnt : nr - 1;
+      double cdf_at = 0.0;
+      for (int q = 0; q <= choice; ++q) cdf_at += mass[q];
+      const double picked = mass[choice];
+      double ro = picked > 0.0 ? (target - (cdf_at - picked)) / picked : 0.0;
+      ro = fmin(fmax(ro, 0.0), one_below());
+      const int32_t o = idx[s];
+      const int64_t row = r0 + choice;
+      Xi[o] = row_lo + row;
+      pmp[o] = prob[s] * (picked / total_m);
+      if (resid) resid[o] = ro;
+      const double *src = U + row * R;
+      double *dst = urow + (int64_t)o * R;
+      for (int c = 0; c < R; ++c) dst[c] = src[c];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(&ctl[2], hi - lo);
+    }
+  }
+}
+
+size_t walk_smem(int R, int warps) {
+  const int Rt = R * (R + 1) / 2;
+  return sizeof(double) * ((size_t)Rt + (size_t)warps * (Rt + R + kMaxLeaf + 2)) +
+         sizeof(uint16_t) * (size_t)Rt + 64;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf) {
+  WalkWs w(J > 0 ? J : 1, rcp_sts_depth(n, leaf));
+  return w.total;
+}
+
+int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
+                 int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
+                 int64_t J, uint64_t key0, uint64_t key1, const double *d_override,
+                 const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
+                 double *d_pmp_i, double *d_resid, double *d_urow_out, void *d_ws,
+                 size_t ws_bytes, int *d_status, void *stream) {
+  if (R < 1 || R > RCP_MAX_RANK || leaf < 1 || leaf > kMaxLeaf || J < 0 || n < 0 ||
+      J >= (1LL << 31))
+    return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  if (n == 0 || !d_tree || !d_U || !d_M || !d_Xi || !d_pmp_i || !d_urow_out || !d_ws)
+    return RCP_ERR_ARG;
+  const int depth = rcp_sts_depth(n, leaf);
+  WalkWs L(J, depth);
+  if (ws_bytes < L.total) return RCP_ERR_ARG;
+  int warps = kWalkWarps;
+  while (warps > 1 && walk_smem(R, warps) > 200 * 1024) --warps;
+  const size_t smem = walk_smem(R, warps);
+  if (smem > 220 * 1024) return RCP_ERR_ARG;
+  cudaStream_t st = RCP_STREAM(stream);
+  char *w = (char *)d_ws;
+  int64_t *key = (int64_t *)(w + L.o_key), *key2 = (int64_t *)(w + L.o_key2);
+  double *r = (double *)(w + L.o_r), *r2 = (double *)(w + L.o_r2);
+  int32_t *idx = (int32_t *)(w + L.o_idx), *idx2 = (int32_t *)(w + L.o_idx2);
+  double *prob = (double *)(w + L.o_prob);
+  Run *runs = (Run *)(w + L.o_runs);
+  int *ready = (int *)(w + L.o_ready);
+  int *ctl = (int *)(w + L.o_ctl);
+  void *cub_tmp = w + L.o_cub;
+  const int64_t nruns = J * (int64_t)(depth + 2) + 16;
+  const unsigned gb = (unsigned)ceil_div(J, 256);
+  walk_prepare_kernel<<<gb, 256, 0, st>>>(d_hkey, J, key0, key1, d_override, d_rin, d_sel,
+                                          sel_value, key, r, idx);
+  RCP_LAUNCH_CHECK("walk_prepare");
+  // sort by r, then stably by key: runs of equal key are contiguous and r-ordered
+  size_t tb = L.cub_bytes;
+  RCP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, r, r2, idx, idx2, (int)J, 0, 64, st));
+  walk_gather_kernel<<<gb, 256, 0, st>>>(key, idx2, J, key2);
+  RCP_LAUNCH_CHECK("walk_gather");
+  tb = L.cub_bytes;
+  RCP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key2, key, idx2, idx, (int)J, 0, 64, st));
+  // r in final order (gather from the original draws)
+  walk_gather_kernel<<<gb, 256, 0, st>>>((const int64_t *)r, idx, J, (int64_t *)r2);
+  RCP_LAUNCH_CHECK("walk_gather_r");
+  RCP_CUDA_TRY(cudaMemsetAsync(ready, 0, sizeof(int) * nruns, st));
+  RCP_CUDA_TRY(cudaMemsetAsync(ctl, 0, 64, st));
+  walk_seed_kernel<<<gb, 256, 0, st>>>(key, idx, J, d_sel ? d_pmp_i : nullptr, prob, runs, ready,
+                                       ctl);
+  RCP_LAUNCH_CHECK("walk_seed");
+  static bool attr = false;
+  if (!attr) {
+    RCP_CUDA_TRY(cudaFuncSetAttribute(walk_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      220 * 1024));
+    attr = true;
+  }
+  int per_sm = 0;
+  RCP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_runs_kernel,
+                                                             warps * 32, smem));
+  if (per_sm < 1) return RCP_ERR_ARG;
+  // persistent: every CTA resident at once (workers wait on the shared queue)
+  const int grid = per_sm * sm_count();
+  walk_runs_kernel<<<grid, warps * 32, smem, st>>>(d_tree, d_U, n, R, leaf, depth, row_lo, d_M,
+                                                  d_H_in, idx, r2, prob, runs, ready, ctl, nruns,
+                                                  d_Xi, d_pmp_i, d_resid, d_urow_out, d_status);
+  RCP_LAUNCH_CHECK("walk_runs");
+  return RCP_OK;
+}
+
+int rcp_row_keys(const int64_t *d_X, int N, int64_t J, const int64_t *h_strides, int64_t *d_out,
+                 void *stream) {
+  if (N < 1 || N > 8 || J < 0 || !h_strides) return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  if (!d_X || !d_out) return RCP_ERR_ARG;
+  Strides8 sd;
+  for (int m = 0; m < 8; ++m) sd.s[m] = m < N ? h_strides[m] : 0;
+  row_keys_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, RCP_STREAM(stream)>>>(d_X, N, J, sd, d_out);
+  RCP_LAUNCH_CHECK("row_keys");
+  return RCP_OK;
+}
+
+}  // extern "C"

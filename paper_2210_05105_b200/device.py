@@ -99,6 +99,8 @@ class Status:
             raise ValueError("zero total leverage mass; nothing to sample from %s" % where)
         if v & _lib.ST_ZERO_PROB:
             raise ValueError("sample with zero probability cannot have been drawn %s" % where)
+        if v & _lib.ST_TIMEOUT:
+            raise RuntimeError("device work queue watchdog expired %s" % where)
         if v & _lib.ST_CAPACITY:
             raise RuntimeError("sampled-MTTKRP workspace too small %s" % where)
         raise RuntimeError("device status 0x%x %s" % (v, where))

@@ -111,6 +111,7 @@ class RankState:
         self.prob_tmp = t.zeros(J, **f64)
         self.urow_tmp = t.zeros((J, R), **f64) if self.P > 1 else None
         self.perm = t.zeros(J, dtype=t.int64, device=dev)
+        self.hkey = t.zeros(J, dtype=t.int64, device=dev)
         self.chain_pinv = t.zeros((R, R), **f64)
         self.M = t.zeros((R, R), **f64)
         self.Gs = t.zeros((R, R), **f64)
@@ -223,9 +224,10 @@ class RankState:
             self.pmp[i].fill_(1.0)
             sel, rin = None, None
         if self.n[i] > 0:
+            hk = ops.walk_key(self.X, self.dims, k, i, self.hkey)
             ops.sts_walk(self.trees[i], self.U[i], self.leaf_of(i), self.lo[i], self.M, H_in,
                          self.J, key, override if self.P == 1 else None, rin, sel, self.rank,
-                         self.X[i], self.pmp[i], self.resid, self.urow)
+                         self.X[i], self.pmp[i], self.resid, self.urow, hkey=hk)
 
     def _ones_H(self):
         if not hasattr(self, "_H1"):

@@ -110,12 +110,34 @@ class Ops:
                 stream_handle())
 
     def sts_walk(self, tree, U, leaf, row_lo, M, H_in, J, key, override, rin, sel, sel_value,
-                 Xi, pmp_i, resid, urow):
+                 Xi, pmp_i, resid, urow, hkey=None):
         n, R = U.shape
+        w = self.ws("sts_walk", self.lib.rcp_sts_walk_ws_bytes(int(J), n, int(leaf)))
         self._c("rcp_sts_walk", ptr(tree), ptr(U), n, R, int(leaf), int(row_lo), ptr(M),
-                ptr(H_in), int(J), key[0], key[1], ptr(override), ptr(rin), ptr(sel),
-                int(sel_value), ptr(Xi), ptr(pmp_i), ptr(resid), ptr(urow), self.status.ptr,
-                stream_handle())
+                ptr(H_in), ptr(hkey), int(J), key[0], key[1], ptr(override), ptr(rin), ptr(sel),
+                int(sel_value), ptr(Xi), ptr(pmp_i), ptr(resid), ptr(urow), ptr(w), w.numel(),
+                self.status.ptr, stream_handle())
+
+    def row_keys(self, X, strides, out):
+        N, J = X.shape
+        st = np.ascontiguousarray(strides, dtype=np.int64)
+        self._c("rcp_row_keys", ptr(X), N, J, st.ctypes.data, ptr(out), stream_handle())
+
+    def walk_key(self, X, dims, k, i, out):
+        """Mixed-radix key of the modes already sampled before constant mode i
+        (modes < i, excluding k); None for the first constant mode."""
+        prev = [m for m in range(i) if m != k]
+        if not prev:
+            return None
+        strides = [0] * len(dims)
+        span = 1
+        for m in prev:
+            strides[m] = span
+            span *= int(dims[m])
+        if span >= (1 << 63):
+            raise ValueError("walk grouping key overflows int64")
+        self.row_keys(X, strides, out)
+        return out
 
     def sts_rank_walk(self, node_grams, depth, P, leaf_rank, M, H, J, key, override, owner,
                       r_out, pmp_i):

@@ -283,6 +283,7 @@ def sts_sample(trees, k, J, gram_chain_pinv, grams, blocks_per_mode, seed, round
     rtop = t.zeros(J, dtype=t.float64, device=dev)
     M = t.zeros((R, R), dtype=t.float64, device=dev)
     ones = t.ones((J, R), dtype=t.float64, device=dev)
+    hkey = t.zeros(J, dtype=t.int64, device=dev)
     ov_all = None
     if uniform_override is not None:
         ov_all = to_dev(np.asarray(uniform_override, dtype=np.float64).T.copy(), dev, t.float64)
@@ -295,6 +296,8 @@ def sts_sample(trees, k, J, gram_chain_pinv, grams, blocks_per_mode, seed, round
         key = rng.stream_key(seed, rng.WALK_UNIFORM, round_id, k, i)
         ov = ov_all[i] if ov_all is not None else None
         H_in = None if first else H
+        dims = [int(tt.block_hi.max()) if tt is not None else 1 for tt in trees]
+        hk = ops.walk_key(X, dims, k, i, hkey)
         depth = trees[i].depth
         if P > 1 and depth > 0:
             ops.sts_rank_walk(tr["node_grams"], depth, P, tr["leaf_rank"], M,
@@ -303,7 +306,8 @@ def sts_sample(trees, k, J, gram_chain_pinv, grams, blocks_per_mode, seed, round
                 if tr["trees"][p] is None:
                     continue
                 ops.sts_walk(tr["trees"][p], tr["U"][p], tr["leaves"][p], int(trees[i].block_lo[p]),
-                             M, H_in, J, key, None, rtop, owner, p, X[i], pmp[i], resid, urow)
+                             M, H_in, J, key, None, rtop, owner, p, X[i], pmp[i], resid, urow,
+                             hkey=hk)
             # samples routed to a rank without rows (ref samplers.py:341-342)
             ops.status.check("in sts_sample")
             if bool((X[i] < 0).any()):
@@ -314,7 +318,7 @@ def sts_sample(trees, k, J, gram_chain_pinv, grams, blocks_per_mode, seed, round
             if tr["trees"][p] is None:
                 raise DegenerateWalkError("walk reached a rank with no rows")
             ops.sts_walk(tr["trees"][p], tr["U"][p], tr["leaves"][p], int(trees[i].block_lo[p]), M,
-                         H_in, J, key, ov, None, None, 0, X[i], pmp[i], resid, urow)
+                         H_in, J, key, ov, None, None, 0, X[i], pmp[i], resid, urow, hkey=hk)
         ops.hadamard_rows(H, urow, init=first)
         first = False
     ops.status.check("in sts_sample")
