@@ -10,10 +10,13 @@
 // modes) see identical node masses.  Sorting the samples by (key of those indices, r)
 // makes each such group contiguous and ordered by r; at every node the left-goers are a
 // prefix of the group.  A group at a node is a *run* [lo, hi) of the sorted array: its
-// masses are computed once, the run splits into a left and a right run, and the walk is a
-// parallel breadth of run splits driven by a device work queue (persistent warps).  The
-// arithmetic per sample is the same as a per-sample walk; the work is proportional to the
-// number of distinct (h, node) pairs instead of samples x levels.
+// masses are computed once, the split point is found by binary search, and the run splits
+// into a left and a right run.  A run carries its path (thresholds T and directions from
+// the root) and the product of its step probabilities, which all its samples share, so no
+// per-sample state is touched above the leaves: a sample's rescaled residual at any level
+// is recomputed from its uniform by replaying the path's rescalings in the reference's
+// order.  Runs flow through a device work queue served by persistent warps.  Work is
+// proportional to the number of distinct (h, node) pairs, not samples x levels.
 #include <cub/device/device_radix_sort.cuh>
 #include <float.h>
 
@@ -34,18 +37,23 @@ int sm_count() {
 
 constexpr int kMaxLeaf = 64;
 constexpr int kWalkWarps = 8;
+constexpr int kMaxDepth = 30;   // local tree depth limit (2^30 leaves)
 
 struct Run {
-  int32_t lo, hi;    // sorted positions
-  int32_t level;     // tree level of `node`
-  int32_t node;      // node index within its level
+  int32_t lo, hi;      // sorted positions [lo, hi)
+  int32_t level;       // tree level of `node`
+  int32_t node;        // node index within its level
+  uint32_t dirs;       // bit l: direction taken at level l (1 = right)
+  int32_t pad;
+  double prob;         // product of the step probabilities so far
+  double T[kMaxDepth]; // thresholds at levels 0 .. level-1
 };
 
 struct WalkWs {
-  size_t o_key, o_key2, o_r, o_r2, o_idx, o_idx2, o_prob, o_runs, o_ready, o_ctl, o_cub, total;
+  size_t o_key, o_key2, o_r, o_r2, o_idx, o_idx2, o_runs, o_ready, o_ctl, o_cub, total;
   size_t cub_bytes;
+  int64_t nruns;
   WalkWs(int64_t J, int depth) {
-    cub_bytes = 0;
     size_t b1 = 0, b2 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b1, (const double *)nullptr, (double *)nullptr,
                                     (const int32_t *)nullptr, (int32_t *)nullptr, (int)J);
@@ -58,14 +66,14 @@ struct WalkWs {
       t = o + bytes;
       return o;
     };
-    const int64_t nruns = J * (int64_t)(depth + 2) + 16;
+    // runs per level partition the samples: at most J per level, depth+1 levels
+    nruns = J * (int64_t)(depth + 1) + 16;
     o_key = add(8 * J);
     o_key2 = add(8 * J);
     o_r = add(8 * J);
     o_r2 = add(8 * J);
     o_idx = add(4 * J);
     o_idx2 = add(4 * J);
-    o_prob = add(8 * J);
     o_runs = add(sizeof(Run) * nruns);
     o_ready = add(4 * nruns);
     o_ctl = add(64);
@@ -76,6 +84,18 @@ struct WalkWs {
 
 // control words: [0] queue tail, [1] queue head, [2] samples finished, [3] participants
 __device__ __forceinline__ int ld_volatile(const int *p) { return *(volatile const int *)p; }
+
+// The reference's per-level residual rescaling (ref samplers.py:436-440).
+__device__ __forceinline__ double rescale(double r, double T, bool right) {
+  const double tiny = DBL_MIN;
+  const double y = right ? (r - T) / fmax(1.0 - T, tiny) : r / fmax(T, tiny);
+  return fmin(fmax(y, 0.0), one_below());
+}
+
+__device__ __forceinline__ double replay(double r, const double *T, uint32_t dirs, int level) {
+  for (int l = 0; l < level; ++l) r = rescale(r, T[l], (dirs >> l) & 1u);
+  return r;
+}
 
 __global__ void walk_prepare_kernel(const int64_t *__restrict__ hkey_in, int64_t J, uint64_t k0,
                                     uint64_t k1, const double *__restrict__ ov,
@@ -94,48 +114,36 @@ __global__ void walk_prepare_kernel(const int64_t *__restrict__ hkey_in, int64_t
   idx[s] = (int32_t)s;
 }
 
-__global__ void walk_gather_kernel(const int64_t *__restrict__ key_in, const int32_t *__restrict__ idx,
-                                   int64_t J, int64_t *__restrict__ key_out) {
+__global__ void walk_gather_kernel(const int64_t *__restrict__ in, const int32_t *__restrict__ idx,
+                                   int64_t J, int64_t *__restrict__ out) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s < J) key_out[s] = key_in[idx[s]];
+  if (s < J) out[s] = in[idx[s]];
 }
 
-// Seed one root run per distinct key; count participants; init per-sample probability.
+// One root run per distinct key; counts participants.
 __global__ void walk_seed_kernel(const int64_t *__restrict__ key, const int32_t *__restrict__ idx,
-                                 int64_t J, const double *__restrict__ pmp_in,
-                                 double *__restrict__ prob, Run *runs, int *ready, int *ctl) {
+                                 int64_t J, const double *__restrict__ pmp_in, Run *runs,
+                                 int *ready, int *ctl) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= J) return;
   const int64_t k = key[s];
-  prob[s] = pmp_in ? pmp_in[idx[s]] : 1.0;
   if (k == INT64_MAX) return;
   atomicAdd(&ctl[3], 1);
   if (s > 0 && key[s - 1] == k) return;
-  // run end: first position with a larger key
-  int64_t lo = s + 1, hi = J;
+  int64_t lo = s + 1, hi = J;   // first position with a larger key
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
     if (key[mid] <= k) lo = mid + 1; else hi = mid;
   }
   const int t = atomicAdd(&ctl[0], 1);
-  Run rr;
+  Run &rr = runs[t];
   rr.lo = (int32_t)s;
   rr.hi = (int32_t)lo;
   rr.level = 0;
   rr.node = 0;
-  runs[t] = rr;
-  ready[t] = 1;
-}
-
-__device__ __forceinline__ void push_run(Run *runs, int *ready, int *ctl, int32_t lo, int32_t hi,
-                                         int32_t level, int32_t node) {
-  const int t = atomicAdd(&ctl[0], 1);
-  Run rr;
-  rr.lo = lo;
-  rr.hi = hi;
-  rr.level = level;
-  rr.node = node;
-  runs[t] = rr;
+  rr.dirs = 0u;
+  // samples of one group share their rank-level path, hence this probability
+  rr.prob = pmp_in ? pmp_in[idx[s]] : 1.0;
   __threadfence();
   atomicExch(&ready[t], 1);
 }
@@ -150,21 +158,47 @@ __global__ void row_keys_kernel(const int64_t *__restrict__ X, int N, int64_t J,
   out[s] = k;
 }
 
+// Warp-cooperative push of a child run (path of the parent + one step).
+__device__ __forceinline__ void push_child(Run *runs, int *ready, int *ctl, const Run &par,
+                                           int32_t lo, int32_t hi, double T, bool right,
+                                           int lane) {
+  int t = 0;
+  if (lane == 0) t = atomicAdd(&ctl[0], 1);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  Run &c = runs[t];
+  const int lev = par.level;
+  if (lane < lev) c.T[lane] = par.T[lane];
+  if (lane == 0) {
+    c.lo = lo;
+    c.hi = hi;
+    c.level = lev + 1;
+    c.node = 2 * par.node + (right ? 1 : 0);
+    c.dirs = par.dirs | ((right ? 1u : 0u) << lev);
+    c.prob = par.prob * (right ? (1.0 - T) : T);
+    c.T[lev] = T;
+  }
+  __syncwarp();
+  __threadfence();
+  if (lane == 0) atomicExch(&ready[t], 1);
+}
+
 __global__ void __launch_bounds__(kWalkWarps * 32)
 walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, int64_t n, int R,
                  int leaf, int depth, int64_t row_lo, const double *__restrict__ Mfull,
                  const double *__restrict__ H, const int32_t *__restrict__ idx,
-                 double *__restrict__ r, double *__restrict__ prob, Run *runs, int *ready, int *ctl,
-                 int64_t cap_runs, int64_t *__restrict__ Xi, double *__restrict__ pmp,
-                 double *__restrict__ resid, double *__restrict__ urow, int *status) {
+                 const double *__restrict__ r, Run *runs, int *ready, int *ctl, int64_t cap_runs,
+                 int64_t *__restrict__ Xi, double *__restrict__ pmp, double *__restrict__ resid,
+                 double *__restrict__ urow, int *status) {
   extern __shared__ double sh[];
   const int Rt = R * (R + 1) / 2;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double *Mp = sh;                                              // Rt, off-diagonals x2
-  double *P = Mp + Rt + (size_t)wid * (Rt + R + kMaxLeaf + 2);  // per warp: Rt
-  double *uv = P + Rt;                                          // R
-  double *mass = uv + R;                                        // leaf
-  uint16_t *pairs = reinterpret_cast<uint16_t *>(Mp + Rt + (size_t)nw * (Rt + R + kMaxLeaf + 2));
+  const size_t per_warp = (size_t)Rt + R + kMaxLeaf + kMaxDepth + 2;
+  double *Mp = sh;                                 // Rt: packed M, off-diagonals x2
+  double *P = Mp + Rt + (size_t)wid * per_warp;    // per warp: Rt
+  double *uv = P + Rt;                             // R
+  double *mass = uv + R;                           // leaf
+  double *Tp = mass + kMaxLeaf;                    // path thresholds of the current run
+  uint16_t *pairs = reinterpret_cast<uint16_t *>(Mp + Rt + (size_t)nw * per_warp);
   for (int e = threadIdx.x; e < Rt; e += blockDim.x) {
     int a = 0, rem = e;
     while (rem >= R - a) {
@@ -177,7 +211,6 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
     Mp[e] = (a == b) ? m : 2.0 * m;
   }
   __syncthreads();
-  const double tiny = DBL_MIN;
   const int total = ld_volatile(&ctl[3]);
 
   while (true) {
@@ -213,12 +246,14 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
         quit = true;
         break;
       }
-      __nanosleep(200);
+      __nanosleep(128);
     }
     if (quit) break;
     __threadfence();
-    const Run run = runs[t];
-    const int32_t lo = run.lo, hi = run.hi;
+    const Run &run = runs[t];
+    const int32_t lo = run.lo, hi = run.hi, level = run.level;
+    const uint32_t dirs = run.dirs;
+    if (lane < level) Tp[lane] = run.T[lane];
     // P = (h h^T) (.) M' of the run's common Hadamard row
     const int32_t s0 = idx[lo];
     for (int e = lane; e < Rt; e += 32) {
@@ -228,9 +263,9 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
       P[e] = ha * hb * Mp[e];
     }
     __syncwarp();
-    if (run.level < depth) {
+    if (level < depth) {
       const int64_t v = run.node;
-      const double *GL = tree + ((1LL << (run.level + 1)) - 1 + 2 * v) * (int64_t)Rt;
+      const double *GL = tree + ((1LL << (level + 1)) - 1 + 2 * v) * (int64_t)Rt;
       const double *GR = GL + Rt;
       double qL = 0.0, qR = 0.0;
       for (int e = lane; e < Rt; e += 32) {
@@ -245,6 +280,7 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
       const double tot = qL + qR;
       if (!(tot > 0.0)) {
         for (int32_t s = lo + lane; s < hi; s += 32) Xi[idx[s]] = -1;
+        __syncwarp();
         if (lane == 0) {
           raise_status(status, RCP_ST_DEGENERATE);
           __threadfence();
@@ -254,36 +290,37 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
       }
       double T = qL / tot;
       T = fmin(fmax(T, 0.0), 1.0);
-      // left-goers (r < T) form a prefix of the r-sorted run
-      int32_t nl = 0;
-      if (lane == 0) {
-        int32_t a = lo, b = hi;
-        while (a < b) {
-          int32_t mid = (a + b) >> 1;
-          if (r[mid] < T) a = mid + 1; else b = mid;
+      // left-goers (replayed r < T) are a prefix of the r-sorted run: 32-ary search
+      int32_t a = lo, b = hi;   // answer in [a, b]
+      while (b - a > 0) {
+        const int32_t span = b - a;
+        const int32_t step = (span + 31) / 32;
+        const int32_t pos = a + lane * step;
+        bool ge = true;   // "replayed r >= T" at pos (positions >= b count as true)
+        if (pos < b) ge = replay(r[pos], Tp, dirs, level) >= T;
+        const unsigned m = __ballot_sync(0xffffffffu, ge);
+        if (m == 0u) {                     // every probe < T: answer beyond the last probe
+          a = a + 31 * step + 1;
+          continue;
         }
-        nl = a - lo;
+        const int first = __ffs(m) - 1;   // first lane whose probe is >= T
+        if (first == 0) {
+          b = a;
+        } else {                           // answer in (probe[first-1], probe[first]]
+          const int32_t na = a + (first - 1) * step + 1;
+          b = min(b, a + first * step);
+          a = na;
+        }
       }
-      nl = __shfl_sync(0xffffffffu, nl, 0);
-      const double den_l = fmax(T, tiny), den_r = fmax(1.0 - T, tiny);
-      for (int32_t s = lo + lane; s < hi; s += 32) {
-        const double x = r[s];
-        const bool right = x >= T;
-        double y = right ? (x - T) / den_r : x / den_l;
-        r[s] = fmin(fmax(y, 0.0), one_below());
-        prob[s] *= right ? (1.0 - T) : T;
-      }
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        if (nl > 0) push_run(runs, ready, ctl, lo, lo + nl, run.level + 1, (int32_t)(2 * v));
-        if (hi - lo - nl > 0) push_run(runs, ready, ctl, lo + nl, hi, run.level + 1, (int32_t)(2 * v + 1));
-      }
+      const int32_t nl = a - lo;
+      if (nl > 0) push_child(runs, ready, ctl, run, lo, lo + nl, T, false, lane);
+      if (hi - lo - nl > 0) push_child(runs, ready, ctl, run, lo + nl, hi, T, true, lane);
       continue;
     }
     // ---- leaf block: masses of its rows, then each sample's inverse CDF
     const int64_t r0 = (int64_t)run.node * leaf;
     const int nr = (int)min((int64_t)leaf, n - r0);
+    const double rprob = run.prob;
     bool bad = nr <= 0;
     double total_m = 0.0;
     if (!bad) {
@@ -306,6 +343,7 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
     }
     if (bad) {
       for (int32_t s = lo + lane; s < hi; s += 32) Xi[idx[s]] = -1;
+      __syncwarp();
       if (lane == 0) {
         raise_status(status, RCP_ST_DEGENERATE);
         __threadfence();
@@ -314,7 +352,7 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
       continue;
     }
     for (int32_t s = lo + lane; s < hi; s += 32) {
-      const double target = r[s] * total_m;
+      const double target = replay(r[s], Tp, dirs, level) * total_m;
       double cdf = 0.0;
       int cnt = 0;
       for (int q = 0; q < nr; ++q) {
@@ -328,13 +366,16 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
       double ro = picked > 0.0 ? (target - (cdf_at - picked)) / picked : 0.0;
       ro = fmin(fmax(ro, 0.0), one_below());
       const int32_t o = idx[s];
-      const int64_t row = r0 + choice;
-      Xi[o] = row_lo + row;
-      pmp[o] = prob[s] * (picked / total_m);
+      Xi[o] = row_lo + r0 + choice;
+      pmp[o] = rprob * (picked / total_m);
       if (resid) resid[o] = ro;
-      const double *src = U + row * R;
-      double *dst = urow + (int64_t)o * R;
-      for (int c = 0; c < R; ++c) dst[c] = src[c];
+    }
+    __syncwarp();
+    // chosen factor rows: warp-cooperative, coalesced per sample
+    for (int32_t s = lo; s < hi; ++s) {
+      const int32_t o = idx[s];
+      const int64_t row = Xi[o] - row_lo;
+      for (int c = lane; c < R; c += 32) urow[(int64_t)o * R + c] = U[row * R + c];
     }
     __syncwarp();
     if (lane == 0) {
@@ -346,7 +387,7 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
 
 size_t walk_smem(int R, int warps) {
   const int Rt = R * (R + 1) / 2;
-  return sizeof(double) * ((size_t)Rt + (size_t)warps * (Rt + R + kMaxLeaf + 2)) +
+  return sizeof(double) * ((size_t)Rt + (size_t)warps * (Rt + R + kMaxLeaf + kMaxDepth + 2)) +
          sizeof(uint16_t) * (size_t)Rt + 64;
 }
 
@@ -372,6 +413,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   if (n == 0 || !d_tree || !d_U || !d_M || !d_Xi || !d_pmp_i || !d_urow_out || !d_ws)
     return RCP_ERR_ARG;
   const int depth = rcp_sts_depth(n, leaf);
+  if (depth > kMaxDepth) return RCP_ERR_ARG;
   WalkWs L(J, depth);
   if (ws_bytes < L.total) return RCP_ERR_ARG;
   int warps = kWalkWarps;
@@ -383,12 +425,10 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   int64_t *key = (int64_t *)(w + L.o_key), *key2 = (int64_t *)(w + L.o_key2);
   double *r = (double *)(w + L.o_r), *r2 = (double *)(w + L.o_r2);
   int32_t *idx = (int32_t *)(w + L.o_idx), *idx2 = (int32_t *)(w + L.o_idx2);
-  double *prob = (double *)(w + L.o_prob);
   Run *runs = (Run *)(w + L.o_runs);
   int *ready = (int *)(w + L.o_ready);
   int *ctl = (int *)(w + L.o_ctl);
   void *cub_tmp = w + L.o_cub;
-  const int64_t nruns = J * (int64_t)(depth + 2) + 16;
   const unsigned gb = (unsigned)ceil_div(J, 256);
   walk_prepare_kernel<<<gb, 256, 0, st>>>(d_hkey, J, key0, key1, d_override, d_rin, d_sel,
                                           sel_value, key, r, idx);
@@ -396,17 +436,17 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   // sort by r, then stably by key: runs of equal key are contiguous and r-ordered
   size_t tb = L.cub_bytes;
   RCP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, r, r2, idx, idx2, (int)J, 0, 64, st));
+  RCP_LAUNCH_CHECK("walk_sort_r");
   walk_gather_kernel<<<gb, 256, 0, st>>>(key, idx2, J, key2);
   RCP_LAUNCH_CHECK("walk_gather");
   tb = L.cub_bytes;
   RCP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key2, key, idx2, idx, (int)J, 0, 64, st));
-  // r in final order (gather from the original draws)
+  RCP_LAUNCH_CHECK("walk_sort_key");
   walk_gather_kernel<<<gb, 256, 0, st>>>((const int64_t *)r, idx, J, (int64_t *)r2);
   RCP_LAUNCH_CHECK("walk_gather_r");
-  RCP_CUDA_TRY(cudaMemsetAsync(ready, 0, sizeof(int) * nruns, st));
+  RCP_CUDA_TRY(cudaMemsetAsync(ready, 0, sizeof(int) * L.nruns, st));
   RCP_CUDA_TRY(cudaMemsetAsync(ctl, 0, 64, st));
-  walk_seed_kernel<<<gb, 256, 0, st>>>(key, idx, J, d_sel ? d_pmp_i : nullptr, prob, runs, ready,
-                                       ctl);
+  walk_seed_kernel<<<gb, 256, 0, st>>>(key, idx, J, d_sel ? d_pmp_i : nullptr, runs, ready, ctl);
   RCP_LAUNCH_CHECK("walk_seed");
   static bool attr = false;
   if (!attr) {
@@ -421,7 +461,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   // persistent: every CTA resident at once (workers wait on the shared queue)
   const int grid = per_sm * sm_count();
   walk_runs_kernel<<<grid, warps * 32, smem, st>>>(d_tree, d_U, n, R, leaf, depth, row_lo, d_M,
-                                                  d_H_in, idx, r2, prob, runs, ready, ctl, nruns,
+                                                  d_H_in, idx, r2, runs, ready, ctl, L.nruns,
                                                   d_Xi, d_pmp_i, d_resid, d_urow_out, d_status);
   RCP_LAUNCH_CHECK("walk_runs");
   return RCP_OK;
