@@ -158,28 +158,34 @@ __global__ void row_keys_kernel(const int64_t *__restrict__ X, int N, int64_t J,
   out[s] = k;
 }
 
-// Warp-cooperative push of a child run (path of the parent + one step).
+// Warp-cooperative push of a child run (path of the parent + one step).  Runs entering the
+// leaf level are cut into chunks so that the per-sample leaf work spreads over warps.
+constexpr int32_t kLeafChunk = 256;
+
 __device__ __forceinline__ void push_child(Run *runs, int *ready, int *ctl, const Run &par,
                                            int32_t lo, int32_t hi, double T, bool right,
-                                           int lane) {
-  int t = 0;
-  if (lane == 0) t = atomicAdd(&ctl[0], 1);
-  t = __shfl_sync(0xffffffffu, t, 0);
-  Run &c = runs[t];
+                                           int depth, int lane) {
   const int lev = par.level;
-  if (lane < lev) c.T[lane] = par.T[lane];
-  if (lane == 0) {
-    c.lo = lo;
-    c.hi = hi;
-    c.level = lev + 1;
-    c.node = 2 * par.node + (right ? 1 : 0);
-    c.dirs = par.dirs | ((right ? 1u : 0u) << lev);
-    c.prob = par.prob * (right ? (1.0 - T) : T);
-    c.T[lev] = T;
+  const int32_t chunk = (lev + 1 == depth) ? kLeafChunk : hi - lo;
+  for (int32_t c0 = lo; c0 < hi; c0 += chunk) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&ctl[0], 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    Run &c = runs[t];
+    if (lane < lev) c.T[lane] = par.T[lane];
+    if (lane == 0) {
+      c.lo = c0;
+      c.hi = min(hi, c0 + chunk);
+      c.level = lev + 1;
+      c.node = 2 * par.node + (right ? 1 : 0);
+      c.dirs = par.dirs | ((right ? 1u : 0u) << lev);
+      c.prob = par.prob * (right ? (1.0 - T) : T);
+      c.T[lev] = T;
+    }
+    __syncwarp();
+    __threadfence();
+    if (lane == 0) atomicExch(&ready[t], 1);
   }
-  __syncwarp();
-  __threadfence();
-  if (lane == 0) atomicExch(&ready[t], 1);
 }
 
 __global__ void __launch_bounds__(kWalkWarps * 32)
@@ -188,7 +194,7 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
                  const double *__restrict__ H, const int32_t *__restrict__ idx,
                  const double *__restrict__ r, Run *runs, int *ready, int *ctl, int64_t cap_runs,
                  int64_t *__restrict__ Xi, double *__restrict__ pmp, double *__restrict__ resid,
-                 double *__restrict__ urow, int *status) {
+                 int *status) {
   extern __shared__ double sh[];
   const int Rt = R * (R + 1) / 2;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -313,8 +319,8 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
         }
       }
       const int32_t nl = a - lo;
-      if (nl > 0) push_child(runs, ready, ctl, run, lo, lo + nl, T, false, lane);
-      if (hi - lo - nl > 0) push_child(runs, ready, ctl, run, lo + nl, hi, T, true, lane);
+      if (nl > 0) push_child(runs, ready, ctl, run, lo, lo + nl, T, false, depth, lane);
+      if (hi - lo - nl > 0) push_child(runs, ready, ctl, run, lo + nl, hi, T, true, depth, lane);
       continue;
     }
     // ---- leaf block: masses of its rows, then each sample's inverse CDF
@@ -371,18 +377,27 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
       if (resid) resid[o] = ro;
     }
     __syncwarp();
-    // chosen factor rows: warp-cooperative, coalesced per sample
-    for (int32_t s = lo; s < hi; ++s) {
-      const int32_t o = idx[s];
-      const int64_t row = Xi[o] - row_lo;
-      for (int c = lane; c < R; c += 32) urow[(int64_t)o * R + c] = U[row * R + c];
-    }
-    __syncwarp();
     if (lane == 0) {
       __threadfence();
       atomicAdd(&ctl[2], hi - lo);
     }
   }
+}
+
+// out[s,:] = U[X_i[s]-row_lo, :] (init) or out[s,:] *= U[...] for the selected samples:
+// the H-row fold after a walk (ref samplers.py:464) and the owner's row payload at P > 1.
+__global__ void fold_rows_kernel(double *__restrict__ out, const double *__restrict__ U, int64_t n,
+                                 int R, int64_t row_lo, const int64_t *__restrict__ Xi, int64_t J,
+                                 int init, const int32_t *__restrict__ sel, int32_t selv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (s >= J) return;
+  if (sel && sel[s] != selv) return;
+  const int64_t row = Xi[s] - row_lo;
+  if (row < 0 || row >= n) return;
+  const double *src = U + row * R;
+  double *dst = out + s * R;
+  for (int c = lane; c < R; c += 32) dst[c] = init ? src[c] : dst[c] * src[c];
 }
 
 size_t walk_smem(int R, int warps) {
@@ -404,14 +419,13 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
                  int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
                  int64_t J, uint64_t key0, uint64_t key1, const double *d_override,
                  const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
-                 double *d_pmp_i, double *d_resid, double *d_urow_out, void *d_ws,
-                 size_t ws_bytes, int *d_status, void *stream) {
+                 double *d_pmp_i, double *d_resid, void *d_ws, size_t ws_bytes, int *d_status,
+                 void *stream) {
   if (R < 1 || R > RCP_MAX_RANK || leaf < 1 || leaf > kMaxLeaf || J < 0 || n < 0 ||
       J >= (1LL << 31))
     return RCP_ERR_ARG;
   if (J == 0) return RCP_OK;
-  if (n == 0 || !d_tree || !d_U || !d_M || !d_Xi || !d_pmp_i || !d_urow_out || !d_ws)
-    return RCP_ERR_ARG;
+  if (n == 0 || !d_tree || !d_U || !d_M || !d_Xi || !d_pmp_i || !d_ws) return RCP_ERR_ARG;
   const int depth = rcp_sts_depth(n, leaf);
   if (depth > kMaxDepth) return RCP_ERR_ARG;
   WalkWs L(J, depth);
@@ -462,8 +476,22 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   const int grid = per_sm * sm_count();
   walk_runs_kernel<<<grid, warps * 32, smem, st>>>(d_tree, d_U, n, R, leaf, depth, row_lo, d_M,
                                                   d_H_in, idx, r2, runs, ready, ctl, L.nruns,
-                                                  d_Xi, d_pmp_i, d_resid, d_urow_out, d_status);
+                                                  d_Xi, d_pmp_i, d_resid, d_status);
   RCP_LAUNCH_CHECK("walk_runs");
+  return RCP_OK;
+}
+
+int rcp_fold_rows(double *d_out, const double *d_U, int64_t n, int R, int64_t row_lo,
+                  const int64_t *d_Xi, int64_t J, int init, const int32_t *d_sel,
+                  int32_t sel_value, void *stream) {
+  if (R < 1 || J < 0 || n < 0) return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  if (!d_out || !d_U || !d_Xi) return RCP_ERR_ARG;
+  const int64_t threads = J * 32;
+  int64_t blocks = ceil_div(threads, 256);
+  fold_rows_kernel<<<(unsigned)blocks, 256, 0, RCP_STREAM(stream)>>>(d_out, d_U, n, R, row_lo, d_Xi,
+                                                                     J, init, d_sel, sel_value);
+  RCP_LAUNCH_CHECK("fold_rows");
   return RCP_OK;
 }
 

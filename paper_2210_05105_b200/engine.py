@@ -227,7 +227,12 @@ class RankState:
             hk = ops.walk_key(self.X, self.dims, k, i, self.hkey)
             ops.sts_walk(self.trees[i], self.U[i], self.leaf_of(i), self.lo[i], self.M, H_in,
                          self.J, key, override if self.P == 1 else None, rin, sel, self.rank,
-                         self.X[i], self.pmp[i], self.resid, self.urow, hkey=hk)
+                         self.X[i], self.pmp[i], self.resid, hkey=hk)
+            if self.P == 1:     # fold straight into the running Hadamard rows
+                ops.fold_rows(self.H, self.U[i], self.lo[i], self.X[i], init=first)
+            else:               # this rank's finished rows, exchanged afterwards
+                ops.fold_rows(self.urow, self.U[i], self.lo[i], self.X[i], init=True,
+                              sel=self.owner, sel_value=self.rank)
 
     def _ones_H(self):
         if not hasattr(self, "_H1"):
@@ -357,8 +362,8 @@ class Cluster:
                     r.sts_mode(i, k, rnd, first, override=ov)
                 if self.P > 1:
                     self._exchange_walk(i)
-                for r in self.ranks:
-                    r.fold_urow(first)
+                    for r in self.ranks:
+                        r.fold_urow(first)
                 first = False
         else:
             first = True

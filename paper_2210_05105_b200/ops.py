@@ -110,13 +110,19 @@ class Ops:
                 stream_handle())
 
     def sts_walk(self, tree, U, leaf, row_lo, M, H_in, J, key, override, rin, sel, sel_value,
-                 Xi, pmp_i, resid, urow, hkey=None):
+                 Xi, pmp_i, resid, hkey=None):
         n, R = U.shape
         w = self.ws("sts_walk", self.lib.rcp_sts_walk_ws_bytes(int(J), n, int(leaf)))
         self._c("rcp_sts_walk", ptr(tree), ptr(U), n, R, int(leaf), int(row_lo), ptr(M),
                 ptr(H_in), ptr(hkey), int(J), key[0], key[1], ptr(override), ptr(rin), ptr(sel),
-                int(sel_value), ptr(Xi), ptr(pmp_i), ptr(resid), ptr(urow), ptr(w), w.numel(),
+                int(sel_value), ptr(Xi), ptr(pmp_i), ptr(resid), ptr(w), w.numel(),
                 self.status.ptr, stream_handle())
+
+    def fold_rows(self, out, U, row_lo, Xi, init, sel=None, sel_value=0):
+        n, R = U.shape
+        J = Xi.shape[0]
+        self._c("rcp_fold_rows", ptr(out), ptr(U), n, R, int(row_lo), ptr(Xi), J,
+                1 if init else 0, ptr(sel), int(sel_value), stream_handle())
 
     def row_keys(self, X, strides, out):
         N, J = X.shape

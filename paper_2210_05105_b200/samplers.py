@@ -306,19 +306,23 @@ def sts_sample(trees, k, J, gram_chain_pinv, grams, blocks_per_mode, seed, round
                 if tr["trees"][p] is None:
                     continue
                 ops.sts_walk(tr["trees"][p], tr["U"][p], tr["leaves"][p], int(trees[i].block_lo[p]),
-                             M, H_in, J, key, None, rtop, owner, p, X[i], pmp[i], resid, urow,
-                             hkey=hk)
+                             M, H_in, J, key, None, rtop, owner, p, X[i], pmp[i], resid, hkey=hk)
             # samples routed to a rank without rows (ref samplers.py:341-342)
             ops.status.check("in sts_sample")
             if bool((X[i] < 0).any()):
                 raise DegenerateWalkError("walk reached a rank with no rows")
+            for p in range(P):
+                if tr["trees"][p] is not None:
+                    ops.fold_rows(urow, tr["U"][p], int(trees[i].block_lo[p]), X[i], True,
+                                  owner, p)
         else:
             p = int(trees[i].leaf_rank[0]) if P > 1 else 0
             owner.fill_(p)
             if tr["trees"][p] is None:
                 raise DegenerateWalkError("walk reached a rank with no rows")
             ops.sts_walk(tr["trees"][p], tr["U"][p], tr["leaves"][p], int(trees[i].block_lo[p]), M,
-                         H_in, J, key, ov, None, None, 0, X[i], pmp[i], resid, urow, hkey=hk)
+                         H_in, J, key, ov, None, None, 0, X[i], pmp[i], resid, hkey=hk)
+            ops.fold_rows(urow, tr["U"][p], int(trees[i].block_lo[p]), X[i], True)
         ops.hadamard_rows(H, urow, init=first)
         first = False
     ops.status.check("in sts_sample")
@@ -349,7 +353,7 @@ def local_sts_leaf_search(h, block_rows, leaf_grams, leaf_offsets, cond, r, row_
     pm = t.ones(1, dtype=t.float64, device=dev)
     rs = t.zeros(1, dtype=t.float64, device=dev)
     ur = t.zeros((1, R), dtype=t.float64, device=dev)
-    ops.sts_walk(tree, W, L, 0, Mt, Hh, 1, (0, 0), ov, None, None, 0, X, pm, rs, ur)
+    ops.sts_walk(tree, W, L, 0, Mt, Hh, 1, (0, 0), ov, None, None, 0, X, pm, rs)
     ops.status.check("in local_sts_leaf_search")
     return int(row_offset + int(X.item()))
 
