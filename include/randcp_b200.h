@@ -137,8 +137,9 @@ int rcp_batch_fold(const int64_t *d_perm, const int64_t *d_rows, const double *d
 /* ------------------------------------------------------------------ STS-CP sampler
  * Ref: sts_build samplers.py:224-288, sts_sample samplers.py:379-468.
  * Device layout: complete binary tree over leaf blocks of `leaf` consecutive rows; level
- * l holds 2^l node Grams, each packed upper-triangular (R(R+1)/2 doubles, row-major);
- * node (l, v) lives at offset ((1<<l) - 1 + v) * R(R+1)/2.  depth = ceil(log2(n_leaves)). */
+ * l holds 2^l node Grams, each packed upper-triangular (R(R+1)/2 doubles, row-major),
+ * node stride S = R(R+1)/2 rounded up to even (zero pad, 16-byte aligned nodes); node
+ * (l, v) lives at offset ((1<<l) - 1 + v) * S.  depth = ceil(log2(n_leaves)). */
 int rcp_sts_depth(int64_t n, int leaf);
 size_t rcp_sts_tree_doubles(int64_t n, int leaf, int R);
 /* Conditioning matrix of constant mode i in a mode-k solve:

@@ -90,6 +90,13 @@ __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) {
   return (a + b - 1) / b;
 }
 
+// Node stride of packed R x R Gram blocks: R(R+1)/2 rounded up to even (16-byte aligned
+// nodes for vector loads; the pad element is zero).
+__host__ __device__ __forceinline__ int tri_stride(int R) {
+  const int t = R * (R + 1) / 2;
+  return (t + 1) & ~1;
+}
+
 // Packed upper-triangular index of (a, b), a <= b, row-major.
 __host__ __device__ __forceinline__ int tri_index(int a, int b, int R) {
   return a * R - (a * (a - 1)) / 2 + (b - a);

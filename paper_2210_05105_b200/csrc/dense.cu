@@ -113,9 +113,15 @@ __global__ void sum_partials_kernel(const double *__restrict__ part, int nparts,
                                     double *__restrict__ out) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= len) return;
-  double s = 0.0;
-  for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * len + e];
-  out[e] = s;
+  // eight independent partial sums (memory-level parallelism), combined in a fixed order
+  double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int p = 0;
+  for (; p + 8 <= nparts; p += 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] += part[(int64_t)(p + q) * len + e];
+  }
+  for (; p < nparts; ++p) a[p & 7] += part[(int64_t)p * len + e];
+  out[e] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
 }
 
 // --------------------------------------------------------------------------- pinv

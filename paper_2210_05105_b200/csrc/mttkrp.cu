@@ -34,9 +34,7 @@ int sm_count() {
 }
 
 constexpr int kMaxModes = 8;
-constexpr int kPrivRows = 40960;   // CTA-private row histogram limit (int32 in smem)
-constexpr int kTileE = 2048;       // entries per traversal tile
-constexpr int kMinRange = 8192;    // min entries per CTA in the histogram/scatter passes
+constexpr int kPrivRows = 49152;   // CTA-private row histogram limit (int32 in smem)
 constexpr int kSpmmChunk = 256;    // entries per warp in the segmented reduction
 
 struct Strides {
@@ -211,80 +209,58 @@ __global__ void rows_hit_kernel(const int64_t *__restrict__ rcnt, int64_t n_rows
 }
 
 // ------------------------------------------------------------ entry traversal
-// The gathered entries e in [0, nnz) are the concatenation of the distinct fibers; entry e
-// of fiber d sits at store position lo_d + (e - off_d).  A tile of kTileE consecutive
-// entries stages the needed slice of the fiber offsets in shared memory (or, when empty
-// fibers make the slice longer than the window, searches it in global memory).
-constexpr int kWinCap = 4096;
+// Work items: chunks of at most kItemE consecutive entries of one fiber.  A fiber's entries
+// are contiguous in the store, so a warp reads an item's rows/values fully coalesced.
+constexpr int64_t kItemE = 1024;
+constexpr int kTraverseThreads = 1024;
 
-struct TileFibers {
-  int64_t d0;            // first fiber of the tile
-  int64_t nwin;          // offsets d0 .. d0+nwin-1 cover the tile
-  const int64_t *off;    // -> those offsets (shared window or global)
+__global__ void item_count_kernel(const int64_t *__restrict__ dlen, const int64_t *__restrict__ Sp,
+                                  int64_t *__restrict__ icnt) {
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d < Sp[0]) icnt[d] = ceil_div(dlen[d], kItemE);
+}
+
+struct ItemSpan {
+  int64_t d, a, b;   // fiber, store range [a, b)
 };
 
-__device__ TileFibers stage_tile(const int64_t *__restrict__ doff, int64_t S, int64_t t0,
-                                 int64_t t1, int64_t *win) {
-  __shared__ int64_t sd0, sd1;
-  if (threadIdx.x == 0) {
-    sd0 = floor_index(doff, S + 1, t0);
-    sd1 = floor_index(doff, S + 1, t1 - 1);
-  }
-  __syncthreads();
-  const int64_t d0 = sd0, d1 = sd1;
-  TileFibers tf;
-  tf.d0 = d0;
-  tf.nwin = d1 - d0 + 2;
-  if (tf.nwin <= kWinCap) {
-    for (int64_t i = threadIdx.x; i < tf.nwin; i += blockDim.x) win[i] = doff[d0 + i];
-    tf.off = win;
-  } else {
-    tf.off = doff + d0;
-  }
-  __syncthreads();
-  return tf;
+__device__ __forceinline__ ItemSpan item_span(int64_t it, const int64_t *__restrict__ ioff, int64_t S,
+                                              const int64_t *__restrict__ dlo,
+                                              const int64_t *__restrict__ dlen) {
+  ItemSpan sp;
+  sp.d = floor_index(ioff, S + 1, it);   // last fiber whose first item <= it (skips empties)
+  const int64_t c = it - ioff[sp.d];
+  const int64_t base = dlo[sp.d];
+  sp.a = base + c * kItemE;
+  sp.b = min(base + dlen[sp.d], sp.a + kItemE);
+  return sp;
 }
 
-__device__ __forceinline__ int64_t fiber_of(const int64_t *off, int64_t nwin, int64_t e) {
-  int64_t lo = 0, hi = nwin - 1;  // off[lo] <= e < off[hi]
-  while (hi - lo > 1) {
-    int64_t mid = (lo + hi) >> 1;
-    if (off[mid] <= e) lo = mid; else hi = mid;
-  }
-  return lo;
+__device__ __forceinline__ void cta_items(int64_t n_items, int64_t &i0, int64_t &i1) {
+  const int64_t per = ceil_div(n_items, (int64_t)gridDim.x);
+  i0 = (int64_t)blockIdx.x * per;
+  i1 = min(i0 + per, n_items);
 }
 
-__device__ __forceinline__ void cta_range(int64_t nnz, int64_t &r0, int64_t &r1) {
-  int64_t per = ceil_div(nnz, (int64_t)gridDim.x);
-  if (per < kMinRange) per = kMinRange;
-  per = ceil_div(per, kTileE) * kTileE;
-  r0 = (int64_t)blockIdx.x * per;
-  r1 = r0 + per;
-  if (r1 > nnz) r1 = nnz;
-}
-
-__global__ void __launch_bounds__(256)
-row_count_kernel(const int64_t *__restrict__ doff, const int64_t *__restrict__ Sp,
-                 const int64_t *__restrict__ nnzp, const int64_t *__restrict__ dlo,
+__global__ void __launch_bounds__(kTraverseThreads)
+row_count_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                 const int64_t *__restrict__ dlo, const int64_t *__restrict__ dlen,
                  const int32_t *__restrict__ rows, int64_t n_rows, int priv,
                  int64_t *__restrict__ rcnt) {
-  extern __shared__ int64_t sm[];
-  int64_t *win = sm;                                      // kWinCap + 2
-  int32_t *hist = reinterpret_cast<int32_t *>(sm + kWinCap + 2);
-  const int64_t nnz = nnzp[0], S = Sp[0];
-  int64_t r0, r1;
-  cta_range(nnz, r0, r1);
-  if (r0 >= r1) return;
+  extern __shared__ int32_t hist[];
+  const int64_t S = Sp[0];
+  int64_t i0, i1;
+  cta_items(ioff[S], i0, i1);
+  if (i0 >= i1) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (priv) {
     for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) hist[i] = 0;
-  }
-  for (int64_t t0 = r0; t0 < r1; t0 += kTileE) {
-    const int64_t t1 = min(t0 + kTileE, r1);
     __syncthreads();
-    TileFibers tf = stage_tile(doff, S, t0, t1, win);
-    for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
-      const int64_t j = fiber_of(tf.off, tf.nwin, e);
-      const int32_t row = rows[dlo[tf.d0 + j] + (e - tf.off[j])];
+  }
+  for (int64_t it = i0 + wid; it < i1; it += nw) {
+    const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
+    for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32) {
+      const int32_t row = rows[pos];
       if (priv) atomicAdd(&hist[row], 1);
       else atomicAdd((unsigned long long *)&rcnt[row], 1ull);
     }
@@ -296,45 +272,38 @@ row_count_kernel(const int64_t *__restrict__ doff, const int64_t *__restrict__ S
   }
 }
 
-__global__ void __launch_bounds__(256)
-scatter_kernel(const int64_t *__restrict__ doff, const int64_t *__restrict__ Sp,
-               const int64_t *__restrict__ nnzp, const int64_t *__restrict__ dlo,
+__global__ void __launch_bounds__(kTraverseThreads)
+scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+               const int64_t *__restrict__ dlo, const int64_t *__restrict__ dlen,
                const int32_t *__restrict__ rows, const double *__restrict__ vals, int64_t n_rows,
                int priv, const int64_t *__restrict__ rptr, int64_t *__restrict__ rcur,
                int32_t *__restrict__ ed, double *__restrict__ ev, int64_t cap, int *status) {
-  extern __shared__ int64_t sm[];
-  int64_t *win = sm;
-  int32_t *hist = reinterpret_cast<int32_t *>(sm + kWinCap + 2);
-  const int64_t nnz = nnzp[0], S = Sp[0];
-  int64_t r0, r1;
-  cta_range(nnz, r0, r1);
-  if (r0 >= r1) return;
+  extern __shared__ int32_t hist[];
+  const int64_t S = Sp[0];
+  int64_t i0, i1;
+  cta_items(ioff[S], i0, i1);
+  if (i0 >= i1) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (priv) {
     // pass A: CTA-local counts; reserve one contiguous run per (CTA, row)
     for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) hist[i] = 0;
-    for (int64_t t0 = r0; t0 < r1; t0 += kTileE) {
-      const int64_t t1 = min(t0 + kTileE, r1);
-      __syncthreads();
-      TileFibers tf = stage_tile(doff, S, t0, t1, win);
-      for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
-        const int64_t j = fiber_of(tf.off, tf.nwin, e);
-        atomicAdd(&hist[rows[dlo[tf.d0 + j] + (e - tf.off[j])]], 1);
-      }
+    __syncthreads();
+    for (int64_t it = i0 + wid; it < i1; it += nw) {
+      const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
+      for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32) atomicAdd(&hist[rows[pos]], 1);
     }
     __syncthreads();
     for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) {
       const int32_t c = hist[i];
       if (c) hist[i] = (int32_t)atomicAdd((unsigned long long *)&rcur[i], (unsigned long long)c);
     }
-  }
-  for (int64_t t0 = r0; t0 < r1; t0 += kTileE) {
-    const int64_t t1 = min(t0 + kTileE, r1);
     __syncthreads();
-    TileFibers tf = stage_tile(doff, S, t0, t1, win);
-    for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
-      const int64_t j = fiber_of(tf.off, tf.nwin, e);
-      const int64_t pos = dlo[tf.d0 + j] + (e - tf.off[j]);
+  }
+  for (int64_t it = i0 + wid; it < i1; it += nw) {
+    const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
+    for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32) {
       const int32_t row = rows[pos];
+      const double v = vals[pos];
       int64_t slot;
       if (priv) slot = atomicAdd(&hist[row], 1);
       else slot = (int64_t)atomicAdd((unsigned long long *)&rcur[row], 1ull);
@@ -343,8 +312,8 @@ scatter_kernel(const int64_t *__restrict__ doff, const int64_t *__restrict__ Sp,
         raise_status(status, RCP_ST_CAPACITY);
         continue;
       }
-      ed[o] = (int32_t)(tf.d0 + j);
-      ev[o] = vals[pos];
+      ed[o] = (int32_t)sp.d;
+      ev[o] = v;
     }
   }
 }
@@ -488,7 +457,8 @@ struct Ws {
 struct MttkrpLayout {
   int64_t T;
   size_t o_tkey, o_tcnt, o_trep, o_twmin, o_twmax, o_twsum, o_dsc, o_bcnt, o_dkey, o_dcnt,
-      o_drep, o_dlo, o_dlen, o_doff, o_Hs, o_scan, o_rcnt, o_rptr, o_ed, o_ev, o_S, o_nnz;
+      o_drep, o_dlo, o_dlen, o_doff, o_ioff, o_Hs, o_scan, o_rcnt, o_rptr, o_ed, o_ev, o_S,
+      o_nnz;
   size_t total;
   MttkrpLayout(int64_t J, int64_t cap, int64_t n_rows, int R) {
     T = 1024;
@@ -508,6 +478,7 @@ struct MttkrpLayout {
     o_dlo = w.add(sizeof(int64_t) * (J + 1));
     o_dlen = w.add(sizeof(int64_t) * (J + 1));
     o_doff = w.add(sizeof(int64_t) * (J + 2));
+    o_ioff = w.add(sizeof(int64_t) * (J + 2));
     o_Hs = w.add(sizeof(double) * (size_t)(J + 1) * R);
     int64_t sc = J + 1 > n_rows + 1 ? J + 1 : n_rows + 1;
     o_scan = w.add(scan_ws_bytes(sc));
@@ -619,18 +590,26 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   if (rc) return rc;
   finalize_counts_kernel<<<1, 32, 0, st>>>(S, doff, nnz, d_stats);
   RCP_LAUNCH_CHECK("finalize_counts");
+  // 3b. work items: fiber chunks of <= kItemE entries (dkey reused for the counts)
+  int64_t *icnt = dkey;
+  int64_t *ioff = (int64_t *)P(L.o_ioff);
+  item_count_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(dlen, S, icnt);
+  RCP_LAUNCH_CHECK("item_count");
+  rc = scan_i64_exclusive(icnt, ioff, J, S, scan_ws, st);
+  if (rc) return rc;
   // 4. row histogram -> row pointers
   const int priv = n_rows <= kPrivRows ? 1 : 0;
-  size_t smem = sizeof(int64_t) * (kWinCap + 2) + (priv ? sizeof(int32_t) * n_rows : 0);
+  size_t smem = priv ? sizeof(int32_t) * n_rows : 0;
   static bool attr = false;
   if (!attr) {
     RCP_CUDA_TRY(cudaFuncSetAttribute(row_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     RCP_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  const int grid = 2 * sm_count();
+  const int grid = sm_count();
   RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
-  row_count_kernel<<<grid, 256, smem, st>>>(doff, S, nnz, dlo, d_rows, n_rows, priv, rcnt);
+  row_count_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, dlo, dlen, d_rows, n_rows, priv,
+                                                         rcnt);
   RCP_LAUNCH_CHECK("row_count");
   rc = scan_i64_exclusive(rcnt, rptr, n_rows, nullptr, scan_ws, st);
   if (rc) return rc;
@@ -642,8 +621,8 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   }
   // 5. scatter into row order (rcnt reused as per-row cursor)
   RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
-  scatter_kernel<<<grid, 256, smem, st>>>(doff, S, nnz, dlo, d_rows, d_vals, n_rows, priv, rptr,
-                                          rcnt, ed, ev, cap, d_status);
+  scatter_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, dlo, dlen, d_rows, d_vals, n_rows,
+                                                       priv, rptr, rcnt, ed, ev, cap, d_status);
   RCP_LAUNCH_CHECK("scatter");
   // 6. segmented reduction
   return launch_spmm<int32_t>(rptr, n_rows, nnz, 0, ed, ev, Hs, nullptr, R, d_out, st);

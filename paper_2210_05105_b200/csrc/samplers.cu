@@ -152,13 +152,15 @@ __global__ void sts_leaf_kernel(const double *__restrict__ U, int64_t n, int R, 
                                 int64_t nleaves, double *__restrict__ level) {
   extern __shared__ double rows[];  // leaf x R
   const int Rt = R * (R + 1) / 2;
+  const int Rs = tri_stride(R);
   for (int64_t v = blockIdx.x; v < nleaves; v += gridDim.x) {
     const int64_t r0 = v * leaf;
     const int nr = (int)min((int64_t)leaf, n - r0);
     __syncthreads();
     for (int e = threadIdx.x; e < nr * R; e += blockDim.x) rows[e] = U[r0 * R + e];
     __syncthreads();
-    double *out = level + v * Rt;
+    double *out = level + v * Rs;
+    if (Rs > Rt && threadIdx.x == 0) out[Rt] = 0.0;
     for (int e = threadIdx.x; e < Rt; e += blockDim.x) {
       // decode packed (a, b)
       int a = 0, rem = e;
@@ -344,7 +346,7 @@ int rcp_sts_depth(int64_t n, int leaf) {
 size_t rcp_sts_tree_doubles(int64_t n, int leaf, int R) {
   if (n <= 0) return 0;
   int d = rcp_sts_depth(n, leaf);
-  return (size_t)((2LL << d) - 1) * (size_t)(R * (R + 1) / 2);
+  return (size_t)((2LL << d) - 1) * (size_t)tri_stride(R);
 }
 
 int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree, void *stream) {
@@ -352,7 +354,7 @@ int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
   if (n == 0) return RCP_OK;
   if (!d_U || !d_tree) return RCP_ERR_ARG;
   cudaStream_t st = RCP_STREAM(stream);
-  const int Rt = R * (R + 1) / 2;
+  const int Rt = tri_stride(R);   // node stride (even; pad entry zero)
   const int depth = rcp_sts_depth(n, leaf);
   const int64_t nleaves = ceil_div(n, leaf);
   const int64_t width = 1LL << depth;

@@ -82,6 +82,13 @@ struct WalkWs {
   }
 };
 
+// Shared doubles per walker warp: P (node stride), h/u row, leaf masses, path; kept even
+// so every warp's P is 16-byte aligned.
+__host__ __device__ __forceinline__ size_t walk_per_warp(int R) {
+  const size_t w = (size_t)tri_stride(R) + R + kMaxLeaf + kMaxDepth + 2;
+  return (w + 1) & ~(size_t)1;
+}
+
 // control words: [0] queue tail, [1] queue head, [2] samples finished, [3] participants
 __device__ __forceinline__ int ld_volatile(const int *p) { return *(volatile const int *)p; }
 
@@ -197,14 +204,16 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
                  int *status) {
   extern __shared__ double sh[];
   const int Rt = R * (R + 1) / 2;
+  const int Rs = tri_stride(R);                    // even node stride (zero pad)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const size_t per_warp = (size_t)Rt + R + kMaxLeaf + kMaxDepth + 2;
-  double *Mp = sh;                                 // Rt: packed M, off-diagonals x2
-  double *P = Mp + Rt + (size_t)wid * per_warp;    // per warp: Rt
-  double *uv = P + Rt;                             // R
+  const size_t per_warp = walk_per_warp(R);
+  double *Mp = sh;                                 // Rs: packed M, off-diagonals x2
+  double *P = Mp + Rs + (size_t)wid * per_warp;    // per warp: Rs (16-byte aligned)
+  double *uv = P + Rs;                             // R
   double *mass = uv + R;                           // leaf
   double *Tp = mass + kMaxLeaf;                    // path thresholds of the current run
-  uint16_t *pairs = reinterpret_cast<uint16_t *>(Mp + Rt + (size_t)nw * per_warp);
+  uint16_t *pairs = reinterpret_cast<uint16_t *>(Mp + Rs + (size_t)nw * per_warp);
+  if (Rs > Rt && threadIdx.x == 0) Mp[Rt] = 0.0;
   for (int e = threadIdx.x; e < Rt; e += blockDim.x) {
     int a = 0, rem = e;
     while (rem >= R - a) {
@@ -262,23 +271,33 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
     if (lane < level) Tp[lane] = run.T[lane];
     // P = (h h^T) (.) M' of the run's common Hadamard row
     const int32_t s0 = idx[lo];
-    for (int e = lane; e < Rt; e += 32) {
-      const uint16_t ab = pairs[e];
-      const double ha = H ? H[(int64_t)s0 * R + (ab & 0xff)] : 1.0;
-      const double hb = H ? H[(int64_t)s0 * R + (ab >> 8)] : 1.0;
-      P[e] = ha * hb * Mp[e];
+    for (int c = lane; c < R; c += 32) uv[c] = H ? H[(int64_t)s0 * R + c] : 1.0;
+    __syncwarp();
+    for (int e = lane; e < Rs; e += 32) {
+      const uint16_t ab = e < Rt ? pairs[e] : 0;
+      P[e] = e < Rt ? uv[ab & 0xff] * uv[ab >> 8] * Mp[e] : 0.0;
     }
     __syncwarp();
     if (level < depth) {
       const int64_t v = run.node;
-      const double *GL = tree + ((1LL << (level + 1)) - 1 + 2 * v) * (int64_t)Rt;
-      const double *GR = GL + Rt;
-      double qL = 0.0, qR = 0.0;
-      for (int e = lane; e < Rt; e += 32) {
-        const double p = P[e];
-        qL = fma(__ldg(GL + e), p, qL);
-        qR = fma(__ldg(GR + e), p, qR);
+      const double2 *GL = reinterpret_cast<const double2 *>(
+          tree + ((1LL << (level + 1)) - 1 + 2 * v) * (int64_t)Rs);
+      const double2 *GR = GL + Rs / 2;
+      const double2 *P2 = reinterpret_cast<const double2 *>(P);
+      double qL = 0.0, qR = 0.0, qL2 = 0.0, qR2 = 0.0;
+      const int n2 = Rs / 2;
+#pragma unroll 4
+      for (int e = lane; e < n2; e += 32) {
+        const double2 gl = __ldg(GL + e);
+        const double2 gr = __ldg(GR + e);
+        const double2 p = P2[e];
+        qL = fma(gl.x, p.x, qL);
+        qL2 = fma(gl.y, p.y, qL2);
+        qR = fma(gr.x, p.x, qR);
+        qR2 = fma(gr.y, p.y, qR2);
       }
+      qL += qL2;
+      qR += qR2;
       qL = warp_sum(qL);
       qR = warp_sum(qR);
       qL = qL > 0.0 ? qL : 0.0;
@@ -401,9 +420,8 @@ __global__ void fold_rows_kernel(double *__restrict__ out, const double *__restr
 }
 
 size_t walk_smem(int R, int warps) {
-  const int Rt = R * (R + 1) / 2;
-  return sizeof(double) * ((size_t)Rt + (size_t)warps * (Rt + R + kMaxLeaf + kMaxDepth + 2)) +
-         sizeof(uint16_t) * (size_t)Rt + 64;
+  return sizeof(double) * ((size_t)tri_stride(R) + (size_t)warps * walk_per_warp(R)) +
+         sizeof(uint16_t) * (size_t)tri_stride(R) + 64;
 }
 
 }  // namespace
