@@ -17,8 +17,11 @@
 // is recomputed from its uniform by replaying the path's rescalings in the reference's
 // order.  Runs flow through a device work queue served by persistent warps.  Work is
 // proportional to the number of distinct (h, node) pairs, not samples x levels.
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <float.h>
+
+namespace cg = cooperative_groups;
 
 #include "common.cuh"
 
@@ -151,8 +154,7 @@ __global__ void walk_seed_kernel(const int64_t *__restrict__ key, const int32_t 
   rr.dirs = 0u;
   // samples of one group share their rank-level path, hence this probability
   rr.prob = pmp_in ? pmp_in[idx[s]] : 1.0;
-  __threadfence();
-  atomicExch(&ready[t], 1);
+  (void)ready;
 }
 
 __global__ void row_keys_kernel(const int64_t *__restrict__ X, int N, int64_t J, Strides8 st,
@@ -190,9 +192,8 @@ __device__ __forceinline__ void push_child(Run *runs, int *ready, int *ctl, cons
       c.T[lev] = T;
     }
     __syncwarp();
-    __threadfence();
-    if (lane == 0) atomicExch(&ready[t], 1);
   }
+  (void)ready;
 }
 
 __global__ void __launch_bounds__(kWalkWarps * 32)
@@ -226,45 +227,15 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
     Mp[e] = (a == b) ? m : 2.0 * m;
   }
   __syncthreads();
-  const int total = ld_volatile(&ctl[3]);
-
-  while (true) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(&ctl[1], 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    // wait for run t to be published, or for every participant to finish
-    bool quit = false;
-    uint64_t t_start = 0;
-    if (lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    while (true) {
-      int rd = 0, dn = 0;
-      if (lane == 0) {
-        rd = t < cap_runs ? ld_volatile(&ready[t]) : 0;
-        dn = ld_volatile(&ctl[2]);
-      }
-      rd = __shfl_sync(0xffffffffu, rd, 0);
-      dn = __shfl_sync(0xffffffffu, dn, 0);
-      if (rd) break;
-      if (dn >= total) {
-        quit = true;
-        break;
-      }
-      // watchdog: a queue that never drains is a bug -- fail loudly instead of hanging
-      int expired = 0;
-      if (lane == 0) {
-        uint64_t now;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-        expired = (now - t_start) > 4000000000ull;
-      }
-      if (__shfl_sync(0xffffffffu, expired, 0)) {
-        if (lane == 0) raise_status(status, RCP_ST_TIMEOUT);
-        quit = true;
-        break;
-      }
-      __nanosleep(128);
-    }
-    if (quit) break;
-    __threadfence();
+  cg::grid_group grid = cg::this_grid();
+  const int64_t gwarp = (int64_t)blockIdx.x * nw + wid;
+  const int64_t nwarps = (int64_t)gridDim.x * nw;
+  int64_t begin = 0;
+  // Level-synchronous breadth: the runs of one tree level are [begin, end); their children
+  // are appended behind `end` and become the next level after a grid-wide barrier.
+  for (int lvl = 0; lvl <= depth; ++lvl) {
+  const int64_t end = min((int64_t)ld_volatile(&ctl[0]), cap_runs);
+  for (int64_t t = begin + gwarp; t < end; t += nwarps) {
     const Run &run = runs[t];
     const int32_t lo = run.lo, hi = run.hi, level = run.level;
     const uint32_t dirs = run.dirs;
@@ -396,10 +367,10 @@ walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, 
       if (resid) resid[o] = ro;
     }
     __syncwarp();
-    if (lane == 0) {
-      __threadfence();
-      atomicAdd(&ctl[2], hi - lo);
-    }
+    if (lane == 0) atomicAdd(&ctl[2], hi - lo);
+  }
+  begin = end;
+  grid.sync();
   }
 }
 
@@ -476,7 +447,6 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   RCP_LAUNCH_CHECK("walk_sort_key");
   walk_gather_kernel<<<gb, 256, 0, st>>>((const int64_t *)r, idx, J, (int64_t *)r2);
   RCP_LAUNCH_CHECK("walk_gather_r");
-  RCP_CUDA_TRY(cudaMemsetAsync(ready, 0, sizeof(int) * L.nruns, st));
   RCP_CUDA_TRY(cudaMemsetAsync(ctl, 0, 64, st));
   walk_seed_kernel<<<gb, 256, 0, st>>>(key, idx, J, d_sel ? d_pmp_i : nullptr, runs, ready, ctl);
   RCP_LAUNCH_CHECK("walk_seed");
@@ -492,9 +462,18 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   if (per_sm < 1) return RCP_ERR_ARG;
   // persistent: every CTA resident at once (workers wait on the shared queue)
   const int grid = per_sm * sm_count();
-  walk_runs_kernel<<<grid, warps * 32, smem, st>>>(d_tree, d_U, n, R, leaf, depth, row_lo, d_M,
-                                                  d_H_in, idx, r2, runs, ready, ctl, L.nruns,
-                                                  d_Xi, d_pmp_i, d_resid, d_status);
+  // cooperative launch: every CTA co-resident, grid-wide barrier between tree levels
+  const double *a_tree = d_tree, *a_U = d_U, *a_M = d_M, *a_H = d_H_in;
+  const int32_t *a_idx = idx;
+  const double *a_r = r2;
+  int64_t a_n = n, a_row_lo = row_lo, a_cap = L.nruns;
+  int a_R = R, a_leaf = leaf, a_depth = depth;
+  void *args[] = {(void *)&a_tree, (void *)&a_U, (void *)&a_n, (void *)&a_R, (void *)&a_leaf,
+                  (void *)&a_depth, (void *)&a_row_lo, (void *)&a_M, (void *)&a_H, (void *)&a_idx,
+                  (void *)&a_r, (void *)&runs, (void *)&ready, (void *)&ctl, (void *)&a_cap,
+                  (void *)&d_Xi, (void *)&d_pmp_i, (void *)&d_resid, (void *)&d_status};
+  RCP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)walk_runs_kernel, dim3(grid),
+                                           dim3(warps * 32), args, smem, st));
   RCP_LAUNCH_CHECK("walk_runs");
   return RCP_OK;
 }
