@@ -183,6 +183,15 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
 int rcp_fold_rows(double *d_out, const double *d_U, int64_t n, int R, int64_t row_lo,
                   const int64_t *d_Xi, int64_t J, int init, const int32_t *d_sel,
                   int32_t sel_value, void *stream);
+/* First constant mode of a single-rank walk (all samples share H = ones): the leaf-by-leaf
+ * inverse CDF collapses to one inverse CDF over every row.  With row masses, normalised
+ * masses and CDF from rcp_arls_build(U, M) (mass = u M u^T, clipped at 0), draw sample s
+ * from WALK_UNIFORM draw s: X_i[s] = row_lo + searchsorted(cdf, u, 'right'),
+ * pmp_i[s] = mass/total.  Same distribution and inverse-CDF map as the tree walk (ref
+ * samplers.py:291-310, 379-468); RCP_ST_DEGENERATE when the total mass is zero. */
+int rcp_sts_flat_draw(const double *d_cdf, const double *d_dist, int64_t n, int64_t row_lo,
+                      const double *d_total_mass, uint64_t key0, uint64_t key1, int64_t J,
+                      int64_t *d_Xi, double *d_pmp_i, int *d_status, void *stream);
 /* d_out[s] = sum_m X[m*J + s] * strides[m] over modes with nonzero stride (mixed-radix
  * key of a subset of a sample's indices; ref matricization.py:41-54 for the MTTKRP
  * column key, and the STS walk's grouping key). */

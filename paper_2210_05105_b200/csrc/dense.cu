@@ -111,17 +111,30 @@ gram_partial_kernel(const double *__restrict__ U, const double *__restrict__ sca
 
 __global__ void sum_partials_kernel(const double *__restrict__ part, int nparts, int64_t len,
                                     double *__restrict__ out) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= len) return;
-  // eight independent partial sums (memory-level parallelism), combined in a fixed order
-  double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int p = 0;
-  for (; p + 8 <= nparts; p += 8) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] += part[(int64_t)(p + q) * len + e];
+  // block = 32 elements x 8 slices; slice s sums partials p = s, s+8, ... (x4 unrolled),
+  // then the 8 slice sums are combined in a fixed order: deterministic.
+  __shared__ double red[8][33];
+  const int el = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int64_t e = blockIdx.x * 32LL + el;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (e < len) {
+    const double *p0 = part + e;
+    int p = sl;
+    for (; p + 24 < nparts; p += 32) {
+      a0 += p0[(int64_t)p * len];
+      a1 += p0[(int64_t)(p + 8) * len];
+      a2 += p0[(int64_t)(p + 16) * len];
+      a3 += p0[(int64_t)(p + 24) * len];
+    }
+    for (; p < nparts; p += 8) a0 += p0[(int64_t)p * len];
   }
-  for (; p < nparts; ++p) a[p & 7] += part[(int64_t)p * len + e];
-  out[e] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  red[sl][el] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (sl == 0 && e < len) {
+    double s = 0.0;
+    for (int q = 0; q < 8; ++q) s += red[q][el];
+    out[e] = s;
+  }
 }
 
 // --------------------------------------------------------------------------- pinv
@@ -482,7 +495,7 @@ int rcp_gram(const double *d_U, const double *d_scale, int64_t n, int R, double 
   gram_partial_kernel<<<grid, kGramThreads, smem, st>>>(d_U, d_scale, n, R, (double *)d_ws);
   RCP_LAUNCH_CHECK("gram_partial");
   int64_t len = (int64_t)R * R;
-  sum_partials_kernel<<<(unsigned)ceil_div(len, 256), 256, 0, st>>>((double *)d_ws, grid, len,
+  sum_partials_kernel<<<(unsigned)ceil_div(len, 32), 256, 0, st>>>((double *)d_ws, grid, len,
                                                                      d_G);
   RCP_LAUNCH_CHECK("gram_reduce");
   return RCP_OK;
@@ -543,7 +556,7 @@ int rcp_update(const double *d_M, int64_t n, int R, const double *d_B, double *d
     default: update_kernel<4><<<grid, kUpdThreads, smem, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
   }
   RCP_LAUNCH_CHECK("update");
-  sum_partials_kernel<<<(unsigned)ceil_div(R, 128), 128, 0, st>>>(part, grid, R, d_colsq);
+  sum_partials_kernel<<<(unsigned)ceil_div(R, 32), 256, 0, st>>>(part, grid, R, d_colsq);
   RCP_LAUNCH_CHECK("update_colsq");
   return RCP_OK;
 }

@@ -112,6 +112,7 @@ class RankState:
         self.urow_tmp = t.zeros((J, R), **f64) if self.P > 1 else None
         self.perm = t.zeros(J, dtype=t.int64, device=dev)
         self.hkey = t.zeros(J, dtype=t.int64, device=dev)
+        self.flat_dist = self.flat_cdf = self.flat_mass = None
         self.chain_pinv = t.zeros((R, R), **f64)
         self.M = t.zeros((R, R), **f64)
         self.Gs = t.zeros((R, R), **f64)
@@ -223,6 +224,19 @@ class RankState:
         else:
             self.pmp[i].fill_(1.0)
             sel, rin = None, None
+        if self.P == 1 and first and override is None and self.n[i] > 0:
+            # every sample shares H = ones: one inverse CDF over all rows' masses u M u^T
+            t = self.t
+            n = self.n[i]
+            if self.flat_dist is None or self.flat_dist.shape[0] < n:
+                self.flat_dist = t.zeros(max(self.n), dtype=t.float64, device=self.dev)
+                self.flat_cdf = t.zeros(max(self.n), dtype=t.float64, device=self.dev)
+                self.flat_mass = t.zeros(1, dtype=t.float64, device=self.dev)
+            ops.arls_build(self.U[i], self.M, self.flat_dist[:n], self.flat_cdf[:n], self.flat_mass)
+            ops.sts_flat_draw(self.flat_cdf[:n], self.flat_dist[:n], self.lo[i], self.flat_mass,
+                              key, self.J, self.X[i], self.pmp[i])
+            ops.fold_rows(self.H, self.U[i], self.lo[i], self.X[i], init=True)
+            return
         if self.n[i] > 0:
             hk = ops.walk_key(self.X, self.dims, k, i, self.hkey)
             ops.sts_walk(self.trees[i], self.U[i], self.leaf_of(i), self.lo[i], self.M, H_in,

@@ -118,6 +118,11 @@ class Ops:
                 int(sel_value), ptr(Xi), ptr(pmp_i), ptr(resid), ptr(w), w.numel(),
                 self.status.ptr, stream_handle())
 
+    def sts_flat_draw(self, cdf, dist, row_lo, mass, key, J, Xi, pmp_i):
+        n = cdf.shape[0]
+        self._c("rcp_sts_flat_draw", ptr(cdf), ptr(dist), n, int(row_lo), ptr(mass), key[0],
+                key[1], int(J), ptr(Xi), ptr(pmp_i), self.status.ptr, stream_handle())
+
     def fold_rows(self, out, U, row_lo, Xi, init, sel=None, sel_value=0):
         n, R = U.shape
         J = Xi.shape[0]
