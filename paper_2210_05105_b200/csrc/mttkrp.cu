@@ -277,7 +277,7 @@ scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
                const int64_t *__restrict__ dlo, const int64_t *__restrict__ dlen,
                const int32_t *__restrict__ rows, const double *__restrict__ vals, int64_t n_rows,
                int priv, const int64_t *__restrict__ rptr, int64_t *__restrict__ rcur,
-               int32_t *__restrict__ ed, double *__restrict__ ev, int64_t cap, int *status) {
+               double2 *__restrict__ ent, int64_t cap, int *status) {
   extern __shared__ int32_t hist[];
   const int64_t S = Sp[0];
   int64_t i0, i1;
@@ -312,19 +312,110 @@ scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
         raise_status(status, RCP_ST_CAPACITY);
         continue;
       }
-      ed[o] = (int32_t)sp.d;
-      ev[o] = v;
+      ent[o] = make_double2(__longlong_as_double((long long)sp.d), v);
+    }
+  }
+}
+
+// Blocks with CTA-private histograms (rows fit in shared memory): no global atomics.
+//  1. every CTA histograms the rows of its items into cmat[cta][row];
+//  2. per row, an exclusive prefix over CTAs (in place) and the row totals;
+//  3. after the row scan, CTA c writes its entries of row r at rptr[r] + cmat[c][r] + k.
+__global__ void __launch_bounds__(kTraverseThreads)
+cta_hist_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                const int64_t *__restrict__ dlo, const int64_t *__restrict__ dlen,
+                const int32_t *__restrict__ rows, int64_t n_rows, int32_t *__restrict__ cmat) {
+  extern __shared__ int32_t hist[];
+  const int64_t S = Sp[0];
+  int64_t i0, i1;
+  cta_items(ioff[S], i0, i1);
+  for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t it = i0 + wid; it < i1; it += nw) {
+    const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
+    for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32) atomicAdd(&hist[rows[pos]], 1);
+  }
+  __syncthreads();
+  int32_t *mine = cmat + (int64_t)blockIdx.x * n_rows;
+  for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) mine[i] = hist[i];
+}
+
+__global__ void cta_prefix_kernel(int32_t *__restrict__ cmat, int G, int64_t n_rows,
+                                  int64_t *__restrict__ rcnt) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  int32_t run = 0;
+  for (int c = 0; c < G; ++c) {
+    const int32_t v = cmat[(int64_t)c * n_rows + r];
+    cmat[(int64_t)c * n_rows + r] = run;
+    run += v;
+  }
+  rcnt[r] = run;
+}
+
+__device__ __forceinline__ void put_entry(double2 *__restrict__ ent, int64_t o, int64_t d, double v) {
+  ent[o] = make_double2(__longlong_as_double((long long)d), v);
+}
+
+__global__ void __launch_bounds__(kTraverseThreads)
+cta_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                   const int64_t *__restrict__ dlo, const int64_t *__restrict__ dlen,
+                   const int32_t *__restrict__ rows, const double *__restrict__ vals,
+                   int64_t n_rows, const int64_t *__restrict__ rptr,
+                   const int32_t *__restrict__ cmat, double2 *__restrict__ ent, int64_t cap,
+                   int *status) {
+  extern __shared__ int32_t cur[];   // absolute next slot per row (< 2^31)
+  const int64_t S = Sp[0];
+  int64_t i0, i1;
+  cta_items(ioff[S], i0, i1);
+  const int32_t *mine = cmat + (int64_t)blockIdx.x * n_rows;
+  for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) cur[i] = (int32_t)(rptr[i] + mine[i]);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t it = i0 + wid; it < i1; it += nw) {
+    const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
+    for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32) {
+      const int32_t row = rows[pos];
+      const double v = vals[pos];
+      const int64_t o = atomicAdd(&cur[row], 1);
+      if (o >= cap) {
+        raise_status(status, RCP_ST_CAPACITY);
+        continue;
+      }
+      put_entry(ent, o, sp.d, v);
     }
   }
 }
 
 // ------------------------------------------------------------ segmented SpMM
 // One warp per chunk of kSpmmChunk row-sorted entries; lanes own output columns.
-template <int RPL, typename ColT>
+// Entries come either packed ({fiber id, value} in one 16-byte word, fused path) or as
+// separate column/value arrays (reference-shaped CSR, drop-in path).
+struct PackedEntries {
+  const double2 *ent;
+  __device__ __forceinline__ void get(int64_t x, int64_t &d, double &v) const {
+    const double2 e = ent[x];
+    d = (int64_t)(int32_t)__double_as_longlong(e.x);
+    v = e.y;
+  }
+};
+
+struct CsrEntries {
+  const int64_t *col;
+  const double *val;
+  const double *scale;
+  __device__ __forceinline__ void get(int64_t x, int64_t &d, double &v) const {
+    d = col[x];
+    v = val[x];
+    if (scale) v *= scale[d];
+  }
+};
+
+template <int RPL, typename Acc>
 __global__ void __launch_bounds__(256)
 spmm_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__restrict__ nnzp,
-            int64_t nnz_host, const ColT *__restrict__ col, const double *__restrict__ val,
-            const double *__restrict__ Hs, const double *__restrict__ scale, int R,
+            int64_t nnz_host, Acc acc_in, const double *__restrict__ Hs, int R,
             double *__restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -344,26 +435,30 @@ spmm_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__r
 #pragma unroll
         for (int j = 0; j < RPL; ++j) acc[j] = 0.0;
         int64_t x = e;
-        for (; x + 2 <= stop; x += 2) {
-          const int64_t d0 = (int64_t)col[x], d1 = (int64_t)col[x + 1];
-          double v0 = val[x], v1 = val[x + 1];
-          if (scale) {
-            v0 *= scale[d0];
-            v1 *= scale[d1];
-          }
+        for (; x + 4 <= stop; x += 4) {
+          int64_t d0, d1, d2, d3;
+          double v0, v1, v2, v3;
+          acc_in.get(x, d0, v0);
+          acc_in.get(x + 1, d1, v1);
+          acc_in.get(x + 2, d2, v2);
+          acc_in.get(x + 3, d3, v3);
 #pragma unroll
           for (int j = 0; j < RPL; ++j) {
             const int c = lane + 32 * j;
             if (c < R) {
-              acc[j] = fma(v0, Hs[d0 * R + c], acc[j]);
-              acc[j] = fma(v1, Hs[d1 * R + c], acc[j]);
+              const double h0 = Hs[d0 * R + c], h1 = Hs[d1 * R + c];
+              const double h2 = Hs[d2 * R + c], h3 = Hs[d3 * R + c];
+              acc[j] = fma(v0, h0, acc[j]);
+              acc[j] = fma(v1, h1, acc[j]);
+              acc[j] = fma(v2, h2, acc[j]);
+              acc[j] = fma(v3, h3, acc[j]);
             }
           }
         }
         for (; x < stop; ++x) {
-          const int64_t d0 = (int64_t)col[x];
-          double v0 = val[x];
-          if (scale) v0 *= scale[d0];
+          int64_t d0;
+          double v0;
+          acc_in.get(x, d0, v0);
 #pragma unroll
           for (int j = 0; j < RPL; ++j) {
             const int c = lane + 32 * j;
@@ -386,10 +481,9 @@ spmm_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__r
   }
 }
 
-template <typename ColT>
+template <typename Acc>
 int launch_spmm(const int64_t *rptr, int64_t n_rows, const int64_t *nnzp, int64_t nnz_host,
-                const ColT *col, const double *val, const double *Hs, const double *scale, int R,
-                double *out, cudaStream_t st) {
+                Acc acc, const double *Hs, int R, double *out, cudaStream_t st) {
   int64_t chunks_host = nnzp ? -1 : ceil_div(nnz_host, kSpmmChunk);
   int64_t blocks = 8LL * sm_count();
   if (chunks_host >= 0) {
@@ -398,10 +492,10 @@ int launch_spmm(const int64_t *rptr, int64_t n_rows, const int64_t *nnzp, int64_
     if (blocks < 1) return RCP_OK;
   }
   switch ((R + 31) / 32) {
-    case 1: spmm_kernel<1, ColT><<<(unsigned)blocks, 256, 0, st>>>(rptr, n_rows, nnzp, nnz_host, col, val, Hs, scale, R, out); break;
-    case 2: spmm_kernel<2, ColT><<<(unsigned)blocks, 256, 0, st>>>(rptr, n_rows, nnzp, nnz_host, col, val, Hs, scale, R, out); break;
-    case 3: spmm_kernel<3, ColT><<<(unsigned)blocks, 256, 0, st>>>(rptr, n_rows, nnzp, nnz_host, col, val, Hs, scale, R, out); break;
-    default: spmm_kernel<4, ColT><<<(unsigned)blocks, 256, 0, st>>>(rptr, n_rows, nnzp, nnz_host, col, val, Hs, scale, R, out); break;
+    case 1: spmm_kernel<1, Acc><<<(unsigned)blocks, 256, 0, st>>>(rptr, n_rows, nnzp, nnz_host, acc, Hs, R, out); break;
+    case 2: spmm_kernel<2, Acc><<<(unsigned)blocks, 256, 0, st>>>(rptr, n_rows, nnzp, nnz_host, acc, Hs, R, out); break;
+    case 3: spmm_kernel<3, Acc><<<(unsigned)blocks, 256, 0, st>>>(rptr, n_rows, nnzp, nnz_host, acc, Hs, R, out); break;
+    default: spmm_kernel<4, Acc><<<(unsigned)blocks, 256, 0, st>>>(rptr, n_rows, nnzp, nnz_host, acc, Hs, R, out); break;
   }
   RCP_LAUNCH_CHECK("spmm");
   return RCP_OK;
@@ -457,7 +551,7 @@ struct Ws {
 struct MttkrpLayout {
   int64_t T;
   size_t o_tkey, o_tcnt, o_trep, o_twmin, o_twmax, o_twsum, o_dsc, o_bcnt, o_dkey, o_dcnt,
-      o_drep, o_dlo, o_dlen, o_doff, o_ioff, o_Hs, o_scan, o_rcnt, o_rptr, o_ed, o_ev, o_S,
+      o_drep, o_dlo, o_dlen, o_doff, o_ioff, o_Hs, o_scan, o_rcnt, o_rptr, o_cmat, o_ent, o_S,
       o_nnz;
   size_t total;
   MttkrpLayout(int64_t J, int64_t cap, int64_t n_rows, int R) {
@@ -484,8 +578,9 @@ struct MttkrpLayout {
     o_scan = w.add(scan_ws_bytes(sc));
     o_rcnt = w.add(sizeof(int64_t) * (n_rows + 1));
     o_rptr = w.add(sizeof(int64_t) * (n_rows + 2));
-    o_ed = w.add(sizeof(int32_t) * (cap + 1));
-    o_ev = w.add(sizeof(double) * (cap + 1));
+    o_cmat = w.add(sizeof(int32_t) * (size_t)sm_count() *
+                   (size_t)(n_rows < kPrivRows ? n_rows : kPrivRows));
+    o_ent = w.add(sizeof(double2) * (cap + 1));
     o_S = w.add(sizeof(int64_t) * 4);
     o_nnz = w.add(sizeof(int64_t) * 4);
     total = w.total + 256;
@@ -505,7 +600,7 @@ size_t rcp_mttkrp_ws_bytes(int64_t J, int64_t store_nnz, int64_t n_rows, int R) 
 static int64_t mttkrp_cap(int64_t J, int64_t n_rows, int R, size_t ws_bytes) {
   MttkrpLayout base(J, 0, n_rows, R);
   if (ws_bytes < base.total) return -1;
-  int64_t cap = (int64_t)((ws_bytes - base.total) / (sizeof(int32_t) + sizeof(double)));
+  int64_t cap = (int64_t)((ws_bytes - base.total) / sizeof(double2));
   MttkrpLayout L(J, cap, n_rows, R);
   while (L.total > ws_bytes && cap > 0) {
     cap -= 64;
@@ -520,7 +615,7 @@ int rcp_mttkrp_layout(int64_t J, int64_t n_rows, int R, size_t ws_bytes, int64_t
   if (cap < 0) return RCP_ERR_ARG;
   MttkrpLayout L(J, cap, n_rows, R);
   const size_t o[] = {L.o_dkey, L.o_dcnt, L.o_drep, L.o_dlo, L.o_dlen, L.o_doff, L.o_Hs,
-                      L.o_rcnt, L.o_rptr, L.o_ed, L.o_ev, L.o_S, L.o_nnz};
+                      L.o_rcnt, L.o_rptr, L.o_ent, L.o_cmat, L.o_S, L.o_nnz};
   for (int i = 0; i < 13; ++i) h_out[i] = (int64_t)o[i];
   h_out[13] = cap;
   return RCP_OK;
@@ -555,8 +650,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   double *Hs = (double *)P(L.o_Hs);
   void *scan_ws = P(L.o_scan);
   int64_t *rcnt = (int64_t *)P(L.o_rcnt), *rptr = (int64_t *)P(L.o_rptr);
-  int32_t *ed = (int32_t *)P(L.o_ed);
-  double *ev = (double *)P(L.o_ev);
+  double2 *ent = (double2 *)P(L.o_ent);
   int64_t *S = (int64_t *)P(L.o_S), *nnz = (int64_t *)P(L.o_nnz);
 
   Strides sd;
@@ -597,35 +691,49 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   RCP_LAUNCH_CHECK("item_count");
   rc = scan_i64_exclusive(icnt, ioff, J, S, scan_ws, st);
   if (rc) return rc;
-  // 4. row histogram -> row pointers
-  const int priv = n_rows <= kPrivRows ? 1 : 0;
-  size_t smem = priv ? sizeof(int32_t) * n_rows : 0;
+  // 4. row histogram -> row pointers; 5. scatter into row order (packed entries)
+  const int priv = (n_rows <= kPrivRows && cap < (1LL << 31)) ? 1 : 0;
   static bool attr = false;
   if (!attr) {
-    RCP_CUDA_TRY(cudaFuncSetAttribute(row_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    RCP_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RCP_CUDA_TRY(cudaFuncSetAttribute(cta_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RCP_CUDA_TRY(cudaFuncSetAttribute(cta_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
   const int grid = sm_count();
-  RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
-  row_count_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, dlo, dlen, d_rows, n_rows, priv,
-                                                         rcnt);
-  RCP_LAUNCH_CHECK("row_count");
-  rc = scan_i64_exclusive(rcnt, rptr, n_rows, nullptr, scan_ws, st);
-  if (rc) return rc;
+  if (priv) {
+    int32_t *cmat = (int32_t *)P(L.o_cmat);
+    const size_t smem = sizeof(int32_t) * n_rows;
+    cta_hist_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, dlo, dlen, d_rows, n_rows, cmat);
+    RCP_LAUNCH_CHECK("cta_hist");
+    cta_prefix_kernel<<<(unsigned)ceil_div(n_rows, 256), 256, 0, st>>>(cmat, grid, n_rows, rcnt);
+    RCP_LAUNCH_CHECK("cta_prefix");
+    rc = scan_i64_exclusive(rcnt, rptr, n_rows, nullptr, scan_ws, st);
+    if (rc) return rc;
+    cta_scatter_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, dlo, dlen, d_rows, d_vals,
+                                                             n_rows, rptr, cmat, ent, cap, d_status);
+    RCP_LAUNCH_CHECK("cta_scatter");
+  } else {
+    RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
+    row_count_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, dlo, dlen, d_rows, n_rows, 0, rcnt);
+    RCP_LAUNCH_CHECK("row_count");
+    rc = scan_i64_exclusive(rcnt, rptr, n_rows, nullptr, scan_ws, st);
+    if (rc) return rc;
+  }
   {
     int64_t b = ceil_div(n_rows, 256);
     if (b > 4LL * sm_count()) b = 4LL * sm_count();
     rows_hit_kernel<<<(unsigned)b, 256, 0, st>>>(rcnt, n_rows, d_stats);
     RCP_LAUNCH_CHECK("rows_hit");
   }
-  // 5. scatter into row order (rcnt reused as per-row cursor)
-  RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
-  scatter_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, dlo, dlen, d_rows, d_vals, n_rows,
-                                                       priv, rptr, rcnt, ed, ev, cap, d_status);
-  RCP_LAUNCH_CHECK("scatter");
+  if (!priv) {   // global per-row cursors (rcnt reused)
+    RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
+    scatter_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, dlo, dlen, d_rows, d_vals, n_rows, 0,
+                                                      rptr, rcnt, ent, cap, d_status);
+    RCP_LAUNCH_CHECK("scatter");
+  }
   // 6. segmented reduction
-  return launch_spmm<int32_t>(rptr, n_rows, nnz, 0, ed, ev, Hs, nullptr, R, d_out, st);
+  PackedEntries acc{ent};
+  return launch_spmm<PackedEntries>(rptr, n_rows, nnz, 0, acc, Hs, R, d_out, st);
 }
 
 int rcp_fiber_lookup(const int64_t *d_keys, int64_t n_cols, const int64_t *d_colptr,
@@ -665,8 +773,8 @@ int rcp_csr_spmm(const int64_t *d_row_ptr, int64_t n_rows, const int64_t *d_col,
   RCP_CUDA_TRY(cudaMemcpyAsync(&nnz, d_row_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   RCP_CUDA_TRY(cudaStreamSynchronize(st));
   if (nnz == 0) return RCP_OK;
-  return launch_spmm<int64_t>(d_row_ptr, n_rows, nullptr, nnz, d_col, d_val, d_H, d_scale, R,
-                              d_out, st);
+  CsrEntries acc{d_col, d_val, d_scale};
+  return launch_spmm<CsrEntries>(d_row_ptr, n_rows, nullptr, nnz, acc, d_H, R, d_out, st);
 }
 
 }  // extern "C"

@@ -77,12 +77,18 @@ leverage_kernel(const double *__restrict__ U, int64_t n, int R, const double *__
   }
 }
 
+// Ordered (deterministic) sum of the per-CTA partial masses; one block of 256 threads.
 __global__ void mass_kernel(const double *__restrict__ part, int nparts, double *mass) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += part[p];
-    mass[0] = s;
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int p = threadIdx.x; p < nparts; p += blockDim.x) s += part[p];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) mass[0] = red[0];
 }
 
 __global__ void normalize_kernel(double *__restrict__ dist, int64_t n, const double *mass) {
@@ -295,7 +301,7 @@ int rcp_arls_build(const double *d_U, int64_t n, int R, const double *d_Gp, doub
     default: leverage_kernel<4><<<grid, 256, smem, st>>>(d_U, n, R, d_Gp, d_dist, part); break;
   }
   RCP_LAUNCH_CHECK("leverage");
-  mass_kernel<<<1, 32, 0, st>>>(part, grid, d_mass);
+  mass_kernel<<<1, 256, 0, st>>>(part, grid, d_mass);
   RCP_LAUNCH_CHECK("leverage_mass");
   int64_t blocks = ceil_div(n, 256);
   if (blocks > 8LL * sm_count()) blocks = 8LL * sm_count();
