@@ -222,7 +222,18 @@ def run_ours(args):
     B = 12.0 * st[2] + 16.0 * st[0] + 8.0 * R * st[1] + 8.0 * R * st[4]
     n_launch = len(mt_events)
     achieved = (B / (mt_ms / 1e3)) / 1e9 if mt_ms > 0 else 0.0
-    e2e = measure_e2e(cl, args, rnd) if world == 1 else None
+    e2e = measure_e2e(cl, args, rnd)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([e2e.pop("_dt"), e2e.pop("_nnz")], dtype=torch.float64, device=dev)
+        gathered = [torch.zeros_like(tt) for _ in range(world)]
+        dist.all_gather(gathered, tt)
+        dt_max = max(float(g[0]) for g in gathered)
+        e2e["value"] = sum(float(g[1]) for g in gathered) / dt_max
+        e2e["ms_per_step"] = dt_max / e2e["steps"] * 1e3
+    else:
+        e2e.pop("_dt")
+        e2e.pop("_nnz")
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": sum(step_ms) / K, "higher_is_better": True,
@@ -285,7 +296,8 @@ def measure_e2e(cl, args, rnd, steps=None):
     return {"value": float(st[3]) / dt, "unit": UNIT,
             "h2d_bytes_per_step": int(sum(h.numel() * 8 for h in host_in)),
             "d2h_bytes_per_step": int(sum(h.numel() * 8 for h in host_out) + 8 * me.R),
-            "steps": steps, "ms_per_step": dt / steps * 1e3}
+            "steps": steps, "ms_per_step": dt / steps * 1e3, "_dt": dt, "_nnz": float(st[3]),
+            "api": "AlsSession.step_host (pinned host factors in, factors + sigma out)"}
 
 
 # ------------------------------------------------------------------ CPU arms

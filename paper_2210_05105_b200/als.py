@@ -198,8 +198,8 @@ class AlsSession:
         download the updated factors and sigma."""
         t = torch()
         r0 = self.cl.ranks[0]
-        if self.cl.P != 1:
-            raise ValueError("step_host drives a single-rank cluster")
+        if len(self.cl.ranks) != 1:
+            raise ValueError("step_host drives one rank per process (P=1 or SPMD)")
         for j, h in enumerate(factors_in):
             r0.U[j].copy_(h, non_blocking=True)
         for j in range(r0.N):

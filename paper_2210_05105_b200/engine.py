@@ -388,14 +388,7 @@ class Cluster:
                 for r in self.ranks:
                     r.arls_draw(i, k, rnd, quota, W)
                 if self.P > 1:
-                    counts = [int(q) for q in quota]
-                    rows = self.comm.all_gather_v([r.rows_tmp for r in self.ranks], counts)
-                    probs = self.comm.all_gather_v([r.prob_tmp for r in self.ranks], counts)
-                    urs = self.comm.all_gather_v([r.urow_tmp for r in self.ranks], counts)
-                    t = torch()
-                    cat_rows = t.cat([rows[p][:counts[p]] for p in range(self.P)])
-                    cat_probs = t.cat([probs[p][:counts[p]] for p in range(self.P)])
-                    cat_urows = t.cat([urs[p][:counts[p]] for p in range(self.P)]).contiguous()
+                    cat_rows, cat_probs, cat_urows = self._gather_arls_draws(quota)
                     for r in self.ranks:
                         r.arls_fold(i, k, rnd, first, cat_rows.to(r.dev), cat_probs.to(r.dev),
                                     cat_urows.to(r.dev))
@@ -405,6 +398,21 @@ class Cluster:
                 first = False
         for r in self.ranks:
             r.weights()
+
+    def _gather_arls_draws(self, quota):
+        """Concatenate every rank's local draws in rank order (ref samplers.py:181-182):
+        one all-gather-v of [row, probability, factor row] per draw (R+2 words)."""
+        t = torch()
+        counts = [int(q) for q in quota]
+        packs = []
+        for r in self.ranks:
+            q = counts[r.rank]
+            packs.append(t.cat([r.rows_tmp[:q].to(t.float64).unsqueeze(1),
+                                r.prob_tmp[:q].unsqueeze(1), r.urow_tmp[:q]], dim=1).contiguous())
+        got = self.comm.all_gather_v(packs, counts)
+        cat = t.cat([got[p][:counts[p]] for p in range(self.P)])
+        return (cat[:, 0].to(t.int64).contiguous(), cat[:, 1].contiguous(),
+                cat[:, 2:].contiguous())
 
     def _arls_quota(self, i, k, rnd):
         """Consistent multinomial split of J over rank masses (ref samplers.py:138-145);
