@@ -346,7 +346,18 @@ __global__ void cta_prefix_kernel(int32_t *__restrict__ cmat, int G, int64_t n_r
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= n_rows) return;
   int32_t run = 0;
-  for (int c = 0; c < G; ++c) {
+  int c = 0;
+  for (; c + 8 <= G; c += 8) {   // batch 8 independent loads before the dependent sums
+    int32_t v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = cmat[(int64_t)(c + q) * n_rows + r];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      cmat[(int64_t)(c + q) * n_rows + r] = run;
+      run += v[q];
+    }
+  }
+  for (; c < G; ++c) {
     const int32_t v = cmat[(int64_t)c * n_rows + r];
     cmat[(int64_t)c * n_rows + r] = run;
     run += v;
@@ -375,15 +386,25 @@ cta_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int64_t it = i0 + wid; it < i1; it += nw) {
     const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
-    for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32) {
-      const int32_t row = rows[pos];
-      const double v = vals[pos];
-      const int64_t o = atomicAdd(&cur[row], 1);
-      if (o >= cap) {
-        raise_status(status, RCP_ST_CAPACITY);
-        continue;
+    for (int64_t pos = sp.a + lane; pos < sp.b; pos += 64) {   // two entries in flight
+      const int64_t p2 = pos + 32;
+      const bool two = p2 < sp.b;
+      const int32_t row0 = rows[pos];
+      const double v0 = vals[pos];
+      int32_t row1 = 0;
+      double v1 = 0.0;
+      if (two) {
+        row1 = rows[p2];
+        v1 = vals[p2];
       }
-      put_entry(ent, o, sp.d, v);
+      const int64_t o0 = atomicAdd(&cur[row0], 1);
+      if (o0 < cap) put_entry(ent, o0, sp.d, v0);
+      else raise_status(status, RCP_ST_CAPACITY);
+      if (two) {
+        const int64_t o1 = atomicAdd(&cur[row1], 1);
+        if (o1 < cap) put_entry(ent, o1, sp.d, v1);
+        else raise_status(status, RCP_ST_CAPACITY);
+      }
     }
   }
 }

@@ -1,0 +1,135 @@
+"""Engine edge cases on the GPU against the CPU oracle: 4-mode tensors, rank exceeding a
+mode dimension, processor grids with empty blocks, several rank counts, empty batches,
+unsupported configurations, determinism.  Mirrors the reference's edge-case suite
+(ref tests/test_edge_cases.py, tests/test_als.py)."""
+
+import numpy as np
+import pytest
+
+from conftest import cuda_ok
+from oracle import randcp_oracle as O
+from paper_2210_05105_b200 import synth
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+
+def rel_err(a, b):
+    scale = max(np.abs(b).max(), 1e-300)
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / scale)
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2210_05105_b200 as pkg
+    return pkg
+
+
+def run_both(P, dims, nnz, R, sampler, J, rounds, procs=1, gdims=None, seed=5):
+    idx, vals = synth.small_random(dims, nnz, seed=seed)
+    t = P.SparseTensorCOO(dims, idx, vals)
+    cfg = P.AlsConfig(rank=R, rounds=rounds, sampler=sampler, samples=J,
+                      schedule="accumulator-stationary", procs=procs, grid_dims=gdims, seed=seed,
+                      fit_every=rounds, record_samples=True, permute=False)
+    res = P.run_als(cfg, tensor=t)
+    st, fits = O.run_as(dims, idx, vals, R, sampler, J, rounds, seed=seed, P=procs,
+                        gdims=gdims)
+    return res, st, fits
+
+
+@pytest.mark.parametrize("sampler", ["sts", "arls-lev"])
+@pytest.mark.parametrize("procs", [1, 2])
+def test_four_mode_als_matches_oracle(P, sampler, procs):
+    res, st, fits = run_both(P, (12, 9, 7, 5), 900, 4, sampler, 300, 3, procs=procs)
+    for a, b in zip(res.sample_log, st.sample_log):
+        assert np.array_equal(a, b)
+    for j in range(4):
+        assert rel_err(res.factors[j], st.full(j)) < 1e-9
+    assert abs(res.final_fit - fits[-1]) < 1e-6
+
+
+@pytest.mark.parametrize("sampler", ["sts", "arls-lev"])
+def test_rank_exceeding_mode_dimension(P, sampler):
+    # overcomplete factor on the short mode => rank-deficient Gram chain (Jacobi pinv path)
+    res, st, fits = run_both(P, (20, 3, 15), 250, 6, sampler, 256, 5, procs=4)
+    assert np.isfinite(res.final_fit)
+    assert res.factors[1].shape == (3, 6)
+    for a, b in zip(res.sample_log, st.sample_log):
+        assert np.array_equal(a, b)
+
+
+def test_grid_dimension_exceeding_mode_dimension(P):
+    # explicit grid with P_1 > I_1 leaves some row blocks empty
+    res, st, fits = run_both(P, (6, 3, 5), 60, 2, "sts", 64, 4, gdims=(1, 4, 1))
+    assert np.isfinite(res.final_fit)
+    for a, b in zip(res.sample_log, st.sample_log):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("procs", [3, 8])
+def test_sts_rank_count_invariance(P, procs):
+    """STS draws do not depend on the processor grid (ref tests/test_samplers.py:223-233)."""
+    r1, _, _ = run_both(P, (16, 12, 10), 800, 3, "sts", 200, 2, procs=1)
+    rp, _, _ = run_both(P, (16, 12, 10), 800, 3, "sts", 200, 2, procs=procs)
+    for a, b in zip(r1.sample_log, rp.sample_log):
+        assert np.array_equal(a, b)
+
+
+def test_determinism_same_seed_same_samples(P):
+    a, _, _ = run_both(P, (15, 11, 9), 600, 3, "sts", 256, 3)
+    b, _, _ = run_both(P, (15, 11, 9), 600, 3, "sts", 256, 3)
+    for x, y in zip(a.sample_log, b.sample_log):
+        assert np.array_equal(x, y)
+    for j in range(3):
+        assert rel_err(a.factors[j], b.factors[j]) < 1e-12
+
+
+def test_unsupported_configurations_raise(P):
+    idx, vals = synth.small_random((5, 4, 3), 20, seed=1)
+    t = P.SparseTensorCOO((5, 4, 3), idx, vals)
+    with pytest.raises(P.ScheduleError):
+        P.run_als(P.AlsConfig(rank=2, rounds=1, sampler="exact",
+                              schedule="accumulator-stationary"), tensor=t)
+    with pytest.raises(P.ScheduleError):
+        P.run_als(P.AlsConfig(rank=2, rounds=1, sampler="sts", samples=8,
+                              schedule="tensor-stationary"), tensor=t)
+    with pytest.raises(ValueError):
+        P.AlsConfig(rank=0, rounds=1).validate()
+
+
+def test_empty_batch_paths(P):
+    idx, vals = synth.small_random((5, 4, 3), 20, seed=10)
+    t = P.SparseTensorCOO((5, 4, 3), idx, vals)
+    m = P.matricize(t, 0)
+    csr = P.gather_sampled_nonzeros_to_csr(m, np.full((0, 3), -1, dtype=np.int64), 0)
+    assert csr.nnz == 0 and csr.n_cols == 0
+    out = P.downsampled_mttkrp(csr, np.ones((0, 2)), np.ones(0))
+    assert np.array_equal(out, np.zeros((5, 2)))
+    with pytest.raises(ValueError):
+        P.downsampled_mttkrp(csr, np.ones((3, 2)), np.ones(0))
+
+
+def test_matricization_row_bounds_enforced(P):
+    with pytest.raises(ValueError):
+        P.Matricization((4, 2, 2), np.array([[0, 0, 0], [3, 0, 0]]), np.ones(2), 0,
+                        row_lo=0, row_hi=2)
+
+
+def test_all_ones_full_cover_reproduces_exact(P):
+    """Every column sampled once with p = 1/n_cols: downsampled == exact MTTKRP
+    (ref tests/test_mttkrp.py:118-146)."""
+    idx, vals = synth.small_random((4, 3, 3), 25, seed=10)
+    t = P.SparseTensorCOO((4, 3, 3), idx, vals)
+    gen = np.random.default_rng(11)
+    factors = [gen.standard_normal((d, 2)) for d in t.dims]
+    m = P.matricize(t, 0)
+    X = np.full((9, 3), -1, dtype=np.int64)
+    s = 0
+    for c in range(3):
+        for b in range(3):
+            X[s, 1], X[s, 2] = b, c
+            s += 1
+    H = factors[1][X[:, 1]] * factors[2][X[:, 2]]
+    got = P.downsampled_mttkrp(P.gather_sampled_nonzeros_to_csr(m, X, 0), H, np.ones(9))
+    ref = P.mttkrp_exact(m, factors)
+    assert np.abs(got - ref).max() < 1e-12
