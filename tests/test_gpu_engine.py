@@ -48,13 +48,31 @@ def test_four_mode_als_matches_oracle(P, sampler, procs):
     assert abs(res.final_fit - fits[-1]) < 1e-6
 
 
+def horizon(dims, nnz, R, sampler, J, rounds, procs, seed=5):
+    """First solve whose samples the reference algorithm itself changes when the tensor
+    values move by one ulp (numerical ties, e.g. exact-integer rank masses hitting p = 0.5
+    in numpy's binomial); len(log) when it never does."""
+    idx, vals = synth.small_random(dims, nnz, seed=seed)
+    base, _ = O.run_as(dims, idx, vals, R, sampler, J, rounds, seed=seed, P=procs, fit=False)
+    h = len(base.sample_log)
+    for eps in (2.0 ** -52, -2.0 ** -52):
+        st, _ = O.run_as(dims, idx, vals * (1 + eps), R, sampler, J, rounds, seed=seed, P=procs,
+                         fit=False)
+        d = [i for i, (a, b) in enumerate(zip(st.sample_log, base.sample_log))
+             if not np.array_equal(a, b)]
+        if d:
+            h = min(h, d[0])
+    return h
+
+
 @pytest.mark.parametrize("sampler", ["sts", "arls-lev"])
 def test_rank_exceeding_mode_dimension(P, sampler):
     # overcomplete factor on the short mode => rank-deficient Gram chain (Jacobi pinv path)
     res, st, fits = run_both(P, (20, 3, 15), 250, 6, sampler, 256, 5, procs=4)
     assert np.isfinite(res.final_fit)
     assert res.factors[1].shape == (3, 6)
-    for a, b in zip(res.sample_log, st.sample_log):
+    h = horizon((20, 3, 15), 250, 6, sampler, 256, 5, 4)
+    for a, b in list(zip(res.sample_log, st.sample_log))[:h]:
         assert np.array_equal(a, b)
 
 
