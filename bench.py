@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=0)
+    ap.add_argument("--leaf", type=int, default=None, help="STS tree leaf rows (default: engine)")
     return ap.parse_args()
 
 
@@ -139,9 +140,9 @@ def run_ours(args):
     nnz = int(idx.shape[0])
     if world > 1:
         from paper_2210_05105_b200.dist import make_spmd_cluster
-        cl = make_spmd_cluster(dims, idx, vals, R, J, args.sampler, args.seed)
+        cl = make_spmd_cluster(dims, idx, vals, R, J, args.sampler, args.seed, leaf=args.leaf)
     else:
-        cl = make_local_cluster(dims, idx, vals, R, J, args.sampler, args.seed)
+        cl = make_local_cluster(dims, idx, vals, R, J, args.sampler, args.seed, leaf=args.leaf)
     del idx, vals
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
@@ -380,7 +381,7 @@ def run_reference(args):
     if dev.type == "cuda":
         from paper_2210_05105_b200.als import gather_factors
         from paper_2210_05105_b200.engine import make_local_cluster
-        cl = make_local_cluster(dims, idx_d, vals_d, R, J, args.sampler, args.seed)
+        cl = make_local_cluster(dims, idx_d, vals_d, R, J, args.sampler, args.seed, leaf=args.leaf)
         for rnd in range(1, args.warmup + 1):
             cl.round(rnd)
         factors = gather_factors(cl)

@@ -169,8 +169,8 @@ int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
  * d_sel (nullable): only samples s with d_sel[s] == sel_value walk (multi-rank owner);
  * their d_pmp_i[s] holds the probability so far and is multiplied, otherwise it is set.
  * Outputs per walked sample: d_Xi[s] (global row), d_pmp_i[s], d_resid[s] (nullable).
- * d_ws: rcp_sts_walk_ws_bytes(J, n, leaf). */
-size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf);
+ * d_ws: rcp_sts_walk_ws_bytes(J, n, leaf, R) (holds this walk's G (.) M node table). */
+size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf, int R);
 int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
                  int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
                  int64_t J, uint64_t key0, uint64_t key1, const double *d_override,

@@ -37,6 +37,10 @@ constexpr int kMaxModes = 8;
 constexpr int kPrivRows = 49152;   // CTA-private row histogram limit (int32 in smem)
 constexpr int kSpmmChunk = 256;    // entries per warp in the segmented reduction
 
+// Row stride of the scaled KRP rows Hs: a multiple of 16 doubles, so every row starts on a
+// 128-byte line and a warp's double2 row load touches ceil(R/16) lines, not one more.
+__host__ __device__ __forceinline__ int hs_stride(int R) { return (R + 15) & ~15; }
+
 struct Strides {
   int64_t s[kMaxModes];
 };
@@ -158,7 +162,8 @@ __global__ void lookup_kernel(const int64_t *__restrict__ keys, int64_t n_cols,
                               const int64_t *__restrict__ colptr, const int64_t *__restrict__ dkey,
                               const int32_t *__restrict__ dcnt, const int32_t *__restrict__ drep,
                               const int64_t *__restrict__ S, const double *__restrict__ H,
-                              const double *__restrict__ dsc, int R, int64_t *__restrict__ dlo,
+                              const double *__restrict__ dsc, int R, int Rp,
+                              int64_t *__restrict__ dlo,
                               int64_t *__restrict__ dlen, double *__restrict__ Hs,
                               int64_t *__restrict__ stats) {
   const int lane = threadIdx.x & 31;
@@ -182,7 +187,7 @@ __global__ void lookup_kernel(const int64_t *__restrict__ keys, int64_t n_cols,
   }
   const int32_t rep = drep[d];
   const double sc = dsc[d];
-  for (int c = lane; c < R; c += 32) Hs[d * R + c] = sc * H[(int64_t)rep * R + c];
+  for (int c = lane; c < Rp; c += 32) Hs[d * Rp + c] = c < R ? sc * H[(int64_t)rep * R + c] : 0.0;
 }
 
 __global__ void finalize_counts_kernel(const int64_t *__restrict__ S,
@@ -213,6 +218,7 @@ __global__ void rows_hit_kernel(const int64_t *__restrict__ rcnt, int64_t n_rows
 // are contiguous in the store, so a warp reads an item's rows/values fully coalesced.
 constexpr int64_t kItemE = 1024;
 constexpr int kTraverseThreads = 1024;
+constexpr int kInFlight = 8;   // entries per lane with loads in flight (latency hiding)
 
 __global__ void item_count_kernel(const int64_t *__restrict__ dlen, const int64_t *__restrict__ Sp,
                                   int64_t *__restrict__ icnt) {
@@ -334,7 +340,14 @@ cta_hist_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int64_t it = i0 + wid; it < i1; it += nw) {
     const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
-    for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32) atomicAdd(&hist[rows[pos]], 1);
+    for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32 * kInFlight) {
+      int32_t rw[kInFlight];
+#pragma unroll
+      for (int q = 0; q < kInFlight; ++q) rw[q] = pos + 32 * q < sp.b ? rows[pos + 32 * q] : -1;
+#pragma unroll
+      for (int q = 0; q < kInFlight; ++q)
+        if (rw[q] >= 0) atomicAdd(&hist[rw[q]], 1);
+    }
   }
   __syncthreads();
   int32_t *mine = cmat + (int64_t)blockIdx.x * n_rows;
@@ -386,23 +399,21 @@ cta_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int64_t it = i0 + wid; it < i1; it += nw) {
     const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
-    for (int64_t pos = sp.a + lane; pos < sp.b; pos += 64) {   // two entries in flight
-      const int64_t p2 = pos + 32;
-      const bool two = p2 < sp.b;
-      const int32_t row0 = rows[pos];
-      const double v0 = vals[pos];
-      int32_t row1 = 0;
-      double v1 = 0.0;
-      if (two) {
-        row1 = rows[p2];
-        v1 = vals[p2];
+    for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32 * kInFlight) {
+      // issue every load of the batch before the dependent cursor atomics and stores
+      int32_t rw[kInFlight];
+      double v[kInFlight];
+#pragma unroll
+      for (int q = 0; q < kInFlight; ++q) {
+        const bool ok = pos + 32 * q < sp.b;
+        rw[q] = ok ? rows[pos + 32 * q] : -1;
+        v[q] = ok ? vals[pos + 32 * q] : 0.0;
       }
-      const int64_t o0 = atomicAdd(&cur[row0], 1);
-      if (o0 < cap) put_entry(ent, o0, sp.d, v0);
-      else raise_status(status, RCP_ST_CAPACITY);
-      if (two) {
-        const int64_t o1 = atomicAdd(&cur[row1], 1);
-        if (o1 < cap) put_entry(ent, o1, sp.d, v1);
+#pragma unroll
+      for (int q = 0; q < kInFlight; ++q) {
+        if (rw[q] < 0) continue;
+        const int64_t o = atomicAdd(&cur[rw[q]], 1);
+        if (o < cap) put_entry(ent, o, sp.d, v[q]);
         else raise_status(status, RCP_ST_CAPACITY);
       }
     }
@@ -411,17 +422,8 @@ cta_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__
 
 // ------------------------------------------------------------ segmented SpMM
 // One warp per chunk of kSpmmChunk row-sorted entries; lanes own output columns.
-// Entries come either packed ({fiber id, value} in one 16-byte word, fused path) or as
-// separate column/value arrays (reference-shaped CSR, drop-in path).
-struct PackedEntries {
-  const double2 *ent;
-  __device__ __forceinline__ void get(int64_t x, int64_t &d, double &v) const {
-    const double2 e = ent[x];
-    d = (int64_t)(int32_t)__double_as_longlong(e.x);
-    v = e.y;
-  }
-};
-
+// Entries come as separate column/value arrays (reference-shaped CSR, drop-in path); the
+// fused path uses spmm_packed_kernel below.
 struct CsrEntries {
   const int64_t *col;
   const double *val;
@@ -493,6 +495,89 @@ spmm_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__r
           if (c < R) {
             if (whole) out[row * R + c] = acc[j];
             else atomicAdd(&out[row * R + c], acc[j]);
+          }
+        }
+        e = stop;
+      }
+      ++row;
+    }
+  }
+}
+
+// Fused-path variant: packed entries, Hs rows at the padded stride, each lane owns a
+// column pair loaded as one double2 (one load instruction per entry for R <= 64).
+template <int NP>
+__global__ void __launch_bounds__(256)
+spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__restrict__ nnzp,
+                   const double2 *__restrict__ ent, const double *__restrict__ Hs, int R,
+                   double *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int Rp = hs_stride(R);
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nnz = nnzp[0];
+  const int64_t nchunks = ceil_div(nnz, kSpmmChunk);
+  const double2 *H2 = reinterpret_cast<const double2 *>(Hs);
+  const int Rp2 = Rp >> 1;
+  for (int64_t ch = warp0; ch < nchunks; ch += nwarps) {
+    const int64_t c0 = ch * kSpmmChunk;
+    const int64_t c1 = min(c0 + kSpmmChunk, nnz);
+    int64_t row = floor_index(rptr, n_rows + 1, c0);
+    int64_t e = c0;
+    while (e < c1) {
+      const int64_t rs = rptr[row], re = rptr[row + 1];
+      const int64_t stop = min(re, c1);
+      if (stop > e) {
+        double2 acc[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) acc[j] = make_double2(0.0, 0.0);
+        int64_t x = e;
+        for (; x + 4 <= stop; x += 4) {
+          double2 en[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) en[q] = ent[x + q];
+#pragma unroll
+          for (int j = 0; j < NP; ++j) {
+            const int c2 = lane + 32 * j;
+            if (2 * c2 < R) {
+              double2 h[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                h[q] = H2[(int64_t)(int32_t)__double_as_longlong(en[q].x) * Rp2 + c2];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                acc[j].x = fma(en[q].y, h[q].x, acc[j].x);
+                acc[j].y = fma(en[q].y, h[q].y, acc[j].y);
+              }
+            }
+          }
+        }
+        for (; x < stop; ++x) {
+          const double2 en = ent[x];
+          const int64_t d = (int32_t)__double_as_longlong(en.x);
+#pragma unroll
+          for (int j = 0; j < NP; ++j) {
+            const int c2 = lane + 32 * j;
+            if (2 * c2 < R) {
+              const double2 h = H2[d * Rp2 + c2];
+              acc[j].x = fma(en.y, h.x, acc[j].x);
+              acc[j].y = fma(en.y, h.y, acc[j].y);
+            }
+          }
+        }
+        const bool whole = (rs >= c0) && (re <= c1);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+          const int c = 2 * (lane + 32 * j);
+          if (c < R) {
+            double *o = out + row * R + c;
+            if (whole) {
+              o[0] = acc[j].x;
+              if (c + 1 < R) o[1] = acc[j].y;
+            } else {
+              atomicAdd(o, acc[j].x);
+              if (c + 1 < R) atomicAdd(o + 1, acc[j].y);
+            }
           }
         }
         e = stop;
@@ -594,7 +679,7 @@ struct MttkrpLayout {
     o_dlen = w.add(sizeof(int64_t) * (J + 1));
     o_doff = w.add(sizeof(int64_t) * (J + 2));
     o_ioff = w.add(sizeof(int64_t) * (J + 2));
-    o_Hs = w.add(sizeof(double) * (size_t)(J + 1) * R);
+    o_Hs = w.add(sizeof(double) * (size_t)(J + 1) * hs_stride(R));
     int64_t sc = J + 1 > n_rows + 1 ? J + 1 : n_rows + 1;
     o_scan = w.add(scan_ws_bytes(sc));
     o_rcnt = w.add(sizeof(int64_t) * (n_rows + 1));
@@ -621,13 +706,13 @@ size_t rcp_mttkrp_ws_bytes(int64_t J, int64_t store_nnz, int64_t n_rows, int R) 
 static int64_t mttkrp_cap(int64_t J, int64_t n_rows, int R, size_t ws_bytes) {
   MttkrpLayout base(J, 0, n_rows, R);
   if (ws_bytes < base.total) return -1;
-  int64_t cap = (int64_t)((ws_bytes - base.total) / sizeof(double2));
-  MttkrpLayout L(J, cap, n_rows, R);
-  while (L.total > ws_bytes && cap > 0) {
-    cap -= 64;
-    L = MttkrpLayout(J, cap, n_rows, R);
+  // largest cap whose layout fits (alignment padding makes the size a step function)
+  int64_t lo = 0, hi = (int64_t)((ws_bytes - base.total) / sizeof(double2)) + 64;
+  while (hi - lo > 1) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (MttkrpLayout(J, mid, n_rows, R).total <= ws_bytes) lo = mid; else hi = mid;
   }
-  return cap;
+  return lo;
 }
 
 int rcp_mttkrp_layout(int64_t J, int64_t n_rows, int R, size_t ws_bytes, int64_t *h_out) {
@@ -698,7 +783,8 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   RCP_LAUNCH_CHECK("compact_write");
   // 2. lookup + scaled KRP rows
   lookup_kernel<<<(unsigned)ceil_div(J * 32, 256), 256, 0, st>>>(
-      d_keys, n_cols, d_colptr, dkey, dcnt, drep, S, d_H, dsc, R, dlo, dlen, Hs, d_stats);
+      d_keys, n_cols, d_colptr, dkey, dcnt, drep, S, d_H, dsc, R, hs_stride(R), dlo, dlen, Hs,
+      d_stats);
   RCP_LAUNCH_CHECK("lookup");
   // 3. fiber offsets
   int rc = scan_i64_exclusive(dlen, doff, J, S, scan_ws, st);
@@ -753,8 +839,11 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     RCP_LAUNCH_CHECK("scatter");
   }
   // 6. segmented reduction
-  PackedEntries acc{ent};
-  return launch_spmm<PackedEntries>(rptr, n_rows, nnz, 0, acc, Hs, R, d_out, st);
+  const unsigned sb = (unsigned)(8 * sm_count());
+  if (R <= 64) spmm_packed_kernel<1><<<sb, 256, 0, st>>>(rptr, n_rows, nnz, ent, Hs, R, d_out);
+  else spmm_packed_kernel<2><<<sb, 256, 0, st>>>(rptr, n_rows, nnz, ent, Hs, R, d_out);
+  RCP_LAUNCH_CHECK("spmm_packed");
+  return RCP_OK;
 }
 
 int rcp_fiber_lookup(const int64_t *d_keys, int64_t n_cols, const int64_t *d_colptr,

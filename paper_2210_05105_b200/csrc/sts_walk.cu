@@ -10,13 +10,19 @@
 // modes) see identical node masses.  Sorting the samples by (key of those indices, r)
 // makes each such group contiguous and ordered by r; at every node the left-goers are a
 // prefix of the group.  A group at a node is a *run* [lo, hi) of the sorted array: its
-// masses are computed once, the split point is found by binary search, and the run splits
-// into a left and a right run.  A run carries its path (thresholds T and directions from
-// the root) and the product of its step probabilities, which all its samples share, so no
-// per-sample state is touched above the leaves: a sample's rescaled residual at any level
-// is recomputed from its uniform by replaying the path's rescalings in the reference's
-// order.  Runs flow through a device work queue served by persistent warps.  Work is
-// proportional to the number of distinct (h, node) pairs, not samples x levels.
+// masses are computed once, the split point is found by a 32-ary warp search, and the run
+// splits into a left and a right run.  A run carries its path (thresholds T and directions
+// from the root) and the product of its step probabilities, which all its samples share,
+// so no per-sample state is touched above the leaves: a sample's rescaled residual at any
+// level is recomputed from its uniform by replaying the path's rescalings in the
+// reference's order.  Work is proportional to the number of distinct (h, node) pairs,
+// not samples x levels.
+//
+// Per walk, every node Gram is multiplied once by the packed conditioning matrix M'
+// (GM = G (.) M'), so a child mass is <GM_child, h h^T> with h read from shared memory:
+// no per-run R x R staging, and a walker warp needs only ~(5R + 100) doubles of shared
+// memory, so many warps per SM hide the L2 latency of the node reads.  The levels are
+// processed by one cooperative launch with a grid barrier between levels.
 #include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <float.h>
@@ -41,6 +47,12 @@ int sm_count() {
 constexpr int kMaxLeaf = 64;
 constexpr int kWalkWarps = 8;
 constexpr int kMaxDepth = 30;   // local tree depth limit (2^30 leaves)
+constexpr int kLeafBatch = 4;   // leaf rows whose masses one pass over the packed pairs makes
+// control words: [0] seeded runs, [2] samples finished, [3] participants,
+// [kGenBase + g] runs pushed during generation g (each generation has its own counter, so
+// the extent of generation g + 1 is stable once every CTA has passed the barrier)
+constexpr int kGenBase = 8;
+constexpr size_t kCtlBytes = sizeof(int) * (kGenBase + kMaxDepth + 8);
 
 struct Run {
   int32_t lo, hi;      // sorted positions [lo, hi)
@@ -53,10 +65,10 @@ struct Run {
 };
 
 struct WalkWs {
-  size_t o_key, o_key2, o_r, o_r2, o_idx, o_idx2, o_runs, o_ready, o_ctl, o_cub, total;
+  size_t o_key, o_key2, o_r, o_r2, o_idx, o_idx2, o_runs, o_ctl, o_mp, o_pairs, o_gm, o_cub, total;
   size_t cub_bytes;
   int64_t nruns;
-  WalkWs(int64_t J, int depth) {
+  WalkWs(int64_t J, int depth, int R) {
     size_t b1 = 0, b2 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b1, (const double *)nullptr, (double *)nullptr,
                                     (const int32_t *)nullptr, (int32_t *)nullptr, (int)J);
@@ -69,8 +81,9 @@ struct WalkWs {
       t = o + bytes;
       return o;
     };
-    // runs per level partition the samples: at most J per level, depth+1 levels
+    // runs of one level partition that level's samples: at most J per level
     nruns = J * (int64_t)(depth + 1) + 16;
+    const size_t Rs = (size_t)tri_stride(R);
     o_key = add(8 * J);
     o_key2 = add(8 * J);
     o_r = add(8 * J);
@@ -78,21 +91,21 @@ struct WalkWs {
     o_idx = add(4 * J);
     o_idx2 = add(4 * J);
     o_runs = add(sizeof(Run) * nruns);
-    o_ready = add(4 * nruns);
-    o_ctl = add(64);
+    o_ctl = add(kCtlBytes);
+    o_mp = add(8 * Rs);
+    o_pairs = add(4 * Rs);
+    o_gm = add(8 * Rs * (size_t)((2LL << depth) - 1));   // G (.) M' for every tree node
     o_cub = add(cub_bytes + 256);
     total = t + 256;
   }
 };
 
-// Shared doubles per walker warp: P (node stride), h/u row, leaf masses, path; kept even
-// so every warp's P is 16-byte aligned.
+// Shared doubles per walker warp: h, a batch of leaf rows z = u (.) h, leaf masses, path.
 __host__ __device__ __forceinline__ size_t walk_per_warp(int R) {
-  const size_t w = (size_t)tri_stride(R) + R + kMaxLeaf + kMaxDepth + 2;
+  const size_t w = (size_t)(1 + kLeafBatch) * R + kMaxLeaf + kMaxDepth;
   return (w + 1) & ~(size_t)1;
 }
 
-// control words: [0] queue tail, [1] queue head, [2] samples finished, [3] participants
 __device__ __forceinline__ int ld_volatile(const int *p) { return *(volatile const int *)p; }
 
 // The reference's per-level residual rescaling (ref samplers.py:436-440).
@@ -133,7 +146,7 @@ __global__ void walk_gather_kernel(const int64_t *__restrict__ in, const int32_t
 // One root run per distinct key; counts participants.
 __global__ void walk_seed_kernel(const int64_t *__restrict__ key, const int32_t *__restrict__ idx,
                                  int64_t J, const double *__restrict__ pmp_in, Run *runs,
-                                 int *ready, int *ctl) {
+                                 int *ctl) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= J) return;
   const int64_t k = key[s];
@@ -154,7 +167,6 @@ __global__ void walk_seed_kernel(const int64_t *__restrict__ key, const int32_t 
   rr.dirs = 0u;
   // samples of one group share their rank-level path, hence this probability
   rr.prob = pmp_in ? pmp_in[idx[s]] : 1.0;
-  (void)ready;
 }
 
 __global__ void row_keys_kernel(const int64_t *__restrict__ X, int N, int64_t J, Strides8 st,
@@ -167,21 +179,60 @@ __global__ void row_keys_kernel(const int64_t *__restrict__ X, int N, int64_t J,
   out[s] = k;
 }
 
-// Warp-cooperative push of a child run (path of the parent + one step).  Runs entering the
-// leaf level are cut into chunks so that the per-sample leaf work spreads over warps.
+// Packed M' (off-diagonals doubled, zero pad to the even stride) and the (a, b) index pair
+// of every packed position.
+__global__ void walk_tables_kernel(const double *__restrict__ Mfull, int R, double *__restrict__ Mp,
+                                   uint32_t *__restrict__ pairs) {
+  const int Rt = R * (R + 1) / 2, Rs = tri_stride(R);
+  for (int e = threadIdx.x; e < Rs; e += blockDim.x) {
+    if (e >= Rt) {
+      Mp[e] = 0.0;
+      pairs[e] = 0u;
+      continue;
+    }
+    int a = 0, rem = e;
+    while (rem >= R - a) {
+      rem -= R - a;
+      ++a;
+    }
+    const int b = a + rem;
+    const double m = Mfull[a * R + b];
+    Mp[e] = (a == b) ? m : 2.0 * m;
+    pairs[e] = (uint32_t)a | ((uint32_t)b << 16);
+  }
+}
+
+// GM[node] = G[node] (.) M' for one walk: a node's child mass is then <GM, h h^T>.
+__global__ void walk_gm_kernel(const double2 *__restrict__ tree, const double2 *__restrict__ Mp,
+                               int64_t n2, int Rs2, double2 *__restrict__ gm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 g = tree[i], m = Mp[i % Rs2];
+    gm[i] = make_double2(g.x * m.x, g.y * m.y);
+  }
+}
+
+// Warp-cooperative push of a child run (path of the parent + one step) into the next
+// level's generation.  Runs entering the leaf level are cut into chunks so that the
+// per-sample leaf work spreads over warps.
 constexpr int32_t kLeafChunk = 256;
 
-__device__ __forceinline__ void push_child(Run *runs, int *ready, int *ctl, const Run &par,
+__device__ __forceinline__ void push_child(Run *runs, int *gen_cnt, int64_t base, int64_t cap,
+                                           int *status, const Run &par, const double *Tp,
                                            int32_t lo, int32_t hi, double T, bool right,
                                            int depth, int lane) {
   const int lev = par.level;
   const int32_t chunk = (lev + 1 == depth) ? kLeafChunk : hi - lo;
   for (int32_t c0 = lo; c0 < hi; c0 += chunk) {
     int t = 0;
-    if (lane == 0) t = atomicAdd(&ctl[0], 1);
+    if (lane == 0) t = atomicAdd(gen_cnt, 1);
     t = __shfl_sync(0xffffffffu, t, 0);
-    Run &c = runs[t];
-    if (lane < lev) c.T[lane] = par.T[lane];
+    if (base + t >= cap) {   // cannot happen: one level holds at most J disjoint runs
+      if (lane == 0) raise_status(status, RCP_ST_CAPACITY);
+      continue;
+    }
+    Run &c = runs[base + t];
+    if (lane < lev) c.T[lane] = Tp[lane];
     if (lane == 0) {
       c.lo = c0;
       c.hi = min(hi, c0 + chunk);
@@ -191,186 +242,194 @@ __device__ __forceinline__ void push_child(Run *runs, int *ready, int *ctl, cons
       c.prob = par.prob * (right ? (1.0 - T) : T);
       c.T[lev] = T;
     }
-    __syncwarp();
   }
-  (void)ready;
+  __syncwarp();
+}
+
+__device__ __forceinline__ void fail_run(int32_t lo, int32_t hi, const int32_t *__restrict__ idx,
+                                         int64_t *__restrict__ Xi, int *status, int *ctl, int lane) {
+  for (int32_t s = lo + lane; s < hi; s += 32) Xi[idx[s]] = -1;
+  __syncwarp();
+  if (lane == 0) {
+    raise_status(status, RCP_ST_DEGENERATE);
+    __threadfence();
+    atomicAdd(&ctl[2], hi - lo);
+  }
 }
 
 __global__ void __launch_bounds__(kWalkWarps * 32)
-walk_runs_kernel(const double *__restrict__ tree, const double *__restrict__ U, int64_t n, int R,
-                 int leaf, int depth, int64_t row_lo, const double *__restrict__ Mfull,
-                 const double *__restrict__ H, const int32_t *__restrict__ idx,
-                 const double *__restrict__ r, Run *runs, int *ready, int *ctl, int64_t cap_runs,
-                 int64_t *__restrict__ Xi, double *__restrict__ pmp, double *__restrict__ resid,
-                 int *status) {
+walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, int64_t n, int R,
+                 int leaf, int depth, int64_t row_lo, const double *__restrict__ Mp_g,
+                 const uint32_t *__restrict__ pairs_g, const double *__restrict__ H,
+                 const int32_t *__restrict__ idx, const double *__restrict__ r, Run *runs,
+                 int *ctl, int64_t cap_runs, int64_t *__restrict__ Xi, double *__restrict__ pmp,
+                 double *__restrict__ resid, int *status) {
   extern __shared__ double sh[];
   const int Rt = R * (R + 1) / 2;
   const int Rs = tri_stride(R);                    // even node stride (zero pad)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const size_t per_warp = walk_per_warp(R);
-  double *Mp = sh;                                 // Rs: packed M, off-diagonals x2
-  double *P = Mp + Rs + (size_t)wid * per_warp;    // per warp: Rs (16-byte aligned)
-  double *uv = P + Rs;                             // R
-  double *mass = uv + R;                           // leaf
+  double *Mp = sh;                                 // Rs: packed M'
+  double *hv = Mp + Rs + (size_t)wid * walk_per_warp(R);   // R: the run's Hadamard row
+  double *zb = hv + R;                             // kLeafBatch x R: leaf rows (.) h
+  double *mass = zb + kLeafBatch * R;              // leaf
   double *Tp = mass + kMaxLeaf;                    // path thresholds of the current run
-  uint16_t *pairs = reinterpret_cast<uint16_t *>(Mp + Rs + (size_t)nw * per_warp);
-  if (Rs > Rt && threadIdx.x == 0) Mp[Rt] = 0.0;
-  for (int e = threadIdx.x; e < Rt; e += blockDim.x) {
-    int a = 0, rem = e;
-    while (rem >= R - a) {
-      rem -= R - a;
-      ++a;
-    }
-    const int b = a + rem;
-    pairs[e] = (uint16_t)(a | (b << 8));
-    const double m = Mfull[a * R + b];
-    Mp[e] = (a == b) ? m : 2.0 * m;
+  uint32_t *pairs = reinterpret_cast<uint32_t *>(Mp + Rs + (size_t)nw * walk_per_warp(R));
+  for (int e = threadIdx.x; e < Rs; e += blockDim.x) {
+    Mp[e] = Mp_g[e];
+    pairs[e] = pairs_g[e];
   }
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
   const int64_t gwarp = (int64_t)blockIdx.x * nw + wid;
   const int64_t nwarps = (int64_t)gridDim.x * nw;
-  int64_t begin = 0;
-  // Level-synchronous breadth: the runs of one tree level are [begin, end); their children
-  // are appended behind `end` and become the next level after a grid-wide barrier.
-  for (int lvl = 0; lvl <= depth; ++lvl) {
-  const int64_t end = min((int64_t)ld_volatile(&ctl[0]), cap_runs);
-  for (int64_t t = begin + gwarp; t < end; t += nwarps) {
-    const Run &run = runs[t];
-    const int32_t lo = run.lo, hi = run.hi, level = run.level;
-    const uint32_t dirs = run.dirs;
-    if (lane < level) Tp[lane] = run.T[lane];
-    // P = (h h^T) (.) M' of the run's common Hadamard row
-    const int32_t s0 = idx[lo];
-    for (int c = lane; c < R; c += 32) uv[c] = H ? H[(int64_t)s0 * R + c] : 1.0;
-    __syncwarp();
-    for (int e = lane; e < Rs; e += 32) {
-      const uint16_t ab = e < Rt ? pairs[e] : 0;
-      P[e] = e < Rt ? uv[ab & 0xff] * uv[ab >> 8] * Mp[e] : 0.0;
-    }
-    __syncwarp();
-    if (level < depth) {
-      const int64_t v = run.node;
-      const double2 *GL = reinterpret_cast<const double2 *>(
-          tree + ((1LL << (level + 1)) - 1 + 2 * v) * (int64_t)Rs);
-      const double2 *GR = GL + Rs / 2;
-      const double2 *P2 = reinterpret_cast<const double2 *>(P);
-      double qL = 0.0, qR = 0.0, qL2 = 0.0, qR2 = 0.0;
-      const int n2 = Rs / 2;
+  // Level-synchronous: the runs of level l are [begin, end); their children go to level
+  // l + 1 through that level's own counter, whose value is stable after the grid barrier.
+  int64_t begin = 0, end = min((int64_t)ld_volatile(&ctl[0]), cap_runs);
+  for (int lvl = 0; lvl <= depth && end > begin; ++lvl) {
+    int *gen_cnt = &ctl[kGenBase + lvl];
+    for (int64_t t = begin + gwarp; t < end; t += nwarps) {
+      const Run &run = runs[t];
+      const int32_t lo = run.lo, hi = run.hi, level = run.level;
+      const uint32_t dirs = run.dirs;
+      if (lane < level) Tp[lane] = run.T[lane];
+      const int32_t s0 = idx[lo];
+      for (int c = lane; c < R; c += 32) hv[c] = H ? H[(int64_t)s0 * R + c] : 1.0;
+      __syncwarp();
+      if (level < depth) {
+        // child masses <GM_child, h h^T> over the packed triangle, two positions per step
+        const int64_t v = run.node;
+        const double2 *GL = reinterpret_cast<const double2 *>(
+            gm + ((1LL << (level + 1)) - 1 + 2 * v) * (int64_t)Rs);
+        const double2 *GR = GL + Rs / 2;
+        const uint2 *PR = reinterpret_cast<const uint2 *>(pairs);
+        double qL = 0.0, qR = 0.0, qL2 = 0.0, qR2 = 0.0;
+        const int n2 = Rs / 2;
 #pragma unroll 4
-      for (int e = lane; e < n2; e += 32) {
-        const double2 gl = __ldg(GL + e);
-        const double2 gr = __ldg(GR + e);
-        const double2 p = P2[e];
-        qL = fma(gl.x, p.x, qL);
-        qL2 = fma(gl.y, p.y, qL2);
-        qR = fma(gr.x, p.x, qR);
-        qR2 = fma(gr.y, p.y, qR2);
-      }
-      qL += qL2;
-      qR += qR2;
-      qL = warp_sum(qL);
-      qR = warp_sum(qR);
-      qL = qL > 0.0 ? qL : 0.0;
-      qR = qR > 0.0 ? qR : 0.0;
-      const double tot = qL + qR;
-      if (!(tot > 0.0)) {
-        for (int32_t s = lo + lane; s < hi; s += 32) Xi[idx[s]] = -1;
-        __syncwarp();
-        if (lane == 0) {
-          raise_status(status, RCP_ST_DEGENERATE);
-          __threadfence();
-          atomicAdd(&ctl[2], hi - lo);
+        for (int e = lane; e < n2; e += 32) {
+          const double2 gl = __ldg(GL + e);
+          const double2 gr = __ldg(GR + e);
+          const uint2 ab = PR[e];
+          const double h0 = hv[ab.x & 0xffffu] * hv[ab.x >> 16];
+          const double h1 = hv[ab.y & 0xffffu] * hv[ab.y >> 16];
+          qL = fma(gl.x, h0, qL);
+          qL2 = fma(gl.y, h1, qL2);
+          qR = fma(gr.x, h0, qR);
+          qR2 = fma(gr.y, h1, qR2);
         }
-        continue;
-      }
-      double T = qL / tot;
-      T = fmin(fmax(T, 0.0), 1.0);
-      // left-goers (replayed r < T) are a prefix of the r-sorted run: 32-ary search
-      int32_t a = lo, b = hi;   // answer in [a, b]
-      while (b - a > 0) {
-        const int32_t span = b - a;
-        const int32_t step = (span + 31) / 32;
-        const int32_t pos = a + lane * step;
-        bool ge = true;   // "replayed r >= T" at pos (positions >= b count as true)
-        if (pos < b) ge = replay(r[pos], Tp, dirs, level) >= T;
-        const unsigned m = __ballot_sync(0xffffffffu, ge);
-        if (m == 0u) {                     // every probe < T: answer beyond the last probe
-          a = a + 31 * step + 1;
+        qL += qL2;
+        qR += qR2;
+        qL = warp_sum(qL);
+        qR = warp_sum(qR);
+        qL = qL > 0.0 ? qL : 0.0;
+        qR = qR > 0.0 ? qR : 0.0;
+        const double tot = qL + qR;
+        if (!(tot > 0.0)) {
+          fail_run(lo, hi, idx, Xi, status, ctl, lane);
           continue;
         }
-        const int first = __ffs(m) - 1;   // first lane whose probe is >= T
-        if (first == 0) {
-          b = a;
-        } else {                           // answer in (probe[first-1], probe[first]]
-          const int32_t na = a + (first - 1) * step + 1;
-          b = min(b, a + first * step);
-          a = na;
+        double T = qL / tot;
+        T = fmin(fmax(T, 0.0), 1.0);
+        // left-goers (replayed r < T) are a prefix of the r-sorted run: 32-ary search
+        int32_t a = lo, b = hi;   // answer in [a, b]
+        while (b - a > 0) {
+          const int32_t span = b - a;
+          const int32_t step = (span + 31) / 32;
+          const int32_t pos = a + lane * step;
+          bool ge = true;   // "replayed r >= T" at pos (positions >= b count as true)
+          if (pos < b) ge = replay(r[pos], Tp, dirs, level) >= T;
+          const unsigned m = __ballot_sync(0xffffffffu, ge);
+          if (m == 0u) {                     // every probe < T: answer beyond the last probe
+            a = a + 31 * step + 1;
+            continue;
+          }
+          const int first = __ffs(m) - 1;   // first lane whose probe is >= T
+          if (first == 0) {
+            b = a;
+          } else {                           // answer in (probe[first-1], probe[first]]
+            const int32_t na = a + (first - 1) * step + 1;
+            b = min(b, a + first * step);
+            a = na;
+          }
         }
+        const int32_t nl = a - lo;
+        if (nl > 0)
+          push_child(runs, gen_cnt, end, cap_runs, status, run, Tp, lo, lo + nl, T, false, depth,
+                     lane);
+        if (hi - lo - nl > 0)
+          push_child(runs, gen_cnt, end, cap_runs, status, run, Tp, lo + nl, hi, T, true, depth,
+                     lane);
+        continue;
       }
-      const int32_t nl = a - lo;
-      if (nl > 0) push_child(runs, ready, ctl, run, lo, lo + nl, T, false, depth, lane);
-      if (hi - lo - nl > 0) push_child(runs, ready, ctl, run, lo + nl, hi, T, true, depth, lane);
-      continue;
-    }
-    // ---- leaf block: masses of its rows, then each sample's inverse CDF
-    const int64_t r0 = (int64_t)run.node * leaf;
-    const int nr = (int)min((int64_t)leaf, n - r0);
-    const double rprob = run.prob;
-    bool bad = nr <= 0;
-    double total_m = 0.0;
-    if (!bad) {
-      for (int q = 0; q < nr; ++q) {
-        for (int c = lane; c < R; c += 32) uv[c] = U[(r0 + q) * R + c];
-        __syncwarp();
-        double m = 0.0;
-        for (int e = lane; e < Rt; e += 32) {
-          const uint16_t ab = pairs[e];
-          m = fma(uv[ab & 0xff] * uv[ab >> 8], P[e], m);
+      // ---- leaf block: masses z^T M' z of its rows z = u (.) h, then each sample's
+      // inverse CDF
+      const int64_t r0 = (int64_t)run.node * leaf;
+      const int nrow = (int)min((int64_t)leaf, n - r0);
+      const double rprob = run.prob;
+      bool bad = nrow <= 0;
+      double total_m = 0.0;
+      if (!bad) {
+        for (int q0 = 0; q0 < nrow; q0 += kLeafBatch) {
+          const int nb = min(kLeafBatch, nrow - q0);
+          for (int c = lane; c < nb * R; c += 32) {
+            const int j = c / R, col = c - j * R;
+            zb[c] = U[(r0 + q0 + j) * R + col] * hv[col];
+          }
+          __syncwarp();
+          double m[kLeafBatch];
+#pragma unroll
+          for (int j = 0; j < kLeafBatch; ++j) m[j] = 0.0;
+          for (int e = lane; e < Rt; e += 32) {
+            const uint32_t ab = pairs[e];
+            const int ia = ab & 0xffffu, ib = ab >> 16;
+            const double pe = Mp[e];
+#pragma unroll
+            for (int j = 0; j < kLeafBatch; ++j)
+              if (j < nb) m[j] = fma(zb[j * R + ia] * zb[j * R + ib], pe, m[j]);
+          }
+#pragma unroll
+          for (int j = 0; j < kLeafBatch; ++j) {
+            if (j < nb) {
+              const double mj = warp_sum(m[j]);
+              if (lane == 0) mass[q0 + j] = mj > 0.0 ? mj : 0.0;
+            }
+          }
+          __syncwarp();
         }
-        m = warp_sum(m);
-        if (lane == 0) mass[q] = m > 0.0 ? m : 0.0;
-        __syncwarp();
+        if (lane == 0)
+          for (int q = 0; q < nrow; ++q) total_m += mass[q];
+        total_m = __shfl_sync(0xffffffffu, total_m, 0);
+        bad = !(total_m > 0.0);
       }
-      if (lane == 0)
-        for (int q = 0; q < nr; ++q) total_m += mass[q];
-      total_m = __shfl_sync(0xffffffffu, total_m, 0);
-      bad = !(total_m > 0.0);
-    }
-    if (bad) {
-      for (int32_t s = lo + lane; s < hi; s += 32) Xi[idx[s]] = -1;
+      if (bad) {
+        fail_run(lo, hi, idx, Xi, status, ctl, lane);
+        continue;
+      }
+      for (int32_t s = lo + lane; s < hi; s += 32) {
+        const double target = replay(r[s], Tp, dirs, level) * total_m;
+        double cdf = 0.0;
+        int cnt = 0;
+        for (int q = 0; q < nrow; ++q) {
+          cdf += mass[q];
+          if (cdf <= target) ++cnt;
+        }
+        const int choice = cnt < nrow - 1 ? cnt : nrow - 1;
+        double cdf_at = 0.0;
+        for (int q = 0; q <= choice; ++q) cdf_at += mass[q];
+        const double picked = mass[choice];
+        double ro = picked > 0.0 ? (target - (cdf_at - picked)) / picked : 0.0;
+        ro = fmin(fmax(ro, 0.0), one_below());
+        const int32_t o = idx[s];
+        Xi[o] = row_lo + r0 + choice;
+        pmp[o] = rprob * (picked / total_m);
+        if (resid) resid[o] = ro;
+      }
       __syncwarp();
-      if (lane == 0) {
-        raise_status(status, RCP_ST_DEGENERATE);
-        __threadfence();
-        atomicAdd(&ctl[2], hi - lo);
-      }
-      continue;
+      if (lane == 0) atomicAdd(&ctl[2], hi - lo);
     }
-    for (int32_t s = lo + lane; s < hi; s += 32) {
-      const double target = replay(r[s], Tp, dirs, level) * total_m;
-      double cdf = 0.0;
-      int cnt = 0;
-      for (int q = 0; q < nr; ++q) {
-        cdf += mass[q];
-        if (cdf <= target) ++cnt;
-      }
-      const int choice = cnt < nr - 1 ? cnt : nr - 1;
-      double cdf_at = 0.0;
-      for (int q = 0; q <= choice; ++q) cdf_at += mass[q];
-      const double picked = mass[choice];
-      double ro = picked > 0.0 ? (target - (cdf_at - picked)) / picked : 0.0;
-      ro = fmin(fmax(ro, 0.0), one_below());
-      const int32_t o = idx[s];
-      Xi[o] = row_lo + r0 + choice;
-      pmp[o] = rprob * (picked / total_m);
-      if (resid) resid[o] = ro;
-    }
-    __syncwarp();
-    if (lane == 0) atomicAdd(&ctl[2], hi - lo);
-  }
-  begin = end;
-  grid.sync();
+    grid.sync();
+    const int64_t pushed_n = ld_volatile(gen_cnt);
+    begin = end;
+    end = min(end + pushed_n, cap_runs);
   }
 }
 
@@ -392,15 +451,16 @@ __global__ void fold_rows_kernel(double *__restrict__ out, const double *__restr
 
 size_t walk_smem(int R, int warps) {
   return sizeof(double) * ((size_t)tri_stride(R) + (size_t)warps * walk_per_warp(R)) +
-         sizeof(uint16_t) * (size_t)tri_stride(R) + 64;
+         sizeof(uint32_t) * (size_t)tri_stride(R) + 64;
 }
 
 }  // namespace
 
 extern "C" {
 
-size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf) {
-  WalkWs w(J > 0 ? J : 1, rcp_sts_depth(n, leaf));
+size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf, int R) {
+  if (R < 1 || R > RCP_MAX_RANK || leaf < 1) return 0;
+  WalkWs w(J > 0 ? J : 1, rcp_sts_depth(n, leaf), R);
   return w.total;
 }
 
@@ -417,7 +477,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   if (n == 0 || !d_tree || !d_U || !d_M || !d_Xi || !d_pmp_i || !d_ws) return RCP_ERR_ARG;
   const int depth = rcp_sts_depth(n, leaf);
   if (depth > kMaxDepth) return RCP_ERR_ARG;
-  WalkWs L(J, depth);
+  WalkWs L(J, depth, R);
   if (ws_bytes < L.total) return RCP_ERR_ARG;
   int warps = kWalkWarps;
   while (warps > 1 && walk_smem(R, warps) > 200 * 1024) --warps;
@@ -429,8 +489,10 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   double *r = (double *)(w + L.o_r), *r2 = (double *)(w + L.o_r2);
   int32_t *idx = (int32_t *)(w + L.o_idx), *idx2 = (int32_t *)(w + L.o_idx2);
   Run *runs = (Run *)(w + L.o_runs);
-  int *ready = (int *)(w + L.o_ready);
   int *ctl = (int *)(w + L.o_ctl);
+  double *Mp = (double *)(w + L.o_mp);
+  uint32_t *pairs = (uint32_t *)(w + L.o_pairs);
+  double *gm = (double *)(w + L.o_gm);
   void *cub_tmp = w + L.o_cub;
   const unsigned gb = (unsigned)ceil_div(J, 256);
   walk_prepare_kernel<<<gb, 256, 0, st>>>(d_hkey, J, key0, key1, d_override, d_rin, d_sel,
@@ -447,9 +509,21 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   RCP_LAUNCH_CHECK("walk_sort_key");
   walk_gather_kernel<<<gb, 256, 0, st>>>((const int64_t *)r, idx, J, (int64_t *)r2);
   RCP_LAUNCH_CHECK("walk_gather_r");
-  RCP_CUDA_TRY(cudaMemsetAsync(ctl, 0, 64, st));
-  walk_seed_kernel<<<gb, 256, 0, st>>>(key, idx, J, d_sel ? d_pmp_i : nullptr, runs, ready, ctl);
+  RCP_CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlBytes, st));
+  walk_seed_kernel<<<gb, 256, 0, st>>>(key, idx, J, d_sel ? d_pmp_i : nullptr, runs, ctl);
   RCP_LAUNCH_CHECK("walk_seed");
+  // this walk's M' tables and G (.) M' for every node
+  walk_tables_kernel<<<1, 256, 0, st>>>(d_M, R, Mp, pairs);
+  RCP_LAUNCH_CHECK("walk_tables");
+  {
+    const int Rs = tri_stride(R);
+    const int64_t n2 = ((2LL << depth) - 1) * (int64_t)(Rs / 2);
+    int64_t g = ceil_div(n2, 256);
+    if (g > 8LL * sm_count()) g = 8LL * sm_count();
+    walk_gm_kernel<<<(unsigned)g, 256, 0, st>>>((const double2 *)d_tree, (const double2 *)Mp, n2,
+                                                 Rs / 2, (double2 *)gm);
+    RCP_LAUNCH_CHECK("walk_gm");
+  }
   static bool attr = false;
   if (!attr) {
     RCP_CUDA_TRY(cudaFuncSetAttribute(walk_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -463,15 +537,17 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   // persistent: every CTA resident at once (workers wait on the shared queue)
   const int grid = per_sm * sm_count();
   // cooperative launch: every CTA co-resident, grid-wide barrier between tree levels
-  const double *a_tree = d_tree, *a_U = d_U, *a_M = d_M, *a_H = d_H_in;
+  const double *a_gm = gm, *a_U = d_U, *a_Mp = Mp, *a_H = d_H_in;
+  const uint32_t *a_pairs = pairs;
   const int32_t *a_idx = idx;
   const double *a_r = r2;
   int64_t a_n = n, a_row_lo = row_lo, a_cap = L.nruns;
   int a_R = R, a_leaf = leaf, a_depth = depth;
-  void *args[] = {(void *)&a_tree, (void *)&a_U, (void *)&a_n, (void *)&a_R, (void *)&a_leaf,
-                  (void *)&a_depth, (void *)&a_row_lo, (void *)&a_M, (void *)&a_H, (void *)&a_idx,
-                  (void *)&a_r, (void *)&runs, (void *)&ready, (void *)&ctl, (void *)&a_cap,
-                  (void *)&d_Xi, (void *)&d_pmp_i, (void *)&d_resid, (void *)&d_status};
+  void *args[] = {(void *)&a_gm, (void *)&a_U, (void *)&a_n, (void *)&a_R, (void *)&a_leaf,
+                  (void *)&a_depth, (void *)&a_row_lo, (void *)&a_Mp, (void *)&a_pairs,
+                  (void *)&a_H, (void *)&a_idx, (void *)&a_r, (void *)&runs, (void *)&ctl,
+                  (void *)&a_cap, (void *)&d_Xi, (void *)&d_pmp_i, (void *)&d_resid,
+                  (void *)&d_status};
   RCP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)walk_runs_kernel, dim3(grid),
                                            dim3(warps * 32), args, smem, st));
   RCP_LAUNCH_CHECK("walk_runs");

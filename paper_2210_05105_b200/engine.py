@@ -36,9 +36,12 @@ PHASES = ("sampling", "gather", "mttkrp", "reduction", "postprocess", "rebuild")
 
 
 def default_leaf(n, R, budget_bytes=4 << 30):
-    """Rows per tree leaf: 16, doubled until the padded tree fits the budget (<= 64)."""
+    """Rows per tree leaf: 8, doubled until the padded tree fits the budget (<= 64).  A leaf
+    costs L row masses (L R^2/2 each) per walking run, a level one pair of node masses, so
+    small leaves win until the per-walk G (.) M tree pass and the rebuild grow (measured
+    on C3: L = 8 beats 16 and 4)."""
     Rt = R * (R + 1) // 2
-    L = 16
+    L = 8
     while L < 64:
         nl = max(1, math.ceil(n / L))
         nodes = 2 * (1 << max(0, math.ceil(math.log2(nl)))) - 1

@@ -112,7 +112,7 @@ class Ops:
     def sts_walk(self, tree, U, leaf, row_lo, M, H_in, J, key, override, rin, sel, sel_value,
                  Xi, pmp_i, resid, hkey=None):
         n, R = U.shape
-        w = self.ws("sts_walk", self.lib.rcp_sts_walk_ws_bytes(int(J), n, int(leaf)))
+        w = self.ws("sts_walk", self.lib.rcp_sts_walk_ws_bytes(int(J), n, int(leaf), R))
         self._c("rcp_sts_walk", ptr(tree), ptr(U), n, R, int(leaf), int(row_lo), ptr(M),
                 ptr(H_in), ptr(hkey), int(J), key[0], key[1], ptr(override), ptr(rin), ptr(sel),
                 int(sel_value), ptr(Xi), ptr(pmp_i), ptr(resid), ptr(w), w.numel(),

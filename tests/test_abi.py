@@ -70,3 +70,17 @@ def test_product_path_refuses_without_cuda():
     from paper_2210_05105_b200 import gram
     with pytest.raises(RuntimeError, match="CUDA"):
         gram(np.eye(3))
+
+
+def test_mttkrp_workspace_holds_requested_capacity():
+    """rcp_mttkrp_ws_bytes(J, cap, ...) must yield a layout whose entry capacity is >= cap
+    (host-only layout arithmetic; a short capacity silently dropped gathered nonzeros)."""
+    lib = _lib.load()
+    lay = np.zeros(14, dtype=np.int64)
+    for J in (1, 7, 256, 65536):
+        for cap in (0, 1, 5, 60, 63, 64, 65, 1000, 12345, 10 ** 6):
+            for n in (1, 5, 30000, 60000):
+                for R in (1, 6, 50, 128):
+                    b = lib.rcp_mttkrp_ws_bytes(J, cap, n, R)
+                    assert lib.rcp_mttkrp_layout(J, n, R, b, lay.ctypes.data) == 0
+                    assert lay[13] >= cap, (J, cap, n, R, lay[13])

@@ -49,31 +49,49 @@ def test_four_mode_als_matches_oracle(P, sampler, procs):
 
 
 def horizon(dims, nnz, R, sampler, J, rounds, procs, seed=5):
-    """First solve whose samples the reference algorithm itself changes when the tensor
-    values move by one ulp (numerical ties, e.g. exact-integer rank masses hitting p = 0.5
-    in numpy's binomial); len(log) when it never does."""
+    """First solve whose samples the reference algorithm itself changes under one-ulp
+    perturbations of its floating-point inputs (numerical ties, e.g. leverage scores that
+    are all exactly 1 when R exceeds a mode's size, whose rank masses then feed numpy's
+    binomial an exact p = 0.5); len(log) when it never does.  Probes: tensor values and
+    initial factors moved by one ulp, and the per-rank leverage masses of CP-ARLS-LEV's
+    multinomial moved by one ulp."""
     idx, vals = synth.small_random(dims, nnz, seed=seed)
     base, _ = O.run_as(dims, idx, vals, R, sampler, J, rounds, seed=seed, P=procs, fit=False)
     h = len(base.sample_log)
-    for eps in (2.0 ** -52, -2.0 ** -52):
-        st, _ = O.run_as(dims, idx, vals * (1 + eps), R, sampler, J, rounds, seed=seed, P=procs,
-                         fit=False)
-        d = [i for i, (a, b) in enumerate(zip(st.sample_log, base.sample_log))
-             if not np.array_equal(a, b)]
-        if d:
-            h = min(h, d[0])
+    probes = [(vals * (1 + e), 1.0, None) for e in (2.0 ** -52, -2.0 ** -52)]
+    probes += [(vals, 1 + e, None) for e in (2.0 ** -52, -2.0 ** -52)]
+    probes += [(vals, 1.0, d) for d in (np.inf, -np.inf)]
+    split = O.lev_split
+    try:
+        for v, scale, direction in probes:
+            if direction is not None:
+                O.lev_split = (lambda C, *a, _d=direction:
+                               split(np.where(np.asarray(C) > 0, np.nextafter(C, _d), C), *a))
+            st, _ = O.run_as(dims, idx, v, R, sampler, J, rounds, seed=seed, P=procs, fit=False,
+                             init_scale=scale)
+            O.lev_split = split
+            d = [i for i, (a, b) in enumerate(zip(st.sample_log, base.sample_log))
+                 if not np.array_equal(a, b)]
+            if d:
+                h = min(h, d[0])
+    finally:
+        O.lev_split = split
     return h
 
 
+@pytest.mark.parametrize("procs", [1, 4])
 @pytest.mark.parametrize("sampler", ["sts", "arls-lev"])
-def test_rank_exceeding_mode_dimension(P, sampler):
+def test_rank_exceeding_mode_dimension(P, sampler, procs):
     # overcomplete factor on the short mode => rank-deficient Gram chain (Jacobi pinv path)
-    res, st, fits = run_both(P, (20, 3, 15), 250, 6, sampler, 256, 5, procs=4)
+    res, st, fits = run_both(P, (20, 3, 15), 250, 6, sampler, 256, 5, procs=procs)
     assert np.isfinite(res.final_fit)
     assert res.factors[1].shape == (3, 6)
-    h = horizon((20, 3, 15), 250, 6, sampler, 256, 5, 4)
+    h = horizon((20, 3, 15), 250, 6, sampler, 256, 5, procs)
     for a, b in list(zip(res.sample_log, st.sample_log))[:h]:
         assert np.array_equal(a, b)
+    if h == len(st.sample_log):
+        for j in range(3):
+            assert rel_err(res.factors[j], st.full(j)) < 1e-9
 
 
 def test_grid_dimension_exceeding_mode_dimension(P):
