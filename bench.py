@@ -104,6 +104,17 @@ def make_tensor(cfg_name, seed, dev):
     return c, idx, vals
 
 
+def traffic_bytes(args):
+    """DRAM bytes (read + write) per rcp_sampled_mttkrp call measured by ncu for this
+    workload (profiles/traffic.json, committed with the profile it came from), else None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                               "traffic.json")) as f:
+            return json.load(f)["entries"].get("%s/%s" % (args.config, args.sampler))
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def peaks():
     p = os.path.join(HERE, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -252,7 +263,7 @@ def run_ours(args):
         "distinct_nnz_per_round": nnz_d / K,
         "roofline": {"kernel": "rcp_sampled_mttkrp (dedup+lookup+transpose+segmented SpMM)",
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / hbm, "traffic": traffic_bytes(args), "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": B / max(n_launch, 1),
                      "avg_launch_ms": mt_ms / max(n_launch, 1), "launches": n_launch,
                      "share_of_step": mt_ms / max(sum(step_ms), 1e-9)},

@@ -162,7 +162,8 @@ int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
  * M = conditioning matrix (R x R, full) for this mode (ref samplers.py:412-415).
  * d_H_in: running Hadamard rows (J x R), NULL = all ones (first constant mode).
  * d_hkey (nullable): per-sample key of the indices already sampled in earlier modes;
- * samples with equal keys must have equal H rows.  Samples are grouped by (key, r) and
+ * samples with equal keys must have equal H rows; keys < 2^key_bits - 1 (key_bits in
+ * [1, 64], the sort touches only those bits).  Samples are grouped by (key, r) and
  * each group descends as runs, so node masses are evaluated once per distinct
  * (H row, node).  Uniforms: d_override (J doubles) or d_rin (residuals after the
  * rank-level levels) else WALK_UNIFORM draws of key (key0,key1).
@@ -173,7 +174,7 @@ int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
 size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf, int R);
 int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
                  int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
-                 int64_t J, uint64_t key0, uint64_t key1, const double *d_override,
+                 int key_bits, int64_t J, uint64_t key0, uint64_t key1, const double *d_override,
                  const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
                  double *d_pmp_i, double *d_resid, void *d_ws, size_t ws_bytes, int *d_status,
                  void *stream);

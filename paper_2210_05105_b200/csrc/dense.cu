@@ -17,30 +17,61 @@ int sm_count() {
 }
 
 // ------------------------------------------------------------------------------ Gram
-constexpr int kGramRows = 32;      // rows staged per tile
+// G = sum_r s_r^2 u_r u_r^T over n rows (U row-major n x R).  One CTA per SM streams
+// 64-row chunks (contiguous 64 R doubles) into shared memory with cp.async, double
+// buffered; each thread accumulates 4x4 tiles of the upper triangle for one row group;
+// row groups are combined in a fixed order, CTA partials by sum_partials (deterministic).
+constexpr int kGramRows = 64;      // rows per staged chunk
 constexpr int kGramThreads = 256;
-constexpr int kGramMaxPairs = 3;   // (R/4)(R/4+1)/2 <= 3*256 for R <= 128
+// tile pairs per thread: (R/4)(R/4+1)/2 <= 3*256 for R <= 128 (template parameter)
 
 int gram_grid(int64_t n) {
   int64_t tiles = ceil_div(n, kGramRows);
-  int64_t g = 2LL * sm_count();
+  int64_t g = sm_count();
   if (tiles < g) g = tiles;
   return (int)(g < 1 ? 1 : g);
 }
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+size_t gram_smem(int R) {
+  const int nT = (R + 3) / 4;
+  const size_t chunk = 2 * ((size_t)kGramRows * R + 8) + 2 * kGramRows;
+  const size_t red = (size_t)kGramThreads * 16;   // row-group partials
+  (void)nT;
+  return sizeof(double) * (chunk > red ? chunk : red) + 64;
+}
+
+template <int kGramMaxPairs>
 __global__ void __launch_bounds__(kGramThreads)
 gram_partial_kernel(const double *__restrict__ U, const double *__restrict__ scale, int64_t n,
-                    int R, double *__restrict__ part) {
-  extern __shared__ double sh[];
+                    int R, int aligned16, double *__restrict__ part) {
+  extern __shared__ __align__(16) double sh[];
   const int nT = (R + 3) / 4;
-  const int RP = nT * 4;
-  double *tile = sh;  // kGramRows x RP
   const int npairs = nT * (nT + 1) / 2;
+  const int cs = kGramRows * R + 8;                 // chunk stride (doubles), even
+  double *buf0 = sh, *buf1 = sh + cs;
+  double *sc0 = sh + 2 * cs, *sc1 = sc0 + kGramRows;
+  // thread -> (row group, pair list)
+  const int groups = npairs <= kGramThreads ? kGramThreads / npairs : 1;
+  const int grp = npairs <= kGramThreads ? (int)threadIdx.x / npairs : 0;
   int pa[kGramMaxPairs], pb[kGramMaxPairs];
   double acc[kGramMaxPairs][4][4];
 #pragma unroll
   for (int p = 0; p < kGramMaxPairs; ++p) {
-    int id = threadIdx.x + p * kGramThreads;
+    int id = npairs <= kGramThreads ? (p == 0 ? (int)threadIdx.x % npairs : npairs)
+                                    : (int)threadIdx.x + p * kGramThreads;
+    if (grp >= groups) id = npairs;
     pa[p] = -1;
     pb[p] = -1;
     if (id < npairs) {  // decode upper-triangular tile pair (ta <= tb)
@@ -57,31 +88,54 @@ gram_partial_kernel(const double *__restrict__ U, const double *__restrict__ sca
 #pragma unroll
       for (int y = 0; y < 4; ++y) acc[p][x][y] = 0.0;
   }
-  const int64_t ntiles = ceil_div(n, kGramRows);
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t r0 = t * kGramRows;
-    __syncthreads();
-    for (int e = threadIdx.x; e < kGramRows * RP; e += blockDim.x) {
-      int rr = e / RP, c = e % RP;
-      int64_t row = r0 + rr;
+  const int64_t nchunks = ceil_div(n, kGramRows);
+  auto issue = [&](int64_t c, double *dst, double *scd) {
+    const int64_t r0 = c * kGramRows;
+    const int rows = (int)min((int64_t)kGramRows, n - r0);
+    const int64_t cnt = (int64_t)rows * R;          // doubles, contiguous from U + r0 R
+    const double *src = U + r0 * R;   // 16-byte aligned when U is (r0 R is even)
+    if (aligned16) {
+      const int64_t n16 = cnt >> 1;
+      for (int64_t e = threadIdx.x; e < n16; e += blockDim.x) cp_async16(dst + 2 * e, src + 2 * e);
+      if ((cnt & 1) && threadIdx.x == 0) cp_async8(dst + cnt - 1, src + cnt - 1);
+    } else {
+      for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) cp_async8(dst + e, src + e);
+    }
+    for (int q = threadIdx.x; q < kGramRows; q += blockDim.x) {
       double v = 0.0;
-      if (row < n && c < R) {
-        v = U[row * R + c];
-        if (scale) v *= scale[row];
+      if (q < rows) {
+        v = scale ? scale[r0 + q] : 1.0;
+        v *= v;
       }
-      tile[e] = v;
+      scd[q] = v;
+    }
+    cp_async_commit();
+  };
+  int cur = 0;
+  if ((int64_t)blockIdx.x < nchunks) issue(blockIdx.x, buf0, sc0);
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int64_t nx = c + gridDim.x;
+    if (nx < nchunks) {
+      issue(nx, cur ? buf0 : buf1, cur ? sc0 : sc1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    const double *tile = cur ? buf1 : buf0;
+    const double *scw = cur ? sc1 : sc0;
+    const int rows = (int)min((int64_t)kGramRows, n - c * kGramRows);
 #pragma unroll
     for (int p = 0; p < kGramMaxPairs; ++p) {
       if (pa[p] < 0) continue;
       const int a0 = pa[p] * 4, b0 = pb[p] * 4;
-      for (int rr = 0; rr < kGramRows; ++rr) {
-        const double *row = tile + rr * RP;
+      for (int rr = grp; rr < rows; rr += groups) {
+        const double *row = tile + rr * R;
+        const double w = scw[rr];
         double av[4], bv[4];
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
-          av[x] = row[a0 + x];
+          av[x] = row[a0 + x] * w;   // columns >= R read the next row: discarded below
           bv[x] = row[b0 + x];
         }
 #pragma unroll
@@ -90,8 +144,37 @@ gram_partial_kernel(const double *__restrict__ U, const double *__restrict__ sca
           for (int y = 0; y < 4; ++y) acc[p][x][y] = fma(av[x], bv[y], acc[p][x][y]);
       }
     }
+    __syncthreads();
+    cur ^= 1;
   }
   double *out = part + (int64_t)blockIdx.x * R * R;
+  if (groups > 1) {
+    // combine the row groups in group order (deterministic), pair-major layout
+    double *red = sh;
+    if (pa[0] >= 0) {
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) red[((size_t)grp * npairs + threadIdx.x % npairs) * 16 + x * 4 + y] = acc[0][x][y];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < npairs * 16; e += blockDim.x) {
+      const int pr = e >> 4, xy = e & 15;
+      double v = 0.0;
+      for (int g = 0; g < groups; ++g) v += red[((size_t)g * npairs + pr) * 16 + xy];
+      int ta = 0, rem = pr;
+      while (rem >= nT - ta) {
+        rem -= nT - ta;
+        ++ta;
+      }
+      const int a = ta * 4 + (xy >> 2), b = (ta + rem) * 4 + (xy & 3);
+      if (a < R && b < R) {
+        out[a * R + b] = v;
+        out[b * R + a] = v;
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int p = 0; p < kGramMaxPairs; ++p) {
     if (pa[p] < 0) continue;
@@ -189,6 +272,95 @@ __device__ void load_input(const double *in, int n_chain, int skip, int R, int L
   }
 }
 
+__device__ __forceinline__ double fast_rcp(double x) {
+  // reciprocal to ~1 ulp: hardware approximation + two Newton steps (no slow path)
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Gauss-Jordan inverse of the SPD matrix in A (no pivoting).  Warp w owns rows
+// w + 16a (a < RA), lane l owns columns l + 32b (b < RB); the RA x RB entries stay in
+// registers for the whole inversion.  Pivot k needs only row k and column k, which their
+// owners publish to a double-buffered shared row/column before the single barrier of the
+// step.  Returns false (uniformly) on a non-positive pivot; A then holds garbage.
+template <int RA, int RB>
+__device__ bool gj_registers(double *A, int LD, int R, double *rcb) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double v[RA][RB];
+#pragma unroll
+  for (int a = 0; a < RA; ++a)
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const int i = w + 16 * a, j = lane + 32 * b;
+      v[a][b] = (i < R && j < R) ? A[i * LD + j] : 0.0;
+    }
+  for (int q = threadIdx.x; q < R; q += blockDim.x) {
+    rcb[q] = A[q];                // row 0
+    rcb[2 * R + q] = A[q * LD];   // column 0
+  }
+  __syncthreads();
+  for (int k = 0; k < R; ++k) {
+    const int pb = k & 1;
+    const double *rowk = rcb + pb * R, *colk = rcb + 2 * R + pb * R;
+    double *rown = rcb + (pb ^ 1) * R, *coln = rcb + 2 * R + (pb ^ 1) * R;
+    const double pk = rowk[k];
+    if (!(pk > 0.0)) return false;   // every thread reads the same pivot
+    const double rk = fast_rcp(pk);
+    // all shared reads of the step first (the publishes below alias nothing read here,
+    // but the compiler cannot prove it and would serialise the rows otherwise)
+    double rj[RB], ci[RA];
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const int j = lane + 32 * b;
+      rj[b] = j < R ? rowk[j] : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < RA; ++a) {
+      const int i = w + 16 * a;
+      ci[a] = i < R ? colk[i] : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < RA; ++a) {
+      const int i = w + 16 * a;
+      const double f = ci[a] * rk;
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        const bool jk = lane + 32 * b == k;
+        const double x = v[a][b];
+        const double row = jk ? rk : x * rk;          // i == k
+        const double oth = jk ? -f : fma(-f, rj[b], x);
+        v[a][b] = (i == k) ? row : oth;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < RA; ++a) {
+      const int i = w + 16 * a;
+      if (i == k + 1) {                          // publish the next pivot row
+#pragma unroll
+        for (int b = 0; b < RB; ++b)
+          if (lane + 32 * b < R) rown[lane + 32 * b] = v[a][b];
+      }
+#pragma unroll
+      for (int b = 0; b < RB; ++b)               // and the next pivot column
+        if (i < R && lane + 32 * b == k + 1) coln[i] = v[a][b];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < RA; ++a)
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const int i = w + 16 * a, j = lane + 32 * b;
+      if (i < R && j < R) A[i * LD + j] = v[a][b];
+    }
+  __syncthreads();
+  return true;
+}
+
 __global__ void __launch_bounds__(kPinvThreads)
 pinv_kernel(const double *__restrict__ in, int n_chain, int skip, int R, double cutoff,
             double *__restrict__ chain_out, double *__restrict__ out, int *status) {
@@ -200,6 +372,7 @@ pinv_kernel(const double *__restrict__ in, int n_chain, int skip, int R, double 
   double *cs = diag + R + 1;            // R/2+1 cosines
   double *sn = cs + (R / 2 + 2);        // sines
   int *pr = reinterpret_cast<int *>(sn + (R / 2 + 2));  // pairs (2*(R/2+1))
+  double *rcb = sn + (R / 2 + 2) + (R / 2 + 2) + 2;  // 4R + 2: pivot row/column (x2), 1/pivot
   __shared__ int flag;
 
   load_input(in, n_chain, skip, R, LD, A, chain_out);
@@ -235,36 +408,31 @@ pinv_kernel(const double *__restrict__ in, int n_chain, int skip, int R, double 
   }
   fro = sqrt(block_reduce(fro, red, false));
 
-  // ---- fast path: in-place Gauss-Jordan inverse (no pivoting; valid for SPD) ----
+  // ---- fast path: Gauss-Jordan inverse (no pivoting; valid for SPD) ----
+  // Every thread keeps its entries (e = tid + 512 m) in registers for the whole inversion;
+  // pivot k needs only row k and column k, which their owners publish to a double-buffered
+  // shared row/column before the single barrier of the step.
   if (threadIdx.x == 0) flag = (fro > 0.0) ? 1 : 0;
   __syncthreads();
-  for (int k = 0; k < R && flag; ++k) {
-    const double pk = A[k * LD + k];
-    if (!(pk > 0.0)) {  // not positive definite (or NaN): fall back
-      __syncthreads();
-      if (threadIdx.x == 0) flag = 0;
-      __syncthreads();
-      break;
-    }
-    for (int j = threadIdx.x; j < R; j += blockDim.x)
-      if (j != k) A[k * LD + j] /= pk;
-    __syncthreads();
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-      int i = e / R, j = e % R;
-      if (i != k && j != k) A[i * LD + j] -= A[i * LD + k] * A[k * LD + j];
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < R; i += blockDim.x) {
-      if (i != k) A[i * LD + k] = -A[i * LD + k] / pk;
-    }
-    if (threadIdx.x == 0) A[k * LD + k] = 1.0 / pk;
+  if (flag) {
+    bool ok;
+    if (R <= 16) ok = gj_registers<1, 1>(A, LD, R, rcb);
+    else if (R <= 32) ok = gj_registers<2, 1>(A, LD, R, rcb);
+    else if (R <= 48) ok = gj_registers<3, 2>(A, LD, R, rcb);
+    else if (R <= 64) ok = gj_registers<4, 2>(A, LD, R, rcb);
+    else if (R <= 80) ok = gj_registers<5, 3>(A, LD, R, rcb);
+    else if (R <= 96) ok = gj_registers<6, 3>(A, LD, R, rcb);
+    else if (R <= 112) ok = gj_registers<7, 4>(A, LD, R, rcb);
+    else ok = gj_registers<8, 4>(A, LD, R, rcb);
+    if (!ok && threadIdx.x == 0) flag = 0;
     __syncthreads();
   }
+  double *Ainv = A;
   if (flag) {
     double ifro = 0.0;
     bool finite = true;
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-      double v = A[(e / R) * LD + (e % R)];
+      double v = Ainv[(e / R) * LD + (e % R)];
       ifro += v * v;
       if (!isfinite(v)) finite = false;
     }
@@ -274,7 +442,7 @@ pinv_kernel(const double *__restrict__ in, int n_chain, int skip, int R, double 
     if (bad == 0.0 && fro * ifro < 1e8 && cutoff <= 1e-9) {
       for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
         int a = e / R, b = e % R;
-        out[e] = 0.5 * (A[a * LD + b] + A[b * LD + a]);
+        out[e] = 0.5 * (Ainv[a * LD + b] + Ainv[b * LD + a]);
       }
       return;
     }
@@ -490,9 +658,26 @@ int rcp_gram(const double *d_U, const double *d_scale, int64_t n, int R, double 
     return RCP_OK;
   }
   const int grid = gram_grid(n);
-  const int RP = ((R + 3) / 4) * 4;
-  size_t smem = sizeof(double) * kGramRows * RP;
-  gram_partial_kernel<<<grid, kGramThreads, smem, st>>>(d_U, d_scale, n, R, (double *)d_ws);
+  const size_t smem = gram_smem(R);
+  static bool attr = false;
+  if (!attr) {
+    RCP_CUDA_TRY(cudaFuncSetAttribute(gram_partial_kernel<1>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RCP_CUDA_TRY(cudaFuncSetAttribute(gram_partial_kernel<2>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RCP_CUDA_TRY(cudaFuncSetAttribute(gram_partial_kernel<3>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  const int al = ((uintptr_t)d_U & 15) == 0 ? 1 : 0;
+  const int nT = (R + 3) / 4, npairs = nT * (nT + 1) / 2;
+  double *part = (double *)d_ws;
+  if (npairs <= kGramThreads)
+    gram_partial_kernel<1><<<grid, kGramThreads, smem, st>>>(d_U, d_scale, n, R, al, part);
+  else if (npairs <= 2 * kGramThreads)
+    gram_partial_kernel<2><<<grid, kGramThreads, smem, st>>>(d_U, d_scale, n, R, al, part);
+  else
+    gram_partial_kernel<3><<<grid, kGramThreads, smem, st>>>(d_U, d_scale, n, R, al, part);
   RCP_LAUNCH_CHECK("gram_partial");
   int64_t len = (int64_t)R * R;
   sum_partials_kernel<<<(unsigned)ceil_div(len, 32), 256, 0, st>>>((double *)d_ws, grid, len,
@@ -504,8 +689,9 @@ int rcp_gram(const double *d_U, const double *d_scale, int64_t n, int R, double 
 int rcp_pinv(const double *d_in, int n_chain, int skip, int R, double rel_cutoff,
              double *d_chain_out, double *d_out, int *d_status, void *stream) {
   if (R < 1 || R > RCP_MAX_RANK || !d_in || !d_out) return RCP_ERR_ARG;
-  size_t smem = sizeof(double) * ((size_t)R * (R + 1) + 40 + (R + 1) + 2 * (R / 2 + 2)) +
-                sizeof(int) * (2 * (R / 2 + 2)) + 64;
+  // A, Jacobi scratch, pivot row/column buffers (see pinv_kernel's layout)
+  const size_t smem =
+      sizeof(double) * ((size_t)R * (R + 1) + 40 + (R + 1) + 3 * (R / 2 + 2) + 2 + 4 * R + 2) + 64;
   static bool attr = false;
   if (!attr) {
     RCP_CUDA_TRY(cudaFuncSetAttribute(pinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

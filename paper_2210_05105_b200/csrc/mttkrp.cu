@@ -69,6 +69,32 @@ __device__ __forceinline__ int64_t lower_bound_i64(const int64_t *__restrict__ a
   return lo;
 }
 
+// First i in [0, n) with a[i] >= x (n if none), found by a whole warp: 32 probes per step
+// (about log_32 n dependent loads instead of log_2 n).  Every lane returns the answer.
+__device__ __forceinline__ int64_t warp_lower_bound(const int64_t *__restrict__ a, int64_t n,
+                                                    int64_t x, int lane) {
+  int64_t lo = 0, hi = n;   // answer in [lo, hi]
+  while (hi - lo >= 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t pos = lo + lane * step;
+    const bool ge = pos < hi ? a[pos] >= x : true;
+    const unsigned m = __ballot_sync(0xffffffffu, ge);
+    if (m == 0u) {
+      lo = lo + 31 * step + 1;
+    } else {
+      const int f = __ffs(m) - 1;
+      if (f == 0) return lo;   // a[lo] >= x
+      const int64_t nlo = lo + (f - 1) * step + 1;
+      hi = min(hi, lo + f * step);
+      lo = nlo;
+    }
+  }
+  const int64_t pos = lo + lane;
+  const bool ge = pos < hi ? a[pos] >= x : true;
+  const unsigned m = __ballot_sync(0xffffffffu, ge);
+  return lo + (__ffs(m) - 1);   // hi - lo <= 31: lane hi - lo always reports true
+}
+
 // largest i in [0, n) with a[i] <= x  (a nondecreasing, a[0] <= x)
 __device__ __forceinline__ int64_t floor_index(const int64_t *__restrict__ a, int64_t n, int64_t x) {
   int64_t lo = 0, hi = n;
@@ -171,9 +197,9 @@ __global__ void lookup_kernel(const int64_t *__restrict__ keys, int64_t n_cols,
   const int64_t nS = S[0];
   if (d >= nS) return;
   int64_t lo = 0, len = 0;
+  const int64_t key = dkey[d];
+  const int64_t c = warp_lower_bound(keys, n_cols, key, lane);
   if (lane == 0) {
-    const int64_t key = dkey[d];
-    int64_t c = lower_bound_i64(keys, n_cols, key);
     if (c < n_cols && keys[c] == key) {
       lo = colptr[c];
       len = colptr[c + 1] - lo;

@@ -466,13 +466,14 @@ size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf, int R) {
 
 int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
                  int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
-                 int64_t J, uint64_t key0, uint64_t key1, const double *d_override,
+                 int key_bits, int64_t J, uint64_t key0, uint64_t key1, const double *d_override,
                  const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
                  double *d_pmp_i, double *d_resid, void *d_ws, size_t ws_bytes, int *d_status,
                  void *stream) {
   if (R < 1 || R > RCP_MAX_RANK || leaf < 1 || leaf > kMaxLeaf || J < 0 || n < 0 ||
-      J >= (1LL << 31))
+      J >= (1LL << 31) || key_bits < 1)
     return RCP_ERR_ARG;
+  if (key_bits > 64 || !d_hkey) key_bits = 64;
   if (J == 0) return RCP_OK;
   if (n == 0 || !d_tree || !d_U || !d_M || !d_Xi || !d_pmp_i || !d_ws) return RCP_ERR_ARG;
   const int depth = rcp_sts_depth(n, leaf);
@@ -505,7 +506,8 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   walk_gather_kernel<<<gb, 256, 0, st>>>(key, idx2, J, key2);
   RCP_LAUNCH_CHECK("walk_gather");
   tb = L.cub_bytes;
-  RCP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key2, key, idx2, idx, (int)J, 0, 64, st));
+  RCP_CUDA_TRY(
+      cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key2, key, idx2, idx, (int)J, 0, key_bits, st));
   RCP_LAUNCH_CHECK("walk_sort_key");
   walk_gather_kernel<<<gb, 256, 0, st>>>((const int64_t *)r, idx, J, (int64_t *)r2);
   RCP_LAUNCH_CHECK("walk_gather_r");

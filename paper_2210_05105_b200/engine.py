@@ -241,10 +241,10 @@ class RankState:
             ops.fold_rows(self.H, self.U[i], self.lo[i], self.X[i], init=True)
             return
         if self.n[i] > 0:
-            hk = ops.walk_key(self.X, self.dims, k, i, self.hkey)
+            hk, kb = ops.walk_key(self.X, self.dims, k, i, self.hkey)
             ops.sts_walk(self.trees[i], self.U[i], self.leaf_of(i), self.lo[i], self.M, H_in,
                          self.J, key, override if self.P == 1 else None, rin, sel, self.rank,
-                         self.X[i], self.pmp[i], self.resid, hkey=hk)
+                         self.X[i], self.pmp[i], self.resid, hkey=hk, key_bits=kb)
             if self.P == 1:     # fold straight into the running Hadamard rows
                 ops.fold_rows(self.H, self.U[i], self.lo[i], self.X[i], init=first)
             else:               # this rank's finished rows, exchanged afterwards

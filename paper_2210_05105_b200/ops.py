@@ -110,11 +110,11 @@ class Ops:
                 stream_handle())
 
     def sts_walk(self, tree, U, leaf, row_lo, M, H_in, J, key, override, rin, sel, sel_value,
-                 Xi, pmp_i, resid, hkey=None):
+                 Xi, pmp_i, resid, hkey=None, key_bits=64):
         n, R = U.shape
         w = self.ws("sts_walk", self.lib.rcp_sts_walk_ws_bytes(int(J), n, int(leaf), R))
         self._c("rcp_sts_walk", ptr(tree), ptr(U), n, R, int(leaf), int(row_lo), ptr(M),
-                ptr(H_in), ptr(hkey), int(J), key[0], key[1], ptr(override), ptr(rin), ptr(sel),
+                ptr(H_in), ptr(hkey), int(key_bits), int(J), key[0], key[1], ptr(override), ptr(rin), ptr(sel),
                 int(sel_value), ptr(Xi), ptr(pmp_i), ptr(resid), ptr(w), w.numel(),
                 self.status.ptr, stream_handle())
 
@@ -136,10 +136,11 @@ class Ops:
 
     def walk_key(self, X, dims, k, i, out):
         """Mixed-radix key of the modes already sampled before constant mode i
-        (modes < i, excluding k); None for the first constant mode."""
+        (modes < i, excluding k) and the number of low bits that hold it; (None, 64) for
+        the first constant mode."""
         prev = [m for m in range(i) if m != k]
         if not prev:
-            return None
+            return None, 64
         strides = [0] * len(dims)
         span = 1
         for m in prev:
@@ -148,7 +149,7 @@ class Ops:
         if span >= (1 << 63):
             raise ValueError("walk grouping key overflows int64")
         self.row_keys(X, strides, out)
-        return out
+        return out, max(1, int(span).bit_length())
 
     def sts_rank_walk(self, node_grams, depth, P, leaf_rank, M, H, J, key, override, owner,
                       r_out, pmp_i):

@@ -297,7 +297,7 @@ def sts_sample(trees, k, J, gram_chain_pinv, grams, blocks_per_mode, seed, round
         ov = ov_all[i] if ov_all is not None else None
         H_in = None if first else H
         dims = [int(tt.block_hi.max()) if tt is not None else 1 for tt in trees]
-        hk = ops.walk_key(X, dims, k, i, hkey)
+        hk, kb = ops.walk_key(X, dims, k, i, hkey)
         depth = trees[i].depth
         if P > 1 and depth > 0:
             ops.sts_rank_walk(tr["node_grams"], depth, P, tr["leaf_rank"], M,
@@ -306,7 +306,8 @@ def sts_sample(trees, k, J, gram_chain_pinv, grams, blocks_per_mode, seed, round
                 if tr["trees"][p] is None:
                     continue
                 ops.sts_walk(tr["trees"][p], tr["U"][p], tr["leaves"][p], int(trees[i].block_lo[p]),
-                             M, H_in, J, key, None, rtop, owner, p, X[i], pmp[i], resid, hkey=hk)
+                             M, H_in, J, key, None, rtop, owner, p, X[i], pmp[i], resid, hkey=hk,
+                             key_bits=kb)
             # samples routed to a rank without rows (ref samplers.py:341-342)
             ops.status.check("in sts_sample")
             if bool((X[i] < 0).any()):
@@ -321,7 +322,8 @@ def sts_sample(trees, k, J, gram_chain_pinv, grams, blocks_per_mode, seed, round
             if tr["trees"][p] is None:
                 raise DegenerateWalkError("walk reached a rank with no rows")
             ops.sts_walk(tr["trees"][p], tr["U"][p], tr["leaves"][p], int(trees[i].block_lo[p]), M,
-                         H_in, J, key, ov, None, None, 0, X[i], pmp[i], resid, hkey=hk)
+                         H_in, J, key, ov, None, None, 0, X[i], pmp[i], resid, hkey=hk,
+                         key_bits=kb)
             ops.fold_rows(urow, tr["U"][p], int(trees[i].block_lo[p]), X[i], True)
         ops.hadamard_rows(H, urow, init=first)
         first = False
