@@ -17,6 +17,8 @@
 //     owned by one warp, fp64 red.add only for rows split across chunks.   [spmm]
 #include <limits.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -192,28 +194,46 @@ __global__ void lookup_kernel(const int64_t *__restrict__ keys, int64_t n_cols,
                               int64_t *__restrict__ dlo,
                               int64_t *__restrict__ dlen, double *__restrict__ Hs,
                               int64_t *__restrict__ stats) {
-  const int lane = threadIdx.x & 31;
-  const int64_t d = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  // persistent warps over the distinct fibers; the stats counters take one atomic per CTA
+  __shared__ unsigned long long cnt_ne[8], cnt_m[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t nS = S[0];
-  if (d >= nS) return;
-  int64_t lo = 0, len = 0;
-  const int64_t key = dkey[d];
-  const int64_t c = warp_lower_bound(keys, n_cols, key, lane);
-  if (lane == 0) {
-    if (c < n_cols && keys[c] == key) {
-      lo = colptr[c];
-      len = colptr[c + 1] - lo;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long ne = 0, nm = 0;
+  for (int64_t d = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; d < nS; d += nwarps) {
+    int64_t lo = 0, len = 0;
+    const int64_t key = dkey[d];
+    const int64_t c = warp_lower_bound(keys, n_cols, key, lane);
+    if (lane == 0) {
+      if (c < n_cols && keys[c] == key) {
+        lo = colptr[c];
+        len = colptr[c + 1] - lo;
+      }
+      dlo[d] = lo;
+      dlen[d] = len;
+      if (len > 0) {
+        ne += 1;
+        nm += (unsigned long long)(len * (int64_t)dcnt[d]);
+      }
     }
-    dlo[d] = lo;
-    dlen[d] = len;
-    if (len > 0) {
-      atomicAdd((unsigned long long *)&stats[1], 1ull);
-      atomicAdd((unsigned long long *)&stats[3], (unsigned long long)(len * (int64_t)dcnt[d]));
-    }
+    const int32_t rep = drep[d];
+    const double sc = dsc[d];
+    for (int q = lane; q < Rp; q += 32) Hs[d * Rp + q] = q < R ? sc * H[(int64_t)rep * R + q] : 0.0;
   }
-  const int32_t rep = drep[d];
-  const double sc = dsc[d];
-  for (int c = lane; c < Rp; c += 32) Hs[d * Rp + c] = c < R ? sc * H[(int64_t)rep * R + c] : 0.0;
+  if (lane == 0) {
+    cnt_ne[wid] = ne;
+    cnt_m[wid] = nm;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long a = 0, b = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += cnt_ne[w];
+      b += cnt_m[w];
+    }
+    if (a) atomicAdd((unsigned long long *)&stats[1], a);
+    if (b) atomicAdd((unsigned long long *)&stats[3], b);
+  }
 }
 
 __global__ void finalize_counts_kernel(const int64_t *__restrict__ S,
@@ -380,28 +400,43 @@ cta_hist_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp
   for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) mine[i] = hist[i];
 }
 
-__global__ void cta_prefix_kernel(int32_t *__restrict__ cmat, int G, int64_t n_rows,
-                                  int64_t *__restrict__ rcnt) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= n_rows) return;
+// Per row, exclusive prefix over the G CTA counts (in place) and the row total.  Four
+// threads per row each own a quarter of the CTAs (independent loads in flight), then the
+// quarters are offset by their predecessors' sums.
+constexpr int kPrefixSeg = 4;
+constexpr int kPrefixRows = 64;    // rows per 256-thread block
+constexpr int kPrefixMaxPer = 48;  // CTA counts one thread keeps in registers (G <= 192)
+
+__global__ void __launch_bounds__(kPrefixRows * kPrefixSeg)
+cta_prefix_kernel(int32_t *__restrict__ cmat, int G, int64_t n_rows, int64_t *__restrict__ rcnt) {
+  __shared__ int32_t seg_sum[kPrefixSeg][kPrefixRows];
+  const int rl = threadIdx.x % kPrefixRows, sg = threadIdx.x / kPrefixRows;
+  const int64_t r = blockIdx.x * (int64_t)kPrefixRows + rl;
+  const int per = (G + kPrefixSeg - 1) / kPrefixSeg;
+  const int c0 = sg * per, c1 = min(G, c0 + per);
+  int32_t v[kPrefixMaxPer];
+  int32_t sum = 0;
+#pragma unroll
+  for (int q = 0; q < kPrefixMaxPer; ++q) {
+    const int c = c0 + q;
+    v[q] = (r < n_rows && c < c1) ? cmat[(int64_t)c * n_rows + r] : 0;
+    sum += v[q];
+  }
+  seg_sum[sg][rl] = sum;
+  __syncthreads();
   int32_t run = 0;
-  int c = 0;
-  for (; c + 8 <= G; c += 8) {   // batch 8 independent loads before the dependent sums
-    int32_t v[8];
+  for (int q = 0; q < sg; ++q) run += seg_sum[q][rl];
+  if (r < n_rows) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = cmat[(int64_t)(c + q) * n_rows + r];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      cmat[(int64_t)(c + q) * n_rows + r] = run;
-      run += v[q];
+    for (int q = 0; q < kPrefixMaxPer; ++q) {
+      const int c = c0 + q;
+      if (c < c1) {
+        cmat[(int64_t)c * n_rows + r] = run;
+        run += v[q];
+      }
     }
+    if (sg == kPrefixSeg - 1) rcnt[r] = run;
   }
-  for (; c < G; ++c) {
-    const int32_t v = cmat[(int64_t)c * n_rows + r];
-    cmat[(int64_t)c * n_rows + r] = run;
-    run += v;
-  }
-  rcnt[r] = run;
 }
 
 __device__ __forceinline__ void put_entry(double2 *__restrict__ ent, int64_t o, int64_t d, double v) {
@@ -808,7 +843,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
                                             dkey, dcnt, drep, dsc, S);
   RCP_LAUNCH_CHECK("compact_write");
   // 2. lookup + scaled KRP rows
-  lookup_kernel<<<(unsigned)ceil_div(J * 32, 256), 256, 0, st>>>(
+  lookup_kernel<<<(unsigned)std::min<int64_t>(ceil_div(J * 32, 256), 8LL * sm_count()), 256, 0, st>>>(
       d_keys, n_cols, d_colptr, dkey, dcnt, drep, S, d_H, dsc, R, hs_stride(R), dlo, dlen, Hs,
       d_stats);
   RCP_LAUNCH_CHECK("lookup");
@@ -825,7 +860,8 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   rc = scan_i64_exclusive(icnt, ioff, J, S, scan_ws, st);
   if (rc) return rc;
   // 4. row histogram -> row pointers; 5. scatter into row order (packed entries)
-  const int priv = (n_rows <= kPrivRows && cap < (1LL << 31)) ? 1 : 0;
+  const int priv =
+      (n_rows <= kPrivRows && cap < (1LL << 31) && sm_count() <= kPrefixSeg * kPrefixMaxPer) ? 1 : 0;
   static bool attr = false;
   if (!attr) {
     RCP_CUDA_TRY(cudaFuncSetAttribute(cta_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -838,7 +874,8 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     const size_t smem = sizeof(int32_t) * n_rows;
     cta_hist_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, dlo, dlen, d_rows, n_rows, cmat);
     RCP_LAUNCH_CHECK("cta_hist");
-    cta_prefix_kernel<<<(unsigned)ceil_div(n_rows, 256), 256, 0, st>>>(cmat, grid, n_rows, rcnt);
+    cta_prefix_kernel<<<(unsigned)ceil_div(n_rows, kPrefixRows), kPrefixRows * kPrefixSeg, 0, st>>>(
+        cmat, grid, n_rows, rcnt);
     RCP_LAUNCH_CHECK("cta_prefix");
     rc = scan_i64_exclusive(rcnt, rptr, n_rows, nullptr, scan_ws, st);
     if (rc) return rc;

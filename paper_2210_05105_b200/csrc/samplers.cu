@@ -188,13 +188,32 @@ __global__ void sts_zero_kernel(double *__restrict__ p, int64_t len) {
     p[i] = 0.0;
 }
 
-__global__ void sts_level_kernel(const double *__restrict__ child, double *__restrict__ parent,
-                                 int64_t nodes, int Rt) {
+// Up to three tree levels per launch: thread (v, e) of the top level reads the 2^L
+// descendants of node v at the bottom level and writes every intermediate node, with the
+// same pairwise additions as a level-by-level pass.  Level l nodes start at 2^l - 1.
+__global__ void sts_levels_kernel(double *__restrict__ tree, int child_level, int L, int Rt) {
+  const int top = child_level - L;
+  const int64_t nodes = 1LL << top;
   const int64_t tot = nodes * Rt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = i / Rt, e = i % Rt;
-    parent[i] = child[(2 * v) * Rt + e] + child[(2 * v + 1) * Rt + e];
+    double acc[8];
+    const int w = 1 << L;
+    const double *ch = tree + ((1LL << child_level) - 1 + v * w) * Rt + e;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < w) acc[q] = ch[(int64_t)q * Rt];
+    for (int l = 1; l <= L; ++l) {           // level child_level - l
+      const int cnt = w >> l;
+      double *lvl = tree + ((1LL << (child_level - l)) - 1 + v * cnt) * Rt + e;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < cnt) {
+          acc[q] = acc[2 * q] + acc[2 * q + 1];
+          lvl[(int64_t)q * Rt] = acc[q];
+        }
+    }
   }
 }
 
@@ -388,14 +407,14 @@ int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
     sts_zero_kernel<<<(unsigned)b, 256, 0, st>>>(lvl + nleaves * Rt, len);
     RCP_LAUNCH_CHECK("sts_pad");
   }
-  for (int lev = depth - 1; lev >= 0; --lev) {
-    const int64_t nodes = 1LL << lev;
-    double *parent = d_tree + (nodes - 1) * (int64_t)Rt;
-    double *child = d_tree + (2 * nodes - 1) * (int64_t)Rt;
+  for (int cl = depth; cl > 0;) {
+    const int L = cl >= 3 ? 3 : cl;
+    const int64_t nodes = 1LL << (cl - L);
     int64_t b = ceil_div(nodes * Rt, 256);
     if (b > 8LL * sm_count()) b = 8LL * sm_count();
-    sts_level_kernel<<<(unsigned)b, 256, 0, st>>>(child, parent, nodes, Rt);
-    RCP_LAUNCH_CHECK("sts_level");
+    sts_levels_kernel<<<(unsigned)b, 256, 0, st>>>(d_tree, cl, L, Rt);
+    RCP_LAUNCH_CHECK("sts_levels");
+    cl -= L;
   }
   return RCP_OK;
 }
