@@ -45,13 +45,14 @@ int sm_count() {
 }
 
 constexpr int kMaxLeaf = 64;
-constexpr int kWalkWarps = 8;
+constexpr int kWalkWarps = 16;
 constexpr int kMaxDepth = 30;   // local tree depth limit (2^30 leaves)
 constexpr int kLeafBatch = 4;   // leaf rows whose masses one pass over the packed pairs makes
 // control words: [0] seeded runs, [2] samples finished, [3] participants,
 // [kGenBase + g] runs pushed during generation g (each generation has its own counter, so
 // the extent of generation g + 1 is stable once every CTA has passed the barrier)
 constexpr int kGenBase = 8;
+constexpr size_t kProfBytes = 16 * (kMaxDepth + 2);
 constexpr size_t kCtlBytes = sizeof(int) * (kGenBase + kMaxDepth + 8);
 
 struct Run {
@@ -59,13 +60,14 @@ struct Run {
   int32_t level;       // tree level of `node`
   int32_t node;        // node index within its level
   uint32_t dirs;       // bit l: direction taken at level l (1 = right)
-  int32_t pad;
+  int32_t rlev;        // levels [0, rlev) already applied to the samples' stored residuals
   double prob;         // product of the step probabilities so far
   double T[kMaxDepth]; // thresholds at levels 0 .. level-1
 };
 
 struct WalkWs {
-  size_t o_key, o_key2, o_r, o_r2, o_idx, o_idx2, o_runs, o_ctl, o_mp, o_pairs, o_gm, o_cub, total;
+  size_t o_key, o_key2, o_r, o_r2, o_idx, o_idx2, o_runs, o_ctl, o_mp, o_pairs, o_gm, o_cub, o_prof,
+      total;
   size_t cub_bytes;
   int64_t nruns;
   WalkWs(int64_t J, int depth, int R) {
@@ -96,14 +98,34 @@ struct WalkWs {
     o_pairs = add(4 * Rs);
     o_gm = add(8 * Rs * (size_t)((2LL << depth) - 1));   // G (.) M' for every tree node
     o_cub = add(cub_bytes + 256);
+    o_prof = add(kProfBytes);   // per level: global timer at the level start, runs
     total = t + 256;
   }
 };
 
-// Shared doubles per walker warp: h, a batch of leaf rows z = u (.) h, leaf masses, path.
+// Leaf masses on the fp64 tensor cores (mma.m8n8k4) when R <= kMmaMaxR: Y = Z M for a
+// tile of 8 leaf rows Z = U_leaf (.) h, mass_q = <Y_q, Z_q>.
+constexpr int kMmaMaxR = 64;
+__host__ __device__ __forceinline__ int mma_rn(int R) { return (R + 7) & ~7; }
+__host__ __device__ __forceinline__ int mma_zs(int R) { return mma_rn(R) + 2; }   // Z row stride
+
+// Shared doubles per walker warp: h, leaf rows z = u (.) h (a batch, or an 8-row mma
+// tile), leaf masses, path.
 __host__ __device__ __forceinline__ size_t walk_per_warp(int R) {
-  const size_t w = (size_t)(1 + kLeafBatch) * R + kMaxLeaf + kMaxDepth;
+  const size_t zb = R <= kMmaMaxR ? (size_t)8 * mma_zs(R) : (size_t)kLeafBatch * R;
+  const size_t w = (size_t)R + zb + kMaxLeaf + kMaxDepth;
   return (w + 1) & ~(size_t)1;
+}
+
+// Block-shared doubles: the full padded M (mma path) or packed M' (fallback).
+__host__ __device__ __forceinline__ size_t walk_block_doubles(int R) {
+  return R <= kMmaMaxR ? (size_t)mma_rn(R) * mma_rn(R) : (size_t)tri_stride(R);
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
 }
 
 __device__ __forceinline__ int ld_volatile(const int *p) { return *(volatile const int *)p; }
@@ -115,8 +137,10 @@ __device__ __forceinline__ double rescale(double r, double T, bool right) {
   return fmin(fmax(y, 0.0), one_below());
 }
 
-__device__ __forceinline__ double replay(double r, const double *T, uint32_t dirs, int level) {
-  for (int l = 0; l < level; ++l) r = rescale(r, T[l], (dirs >> l) & 1u);
+// Residual after levels [from, to) of the path, from the residual stored after level from.
+__device__ __forceinline__ double replay(double r, const double *T, uint32_t dirs, int from,
+                                         int to) {
+  for (int l = from; l < to; ++l) r = rescale(r, T[l], (dirs >> l) & 1u);
   return r;
 }
 
@@ -165,6 +189,7 @@ __global__ void walk_seed_kernel(const int64_t *__restrict__ key, const int32_t 
   rr.level = 0;
   rr.node = 0;
   rr.dirs = 0u;
+  rr.rlev = 0;
   // samples of one group share their rank-level path, hence this probability
   rr.prob = pmp_in ? pmp_in[idx[s]] : 1.0;
 }
@@ -216,11 +241,14 @@ __global__ void walk_gm_kernel(const double2 *__restrict__ tree, const double2 *
 // level's generation.  Runs entering the leaf level are cut into chunks so that the
 // per-sample leaf work spreads over warps.
 constexpr int32_t kLeafChunk = 256;
+// runs up to this size rescale their samples' stored residuals at every split (so deeper
+// levels need no replay); larger runs (top levels) leave it to their descendants
+constexpr int32_t kEagerRescale = 256;
 
 __device__ __forceinline__ void push_child(Run *runs, int *gen_cnt, int64_t base, int64_t cap,
                                            int *status, const Run &par, const double *Tp,
                                            int32_t lo, int32_t hi, double T, bool right,
-                                           int depth, int lane) {
+                                           int depth, int rlev, int lane) {
   const int lev = par.level;
   const int32_t chunk = (lev + 1 == depth) ? kLeafChunk : hi - lo;
   for (int32_t c0 = lo; c0 < hi; c0 += chunk) {
@@ -239,6 +267,7 @@ __device__ __forceinline__ void push_child(Run *runs, int *gen_cnt, int64_t base
       c.level = lev + 1;
       c.node = 2 * par.node + (right ? 1 : 0);
       c.dirs = par.dirs | ((right ? 1u : 0u) << lev);
+      c.rlev = rlev;
       c.prob = par.prob * (right ? (1.0 - T) : T);
       c.T[lev] = T;
     }
@@ -257,40 +286,63 @@ __device__ __forceinline__ void fail_run(int32_t lo, int32_t hi, const int32_t *
   }
 }
 
-__global__ void __launch_bounds__(kWalkWarps * 32)
+__global__ void __launch_bounds__(kWalkWarps * 32, 2)
 walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, int64_t n, int R,
                  int leaf, int depth, int64_t row_lo, const double *__restrict__ Mp_g,
+                 const double *__restrict__ Mfull,
                  const uint32_t *__restrict__ pairs_g, const double *__restrict__ H,
-                 const int32_t *__restrict__ idx, const double *__restrict__ r, Run *runs,
+                 const int32_t *__restrict__ idx, double *__restrict__ r, Run *runs,
                  int *ctl, int64_t cap_runs, int64_t *__restrict__ Xi, double *__restrict__ pmp,
-                 double *__restrict__ resid, int *status) {
+                 double *__restrict__ resid, int *status, unsigned long long *prof) {
   extern __shared__ double sh[];
   const int Rt = R * (R + 1) / 2;
   const int Rs = tri_stride(R);                    // even node stride (zero pad)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double *Mp = sh;                                 // Rs: packed M'
-  double *hv = Mp + Rs + (size_t)wid * walk_per_warp(R);   // R: the run's Hadamard row
-  double *zb = hv + R;                             // kLeafBatch x R: leaf rows (.) h
-  double *mass = zb + kLeafBatch * R;              // leaf
+  const bool use_mma = R <= kMmaMaxR;
+  const int Rn = mma_rn(R), Zs = mma_zs(R);
+  const size_t bd = walk_block_doubles(R);
+  double *Mp = sh;                                 // packed M' (fallback) or full M (mma)
+  double *hv = sh + bd + (size_t)wid * walk_per_warp(R);   // R: the run's Hadamard row
+  double *zb = hv + R;                             // leaf rows (.) h
+  double *mass = zb + (use_mma ? 8 * Zs : kLeafBatch * R);   // leaf
   double *Tp = mass + kMaxLeaf;                    // path thresholds of the current run
-  uint32_t *pairs = reinterpret_cast<uint32_t *>(Mp + Rs + (size_t)nw * walk_per_warp(R));
-  for (int e = threadIdx.x; e < Rs; e += blockDim.x) {
-    Mp[e] = Mp_g[e];
-    pairs[e] = pairs_g[e];
+  uint32_t *pairs = reinterpret_cast<uint32_t *>(sh + bd + (size_t)nw * walk_per_warp(R));
+  for (int e = threadIdx.x; e < Rs; e += blockDim.x) pairs[e] = pairs_g[e];
+  if (use_mma) {
+    for (int e = threadIdx.x; e < Rn * Rn; e += blockDim.x) {
+      const int k = e / Rn, c = e - k * Rn;
+      Mp[e] = (k < R && c < R) ? Mfull[k * R + c] : 0.0;
+    }
+  } else {
+    for (int e = threadIdx.x; e < Rs; e += blockDim.x) Mp[e] = Mp_g[e];
   }
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
-  const int64_t gwarp = (int64_t)blockIdx.x * nw + wid;
-  const int64_t nwarps = (int64_t)gridDim.x * nw;
   // Level-synchronous: the runs of level l are [begin, end); their children go to level
   // l + 1 through that level's own counter, whose value is stable after the grid barrier.
+  __shared__ int claim;
   int64_t begin = 0, end = min((int64_t)ld_volatile(&ctl[0]), cap_runs);
   for (int lvl = 0; lvl <= depth && end > begin; ++lvl) {
     int *gen_cnt = &ctl[kGenBase + lvl];
-    for (int64_t t = begin + gwarp; t < end; t += nwarps) {
+    // this CTA's runs begin + blockIdx.x + k gridDim.x (spread over the level), claimed one
+    // by one by its warps
+    if (threadIdx.x == 0) claim = 0;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {   // level start time and run count
+      unsigned long long tnow;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+      prof[2 * lvl] = tnow;
+      prof[2 * lvl + 1] = (unsigned long long)(end - begin);
+    }
+    __syncthreads();
+    while (true) {
+      int tc = 0;
+      if (lane == 0) tc = atomicAdd(&claim, 1);
+      const int64_t t = begin + blockIdx.x + (int64_t)__shfl_sync(0xffffffffu, tc, 0) * gridDim.x;
+      if (t >= end) break;
       const Run &run = runs[t];
       const int32_t lo = run.lo, hi = run.hi, level = run.level;
       const uint32_t dirs = run.dirs;
+      const int rlev = run.rlev;
       if (lane < level) Tp[lane] = run.T[lane];
       const int32_t s0 = idx[lo];
       for (int c = lane; c < R; c += 32) hv[c] = H ? H[(int64_t)s0 * R + c] : 1.0;
@@ -336,7 +388,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
           const int32_t step = (span + 31) / 32;
           const int32_t pos = a + lane * step;
           bool ge = true;   // "replayed r >= T" at pos (positions >= b count as true)
-          if (pos < b) ge = replay(r[pos], Tp, dirs, level) >= T;
+          if (pos < b) ge = replay(r[pos], Tp, dirs, rlev, level) >= T;
           const unsigned m = __ballot_sync(0xffffffffu, ge);
           if (m == 0u) {                     // every probe < T: answer beyond the last probe
             a = a + 31 * step + 1;
@@ -352,12 +404,18 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
           }
         }
         const int32_t nl = a - lo;
+        int crlev = rlev;
+        if (hi - lo <= kEagerRescale) {   // bring the stored residuals past this level
+          for (int32_t q = lo + lane; q < hi; q += 32)
+            r[q] = rescale(replay(r[q], Tp, dirs, rlev, level), T, q >= lo + nl);
+          crlev = level + 1;
+        }
         if (nl > 0)
           push_child(runs, gen_cnt, end, cap_runs, status, run, Tp, lo, lo + nl, T, false, depth,
-                     lane);
+                     crlev, lane);
         if (hi - lo - nl > 0)
           push_child(runs, gen_cnt, end, cap_runs, status, run, Tp, lo + nl, hi, T, true, depth,
-                     lane);
+                     crlev, lane);
         continue;
       }
       // ---- leaf block: masses z^T M' z of its rows z = u (.) h, then each sample's
@@ -367,7 +425,31 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
       const double rprob = run.prob;
       bool bad = nrow <= 0;
       double total_m = 0.0;
-      if (!bad) {
+      if (!bad && use_mma) {
+        // 8-row tiles: Y = Z M on the fp64 tensor cores, mass_q = <Y_q, Z_q>
+        const int row = lane >> 2, quad = lane & 3;
+        for (int q0 = 0; q0 < nrow; q0 += 8) {
+          const int nb = min(8, nrow - q0);
+          for (int c = lane; c < 8 * Zs; c += 32) {
+            const int j = c / Zs, col = c - j * Zs;
+            zb[c] = (j < nb && col < R) ? U[(r0 + q0 + j) * R + col] * hv[col] : 0.0;
+          }
+          __syncwarp();
+          const double *zr = zb + row * Zs;
+          double msum = 0.0;
+          for (int nt = 0; nt < Rn; nt += 8) {
+            double c0 = 0.0, c1 = 0.0;
+            for (int ks = 0; ks < Rn; ks += 4)
+              dmma_8x8x4(c0, c1, zr[ks + quad], Mp[(ks + quad) * Rn + nt + row]);
+            msum = fma(c0, zr[nt + 2 * quad], msum);
+            msum = fma(c1, zr[nt + 2 * quad + 1], msum);
+          }
+          msum += __shfl_xor_sync(0xffffffffu, msum, 1);
+          msum += __shfl_xor_sync(0xffffffffu, msum, 2);
+          if (quad == 0 && row < nb) mass[q0 + row] = msum > 0.0 ? msum : 0.0;
+          __syncwarp();
+        }
+      } else if (!bad) {
         for (int q0 = 0; q0 < nrow; q0 += kLeafBatch) {
           const int nb = min(kLeafBatch, nrow - q0);
           for (int c = lane; c < nb * R; c += 32) {
@@ -395,6 +477,8 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
           }
           __syncwarp();
         }
+      }
+      if (!bad) {
         if (lane == 0)
           for (int q = 0; q < nrow; ++q) total_m += mass[q];
         total_m = __shfl_sync(0xffffffffu, total_m, 0);
@@ -405,7 +489,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         continue;
       }
       for (int32_t s = lo + lane; s < hi; s += 32) {
-        const double target = replay(r[s], Tp, dirs, level) * total_m;
+        const double target = replay(r[s], Tp, dirs, rlev, level) * total_m;
         double cdf = 0.0;
         int cnt = 0;
         for (int q = 0; q < nrow; ++q) {
@@ -431,6 +515,11 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
     begin = end;
     end = min(end + pushed_n, cap_runs);
   }
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long tnow;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+    prof[2 * (kMaxDepth + 1)] = tnow;
+  }
 }
 
 // out[s,:] = U[X_i[s]-row_lo, :] (init) or out[s,:] *= U[...] for the selected samples:
@@ -450,7 +539,7 @@ __global__ void fold_rows_kernel(double *__restrict__ out, const double *__restr
 }
 
 size_t walk_smem(int R, int warps) {
-  return sizeof(double) * ((size_t)tri_stride(R) + (size_t)warps * walk_per_warp(R)) +
+  return sizeof(double) * (walk_block_doubles(R) + (size_t)warps * walk_per_warp(R)) +
          sizeof(uint32_t) * (size_t)tri_stride(R) + 64;
 }
 
@@ -512,6 +601,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   walk_gather_kernel<<<gb, 256, 0, st>>>((const int64_t *)r, idx, J, (int64_t *)r2);
   RCP_LAUNCH_CHECK("walk_gather_r");
   RCP_CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlBytes, st));
+  RCP_CUDA_TRY(cudaMemsetAsync(w + L.o_prof, 0, kProfBytes, st));
   walk_seed_kernel<<<gb, 256, 0, st>>>(key, idx, J, d_sel ? d_pmp_i : nullptr, runs, ctl);
   RCP_LAUNCH_CHECK("walk_seed");
   // this walk's M' tables and G (.) M' for every node
@@ -539,17 +629,19 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   // persistent: every CTA resident at once (workers wait on the shared queue)
   const int grid = per_sm * sm_count();
   // cooperative launch: every CTA co-resident, grid-wide barrier between tree levels
-  const double *a_gm = gm, *a_U = d_U, *a_Mp = Mp, *a_H = d_H_in;
+  const double *a_gm = gm, *a_U = d_U, *a_Mp = Mp, *a_H = d_H_in, *a_Mf = d_M;
   const uint32_t *a_pairs = pairs;
   const int32_t *a_idx = idx;
-  const double *a_r = r2;
+  double *a_r = r2;
+  unsigned long long *a_prof = (unsigned long long *)(w + L.o_prof);
   int64_t a_n = n, a_row_lo = row_lo, a_cap = L.nruns;
   int a_R = R, a_leaf = leaf, a_depth = depth;
   void *args[] = {(void *)&a_gm, (void *)&a_U, (void *)&a_n, (void *)&a_R, (void *)&a_leaf,
-                  (void *)&a_depth, (void *)&a_row_lo, (void *)&a_Mp, (void *)&a_pairs,
+                  (void *)&a_depth, (void *)&a_row_lo, (void *)&a_Mp, (void *)&a_Mf,
+                  (void *)&a_pairs,
                   (void *)&a_H, (void *)&a_idx, (void *)&a_r, (void *)&runs, (void *)&ctl,
                   (void *)&a_cap, (void *)&d_Xi, (void *)&d_pmp_i, (void *)&d_resid,
-                  (void *)&d_status};
+                  (void *)&d_status, (void *)&a_prof};
   RCP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)walk_runs_kernel, dim3(grid),
                                            dim3(warps * 32), args, smem, st));
   RCP_LAUNCH_CHECK("walk_runs");
