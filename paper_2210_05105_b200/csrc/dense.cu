@@ -1,6 +1,8 @@
 // Small dense fp64 algebra on the hot path: Gram matrices, the R x R pseudo-inverse,
 // the factor update GEMM with its column norms, renormalisation, sample weights.
 // Ref: linalg.py:64-111, schedules.py:104-128, samplers.py:89-96, als.py:129-138.
+#include <algorithm>
+
 #include "common.cuh"
 
 using namespace rcp;
@@ -546,6 +548,98 @@ pinv_kernel(const double *__restrict__ in, int n_chain, int skip, int R, double 
 // ------------------------------------------------------------------- update GEMM
 constexpr int kUpdThreads = 256;
 
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// U = M B on the fp64 tensor cores (mma.m8n8k4), R <= 64: each warp takes 8-row tiles of
+// M (staged in shared memory, zero padded to Rn = R rounded up to 8), keeps the tile's A
+// fragments in registers and sweeps the n-tiles of B (block-shared, padded).  Column sums
+// of squares per lane -> fixed-order warp/CTA reduction (deterministic).
+template <int KS>   // k-steps = Rn / 4
+__global__ void __launch_bounds__(kUpdThreads)
+update_mma_kernel(const double *__restrict__ M, int64_t n, int R, const double *__restrict__ B,
+                  double *__restrict__ U, double *__restrict__ part, int *status) {
+  extern __shared__ double sh[];
+  const int Rn = KS * 4;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int row = lane >> 2, quad = lane & 3;
+  double *Bs = sh;                                   // Rn x Rn
+  double *Ms = sh + Rn * Rn + (size_t)wid * 8 * Rn;  // per warp: 8 x Rn
+  for (int e = threadIdx.x; e < Rn * Rn; e += blockDim.x) {
+    const int k = e / Rn, c = e - k * Rn;
+    Bs[e] = (k < R && c < R) ? B[k * R + c] : 0.0;
+  }
+  __syncthreads();
+  double sq[KS / 2][2];   // this lane's columns nt*8 + 2 quad + {0,1}, nt < Rn/8
+#pragma unroll
+  for (int t = 0; t < KS / 2; ++t) sq[t][0] = sq[t][1] = 0.0;
+  bool bad = false;
+  const int64_t ntiles = ceil_div(n, (int64_t)8);
+  for (int64_t tile = (int64_t)blockIdx.x * nw + wid; tile < ntiles;
+       tile += (int64_t)gridDim.x * nw) {
+    const int64_t r0 = tile * 8;
+    const int nr = (int)min((int64_t)8, n - r0);
+    __syncwarp();
+    for (int e = lane; e < 8 * Rn; e += 32) {
+      const int q = e / Rn, c = e - q * Rn;
+      Ms[e] = (q < nr && c < R) ? M[(r0 + q) * R + c] : 0.0;
+    }
+    __syncwarp();
+    double a[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) a[ks] = Ms[row * Rn + ks * 4 + quad];
+#pragma unroll
+    for (int nt = 0; nt < KS / 2; ++nt) {
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) dmma_8x8x4(c0, c1, a[ks], Bs[(ks * 4 + quad) * Rn + nt * 8 + row]);
+      const int col = nt * 8 + 2 * quad;
+      if (row < nr) {
+        if (col < R) {
+          U[(r0 + row) * R + col] = c0;
+          sq[nt][0] = fma(c0, c0, sq[nt][0]);
+          if (!isfinite(c0)) bad = true;
+        }
+        if (col + 1 < R) {
+          U[(r0 + row) * R + col + 1] = c1;
+          sq[nt][1] = fma(c1, c1, sq[nt][1]);
+          if (!isfinite(c1)) bad = true;
+        }
+      }
+    }
+  }
+  if (bad) raise_status(status, RCP_ST_NONFINITE);
+  // lanes with equal quad hold the same columns: reduce over the 8 rows, then warps
+#pragma unroll
+  for (int nt = 0; nt < KS / 2; ++nt)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      double v = sq[nt][u];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      sq[nt][u] = v;
+    }
+  __syncthreads();
+  double *wsq = sh;   // reuse: nw x Rn
+  if (row == 0) {
+#pragma unroll
+    for (int nt = 0; nt < KS / 2; ++nt) {
+      wsq[wid * Rn + nt * 8 + 2 * quad] = sq[nt][0];
+      wsq[wid * Rn + nt * 8 + 2 * quad + 1] = sq[nt][1];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < R; c += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < nw; ++w) v += wsq[w * Rn + c];
+    part[(int64_t)blockIdx.x * R + c] = v;
+  }
+}
+
 template <int RPL>
 __global__ void __launch_bounds__(kUpdThreads)
 update_kernel(const double *__restrict__ M, int64_t n, int R, const double *__restrict__ B,
@@ -735,6 +829,37 @@ int rcp_update(const double *d_M, int64_t n, int R, const double *d_B, double *d
     attr = true;
   }
   double *part = (double *)d_ws;
+  if (R <= 64) {   // fp64 tensor cores
+    static bool attr_mma = false;
+    if (!attr_mma) {
+#define RCP_UPD_ATTR(K)                                                                  \
+  RCP_CUDA_TRY(cudaFuncSetAttribute(update_mma_kernel<K>,                                \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024))
+      RCP_UPD_ATTR(2); RCP_UPD_ATTR(4); RCP_UPD_ATTR(6); RCP_UPD_ATTR(8);
+      RCP_UPD_ATTR(10); RCP_UPD_ATTR(12); RCP_UPD_ATTR(14); RCP_UPD_ATTR(16);
+#undef RCP_UPD_ATTR
+      attr_mma = true;
+    }
+    const int Rn = (R + 7) & ~7;
+    const int ks = Rn / 4;
+    int64_t tiles = ceil_div(n, (int64_t)8);
+    int g = (int)std::min<int64_t>(ceil_div(tiles, (int64_t)nw), 4LL * sm_count());
+    const size_t sm2 = sizeof(double) * ((size_t)Rn * Rn + (size_t)nw * 8 * Rn);
+    switch (ks) {
+      case 2: update_mma_kernel<2><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 4: update_mma_kernel<4><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 6: update_mma_kernel<6><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 8: update_mma_kernel<8><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 10: update_mma_kernel<10><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 12: update_mma_kernel<12><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 14: update_mma_kernel<14><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      default: update_mma_kernel<16><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+    }
+    RCP_LAUNCH_CHECK("update_mma");
+    sum_partials_kernel<<<(unsigned)ceil_div(R, 32), 256, 0, st>>>(part, g, R, d_colsq);
+    RCP_LAUNCH_CHECK("update_colsq");
+    return RCP_OK;
+  }
   switch ((R + 31) / 32) {
     case 1: update_kernel<1><<<grid, kUpdThreads, smem, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
     case 2: update_kernel<2><<<grid, kUpdThreads, smem, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;

@@ -272,15 +272,24 @@ __global__ void item_count_kernel(const int64_t *__restrict__ dlen, const int64_
   if (d < Sp[0]) icnt[d] = ceil_div(dlen[d], kItemE);
 }
 
+// item -> fiber table: fiber d owns items [ioff[d], ioff[d+1])
+__global__ void item_fill_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                                 int32_t *__restrict__ ifib) {
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= Sp[0]) return;
+  for (int64_t it = ioff[d]; it < ioff[d + 1]; ++it) ifib[it] = (int32_t)d;
+}
+
 struct ItemSpan {
   int64_t d, a, b;   // fiber, store range [a, b)
 };
 
-__device__ __forceinline__ ItemSpan item_span(int64_t it, const int64_t *__restrict__ ioff, int64_t S,
+__device__ __forceinline__ ItemSpan item_span(int64_t it, const int64_t *__restrict__ ioff,
+                                              const int32_t *__restrict__ ifib,
                                               const int64_t *__restrict__ dlo,
                                               const int64_t *__restrict__ dlen) {
   ItemSpan sp;
-  sp.d = floor_index(ioff, S + 1, it);   // last fiber whose first item <= it (skips empties)
+  sp.d = ifib[it];   // fiber of the item (table filled by item_fill_kernel)
   const int64_t c = it - ioff[sp.d];
   const int64_t base = dlo[sp.d];
   sp.a = base + c * kItemE;
@@ -296,6 +305,7 @@ __device__ __forceinline__ void cta_items(int64_t n_items, int64_t &i0, int64_t 
 
 __global__ void __launch_bounds__(kTraverseThreads)
 row_count_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                 const int32_t *__restrict__ ifib,
                  const int64_t *__restrict__ dlo, const int64_t *__restrict__ dlen,
                  const int32_t *__restrict__ rows, int64_t n_rows, int priv,
                  int64_t *__restrict__ rcnt) {
@@ -310,7 +320,7 @@ row_count_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ S
     __syncthreads();
   }
   for (int64_t it = i0 + wid; it < i1; it += nw) {
-    const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
+    const ItemSpan sp = item_span(it, ioff, ifib, dlo, dlen);
     for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32) {
       const int32_t row = rows[pos];
       if (priv) atomicAdd(&hist[row], 1);
@@ -326,6 +336,7 @@ row_count_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ S
 
 __global__ void __launch_bounds__(kTraverseThreads)
 scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                 const int32_t *__restrict__ ifib,
                const int64_t *__restrict__ dlo, const int64_t *__restrict__ dlen,
                const int32_t *__restrict__ rows, const double *__restrict__ vals, int64_t n_rows,
                int priv, const int64_t *__restrict__ rptr, int64_t *__restrict__ rcur,
@@ -341,7 +352,7 @@ scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
     for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     for (int64_t it = i0 + wid; it < i1; it += nw) {
-      const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
+      const ItemSpan sp = item_span(it, ioff, ifib, dlo, dlen);
       for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32) atomicAdd(&hist[rows[pos]], 1);
     }
     __syncthreads();
@@ -352,7 +363,7 @@ scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
     __syncthreads();
   }
   for (int64_t it = i0 + wid; it < i1; it += nw) {
-    const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
+    const ItemSpan sp = item_span(it, ioff, ifib, dlo, dlen);
     for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32) {
       const int32_t row = rows[pos];
       const double v = vals[pos];
@@ -375,6 +386,7 @@ scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
 //  3. after the row scan, CTA c writes its entries of row r at rptr[r] + cmat[c][r] + k.
 __global__ void __launch_bounds__(kTraverseThreads)
 cta_hist_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                 const int32_t *__restrict__ ifib,
                 const int64_t *__restrict__ dlo, const int64_t *__restrict__ dlen,
                 const int32_t *__restrict__ rows, int64_t n_rows, int32_t *__restrict__ cmat) {
   extern __shared__ int32_t hist[];
@@ -385,7 +397,7 @@ cta_hist_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int64_t it = i0 + wid; it < i1; it += nw) {
-    const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
+    const ItemSpan sp = item_span(it, ioff, ifib, dlo, dlen);
     for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32 * kInFlight) {
       int32_t rw[kInFlight];
 #pragma unroll
@@ -445,6 +457,7 @@ __device__ __forceinline__ void put_entry(double2 *__restrict__ ent, int64_t o, 
 
 __global__ void __launch_bounds__(kTraverseThreads)
 cta_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                   const int32_t *__restrict__ ifib,
                    const int64_t *__restrict__ dlo, const int64_t *__restrict__ dlen,
                    const int32_t *__restrict__ rows, const double *__restrict__ vals,
                    int64_t n_rows, const int64_t *__restrict__ rptr,
@@ -459,7 +472,7 @@ cta_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int64_t it = i0 + wid; it < i1; it += nw) {
-    const ItemSpan sp = item_span(it, ioff, S, dlo, dlen);
+    const ItemSpan sp = item_span(it, ioff, ifib, dlo, dlen);
     for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32 * kInFlight) {
       // issue every load of the batch before the dependent cursor atomics and stores
       int32_t rw[kInFlight];
@@ -570,8 +583,8 @@ spmm_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__r
 template <int NP>
 __global__ void __launch_bounds__(256)
 spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__restrict__ nnzp,
-                   const double2 *__restrict__ ent, const double *__restrict__ Hs, int R,
-                   double *__restrict__ out) {
+                   const double2 *__restrict__ ent,
+                   const double *__restrict__ Hs, int R, double *__restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int Rp = hs_stride(R);
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -583,7 +596,7 @@ spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64
   for (int64_t ch = warp0; ch < nchunks; ch += nwarps) {
     const int64_t c0 = ch * kSpmmChunk;
     const int64_t c1 = min(c0 + kSpmmChunk, nnz);
-    int64_t row = floor_index(rptr, n_rows + 1, c0);
+    int64_t row = floor_index(rptr, n_rows + 1, c0);   // (top levels stay in L1)
     int64_t e = c0;
     while (e < c1) {
       const int64_t rs = rptr[row], re = rptr[row + 1];
@@ -718,7 +731,8 @@ struct Ws {
 struct MttkrpLayout {
   int64_t T;
   size_t o_tkey, o_tcnt, o_trep, o_twmin, o_twmax, o_twsum, o_dsc, o_bcnt, o_dkey, o_dcnt,
-      o_drep, o_dlo, o_dlen, o_doff, o_ioff, o_Hs, o_scan, o_rcnt, o_rptr, o_cmat, o_ent, o_S,
+      o_drep, o_dlo, o_dlen, o_doff, o_ioff, o_ifib, o_Hs, o_scan, o_rcnt, o_rptr, o_cmat,
+      o_ent, o_S,
       o_nnz;
   size_t total;
   MttkrpLayout(int64_t J, int64_t cap, int64_t n_rows, int R) {
@@ -740,6 +754,7 @@ struct MttkrpLayout {
     o_dlen = w.add(sizeof(int64_t) * (J + 1));
     o_doff = w.add(sizeof(int64_t) * (J + 2));
     o_ioff = w.add(sizeof(int64_t) * (J + 2));
+    o_ifib = w.add(sizeof(int32_t) * (J + cap / kItemE + 2));     // items <= S + nnz / kItemE
     o_Hs = w.add(sizeof(double) * (size_t)(J + 1) * hs_stride(R));
     int64_t sc = J + 1 > n_rows + 1 ? J + 1 : n_rows + 1;
     o_scan = w.add(scan_ws_bytes(sc));
@@ -795,7 +810,8 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
                        int64_t *d_stats, void *d_ws, size_t ws_bytes, int *d_status,
                        void *stream) {
   if (N < 2 || N > kMaxModes || k < 0 || k >= N || R < 1 || R > RCP_MAX_RANK || J < 0 ||
-      n_rows < 0 || n_cols < 0 || !h_strides || !d_stats)
+      J >= (1LL << 26) || n_rows < 0 || n_rows >= (1LL << 31) || n_cols < 0 || !h_strides ||
+      !d_stats)
     return RCP_ERR_ARG;
   cudaStream_t st = RCP_STREAM(stream);
   if (n_rows > 0) RCP_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(double) * n_rows * R, st));
@@ -859,6 +875,9 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   RCP_LAUNCH_CHECK("item_count");
   rc = scan_i64_exclusive(icnt, ioff, J, S, scan_ws, st);
   if (rc) return rc;
+  int32_t *ifib = (int32_t *)P(L.o_ifib);
+  item_fill_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(ioff, S, ifib);
+  RCP_LAUNCH_CHECK("item_fill");
   // 4. row histogram -> row pointers; 5. scatter into row order (packed entries)
   const int priv =
       (n_rows <= kPrivRows && cap < (1LL << 31) && sm_count() <= kPrefixSeg * kPrefixMaxPer) ? 1 : 0;
@@ -872,19 +891,19 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   if (priv) {
     int32_t *cmat = (int32_t *)P(L.o_cmat);
     const size_t smem = sizeof(int32_t) * n_rows;
-    cta_hist_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, dlo, dlen, d_rows, n_rows, cmat);
+    cta_hist_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, ifib, dlo, dlen, d_rows, n_rows, cmat);
     RCP_LAUNCH_CHECK("cta_hist");
     cta_prefix_kernel<<<(unsigned)ceil_div(n_rows, kPrefixRows), kPrefixRows * kPrefixSeg, 0, st>>>(
         cmat, grid, n_rows, rcnt);
     RCP_LAUNCH_CHECK("cta_prefix");
     rc = scan_i64_exclusive(rcnt, rptr, n_rows, nullptr, scan_ws, st);
     if (rc) return rc;
-    cta_scatter_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, dlo, dlen, d_rows, d_vals,
+    cta_scatter_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, ifib, dlo, dlen, d_rows, d_vals,
                                                              n_rows, rptr, cmat, ent, cap, d_status);
     RCP_LAUNCH_CHECK("cta_scatter");
   } else {
     RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
-    row_count_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, dlo, dlen, d_rows, n_rows, 0, rcnt);
+    row_count_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, n_rows, 0, rcnt);
     RCP_LAUNCH_CHECK("row_count");
     rc = scan_i64_exclusive(rcnt, rptr, n_rows, nullptr, scan_ws, st);
     if (rc) return rc;
@@ -897,7 +916,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   }
   if (!priv) {   // global per-row cursors (rcnt reused)
     RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
-    scatter_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, dlo, dlen, d_rows, d_vals, n_rows, 0,
+    scatter_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, d_vals, n_rows, 0,
                                                       rptr, rcnt, ent, cap, d_status);
     RCP_LAUNCH_CHECK("scatter");
   }

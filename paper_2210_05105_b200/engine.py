@@ -95,6 +95,7 @@ class RankState:
         self.grams = t.zeros((N, R, R), **f64)
         self.block_grams = [None] * N          # (P, R, R) per mode (P > 1)
         self.trees = [None] * N
+        self.tree_stale = [True] * N
         self.rank_tree = [None] * N            # (node_grams, leaf_rank, depth) per mode
         self.dist = [None] * N
         self.cdf = [None] * N
@@ -170,10 +171,18 @@ class RankState:
             self.block_grams[k] = torch().stack([b for b in blocks])
 
     def build_tree(self, k):
-        if self.n[k] > 0:
-            self.trees[k] = self.ops.sts_build(self.U[k], self.leaf_of(k), self.trees[k])
+        """Mark the local tree of mode k stale (it is rebuilt on its first walk: at P = 1 the
+        first constant mode draws from a flat CDF, so mode 0's tree is never walked there)
+        and rebuild the small rank-level tree."""
+        self.tree_stale[k] = True
         if self.P > 1:
             self._build_rank_tree(k)
+
+    def local_tree(self, k):
+        if self.tree_stale[k] and self.n[k] > 0:
+            self.trees[k] = self.ops.sts_build(self.U[k], self.leaf_of(k), self.trees[k])
+        self.tree_stale[k] = False
+        return self.trees[k]
 
     def _build_rank_tree(self, k):
         """Padded complete tree over ranks in global row order (ref samplers.py:239-275)."""
@@ -242,7 +251,7 @@ class RankState:
             return
         if self.n[i] > 0:
             hk, kb = ops.walk_key(self.X, self.dims, k, i, self.hkey)
-            ops.sts_walk(self.trees[i], self.U[i], self.leaf_of(i), self.lo[i], self.M, H_in,
+            ops.sts_walk(self.local_tree(i), self.U[i], self.leaf_of(i), self.lo[i], self.M, H_in,
                          self.J, key, override if self.P == 1 else None, rin, sel, self.rank,
                          self.X[i], self.pmp[i], self.resid, hkey=hk, key_bits=kb)
             if self.P == 1:     # fold straight into the running Hadamard rows
