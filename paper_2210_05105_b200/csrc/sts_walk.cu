@@ -7,22 +7,18 @@
 // rows' masses (u (.) h)^T M (u (.) h).
 //
 // Samples whose running Hadamard rows h are equal (equal indices in the already-sampled
-// modes) see identical node masses.  Sorting the samples by (key of those indices, r)
-// makes each such group contiguous and ordered by r; at every node the left-goers are a
-// prefix of the group.  A group at a node is a *run* [lo, hi) of the sorted array: its
-// masses are computed once, the split point is found by a 32-ary warp search, and the run
-// splits into a left and a right run.  A run carries its path (thresholds T and directions
-// from the root) and the product of its step probabilities, which all its samples share,
-// so no per-sample state is touched above the leaves: a sample's rescaled residual at any
-// level is recomputed from its uniform by replaying the path's rescalings in the
-// reference's order.  Work is proportional to the number of distinct (h, node) pairs,
-// not samples x levels.
+// modes) see identical node masses.  Sorting the samples by the key of those indices makes
+// each such group contiguous.  A group at a node is a *run* [lo, hi) of the array: its
+// child masses are computed once; its samples' residuals r are compared with the split
+// T = qL / (qL + qR), rescaled exactly as the reference does (ref samplers.py:436-440), and
+// partitioned into the left and right child runs of the next level (double-buffered
+// (r, sample) arrays).  Work is proportional to the number of distinct (h, node) pairs
+// plus one pass over the samples per level.
 //
 // Per walk, every node Gram is multiplied once by the packed conditioning matrix M'
-// (GM = G (.) M'), so a child mass is <GM_child, h h^T> with h read from shared memory:
-// no per-run R x R staging, and a walker warp needs only ~(5R + 100) doubles of shared
-// memory, so many warps per SM hide the L2 latency of the node reads.  The levels are
-// processed by one cooperative launch with a grid barrier between levels.
+// (GM = G (.) M'), so a child mass is <GM_child, h h^T> with h read from shared memory.
+// Leaf row masses z^T M z (z = u (.) h) run on the fp64 tensor cores for R <= 64.  The
+// levels are processed by one cooperative launch with a grid barrier between levels.
 #include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <float.h>
@@ -45,6 +41,12 @@ int sm_count() {
 }
 
 constexpr int kMaxLeaf = 64;
+// Runs entering the leaf level are cut into chunks so that the per-sample leaf work
+// spreads over warps; longer runs elsewhere are cut into pieces of at most kMaxRun samples
+// (same key, same node): each piece recomputes the same child masses, but no warp
+// partitions more than kMaxRun samples.
+constexpr int32_t kLeafChunk = 256;
+constexpr int32_t kMaxRun = 1024;
 constexpr int kWalkWarps = 16;
 constexpr int kMaxDepth = 30;   // local tree depth limit (2^30 leaves)
 constexpr int kLeafBatch = 4;   // leaf rows whose masses one pass over the packed pairs makes
@@ -56,24 +58,19 @@ constexpr size_t kProfBytes = 16 * (kMaxDepth + 2);
 constexpr size_t kCtlBytes = sizeof(int) * (kGenBase + kMaxDepth + 8);
 
 struct Run {
-  int32_t lo, hi;      // sorted positions [lo, hi)
+  int32_t lo, hi;      // positions [lo, hi) in the level's (r, sample) buffer
   int32_t level;       // tree level of `node`
   int32_t node;        // node index within its level
-  uint32_t dirs;       // bit l: direction taken at level l (1 = right)
-  int32_t rlev;        // levels [0, rlev) already applied to the samples' stored residuals
   double prob;         // product of the step probabilities so far
-  double T[kMaxDepth]; // thresholds at levels 0 .. level-1
 };
 
 struct WalkWs {
-  size_t o_key, o_key2, o_r, o_r2, o_idx, o_idx2, o_runs, o_ctl, o_mp, o_pairs, o_gm, o_cub, o_prof,
-      total;
+  size_t o_key, o_key2, o_r, o_r2, o_idx, o_idx2, o_idx3, o_runs, o_ctl, o_mp, o_pairs, o_gm,
+      o_cub, o_prof, total;
   size_t cub_bytes;
   int64_t nruns;
   WalkWs(int64_t J, int depth, int R) {
     size_t b1 = 0, b2 = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, b1, (const double *)nullptr, (double *)nullptr,
-                                    (const int32_t *)nullptr, (int32_t *)nullptr, (int)J);
     cub::DeviceRadixSort::SortPairs(nullptr, b2, (const int64_t *)nullptr, (int64_t *)nullptr,
                                     (const int32_t *)nullptr, (int32_t *)nullptr, (int)J);
     cub_bytes = b1 > b2 ? b1 : b2;
@@ -92,6 +89,7 @@ struct WalkWs {
     o_r2 = add(8 * J);
     o_idx = add(4 * J);
     o_idx2 = add(4 * J);
+    o_idx3 = add(4 * J);
     o_runs = add(sizeof(Run) * nruns);
     o_ctl = add(kCtlBytes);
     o_mp = add(8 * Rs);
@@ -113,7 +111,7 @@ __host__ __device__ __forceinline__ int mma_zs(int R) { return mma_rn(R) + 2; } 
 // tile), leaf masses, path.
 __host__ __device__ __forceinline__ size_t walk_per_warp(int R) {
   const size_t zb = R <= kMmaMaxR ? (size_t)8 * mma_zs(R) : (size_t)kLeafBatch * R;
-  const size_t w = (size_t)R + zb + kMaxLeaf + kMaxDepth;
+  const size_t w = (size_t)R + zb + kMaxLeaf;
   return (w + 1) & ~(size_t)1;
 }
 
@@ -137,34 +135,28 @@ __device__ __forceinline__ double rescale(double r, double T, bool right) {
   return fmin(fmax(y, 0.0), one_below());
 }
 
-// Residual after levels [from, to) of the path, from the residual stored after level from.
-__device__ __forceinline__ double replay(double r, const double *T, uint32_t dirs, int from,
-                                         int to) {
-  for (int l = from; l < to; ++l) r = rescale(r, T[l], (dirs >> l) & 1u);
-  return r;
-}
-
-__global__ void walk_prepare_kernel(const int64_t *__restrict__ hkey_in, int64_t J, uint64_t k0,
-                                    uint64_t k1, const double *__restrict__ ov,
-                                    const double *__restrict__ rin, const int32_t *__restrict__ sel,
-                                    int32_t selv, int64_t *__restrict__ key, double *__restrict__ r,
-                                    int32_t *__restrict__ idx) {
+__global__ void walk_prepare_kernel(const int64_t *__restrict__ hkey_in, int64_t J,
+                                    const int32_t *__restrict__ sel, int32_t selv,
+                                    int64_t *__restrict__ key, int32_t *__restrict__ idx) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= J) return;
-  double u;
-  if (ov) u = ov[s];
-  else if (rin) u = rin[s];
-  else u = u64_to_unit(philox_word(k0, k1, (uint64_t)s));
   const bool mine = !sel || sel[s] == selv;
-  r[s] = u;
   key[s] = mine ? (hkey_in ? hkey_in[s] : 0) : INT64_MAX;
   idx[s] = (int32_t)s;
 }
 
-__global__ void walk_gather_kernel(const int64_t *__restrict__ in, const int32_t *__restrict__ idx,
-                                   int64_t J, int64_t *__restrict__ out) {
-  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s < J) out[s] = in[idx[s]];
+// Level-0 buffer: the uniform of each sample in key order.
+__global__ void walk_fill_r_kernel(const int32_t *__restrict__ idx, int64_t J, uint64_t k0,
+                                   uint64_t k1, const double *__restrict__ ov,
+                                   const double *__restrict__ rin, double *__restrict__ r) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= J) return;
+  const int32_t s = idx[i];
+  double u;
+  if (ov) u = ov[s];
+  else if (rin) u = rin[s];
+  else u = u64_to_unit(philox_word(k0, k1, (uint64_t)s));
+  r[i] = u;
 }
 
 // One root run per distinct key; counts participants.
@@ -182,16 +174,19 @@ __global__ void walk_seed_kernel(const int64_t *__restrict__ key, const int32_t 
     int64_t mid = (lo + hi) >> 1;
     if (key[mid] <= k) lo = mid + 1; else hi = mid;
   }
-  const int t = atomicAdd(&ctl[0], 1);
-  Run &rr = runs[t];
-  rr.lo = (int32_t)s;
-  rr.hi = (int32_t)lo;
-  rr.level = 0;
-  rr.node = 0;
-  rr.dirs = 0u;
-  rr.rlev = 0;
   // samples of one group share their rank-level path, hence this probability
-  rr.prob = pmp_in ? pmp_in[idx[s]] : 1.0;
+  const double prob = pmp_in ? pmp_in[idx[s]] : 1.0;
+  const int pieces = (int)((lo - s + kMaxRun - 1) / kMaxRun);
+  const int t = atomicAdd(&ctl[0], pieces);
+  for (int q = 0; q < pieces; ++q) {
+    Run rr;
+    rr.lo = (int32_t)(s + (int64_t)q * kMaxRun);
+    rr.hi = (int32_t)min(lo, s + (int64_t)(q + 1) * kMaxRun);
+    rr.level = 0;
+    rr.node = 0;
+    rr.prob = prob;
+    runs[t + q] = rr;
+  }
 }
 
 __global__ void row_keys_kernel(const int64_t *__restrict__ X, int N, int64_t J, Strides8 st,
@@ -240,36 +235,27 @@ __global__ void walk_gm_kernel(const double2 *__restrict__ tree, const double2 *
 // Warp-cooperative push of a child run (path of the parent + one step) into the next
 // level's generation.  Runs entering the leaf level are cut into chunks so that the
 // per-sample leaf work spreads over warps.
-constexpr int32_t kLeafChunk = 256;
-// runs up to this size rescale their samples' stored residuals at every split (so deeper
-// levels need no replay); larger runs (top levels) leave it to their descendants
-constexpr int32_t kEagerRescale = 256;
+
 
 __device__ __forceinline__ void push_child(Run *runs, int *gen_cnt, int64_t base, int64_t cap,
-                                           int *status, const Run &par, const double *Tp,
-                                           int32_t lo, int32_t hi, double T, bool right,
-                                           int depth, int rlev, int lane) {
+                                           int *status, const Run &par, int32_t lo, int32_t hi,
+                                           double T, bool right, int depth, int lane) {
   const int lev = par.level;
-  const int32_t chunk = (lev + 1 == depth) ? kLeafChunk : hi - lo;
+  const int32_t chunk = (lev + 1 == depth) ? kLeafChunk : kMaxRun;
   for (int32_t c0 = lo; c0 < hi; c0 += chunk) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(gen_cnt, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (base + t >= cap) {   // cannot happen: one level holds at most J disjoint runs
-      if (lane == 0) raise_status(status, RCP_ST_CAPACITY);
-      continue;
-    }
-    Run &c = runs[base + t];
-    if (lane < lev) c.T[lane] = Tp[lane];
     if (lane == 0) {
+      const int t = atomicAdd(gen_cnt, 1);
+      if (base + t >= cap) {   // cannot happen: one level holds at most J disjoint runs
+        raise_status(status, RCP_ST_CAPACITY);
+        continue;
+      }
+      Run c;
       c.lo = c0;
       c.hi = min(hi, c0 + chunk);
       c.level = lev + 1;
       c.node = 2 * par.node + (right ? 1 : 0);
-      c.dirs = par.dirs | ((right ? 1u : 0u) << lev);
-      c.rlev = rlev;
       c.prob = par.prob * (right ? (1.0 - T) : T);
-      c.T[lev] = T;
+      runs[base + t] = c;
     }
   }
   __syncwarp();
@@ -291,7 +277,8 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
                  int leaf, int depth, int64_t row_lo, const double *__restrict__ Mp_g,
                  const double *__restrict__ Mfull,
                  const uint32_t *__restrict__ pairs_g, const double *__restrict__ H,
-                 const int32_t *__restrict__ idx, double *__restrict__ r, Run *runs,
+                 double *__restrict__ rA, double *__restrict__ rB, int32_t *__restrict__ iA,
+                 int32_t *__restrict__ iB, Run *runs,
                  int *ctl, int64_t cap_runs, int64_t *__restrict__ Xi, double *__restrict__ pmp,
                  double *__restrict__ resid, int *status, unsigned long long *prof) {
   extern __shared__ double sh[];
@@ -305,7 +292,6 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
   double *hv = sh + bd + (size_t)wid * walk_per_warp(R);   // R: the run's Hadamard row
   double *zb = hv + R;                             // leaf rows (.) h
   double *mass = zb + (use_mma ? 8 * Zs : kLeafBatch * R);   // leaf
-  double *Tp = mass + kMaxLeaf;                    // path thresholds of the current run
   uint32_t *pairs = reinterpret_cast<uint32_t *>(sh + bd + (size_t)nw * walk_per_warp(R));
   for (int e = threadIdx.x; e < Rs; e += blockDim.x) pairs[e] = pairs_g[e];
   if (use_mma) {
@@ -339,12 +325,11 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
       if (lane == 0) tc = atomicAdd(&claim, 1);
       const int64_t t = begin + blockIdx.x + (int64_t)__shfl_sync(0xffffffffu, tc, 0) * gridDim.x;
       if (t >= end) break;
-      const Run &run = runs[t];
+      const Run run = runs[t];
       const int32_t lo = run.lo, hi = run.hi, level = run.level;
-      const uint32_t dirs = run.dirs;
-      const int rlev = run.rlev;
-      if (lane < level) Tp[lane] = run.T[lane];
-      const int32_t s0 = idx[lo];
+      const double *rs = (level & 1) ? rB : rA;
+      const int32_t *is = (level & 1) ? iB : iA;
+      const int32_t s0 = is[lo];
       for (int c = lane; c < R; c += 32) hv[c] = H ? H[(int64_t)s0 * R + c] : 1.0;
       __syncwarp();
       if (level < depth) {
@@ -376,46 +361,48 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         qR = qR > 0.0 ? qR : 0.0;
         const double tot = qL + qR;
         if (!(tot > 0.0)) {
-          fail_run(lo, hi, idx, Xi, status, ctl, lane);
+          fail_run(lo, hi, is, Xi, status, ctl, lane);
           continue;
         }
         double T = qL / tot;
         T = fmin(fmax(T, 0.0), 1.0);
-        // left-goers (replayed r < T) are a prefix of the r-sorted run: 32-ary search
-        int32_t a = lo, b = hi;   // answer in [a, b]
-        while (b - a > 0) {
-          const int32_t span = b - a;
-          const int32_t step = (span + 31) / 32;
-          const int32_t pos = a + lane * step;
-          bool ge = true;   // "replayed r >= T" at pos (positions >= b count as true)
-          if (pos < b) ge = replay(r[pos], Tp, dirs, rlev, level) >= T;
-          const unsigned m = __ballot_sync(0xffffffffu, ge);
-          if (m == 0u) {                     // every probe < T: answer beyond the last probe
-            a = a + 31 * step + 1;
-            continue;
+        // partition the run's samples into the children's ranges of the next level's
+        // buffer (left from the front, right from the back), rescaling each residual
+        double *rd = (level & 1) ? rA : rB;
+        int32_t *id = (level & 1) ? iA : iB;
+        int32_t nl = 0, nr = 0;
+        const unsigned below = (1u << lane) - 1u;
+        constexpr int kPU = 4;   // 32-sample groups with loads in flight per step
+        for (int32_t q0 = lo; q0 < hi; q0 += 32 * kPU) {
+          double rv[kPU];
+          int32_t sv[kPU];
+#pragma unroll
+          for (int u = 0; u < kPU; ++u) {
+            const int32_t q = q0 + 32 * u + lane;
+            rv[u] = q < hi ? rs[q] : 0.0;
+            sv[u] = q < hi ? is[q] : 0;
           }
-          const int first = __ffs(m) - 1;   // first lane whose probe is >= T
-          if (first == 0) {
-            b = a;
-          } else {                           // answer in (probe[first-1], probe[first]]
-            const int32_t na = a + (first - 1) * step + 1;
-            b = min(b, a + first * step);
-            a = na;
+#pragma unroll
+          for (int u = 0; u < kPU; ++u) {
+            const int32_t q = q0 + 32 * u + lane;
+            const bool valid = q < hi;
+            const bool right = rv[u] >= T;
+            const unsigned ml = __ballot_sync(0xffffffffu, valid && !right);
+            const unsigned mr = __ballot_sync(0xffffffffu, valid && right);
+            if (valid) {
+              const int32_t o =
+                  right ? hi - 1 - (nr + __popc(mr & below)) : lo + nl + __popc(ml & below);
+              rd[o] = rescale(rv[u], T, right);
+              id[o] = sv[u];
+            }
+            nl += __popc(ml);
+            nr += __popc(mr);
           }
-        }
-        const int32_t nl = a - lo;
-        int crlev = rlev;
-        if (hi - lo <= kEagerRescale) {   // bring the stored residuals past this level
-          for (int32_t q = lo + lane; q < hi; q += 32)
-            r[q] = rescale(replay(r[q], Tp, dirs, rlev, level), T, q >= lo + nl);
-          crlev = level + 1;
         }
         if (nl > 0)
-          push_child(runs, gen_cnt, end, cap_runs, status, run, Tp, lo, lo + nl, T, false, depth,
-                     crlev, lane);
-        if (hi - lo - nl > 0)
-          push_child(runs, gen_cnt, end, cap_runs, status, run, Tp, lo + nl, hi, T, true, depth,
-                     crlev, lane);
+          push_child(runs, gen_cnt, end, cap_runs, status, run, lo, lo + nl, T, false, depth, lane);
+        if (nr > 0)
+          push_child(runs, gen_cnt, end, cap_runs, status, run, lo + nl, hi, T, true, depth, lane);
         continue;
       }
       // ---- leaf block: masses z^T M' z of its rows z = u (.) h, then each sample's
@@ -485,11 +472,11 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         bad = !(total_m > 0.0);
       }
       if (bad) {
-        fail_run(lo, hi, idx, Xi, status, ctl, lane);
+        fail_run(lo, hi, is, Xi, status, ctl, lane);
         continue;
       }
       for (int32_t s = lo + lane; s < hi; s += 32) {
-        const double target = replay(r[s], Tp, dirs, rlev, level) * total_m;
+        const double target = rs[s] * total_m;
         double cdf = 0.0;
         int cnt = 0;
         for (int q = 0; q < nrow; ++q) {
@@ -502,7 +489,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         const double picked = mass[choice];
         double ro = picked > 0.0 ? (target - (cdf_at - picked)) / picked : 0.0;
         ro = fmin(fmax(ro, 0.0), one_below());
-        const int32_t o = idx[s];
+        const int32_t o = is[s];
         Xi[o] = row_lo + r0 + choice;
         pmp[o] = rprob * (picked / total_m);
         if (resid) resid[o] = ro;
@@ -585,24 +572,19 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   double *gm = (double *)(w + L.o_gm);
   void *cub_tmp = w + L.o_cub;
   const unsigned gb = (unsigned)ceil_div(J, 256);
-  walk_prepare_kernel<<<gb, 256, 0, st>>>(d_hkey, J, key0, key1, d_override, d_rin, d_sel,
-                                          sel_value, key, r, idx);
+  walk_prepare_kernel<<<gb, 256, 0, st>>>(d_hkey, J, d_sel, sel_value, key, idx);
   RCP_LAUNCH_CHECK("walk_prepare");
-  // sort by r, then stably by key: runs of equal key are contiguous and r-ordered
+  // group samples by key (only the key's bits); level 0 holds their uniforms in that order
+  int32_t *idx3 = (int32_t *)(w + L.o_idx3);
   size_t tb = L.cub_bytes;
-  RCP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, r, r2, idx, idx2, (int)J, 0, 64, st));
-  RCP_LAUNCH_CHECK("walk_sort_r");
-  walk_gather_kernel<<<gb, 256, 0, st>>>(key, idx2, J, key2);
-  RCP_LAUNCH_CHECK("walk_gather");
-  tb = L.cub_bytes;
   RCP_CUDA_TRY(
-      cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key2, key, idx2, idx, (int)J, 0, key_bits, st));
+      cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key, key2, idx, idx2, (int)J, 0, key_bits, st));
   RCP_LAUNCH_CHECK("walk_sort_key");
-  walk_gather_kernel<<<gb, 256, 0, st>>>((const int64_t *)r, idx, J, (int64_t *)r2);
-  RCP_LAUNCH_CHECK("walk_gather_r");
+  walk_fill_r_kernel<<<gb, 256, 0, st>>>(idx2, J, key0, key1, d_override, d_rin, r);
+  RCP_LAUNCH_CHECK("walk_fill_r");
   RCP_CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlBytes, st));
   RCP_CUDA_TRY(cudaMemsetAsync(w + L.o_prof, 0, kProfBytes, st));
-  walk_seed_kernel<<<gb, 256, 0, st>>>(key, idx, J, d_sel ? d_pmp_i : nullptr, runs, ctl);
+  walk_seed_kernel<<<gb, 256, 0, st>>>(key2, idx2, J, d_sel ? d_pmp_i : nullptr, runs, ctl);
   RCP_LAUNCH_CHECK("walk_seed");
   // this walk's M' tables and G (.) M' for every node
   walk_tables_kernel<<<1, 256, 0, st>>>(d_M, R, Mp, pairs);
@@ -631,15 +613,16 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   // cooperative launch: every CTA co-resident, grid-wide barrier between tree levels
   const double *a_gm = gm, *a_U = d_U, *a_Mp = Mp, *a_H = d_H_in, *a_Mf = d_M;
   const uint32_t *a_pairs = pairs;
-  const int32_t *a_idx = idx;
-  double *a_r = r2;
+  double *a_rA = r, *a_rB = r2;
+  int32_t *a_iA = idx2, *a_iB = idx3;
   unsigned long long *a_prof = (unsigned long long *)(w + L.o_prof);
   int64_t a_n = n, a_row_lo = row_lo, a_cap = L.nruns;
   int a_R = R, a_leaf = leaf, a_depth = depth;
   void *args[] = {(void *)&a_gm, (void *)&a_U, (void *)&a_n, (void *)&a_R, (void *)&a_leaf,
                   (void *)&a_depth, (void *)&a_row_lo, (void *)&a_Mp, (void *)&a_Mf,
                   (void *)&a_pairs,
-                  (void *)&a_H, (void *)&a_idx, (void *)&a_r, (void *)&runs, (void *)&ctl,
+                  (void *)&a_H, (void *)&a_rA, (void *)&a_rB, (void *)&a_iA, (void *)&a_iB,
+                  (void *)&runs, (void *)&ctl,
                   (void *)&a_cap, (void *)&d_Xi, (void *)&d_pmp_i, (void *)&d_resid,
                   (void *)&d_status, (void *)&a_prof};
   RCP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)walk_runs_kernel, dim3(grid),
