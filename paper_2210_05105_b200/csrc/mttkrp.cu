@@ -262,7 +262,7 @@ __global__ void rows_hit_kernel(const int64_t *__restrict__ rcnt, int64_t n_rows
 // ------------------------------------------------------------ entry traversal
 // Work items: chunks of at most kItemE consecutive entries of one fiber.  A fiber's entries
 // are contiguous in the store, so a warp reads an item's rows/values fully coalesced.
-constexpr int64_t kItemE = 1024;
+constexpr int64_t kItemE = 512;
 constexpr int kTraverseThreads = 1024;
 constexpr int kInFlight = 8;   // entries per lane with loads in flight (latency hiding)
 
@@ -393,10 +393,16 @@ cta_hist_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp
   const int64_t S = Sp[0];
   int64_t i0, i1;
   cta_items(ioff[S], i0, i1);
+  __shared__ int claim;
   for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) hist[i] = 0;
+  if (threadIdx.x == 0) claim = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int64_t it = i0 + wid; it < i1; it += nw) {
+  const int lane = threadIdx.x & 31;
+  while (true) {   // the CTA's items, claimed one at a time by its warps
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&claim, 1);
+    const int64_t it = i0 + __shfl_sync(0xffffffffu, c, 0);
+    if (it >= i1) break;
     const ItemSpan sp = item_span(it, ioff, ifib, dlo, dlen);
     for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32 * kInFlight) {
       int32_t rw[kInFlight];
@@ -468,10 +474,16 @@ cta_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__
   int64_t i0, i1;
   cta_items(ioff[S], i0, i1);
   const int32_t *mine = cmat + (int64_t)blockIdx.x * n_rows;
+  __shared__ int claim;
   for (int64_t i = threadIdx.x; i < n_rows; i += blockDim.x) cur[i] = (int32_t)(rptr[i] + mine[i]);
+  if (threadIdx.x == 0) claim = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int64_t it = i0 + wid; it < i1; it += nw) {
+  const int lane = threadIdx.x & 31;
+  while (true) {   // the CTA's items, claimed one at a time by its warps
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&claim, 1);
+    const int64_t it = i0 + __shfl_sync(0xffffffffu, c, 0);
+    if (it >= i1) break;
     const ItemSpan sp = item_span(it, ioff, ifib, dlo, dlen);
     for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32 * kInFlight) {
       // issue every load of the batch before the dependent cursor atomics and stores

@@ -1,6 +1,8 @@
 """One C3 round under cudaProfilerStart/Stop (for ncu --profile-from-start off)."""
 import sys, os, torch
 sys.path.insert(0, '.')
+from paper_2210_05105_b200 import _lib
+if os.environ.get("OLDLIB"): _lib.load(os.environ["OLDLIB"])
 import bench
 from paper_2210_05105_b200.engine import make_local_cluster
 dev = torch.device("cuda", 0)
