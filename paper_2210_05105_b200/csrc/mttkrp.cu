@@ -506,6 +506,130 @@ cta_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__
   }
 }
 
+// ------------------------------------------------------------ bucketed transpose
+// The single-pass scatter above writes every entry to a random 16-B slot (each write fills
+// a 32-B sector: half the DRAM traffic is wasted).  The bucketed variant moves the same
+// entries in two near-sequential passes:
+//  A. per CTA, entries of row bucket b (rows [b 2^sh, (b+1) 2^sh), <= 256 buckets) go to the
+//     CTA's contiguous slice of the bucket's final range — ~256 write streams per CTA
+//     instead of one per row — as {row, fiber, value};
+//  B. one CTA per bucket orders its range by row in place of the final array (the range,
+//     ~1/256 of the entries, stays L2-resident while its rows' cursors advance).
+constexpr int kBucketMax = 512;
+constexpr int64_t kBucketMinRows = 4096;   // below: the single-pass scatter is faster
+
+// bofs[cta][b] = start of the CTA's slice of bucket b = rptr[b << sh] + sum over the
+// bucket's rows of the CTA-exclusive prefix cmat[cta][row]
+__global__ void bucket_offsets_kernel(const int32_t *__restrict__ cmat, int G, int64_t n_rows,
+                                      int sh, int nb, const int64_t *__restrict__ rptr,
+                                      int64_t *__restrict__ bofs) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)G * nb) return;
+  const int c = (int)(i / nb), b = (int)(i - (int64_t)c * nb);
+  const int64_t r0 = (int64_t)b << sh, r1 = min(n_rows, r0 + ((int64_t)1 << sh));
+  const int32_t *row = cmat + (int64_t)c * n_rows;
+  int64_t acc = 0;
+  for (int64_t r = r0; r < r1; ++r) acc += row[r];
+  bofs[i] = rptr[r0] + acc;
+}
+
+// warp-aggregated shared-memory cursor: lanes with equal key share one atomic
+__device__ __forceinline__ int agg_slot(int *ctr, int key, bool active) {
+  const unsigned act = __ballot_sync(0xffffffffu, active);
+  int slot = 0;
+  if (active) {
+    const unsigned peers = __match_any_sync(act, key);
+    const int leader = __ffs(peers) - 1;
+    const int lane = threadIdx.x & 31;
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&ctr[key], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    slot = base + rank;
+  }
+  return slot;
+}
+
+__global__ void __launch_bounds__(kTraverseThreads)
+bucket_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                      const int32_t *__restrict__ ifib, const int64_t *__restrict__ dlo,
+                      const int64_t *__restrict__ dlen, const int32_t *__restrict__ rows,
+                      const double *__restrict__ vals, int sh, int nb,
+                      const int64_t *__restrict__ bofs, double2 *__restrict__ tmp, int64_t cap,
+                      int *status) {
+  __shared__ int bcur[kBucketMax];   // offsets relative to the CTA's slice base (< 2^31)
+  __shared__ int64_t bbase[kBucketMax];
+  __shared__ int claim;
+  const int64_t S = Sp[0];
+  int64_t i0, i1;
+  cta_items(ioff[S], i0, i1);
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    bcur[b] = 0;
+    bbase[b] = bofs[(int64_t)blockIdx.x * nb + b];
+  }
+  if (threadIdx.x == 0) claim = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&claim, 1);
+    const int64_t it = i0 + __shfl_sync(0xffffffffu, c, 0);
+    if (it >= i1) break;
+    const ItemSpan sp = item_span(it, ioff, ifib, dlo, dlen);
+    for (int64_t pos0 = sp.a; pos0 < sp.b; pos0 += 32 * kInFlight) {
+      int32_t rw[kInFlight];
+      double v[kInFlight];
+#pragma unroll
+      for (int q = 0; q < kInFlight; ++q) {
+        const int64_t pos = pos0 + 32 * q + lane;
+        const bool ok = pos < sp.b;
+        rw[q] = ok ? rows[pos] : -1;
+        v[q] = ok ? vals[pos] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kInFlight; ++q) {
+        if (pos0 + 32 * q >= sp.b) break;   // warp-uniform
+        const bool ok = rw[q] >= 0;
+        const int b = ok ? (rw[q] >> sh) : 0;
+        const int slot = agg_slot(bcur, b, ok);
+        if (ok) {
+          const int64_t o = bbase[b] + slot;
+          if (o < cap)
+            tmp[o] = make_double2(
+                __longlong_as_double((long long)(((uint64_t)(uint32_t)rw[q] << 32) | (uint32_t)sp.d)),
+                v[q]);
+          else
+            raise_status(status, RCP_ST_CAPACITY);
+        }
+      }
+    }
+  }
+}
+
+// One CTA per bucket: entries of [rptr[b << sh], rptr[(b+1) << sh]) ordered by row.
+__global__ void __launch_bounds__(256)
+bucket_rows_kernel(const double2 *__restrict__ tmp, int64_t n_rows, int sh,
+                   const int64_t *__restrict__ rptr, double2 *__restrict__ ent) {
+  extern __shared__ int rcur[];   // per row of the bucket, relative to the row start
+  const int b = blockIdx.x;
+  const int64_t r0 = (int64_t)b << sh, r1 = min(n_rows, r0 + ((int64_t)1 << sh));
+  const int nr = (int)(r1 - r0);
+  for (int q = threadIdx.x; q < nr; q += blockDim.x) rcur[q] = 0;
+  __syncthreads();
+  const int64_t e0 = rptr[r0], e1 = rptr[r1];
+  for (int64_t base = e0; base < e1; base += blockDim.x) {
+    const int64_t e = base + threadIdx.x;
+    const bool ok = e < e1;
+    double2 t = make_double2(0.0, 0.0);
+    if (ok) t = tmp[e];
+    const uint64_t key = (uint64_t)__double_as_longlong(t.x);
+    const int row = ok ? (int)(key >> 32) : 0;
+    if (ok)
+      ent[rptr[row] + atomicAdd(&rcur[row - r0], 1)] =
+          make_double2(__longlong_as_double((long long)(uint32_t)(key & 0xffffffffu)), t.y);
+  }
+}
+
 // ------------------------------------------------------------ segmented SpMM
 // One warp per chunk of kSpmmChunk row-sorted entries; lanes own output columns.
 // Entries come as separate column/value arrays (reference-shaped CSR, drop-in path); the
@@ -744,7 +868,7 @@ struct MttkrpLayout {
   int64_t T;
   size_t o_tkey, o_tcnt, o_trep, o_twmin, o_twmax, o_twsum, o_dsc, o_bcnt, o_dkey, o_dcnt,
       o_drep, o_dlo, o_dlen, o_doff, o_ioff, o_ifib, o_Hs, o_scan, o_rcnt, o_rptr, o_cmat,
-      o_ent, o_S,
+      o_ent, o_tmp, o_bofs, o_S,
       o_nnz;
   size_t total;
   MttkrpLayout(int64_t J, int64_t cap, int64_t n_rows, int R) {
@@ -775,6 +899,8 @@ struct MttkrpLayout {
     o_cmat = w.add(sizeof(int32_t) * (size_t)sm_count() *
                    (size_t)(n_rows < kPrivRows ? n_rows : kPrivRows));
     o_ent = w.add(sizeof(double2) * (cap + 1));
+    o_tmp = w.add(sizeof(double2) * (cap + 1));
+    o_bofs = w.add(sizeof(int64_t) * (size_t)sm_count() * kBucketMax);
     o_S = w.add(sizeof(int64_t) * 4);
     o_nnz = w.add(sizeof(int64_t) * 4);
     total = w.total + 256;
@@ -910,9 +1036,27 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     RCP_LAUNCH_CHECK("cta_prefix");
     rc = scan_i64_exclusive(rcnt, rptr, n_rows, nullptr, scan_ws, st);
     if (rc) return rc;
-    cta_scatter_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, ifib, dlo, dlen, d_rows, d_vals,
-                                                             n_rows, rptr, cmat, ent, cap, d_status);
-    RCP_LAUNCH_CHECK("cta_scatter");
+    if (n_rows < kBucketMinRows) {   // few rows: their segments are long, scatter directly
+      cta_scatter_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, ifib, dlo, dlen, d_rows,
+                                                               d_vals, n_rows, rptr, cmat, ent, cap,
+                                                               d_status);
+      RCP_LAUNCH_CHECK("cta_scatter");
+    } else {
+    // bucketed transpose (two near-sequential passes)
+    int sh = 0;
+    while ((ceil_div(n_rows, (int64_t)1 << sh)) > kBucketMax) ++sh;
+    const int nb = (int)ceil_div(n_rows, (int64_t)1 << sh);
+    int64_t *bofs = (int64_t *)P(L.o_bofs);
+    double2 *tmp = (double2 *)P(L.o_tmp);
+    bucket_offsets_kernel<<<(unsigned)ceil_div((int64_t)grid * nb, 256), 256, 0, st>>>(
+        cmat, grid, n_rows, sh, nb, rptr, bofs);
+    RCP_LAUNCH_CHECK("bucket_offsets");
+    bucket_scatter_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, d_vals,
+                                                             sh, nb, bofs, tmp, cap, d_status);
+    RCP_LAUNCH_CHECK("bucket_scatter");
+    bucket_rows_kernel<<<nb, 256, sizeof(int) * ((size_t)1 << sh), st>>>(tmp, n_rows, sh, rptr, ent);
+    RCP_LAUNCH_CHECK("bucket_rows");
+    }
   } else {
     RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
     row_count_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, n_rows, 0, rcnt);

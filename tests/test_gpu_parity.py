@@ -191,12 +191,16 @@ def test_gather_csr_and_downsampled_match_reference(pkg):
         assert rel_err(out, g0["out%d" % k]) < 1e-13
 
 
-def test_fused_sampled_mttkrp_matches_oracle(pkg):
+@pytest.mark.parametrize("dims,nnz", [
+    ((40, 35, 30), 6000),        # CTA-private histograms, single-pass scatter
+    ((6000, 35, 30), 60000),     # >= 4096 rows in mode 0: bucketed two-pass transpose
+    ((60000, 12, 10), 50000),    # > 49152 rows in mode 0: global-atomic row cursors
+])
+def test_fused_sampled_mttkrp_matches_oracle(pkg, dims, nnz):
     import torch
     from paper_2210_05105_b200.ops import ops_for
     from paper_2210_05105_b200.store import build_store
-    dims = (40, 35, 30)
-    idx, vals = synth.small_random(dims, 6000, seed=2)
+    idx, vals = synth.small_random(dims, nnz, seed=2)
     gen = np.random.default_rng(4)
     R = 37
     factors = [gen.standard_normal((d, R)) for d in dims]
