@@ -38,6 +38,7 @@ int sm_count() {
 constexpr int kMaxModes = 8;
 constexpr int kPrivRows = 49152;   // CTA-private row histogram limit (int32 in smem)
 constexpr int kSpmmChunk = 256;    // entries per warp in the segmented reduction
+constexpr int kSpmmU = 4;          // entries (Hs-row loads) in flight per lane
 
 // Row stride of the scaled KRP rows Hs: a multiple of 16 doubles, so every row starts on a
 // 128-byte line and a warp's double2 row load touches ceil(R/16) lines, not one more.
@@ -742,20 +743,20 @@ spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64
 #pragma unroll
         for (int j = 0; j < NP; ++j) acc[j] = make_double2(0.0, 0.0);
         int64_t x = e;
-        for (; x + 4 <= stop; x += 4) {
-          double2 en[4];
+        for (; x + kSpmmU <= stop; x += kSpmmU) {
+          double2 en[kSpmmU];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) en[q] = ent[x + q];
+          for (int q = 0; q < kSpmmU; ++q) en[q] = ent[x + q];
 #pragma unroll
           for (int j = 0; j < NP; ++j) {
             const int c2 = lane + 32 * j;
             if (2 * c2 < R) {
-              double2 h[4];
+              double2 h[kSpmmU];
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
+              for (int q = 0; q < kSpmmU; ++q)
                 h[q] = H2[(int64_t)(int32_t)__double_as_longlong(en[q].x) * Rp2 + c2];
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
+              for (int q = 0; q < kSpmmU; ++q) {
                 acc[j].x = fma(en[q].y, h[q].x, acc[j].x);
                 acc[j].y = fma(en[q].y, h[q].y, acc[j].y);
               }

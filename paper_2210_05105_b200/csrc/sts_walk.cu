@@ -201,13 +201,21 @@ __global__ void row_keys_kernel(const int64_t *__restrict__ X, int N, int64_t J,
 
 // Packed M' (off-diagonals doubled, zero pad to the even stride) and the (a, b) index pair
 // of every packed position.
+// Tables are stored in split-half order: position 2i holds packed element i, position
+// 2i+1 element i + Rs/2, so a lane's double2 at index i covers two elements whose (a, b)
+// indices run consecutively across lanes (conflict-free h[b] reads in shared memory).
+__host__ __device__ __forceinline__ int split_pos(int e, int n2) {
+  return e < n2 ? 2 * e : 2 * (e - n2) + 1;
+}
+
 __global__ void walk_tables_kernel(const double *__restrict__ Mfull, int R, double *__restrict__ Mp,
                                    uint32_t *__restrict__ pairs) {
-  const int Rt = R * (R + 1) / 2, Rs = tri_stride(R);
+  const int Rt = R * (R + 1) / 2, Rs = tri_stride(R), n2 = Rs / 2;
   for (int e = threadIdx.x; e < Rs; e += blockDim.x) {
+    const int ps = split_pos(e, n2);
     if (e >= Rt) {
-      Mp[e] = 0.0;
-      pairs[e] = 0u;
+      Mp[ps] = 0.0;
+      pairs[ps] = 0u;
       continue;
     }
     int a = 0, rem = e;
@@ -217,18 +225,21 @@ __global__ void walk_tables_kernel(const double *__restrict__ Mfull, int R, doub
     }
     const int b = a + rem;
     const double m = Mfull[a * R + b];
-    Mp[e] = (a == b) ? m : 2.0 * m;
-    pairs[e] = (uint32_t)a | ((uint32_t)b << 16);
+    Mp[ps] = (a == b) ? m : 2.0 * m;
+    pairs[ps] = (uint32_t)a | ((uint32_t)b << 16);
   }
 }
 
-// GM[node] = G[node] (.) M' for one walk: a node's child mass is then <GM, h h^T>.
-__global__ void walk_gm_kernel(const double2 *__restrict__ tree, const double2 *__restrict__ Mp,
+// GM[node] = G[node] (.) M' for one walk (split-half order): a node's child mass is then
+// <GM, h h^T>.  n2: double2 slots over all nodes; Rs2 = Rs / 2 slots per node.
+__global__ void walk_gm_kernel(const double *__restrict__ tree, const double2 *__restrict__ Mp,
                                int64_t n2, int Rs2, double2 *__restrict__ gm) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double2 g = tree[i], m = Mp[i % Rs2];
-    gm[i] = make_double2(g.x * m.x, g.y * m.y);
+    const int64_t node = i / Rs2, j = i - node * Rs2;
+    const double *g = tree + node * 2 * Rs2;
+    const double2 m = Mp[j];
+    gm[i] = make_double2(g[j] * m.x, g[j + Rs2] * m.y);
   }
 }
 
@@ -594,7 +605,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
     const int64_t n2 = ((2LL << depth) - 1) * (int64_t)(Rs / 2);
     int64_t g = ceil_div(n2, 256);
     if (g > 8LL * sm_count()) g = 8LL * sm_count();
-    walk_gm_kernel<<<(unsigned)g, 256, 0, st>>>((const double2 *)d_tree, (const double2 *)Mp, n2,
+    walk_gm_kernel<<<(unsigned)g, 256, 0, st>>>(d_tree, (const double2 *)Mp, n2,
                                                  Rs / 2, (double2 *)gm);
     RCP_LAUNCH_CHECK("walk_gm");
   }
