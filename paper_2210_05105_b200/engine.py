@@ -342,6 +342,7 @@ class Cluster:
         self.timings = {p: 0.0 for p in PHASES}
         self.timed = False
         self.phase_events = None
+        self._side = None
 
     def _tick(self, phase, t0):
         if not self.timed:
@@ -482,12 +483,21 @@ class Cluster:
             for r in self.ranks:
                 injected(r)
         t0 = self._tick("sampling", t0)
+        # Gs = (H w)^T (H w) and its pseudo-inverse depend only on the batch: they run on a
+        # side stream, overlapped with the sampled MTTKRP, and join before the update
         self._ev("gram+pinv")
-        for r in self.ranks:
-            r.sketched_system()
+        t = torch()
+        main = t.cuda.current_stream()
+        if self._side is None:
+            self._side = t.cuda.Stream(device=main.device)
+        self._side.wait_stream(main)
+        with t.cuda.stream(self._side):
+            for r in self.ranks:
+                r.sketched_system()
         self._ev("mttkrp")
         for r in self.ranks:
             r.mttkrp(k)
+        main.wait_stream(self._side)
         t0 = self._tick("mttkrp", t0)
         self._ev("update")
         parts = self.comm.all_gather([r.update(k) for r in self.ranks])
