@@ -169,14 +169,18 @@ int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
  * rank-level levels) else WALK_UNIFORM draws of key (key0,key1).
  * d_sel (nullable): only samples s with d_sel[s] == sel_value walk (multi-rank owner);
  * their d_pmp_i[s] holds the probability so far and is multiplied, otherwise it is set.
- * Outputs per walked sample: d_Xi[s] (global row), d_pmp_i[s], d_resid[s] (nullable).
+ * Outputs per walked sample: d_Xi[s] (global row), d_pmp_i[s], d_resid[s] (nullable),
+ * d_H_out[s,:] = d_H_in[s,:] (.) U[row,:] (or U[row,:] when d_H_in is NULL) when d_H_out is
+ * non-NULL (must not alias d_H_in: samples of one group read their common row while others
+ * finish).
  * d_ws: rcp_sts_walk_ws_bytes(J, n, leaf, R) (holds this walk's G (.) M node table). */
 size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf, int R);
 int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
                  int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
                  int key_bits, int64_t J, uint64_t key0, uint64_t key1, const double *d_override,
                  const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
-                 double *d_pmp_i, double *d_resid, void *d_ws, size_t ws_bytes, int *d_status,
+                 double *d_pmp_i, double *d_resid, double *d_H_out, void *d_ws, size_t ws_bytes,
+                 int *d_status,
                  void *stream);
 /* Fold the walked rows: d_out[s,:] = U[X_i[s]-row_lo, :] (init != 0) or
  * d_out[s,:] *= U[X_i[s]-row_lo, :], for samples with d_sel[s] == sel_value (all when

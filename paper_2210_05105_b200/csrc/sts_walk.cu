@@ -291,7 +291,8 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
                  double *__restrict__ rA, double *__restrict__ rB, int32_t *__restrict__ iA,
                  int32_t *__restrict__ iB, Run *runs,
                  int *ctl, int64_t cap_runs, int64_t *__restrict__ Xi, double *__restrict__ pmp,
-                 double *__restrict__ resid, int *status, unsigned long long *prof) {
+                 double *__restrict__ resid, double *__restrict__ Hout, int *status,
+                 unsigned long long *prof) {
   extern __shared__ double sh[];
   const int Rt = R * (R + 1) / 2;
   const int Rs = tri_stride(R);                    // even node stride (zero pad)
@@ -486,26 +487,42 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         fail_run(lo, hi, is, Xi, status, ctl, lane);
         continue;
       }
-      for (int32_t s = lo + lane; s < hi; s += 32) {
-        const double target = rs[s] * total_m;
-        double cdf = 0.0;
-        int cnt = 0;
-        for (int q = 0; q < nrow; ++q) {
-          cdf += mass[q];
-          if (cdf <= target) ++cnt;
+      // blocks of kLeafChunk samples: lanes pick rows, then (optionally) the warp writes the
+      // folded Hadamard rows from the staged leaf rows z = u (.) h
+      const bool zrows = use_mma && nrow <= 8;   // zb holds every row of this leaf
+      for (int32_t b0 = lo; b0 < hi; b0 += kLeafChunk) {
+        const int32_t b1 = min(hi, b0 + kLeafChunk);
+        for (int32_t s = b0 + lane; s < b1; s += 32) {
+          const double target = rs[s] * total_m;
+          double cdf = 0.0;
+          int cnt = 0;
+          for (int q = 0; q < nrow; ++q) {
+            cdf += mass[q];
+            if (cdf <= target) ++cnt;
+          }
+          const int choice = cnt < nrow - 1 ? cnt : nrow - 1;
+          double cdf_at = 0.0;
+          for (int q = 0; q <= choice; ++q) cdf_at += mass[q];
+          const double picked = mass[choice];
+          double ro = picked > 0.0 ? (target - (cdf_at - picked)) / picked : 0.0;
+          ro = fmin(fmax(ro, 0.0), one_below());
+          const int32_t o = is[s];
+          Xi[o] = row_lo + r0 + choice;
+          pmp[o] = rprob * (picked / total_m);
+          if (resid) resid[o] = ro;
+          if (Hout) {   // fold the chosen factor row into the sample's Hadamard row
+            double *dst = Hout + (int64_t)o * R;
+            if (zrows) {
+              const double *z = zb + choice * Zs;
+              for (int c = 0; c < R; ++c) dst[c] = z[c];
+            } else {
+              const double *u = U + (r0 + choice) * R;
+              for (int c = 0; c < R; ++c) dst[c] = u[c] * hv[c];
+            }
+          }
         }
-        const int choice = cnt < nrow - 1 ? cnt : nrow - 1;
-        double cdf_at = 0.0;
-        for (int q = 0; q <= choice; ++q) cdf_at += mass[q];
-        const double picked = mass[choice];
-        double ro = picked > 0.0 ? (target - (cdf_at - picked)) / picked : 0.0;
-        ro = fmin(fmax(ro, 0.0), one_below());
-        const int32_t o = is[s];
-        Xi[o] = row_lo + r0 + choice;
-        pmp[o] = rprob * (picked / total_m);
-        if (resid) resid[o] = ro;
+        __syncwarp();
       }
-      __syncwarp();
       if (lane == 0) atomicAdd(&ctl[2], hi - lo);
     }
     grid.sync();
@@ -555,7 +572,8 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
                  int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
                  int key_bits, int64_t J, uint64_t key0, uint64_t key1, const double *d_override,
                  const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
-                 double *d_pmp_i, double *d_resid, void *d_ws, size_t ws_bytes, int *d_status,
+                 double *d_pmp_i, double *d_resid, double *d_H_out, void *d_ws, size_t ws_bytes,
+                 int *d_status,
                  void *stream) {
   if (R < 1 || R > RCP_MAX_RANK || leaf < 1 || leaf > kMaxLeaf || J < 0 || n < 0 ||
       J >= (1LL << 31) || key_bits < 1)
@@ -634,7 +652,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
                   (void *)&a_pairs,
                   (void *)&a_H, (void *)&a_rA, (void *)&a_rB, (void *)&a_iA, (void *)&a_iB,
                   (void *)&runs, (void *)&ctl,
-                  (void *)&a_cap, (void *)&d_Xi, (void *)&d_pmp_i, (void *)&d_resid,
+                  (void *)&a_cap, (void *)&d_Xi, (void *)&d_pmp_i, (void *)&d_resid, (void *)&d_H_out,
                   (void *)&d_status, (void *)&a_prof};
   RCP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)walk_runs_kernel, dim3(grid),
                                            dim3(warps * 32), args, smem, st));

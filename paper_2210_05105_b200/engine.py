@@ -108,6 +108,7 @@ class RankState:
         self.w = t.ones(J, **f64)
         self.resid = t.zeros(J, **f64)
         self.H = t.ones((J, R), **f64)
+        self.H_alt = t.empty((J, R), **f64)      # walk output buffer (swapped with H)
         self.urow = t.zeros((J, R), **f64)
         self.owner = t.zeros(J, dtype=t.int32, device=dev)
         self.rtop = t.zeros(J, **f64)
@@ -251,11 +252,13 @@ class RankState:
             return
         if self.n[i] > 0:
             hk, kb = ops.walk_key(self.X, self.dims, k, i, self.hkey)
+            fused = self.P == 1   # the walk folds U rows into the Hadamard rows itself
             ops.sts_walk(self.local_tree(i), self.U[i], self.leaf_of(i), self.lo[i], self.M, H_in,
                          self.J, key, override if self.P == 1 else None, rin, sel, self.rank,
-                         self.X[i], self.pmp[i], self.resid, hkey=hk, key_bits=kb)
-            if self.P == 1:     # fold straight into the running Hadamard rows
-                ops.fold_rows(self.H, self.U[i], self.lo[i], self.X[i], init=first)
+                         self.X[i], self.pmp[i], self.resid, hkey=hk, key_bits=kb,
+                         H_out=self.H_alt if fused else None)
+            if fused:
+                self.H, self.H_alt = self.H_alt, self.H
             else:               # this rank's finished rows, exchanged afterwards
                 ops.fold_rows(self.urow, self.U[i], self.lo[i], self.X[i], init=True,
                               sel=self.owner, sel_value=self.rank)

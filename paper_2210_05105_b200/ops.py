@@ -110,12 +110,12 @@ class Ops:
                 stream_handle())
 
     def sts_walk(self, tree, U, leaf, row_lo, M, H_in, J, key, override, rin, sel, sel_value,
-                 Xi, pmp_i, resid, hkey=None, key_bits=64):
+                 Xi, pmp_i, resid, hkey=None, key_bits=64, H_out=None):
         n, R = U.shape
         w = self.ws("sts_walk", self.lib.rcp_sts_walk_ws_bytes(int(J), n, int(leaf), R))
         self._c("rcp_sts_walk", ptr(tree), ptr(U), n, R, int(leaf), int(row_lo), ptr(M),
                 ptr(H_in), ptr(hkey), int(key_bits), int(J), key[0], key[1], ptr(override), ptr(rin), ptr(sel),
-                int(sel_value), ptr(Xi), ptr(pmp_i), ptr(resid), ptr(w), w.numel(),
+                int(sel_value), ptr(Xi), ptr(pmp_i), ptr(resid), ptr(H_out), ptr(w), w.numel(),
                 self.status.ptr, stream_handle())
 
     def sts_flat_draw(self, cdf, dist, row_lo, mass, key, J, Xi, pmp_i):
