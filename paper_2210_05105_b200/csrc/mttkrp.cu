@@ -611,23 +611,33 @@ bucket_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restric
 __global__ void __launch_bounds__(256)
 bucket_rows_kernel(const double2 *__restrict__ tmp, int64_t n_rows, int sh,
                    const int64_t *__restrict__ rptr, double2 *__restrict__ ent) {
-  extern __shared__ int rcur[];   // per row of the bucket, relative to the row start
+  extern __shared__ int64_t rbase[];   // per row of the bucket: row start, then int32 cursors
   const int b = blockIdx.x;
   const int64_t r0 = (int64_t)b << sh, r1 = min(n_rows, r0 + ((int64_t)1 << sh));
   const int nr = (int)(r1 - r0);
-  for (int q = threadIdx.x; q < nr; q += blockDim.x) rcur[q] = 0;
+  int *rcur = reinterpret_cast<int *>(rbase + ((int64_t)1 << sh));
+  for (int q = threadIdx.x; q < nr; q += blockDim.x) {
+    rbase[q] = rptr[r0 + q];
+    rcur[q] = 0;
+  }
   __syncthreads();
   const int64_t e0 = rptr[r0], e1 = rptr[r1];
-  for (int64_t base = e0; base < e1; base += blockDim.x) {
-    const int64_t e = base + threadIdx.x;
-    const bool ok = e < e1;
-    double2 t = make_double2(0.0, 0.0);
-    if (ok) t = tmp[e];
-    const uint64_t key = (uint64_t)__double_as_longlong(t.x);
-    const int row = ok ? (int)(key >> 32) : 0;
-    if (ok)
-      ent[rptr[row] + atomicAdd(&rcur[row - r0], 1)] =
-          make_double2(__longlong_as_double((long long)(uint32_t)(key & 0xffffffffu)), t.y);
+  constexpr int U = 8;   // entries in flight per thread
+  for (int64_t base = e0; base < e1; base += (int64_t)blockDim.x * U) {
+    double2 t[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = base + (int64_t)u * blockDim.x + threadIdx.x;
+      t[u] = e < e1 ? tmp[e] : make_double2(__longlong_as_double(-1LL), 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t key = (uint64_t)__double_as_longlong(t[u].x);
+      if (key == ~0ull) continue;
+      const int row = (int)(key >> 32);
+      const int64_t o = rbase[row - r0] + atomicAdd(&rcur[row - r0], 1);
+      ent[o] = make_double2(__longlong_as_double((long long)(uint32_t)(key & 0xffffffffu)), t[u].y);
+    }
   }
 }
 
@@ -1055,7 +1065,8 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     bucket_scatter_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, d_vals,
                                                              sh, nb, bofs, tmp, cap, d_status);
     RCP_LAUNCH_CHECK("bucket_scatter");
-    bucket_rows_kernel<<<nb, 256, sizeof(int) * ((size_t)1 << sh), st>>>(tmp, n_rows, sh, rptr, ent);
+    bucket_rows_kernel<<<nb, 256, (sizeof(int64_t) + sizeof(int)) * ((size_t)1 << sh), st>>>(
+        tmp, n_rows, sh, rptr, ent);
     RCP_LAUNCH_CHECK("bucket_rows");
     }
   } else {
