@@ -524,31 +524,18 @@ constexpr int64_t kBucketMinRows = 4096;   // below: the single-pass scatter is 
 __global__ void bucket_offsets_kernel(const int32_t *__restrict__ cmat, int G, int64_t n_rows,
                                       int sh, int nb, const int64_t *__restrict__ rptr,
                                       int64_t *__restrict__ bofs) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // one warp per (CTA, bucket): lanes read the bucket's rows coalesced
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (i >= (int64_t)G * nb) return;
   const int c = (int)(i / nb), b = (int)(i - (int64_t)c * nb);
   const int64_t r0 = (int64_t)b << sh, r1 = min(n_rows, r0 + ((int64_t)1 << sh));
   const int32_t *row = cmat + (int64_t)c * n_rows;
-  int64_t acc = 0;
-  for (int64_t r = r0; r < r1; ++r) acc += row[r];
-  bofs[i] = rptr[r0] + acc;
-}
-
-// warp-aggregated shared-memory cursor: lanes with equal key share one atomic
-__device__ __forceinline__ int agg_slot(int *ctr, int key, bool active) {
-  const unsigned act = __ballot_sync(0xffffffffu, active);
-  int slot = 0;
-  if (active) {
-    const unsigned peers = __match_any_sync(act, key);
-    const int leader = __ffs(peers) - 1;
-    const int lane = threadIdx.x & 31;
-    const int rank = __popc(peers & ((1u << lane) - 1u));
-    int base = 0;
-    if (lane == leader) base = atomicAdd(&ctr[key], __popc(peers));
-    base = __shfl_sync(peers, base, leader);
-    slot = base + rank;
-  }
-  return slot;
+  long long acc = 0;
+  for (int64_t r = r0 + lane; r < r1; r += 32) acc += row[r];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) bofs[i] = rptr[r0] + acc;
 }
 
 __global__ void __launch_bounds__(kTraverseThreads)
@@ -591,10 +578,9 @@ bucket_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restric
       for (int q = 0; q < kInFlight; ++q) {
         if (pos0 + 32 * q >= sp.b) break;   // warp-uniform
         const bool ok = rw[q] >= 0;
-        const int b = ok ? (rw[q] >> sh) : 0;
-        const int slot = agg_slot(bcur, b, ok);
         if (ok) {
-          const int64_t o = bbase[b] + slot;
+          const int b = rw[q] >> sh;
+          const int64_t o = bbase[b] + atomicAdd(&bcur[b], 1);
           if (o < cap)
             tmp[o] = make_double2(
                 __longlong_as_double((long long)(((uint64_t)(uint32_t)rw[q] << 32) | (uint32_t)sp.d)),
@@ -1059,7 +1045,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     const int nb = (int)ceil_div(n_rows, (int64_t)1 << sh);
     int64_t *bofs = (int64_t *)P(L.o_bofs);
     double2 *tmp = (double2 *)P(L.o_tmp);
-    bucket_offsets_kernel<<<(unsigned)ceil_div((int64_t)grid * nb, 256), 256, 0, st>>>(
+    bucket_offsets_kernel<<<(unsigned)ceil_div((int64_t)grid * nb * 32, 256), 256, 0, st>>>(
         cmat, grid, n_rows, sh, nb, rptr, bofs);
     RCP_LAUNCH_CHECK("bucket_offsets");
     bucket_scatter_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, d_vals,
