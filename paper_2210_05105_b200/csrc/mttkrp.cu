@@ -38,7 +38,6 @@ int sm_count() {
 constexpr int kMaxModes = 8;
 constexpr int kPrivRows = 49152;   // CTA-private row histogram limit (int32 in smem)
 constexpr int kSpmmChunk = 256;    // entries per warp in the segmented reduction
-constexpr int kSpmmU = 4;          // entries (Hs-row loads) in flight per lane
 
 // Row stride of the scaled KRP rows Hs: a multiple of 16 doubles, so every row starts on a
 // 128-byte line and a warp's double2 row load touches ceil(R/16) lines, not one more.
@@ -712,12 +711,15 @@ spmm_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__r
 }
 
 // Fused-path variant: packed entries, Hs rows at the padded stride, each lane owns a
-// column pair loaded as one double2 (one load instruction per entry for R <= 64).
+// column pair loaded as one double2 (one load instruction per entry for R <= 64).  The
+// warp loads 32 entries at once (one per lane) and broadcasts them with shuffles: a
+// broadcast load would cost the L1 as many register-writeback cycles as an Hs row
+// (measured: writeback was the limiter at ~75% busy).
 template <int NP>
 __global__ void __launch_bounds__(256)
 spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__restrict__ nnzp,
-                   const double2 *__restrict__ ent,
-                   const double *__restrict__ Hs, int R, double *__restrict__ out) {
+                   const double2 *__restrict__ ent, const double *__restrict__ Hs, int R,
+                   double *__restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int Rp = hs_stride(R);
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -730,48 +732,12 @@ spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64
     const int64_t c0 = ch * kSpmmChunk;
     const int64_t c1 = min(c0 + kSpmmChunk, nnz);
     int64_t row = floor_index(rptr, n_rows + 1, c0);   // (top levels stay in L1)
-    int64_t e = c0;
-    while (e < c1) {
-      const int64_t rs = rptr[row], re = rptr[row + 1];
-      const int64_t stop = min(re, c1);
-      if (stop > e) {
-        double2 acc[NP];
+    int64_t rs = rptr[row], re = rptr[row + 1];
+    double2 acc[NP];
 #pragma unroll
-        for (int j = 0; j < NP; ++j) acc[j] = make_double2(0.0, 0.0);
-        int64_t x = e;
-        for (; x + kSpmmU <= stop; x += kSpmmU) {
-          double2 en[kSpmmU];
-#pragma unroll
-          for (int q = 0; q < kSpmmU; ++q) en[q] = ent[x + q];
-#pragma unroll
-          for (int j = 0; j < NP; ++j) {
-            const int c2 = lane + 32 * j;
-            if (2 * c2 < R) {
-              double2 h[kSpmmU];
-#pragma unroll
-              for (int q = 0; q < kSpmmU; ++q)
-                h[q] = H2[(int64_t)(int32_t)__double_as_longlong(en[q].x) * Rp2 + c2];
-#pragma unroll
-              for (int q = 0; q < kSpmmU; ++q) {
-                acc[j].x = fma(en[q].y, h[q].x, acc[j].x);
-                acc[j].y = fma(en[q].y, h[q].y, acc[j].y);
-              }
-            }
-          }
-        }
-        for (; x < stop; ++x) {
-          const double2 en = ent[x];
-          const int64_t d = (int32_t)__double_as_longlong(en.x);
-#pragma unroll
-          for (int j = 0; j < NP; ++j) {
-            const int c2 = lane + 32 * j;
-            if (2 * c2 < R) {
-              const double2 h = H2[d * Rp2 + c2];
-              acc[j].x = fma(en.y, h.x, acc[j].x);
-              acc[j].y = fma(en.y, h.y, acc[j].y);
-            }
-          }
-        }
+    for (int j = 0; j < NP; ++j) acc[j] = make_double2(0.0, 0.0);
+    auto flush = [&]() {
+      if (re > rs) {
         const bool whole = (rs >= c0) && (re <= c1);
 #pragma unroll
         for (int j = 0; j < NP; ++j) {
@@ -787,10 +753,67 @@ spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64
             }
           }
         }
-        e = stop;
       }
-      ++row;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) acc[j] = make_double2(0.0, 0.0);
+    };
+    for (int64_t base = c0; base < c1; base += 32) {
+      const int nb = (int)min((int64_t)32, c1 - base);
+      double2 mine = make_double2(0.0, 0.0);
+      if (lane < nb) mine = ent[base + lane];
+      const int md = (int)(int32_t)__double_as_longlong(mine.x);
+      const double mv = mine.y;
+      int q = 0;
+      while (q < nb) {
+        while (base + q >= re) {   // next non-finished row (warp-uniform)
+          flush();
+          ++row;
+          rs = re;
+          re = rptr[row + 1];
+        }
+        const int run = (int)min((int64_t)(nb - q), re - (base + q));   // entries of this row here
+        int t = 0;
+        for (; t + 4 <= run; t += 4) {
+          int dq[4];
+          double vq[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            dq[u] = __shfl_sync(0xffffffffu, md, q + t + u);
+            vq[u] = __shfl_sync(0xffffffffu, mv, q + t + u);
+          }
+#pragma unroll
+          for (int j = 0; j < NP; ++j) {
+            const int c2 = lane + 32 * j;
+            if (2 * c2 < R) {
+              double2 h[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) h[u] = H2[(int64_t)dq[u] * Rp2 + c2];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                acc[j].x = fma(vq[u], h[u].x, acc[j].x);
+                acc[j].y = fma(vq[u], h[u].y, acc[j].y);
+              }
+            }
+          }
+        }
+        for (; t < run; ++t) {
+          const int d = __shfl_sync(0xffffffffu, md, q + t);
+          const double v = __shfl_sync(0xffffffffu, mv, q + t);
+#pragma unroll
+          for (int j = 0; j < NP; ++j) {
+            const int c2 = lane + 32 * j;
+            if (2 * c2 < R) {
+              const double2 h = H2[(int64_t)d * Rp2 + c2];
+              acc[j].x = fma(v, h.x, acc[j].x);
+              acc[j].y = fma(v, h.y, acc[j].y);
+            }
+          }
+        }
+        q += run;
+      }
     }
+    // the row holding the chunk's last entry
+    flush();
   }
 }
 
