@@ -38,6 +38,7 @@ int sm_count() {
 constexpr int kMaxModes = 8;
 constexpr int kPrivRows = 49152;   // CTA-private row histogram limit (int32 in smem)
 constexpr int kSpmmChunk = 256;    // entries per warp in the segmented reduction
+constexpr int kSpmmU = 4;          // Hs-row loads in flight per lane
 
 // Row stride of the scaled KRP rows Hs: a multiple of 16 doubles, so every row starts on a
 // 128-byte line and a warp's double2 row load touches ceil(R/16) lines, not one more.
@@ -773,11 +774,11 @@ spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64
         }
         const int run = (int)min((int64_t)(nb - q), re - (base + q));   // entries of this row here
         int t = 0;
-        for (; t + 4 <= run; t += 4) {
-          int dq[4];
-          double vq[4];
+        for (; t + kSpmmU <= run; t += kSpmmU) {
+          int dq[kSpmmU];
+          double vq[kSpmmU];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kSpmmU; ++u) {
             dq[u] = __shfl_sync(0xffffffffu, md, q + t + u);
             vq[u] = __shfl_sync(0xffffffffu, mv, q + t + u);
           }
@@ -785,11 +786,11 @@ spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64
           for (int j = 0; j < NP; ++j) {
             const int c2 = lane + 32 * j;
             if (2 * c2 < R) {
-              double2 h[4];
+              double2 h[kSpmmU];
 #pragma unroll
-              for (int u = 0; u < 4; ++u) h[u] = H2[(int64_t)dq[u] * Rp2 + c2];
+              for (int u = 0; u < kSpmmU; ++u) h[u] = H2[(int64_t)dq[u] * Rp2 + c2];
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
+              for (int u = 0; u < kSpmmU; ++u) {
                 acc[j].x = fma(vq[u], h[u].x, acc[j].x);
                 acc[j].y = fma(vq[u], h[u].y, acc[j].y);
               }
