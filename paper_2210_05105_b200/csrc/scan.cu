@@ -1,5 +1,7 @@
 // Deterministic tiled prefix scans (fixed 2048-element tiles, ordered carries), used for
 // the CP-ARLS-LEV cdf (numpy cumsum analogue) and for sampled-fiber/row offsets.
+#include <cub/device/device_scan.cuh>
+
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -148,17 +150,34 @@ int scan_impl(const T *in, T *out, int64_t n_max, const int64_t *d_n, void *ws, 
 
 }  // namespace
 
+static size_t cub_scan_bytes(int64_t n_items) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (const int64_t *)nullptr, (int64_t *)nullptr,
+                                (int)(n_items > 0 ? n_items : 1));
+  return b;
+}
+
 size_t scan_ws_bytes(int64_t n_max) {
-  return (size_t)(ceil_div(n_max > 0 ? n_max : 1, kTile) + 1) * 8;
+  const size_t tiles = (size_t)(ceil_div(n_max > 0 ? n_max : 1, kTile) + 1) * 8;
+  const size_t cb = cub_scan_bytes(n_max + 1) + 256;
+  return tiles > cb ? tiles : cb;
 }
 
 int scan_f64_inclusive(const double *in, double *out, int64_t n, void *ws, cudaStream_t st) {
   return scan_impl<double>(in, out, n, nullptr, ws, 0, st);
 }
 
+// Integer offsets: one CUB decoupled-look-back pass over n_max + 1 items (exact in any
+// order).  out[i] for i <= n depends only on in[0, n), so the device count d_n needs no
+// host round trip; in[] must have n_max + 1 readable items.
 int scan_i64_exclusive(const int64_t *in, int64_t *out, int64_t n_max, const int64_t *d_n,
                        void *ws, cudaStream_t st) {
-  return scan_impl<int64_t>(in, out, n_max, d_n, ws, 1, st);
+  (void)d_n;
+  if (n_max < 0) return RCP_ERR_ARG;
+  size_t bytes = cub_scan_bytes(n_max + 1);
+  RCP_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws, bytes, in, out, (int)(n_max + 1), st));
+  RCP_LAUNCH_CHECK("scan_i64");
+  return RCP_OK;
 }
 
 }  // namespace rcp
