@@ -38,6 +38,7 @@ int sm_count() {
 constexpr int kMaxModes = 8;
 constexpr int kPrivRows = 49152;   // CTA-private row histogram limit (int32 in smem)
 constexpr int kSpmmChunk = 256;    // entries per warp in the segmented reduction
+constexpr int64_t kItemE = 512;    // entries per traversal item (a fiber chunk)
 constexpr int kSpmmU = 4;          // Hs-row loads in flight per lane
 
 // Row stride of the scaled KRP rows Hs: a multiple of 16 doubles, so every row starts on a
@@ -106,6 +107,24 @@ __device__ __forceinline__ int64_t floor_index(const int64_t *__restrict__ a, in
     if (a[mid] <= x) lo = mid; else hi = mid;
   }
   return lo;
+}
+
+// One launch for every per-call initialisation: the output rows and the hash table.
+__global__ void mttkrp_init_kernel(double *__restrict__ out, int64_t n_out, int64_t T,
+                                   unsigned long long *__restrict__ tkey, int32_t *__restrict__ tcnt,
+                                   int32_t *__restrict__ trep, unsigned long long *__restrict__ twmin,
+                                   unsigned long long *__restrict__ twmax, double *__restrict__ twsum) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_out; i += stride)
+    out[i] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T; i += stride) {
+    tkey[i] = ~0ull;
+    tcnt[i] = 0;
+    trep[i] = INT_MAX;
+    twmin[i] = ~0ull;
+    twmax[i] = 0ull;
+    twsum[i] = 0.0;
+  }
 }
 
 // ------------------------------------------------------------------------- dedup
@@ -188,13 +207,13 @@ __global__ void compact_write_kernel(const unsigned long long *__restrict__ tkey
 
 // ------------------------------------------------------------------------ lookup
 __global__ void lookup_kernel(const int64_t *__restrict__ keys, int64_t n_cols,
-                              const int64_t *__restrict__ colptr, const int64_t *__restrict__ dkey,
+                              const int64_t *__restrict__ colptr, const int64_t *dkey,
                               const int32_t *__restrict__ dcnt, const int32_t *__restrict__ drep,
                               const int64_t *__restrict__ S, const double *__restrict__ H,
                               const double *__restrict__ dsc, int R, int Rp,
                               int64_t *__restrict__ dlo,
                               int64_t *__restrict__ dlen, double *__restrict__ Hs,
-                              int64_t *__restrict__ stats) {
+                              int64_t *icnt /* aliases dkey */, int64_t *__restrict__ stats) {
   // persistent warps over the distinct fibers; the stats counters take one atomic per CTA
   __shared__ unsigned long long cnt_ne[8], cnt_m[8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -212,6 +231,7 @@ __global__ void lookup_kernel(const int64_t *__restrict__ keys, int64_t n_cols,
       }
       dlo[d] = lo;
       dlen[d] = len;
+      icnt[d] = ceil_div(len, kItemE);   // traversal items of this fiber (aliases dkey[d])
       if (len > 0) {
         ne += 1;
         nm += (unsigned long long)(len * (int64_t)dcnt[d]);
@@ -263,15 +283,8 @@ __global__ void rows_hit_kernel(const int64_t *__restrict__ rcnt, int64_t n_rows
 // ------------------------------------------------------------ entry traversal
 // Work items: chunks of at most kItemE consecutive entries of one fiber.  A fiber's entries
 // are contiguous in the store, so a warp reads an item's rows/values fully coalesced.
-constexpr int64_t kItemE = 512;
 constexpr int kTraverseThreads = 1024;
 constexpr int kInFlight = 8;   // entries per lane with loads in flight (latency hiding)
-
-__global__ void item_count_kernel(const int64_t *__restrict__ dlen, const int64_t *__restrict__ Sp,
-                                  int64_t *__restrict__ icnt) {
-  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (d < Sp[0]) icnt[d] = ceil_div(dlen[d], kItemE);
-}
 
 // item -> fiber table: fiber d owns items [ioff[d], ioff[d+1])
 __global__ void item_fill_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
@@ -973,8 +986,10 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
       !d_stats)
     return RCP_ERR_ARG;
   cudaStream_t st = RCP_STREAM(stream);
-  if (n_rows > 0) RCP_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(double) * n_rows * R, st));
-  if (J == 0 || n_rows == 0 || n_cols == 0) return RCP_OK;
+  if (J == 0 || n_rows == 0 || n_cols == 0) {
+    if (n_rows > 0) RCP_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(double) * n_rows * R, st));
+    return RCP_OK;
+  }
   if (!d_keys || !d_colptr || !d_rows || !d_vals || !d_X || !d_H || !d_w || !d_out || !d_ws)
     return RCP_ERR_ARG;
   // the capacity of the entry arrays is implied by ws_bytes
@@ -999,15 +1014,13 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   for (int m = 0; m < kMaxModes; ++m) sd.s[m] = m < N ? h_strides[m] : 0;
 
   // 1. dedup
-  RCP_CUDA_TRY(cudaMemsetAsync(tkey, 0xff, sizeof(int64_t) * L.T, st));
-  RCP_CUDA_TRY(cudaMemsetAsync(tcnt, 0, sizeof(int32_t) * L.T, st));
-  RCP_CUDA_TRY(cudaMemsetAsync(trep, 0x7f, sizeof(int32_t) * L.T, st));
+
   unsigned long long *twmin = (unsigned long long *)P(L.o_twmin);
   unsigned long long *twmax = (unsigned long long *)P(L.o_twmax);
   double *twsum = (double *)P(L.o_twsum), *dsc = (double *)P(L.o_dsc);
-  RCP_CUDA_TRY(cudaMemsetAsync(twmin, 0xff, sizeof(int64_t) * L.T, st));
-  RCP_CUDA_TRY(cudaMemsetAsync(twmax, 0, sizeof(int64_t) * L.T, st));
-  RCP_CUDA_TRY(cudaMemsetAsync(twsum, 0, sizeof(double) * L.T, st));
+  mttkrp_init_kernel<<<4 * sm_count(), 256, 0, st>>>(d_out, n_rows * (int64_t)R, L.T, tkey, tcnt,
+                                                      trep, twmin, twmax, twsum);
+  RCP_LAUNCH_CHECK("mttkrp_init");
   hash_insert_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(
       d_X, N, J, k, sd, L.T - 1, d_w, tkey, tcnt, trep, twmin, twmax, twsum);
   RCP_LAUNCH_CHECK("hash_insert");
@@ -1020,7 +1033,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   // 2. lookup + scaled KRP rows
   lookup_kernel<<<(unsigned)std::min<int64_t>(ceil_div(J * 32, 256), 8LL * sm_count()), 256, 0, st>>>(
       d_keys, n_cols, d_colptr, dkey, dcnt, drep, S, d_H, dsc, R, hs_stride(R), dlo, dlen, Hs,
-      d_stats);
+      dkey, d_stats);
   RCP_LAUNCH_CHECK("lookup");
   // 3. fiber offsets
   int rc = scan_i64_exclusive(dlen, doff, J, S, scan_ws, st);
@@ -1030,8 +1043,6 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   // 3b. work items: fiber chunks of <= kItemE entries (dkey reused for the counts)
   int64_t *icnt = dkey;
   int64_t *ioff = (int64_t *)P(L.o_ioff);
-  item_count_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(dlen, S, icnt);
-  RCP_LAUNCH_CHECK("item_count");
   rc = scan_i64_exclusive(icnt, ioff, J, S, scan_ws, st);
   if (rc) return rc;
   int32_t *ifib = (int32_t *)P(L.o_ifib);
