@@ -137,8 +137,13 @@ __device__ __forceinline__ double rescale(double r, double T, bool right) {
 
 __global__ void walk_prepare_kernel(const int64_t *__restrict__ hkey_in, int64_t J,
                                     const int32_t *__restrict__ sel, int32_t selv,
-                                    int64_t *__restrict__ key, int32_t *__restrict__ idx) {
+                                    int64_t *__restrict__ key, int32_t *__restrict__ idx,
+                                    int *__restrict__ ctl, unsigned long long *__restrict__ prof) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (blockIdx.x == 0) {   // control words and the per-level timing record
+    for (int q = threadIdx.x; q < (int)(kCtlBytes / sizeof(int)); q += blockDim.x) ctl[q] = 0;
+    for (int q = threadIdx.x; q < (int)(kProfBytes / 8); q += blockDim.x) prof[q] = 0ull;
+  }
   if (s >= J) return;
   const bool mine = !sel || sel[s] == selv;
   key[s] = mine ? (hkey_in ? hkey_in[s] : 0) : INT64_MAX;
@@ -211,7 +216,7 @@ __host__ __device__ __forceinline__ int split_pos(int e, int n2) {
 __global__ void walk_tables_kernel(const double *__restrict__ Mfull, int R, double *__restrict__ Mp,
                                    uint32_t *__restrict__ pairs) {
   const int Rt = R * (R + 1) / 2, Rs = tri_stride(R), n2 = Rs / 2;
-  for (int e = threadIdx.x; e < Rs; e += blockDim.x) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < Rs; e += gridDim.x * blockDim.x) {
     const int ps = split_pos(e, n2);
     if (e >= Rt) {
       Mp[ps] = 0.0;
@@ -601,7 +606,8 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   double *gm = (double *)(w + L.o_gm);
   void *cub_tmp = w + L.o_cub;
   const unsigned gb = (unsigned)ceil_div(J, 256);
-  walk_prepare_kernel<<<gb, 256, 0, st>>>(d_hkey, J, d_sel, sel_value, key, idx);
+  walk_prepare_kernel<<<gb, 256, 0, st>>>(d_hkey, J, d_sel, sel_value, key, idx, ctl,
+                                          (unsigned long long *)(w + L.o_prof));
   RCP_LAUNCH_CHECK("walk_prepare");
   // group samples by key (only the key's bits); level 0 holds their uniforms in that order
   int32_t *idx3 = (int32_t *)(w + L.o_idx3);
@@ -611,12 +617,10 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   RCP_LAUNCH_CHECK("walk_sort_key");
   walk_fill_r_kernel<<<gb, 256, 0, st>>>(idx2, J, key0, key1, d_override, d_rin, r);
   RCP_LAUNCH_CHECK("walk_fill_r");
-  RCP_CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlBytes, st));
-  RCP_CUDA_TRY(cudaMemsetAsync(w + L.o_prof, 0, kProfBytes, st));
   walk_seed_kernel<<<gb, 256, 0, st>>>(key2, idx2, J, d_sel ? d_pmp_i : nullptr, runs, ctl);
   RCP_LAUNCH_CHECK("walk_seed");
   // this walk's M' tables and G (.) M' for every node
-  walk_tables_kernel<<<1, 256, 0, st>>>(d_M, R, Mp, pairs);
+  walk_tables_kernel<<<(unsigned)ceil_div(tri_stride(R), 128), 128, 0, st>>>(d_M, R, Mp, pairs);
   RCP_LAUNCH_CHECK("walk_tables");
   {
     const int Rs = tri_stride(R);

@@ -234,8 +234,7 @@ class RankState:
             ops.sts_rank_walk(node_grams, depth, self.P, leaf_rank, self.M, self.H if not first else self._ones_H(),
                               self.J, key, override, self.owner, self.rtop, self.pmp[i])
             sel, rin = self.owner, self.rtop
-        else:
-            self.pmp[i].fill_(1.0)
+        else:   # the walk / flat draw sets every sample's probability (no rank-level factor)
             sel, rin = None, None
         if self.P == 1 and first and override is None and self.n[i] > 0:
             # every sample shares H = ones: one inverse CDF over all rows' masses u M u^T
