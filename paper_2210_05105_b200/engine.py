@@ -51,6 +51,50 @@ def default_leaf(n, R, budget_bytes=4 << 30):
     return L
 
 
+class ShufflePrefetch:
+    """Generator.permutation(J) of the CP-ARLS-LEV SHUFFLE streams (ref samplers.py:183-185)
+    computed ahead on host threads into pinned buffers.  The permutation is a sequential
+    rejection-sampling chain (host native code, ~1 ms for J = 65536; the ctypes call
+    releases the GIL); it depends only on (seed, round, k, i), so the next round's six are
+    produced while the GPU runs the current one and uploaded asynchronously."""
+
+    def __init__(self, seed, J, N, workers=4):
+        from concurrent.futures import ThreadPoolExecutor
+        self.seed, self.J, self.N = int(seed), int(J), int(N)
+        self.pool = ThreadPoolExecutor(max_workers=workers)
+        self.futs = {}
+        self.inflight = []   # (event, pinned buffer) kept alive until its copy is done
+
+    def _make(self, rnd, k, i):
+        t = torch()
+        key = np.array(rng.stream_key(self.seed, rng.SHUFFLE, rnd, k, i), dtype=np.uint64)
+        buf = t.empty(self.J, dtype=t.int64, pin_memory=True)
+        from . import _lib
+        _lib.call("rcp_permutation_host", key.ctypes.data, self.J, buf.data_ptr())
+        return buf
+
+    def _request(self, rnd):
+        for k in range(self.N):
+            for i in range(self.N):
+                if i != k and (rnd, k, i) not in self.futs:
+                    self.futs[(rnd, k, i)] = self.pool.submit(self._make, rnd, k, i)
+
+    def copy_to(self, dst, rnd, k, i):
+        t = torch()
+        self._request(rnd)
+        self._request(rnd + 1)
+        fut = self.futs.pop((rnd, k, i))
+        buf = fut.result()
+        dst.copy_(buf, non_blocking=True)
+        ev = t.cuda.Event()
+        ev.record()
+        self.inflight.append((ev, buf))
+        while self.inflight and self.inflight[0][0].query():
+            self.inflight.pop(0)
+        for key in [q for q in self.futs if q[0] < rnd]:   # rounds that will not come back
+            self.futs.pop(key)
+
+
 class LocalComm:
     """P virtual ranks in one process (list collectives, rank order)."""
 
@@ -116,6 +160,7 @@ class RankState:
         self.prob_tmp = t.zeros(J, **f64)
         self.urow_tmp = t.zeros((J, R), **f64) if self.P > 1 else None
         self.perm = t.zeros(J, dtype=t.int64, device=dev)
+        self.shuffles = None   # ShufflePrefetch, created on the first CP-ARLS-LEV fold
         self.hkey = t.zeros(J, dtype=t.int64, device=dev)
         self.flat_dist = self.flat_cdf = self.flat_mass = None
         self.chain_pinv = t.zeros((R, R), **f64)
@@ -290,9 +335,9 @@ class RankState:
         return q
 
     def arls_fold(self, i, k, rnd, first, rows, probs, urows):
-        key = rng.stream_key(self.seed, rng.SHUFFLE, rnd, k, i)
-        perm = rng.permutation(key, self.J)
-        self.perm.copy_(self.t.from_numpy(perm), non_blocking=False)
+        if self.shuffles is None:
+            self.shuffles = ShufflePrefetch(self.seed, self.J, self.N)
+        self.shuffles.copy_to(self.perm, rnd, k, i)
         self.ops.batch_fold(self.perm, rows, probs, self.U[i] if urows is None else None,
                             self.lo[i], urows, first, self.X[i], self.pmp[i], self.H)
 
