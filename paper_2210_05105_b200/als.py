@@ -183,6 +183,7 @@ class AlsSession:
     def __init__(self, cluster):
         self.cl = cluster
         self.sigma = None
+        self.copy = None   # copy stream for the host transfers
 
     def pinned_factors(self):
         t = torch()
@@ -195,20 +196,39 @@ class AlsSession:
 
     def step_host(self, factors_in, factors_out, rnd):
         """Upload factors (pinned host) -> rebuild sampler state -> one ALS round ->
-        download the updated factors and sigma."""
+        download the updated factors and sigma.  Transfers run on a copy stream: mode j's
+        upload overlaps the rebuild of the modes before it, and factor k's download
+        overlaps the solves after k."""
         t = torch()
         r0 = self.cl.ranks[0]
         if len(self.cl.ranks) != 1:
             raise ValueError("step_host drives one rank per process (P=1 or SPMD)")
-        for j, h in enumerate(factors_in):
-            r0.U[j].copy_(h, non_blocking=True)
+        main = t.cuda.current_stream()
+        if self.copy is None:
+            self.copy = t.cuda.Stream(device=main.device)
+        self.copy.wait_stream(main)   # previous users of the factor buffers are done
+        ups = []
+        with t.cuda.stream(self.copy):
+            for j, h in enumerate(factors_in):
+                r0.U[j].copy_(h, non_blocking=True)
+                ev = t.cuda.Event()
+                ev.record()
+                ups.append(ev)
         for j in range(r0.N):
+            main.wait_event(ups[j])
             self.cl.rebuild(j)
-        self.cl.round(rnd, check=False)
-        for j, h in enumerate(factors_out):
-            h.copy_(r0.U[j], non_blocking=True)
+
+        def download(k):
+            ev = t.cuda.Event()
+            ev.record()
+            self.copy.wait_event(ev)
+            with t.cuda.stream(self.copy):
+                factors_out[k].copy_(r0.U[k], non_blocking=True)
+
+        self.cl.round(rnd, check=False, on_solved=download)
         self.sigma = r0.sigma.to("cpu", non_blocking=True)
-        t.cuda.current_stream().synchronize()
+        main.wait_stream(self.copy)
+        main.synchronize()
         self.cl.check("in AlsSession.step_host")
         return factors_out
 

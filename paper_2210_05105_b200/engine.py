@@ -573,9 +573,13 @@ class Cluster:
         for r in self.ranks:
             r.ops.status.check(where)
 
-    def round(self, rnd, check=True):
+    def round(self, rnd, check=True, on_solved=None):
+        """One ALS round; on_solved(k) is called (host side, stream-ordered) once factor k
+        is final for the round (after its update and renormalisation)."""
         for k in range(self.N):
             self.solve(k, rnd)
+            if on_solved is not None:
+                on_solved(k)
             if check:
                 self.check("after round %d mode %d solve" % (rnd, k))
 

@@ -169,3 +169,30 @@ def test_all_ones_full_cover_reproduces_exact(P):
     got = P.downsampled_mttkrp(P.gather_sampled_nonzeros_to_csr(m, X, 0), H, np.ones(9))
     ref = P.mttkrp_exact(m, factors)
     assert np.abs(got - ref).max() < 1e-12
+
+
+def test_host_step_api_matches_device_round(P):
+    """AlsSession.step_host (pinned host factors in, overlapped transfers, factors and sigma
+    out) computes the same round as the device-resident engine."""
+    import torch
+    from paper_2210_05105_b200.als import AlsSession
+    from paper_2210_05105_b200.engine import make_local_cluster
+    dims = (300, 200, 150)
+    idx, vals = synth.small_random(dims, 20000, seed=3)
+    dev = torch.device("cuda")
+    ti, tv = torch.as_tensor(idx, device=dev), torch.as_tensor(vals, device=dev)
+    a = make_local_cluster(dims, ti, tv, 8, 1024, "sts", 7)
+    b = make_local_cluster(dims, ti, tv, 8, 1024, "sts", 7)
+    a.round(1)
+    b.round(1)
+    sess = AlsSession(a)
+    host_in, host_out = sess.pinned_factors(), sess.pinned_factors()
+    sess.step_host(host_in, host_out, 2)
+    for j in range(3):          # step_host re-uploads the same factors, then rebuilds
+        b.rebuild(j)
+    b.round(2)
+    for j in range(3):
+        got = host_out[j].numpy()
+        ref = b.ranks[0].U[j].cpu().numpy()
+        assert rel_err(got, ref) < 1e-12
+    assert rel_err(sess.sigma.numpy(), b.ranks[0].sigma.cpu().numpy()) < 1e-12
