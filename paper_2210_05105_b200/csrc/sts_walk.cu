@@ -62,6 +62,7 @@ struct Run {
   int32_t level;       // tree level of `node`
   int32_t node;        // node index within its level
   double prob;         // product of the step probabilities so far
+  double qv;           // h'(G_node (.) M)h when known (left children inherit it), else NaN
 };
 
 struct WalkWs {
@@ -190,6 +191,7 @@ __global__ void walk_seed_kernel(const int64_t *__restrict__ key, const int32_t 
     rr.level = 0;
     rr.node = 0;
     rr.prob = prob;
+    rr.qv = __longlong_as_double(0x7ff8000000000000LL);   // unknown
     runs[t + q] = rr;
   }
 }
@@ -255,7 +257,7 @@ __global__ void walk_gm_kernel(const double *__restrict__ tree, const double2 *_
 
 __device__ __forceinline__ void push_child(Run *runs, int *gen_cnt, int64_t base, int64_t cap,
                                            int *status, const Run &par, int32_t lo, int32_t hi,
-                                           double T, bool right, int depth, int lane) {
+                                           double T, bool right, double qv, int depth, int lane) {
   const int lev = par.level;
   const int32_t chunk = (lev + 1 == depth) ? kLeafChunk : kMaxRun;
   for (int32_t c0 = lo; c0 < hi; c0 += chunk) {
@@ -271,6 +273,7 @@ __device__ __forceinline__ void push_child(Run *runs, int *gen_cnt, int64_t base
       c.level = lev + 1;
       c.node = 2 * par.node + (right ? 1 : 0);
       c.prob = par.prob * (right ? (1.0 - T) : T);
+      c.qv = qv;
       runs[base + t] = c;
     }
   }
@@ -351,37 +354,49 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
       __syncwarp();
       if (level < depth) {
         // child masses <GM_child, h h^T> over the packed triangle, two positions per step
+        // T = max(q_left, 0) / q_node (ref samplers.py:423-451).  q_node is inherited from
+        // the parent by left children; right children and seeds compute it here, in the
+        // same pass as q_left.
         const int64_t v = run.node;
         const double2 *GL = reinterpret_cast<const double2 *>(
             gm + ((1LL << (level + 1)) - 1 + 2 * v) * (int64_t)Rs);
-        const double2 *GR = GL + Rs / 2;
+        const double2 *GV = reinterpret_cast<const double2 *>(
+            gm + ((1LL << level) - 1 + v) * (int64_t)Rs);
         const uint2 *PR = reinterpret_cast<const uint2 *>(pairs);
-        double qL = 0.0, qR = 0.0, qL2 = 0.0, qR2 = 0.0;
+        const bool known = !isnan(run.qv);
+        double qL = 0.0, qV = 0.0, qL2 = 0.0, qV2 = 0.0;
         const int n2 = Rs / 2;
+        if (known) {
 #pragma unroll 4
-        for (int e = lane; e < n2; e += 32) {
-          const double2 gl = __ldg(GL + e);
-          const double2 gr = __ldg(GR + e);
-          const uint2 ab = PR[e];
-          const double h0 = hv[ab.x & 0xffffu] * hv[ab.x >> 16];
-          const double h1 = hv[ab.y & 0xffffu] * hv[ab.y >> 16];
-          qL = fma(gl.x, h0, qL);
-          qL2 = fma(gl.y, h1, qL2);
-          qR = fma(gr.x, h0, qR);
-          qR2 = fma(gr.y, h1, qR2);
+          for (int e = lane; e < n2; e += 32) {
+            const double2 gl = __ldg(GL + e);
+            const uint2 ab = PR[e];
+            const double h0 = hv[ab.x & 0xffffu] * hv[ab.x >> 16];
+            const double h1 = hv[ab.y & 0xffffu] * hv[ab.y >> 16];
+            qL = fma(gl.x, h0, qL);
+            qL2 = fma(gl.y, h1, qL2);
+          }
+        } else {
+#pragma unroll 4
+          for (int e = lane; e < n2; e += 32) {
+            const double2 gl = __ldg(GL + e);
+            const double2 gv = __ldg(GV + e);
+            const uint2 ab = PR[e];
+            const double h0 = hv[ab.x & 0xffffu] * hv[ab.x >> 16];
+            const double h1 = hv[ab.y & 0xffffu] * hv[ab.y >> 16];
+            qL = fma(gl.x, h0, qL);
+            qL2 = fma(gl.y, h1, qL2);
+            qV = fma(gv.x, h0, qV);
+            qV2 = fma(gv.y, h1, qV2);
+          }
         }
-        qL += qL2;
-        qR += qR2;
-        qL = warp_sum(qL);
-        qR = warp_sum(qR);
-        qL = qL > 0.0 ? qL : 0.0;
-        qR = qR > 0.0 ? qR : 0.0;
-        const double tot = qL + qR;
-        if (!(tot > 0.0)) {
+        qL = warp_sum(qL + qL2);
+        const double qnode = known ? run.qv : warp_sum(qV + qV2);
+        if (!(qnode > 0.0)) {
           fail_run(lo, hi, is, Xi, status, ctl, lane);
           continue;
         }
-        double T = qL / tot;
+        double T = (qL > 0.0 ? qL : 0.0) / qnode;
         T = fmin(fmax(T, 0.0), 1.0);
         // partition the run's samples into the children's ranges of the next level's
         // buffer (left from the front, right from the back), rescaling each residual
@@ -416,10 +431,13 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
             nr += __popc(mr);
           }
         }
+        const double unknown = __longlong_as_double(0x7ff8000000000000LL);
         if (nl > 0)
-          push_child(runs, gen_cnt, end, cap_runs, status, run, lo, lo + nl, T, false, depth, lane);
+          push_child(runs, gen_cnt, end, cap_runs, status, run, lo, lo + nl, T, false, qL, depth,
+                     lane);
         if (nr > 0)
-          push_child(runs, gen_cnt, end, cap_runs, status, run, lo + nl, hi, T, true, depth, lane);
+          push_child(runs, gen_cnt, end, cap_runs, status, run, lo + nl, hi, T, true, unknown,
+                     depth, lane);
         continue;
       }
       // ---- leaf block: masses z^T M' z of its rows z = u (.) h, then each sample's
