@@ -55,20 +55,29 @@ class ShufflePrefetch:
     """Generator.permutation(J) of the CP-ARLS-LEV SHUFFLE streams (ref samplers.py:183-185)
     computed ahead on host threads into pinned buffers.  The permutation is a sequential
     rejection-sampling chain (host native code, ~1 ms for J = 65536; the ctypes call
-    releases the GIL); it depends only on (seed, round, k, i), so the next round's six are
-    produced while the GPU runs the current one and uploaded asynchronously."""
+    releases the GIL); it depends only on (seed, round, k, i), so the next round's
+    permutations are produced while the GPU runs the current one and uploaded
+    asynchronously.  Pinned buffers are recycled once their copy has completed."""
 
     def __init__(self, seed, J, N, workers=4):
+        import threading
         from concurrent.futures import ThreadPoolExecutor
         self.seed, self.J, self.N = int(seed), int(J), int(N)
         self.pool = ThreadPoolExecutor(max_workers=workers)
         self.futs = {}
-        self.inflight = []   # (event, pinned buffer) kept alive until its copy is done
+        self.free = []          # recycled pinned buffers
+        self.lock = threading.Lock()
+        self.inflight = []      # (event, buffer) until the upload is done
 
-    def _make(self, rnd, k, i):
+    def _buffer(self):
+        with self.lock:
+            if self.free:
+                return self.free.pop()
         t = torch()
+        return t.empty(self.J, dtype=t.int64, pin_memory=True)
+
+    def _make(self, rnd, k, i, buf):
         key = np.array(rng.stream_key(self.seed, rng.SHUFFLE, rnd, k, i), dtype=np.uint64)
-        buf = t.empty(self.J, dtype=t.int64, pin_memory=True)
         from . import _lib
         _lib.call("rcp_permutation_host", key.ctypes.data, self.J, buf.data_ptr())
         return buf
@@ -77,20 +86,20 @@ class ShufflePrefetch:
         for k in range(self.N):
             for i in range(self.N):
                 if i != k and (rnd, k, i) not in self.futs:
-                    self.futs[(rnd, k, i)] = self.pool.submit(self._make, rnd, k, i)
+                    self.futs[(rnd, k, i)] = self.pool.submit(self._make, rnd, k, i, self._buffer())
 
     def copy_to(self, dst, rnd, k, i):
         t = torch()
         self._request(rnd)
         self._request(rnd + 1)
-        fut = self.futs.pop((rnd, k, i))
-        buf = fut.result()
+        buf = self.futs.pop((rnd, k, i)).result()
         dst.copy_(buf, non_blocking=True)
         ev = t.cuda.Event()
         ev.record()
         self.inflight.append((ev, buf))
         while self.inflight and self.inflight[0][0].query():
-            self.inflight.pop(0)
+            with self.lock:
+                self.free.append(self.inflight.pop(0)[1])
         for key in [q for q in self.futs if q[0] < rnd]:   # rounds that will not come back
             self.futs.pop(key)
 
