@@ -251,6 +251,36 @@ int rcp_csr_spmm(const int64_t *d_row_ptr, int64_t n_rows, const int64_t *d_col,
                  const double *d_val, const double *d_H, const double *d_scale, int R,
                  double *d_out, void *stream);
 
+/* ---------------------------------------------------------------- exact fit (row F1)
+ * Ref compute_fit linalg.py:130-151: fit = 1 - sqrt(max(||T||^2 - 2<T,T_hat> + ||T_hat||^2,
+ * 0)) / ||T||.  The three scalars are computed on the device from the mode-k store.
+ *   h_U[m]  device pointer of mode m's factor rows (row-major, R columns), first row h_lo[m]
+ *           (NULL h_lo = 0); h_U[k] is ignored (d_Uk is the store's own row block).
+ *   h_strides  the store's off-mode key strides (ref matricization.py:21-38).
+ * Workspace: rcp_fit_ws_bytes(nnz).  Sums are added in a fixed order (reproducible). */
+size_t rcp_fit_ws_bytes(int64_t nnz);
+/* <T, T_hat> restricted to the store's nonzeros: sum_e v_e sum_r sigma_r U_k[row_e, r]
+ * prod_{m != k} U_m[i_m(e), r]  -> d_out[0]. */
+int rcp_fit_cross(const int64_t *d_keys, const int64_t *d_colptr, int64_t n_cols,
+                  const int32_t *d_rows, const double *d_vals, int64_t nnz, int N, int k,
+                  const int64_t *h_dims, const int64_t *h_strides, const double *const *h_U,
+                  const int64_t *h_lo, const double *d_Uk, int R, const double *d_sigma,
+                  double *d_out, void *d_ws, size_t ws_bytes, void *stream);
+/* sum_i v_i^2 -> d_out[0] (ref SparseTensorCOO.norm_squared). */
+int rcp_sum_squares(const double *d_v, int64_t n, double *d_out, void *d_ws, size_t ws_bytes,
+                    void *stream);
+/* sigma^T (G_0 (.) ... (.) G_{N-1}) sigma -> d_out[0]; d_grams N x R x R (ref
+ * linalg.py:145-146 with hadamard_gram_chain linalg.py:73-82). */
+int rcp_model_norm(const double *d_grams, int N, int R, const double *d_sigma, double *d_out,
+                   void *stream);
+/* Exact local MTTKRP (drop-in for mttkrp_exact, ref mttkrp.py:65-108): d_out (n_rows x R,
+ * local rows) = sum over the store's entries of v * prod_{m != k} U_m[i_m]. */
+int rcp_exact_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n_cols,
+                     const int32_t *d_rows, const double *d_vals, int64_t nnz, int64_t n_rows,
+                     int N, int k, const int64_t *h_dims, const int64_t *h_strides,
+                     const double *const *h_U, const int64_t *h_lo, int R, double *d_out,
+                     void *stream);
+
 #ifdef __cplusplus
 }
 #endif

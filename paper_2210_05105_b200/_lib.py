@@ -71,6 +71,13 @@ _SIGS = {
     "rcp_fiber_lookup": (_i32, [_vp, _i64, _vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp]),
     "rcp_fiber_expand": (_i32, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rcp_csr_spmm": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),
+    "rcp_fit_ws_bytes": (_sz, [_i64]),
+    "rcp_fit_cross": (_i32, [_vp, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
+                             _i32, _vp, _vp, _vp, _sz, _vp]),
+    "rcp_sum_squares": (_i32, [_vp, _i64, _vp, _vp, _sz, _vp]),
+    "rcp_model_norm": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp]),
+    "rcp_exact_mttkrp": (_i32, [_vp, _vp, _i64, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp, _vp,
+                                _vp, _i32, _vp, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

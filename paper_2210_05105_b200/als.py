@@ -145,7 +145,7 @@ def run_als(cfg: AlsConfig, tensor=None, perms=None, grid=None, partition=None,
         sigma = to_host(cl.ranks[0].sigma).copy()
         if cfg.compute_fits and (rnd % cfg.fit_every == 0 or rnd == cfg.rounds):
             tf = time.perf_counter()
-            f = compute_fit(tensor, gather_factors(cl), sigma)
+            f = cl.fit()
             best = max(best, f)
             fit_history.append((rnd, f))
             running_max.append(best)

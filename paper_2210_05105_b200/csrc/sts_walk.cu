@@ -255,18 +255,26 @@ __global__ void walk_gm_kernel(const double *__restrict__ tree, const double2 *_
 // per-sample leaf work spreads over warps.
 
 
+// Child runs are staged in a per-CTA shared buffer and published with one global
+// reservation per CTA and level (a global counter taking one atomic per child run
+// serialised ~2*10^4 same-address atomics per level); a full buffer falls back to the
+// global counter.
+constexpr int kStage = 288;
+
+struct Stage {
+  Run buf[kStage];
+  int count;
+  int base;
+};
+
 __device__ __forceinline__ void push_child(Run *runs, int *gen_cnt, int64_t base, int64_t cap,
-                                           int *status, const Run &par, int32_t lo, int32_t hi,
-                                           double T, bool right, double qv, int depth, int lane) {
+                                           int *status, Stage &stg, const Run &par, int32_t lo,
+                                           int32_t hi, double T, bool right, double qv, int depth,
+                                           int lane) {
   const int lev = par.level;
   const int32_t chunk = (lev + 1 == depth) ? kLeafChunk : kMaxRun;
   for (int32_t c0 = lo; c0 < hi; c0 += chunk) {
     if (lane == 0) {
-      const int t = atomicAdd(gen_cnt, 1);
-      if (base + t >= cap) {   // cannot happen: one level holds at most J disjoint runs
-        raise_status(status, RCP_ST_CAPACITY);
-        continue;
-      }
       Run c;
       c.lo = c0;
       c.hi = min(hi, c0 + chunk);
@@ -274,10 +282,32 @@ __device__ __forceinline__ void push_child(Run *runs, int *gen_cnt, int64_t base
       c.node = 2 * par.node + (right ? 1 : 0);
       c.prob = par.prob * (right ? (1.0 - T) : T);
       c.qv = qv;
-      runs[base + t] = c;
+      const int t = atomicAdd(&stg.count, 1);
+      if (t < kStage) {
+        stg.buf[t] = c;
+      } else {
+        const int g = atomicAdd(gen_cnt, 1);
+        if (base + g >= cap) raise_status(status, RCP_ST_CAPACITY);   // cannot happen: one
+        else runs[base + g] = c;   // level holds at most J disjoint runs
+      }
     }
   }
   __syncwarp();
+}
+
+// End of a level: the CTA's staged children go to the next level's array.
+__device__ __forceinline__ void publish_children(Run *runs, int *gen_cnt, int64_t base,
+                                                 int64_t cap, int *status, Stage &stg) {
+  __syncthreads();
+  const int n = min(stg.count, kStage);
+  if (threadIdx.x == 0) stg.base = n ? atomicAdd(gen_cnt, n) : 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t o = base + stg.base + i;
+    if (o >= cap) raise_status(status, RCP_ST_CAPACITY);
+    else runs[o] = stg.buf[i];
+  }
+  if (threadIdx.x == 0) stg.count = 0;
 }
 
 __device__ __forceinline__ void fail_run(int32_t lo, int32_t hi, const int32_t *__restrict__ idx,
@@ -327,6 +357,8 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
   // Level-synchronous: the runs of level l are [begin, end); their children go to level
   // l + 1 through that level's own counter, whose value is stable after the grid barrier.
   __shared__ int claim;
+  __shared__ Stage stg;
+  if (threadIdx.x == 0) stg.count = 0;
   int64_t begin = 0, end = min((int64_t)ld_volatile(&ctl[0]), cap_runs);
   for (int lvl = 0; lvl <= depth && end > begin; ++lvl) {
     int *gen_cnt = &ctl[kGenBase + lvl];
@@ -433,10 +465,10 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         }
         const double unknown = __longlong_as_double(0x7ff8000000000000LL);
         if (nl > 0)
-          push_child(runs, gen_cnt, end, cap_runs, status, run, lo, lo + nl, T, false, qL, depth,
+          push_child(runs, gen_cnt, end, cap_runs, status, stg, run, lo, lo + nl, T, false, qL, depth,
                      lane);
         if (nr > 0)
-          push_child(runs, gen_cnt, end, cap_runs, status, run, lo + nl, hi, T, true, unknown,
+          push_child(runs, gen_cnt, end, cap_runs, status, stg, run, lo + nl, hi, T, true, unknown,
                      depth, lane);
         continue;
       }
@@ -548,6 +580,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
       }
       if (lane == 0) atomicAdd(&ctl[2], hi - lo);
     }
+    publish_children(runs, gen_cnt, end, cap_runs, status, stg);
     grid.sync();
     const int64_t pushed_n = ld_volatile(gen_cnt);
     begin = end;
@@ -611,7 +644,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   int warps = kWalkWarps;
   while (warps > 1 && walk_smem(R, warps) > 200 * 1024) --warps;
   const size_t smem = walk_smem(R, warps);
-  if (smem > 220 * 1024) return RCP_ERR_ARG;
+  if (smem > 200 * 1024) return RCP_ERR_ARG;
   cudaStream_t st = RCP_STREAM(stream);
   char *w = (char *)d_ws;
   int64_t *key = (int64_t *)(w + L.o_key), *key2 = (int64_t *)(w + L.o_key2);
@@ -652,7 +685,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   static bool attr = false;
   if (!attr) {
     RCP_CUDA_TRY(cudaFuncSetAttribute(walk_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      220 * 1024));
+                                      200 * 1024));
     attr = true;
   }
   int per_sm = 0;

@@ -568,6 +568,61 @@ class Cluster:
         self._tick("rebuild", t0)
         self._ev("end")
 
+    # ------------------------------------------------------------ exact fit (F1)
+    def full_factor(self, j):
+        """Full mode-j factor on each local rank's device: the row blocks all-gathered and
+        placed at their global offsets.  Returns one tensor per local rank."""
+        t = torch()
+        grid = self.ranks[0].grid
+        counts = [grid.block_range(j, p)[1] - grid.block_range(j, p)[0] for p in range(self.P)]
+        blocks = self.comm.all_gather_v([r.U[j] for r in self.ranks], counts)
+        outs = []
+        for r in self.ranks:
+            full = t.empty((r.dims[j], r.R), dtype=t.float64, device=r.dev)
+            for p, blk in enumerate(blocks):
+                lo = grid.block_range(j, p)[0]
+                if counts[p]:
+                    full[lo:lo + counts[p]].copy_(blk[:counts[p]])
+            outs.append(full)
+        return outs
+
+    def fit(self):
+        """Exact fit 1 - ||T - T_hat||_F / ||T||_F of the current model (ref compute_fit
+        linalg.py:130-151), computed on the devices from the last-mode stores: every rank
+        adds v <sigma (.) prod U_m[i_m], U_last[row]> over its nonzeros, ||T||^2 over the
+        same store (cached), ||T_hat||^2 = sigma^T (Hadamard of the Grams) sigma.  One
+        all-gather of two scalars per rank at P > 1; nothing is copied to the host but the
+        three scalars."""
+        t = torch()
+        N = self.N
+        last = N - 1
+        fulls = [self.full_factor(j) if j != last else None for j in range(N)]
+        parts = []
+        for q, r in enumerate(self.ranks):
+            st = r.stores[last]
+            v = t.zeros(3, dtype=t.float64, device=r.dev)
+            if getattr(r, "norm_sq", None) is None:
+                r.norm_sq = t.zeros(1, dtype=t.float64, device=r.dev)
+                r.ops.sum_squares(st.vals, r.norm_sq)
+            v[0:1].copy_(r.norm_sq)
+            if st.nnz:
+                facs = [fulls[m][q] if m != last else None for m in range(N)]
+                r.ops.fit_cross(st, facs, [0] * N, r.U[last], r.sigma, v[1:2])
+            parts.append(v)
+        allp = self.comm.all_gather(parts)
+        tot = allp[0].clone()
+        for p in allp[1:]:
+            tot += p.to(tot.device)
+        r0 = self.ranks[0]
+        model = t.zeros(1, dtype=t.float64, device=r0.dev)
+        r0.ops.model_norm(r0.grams, r0.sigma, model)
+        norm_sq, cross = (float(x) for x in tot[:2].cpu())
+        model_sq = float(model.cpu())
+        if norm_sq == 0.0:
+            raise ValueError("fit is undefined for an all-zero tensor")
+        resid_sq = max(norm_sq - 2.0 * cross + model_sq, 0.0)
+        return 1.0 - math.sqrt(resid_sq) / math.sqrt(norm_sq)
+
     def phase_breakdown(self):
         """ms per phase from the recorded events (after synchronisation)."""
         out = {}

@@ -110,12 +110,8 @@ def mttkrp_exact(mat: Matricization, factors, offsets=None, workers=1):
         return np.zeros((mat.n_rows, R))
     dev = require_cuda()
     t = torch()
-    idx = to_dev(mat.idx, dev, t.int64)
-    prod = to_dev(mat.vals, dev, t.float64).unsqueeze(1).expand(-1, R).clone()
-    for i, f in enumerate(factors):
-        if i == j or f is None:
-            continue
-        prod *= to_dev(f, dev, t.float64)[idx[:, i] - offsets[i]]
-    out = t.zeros((mat.n_rows, R), dtype=t.float64, device=dev)
-    out.index_add_(0, idx[:, j] - mat.row_lo, prod)
+    facs = [to_dev(np.ascontiguousarray(f, dtype=np.float64), dev, t.float64)
+            if (i != j and f is not None) else None for i, f in enumerate(factors)]
+    out = t.empty((mat.n_rows, R), dtype=t.float64, device=dev)
+    ops_for(dev).exact_mttkrp(mat.store, facs, offsets, out)
     return to_host(out)

@@ -190,6 +190,51 @@ class Ops:
         self._c("rcp_csr_spmm", ptr(row_ptr), n_rows, ptr(col), ptr(val), ptr(H), ptr(scale), R,
                 ptr(out), stream_handle())
 
+    # ------------------------------------------------------------- exact fit (F1)
+    @staticmethod
+    def _factor_arrays(factors, los, N):
+        import ctypes as C
+        U = (C.c_void_p * N)(*[C.c_void_p(ptr(f)) if f is not None else None for f in factors])
+        lo = np.ascontiguousarray([int(x) for x in los], dtype=np.int64)
+        return U, lo
+
+    def fit_cross(self, store, factors, los, Uk, sigma, out):
+        """out[0] = sum over the store's entries of v <sigma (.) prod_m U_m[i_m], U_k[row]>."""
+        N = len(store.dims)
+        R = Uk.shape[1]
+        U, lo = self._factor_arrays(factors, los, N)
+        dims = np.ascontiguousarray(store.dims, dtype=np.int64)
+        strides = np.ascontiguousarray([max(int(x), 1) for x in store.strides], dtype=np.int64)
+        w = self.ws("fit", self.lib.rcp_fit_ws_bytes(store.nnz))
+        self._c("rcp_fit_cross", ptr(store.keys), ptr(store.colptr), store.n_cols, ptr(store.rows),
+                ptr(store.vals), store.nnz, N, int(store.mode), dims.ctypes.data,
+                strides.ctypes.data, U, lo.ctypes.data, ptr(Uk), R, ptr(sigma), ptr(out), ptr(w),
+                w.numel(), stream_handle())
+        return out
+
+    def sum_squares(self, v, out):
+        n = v.numel()
+        w = self.ws("fit", self.lib.rcp_fit_ws_bytes(n))
+        self._c("rcp_sum_squares", ptr(v), n, ptr(out), ptr(w), w.numel(), stream_handle())
+        return out
+
+    def model_norm(self, grams, sigma, out):
+        N, R = grams.shape[0], grams.shape[1]
+        self._c("rcp_model_norm", ptr(grams), N, R, ptr(sigma), ptr(out), stream_handle())
+        return out
+
+    def exact_mttkrp(self, store, factors, los, out):
+        N = len(store.dims)
+        R = out.shape[1]
+        U, lo = self._factor_arrays(factors, los, N)
+        dims = np.ascontiguousarray(store.dims, dtype=np.int64)
+        strides = np.ascontiguousarray([max(int(x), 1) for x in store.strides], dtype=np.int64)
+        self._c("rcp_exact_mttkrp", ptr(store.keys), ptr(store.colptr), store.n_cols,
+                ptr(store.rows), ptr(store.vals), store.nnz, store.n_rows, N, int(store.mode),
+                dims.ctypes.data, strides.ctypes.data, U, lo.ctypes.data, R, ptr(out),
+                stream_handle())
+        return out
+
 
 _OPS = {}
 

@@ -1,0 +1,122 @@
+"""Build and run the SpMM lab on the workspace of real C3 sampled-MTTKRP calls (GPU box).
+    python tools/lab/run_lab.py [variants...]"""
+import ctypes
+import glob
+import json
+import os
+import subprocess
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+LAB = os.path.join(ROOT, "tools", "lab")
+
+
+def build():
+    so = os.path.join(LAB, "libspmm_lab.so")
+    srcs = [s for s in sorted(glob.glob(os.path.join(ROOT, "paper_2210_05105_b200", "csrc", "*.cu")))
+            if not s.endswith(("mttkrp.cu", "sts_walk.cu"))] + \
+        [os.path.join(LAB, "spmm_lab.cu"), os.path.join(LAB, "walk_lab.cu")]
+    cmd = ["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+           "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-shared",
+           "-o", so] + srcs
+    if not os.path.exists(so) or any(os.path.getmtime(s) > os.path.getmtime(so) for s in srcs):
+        subprocess.check_call(cmd)
+    return so
+
+
+def main():
+    variants = [int(v) for v in sys.argv[1:]] or [0, 1, 2, 3, 4, 5, 6, 7, 10, 11, 12]
+    lab = ctypes.CDLL(build())
+    import bench
+    from paper_2210_05105_b200 import _lib
+    from paper_2210_05105_b200.engine import make_local_cluster
+    dev = torch.device("cuda", 0)
+    _lib.load()
+    cfg = os.environ.get("CFG", "c3")
+    sampler = os.environ.get("SAMPLER", "sts")
+    c, idx, vals = bench.make_tensor(cfg, 0, dev)
+    cl = make_local_cluster(c["dims"], idx, vals, c["R"], c["J"], sampler, 0)
+    me = cl.ranks[0]
+    for rnd in range(1, 4):
+        cl.round(rnd)
+    orig = me.mttkrp
+    res = []
+
+    def hook(k):
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        out = orig(k)
+        e.record()
+        torch.cuda.synchronize()
+        ref = out.clone()
+        ws = me.ops._ws["mttkrp"]
+        n = me.n[k]
+        row = {"mode": k, "n_rows": n, "product_call_ms": s.elapsed_time(e)}
+        tmp = torch.empty_like(ref)
+        for v in variants:
+            for gm in (8,) if v < 10 else (2, 4):
+                ms = ctypes.c_float(0)
+                rc = lab.lab_spmm(v, ctypes.c_void_p(ws.data_ptr()), ctypes.c_size_t(ws.numel()),
+                                  ctypes.c_int64(me.J), ctypes.c_int64(n), me.R,
+                                  ctypes.c_void_p(tmp.data_ptr()), 5, ctypes.byref(ms), gm)
+                torch.cuda.synchronize()
+                err = float((tmp - ref).abs().max() / ref.abs().max())
+                row["v%d_g%d" % (v, gm)] = {"rc": rc, "ms": round(ms.value, 4), "relerr": err}
+        res.append(row)
+        print(json.dumps(row), flush=True)
+        return out
+
+    if os.environ.get("LABMODE") == "probe":
+        out = torch.zeros(28818 * 64 + 64, dtype=torch.float64, device=dev)
+        for mode, name in ((0, "red_2x_f64"), (1, "red_1x_f64"), (2, "gather_v2")):
+            ms = ctypes.c_float(0)
+            nf = 1 << 20
+            lab.lab_red_probe(ctypes.c_void_p(out.data_ptr()), ctypes.c_int64(28818), 50,
+                              ctypes.c_int64(nf), mode, ctypes.byref(ms))
+            print(json.dumps({"probe": name, "rows": nf, "ms": ms.value,
+                              "GB/s": nf * 400 / ms.value / 1e6}), flush=True)
+        return
+    if os.environ.get("LABMODE") == "walk":
+        ops = me.ops
+        owalk = ops.sts_walk
+
+        def walk_hook(tree, U, leaf, *a, **kw):
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            owalk(tree, U, leaf, *a, **kw)
+            e.record()
+            torch.cuda.synchronize()
+            J = a[3]
+            buf = (ctypes.c_ulonglong * 64)()
+            lab.lab_walk_prof(ctypes.c_void_p(ops._ws["sts_walk"].data_ptr()), ctypes.c_int64(J),
+                              ctypes.c_int64(U.shape[0]), int(leaf), U.shape[1], buf)
+            t = list(buf)
+            lv = []
+            for l in range(30):
+                if t[2 * l] == 0:
+                    break
+                lv.append((t[2 * l + 1], t[2 * l]))
+            end = t[2 * 31]
+            per = [{"runs": r, "us": round(((lv[i + 1][1] if i + 1 < len(lv) else end) - t0) / 1e3, 1)}
+                   for i, (r, t0) in enumerate(lv)]
+            row = {"walk_n": U.shape[0], "leaf": int(leaf), "walk_ms": s.elapsed_time(e),
+                   "kernel_us": round((end - lv[0][1]) / 1e3, 1), "levels": per}
+            res.append(row)
+            print(json.dumps(row), flush=True)
+        ops.sts_walk = walk_hook
+    else:
+        me.mttkrp = hook
+    cl.round(4)
+    torch.cuda.synchronize()
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "lab_%s_%s.json" % (cfg, sampler)), "w") as f:
+        json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,74 @@
+"""Structure of the sampled MTTKRP operands in a real round (design input, GPU box):
+distinct fibers, fiber lengths, rows hit, entries per row, and how many (row tile, fiber)
+pairs a row-tiled traversal would visit.  Writes gpurun_out/mttkrp_stats.json."""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+from paper_2210_05105_b200 import _lib  # noqa: E402
+from paper_2210_05105_b200.engine import make_local_cluster  # noqa: E402
+
+cfg = os.environ.get("CFG", "c3")
+sampler = os.environ.get("SAMPLER", "sts")
+dev = torch.device("cuda", 0)
+_lib.load()
+c, idx, vals = bench.make_tensor(cfg, 0, dev)
+cl = make_local_cluster(c["dims"], idx, vals, c["R"], c["J"], sampler, 0)
+me = cl.ranks[0]
+res = []
+orig = me.mttkrp
+
+
+def hook(k):
+    st = me.stores[k]
+    key = torch.zeros(me.J, dtype=torch.int64, device=dev)
+    for m in range(me.N):
+        if m != k:
+            key += me.X[m] * int(st.strides[m])
+    u, cnt = torch.unique(key, return_counts=True)
+    c_ = torch.searchsorted(st.keys, u)
+    c_ = c_.clamp(max=st.n_cols - 1)
+    hit = st.keys[c_] == u
+    lo = torch.where(hit, st.colptr[c_], torch.zeros_like(c_))
+    ln = torch.where(hit, st.colptr[c_ + 1] - st.colptr[c_], torch.zeros_like(c_))
+    nnz_d = int(ln.sum())
+    fid = torch.repeat_interleave(torch.arange(u.numel(), device=dev), ln)
+    off = torch.cumsum(ln, 0) - ln
+    pos = torch.repeat_interleave(lo - off, ln) + torch.arange(nnz_d, device=dev)
+    rows = st.rows[pos].long()
+    rh = torch.bincount(rows, minlength=st.n_rows)
+    d = {"mode": k, "n_rows": st.n_rows, "n_cols": st.n_cols, "store_nnz": st.nnz,
+         "S_d": int(u.numel()), "S_ne": int(hit.sum()), "nnz_d": nnz_d,
+         "nnz_m": int((ln * cnt).sum()), "rows_hit": int((rh > 0).sum()),
+         "fiber_len_pct": [int(x) for x in torch.quantile(ln[hit].double(), torch.tensor(
+             [0.5, 0.9, 0.99, 1.0], dtype=torch.float64, device=dev)).long()],
+         "row_cnt_pct": [int(x) for x in torch.quantile(rh.double(), torch.tensor(
+             [0.5, 0.9, 0.99, 1.0], dtype=torch.float64, device=dev)).long()],
+         "top_rows_share": [float(torch.topk(rh, t).values.sum()) / max(nnz_d, 1)
+                            for t in (1, 16, 256)],
+         "top_fibers_share": [float(torch.topk(ln, min(t, ln.numel())).values.sum()) / max(nnz_d, 1)
+                              for t in (1, 16, 256, 4096)],
+         "mult_pct": [int(x) for x in torch.quantile(cnt.double(), torch.tensor(
+             [0.5, 0.9, 0.99, 1.0], dtype=torch.float64, device=dev)).long()]}
+    pairs = {}
+    for T in (64, 256, 512, 1024, 4096):
+        nt = (st.n_rows + T - 1) // T
+        pairs[str(T)] = int(torch.unique(fid * nt + rows // T).numel())
+    d["tile_fiber_pairs"] = pairs
+    res.append(d)
+    return orig(k)
+
+
+for rnd in range(1, 4):
+    cl.round(rnd)
+me.mttkrp = hook
+cl.round(4)
+torch.cuda.synchronize()
+os.makedirs("gpurun_out", exist_ok=True)
+with open("gpurun_out/mttkrp_stats_%s_%s.json" % (cfg, sampler), "w") as f:
+    json.dump(res, f, indent=1)
+print(json.dumps(res, indent=1))
