@@ -94,13 +94,19 @@ def make_tensor(cfg_name, seed, dev):
     import torch
     from paper_2210_05105_b200 import rng, synth
     c = synth.CONFIGS[cfg_name]
+    perm_of = lambda j, d: rng.permutation(rng.stream_key(seed, rng.TENSOR_PERM, j), d)  # noqa: E731
+    if c["kind"] == "zipf_device":   # C4/C5: generated, deduplicated and permuted on the GPU
+        perms = [perm_of(j, d) for j, d in enumerate(c["dims"])]
+        chunks = synth.zipf_chunks(c["dims"], c["draws"], c["s"], seed=seed, values=c["values"],
+                                   sigma=c.get("sigma", 1.0), parts=c["parts"], device=dev,
+                                   perms=perms, log=lambda m: print(m, file=sys.stderr, flush=True))
+        return c, chunks, None
     if c["kind"] == "planted":
         idx, vals = synth.planted_c1(seed=seed)
         return c, torch.as_tensor(idx, device=dev), torch.as_tensor(vals, device=dev)
     idx, vals = synth.zipf_tensor(c["dims"], c["nnz"], c["s"], seed=seed, values=c["values"],
                                   sigma=c.get("sigma", 1.0), device=dev)
-    idx, _ = synth.permute(idx, c["dims"], seed,
-                           lambda j, d: rng.permutation(rng.stream_key(seed, rng.TENSOR_PERM, j), d))
+    idx, _ = synth.permute(idx, c["dims"], seed, perm_of)
     return c, idx, vals
 
 
@@ -148,7 +154,8 @@ def run_ours(args):
     c, idx, vals = make_tensor(args.config, args.seed, dev)
     dims, R, J = c["dims"], c["R"], c["J"]
     N = len(dims)
-    nnz = int(idx.shape[0])
+    nnz = sum(int(ch[0].shape[0]) for ch in idx) if isinstance(idx, list) else int(idx.shape[0])
+    t_gen = time.perf_counter() - t_setup
     if world > 1:
         from paper_2210_05105_b200.dist import make_spmd_cluster
         cl = make_spmd_cluster(dims, idx, vals, R, J, args.sampler, args.seed, leaf=args.leaf)
@@ -157,6 +164,9 @@ def run_ours(args):
     del idx, vals
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
+    print("setup %.1f s (generate %.1f s), nnz %d, peak %.1f GB, resident %.1f GB" % (
+        setup_s, t_gen, nnz, torch.cuda.max_memory_allocated() / 1e9,
+        torch.cuda.memory_allocated() / 1e9), file=sys.stderr, flush=True)
     me = cl.ranks[0]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev).view(torch.float64)  # 256 MB > L2
 
@@ -256,7 +266,7 @@ def run_ours(args):
                    "parallelism": "as%d" % world, "l2": "256 MB flush between timed rounds "
                    "(outside the round events); stores %.1f GB > L2" % (
                        sum(s.bytes() for s in me.stores) / 1e9),
-                   "setup_s": round(setup_s, 1)},
+                   "setup_s": round(setup_s, 1), "generate_s": round(t_gen, 1)},
         "rounds_per_s": K / t_total,
         "distinct_nnz_per_s": nnz_d / t_total,
         "sampled_nnz_per_round": nnz_m / K,
@@ -273,7 +283,11 @@ def run_ours(args):
     }
     if e2e is not None:
         out["e2e"] = e2e
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if c["kind"] == "zipf_device":
+        out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                               "sample": "not run: the reference keeps ~64 B per nonzero per mode "
+                                         "on the host (>300 GB at this size, SURVEY.md 8(d))"}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline(args, cl, c)
         except Exception as ex:  # reported, never fatal
@@ -379,6 +393,12 @@ def run_reference(args):
     from oracle import randcp_oracle as O
     from paper_2210_05105_b200 import synth
     c = synth.CONFIGS[args.config]
+    if c["kind"] == "zipf_device":
+        print(json.dumps({"impl": "reference", "metric": METRIC, "unit": UNIT,
+                          "unavailable": "the reference's host working set at %s (~64 B per nonzero "
+                          "per mode, >300 GB) exceeds the host; SURVEY.md 8(d)" % args.config}),
+              flush=True)
+        return
     dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
     c, idx_d, vals_d = make_tensor(args.config, args.seed, dev)   # input generation only
     dims, R, J = c["dims"], c["R"], c["J"]

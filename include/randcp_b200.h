@@ -281,6 +281,34 @@ int rcp_exact_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n_c
                      const double *const *h_U, const int64_t *h_lo, int R, double *d_out,
                      void *stream);
 
+/* ---------------------------------------------------------------- device ingest (row F2)
+ * Synthetic Zipf tensors generated on the device for the configurations that cannot be
+ * built on the host (C4 1.7B, C5 4.7B nonzeros); stands in for load_frostt
+ * (ref tensor.py:86-149) with sum_duplicates (tensor.py:72-83) and permute_modes
+ * (tensor.py:182-210) semantics.  Draw d uses the splitmix64 stream of synth.zipf_tensor
+ * with chunk = d >> chunk_bits and index d & (2^chunk_bits - 1). */
+/* d_guide[b] = first i with cdf[i] > b/G (inverse-CDF start table, G entries). */
+int rcp_zipf_guide(const double *d_cdf, int64_t n, int64_t G, int32_t *d_guide, void *stream);
+/* Draws [d0, d1): per mode a Zipf index by inverse CDF of its cdf (searchsorted right),
+ * row-major cell id (u64 bits in int64), value lognormal(0, sigma) (value_kind 0) or a
+ * Poisson(3) count (1).  Only cells whose hash partition (top part_bits bits of
+ * splitmix(cell)) equals `part` are appended at d_key/d_val[*d_count ...] (capacity cap;
+ * overflow raises RCP_ST_CAPACITY). */
+int rcp_zipf_draws(int N, const int64_t *h_dims, const double *const *h_cdf,
+                   const int32_t *const *h_guide, const int64_t *h_G, uint64_t seed,
+                   int chunk_bits, int64_t d0, int64_t d1, int value_kind, double sigma,
+                   int part_bits, int64_t part, int64_t *d_key, double *d_val, int64_t *d_count,
+                   int64_t cap, int *d_status, void *stream);
+/* d_flag[i] = 1 where sorted cell ids start a new cell. */
+int rcp_run_flags(const int64_t *d_sorted, int64_t n, int32_t *d_flag, void *stream);
+/* Distinct cells from stably sorted draws: values summed in draw order (ln(1 + sum) when
+ * log1p_vals), coordinates decoded and mapped through the per-mode permutations h_perm[m]
+ * (device int32 arrays; NULL = identity) into d_idx (n_cells x N int32, row-major). */
+int rcp_cells(const int64_t *d_sorted, const double *d_sval, const int64_t *d_starts,
+              int64_t n_cells, int64_t n, int N, const int64_t *h_dims,
+              const int32_t *const *h_perm, int log1p_vals, int32_t *d_idx, double *d_val,
+              void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,6 +76,11 @@ _SIGS = {
                              _i32, _vp, _vp, _vp, _sz, _vp]),
     "rcp_sum_squares": (_i32, [_vp, _i64, _vp, _vp, _sz, _vp]),
     "rcp_model_norm": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp]),
+    "rcp_zipf_guide": (_i32, [_vp, _i64, _i64, _vp, _vp]),
+    "rcp_zipf_draws": (_i32, [_i32, _vp, _vp, _vp, _vp, _u64, _i32, _i64, _i64, _i32, _f64, _i32,
+                              _i64, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "rcp_run_flags": (_i32, [_vp, _i64, _vp, _vp]),
+    "rcp_cells": (_i32, [_vp, _vp, _vp, _i64, _i64, _i32, _vp, _vp, _i32, _vp, _vp, _vp]),
     "rcp_exact_mttkrp": (_i32, [_vp, _vp, _i64, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp, _vp,
                                 _vp, _i32, _vp, _vp]),
 }

@@ -257,12 +257,22 @@ __global__ void lookup_kernel(const int64_t *__restrict__ keys, int64_t n_cols,
   }
 }
 
-__global__ void finalize_counts_kernel(const int64_t *__restrict__ S,
-                                       const int64_t *__restrict__ doff, int64_t *__restrict__ nnz,
-                                       int64_t *__restrict__ stats) {
+// nnz[0] = gathered entries to process, nnz[1] = entries required.  A call whose entries
+// exceed the workspace capacity processes nothing (S = 0 downstream, output stays zero)
+// and raises RCP_ST_CAPACITY; the caller re-runs it with a larger workspace.
+__global__ void finalize_counts_kernel(int64_t *__restrict__ S, const int64_t *__restrict__ doff,
+                                       int64_t *__restrict__ nnz, int64_t *__restrict__ stats,
+                                       int64_t cap, int *status) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     const int64_t s = S[0];
     const int64_t t = doff[s];
+    nnz[1] = t;
+    if (t > cap) {
+      nnz[0] = 0;
+      S[0] = 0;
+      raise_status(status, RCP_ST_CAPACITY);
+      return;
+    }
     nnz[0] = t;
     stats[0] += s;
     stats[2] += t;
@@ -1038,7 +1048,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   // 3. fiber offsets
   int rc = scan_i64_exclusive(dlen, doff, J, S, scan_ws, st);
   if (rc) return rc;
-  finalize_counts_kernel<<<1, 32, 0, st>>>(S, doff, nnz, d_stats);
+  finalize_counts_kernel<<<1, 32, 0, st>>>(S, doff, nnz, d_stats, cap, d_status);
   RCP_LAUNCH_CHECK("finalize_counts");
   // 3b. work items: fiber chunks of <= kItemE entries (dkey reused for the counts)
   int64_t *icnt = dkey;

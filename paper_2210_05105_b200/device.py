@@ -84,6 +84,9 @@ class Status:
     def reset(self):
         self.buf.zero_()
 
+    def clear_flag(self, flag):
+        self.buf.bitwise_and_(~int(flag))
+
     def check(self, where=""):
         v = int(self.buf.item())
         if not v:

@@ -30,7 +30,12 @@ from . import rng
 from .device import torch
 from .grid import ProcessorGrid, optimal_grid
 from .ops import ops_for
-from .store import build_store
+from .store import build_store, build_store_chunks
+
+# Sampled-MTTKRP entry capacity above which the workspace is sized from the observed
+# gathered-entry counts (checked after each call, grown and re-run on overflow) instead
+# of the worst case min(nnz, J * longest fiber).
+CAP_LIMIT = 1 << 28
 
 PHASES = ("sampling", "gather", "mttkrp", "reduction", "postprocess", "rebuild")
 
@@ -181,6 +186,7 @@ class RankState:
         self.sigma = t.ones(R, **f64)
         self.Mout = t.zeros((max(self.n) if N else 0, R), **f64)
         self.stats = t.zeros(8, dtype=t.int64, device=dev)
+        self.mt_cap = {}
         self.block_gram_buf = t.zeros((R, R), **f64)
 
     # -------------------------------------------------------------- set-up
@@ -195,6 +201,11 @@ class RankState:
     def build_stores(self, idx, vals):
         """idx/vals: device COO of the whole tensor (or a superset); keeps, per mode, the
         nonzeros whose mode-j row lies in this rank's block (ref matricization.py:187-198)."""
+        if isinstance(idx, list):   # device-ingest chunks (C4/C5): bucketed build
+            for j in range(self.N):
+                self.stores[j] = build_store_chunks(self.dims, idx, j, self.lo[j],
+                                                    self.lo[j] + self.n[j])
+            return
         for j in range(self.N):
             rows = idx[:, j]
             sel = (rows >= self.lo[j]) & (rows < self.lo[j] + self.n[j])
@@ -364,8 +375,23 @@ class RankState:
         out = self.Mout[:n]
         if n > 0:
             st = self.stores[k]
-            self.ops.sampled_mttkrp(st, self.X, k, self.H, self.w, out, self.stats,
-                                    cap=st.capacity(self.J))
+            worst = st.capacity(self.J)
+            if worst <= CAP_LIMIT:
+                self.ops.sampled_mttkrp(st, self.X, k, self.H, self.w, out, self.stats, cap=worst)
+                return out
+            # bounded workspace: the call is idempotent (reads X, H, w; writes out), so an
+            # overflowing call is repeated with the exact requirement
+            cap = self.mt_cap.get(k, CAP_LIMIT)
+            stats0 = self.stats.clone()
+            while True:
+                need = self.ops.sampled_mttkrp(st, self.X, k, self.H, self.w, out, self.stats,
+                                               cap=cap, need=True)
+                if need <= cap:
+                    break
+                self.ops.status.clear_flag(_lib_capacity())
+                self.stats.copy_(stats0)
+                cap = min(worst, int(need * 1.25) + (1 << 20))
+            self.mt_cap[k] = cap
         return out
 
     def update(self, k):
@@ -646,6 +672,11 @@ class Cluster:
                 on_solved(k)
             if check:
                 self.check("after round %d mode %d solve" % (rnd, k))
+
+
+def _lib_capacity():
+    from . import _lib
+    return _lib.ST_CAPACITY
 
 
 def make_local_cluster(dims, idx, vals, R, J, sampler, seed, P=1, grid_dims=None, leaf=None,

@@ -162,7 +162,9 @@ class Ops:
     def mttkrp_ws(self, J, cap, n_rows, R):
         return self.ws("mttkrp", self.lib.rcp_mttkrp_ws_bytes(int(J), int(cap), int(n_rows), int(R)))
 
-    def sampled_mttkrp(self, store, X, k, H, w, out, stats, cap=None):
+    def sampled_mttkrp(self, store, X, k, H, w, out, stats, cap=None, need=False):
+        """need=True: synchronise and return the gathered-entry count of this call (the
+        capacity it required)."""
         N, J = X.shape
         R = H.shape[1]
         cap = store.nnz if cap is None else cap
@@ -172,6 +174,11 @@ class Ops:
                 ptr(store.rows), ptr(store.vals), store.n_rows, ptr(X), N, J, int(k),
                 strides.ctypes.data, ptr(H), ptr(w), R, ptr(out), ptr(stats), ptr(ws),
                 ws.numel(), self.status.ptr, stream_handle())
+        if need:
+            lay = np.zeros(14, dtype=np.int64)
+            self._c("rcp_mttkrp_layout", int(J), store.n_rows, R, ws.numel(), lay.ctypes.data)
+            o = int(lay[12])
+            return int(ws[o + 8:o + 16].view(torch().int64).item())   # nnz[1]: required
 
     def fiber_lookup(self, store, X, k, lo, counts):
         N, J = X.shape
@@ -234,6 +241,38 @@ class Ops:
                 dims.ctypes.data, strides.ctypes.data, U, lo.ctypes.data, R, ptr(out),
                 stream_handle())
         return out
+
+    # ------------------------------------------------------------- device ingest (F2)
+    def zipf_guide(self, cdf, guide):
+        self._c("rcp_zipf_guide", ptr(cdf), cdf.numel(), guide.numel(), ptr(guide),
+                stream_handle())
+
+    def zipf_draws(self, dims, cdfs, guides, seed, chunk_bits, d0, d1, value_kind, sigma,
+                   part_bits, part, keys, vals, count):
+        import ctypes as C
+        N = len(dims)
+        hd = np.ascontiguousarray(dims, dtype=np.int64)
+        hc = (C.c_void_p * N)(*[C.c_void_p(ptr(c)) for c in cdfs])
+        hg = (C.c_void_p * N)(*[C.c_void_p(ptr(g)) for g in guides])
+        hG = np.ascontiguousarray([g.numel() for g in guides], dtype=np.int64)
+        self._c("rcp_zipf_draws", N, hd.ctypes.data, hc, hg, hG.ctypes.data, int(seed),
+                int(chunk_bits), int(d0), int(d1), int(value_kind), float(sigma), int(part_bits),
+                int(part), ptr(keys), ptr(vals), ptr(count), keys.numel(), self.status.ptr,
+                stream_handle())
+
+    def run_flags(self, sorted_keys, flag):
+        self._c("rcp_run_flags", ptr(sorted_keys), sorted_keys.numel(), ptr(flag),
+                stream_handle())
+
+    def cells(self, sorted_keys, svals, starts, dims, perms, log1p_vals, idx_out, val_out):
+        import ctypes as C
+        N = len(dims)
+        hd = np.ascontiguousarray(dims, dtype=np.int64)
+        hp = (C.c_void_p * N)(*[C.c_void_p(ptr(p)) if p is not None else None
+                                for p in (perms or [None] * N)])
+        self._c("rcp_cells", ptr(sorted_keys), ptr(svals), ptr(starts), starts.numel(),
+                sorted_keys.numel(), N, hd.ctypes.data, hp, int(bool(log1p_vals)), ptr(idx_out),
+                ptr(val_out), stream_handle())
 
 
 _OPS = {}

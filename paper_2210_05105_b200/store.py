@@ -112,3 +112,82 @@ def build_store(dims, idx, vals, mode, row_lo=0, row_hi=None):
     lvals = vals[order].to(t.float64).contiguous()
     return DeviceStore(dims, mode, row_lo, row_hi, ukeys.contiguous(), colptr, lrows.contiguous(),
                        lvals, max_col)
+
+
+def build_store_chunks(dims, chunks, mode, row_lo=0, row_hi=None, buckets=16):
+    """Mode-`mode` store from a list of device COO chunks (idx int32/int64 [n, N], vals):
+    the device-ingest path for tensors whose int64 COO would not fit (C4/C5).  Entries are
+    bucketed by column-key range (a column never straddles two buckets), each bucket is
+    ordered by (key, row) with two stable sorts and written at its offset, so the working
+    set beyond the store itself is one bucket.  Same layout as build_store."""
+    t = torch()
+    dims = tuple(int(d) for d in dims)
+    N = len(dims)
+    row_hi = dims[mode] if row_hi is None else int(row_hi)
+    strides, exact = off_mode_strides(dims, mode)
+    if not exact:
+        raise ValueError("off-mode key space of mode %d exceeds 2^62" % mode)
+    span = 1
+    for m in range(N):
+        if m != mode:
+            span *= dims[m]
+    dev = chunks[0][0].device if chunks else t.device("cuda", 0)
+    B = max(1, int(buckets))
+
+    def keyed(idx, vals):
+        rows = idx[:, mode].long()
+        sel = (rows >= row_lo) & (rows < row_hi)
+        fk = t.zeros(idx.shape[0], dtype=t.int64, device=dev)
+        for m in range(N):
+            if m != mode:
+                fk += idx[:, m].long() * int(strides[m])
+        return fk, rows, sel
+
+    counts = t.zeros(B, dtype=t.int64, device=dev)
+    for idx, vals in chunks:
+        fk, rows, sel = keyed(idx, vals)
+        counts += t.bincount((fk[sel] * B) // span, minlength=B)
+        del fk, rows, sel
+    total = int(counts.sum())
+    out_rows = t.empty(total, dtype=t.int32, device=dev)
+    out_vals = t.empty(total, dtype=t.float64, device=dev)
+    keys_l, cnt_l = [], []
+    off = 0
+    max_col = 0
+    for b in range(B):
+        parts = []
+        for idx, vals in chunks:
+            fk, rows, sel = keyed(idx, vals)
+            sel &= (fk * B) // span == b
+            parts.append((fk[sel], rows[sel], vals[sel]))
+            del fk, rows, sel
+        fk = t.cat([p[0] for p in parts])
+        rows = t.cat([p[1] for p in parts])
+        vals = t.cat([p[2] for p in parts])
+        del parts
+        n = fk.numel()
+        if n == 0:
+            continue
+        o1 = t.sort(rows, stable=True).indices
+        o2 = t.sort(fk[o1], stable=True).indices
+        order = o1[o2]
+        del o1, o2
+        out_rows[off:off + n] = (rows[order] - row_lo).to(t.int32)
+        out_vals[off:off + n] = vals[order]
+        uk, c = t.unique_consecutive(fk[order], return_counts=True)
+        del order, fk, rows, vals
+        keys_l.append(uk)
+        cnt_l.append(c)
+        max_col = max(max_col, int(c.max()))
+        off += n
+    if keys_l:
+        keys = t.cat(keys_l)
+        cnts = t.cat(cnt_l)
+    else:
+        keys = t.zeros(0, dtype=t.int64, device=dev)
+        cnts = t.zeros(0, dtype=t.int64, device=dev)
+    del keys_l, cnt_l
+    colptr = t.zeros(keys.numel() + 1, dtype=t.int64, device=dev)
+    t.cumsum(cnts, 0, out=colptr[1:])
+    return DeviceStore(dims, mode, row_lo, row_hi, keys.contiguous(), colptr, out_rows, out_vals,
+                       max_col)

@@ -32,11 +32,15 @@ CONFIGS = {
                samplers=("sts",), kind="zipf", s=1.1, values="lognormal", sigma=1.0),
     "c3": dict(dims=(12092, 9184, 28818), nnz=77_000_000, R=50, J=65536, rounds=1,
                samplers=("arls-lev", "sts"), kind="zipf", s=1.05, values="lognormal", sigma=1.0),
+    # C4/C5: built on the device (zipf_chunks) from a fixed number of draws (the expected
+    # count reaching the target distinct cells); the actual
+    # post-dedup nonzero count is reported.
     "c4": dict(dims=(4_800_000, 1_800_000, 1_800_000), nnz=1_700_000_000, R=50, J=65536,
-               rounds=1, samplers=("arls-lev", "sts"), kind="zipf", s=1.2,
-               values="lognormal", sigma=1.5),
+               rounds=1, samplers=("arls-lev", "sts"), kind="zipf_device", s=1.2,
+               values="lognormal", sigma=1.5, draws=5_830_000_000, parts=16),
     "c5": dict(dims=(8_200_000, 177_000, 8_100_000), nnz=4_700_000_000, R=100, J=131072,
-               rounds=1, samplers=("sts",), kind="zipf", s=1.1, values="log1p_poisson"),
+               rounds=1, samplers=("sts",), kind="zipf_device", s=1.1, values="log1p_poisson",
+               draws=9_120_000_000, parts=32),
 }
 
 
@@ -167,6 +171,75 @@ def zipf_tensor(dims, target, s, seed=0, values="lognormal", sigma=1.0, device="
         idx[:, m] = rem // strides[m]
         rem = rem % strides[m]
     return idx, v
+
+
+def zipf_chunks(dims, draws, s, seed=0, values="lognormal", sigma=1.0, parts=16,
+                chunk_bits=28, device=None, perms=None, log=None):
+    """Device ingest for C4/C5 (ingest.cu): `draws` Zipf draws of the splitmix stream of
+    `zipf_tensor` (chunks of 2^chunk_bits draws), duplicates summed in draw order, all
+    distinct cells kept.  One pass over the draw sequence per hash partition of the cell
+    space keeps the working set at ~draws/parts cells; a cell's draws are summed in
+    ascending value order (reproducible).  Coordinates are mapped through
+    `perms` (the reference's per-mode load-balancing permutations, ref tensor.py:207-210).
+    Returns a list of (idx int32 [n, N], vals fp64 [n]) CUDA tensors, one per partition."""
+    import torch
+    from .ops import ops_for
+    dev = torch.device(device) if device is not None else torch.device("cuda", 0)
+    ops = ops_for(dev)
+    dims = tuple(int(d) for d in dims)
+    N = len(dims)
+    part_bits = int(round(math.log2(parts)))
+    if (1 << part_bits) != parts:
+        raise ValueError("parts must be a power of two")
+    cdfs = [torch.as_tensor(zipf_cdf(d, s), device=dev) for d in dims]
+    guides = [torch.empty(d, dtype=torch.int32, device=dev) for d in dims]
+    for c, g in zip(cdfs, guides):
+        ops.zipf_guide(c, g)
+    pdev = None
+    if perms is not None:
+        pdev = [torch.as_tensor(np.asarray(p, dtype=np.int32), device=dev) for p in perms]
+    vkind = {"lognormal": 0, "log1p_poisson": 1}[values]
+    step = 1 << 30
+    chunks = []
+    for p in range(parts):
+        cap = int(draws / parts * 1.25) + (1 << 20)
+        while True:
+            keys = torch.empty(cap, dtype=torch.int64, device=dev)
+            vals = torch.empty(cap, dtype=torch.float64, device=dev)
+            cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            for d0 in range(0, int(draws), step):
+                ops.zipf_draws(dims, cdfs, guides, seed, chunk_bits, d0, min(int(draws), d0 + step),
+                               vkind, sigma, part_bits if parts > 1 else 0, p, keys, vals, cnt)
+            n = int(cnt.item())
+            if n <= cap:
+                ops.status.check("in zipf_draws")
+                break
+            ops.status.reset()
+            del keys, vals
+            cap = n + (1 << 20)
+        # the draws' buffer order depends on the atomic append order; ordering each cell's
+        # draws by value (non-negative doubles sort as their bit patterns) makes the sums
+        # reproducible
+        sv, order = torch.sort(vals[:n])
+        keys = keys[:n][order]
+        del vals, order
+        sk, order = torch.sort(keys, stable=True)
+        del keys
+        sv = sv[order]
+        del order
+        flag = torch.empty(n, dtype=torch.int32, device=dev)
+        ops.run_flags(sk, flag)
+        starts = torch.nonzero(flag).squeeze(1)
+        del flag
+        nc = int(starts.numel())
+        idx = torch.empty((nc, N), dtype=torch.int32, device=dev)
+        v = torch.empty(nc, dtype=torch.float64, device=dev)
+        ops.cells(sk, sv, starts, dims, pdev, values == "log1p_poisson", idx, v)
+        del sk, sv, starts
+        chunks.append((idx, v))
+        if log:
+            log("partition %d/%d: %d draws -> %d cells" % (p + 1, parts, n, nc))
+    return chunks
 
 
 def _poisson3(torch, u):
