@@ -539,7 +539,9 @@ cta_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__
 //     instead of one per row — as {row, fiber, value};
 //  B. one CTA per bucket orders its range by row in place of the final array (the range,
 //     ~1/256 of the entries, stays L2-resident while its rows' cursors advance).
-constexpr int kBucketMax = 512;
+constexpr int kBucketMax = 512;        // buckets of the small-row (CTA-histogram) path
+constexpr int kBigBucketMax = 2048;    // buckets of the large-row path (<= 2^14 rows each)
+constexpr int kBigMaxShift = 14;
 constexpr int64_t kBucketMinRows = 4096;   // below: the single-pass scatter is faster
 
 // bofs[cta][b] = start of the CTA's slice of bucket b = rptr[b << sh] + sum over the
@@ -568,8 +570,8 @@ bucket_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restric
                       const double *__restrict__ vals, int sh, int nb,
                       const int64_t *__restrict__ bofs, double2 *__restrict__ tmp, int64_t cap,
                       int *status) {
-  __shared__ int bcur[kBucketMax];   // offsets relative to the CTA's slice base (< 2^31)
-  __shared__ int64_t bbase[kBucketMax];
+  __shared__ int bcur[kBigBucketMax];   // offsets relative to the CTA's slice base (< 2^31)
+  __shared__ int64_t bbase[kBigBucketMax];
   __shared__ int claim;
   const int64_t S = Sp[0];
   int64_t i0, i1;
@@ -648,6 +650,169 @@ bucket_rows_kernel(const double2 *__restrict__ tmp, int64_t n_rows, int sh,
       ent[o] = make_double2(__longlong_as_double((long long)(uint32_t)(key & 0xffffffffu)), t[u].y);
     }
   }
+}
+
+// ------------------------------------------------------------ large-row transpose
+// Row counts above the CTA-histogram limit (C4/C5 factor modes: 10^6..10^7 rows): no
+// per-row global atomics.  Entries are bucketed by row >> sh (<= 2048 buckets of
+// <= 2^14 rows): per-CTA bucket counts, per-bucket prefix over CTAs, pass A (the shared
+// bucket_scatter_kernel) writes each CTA's entries to its slice of the bucket, and pass B
+// counting-sorts each bucket by row in shared memory, emitting the row pointers.
+
+__global__ void __launch_bounds__(kTraverseThreads)
+big_hist_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                const int32_t *__restrict__ ifib, const int64_t *__restrict__ dlo,
+                const int64_t *__restrict__ dlen, const int32_t *__restrict__ rows, int sh, int nb,
+                int32_t *__restrict__ bmat) {
+  __shared__ int cnt[kBigBucketMax];
+  __shared__ int claim;
+  const int64_t S = Sp[0];
+  int64_t i0, i1;
+  cta_items(ioff[S], i0, i1);
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
+  if (threadIdx.x == 0) claim = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&claim, 1);
+    const int64_t it = i0 + __shfl_sync(0xffffffffu, c, 0);
+    if (it >= i1) break;
+    const ItemSpan sp = item_span(it, ioff, ifib, dlo, dlen);
+    for (int64_t pos = sp.a + lane; pos < sp.b; pos += 32 * kInFlight) {
+      int32_t rw[kInFlight];
+#pragma unroll
+      for (int q = 0; q < kInFlight; ++q) rw[q] = pos + 32 * q < sp.b ? rows[pos + 32 * q] : -1;
+#pragma unroll
+      for (int q = 0; q < kInFlight; ++q)
+        if (rw[q] >= 0) atomicAdd(&cnt[rw[q] >> sh], 1);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) bmat[(int64_t)blockIdx.x * nb + b] = cnt[b];
+}
+
+// per bucket: exclusive prefix over the CTAs (in place) and the bucket total
+__global__ void big_colprefix_kernel(int32_t *__restrict__ bmat, int G, int nb,
+                                     int64_t *__restrict__ btot) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > nb) return;
+  if (b == nb) {   // the scan below reads one element past the buckets
+    btot[nb] = 0;
+    return;
+  }
+  int64_t run = 0;
+  for (int c = 0; c < G; ++c) {
+    const int32_t v = bmat[(int64_t)c * nb + b];
+    bmat[(int64_t)c * nb + b] = (int32_t)run;
+    run += v;
+  }
+  btot[b] = run;
+}
+
+__global__ void big_offsets_kernel(const int32_t *__restrict__ bmat, const int64_t *__restrict__ bstart,
+                                   int G, int nb, int64_t *__restrict__ bofs) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)G * nb) return;
+  bofs[i] = bstart[i % nb] + bmat[i];
+}
+
+constexpr int kBigRowsThreads = 1024;
+
+// One CTA per bucket: row counts -> row pointers (and rows hit) -> entries in row order.
+__global__ void __launch_bounds__(kBigRowsThreads)
+big_rows_kernel(const double2 *__restrict__ tmp, int64_t n_rows, int sh,
+                const int64_t *__restrict__ bstart, int64_t *__restrict__ rptr,
+                double2 *__restrict__ ent, int64_t *__restrict__ stats) {
+  extern __shared__ int cnt[];   // per row of the bucket
+  __shared__ int wsum[32];
+  __shared__ int hit_s;
+  const int b = blockIdx.x;
+  const int64_t r0 = (int64_t)b << sh;
+  const int nr = (int)min((int64_t)1 << sh, n_rows - r0);
+  const int64_t e0 = bstart[b], e1 = bstart[b + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int q = threadIdx.x; q < nr; q += blockDim.x) cnt[q] = 0;
+  if (threadIdx.x == 0) hit_s = 0;
+  __syncthreads();
+  constexpr int U = 8;
+  for (int64_t base = e0; base < e1; base += (int64_t)blockDim.x * U) {
+    int rr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = base + (int64_t)u * blockDim.x + threadIdx.x;
+      rr[u] = e < e1 ? (int)((uint64_t)__double_as_longlong(tmp[e].x) >> 32) - (int)r0 : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (rr[u] >= 0) atomicAdd(&cnt[rr[u]], 1);
+  }
+  __syncthreads();
+  // exclusive scan of cnt[0, nr): each thread owns a contiguous run of rows
+  const int per = (nr + blockDim.x - 1) / blockDim.x;
+  const int q0 = min(nr, (int)threadIdx.x * per), q1 = min(nr, q0 + per);
+  int mine = 0, hits = 0;
+  for (int q = q0; q < q1; ++q) {
+    mine += cnt[q];
+    hits += cnt[q] > 0;
+  }
+  int x = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
+  if (lane == 0 && hits) atomicAdd(&hit_s, hits);
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    int v = lane < nw ? wsum[lane] : 0;
+    int z = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    if (lane < nw) wsum[lane] = z - v;
+  }
+  __syncthreads();
+  int run = wsum[wid] + x - mine;
+  for (int q = q0; q < q1; ++q) {
+    const int c = cnt[q];
+    cnt[q] = run;
+    rptr[r0 + q] = e0 + run;
+    run += c;
+  }
+  if (threadIdx.x == 0) {
+    if (hit_s) atomicAdd((unsigned long long *)&stats[4], (unsigned long long)hit_s);
+    if (r0 + nr == n_rows) rptr[n_rows] = e1;
+  }
+  __syncthreads();
+  for (int64_t base = e0; base < e1; base += (int64_t)blockDim.x * U) {
+    double2 t[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = base + (int64_t)u * blockDim.x + threadIdx.x;
+      t[u] = e < e1 ? tmp[e] : make_double2(__longlong_as_double(-1LL), 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t key = (uint64_t)__double_as_longlong(t[u].x);
+      if (key == ~0ull) continue;
+      const int row = (int)(key >> 32) - (int)r0;
+      const int64_t o = e0 + atomicAdd(&cnt[row], 1);
+      ent[o] = make_double2(__longlong_as_double((long long)(uint32_t)(key & 0xffffffffu)), t[u].y);
+    }
+  }
+}
+
+int big_shift(int64_t n_rows) {
+  int sh = 0;
+  while (ceil_div(n_rows, (int64_t)1 << sh) > kBigBucketMax) ++sh;
+  return sh;
 }
 
 // ------------------------------------------------------------ segmented SpMM
@@ -944,7 +1109,7 @@ struct MttkrpLayout {
                    (size_t)(n_rows < kPrivRows ? n_rows : kPrivRows));
     o_ent = w.add(sizeof(double2) * (cap + 1));
     o_tmp = w.add(sizeof(double2) * (cap + 1));
-    o_bofs = w.add(sizeof(int64_t) * (size_t)sm_count() * kBucketMax);
+    o_bofs = w.add(sizeof(int64_t) * ((size_t)sm_count() + 1) * (kBigBucketMax + 1));
     o_S = w.add(sizeof(int64_t) * 4);
     o_nnz = w.add(sizeof(int64_t) * 4);
     total = w.total + 256;
@@ -1100,24 +1265,58 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
         tmp, n_rows, sh, rptr, ent);
     RCP_LAUNCH_CHECK("bucket_rows");
     }
+  } else if (big_shift(n_rows) <= kBigMaxShift && cap < (1LL << 40)) {
+    // large-row bucketed transpose (no per-row global atomics)
+    const int sh = big_shift(n_rows);
+    const int nb = (int)ceil_div(n_rows, (int64_t)1 << sh);
+    int32_t *bmat = (int32_t *)P(L.o_cmat);            // grid x nb <= grid x kPrivRows
+    int64_t *bofs = (int64_t *)P(L.o_bofs);            // grid x nb, then btot, bstart
+    int64_t *btot = bofs + (int64_t)grid * nb;
+    int64_t *bstart = btot + (nb + 1);
+    double2 *tmp = (double2 *)P(L.o_tmp);
+    big_hist_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, sh, nb, bmat);
+    RCP_LAUNCH_CHECK("big_hist");
+    big_colprefix_kernel<<<(unsigned)ceil_div(nb + 1, 256), 256, 0, st>>>(bmat, grid, nb, btot);
+    RCP_LAUNCH_CHECK("big_colprefix");
+    rc = scan_i64_exclusive(btot, bstart, nb, nullptr, scan_ws, st);
+    if (rc) return rc;
+    big_offsets_kernel<<<(unsigned)ceil_div((int64_t)grid * nb, 256), 256, 0, st>>>(bmat, bstart, grid,
+                                                                                    nb, bofs);
+    RCP_LAUNCH_CHECK("big_offsets");
+    bucket_scatter_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, d_vals,
+                                                             sh, nb, bofs, tmp, cap, d_status);
+    RCP_LAUNCH_CHECK("bucket_scatter");
+    static bool battr = false;
+    if (!battr) {
+      RCP_CUDA_TRY(cudaFuncSetAttribute(big_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(sizeof(int) << kBigMaxShift)));
+      battr = true;
+    }
+    big_rows_kernel<<<nb, kBigRowsThreads, sizeof(int) << sh, st>>>(tmp, n_rows, sh, bstart, rptr, ent,
+                                                                   d_stats);
+    RCP_LAUNCH_CHECK("big_rows");
   } else {
     RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
     row_count_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, n_rows, 0, rcnt);
     RCP_LAUNCH_CHECK("row_count");
     rc = scan_i64_exclusive(rcnt, rptr, n_rows, nullptr, scan_ws, st);
     if (rc) return rc;
-  }
-  {
-    int64_t b = ceil_div(n_rows, 256);
-    if (b > 4LL * sm_count()) b = 4LL * sm_count();
-    rows_hit_kernel<<<(unsigned)b, 256, 0, st>>>(rcnt, n_rows, d_stats);
-    RCP_LAUNCH_CHECK("rows_hit");
-  }
-  if (!priv) {   // global per-row cursors (rcnt reused)
+    {
+      int64_t b = ceil_div(n_rows, 256);
+      if (b > 4LL * sm_count()) b = 4LL * sm_count();
+      rows_hit_kernel<<<(unsigned)b, 256, 0, st>>>(rcnt, n_rows, d_stats);
+      RCP_LAUNCH_CHECK("rows_hit");
+    }
     RCP_CUDA_TRY(cudaMemsetAsync(rcnt, 0, sizeof(int64_t) * (n_rows + 1), st));
     scatter_kernel<<<grid, kTraverseThreads, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, d_vals, n_rows, 0,
                                                       rptr, rcnt, ent, cap, d_status);
     RCP_LAUNCH_CHECK("scatter");
+  }
+  if (priv) {
+    int64_t b = ceil_div(n_rows, 256);
+    if (b > 4LL * sm_count()) b = 4LL * sm_count();
+    rows_hit_kernel<<<(unsigned)b, 256, 0, st>>>(rcnt, n_rows, d_stats);
+    RCP_LAUNCH_CHECK("rows_hit");
   }
   // 6. segmented reduction
   const unsigned sb = (unsigned)(8 * sm_count());

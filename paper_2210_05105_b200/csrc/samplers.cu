@@ -77,6 +77,74 @@ leverage_kernel(const double *__restrict__ U, int64_t n, int R, const double *__
   }
 }
 
+// R <= 64: row leverages on the fp64 tensor cores.  A warp takes 8-row tiles Z of U
+// (staged in shared memory), forms Y = Z G+ with mma.m8n8k4 (G+ zero-padded to Rn x Rn in
+// shared memory) and d_q = <Y_q, Z_q>.  Tiles are assigned to warps in a fixed order, so
+// the per-CTA partial masses (and the ordered total) are reproducible.
+constexpr int kLevMmaMaxR = 64;
+__host__ __device__ __forceinline__ int lev_rn(int R) { return (R + 7) & ~7; }
+__host__ __device__ __forceinline__ int lev_zs(int R) { return lev_rn(R) + 2; }
+
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256)
+leverage_mma_kernel(const double *__restrict__ U, int64_t n, int R, const double *__restrict__ Gp,
+                    double *__restrict__ lev, double *__restrict__ part) {
+  extern __shared__ double sh[];
+  const int Rn = lev_rn(R), Zs = lev_zs(R);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double *G = sh;                                   // Rn x Rn
+  double *zb = sh + Rn * Rn + (size_t)wid * 8 * Zs;  // this warp's 8 x Zs tile
+  for (int e = threadIdx.x; e < Rn * Rn; e += blockDim.x) {
+    const int a = e / Rn, b = e - a * Rn;
+    G[e] = (a < R && b < R) ? Gp[a * R + b] : 0.0;
+  }
+  __syncthreads();
+  const int row = lane >> 2, quad = lane & 3;
+  double local = 0.0;
+  const int64_t tiles = (n + 7) >> 3;
+  for (int64_t tl = (int64_t)blockIdx.x * nw + wid; tl < tiles; tl += (int64_t)gridDim.x * nw) {
+    const int64_t r0 = tl << 3;
+    const int nb = (int)min((int64_t)8, n - r0);
+    for (int c = lane; c < 8 * Zs; c += 32) {
+      const int j = c / Zs, col = c - j * Zs;
+      zb[c] = (j < nb && col < R) ? U[(r0 + j) * R + col] : 0.0;
+    }
+    __syncwarp();
+    const double *zr = zb + row * Zs;
+    double msum = 0.0;
+    for (int nt = 0; nt < Rn; nt += 8) {
+      double c0 = 0.0, c1 = 0.0;
+      for (int ks = 0; ks < Rn; ks += 4)
+        dmma_8x8x4(c0, c1, zr[ks + quad], G[(ks + quad) * Rn + nt + row]);
+      msum = fma(c0, zr[nt + 2 * quad], msum);
+      msum = fma(c1, zr[nt + 2 * quad + 1], msum);
+    }
+    msum += __shfl_xor_sync(0xffffffffu, msum, 1);
+    msum += __shfl_xor_sync(0xffffffffu, msum, 2);
+    const double d = msum > 0.0 ? msum : 0.0;
+    if (quad == 0 && row < nb) lev[r0 + row] = d;
+    // fixed-order warp partial: rows of the tile in order
+    double t = (quad == 0 && row < nb) ? d : 0.0;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    local += t;
+    __syncwarp();
+  }
+  __syncthreads();
+  if (lane == 0) sh[wid] = local;   // reuse (G no longer needed)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += sh[w];
+    part[blockIdx.x] = s;
+  }
+}
+
 // Ordered (deterministic) sum of the per-CTA partial masses; one block of 256 threads.
 __global__ void mass_kernel(const double *__restrict__ part, int nparts, double *mass) {
   __shared__ double red[256];
@@ -305,7 +373,7 @@ int rcp_arls_build(const double *d_U, int64_t n, int R, const double *d_Gp, doub
   double *part = (double *)d_ws;
   void *scan_ws = (char *)d_ws + (size_t)4 * sm_count() * sizeof(double);
   size_t smem = sizeof(double) * R * R;
-  static bool attr = false;
+  static bool attr = false, attr_mma = false;
   if (!attr) {
     RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
     RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
@@ -313,7 +381,14 @@ int rcp_arls_build(const double *d_U, int64_t n, int R, const double *d_Gp, doub
     RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
     attr = true;
   }
-  switch ((R + 31) / 32) {
+  if (R <= kLevMmaMaxR) {
+    if (!attr_mma) {
+      RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+      attr_mma = true;
+    }
+    const size_t sm = sizeof(double) * ((size_t)lev_rn(R) * lev_rn(R) + 8 * 8 * (size_t)lev_zs(R));
+    leverage_mma_kernel<<<grid, 256, sm, st>>>(d_U, n, R, d_Gp, d_dist, part);
+  } else switch ((R + 31) / 32) {
     case 1: leverage_kernel<1><<<grid, 256, smem, st>>>(d_U, n, R, d_Gp, d_dist, part); break;
     case 2: leverage_kernel<2><<<grid, 256, smem, st>>>(d_U, n, R, d_Gp, d_dist, part); break;
     case 3: leverage_kernel<3><<<grid, 256, smem, st>>>(d_U, n, R, d_Gp, d_dist, part); break;

@@ -384,9 +384,9 @@ class RankState:
             cap = self.mt_cap.get(k, CAP_LIMIT)
             stats0 = self.stats.clone()
             while True:
-                need = self.ops.sampled_mttkrp(st, self.X, k, self.H, self.w, out, self.stats,
-                                               cap=cap, need=True)
-                if need <= cap:
+                need, have = self.ops.sampled_mttkrp(st, self.X, k, self.H, self.w, out,
+                                                     self.stats, cap=cap, need=True)
+                if need <= have:
                     break
                 self.ops.status.clear_flag(_lib_capacity())
                 self.stats.copy_(stats0)

@@ -163,8 +163,9 @@ class Ops:
         return self.ws("mttkrp", self.lib.rcp_mttkrp_ws_bytes(int(J), int(cap), int(n_rows), int(R)))
 
     def sampled_mttkrp(self, store, X, k, H, w, out, stats, cap=None, need=False):
-        """need=True: synchronise and return the gathered-entry count of this call (the
-        capacity it required)."""
+        """need=True: synchronise and return (gathered entries this call required, entry
+        capacity of the workspace it ran with); it overflowed iff the first exceeds the
+        second (then it processed nothing and raised the capacity flag)."""
         N, J = X.shape
         R = H.shape[1]
         cap = store.nnz if cap is None else cap
@@ -174,11 +175,11 @@ class Ops:
                 ptr(store.rows), ptr(store.vals), store.n_rows, ptr(X), N, J, int(k),
                 strides.ctypes.data, ptr(H), ptr(w), R, ptr(out), ptr(stats), ptr(ws),
                 ws.numel(), self.status.ptr, stream_handle())
-        if need:
+        if need:   # (entries required, entry capacity of the workspace used)
             lay = np.zeros(14, dtype=np.int64)
             self._c("rcp_mttkrp_layout", int(J), store.n_rows, R, ws.numel(), lay.ctypes.data)
             o = int(lay[12])
-            return int(ws[o + 8:o + 16].view(torch().int64).item())   # nnz[1]: required
+            return int(ws[o + 8:o + 16].view(torch().int64).item()), int(lay[13])
 
     def fiber_lookup(self, store, X, k, lo, counts):
         N, J = X.shape

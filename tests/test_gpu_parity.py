@@ -194,7 +194,8 @@ def test_gather_csr_and_downsampled_match_reference(pkg):
 @pytest.mark.parametrize("dims,nnz", [
     ((40, 35, 30), 6000),        # CTA-private histograms, single-pass scatter
     ((6000, 35, 30), 60000),     # >= 4096 rows in mode 0: bucketed two-pass transpose
-    ((60000, 12, 10), 50000),    # > 49152 rows in mode 0: global-atomic row cursors
+    ((60000, 12, 10), 50000),    # > 49152 rows in mode 0: large-row bucketed transpose
+    ((300000, 6, 5), 40000),     # 2^8-row buckets
 ])
 def test_fused_sampled_mttkrp_matches_oracle(pkg, dims, nnz):
     import torch
@@ -230,7 +231,60 @@ def test_fused_sampled_mttkrp_matches_oracle(pkg, dims, nnz):
         csr = O.sampled_csr(O.Store(dims, idx, vals, k), X, k)
         s = stats.cpu().numpy()
         assert s[3] == csr.nnz                       # gathered nnz with multiplicity
+        assert s[4] == np.count_nonzero(np.diff(csr.row_ptr))   # rows hit
         assert np.array_equal(got == 0, ref == 0)    # untouched rows exactly zero
+
+
+def test_sampled_mttkrp_capacity_overflow_and_engine_retry(pkg, monkeypatch):
+    """A call whose gathered entries exceed the workspace processes nothing, reports the
+    requirement and raises the capacity flag; the engine's bounded-workspace mode re-runs
+    it and reproduces the unbounded result."""
+    import torch
+    from paper_2210_05105_b200 import engine
+    from paper_2210_05105_b200.engine import make_local_cluster
+    from paper_2210_05105_b200.ops import ops_for
+    from paper_2210_05105_b200.store import build_store
+    dims = (70000, 20, 15)
+    idx, vals = synth.small_random(dims, 60000, seed=8)
+    dev = torch.device("cuda")
+    ops = ops_for(dev)
+    st = build_store(dims, torch.as_tensor(idx, device=dev), torch.as_tensor(vals, device=dev), 0)
+    gen = np.random.default_rng(1)
+    J, R = 500, 9
+    X = np.stack([gen.integers(0, d, J) for d in dims], 1).astype(np.int64)
+    X[:, 0] = -1
+    Xd = torch.as_tensor(np.ascontiguousarray(X.T), device=dev)
+    H = torch.as_tensor(gen.standard_normal((J, R)), device=dev)
+    w = torch.ones(J, dtype=torch.float64, device=dev)
+    out = torch.full((dims[0], R), 7.0, dtype=torch.float64, device=dev)
+    stats = torch.zeros(8, dtype=torch.int64, device=dev)
+    ops._ws.pop("mttkrp", None)          # a workspace sized for 10 entries
+    ops.status.check()
+    need, have = ops.sampled_mttkrp(st, Xd, 0, H, w, out, stats, cap=10, need=True)
+    assert have < need
+    assert int(ops.status.buf.item()) == pkg._lib.ST_CAPACITY
+    ops.status.reset()
+    assert float(out.abs().max()) == 0.0
+    got, have = ops.sampled_mttkrp(st, Xd, 0, H, w, out, stats, cap=need, need=True)
+    assert got == need <= have
+    ops.status.check()
+    assert float(out.abs().max()) > 0.0
+
+    c_idx = torch.as_tensor(idx, device=dev)
+    c_vals = torch.as_tensor(vals, device=dev)
+    a = make_local_cluster(dims, c_idx, c_vals, 5, 400, "sts", 2)
+    monkeypatch.setattr(engine, "CAP_LIMIT", 16)
+    b = make_local_cluster(dims, c_idx, c_vals, 5, 400, "sts", 2)
+    ops._ws.pop("mttkrp", None)
+    for rnd in (1, 2):                  # b first: its workspace starts at 16 entries
+        b.round(rnd)
+    for rnd in (1, 2):
+        a.round(rnd)
+    assert b.ranks[0].mt_cap[0] > 16     # the first bounded call overflowed and grew
+    for j in range(3):
+        assert torch.equal(a.ranks[0].X, b.ranks[0].X)
+        assert rel_err(b.ranks[0].U[j].cpu().numpy(), a.ranks[0].U[j].cpu().numpy()) < 1e-11
+    assert torch.equal(a.ranks[0].stats, b.ranks[0].stats)
 
 
 # ------------------------------------------------------------------- full ALS
