@@ -28,6 +28,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 METRIC = "sampled-MTTKRP nnz/s"
+L2_GATHER_GBS = 15765.0   # measured: 2^26 random 400-B rows of a 7 MB table, profiles/r01_l2_gather.json
 UNIT = "nnz/s"
 
 
@@ -212,6 +213,7 @@ def run_ours(args):
         step_ms.append(s.elapsed_time(e))
     torch.cuda.synchronize()
     clk = clocks.stop()
+    print("step ms: " + " ".join("%.2f" % x for x in step_ms), file=sys.stderr, flush=True)
     launches = lib.rcp_launch_count() - launches0
     cl.check("in timed rounds")
     # one extra (untimed) round with device phase markers for the breakdown
@@ -276,7 +278,16 @@ def run_ours(args):
                      "frac": achieved / hbm, "traffic": traffic_bytes(args), "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": B / max(n_launch, 1),
                      "avg_launch_ms": mt_ms / max(n_launch, 1), "launches": n_launch,
-                     "share_of_step": mt_ms / max(sum(step_ms), 1e-9)},
+                     "share_of_step": mt_ms / max(sum(step_ms), 1e-9),
+                     # the bound the segmented SpMM actually meets: every distinct gathered
+                     # entry pulls its scaled KRP row (8R bytes) from L2; peak = random 400-B
+                     # row gathers measured on B200 (tools/lab/run_lab.py LABMODE=gather)
+                     "l2_gather": {"bytes_per_launch": 8.0 * R * st[2] / max(n_launch, 1),
+                                   "achieved": (8.0 * R * st[2] / (mt_ms / 1e3)) / 1e9
+                                   if mt_ms > 0 else 0.0,
+                                   "peak": L2_GATHER_GBS, "unit": "GB/s",
+                                   "frac": ((8.0 * R * st[2] / (mt_ms / 1e3)) / 1e9) / L2_GATHER_GBS
+                                   if mt_ms > 0 else 0.0}},
         "clocks": clk,
         "gpu_launches": int(launches),
         "phases_ms_per_round": phases,

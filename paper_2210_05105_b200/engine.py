@@ -87,7 +87,19 @@ class ShufflePrefetch:
         _lib.call("rcp_permutation_host", key.ctypes.data, self.J, buf.data_ptr())
         return buf
 
+    def _prime(self):
+        """Pinned buffers for three rounds up front (a pinned allocation inside a timed
+        round can stall it for milliseconds)."""
+        if getattr(self, "_primed", False):
+            return
+        t = torch()
+        n = 3 * self.N * (self.N - 1)
+        with self.lock:
+            self.free.extend(t.empty(self.J, dtype=t.int64, pin_memory=True) for _ in range(n))
+        self._primed = True
+
     def _request(self, rnd):
+        self._prime()
         for k in range(self.N):
             for i in range(self.N):
                 if i != k and (rnd, k, i) not in self.futs:

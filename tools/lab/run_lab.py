@@ -37,6 +37,8 @@ def main():
     _lib.load()
     cfg = os.environ.get("CFG", "c3")
     sampler = os.environ.get("SAMPLER", "sts")
+    if os.environ.get("LABMODE") == "gather":
+        cfg = "c1"
     c, idx, vals = bench.make_tensor(cfg, 0, dev)
     cl = make_local_cluster(c["dims"], idx, vals, c["R"], c["J"], sampler, 0)
     me = cl.ranks[0]
@@ -70,6 +72,21 @@ def main():
         print(json.dumps(row), flush=True)
         return out
 
+    if os.environ.get("LABMODE") == "gather":
+        for rows in (13690, 65536, 1 << 17):
+            tab = torch.randn(rows * 64, dtype=torch.float64, device=dev)
+            n = 1 << 26
+            sink = torch.zeros(8 + n // 2, dtype=torch.float64, device=dev)
+            sink[8:].view(torch.int32).copy_(torch.randint(0, rows, (n,), dtype=torch.int32,
+                                                           device=dev))
+            ms = ctypes.c_float(0)
+            lab.lab_gather_probe(ctypes.c_void_p(tab.data_ptr()), ctypes.c_int64(rows),
+                                 ctypes.c_int64(n), ctypes.c_void_p(sink.data_ptr()),
+                                 ctypes.byref(ms))
+            print(json.dumps({"probe": "gather400", "table_MB": rows * 512 / 1e6, "gathers": n,
+                              "ms": ms.value, "useful_GBps": n * 400 / ms.value / 1e6,
+                              "sector_GBps": n * 416 / ms.value / 1e6}), flush=True)
+        return
     if os.environ.get("LABMODE") == "probe":
         out = torch.zeros(28818 * 64 + 64, dtype=torch.float64, device=dev)
         for mode, name in ((0, "red_2x_f64"), (1, "red_1x_f64"), (2, "gather_v2")):
