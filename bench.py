@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=0)
     ap.add_argument("--leaf", type=int, default=None, help="STS tree leaf rows (default: engine)")
+    ap.add_argument("--rank", type=int, default=None, help="CP rank (default: the config's)")
+    ap.add_argument("--samples", type=int, default=None, help="J (default: the config's)")
     return ap.parse_args()
 
 
@@ -153,7 +155,9 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     t_setup = time.perf_counter()
     c, idx, vals = make_tensor(args.config, args.seed, dev)
-    dims, R, J = c["dims"], c["R"], c["J"]
+    dims = c["dims"]
+    R = args.rank or c["R"]
+    J = args.samples or c["J"]
     N = len(dims)
     nnz = sum(int(ch[0].shape[0]) for ch in idx) if isinstance(idx, list) else int(idx.shape[0])
     t_gen = time.perf_counter() - t_setup
@@ -346,7 +350,7 @@ def cpu_baseline(args, cl, c, samples=None):
     from oracle import randcp_oracle as O
     me = cl.ranks[0]
     k = me.N - 1
-    samples = samples or args.cpu_samples or (2048 if c["J"] >= 2048 else c["J"])
+    samples = samples or args.cpu_samples or min(2048, cl.J)
     st = me.stores[k]
     # host copy of the mode-k store in the oracle's own layout (built untimed)
     t0 = time.perf_counter()
@@ -364,7 +368,7 @@ def cpu_baseline(args, cl, c, samples=None):
     return {"value": csr.nnz / dt, "unit": UNIT, "cores": workers, "kind": "port",
             "sample": "oracle gather_sampled_nonzeros_to_csr + downsampled_mttkrp, mode %d of %s, "
                       "first %d of J=%d samples of a device STS/ARLS batch; %d nnz iterated in %.2f s "
-                      "(store conversion %.1f s untimed)" % (k, args.config, samples, c["J"], csr.nnz,
+                      "(store conversion %.1f s untimed)" % (k, args.config, samples, cl.J, csr.nnz,
                                                              dt, build_s)}
 
 
@@ -412,7 +416,9 @@ def run_reference(args):
         return
     dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
     c, idx_d, vals_d = make_tensor(args.config, args.seed, dev)   # input generation only
-    dims, R, J = c["dims"], c["R"], c["J"]
+    dims = c["dims"]
+    R = args.rank or c["R"]
+    J = args.samples or c["J"]
     N = len(dims)
     k = N - 1
     # Input state: the factors our timed rounds start from (after `warmup` ALS rounds),

@@ -640,66 +640,6 @@ update_mma_kernel(const double *__restrict__ M, int64_t n, int R, const double *
   }
 }
 
-template <int RPL>
-__global__ void __launch_bounds__(kUpdThreads)
-update_kernel(const double *__restrict__ M, int64_t n, int R, const double *__restrict__ B,
-              double *__restrict__ U, double *__restrict__ part, int *status) {
-  extern __shared__ double sh[];
-  double *Bs = sh;  // R x R
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Bs[e] = B[e];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double sq[RPL];
-  bool bad = false;
-#pragma unroll
-  for (int j = 0; j < RPL; ++j) sq[j] = 0.0;
-  for (int64_t row = (int64_t)blockIdx.x * nw + wid; row < n; row += (int64_t)gridDim.x * nw) {
-    double mv[RPL], acc[RPL];
-#pragma unroll
-    for (int j = 0; j < RPL; ++j) {
-      int c = lane + 32 * j;
-      mv[j] = c < R ? M[row * R + c] : 0.0;
-      acc[j] = 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < RPL; ++j) {
-      const int amax = min(32, R - 32 * j);
-      for (int t = 0; t < amax; ++t) {
-        double ma = __shfl_sync(0xffffffffu, mv[j], t);
-        const double *brow = Bs + (32 * j + t) * R;
-#pragma unroll
-        for (int jj = 0; jj < RPL; ++jj) {
-          int c = lane + 32 * jj;
-          if (c < R) acc[jj] = fma(ma, brow[c], acc[jj]);
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < RPL; ++j) {
-      int c = lane + 32 * j;
-      if (c < R) {
-        U[row * R + c] = acc[j];
-        sq[j] += acc[j] * acc[j];
-        if (!isfinite(acc[j])) bad = true;
-      }
-    }
-  }
-  if (bad) raise_status(status, RCP_ST_NONFINITE);
-  // per-CTA column partials in fixed warp order (deterministic)
-  __syncthreads();
-  double *wsq = sh;  // reuse: nw x R
-#pragma unroll
-  for (int j = 0; j < RPL; ++j) {
-    int c = lane + 32 * j;
-    if (c < R) wsq[wid * R + c] = sq[j];
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < R; c += blockDim.x) {
-    double s = 0.0;
-    for (int w = 0; w < nw; ++w) s += wsq[w * R + c];
-    part[(int64_t)blockIdx.x * R + c] = s;
-  }
-}
 
 __global__ void renorm_kernel(double *__restrict__ U, int64_t n, int R,
                               const double *__restrict__ colsq, double *__restrict__ sigma) {
@@ -813,30 +753,17 @@ int rcp_update(const double *d_M, int64_t n, int R, const double *d_B, double *d
     return RCP_OK;
   }
   const int nw = kUpdThreads / 32;
-  int64_t want = ceil_div(n, nw);
-  int grid = (int)(want < 4LL * sm_count() ? want : 4LL * sm_count());
-  size_t smem = sizeof(double) * (size_t)((R * R > nw * R) ? R * R : nw * R);
-  static bool attr = false;
-  if (!attr) {
-    RCP_CUDA_TRY(cudaFuncSetAttribute(update_kernel<1>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
-    RCP_CUDA_TRY(cudaFuncSetAttribute(update_kernel<2>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
-    RCP_CUDA_TRY(cudaFuncSetAttribute(update_kernel<3>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
-    RCP_CUDA_TRY(cudaFuncSetAttribute(update_kernel<4>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
-    attr = true;
-  }
   double *part = (double *)d_ws;
-  if (R <= 64) {   // fp64 tensor cores
+  {   // fp64 tensor cores (every R <= RCP_MAX_RANK)
     static bool attr_mma = false;
     if (!attr_mma) {
 #define RCP_UPD_ATTR(K)                                                                  \
   RCP_CUDA_TRY(cudaFuncSetAttribute(update_mma_kernel<K>,                                \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024))
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
       RCP_UPD_ATTR(2); RCP_UPD_ATTR(4); RCP_UPD_ATTR(6); RCP_UPD_ATTR(8);
       RCP_UPD_ATTR(10); RCP_UPD_ATTR(12); RCP_UPD_ATTR(14); RCP_UPD_ATTR(16);
+      RCP_UPD_ATTR(18); RCP_UPD_ATTR(20); RCP_UPD_ATTR(22); RCP_UPD_ATTR(24);
+      RCP_UPD_ATTR(26); RCP_UPD_ATTR(28); RCP_UPD_ATTR(30); RCP_UPD_ATTR(32);
 #undef RCP_UPD_ATTR
       attr_mma = true;
     }
@@ -853,22 +780,20 @@ int rcp_update(const double *d_M, int64_t n, int R, const double *d_B, double *d
       case 10: update_mma_kernel<10><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
       case 12: update_mma_kernel<12><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
       case 14: update_mma_kernel<14><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      default: update_mma_kernel<16><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 16: update_mma_kernel<16><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 18: update_mma_kernel<18><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 20: update_mma_kernel<20><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 22: update_mma_kernel<22><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 24: update_mma_kernel<24><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 26: update_mma_kernel<26><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 28: update_mma_kernel<28><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 30: update_mma_kernel<30><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      default: update_mma_kernel<32><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
     }
     RCP_LAUNCH_CHECK("update_mma");
     sum_partials_kernel<<<(unsigned)ceil_div(R, 32), 256, 0, st>>>(part, g, R, d_colsq);
     RCP_LAUNCH_CHECK("update_colsq");
-    return RCP_OK;
   }
-  switch ((R + 31) / 32) {
-    case 1: update_kernel<1><<<grid, kUpdThreads, smem, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-    case 2: update_kernel<2><<<grid, kUpdThreads, smem, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-    case 3: update_kernel<3><<<grid, kUpdThreads, smem, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-    default: update_kernel<4><<<grid, kUpdThreads, smem, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-  }
-  RCP_LAUNCH_CHECK("update");
-  sum_partials_kernel<<<(unsigned)ceil_div(R, 32), 256, 0, st>>>(part, grid, R, d_colsq);
-  RCP_LAUNCH_CHECK("update_colsq");
   return RCP_OK;
 }
 

@@ -26,62 +26,12 @@ int sm_count() {
 }
 
 // ------------------------------------------------------------------ ARLS leverage
-template <int RPL>
-__global__ void __launch_bounds__(256)
-leverage_kernel(const double *__restrict__ U, int64_t n, int R, const double *__restrict__ Gp,
-                double *__restrict__ lev, double *__restrict__ part) {
-  extern __shared__ double sh[];
-  double *G = sh;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) G[e] = Gp[e];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double local = 0.0;
-  for (int64_t row = (int64_t)blockIdx.x * nw + wid; row < n; row += (int64_t)gridDim.x * nw) {
-    double u[RPL], y[RPL];
-#pragma unroll
-    for (int j = 0; j < RPL; ++j) {
-      int c = lane + 32 * j;
-      u[j] = c < R ? U[row * R + c] : 0.0;
-      y[j] = 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < RPL; ++j) {
-      const int amax = min(32, R - 32 * j);
-      for (int t = 0; t < amax; ++t) {
-        double ua = __shfl_sync(0xffffffffu, u[j], t);
-        const double *grow = G + (32 * j + t) * R;
-#pragma unroll
-        for (int jj = 0; jj < RPL; ++jj) {
-          int c = lane + 32 * jj;
-          if (c < R) y[jj] = fma(ua, grow[c], y[jj]);
-        }
-      }
-    }
-    double d = 0.0;
-#pragma unroll
-    for (int j = 0; j < RPL; ++j) d += u[j] * y[j];
-    d = warp_sum(d);
-    d = d > 0.0 ? d : 0.0;
-    if (lane == 0) {
-      lev[row] = d;
-      local += d;
-    }
-  }
-  __syncthreads();
-  if (lane == 0) sh[wid] = local;  // reuse (G no longer needed)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < nw; ++w) s += sh[w];
-    part[blockIdx.x] = s;
-  }
-}
-
-// R <= 64: row leverages on the fp64 tensor cores.  A warp takes 8-row tiles Z of U
+// Row leverages on the fp64 tensor cores (every R <= RCP_MAX_RANK).  A warp takes 8-row tiles Z of U
 // (staged in shared memory), forms Y = Z G+ with mma.m8n8k4 (G+ zero-padded to Rn x Rn in
 // shared memory) and d_q = <Y_q, Z_q>.  Tiles are assigned to warps in a fixed order, so
 // the per-CTA partial masses (and the ordered total) are reproducible.
-constexpr int kLevMmaMaxR = 64;
+constexpr int kLevMmaMaxR = 128;
+static_assert(kLevMmaMaxR >= RCP_MAX_RANK, "leverage scores run on the tensor cores for every rank");
 __host__ __device__ __forceinline__ int lev_rn(int R) { return (R + 7) & ~7; }
 __host__ __device__ __forceinline__ int lev_zs(int R) { return lev_rn(R) + 2; }
 
@@ -368,32 +318,17 @@ int rcp_arls_build(const double *d_U, int64_t n, int R, const double *d_Gp, doub
     RCP_CUDA_TRY(cudaMemsetAsync(d_mass, 0, sizeof(double), st));
     return RCP_OK;
   }
-  int64_t want = ceil_div(n, 8);
+  int64_t want = ceil_div(n, 64);   // 8-row tiles, 8 warps per CTA
   int grid = (int)(want < 4LL * sm_count() ? want : 4LL * sm_count());
   double *part = (double *)d_ws;
   void *scan_ws = (char *)d_ws + (size_t)4 * sm_count() * sizeof(double);
-  size_t smem = sizeof(double) * R * R;
-  static bool attr = false, attr_mma = false;
-  if (!attr) {
-    RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
-    RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
-    RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
-    RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024));
-    attr = true;
+  static bool attr_mma = false;
+  if (!attr_mma) {
+    RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_mma = true;
   }
-  if (R <= kLevMmaMaxR) {
-    if (!attr_mma) {
-      RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-      attr_mma = true;
-    }
-    const size_t sm = sizeof(double) * ((size_t)lev_rn(R) * lev_rn(R) + 8 * 8 * (size_t)lev_zs(R));
-    leverage_mma_kernel<<<grid, 256, sm, st>>>(d_U, n, R, d_Gp, d_dist, part);
-  } else switch ((R + 31) / 32) {
-    case 1: leverage_kernel<1><<<grid, 256, smem, st>>>(d_U, n, R, d_Gp, d_dist, part); break;
-    case 2: leverage_kernel<2><<<grid, 256, smem, st>>>(d_U, n, R, d_Gp, d_dist, part); break;
-    case 3: leverage_kernel<3><<<grid, 256, smem, st>>>(d_U, n, R, d_Gp, d_dist, part); break;
-    default: leverage_kernel<4><<<grid, 256, smem, st>>>(d_U, n, R, d_Gp, d_dist, part); break;
-  }
+  const size_t sm = sizeof(double) * ((size_t)lev_rn(R) * lev_rn(R) + 8 * 8 * (size_t)lev_zs(R));
+  leverage_mma_kernel<<<grid, 256, sm, st>>>(d_U, n, R, d_Gp, d_dist, part);
   RCP_LAUNCH_CHECK("leverage");
   mass_kernel<<<1, 256, 0, st>>>(part, grid, d_mass);
   RCP_LAUNCH_CHECK("leverage_mass");

@@ -46,10 +46,9 @@ constexpr int kMaxLeaf = 64;
 // (same key, same node): each piece recomputes the same child masses, but no warp
 // partitions more than kMaxRun samples.
 constexpr int32_t kLeafChunk = 256;
-constexpr int32_t kMaxRun = 1024;
+constexpr int32_t kMaxRun = 256;
 constexpr int kWalkWarps = 16;
 constexpr int kMaxDepth = 30;   // local tree depth limit (2^30 leaves)
-constexpr int kLeafBatch = 4;   // leaf rows whose masses one pass over the packed pairs makes
 // control words: [0] seeded runs, [2] samples finished, [3] participants,
 // [kGenBase + g] runs pushed during generation g (each generation has its own counter, so
 // the extent of generation g + 1 is stable once every CTA has passed the barrier)
@@ -104,21 +103,22 @@ struct WalkWs {
 
 // Leaf masses on the fp64 tensor cores (mma.m8n8k4) when R <= kMmaMaxR: Y = Z M for a
 // tile of 8 leaf rows Z = U_leaf (.) h, mass_q = <Y_q, Z_q>.
-constexpr int kMmaMaxR = 64;
+constexpr int kMmaMaxR = 128;
+static_assert(kMmaMaxR >= RCP_MAX_RANK, "leaf masses run on the tensor cores for every rank");
 __host__ __device__ __forceinline__ int mma_rn(int R) { return (R + 7) & ~7; }
 __host__ __device__ __forceinline__ int mma_zs(int R) { return mma_rn(R) + 2; }   // Z row stride
 
 // Shared doubles per walker warp: h, leaf rows z = u (.) h (a batch, or an 8-row mma
 // tile), leaf masses, path.
 __host__ __device__ __forceinline__ size_t walk_per_warp(int R) {
-  const size_t zb = R <= kMmaMaxR ? (size_t)8 * mma_zs(R) : (size_t)kLeafBatch * R;
+  const size_t zb = (size_t)8 * mma_zs(R);
   const size_t w = (size_t)R + zb + kMaxLeaf;
   return (w + 1) & ~(size_t)1;
 }
 
 // Block-shared doubles: the full padded M (mma path) or packed M' (fallback).
 __host__ __device__ __forceinline__ size_t walk_block_doubles(int R) {
-  return R <= kMmaMaxR ? (size_t)mma_rn(R) * mma_rn(R) : (size_t)tri_stride(R);
+  return (size_t)mma_rn(R) * mma_rn(R);
 }
 
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
@@ -323,7 +323,7 @@ __device__ __forceinline__ void fail_run(int32_t lo, int32_t hi, const int32_t *
 
 __global__ void __launch_bounds__(kWalkWarps * 32, 2)
 walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, int64_t n, int R,
-                 int leaf, int depth, int64_t row_lo, const double *__restrict__ Mp_g,
+                 int leaf, int depth, int64_t row_lo,
                  const double *__restrict__ Mfull,
                  const uint32_t *__restrict__ pairs_g, const double *__restrict__ H,
                  double *__restrict__ rA, double *__restrict__ rB, int32_t *__restrict__ iA,
@@ -332,25 +332,19 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
                  double *__restrict__ resid, double *__restrict__ Hout, int *status,
                  unsigned long long *prof) {
   extern __shared__ double sh[];
-  const int Rt = R * (R + 1) / 2;
   const int Rs = tri_stride(R);                    // even node stride (zero pad)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const bool use_mma = R <= kMmaMaxR;
   const int Rn = mma_rn(R), Zs = mma_zs(R);
   const size_t bd = walk_block_doubles(R);
-  double *Mp = sh;                                 // packed M' (fallback) or full M (mma)
+  double *Mp = sh;                                 // full M, zero-padded to Rn x Rn
   double *hv = sh + bd + (size_t)wid * walk_per_warp(R);   // R: the run's Hadamard row
   double *zb = hv + R;                             // leaf rows (.) h
-  double *mass = zb + (use_mma ? 8 * Zs : kLeafBatch * R);   // leaf
+  double *mass = zb + 8 * Zs;                      // leaf
   uint32_t *pairs = reinterpret_cast<uint32_t *>(sh + bd + (size_t)nw * walk_per_warp(R));
   for (int e = threadIdx.x; e < Rs; e += blockDim.x) pairs[e] = pairs_g[e];
-  if (use_mma) {
-    for (int e = threadIdx.x; e < Rn * Rn; e += blockDim.x) {
-      const int k = e / Rn, c = e - k * Rn;
-      Mp[e] = (k < R && c < R) ? Mfull[k * R + c] : 0.0;
-    }
-  } else {
-    for (int e = threadIdx.x; e < Rs; e += blockDim.x) Mp[e] = Mp_g[e];
+  for (int e = threadIdx.x; e < Rn * Rn; e += blockDim.x) {
+    const int k = e / Rn, c = e - k * Rn;
+    Mp[e] = (k < R && c < R) ? Mfull[k * R + c] : 0.0;
   }
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
@@ -479,7 +473,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
       const double rprob = run.prob;
       bool bad = nrow <= 0;
       double total_m = 0.0;
-      if (!bad && use_mma) {
+      if (!bad) {
         // 8-row tiles: Y = Z M on the fp64 tensor cores, mass_q = <Y_q, Z_q>
         const int row = lane >> 2, quad = lane & 3;
         for (int q0 = 0; q0 < nrow; q0 += 8) {
@@ -503,34 +497,6 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
           if (quad == 0 && row < nb) mass[q0 + row] = msum > 0.0 ? msum : 0.0;
           __syncwarp();
         }
-      } else if (!bad) {
-        for (int q0 = 0; q0 < nrow; q0 += kLeafBatch) {
-          const int nb = min(kLeafBatch, nrow - q0);
-          for (int c = lane; c < nb * R; c += 32) {
-            const int j = c / R, col = c - j * R;
-            zb[c] = U[(r0 + q0 + j) * R + col] * hv[col];
-          }
-          __syncwarp();
-          double m[kLeafBatch];
-#pragma unroll
-          for (int j = 0; j < kLeafBatch; ++j) m[j] = 0.0;
-          for (int e = lane; e < Rt; e += 32) {
-            const uint32_t ab = pairs[e];
-            const int ia = ab & 0xffffu, ib = ab >> 16;
-            const double pe = Mp[e];
-#pragma unroll
-            for (int j = 0; j < kLeafBatch; ++j)
-              if (j < nb) m[j] = fma(zb[j * R + ia] * zb[j * R + ib], pe, m[j]);
-          }
-#pragma unroll
-          for (int j = 0; j < kLeafBatch; ++j) {
-            if (j < nb) {
-              const double mj = warp_sum(m[j]);
-              if (lane == 0) mass[q0 + j] = mj > 0.0 ? mj : 0.0;
-            }
-          }
-          __syncwarp();
-        }
       }
       if (!bad) {
         if (lane == 0)
@@ -544,7 +510,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
       }
       // blocks of kLeafChunk samples: lanes pick rows, then (optionally) the warp writes the
       // folded Hadamard rows from the staged leaf rows z = u (.) h
-      const bool zrows = use_mma && nrow <= 8;   // zb holds every row of this leaf
+      const bool zrows = nrow <= 8;   // zb holds every row of this leaf
       for (int32_t b0 = lo; b0 < hi; b0 += kLeafChunk) {
         const int32_t b1 = min(hi, b0 + kLeafChunk);
         for (int32_t s = b0 + lane; s < b1; s += 32) {
@@ -695,7 +661,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   // persistent: every CTA resident at once (workers wait on the shared queue)
   const int grid = per_sm * sm_count();
   // cooperative launch: every CTA co-resident, grid-wide barrier between tree levels
-  const double *a_gm = gm, *a_U = d_U, *a_Mp = Mp, *a_H = d_H_in, *a_Mf = d_M;
+  const double *a_gm = gm, *a_U = d_U, *a_H = d_H_in, *a_Mf = d_M;
   const uint32_t *a_pairs = pairs;
   double *a_rA = r, *a_rB = r2;
   int32_t *a_iA = idx2, *a_iB = idx3;
@@ -703,7 +669,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   int64_t a_n = n, a_row_lo = row_lo, a_cap = L.nruns;
   int a_R = R, a_leaf = leaf, a_depth = depth;
   void *args[] = {(void *)&a_gm, (void *)&a_U, (void *)&a_n, (void *)&a_R, (void *)&a_leaf,
-                  (void *)&a_depth, (void *)&a_row_lo, (void *)&a_Mp, (void *)&a_Mf,
+                  (void *)&a_depth, (void *)&a_row_lo, (void *)&a_Mf,
                   (void *)&a_pairs,
                   (void *)&a_H, (void *)&a_rA, (void *)&a_rB, (void *)&a_iA, (void *)&a_iB,
                   (void *)&runs, (void *)&ctl,

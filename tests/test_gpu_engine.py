@@ -198,13 +198,14 @@ def test_host_step_api_matches_device_round(P):
     assert rel_err(sess.sigma.numpy(), b.ranks[0].sigma.cpu().numpy()) < 1e-12
 
 
-@pytest.mark.parametrize("sampler", ["sts", "arls-lev"])
-def test_rank_above_64_generic_paths(P, sampler):
-    """R > 64 leaves the fp64 tensor-core paths (leaf masses, update GEMM) and uses the
-    generic kernels (two column pairs per lane in the SpMM, register GJ with 8x4 tiles)."""
+@pytest.mark.parametrize("sampler,R", [("sts", 70), ("arls-lev", 70), ("sts", 128)])
+def test_rank_above_64(P, sampler, R):
+    """R > 64: tensor-core tiles padded past 64 columns (leaf masses, leverage, update
+    GEMM), two column pairs per lane in the SpMM, register GJ with 8x4 tiles; R = 128 is
+    the largest supported rank (fewer walker warps fit in shared memory)."""
     dims = (120, 100, 90)
-    res, st, fits = run_both(P, dims, 30000, 70, sampler, 512, 2)
-    h = horizon(dims, 30000, 70, sampler, 512, 2, 1)
+    res, st, fits = run_both(P, dims, 30000, R, sampler, 512, 2)
+    h = horizon(dims, 30000, R, sampler, 512, 2, 1)
     for a, b in list(zip(res.sample_log, st.sample_log))[:h]:
         assert np.array_equal(a, b)
     if h == len(st.sample_log):
