@@ -41,11 +41,13 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
                : "d"(a), "d"(b));
 }
 
+template <int KS>   // k-steps = Rn / 4
 __global__ void __launch_bounds__(256)
 leverage_mma_kernel(const double *__restrict__ U, int64_t n, int R, const double *__restrict__ Gp,
                     double *__restrict__ lev, double *__restrict__ part) {
   extern __shared__ double sh[];
-  const int Rn = lev_rn(R), Zs = lev_zs(R);
+  constexpr int Rn = KS * 4;
+  const int Zs = lev_zs(R);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double *G = sh;                                   // Rn x Rn
   double *zb = sh + Rn * Rn + (size_t)wid * 8 * Zs;  // this warp's 8 x Zs tile
@@ -66,11 +68,16 @@ leverage_mma_kernel(const double *__restrict__ U, int64_t n, int R, const double
     }
     __syncwarp();
     const double *zr = zb + row * Zs;
+    double a[KS];   // A fragments of the tile, reused by every n-tile
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) a[ks] = zr[ks * 4 + quad];
     double msum = 0.0;
+#pragma unroll
     for (int nt = 0; nt < Rn; nt += 8) {
       double c0 = 0.0, c1 = 0.0;
-      for (int ks = 0; ks < Rn; ks += 4)
-        dmma_8x8x4(c0, c1, zr[ks + quad], G[(ks + quad) * Rn + nt + row]);
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks)
+        dmma_8x8x4(c0, c1, a[ks], G[(ks * 4 + quad) * Rn + nt + row]);
       msum = fma(c0, zr[nt + 2 * quad], msum);
       msum = fma(c1, zr[nt + 2 * quad + 1], msum);
     }
@@ -322,13 +329,24 @@ int rcp_arls_build(const double *d_U, int64_t n, int R, const double *d_Gp, doub
   int grid = (int)(want < 4LL * sm_count() ? want : 4LL * sm_count());
   double *part = (double *)d_ws;
   void *scan_ws = (char *)d_ws + (size_t)4 * sm_count() * sizeof(double);
-  static bool attr_mma = false;
-  if (!attr_mma) {
-    RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_mma = true;
-  }
   const size_t sm = sizeof(double) * ((size_t)lev_rn(R) * lev_rn(R) + 8 * 8 * (size_t)lev_zs(R));
-  leverage_mma_kernel<<<grid, 256, sm, st>>>(d_U, n, R, d_Gp, d_dist, part);
+  static bool attr_set[17] = {};
+#define RCP_LEV(K)                                                                              \
+  case K:                                                                                       \
+    if (!attr_set[K / 2]) {                                                                     \
+      RCP_CUDA_TRY(cudaFuncSetAttribute(leverage_mma_kernel<K>,                                 \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
+      attr_set[K / 2] = true;                                                                   \
+    }                                                                                           \
+    leverage_mma_kernel<K><<<grid, 256, sm, st>>>(d_U, n, R, d_Gp, d_dist, part);               \
+    break
+  switch (lev_rn(R) / 4) {
+    RCP_LEV(2); RCP_LEV(4); RCP_LEV(6); RCP_LEV(8); RCP_LEV(10); RCP_LEV(12); RCP_LEV(14);
+    RCP_LEV(16); RCP_LEV(18); RCP_LEV(20); RCP_LEV(22); RCP_LEV(24); RCP_LEV(26); RCP_LEV(28);
+    RCP_LEV(30); RCP_LEV(32);
+    default: return RCP_ERR_ARG;
+  }
+#undef RCP_LEV
   RCP_LAUNCH_CHECK("leverage");
   mass_kernel<<<1, 256, 0, st>>>(part, grid, d_mass);
   RCP_LAUNCH_CHECK("leverage_mass");

@@ -10,7 +10,8 @@ import sys
 MTTKRP = ("hash_insert", "compact_count", "compact_write", "lookup_kernel", "finalize_counts",
           "item_count", "item_fill", "cta_hist", "cta_prefix", "rows_hit", "cta_scatter",
           "bucket_offsets", "bucket_scatter", "bucket_rows", "spmm_packed", "row_count",
-          "scatter_kernel")
+          "scatter_kernel", "big_hist", "big_colprefix", "big_offsets", "big_rows",
+          "mttkrp_init")
 
 
 def short(name):
