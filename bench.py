@@ -147,10 +147,13 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # RCP_SPMD=1 runs the torch.distributed (NCCL) code path even at world size 1 (a check
+    # of the multi-GPU plumbing on a single GPU)
+    spmd = world > 1 or os.environ.get("RCP_SPMD") == "1"
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     _lib.load()
-    if world > 1:
+    if spmd:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     t_setup = time.perf_counter()
@@ -161,7 +164,7 @@ def run_ours(args):
     N = len(dims)
     nnz = sum(int(ch[0].shape[0]) for ch in idx) if isinstance(idx, list) else int(idx.shape[0])
     t_gen = time.perf_counter() - t_setup
-    if world > 1:
+    if spmd:
         from paper_2210_05105_b200.dist import make_spmd_cluster
         cl = make_spmd_cluster(dims, idx, vals, R, J, args.sampler, args.seed, leaf=args.leaf)
     else:
@@ -196,7 +199,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     mt_events.clear()
     stats0 = me.stats.clone()
-    if world > 1:
+    if spmd:
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize()
@@ -232,7 +235,7 @@ def run_ours(args):
     st = (me.stats - stats0).cpu().numpy().astype(np.int64)
     mt_ms = sum(a.elapsed_time(b) for a, b in mt_events)
     t_total = sum(step_ms) / 1e3
-    if world > 1:
+    if spmd:
         import torch.distributed as dist
         tt = torch.tensor([t_total, float(st[3]), float(st[2])], dtype=torch.float64, device=dev)
         gathered = [torch.zeros_like(tt) for _ in range(world)]
@@ -251,7 +254,7 @@ def run_ours(args):
     n_launch = len(mt_events)
     achieved = (B / (mt_ms / 1e3)) / 1e9 if mt_ms > 0 else 0.0
     e2e = measure_e2e(cl, args, rnd)
-    if world > 1:
+    if spmd:
         import torch.distributed as dist
         tt = torch.tensor([e2e.pop("_dt"), e2e.pop("_nnz")], dtype=torch.float64, device=dev)
         gathered = [torch.zeros_like(tt) for _ in range(world)]
@@ -309,7 +312,7 @@ def run_ours(args):
             out["cpu_baseline"] = {"value": None, "error": repr(ex)[:200]}
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if spmd:
         import torch.distributed as dist
         dist.destroy_process_group()
 
