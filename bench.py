@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--cpu-samples", type=int, default=0)
     ap.add_argument("--leaf", type=int, default=None, help="STS tree leaf rows (default: engine)")
     ap.add_argument("--rank", type=int, default=None, help="CP rank (default: the config's)")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch every kernel from the host (default: replay STS rounds from a "
+                         "CUDA graph when the cluster allows it)")
     ap.add_argument("--samples", type=int, default=None, help="J (default: the config's)")
     return ap.parse_args()
 
@@ -190,12 +193,19 @@ def run_ours(args):
         e.record()
         mt_events.append((s, e))
         return out
-    me.mttkrp = timed_mttkrp
-
+    use_graph = (not args.eager) and cl.graph_ok()
+    # events cannot time calls inside a replayed graph: with graphs, the MTTKRP call
+    # durations come from eager rounds of the same kernels after the timed region
+    me.mttkrp = orig if use_graph else timed_mttkrp
     rnd = 0
-    for _ in range(args.warmup):
+    for w in range(args.warmup):
         rnd += 1
-        cl.round(rnd)
+        if use_graph and w > 0:   # the first warm-up round sizes every workspace eagerly
+            cl.round_graph(rnd)
+            torch.cuda.synchronize()
+            cl.check("in warm-up round %d" % rnd)
+        else:
+            cl.round(rnd)
     torch.cuda.synchronize()
     mt_events.clear()
     stats0 = me.stats.clone()
@@ -214,7 +224,10 @@ def run_ours(args):
         e = torch.cuda.Event(enable_timing=True)
         rnd += 1
         s.record()
-        cl.round(rnd, check=False)
+        if use_graph:
+            cl.round_graph(rnd)
+        else:
+            cl.round(rnd, check=False)
         e.record()
         e.synchronize()
         step_ms.append(s.elapsed_time(e))
@@ -222,7 +235,24 @@ def run_ours(args):
     clk = clocks.stop()
     print("step ms: " + " ".join("%.2f" % x for x in step_ms), file=sys.stderr, flush=True)
     launches = lib.rcp_launch_count() - launches0
+    if use_graph:   # replayed kernels do not pass through the host-side launch counter
+        launches += cl.graph_kernels * args.steps
     cl.check("in timed rounds")
+    st = (me.stats - stats0).cpu().numpy().astype(np.int64)
+    if use_graph:
+        me.mttkrp = timed_mttkrp
+        mt_events.clear()
+        s1 = me.stats.clone()
+        for _ in range(args.steps):
+            flush_l2(flush)
+            rnd += 1
+            cl.round(rnd, check=False)
+        torch.cuda.synchronize()
+        st_mt = (me.stats - s1).cpu().numpy().astype(np.int64)
+    else:
+        st_mt = st
+    mt_ms = sum(a.elapsed_time(b) for a, b in mt_events)
+    n_launch = len(mt_events)
     # one extra (untimed) round with device phase markers for the breakdown
     cl.phase_events = []
     me.mttkrp = orig
@@ -231,9 +261,6 @@ def run_ours(args):
     torch.cuda.synchronize()
     phases = {k: round(v, 4) for k, v in cl.phase_breakdown().items()}
     cl.phase_events = None
-    me.mttkrp = timed_mttkrp
-    st = (me.stats - stats0).cpu().numpy().astype(np.int64)
-    mt_ms = sum(a.elapsed_time(b) for a, b in mt_events)
     t_total = sum(step_ms) / 1e3
     if spmd:
         import torch.distributed as dist
@@ -250,8 +277,7 @@ def run_ours(args):
     hbm, peak_kind = peaks()
     # algorithmic bytes of the sampled MTTKRP:
     #   12 nnz_d + 16 S_d + 8R S_ne + 8R rows_hit  per solve, summed over the timed solves
-    B = 12.0 * st[2] + 16.0 * st[0] + 8.0 * R * st[1] + 8.0 * R * st[4]
-    n_launch = len(mt_events)
+    B = 12.0 * st_mt[2] + 16.0 * st_mt[0] + 8.0 * R * st_mt[1] + 8.0 * R * st_mt[4]
     achieved = (B / (mt_ms / 1e3)) / 1e9 if mt_ms > 0 else 0.0
     e2e = measure_e2e(cl, args, rnd)
     if spmd:
@@ -275,7 +301,8 @@ def run_ours(args):
                    "parallelism": "as%d" % world, "l2": "256 MB flush between timed rounds "
                    "(outside the round events); stores %.1f GB > L2" % (
                        sum(s.bytes() for s in me.stores) / 1e9),
-                   "setup_s": round(setup_s, 1), "generate_s": round(t_gen, 1)},
+                   "setup_s": round(setup_s, 1), "generate_s": round(t_gen, 1),
+                   "launch": "cuda-graph replay of the round" if use_graph else "eager"},
         "rounds_per_s": K / t_total,
         "distinct_nnz_per_s": nnz_d / t_total,
         "sampled_nnz_per_round": nnz_m / K,
@@ -289,12 +316,14 @@ def run_ours(args):
                      # the bound the segmented SpMM actually meets: every distinct gathered
                      # entry pulls its scaled KRP row (8R bytes) from L2; peak = random 400-B
                      # row gathers measured on B200 (tools/lab/run_lab.py LABMODE=gather)
-                     "l2_gather": {"bytes_per_launch": 8.0 * R * st[2] / max(n_launch, 1),
-                                   "achieved": (8.0 * R * st[2] / (mt_ms / 1e3)) / 1e9
+                     "l2_gather": {"bytes_per_launch": 8.0 * R * st_mt[2] / max(n_launch, 1),
+                                   "achieved": (8.0 * R * st_mt[2] / (mt_ms / 1e3)) / 1e9
                                    if mt_ms > 0 else 0.0,
                                    "peak": L2_GATHER_GBS, "unit": "GB/s",
-                                   "frac": ((8.0 * R * st[2] / (mt_ms / 1e3)) / 1e9) / L2_GATHER_GBS
-                                   if mt_ms > 0 else 0.0}},
+                                   "frac": ((8.0 * R * st_mt[2] / (mt_ms / 1e3)) / 1e9) / L2_GATHER_GBS
+                                   if mt_ms > 0 else 0.0},
+                     "launch_timing": "eager rounds after the timed region" if use_graph
+                     else "inside the timed rounds"},
         "clocks": clk,
         "gpu_launches": int(launches),
         "phases_ms_per_round": phases,
@@ -328,12 +357,14 @@ def measure_e2e(cl, args, rnd, steps=None):
     host_out = sess.pinned_factors()
     steps = steps or max(2, args.steps)
     me = cl.ranks[0]
-    sess.step_host(host_in, host_out, rnd + 1)
+    graph = not args.eager
+    sess.step_host(host_in, host_out, rnd + 1)   # eager: sizes every workspace
+    sess.step_host(host_in, host_out, rnd + 2, graph=graph)
     torch.cuda.synchronize()
     st0 = me.stats.clone()
     t0 = time.perf_counter()
     for s in range(steps):
-        sess.step_host(host_in, host_out, rnd + 2 + s)
+        sess.step_host(host_in, host_out, rnd + 3 + s, graph=graph)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     st = (me.stats - st0).cpu().numpy()
@@ -341,7 +372,8 @@ def measure_e2e(cl, args, rnd, steps=None):
             "h2d_bytes_per_step": int(sum(h.numel() * 8 for h in host_in)),
             "d2h_bytes_per_step": int(sum(h.numel() * 8 for h in host_out) + 8 * me.R),
             "steps": steps, "ms_per_step": dt / steps * 1e3, "_dt": dt, "_nnz": float(st[3]),
-            "api": "AlsSession.step_host (pinned host factors in, factors + sigma out)"}
+            "api": "AlsSession.step_host (pinned host factors in, factors + sigma out)" +
+                   (", round replayed from a CUDA graph" if graph and cl.graph_ok() else "")}
 
 
 # ------------------------------------------------------------------ CPU arms

@@ -50,6 +50,10 @@ extern "C" {
 
 #define RCP_MAX_RANK 128
 
+/* Stream keys: entry points that draw from a Philox stream take its key by value
+ * (key0, key1) and, optionally, `d_key`: a device pointer to the two key words that
+ * overrides them when non-NULL, so a captured CUDA graph can replay a round with the
+ * next round's keys written into device memory beforehand. */
 /* ---------------------------------------------------------------- version / errors */
 const char *rcp_version(void);
 const char *rcp_last_error(void);
@@ -123,8 +127,9 @@ int rcp_arls_build(const double *d_U, int64_t n, int R, const double *d_Gp, doub
  * d_urow_out (nullable): also copies the drawn factor rows U[row - row_lo] (q x R). */
 int rcp_arls_draw(const double *d_cdf, const double *d_dist, int64_t n, int64_t row_lo,
                   double mass_ratio, const double *d_total_mass, uint64_t key0, uint64_t key1,
-                  int64_t q, int64_t offset, int64_t *d_rows_out, double *d_prob_out,
-                  const double *d_U, int R, double *d_urow_out, int *d_status, void *stream);
+                  const uint64_t *d_key, int64_t q, int64_t offset, int64_t *d_rows_out,
+                  double *d_prob_out, const double *d_U, int R, double *d_urow_out, int *d_status,
+                  void *stream);
 /* Apply the SHUFFLE permutation and fold mode i into the batch:
  * X_i[s] = rows[perm[s]], pmp_i[s] = prob[perm[s]], H[s,:] (*)= row(perm[s]) where
  * row(t) = d_urows[t,:] when d_urows != NULL, else U[rows[t] - u_row_lo, :].
@@ -177,7 +182,8 @@ int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
 size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf, int R);
 int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
                  int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
-                 int key_bits, int64_t J, uint64_t key0, uint64_t key1, const double *d_override,
+                 int key_bits, int64_t J, uint64_t key0, uint64_t key1, const uint64_t *d_key,
+                 const double *d_override,
                  const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
                  double *d_pmp_i, double *d_resid, double *d_H_out, void *d_ws, size_t ws_bytes,
                  int *d_status,
@@ -195,7 +201,8 @@ int rcp_fold_rows(double *d_out, const double *d_U, int64_t n, int R, int64_t ro
  * pmp_i[s] = mass/total.  Same distribution and inverse-CDF map as the tree walk (ref
  * samplers.py:291-310, 379-468); RCP_ST_DEGENERATE when the total mass is zero. */
 int rcp_sts_flat_draw(const double *d_cdf, const double *d_dist, int64_t n, int64_t row_lo,
-                      const double *d_total_mass, uint64_t key0, uint64_t key1, int64_t J,
+                      const double *d_total_mass, uint64_t key0, uint64_t key1,
+                      const uint64_t *d_key, int64_t J,
                       int64_t *d_Xi, double *d_pmp_i, int *d_status, void *stream);
 /* d_out[s] = sum_m X[m*J + s] * strides[m] over modes with nonzero stride (mixed-radix
  * key of a subset of a sample's indices; ref matricization.py:41-54 for the MTTKRP

@@ -46,8 +46,8 @@ _SIGS = {
     "rcp_renormalize": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "rcp_arls_build_ws_bytes": (_sz, [_i64, _i32]),
     "rcp_arls_build": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "rcp_arls_draw": (_i32, [_vp, _vp, _i64, _i64, _f64, _vp, _u64, _u64, _i64, _i64, _vp, _vp,
-                             _vp, _i32, _vp, _vp, _vp]),
+    "rcp_arls_draw": (_i32, [_vp, _vp, _i64, _i64, _f64, _vp, _u64, _u64, _vp, _i64, _i64, _vp,
+                             _vp, _vp, _i32, _vp, _vp, _vp]),
     "rcp_batch_fold": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _vp, _i32, _i32, _vp, _vp, _vp,
                               _vp]),
     "rcp_sts_depth": (_i32, [_i64, _i32]),
@@ -58,10 +58,11 @@ _SIGS = {
     "rcp_sts_build": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp]),
     "rcp_sts_walk_ws_bytes": (_sz, [_i64, _i64, _i32, _i32]),
     "rcp_sts_walk": (_i32, [_vp, _vp, _i64, _i32, _i32, _i64, _vp, _vp, _vp, _i32, _i64, _u64, _u64,
-                            _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
+                            _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     "rcp_fold_rows": (_i32, [_vp, _vp, _i64, _i32, _i64, _vp, _i64, _i32, _vp, _i32, _vp]),
     "rcp_row_keys": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp]),
-    "rcp_sts_flat_draw": (_i32, [_vp, _vp, _i64, _i64, _vp, _u64, _u64, _i64, _vp, _vp, _vp, _vp]),
+    "rcp_sts_flat_draw": (_i32, [_vp, _vp, _i64, _i64, _vp, _u64, _u64, _vp, _i64, _vp, _vp, _vp,
+                                 _vp]),
     "rcp_hadamard_rows": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp]),
     "rcp_weights": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp, _vp]),
     "rcp_mttkrp_ws_bytes": (_sz, [_i64, _i64, _i64, _i32]),

@@ -194,11 +194,13 @@ class AlsSession:
             out.append(h)
         return out
 
-    def step_host(self, factors_in, factors_out, rnd):
+    def step_host(self, factors_in, factors_out, rnd, graph=False):
         """Upload factors (pinned host) -> rebuild sampler state -> one ALS round ->
         download the updated factors and sigma.  Transfers run on a copy stream: mode j's
         upload overlaps the rebuild of the modes before it, and factor k's download
-        overlaps the solves after k."""
+        overlaps the solves after k.  graph=True replays the round (with its downloads)
+        from a CUDA graph when the cluster allows it (Cluster.graph_ok); the buffers in
+        `factors_out` must then be the same on every call."""
         t = torch()
         r0 = self.cl.ranks[0]
         if len(self.cl.ranks) != 1:
@@ -225,7 +227,10 @@ class AlsSession:
             with t.cuda.stream(self.copy):
                 factors_out[k].copy_(r0.U[k], non_blocking=True)
 
-        self.cl.round(rnd, check=False, on_solved=download)
+        if graph and self.cl.graph_ok():
+            self.cl.round_graph(rnd, on_solved=download, join=(self.copy,), tag="step_host")
+        else:
+            self.cl.round(rnd, check=False, on_solved=download)
         self.sigma = r0.sigma.to("cpu", non_blocking=True)
         main.wait_stream(self.copy)
         main.synchronize()

@@ -132,12 +132,17 @@ __global__ void cdf_div_kernel(double *__restrict__ cdf, int64_t n) {
 
 __global__ void arls_draw_kernel(const double *__restrict__ cdf, const double *__restrict__ dist,
                                  int64_t n, int64_t row_lo, double ratio, const double *tmass,
-                                 uint64_t k0, uint64_t k1, int64_t q, int64_t offset,
+                                 uint64_t k0, uint64_t k1, const uint64_t *__restrict__ dkey,
+                                 int64_t q, int64_t offset,
                                  int64_t *__restrict__ rows, double *__restrict__ prob,
                                  const double *__restrict__ U, int R, double *__restrict__ urow,
                                  int *status, int zero_flag) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= q) return;
+  if (dkey) {   // stream key resident on the device (graph-replayed rounds)
+    k0 = dkey[0];
+    k1 = dkey[1];
+  }
   if (tmass && !(tmass[0] > 0.0)) {
     if (t == 0) raise_status(status, zero_flag);
     rows[offset + t] = row_lo;
@@ -363,25 +368,27 @@ int rcp_arls_build(const double *d_U, int64_t n, int R, const double *d_Gp, doub
 
 int rcp_arls_draw(const double *d_cdf, const double *d_dist, int64_t n, int64_t row_lo,
                   double mass_ratio, const double *d_total_mass, uint64_t key0, uint64_t key1,
-                  int64_t q, int64_t offset, int64_t *d_rows_out, double *d_prob_out,
-                  const double *d_U, int R, double *d_urow_out, int *d_status, void *stream) {
+                  const uint64_t *d_key, int64_t q, int64_t offset, int64_t *d_rows_out,
+                  double *d_prob_out, const double *d_U, int R, double *d_urow_out, int *d_status,
+                  void *stream) {
   if (q < 0 || n < 1 || !d_cdf || !d_dist || !d_rows_out || !d_prob_out) return RCP_ERR_ARG;
   if (d_urow_out && (!d_U || R < 1)) return RCP_ERR_ARG;
   if (q == 0) return RCP_OK;
   arls_draw_kernel<<<(unsigned)ceil_div(q, 256), 256, 0, RCP_STREAM(stream)>>>(
-      d_cdf, d_dist, n, row_lo, mass_ratio, d_total_mass, key0, key1, q, offset, d_rows_out,
+      d_cdf, d_dist, n, row_lo, mass_ratio, d_total_mass, key0, key1, d_key, q, offset, d_rows_out,
       d_prob_out, d_U, R, d_urow_out, d_status, RCP_ST_ZERO_MASS);
   RCP_LAUNCH_CHECK("arls_draw");
   return RCP_OK;
 }
 
 int rcp_sts_flat_draw(const double *d_cdf, const double *d_dist, int64_t n, int64_t row_lo,
-                      const double *d_total_mass, uint64_t key0, uint64_t key1, int64_t J,
+                      const double *d_total_mass, uint64_t key0, uint64_t key1,
+                      const uint64_t *d_key, int64_t J,
                       int64_t *d_Xi, double *d_pmp_i, int *d_status, void *stream) {
   if (J < 0 || n < 1 || !d_cdf || !d_dist || !d_Xi || !d_pmp_i || !d_total_mass) return RCP_ERR_ARG;
   if (J == 0) return RCP_OK;
   arls_draw_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, RCP_STREAM(stream)>>>(
-      d_cdf, d_dist, n, row_lo, 1.0, d_total_mass, key0, key1, J, 0, d_Xi, d_pmp_i, nullptr, 0,
+      d_cdf, d_dist, n, row_lo, 1.0, d_total_mass, key0, key1, d_key, J, 0, d_Xi, d_pmp_i, nullptr, 0,
       nullptr, d_status, RCP_ST_DEGENERATE);
   RCP_LAUNCH_CHECK("sts_flat_draw");
   return RCP_OK;

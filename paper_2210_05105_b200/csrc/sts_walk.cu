@@ -153,10 +153,15 @@ __global__ void walk_prepare_kernel(const int64_t *__restrict__ hkey_in, int64_t
 
 // Level-0 buffer: the uniform of each sample in key order.
 __global__ void walk_fill_r_kernel(const int32_t *__restrict__ idx, int64_t J, uint64_t k0,
-                                   uint64_t k1, const double *__restrict__ ov,
+                                   uint64_t k1, const uint64_t *__restrict__ dkey,
+                                   const double *__restrict__ ov,
                                    const double *__restrict__ rin, double *__restrict__ r) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= J) return;
+  if (dkey) {   // stream key resident on the device (graph-replayed rounds)
+    k0 = dkey[0];
+    k1 = dkey[1];
+  }
   const int32_t s = idx[i];
   double u;
   if (ov) u = ov[s];
@@ -592,7 +597,8 @@ size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf, int R) {
 
 int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
                  int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
-                 int key_bits, int64_t J, uint64_t key0, uint64_t key1, const double *d_override,
+                 int key_bits, int64_t J, uint64_t key0, uint64_t key1, const uint64_t *d_key,
+                 const double *d_override,
                  const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
                  double *d_pmp_i, double *d_resid, double *d_H_out, void *d_ws, size_t ws_bytes,
                  int *d_status,
@@ -632,7 +638,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   RCP_CUDA_TRY(
       cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key, key2, idx, idx2, (int)J, 0, key_bits, st));
   RCP_LAUNCH_CHECK("walk_sort_key");
-  walk_fill_r_kernel<<<gb, 256, 0, st>>>(idx2, J, key0, key1, d_override, d_rin, r);
+  walk_fill_r_kernel<<<gb, 256, 0, st>>>(idx2, J, key0, key1, d_key, d_override, d_rin, r);
   RCP_LAUNCH_CHECK("walk_fill_r");
   walk_seed_kernel<<<gb, 256, 0, st>>>(key2, idx2, J, d_sel ? d_pmp_i : nullptr, runs, ctl);
   RCP_LAUNCH_CHECK("walk_seed");

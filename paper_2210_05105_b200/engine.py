@@ -199,6 +199,7 @@ class RankState:
         self.Mout = t.zeros((max(self.n) if N else 0, R), **f64)
         self.stats = t.zeros(8, dtype=t.int64, device=dev)
         self.mt_cap = {}
+        self.dkeys = None        # (N, N, 2) WALK_UNIFORM keys of the round (graph mode)
         self.block_gram_buf = t.zeros((R, R), **f64)
 
     # -------------------------------------------------------------- set-up
@@ -304,7 +305,10 @@ class RankState:
         leaf lies in its block (all of them when P == 1)."""
         ops = self.ops
         ops.sts_cond(self.chain_pinv, self.grams, i, k, self.M)
-        key = rng.stream_key(self.seed, rng.WALK_UNIFORM, rnd, k, i)
+        if self.dkeys is not None:   # graph-replayed round: the key is read on the device
+            key = self.dkeys[k, i]
+        else:
+            key = rng.stream_key(self.seed, rng.WALK_UNIFORM, rnd, k, i)
         H_in = None if first else self.H
         if self.P > 1:
             node_grams, leaf_rank, depth = self.rank_tree[i]
@@ -684,6 +688,63 @@ class Cluster:
                 on_solved(k)
             if check:
                 self.check("after round %d mode %d solve" % (rnd, k))
+
+    # ------------------------------------------------------------ CUDA-graph rounds
+    def graph_ok(self):
+        """A round is replayable from a CUDA graph when nothing in it depends on the host
+        between launches: one rank, STS (its only per-round host input is the walk keys,
+        which move to device memory), and workspaces sized up front (no bounded-capacity
+        MTTKRP, which checks its entry count on the host)."""
+        return (self.P == 1 and self.sampler == "sts" and
+                all(st.capacity(self.J) <= CAP_LIMIT for st in self.ranks[0].stores))
+
+    def round_graph(self, rnd, on_solved=None, join=(), tag="round"):
+        """One ALS round replayed from a CUDA graph (captured on the first call, after at
+        least one eager round has sized every workspace).  The round's WALK_UNIFORM keys
+        are written to device memory before each replay; the replay issues the same
+        kernels with the same arguments as an eager round (tests/test_gpu_graph.py).
+        on_solved/join: as in round(), with the side streams its work forks into (joined
+        before the capture ends); one graph is kept per `tag`."""
+        t = torch()
+        if not self.graph_ok():
+            raise RuntimeError("this cluster's rounds cannot be replayed from a graph")
+        r = self.ranks[0]
+        N = self.N
+        if r.dkeys is None:
+            r.dkeys = t.zeros((N, N, 2), dtype=t.int64, device=r.dev)
+            self._gkeys = [t.zeros((N, N, 2), dtype=t.int64, pin_memory=True) for _ in range(2)]
+            self._gkey_ev = [None, None]
+            self._gslot = 0
+        slot = self._gslot
+        self._gslot ^= 1
+        if self._gkey_ev[slot] is not None:
+            self._gkey_ev[slot].synchronize()   # its previous upload has been consumed
+        host = np.zeros((N, N, 2), dtype=np.uint64)
+        for k in range(N):
+            for i in range(N):
+                if i != k:
+                    host[k, i] = rng.stream_key(self.seed, rng.WALK_UNIFORM, rnd, k, i)
+        self._gkeys[slot].numpy()[...] = host.view(np.int64)
+        r.dkeys.copy_(self._gkeys[slot], non_blocking=True)
+        ev = t.cuda.Event()
+        ev.record()
+        self._gkey_ev[slot] = ev
+        if not hasattr(self, "_graphs"):
+            self._graphs = {}
+        g = self._graphs.get(tag)
+        if g is None:
+            from . import _lib
+            lib = _lib.lib()
+            g = t.cuda.CUDAGraph()
+            n0 = lib.rcp_launch_count()
+            with t.cuda.graph(g):
+                self.round(rnd, check=False, on_solved=on_solved)
+                cap = t.cuda.current_stream()
+                for st in join:
+                    cap.wait_stream(st)
+            self.graph_kernels = lib.rcp_launch_count() - n0
+            self._graphs[tag] = g
+        g.replay()
 
 
 def _lib_capacity():

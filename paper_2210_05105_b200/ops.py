@@ -11,6 +11,14 @@ from .device import Status, ptr, stream_handle, torch
 CUTOFF = 1e-10   # ref linalg.py:16
 
 
+def _key_args(key):
+    """(key0, key1, d_key): a host key pair, or a device tensor of two words (int64 view of
+    the uint64 key) read by the kernel itself (graph-replayed rounds)."""
+    if hasattr(key, "data_ptr"):
+        return 0, 0, key.data_ptr()
+    return int(key[0]), int(key[1]), None
+
+
 class Ops:
     def __init__(self, dev):
         self.dev = dev
@@ -82,8 +90,9 @@ class Ops:
                   prob_out, U=None, urow_out=None):
         n = cdf.shape[0]
         R = U.shape[1] if U is not None else 0
+        k0, k1, dk = _key_args(key)
         self._c("rcp_arls_draw", ptr(cdf), ptr(dist), n, int(row_lo), float(ratio),
-                ptr(total_mass), key[0], key[1], int(q), int(offset), ptr(rows_out),
+                ptr(total_mass), k0, k1, dk, int(q), int(offset), ptr(rows_out),
                 ptr(prob_out), ptr(U), R, ptr(urow_out), self.status.ptr, stream_handle())
 
     def batch_fold(self, perm, rows, prob, U, u_row_lo, urows, first, Xi, pmp_i, H):
@@ -113,15 +122,18 @@ class Ops:
                  Xi, pmp_i, resid, hkey=None, key_bits=64, H_out=None):
         n, R = U.shape
         w = self.ws("sts_walk", self.lib.rcp_sts_walk_ws_bytes(int(J), n, int(leaf), R))
+        k0, k1, dk = _key_args(key)
         self._c("rcp_sts_walk", ptr(tree), ptr(U), n, R, int(leaf), int(row_lo), ptr(M),
-                ptr(H_in), ptr(hkey), int(key_bits), int(J), key[0], key[1], ptr(override), ptr(rin), ptr(sel),
+                ptr(H_in), ptr(hkey), int(key_bits), int(J), k0, k1, dk, ptr(override), ptr(rin),
+                ptr(sel),
                 int(sel_value), ptr(Xi), ptr(pmp_i), ptr(resid), ptr(H_out), ptr(w), w.numel(),
                 self.status.ptr, stream_handle())
 
     def sts_flat_draw(self, cdf, dist, row_lo, mass, key, J, Xi, pmp_i):
         n = cdf.shape[0]
-        self._c("rcp_sts_flat_draw", ptr(cdf), ptr(dist), n, int(row_lo), ptr(mass), key[0],
-                key[1], int(J), ptr(Xi), ptr(pmp_i), self.status.ptr, stream_handle())
+        k0, k1, dk = _key_args(key)
+        self._c("rcp_sts_flat_draw", ptr(cdf), ptr(dist), n, int(row_lo), ptr(mass), k0, k1, dk,
+                int(J), ptr(Xi), ptr(pmp_i), self.status.ptr, stream_handle())
 
     def fold_rows(self, out, U, row_lo, Xi, init, sel=None, sel_value=0):
         n, R = U.shape

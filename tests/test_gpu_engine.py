@@ -171,9 +171,11 @@ def test_all_ones_full_cover_reproduces_exact(P):
     assert np.abs(got - ref).max() < 1e-12
 
 
-def test_host_step_api_matches_device_round(P):
+@pytest.mark.parametrize("graph", [False, True])
+def test_host_step_api_matches_device_round(P, graph):
     """AlsSession.step_host (pinned host factors in, overlapped transfers, factors and sigma
-    out) computes the same round as the device-resident engine."""
+    out; eager or replayed from a CUDA graph) computes the same rounds as the
+    device-resident engine."""
     import torch
     from paper_2210_05105_b200.als import AlsSession
     from paper_2210_05105_b200.engine import make_local_cluster
@@ -187,15 +189,20 @@ def test_host_step_api_matches_device_round(P):
     b.round(1)
     sess = AlsSession(a)
     host_in, host_out = sess.pinned_factors(), sess.pinned_factors()
-    sess.step_host(host_in, host_out, 2)
-    for j in range(3):          # step_host re-uploads the same factors, then rebuilds
-        b.rebuild(j)
-    b.round(2)
-    for j in range(3):
-        got = host_out[j].numpy()
-        ref = b.ranks[0].U[j].cpu().numpy()
-        assert rel_err(got, ref) < 1e-12
-    assert rel_err(sess.sigma.numpy(), b.ranks[0].sigma.cpu().numpy()) < 1e-12
+    for rnd in (2, 3, 4):
+        sess.step_host(host_in, host_out, rnd, graph=graph)
+        for j in range(3):      # step_host re-uploads the host factors, then rebuilds
+            b.ranks[0].U[j].copy_(host_in[j].to(dev))
+            b.rebuild(j)
+        b.round(rnd)
+        assert torch.equal(a.ranks[0].X, b.ranks[0].X), rnd
+        for j in range(3):
+            got = host_out[j].numpy()
+            ref = b.ranks[0].U[j].cpu().numpy()
+            assert rel_err(got, ref) < 1e-12
+        assert rel_err(sess.sigma.numpy(), b.ranks[0].sigma.cpu().numpy()) < 1e-12
+        for j in range(3):      # the next step starts from this step's output
+            host_in[j].copy_(host_out[j])
 
 
 @pytest.mark.parametrize("sampler,R", [("sts", 70), ("arls-lev", 70), ("sts", 128)])
