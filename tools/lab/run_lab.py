@@ -1,5 +1,5 @@
-"""Build and run the SpMM lab on the workspace of real C3 sampled-MTTKRP calls (GPU box).
-    python tools/lab/run_lab.py [variants...]"""
+"""Build and run the lab probes on the GPU box.
+    LABMODE=walk|gsync|gather|probe python tools/lab/run_lab.py"""
 import ctypes
 import glob
 import json
@@ -28,7 +28,6 @@ def build():
 
 
 def main():
-    variants = [int(v) for v in sys.argv[1:]] or [0, 1, 2, 3, 4, 5, 6, 7, 10, 11, 12]
     lab = ctypes.CDLL(build())
     import bench
     from paper_2210_05105_b200 import _lib
@@ -37,41 +36,22 @@ def main():
     _lib.load()
     cfg = os.environ.get("CFG", "c3")
     sampler = os.environ.get("SAMPLER", "sts")
-    if os.environ.get("LABMODE") == "gather":
+    if os.environ.get("LABMODE") in ("gather", "gsync"):
         cfg = "c1"
     c, idx, vals = bench.make_tensor(cfg, 0, dev)
     cl = make_local_cluster(c["dims"], idx, vals, c["R"], c["J"], sampler, 0)
     me = cl.ranks[0]
     for rnd in range(1, 4):
         cl.round(rnd)
-    orig = me.mttkrp
     res = []
 
-    def hook(k):
-        s = torch.cuda.Event(enable_timing=True)
-        e = torch.cuda.Event(enable_timing=True)
-        s.record()
-        out = orig(k)
-        e.record()
-        torch.cuda.synchronize()
-        ref = out.clone()
-        ws = me.ops._ws["mttkrp"]
-        n = me.n[k]
-        row = {"mode": k, "n_rows": n, "product_call_ms": s.elapsed_time(e)}
-        tmp = torch.empty_like(ref)
-        for v in variants:
-            for gm in (8,) if v < 10 else (2, 4):
-                ms = ctypes.c_float(0)
-                rc = lab.lab_spmm(v, ctypes.c_void_p(ws.data_ptr()), ctypes.c_size_t(ws.numel()),
-                                  ctypes.c_int64(me.J), ctypes.c_int64(n), me.R,
-                                  ctypes.c_void_p(tmp.data_ptr()), 5, ctypes.byref(ms), gm)
-                torch.cuda.synchronize()
-                err = float((tmp - ref).abs().max() / ref.abs().max())
-                row["v%d_g%d" % (v, gm)] = {"rc": rc, "ms": round(ms.value, 4), "relerr": err}
-        res.append(row)
-        print(json.dumps(row), flush=True)
-        return out
-
+    if os.environ.get("LABMODE") == "gsync":
+        sink = torch.zeros(4, dtype=torch.int32, device=dev)
+        for iters in (1, 101):
+            ms = ctypes.c_float(0)
+            rc = lab.lab_gsync_probe(iters, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(ms))
+            print(json.dumps({"probe": "grid.sync", "iters": iters, "ms": ms.value, "rc": rc}))
+        return
     if os.environ.get("LABMODE") == "gather":
         for rows in (13690, 65536, 1 << 17):
             tab = torch.randn(rows * 64, dtype=torch.float64, device=dev)
@@ -127,7 +107,7 @@ def main():
             print(json.dumps(row), flush=True)
         ops.sts_walk = walk_hook
     else:
-        me.mttkrp = hook
+        raise SystemExit("LABMODE must be one of walk, gsync, gather, probe")
     cl.round(4)
     torch.cuda.synchronize()
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
