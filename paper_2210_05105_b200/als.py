@@ -15,11 +15,11 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .coo import ModePermutations
+from .coo import ModePermutations, permute_modes
 from .device import require_cuda, to_dev, to_host, torch
 from .engine import PHASES, make_local_cluster
 from .grid import ProcessorGrid, optimal_grid
-from .linalg import compute_fit, init_factors
+from .linalg import init_factors
 from .schedules import ScheduleError
 
 SAMPLERS = ("exact", "arls-lev", "sts")
@@ -112,9 +112,13 @@ def run_als(cfg: AlsConfig, tensor=None, perms=None, grid=None, partition=None,
     """One ALS trial (ref als.py:141-218) on the device engine."""
     cfg.validate()
     _check_supported(cfg)
-    if tensor is None:
-        raise ValueError("no tensor given (FROSTT ingest is outside this build; pass a "
-                         "SparseTensorCOO)")
+    if tensor is None:   # (ref als.py:148-154)
+        if cfg.tensor_path is None:
+            raise ValueError("no tensor given and no tensor_path configured")
+        from .tensorio import load_frostt
+        tensor = load_frostt(cfg.tensor_path, log_transform=cfg.log_transform, dedup=cfg.dedup)
+        if cfg.permute:
+            tensor, perms = permute_modes(tensor, cfg.seed)
     timings = {"load": 0.0, "fit": 0.0}
     t0 = time.perf_counter()
     dev = require_cuda()
@@ -239,10 +243,17 @@ class AlsSession:
 
 
 def run_trials(cfg: AlsConfig, trials: int, tensor=None):
-    """Mean-of-trials harness with shared tensor (ref als.py:221-237)."""
+    """Mean-of-trials harness with shared tensor (ref als.py:221-237): the tensor is
+    loaded (and permuted) once."""
     cfg.validate()
+    perms = None
+    if tensor is None and cfg.tensor_path is not None:
+        from .tensorio import load_frostt
+        tensor = load_frostt(cfg.tensor_path, log_transform=cfg.log_transform, dedup=cfg.dedup)
+        if cfg.permute:
+            tensor, perms = permute_modes(tensor, cfg.seed)
     results = []
     for tr in range(trials):
         trial_cfg = AlsConfig(**{**cfg.__dict__, "trial": tr})
-        results.append(run_als(trial_cfg, tensor=tensor))
+        results.append(run_als(trial_cfg, tensor=tensor, perms=perms))
     return results

@@ -1,9 +1,8 @@
 """Minimal coordinate-format tensor container used by the drop-in API.
 
-Ingest (FROSTT parsing, dedup, permutation files) is outside this build's hot-path scope
-(SURVEY.md section 2, row 9); this class only carries (dims, idx, vals) with the
-reference's validation rules (ref tensor.py:22-69) so the AS partition and ALS driver can
-take the same inputs as the reference.
+The container carries (dims, idx, vals) with the reference's validation rules (ref
+tensor.py:22-69) so the AS partition and ALS driver take the same inputs as the
+reference; FROSTT parsing and result files live in tensorio.py.
 """
 
 from __future__ import annotations
@@ -71,10 +70,15 @@ class ModePermutations:
         return U[self.perms[mode]]
 
 
-def permute_modes(t: SparseTensorCOO, seed):
-    """Load-balancing random relabelling of every mode (ref tensor.py:182-210)."""
-    mp = ModePermutations.random(t.dims, seed)
+def apply_permutations(t: SparseTensorCOO, mp: ModePermutations):
+    """idx'[:, j] = perm_j[idx[:, j]] for every mode (ref tensor.py:199-205)."""
     idx = np.empty_like(t.idx)
     for j, p in enumerate(mp.perms):
         idx[:, j] = p[t.idx[:, j]]
-    return SparseTensorCOO(t.dims, idx, t.vals.copy(), validate=False), mp
+    return SparseTensorCOO(t.dims, idx, t.vals.copy(), validate=False)
+
+
+def permute_modes(t: SparseTensorCOO, seed):
+    """Load-balancing random relabelling of every mode (ref tensor.py:182-210)."""
+    mp = ModePermutations.random(t.dims, seed)
+    return apply_permutations(t, mp), mp

@@ -218,3 +218,32 @@ def test_rank_above_64(P, sampler, R):
     if h == len(st.sample_log):
         for j in range(3):
             assert rel_err(res.factors[j], st.full(j)) < 1e-9
+
+
+def test_tensor_path_trials_and_result_files(P, tmp_path):
+    """run_trials from a FROSTT file (loaded and permuted once, ref als.py:141-237) and the
+    `decompose --out` files (ref cli.py:93-104): factors in the file's index order."""
+    from paper_2210_05105_b200.tensorio import read_matrix, write_results
+    dims = (30, 20, 25)
+    idx, vals = synth.small_random(dims, 1500, seed=2)
+    path = tmp_path / "t.tns"
+    with open(path, "w") as fh:
+        for (a, b, c), v in zip(idx + 1, vals):
+            fh.write("%d %d %d %.17g\n" % (a, b, c, v))
+    cfg = P.AlsConfig(rank=4, rounds=2, tensor_path=str(path), sampler="sts", samples=200,
+                      schedule="accumulator-stationary", seed=5, fit_every=1)
+    res = P.run_trials(cfg, 2)
+    t = P.load_frostt(str(path))
+    tp, mp = P.permute_modes(t, 5)
+    ref = P.run_als(cfg, tensor=tp, perms=mp)
+    for j in range(3):
+        assert rel_err(res[0].factors[j], ref.factors[j]) < 1e-12
+        assert res[0].factors[j].shape == (t.dims[j], 4)
+    assert np.isfinite(res[1].final_fit)
+    write_results(res, str(tmp_path / "out"))
+    for tr in range(2):
+        d = tmp_path / "out" / ("trial%d" % tr)
+        for j in range(3):
+            assert np.array_equal(read_matrix(str(d / ("factor_mode%d.bin" % j))), res[tr].factors[j])
+        assert read_matrix(str(d / "sigma.bin")).shape == (4, 1)
+        assert "final_fit" in (d / "summary.txt").read_text()
