@@ -77,6 +77,10 @@ int rcp_uniform_host(const uint64_t *h_key, int64_t first, int64_t n, double *h_
  * random_interval on buffered uint32 draws).  Used for the CP-ARLS-LEV SHUFFLE stream
  * (ref samplers.py:183). */
 int rcp_permutation_host(const uint64_t *h_key, int64_t n, int64_t *h_out);
+/* `count` permutations of the streams h_keys[2c], h_keys[2c+1] into h_outs[c] (n each),
+ * spread over `threads` host threads (the CP-ARLS-LEV SHUFFLE streams of a round). */
+int rcp_permutations_host(const uint64_t *h_keys, int count, int64_t n, int64_t *const *h_outs,
+                          int threads);
 /* Device: d_out[i] = draw (first+i) of Generator.random(). */
 int rcp_uniform(uint64_t key0, uint64_t key1, int64_t first, int64_t n, double *d_out,
                 void *stream);

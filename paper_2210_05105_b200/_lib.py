@@ -37,6 +37,7 @@ _SIGS = {
     "rcp_stream_key": (_i32, [_u64, _u64, _vp, _i32, _vp]),
     "rcp_uniform_host": (_i32, [_vp, _i64, _i64, _vp]),
     "rcp_permutation_host": (_i32, [_vp, _i64, _vp]),
+    "rcp_permutations_host": (_i32, [_vp, _i32, _i64, _vp, _i32]),
     "rcp_uniform": (_i32, [_u64, _u64, _i64, _i64, _vp, _vp]),
     "rcp_gram_ws_bytes": (_sz, [_i64, _i32]),
     "rcp_gram": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp]),

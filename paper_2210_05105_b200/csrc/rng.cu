@@ -3,6 +3,7 @@
 #include <stdio.h>
 
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -171,6 +172,28 @@ int rcp_permutation_host(const uint64_t *h_key, int64_t n, int64_t *h_out) {
     h_out[i] = h_out[j];
     h_out[j] = t;
   }
+  return RCP_OK;
+}
+
+// Several permutations at once on native threads: one foreign call (the caller's
+// interpreter lock is released once) instead of one call per stream.
+int rcp_permutations_host(const uint64_t *h_keys, int count, int64_t n, int64_t *const *h_outs,
+                          int threads) {
+  if (count < 0 || n < 0 || (count > 0 && (!h_keys || !h_outs))) return RCP_ERR_ARG;
+  for (int c = 0; c < count; ++c)
+    if (n > 0 && !h_outs[c]) return RCP_ERR_ARG;
+  if (threads < 1) threads = 1;
+  if (threads > count) threads = count;
+  if (threads <= 1) {
+    for (int c = 0; c < count; ++c) rcp_permutation_host(h_keys + 2 * c, n, h_outs[c]);
+    return RCP_OK;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([=]() {
+      for (int c = t; c < count; c += threads) rcp_permutation_host(h_keys + 2 * c, n, h_outs[c]);
+    });
+  for (auto &th : pool) th.join();
   return RCP_OK;
 }
 

@@ -58,68 +58,64 @@ def default_leaf(n, R, budget_bytes=4 << 30):
 
 class ShufflePrefetch:
     """Generator.permutation(J) of the CP-ARLS-LEV SHUFFLE streams (ref samplers.py:183-185)
-    computed ahead on host threads into pinned buffers.  The permutation is a sequential
-    rejection-sampling chain (host native code, ~1 ms for J = 65536; the ctypes call
-    releases the GIL); it depends only on (seed, round, k, i), so the next round's
-    permutations are produced while the GPU runs the current one and uploaded
-    asynchronously.  Pinned buffers are recycled once their copy has completed."""
+    computed ahead on the host.  The permutation is a sequential rejection-sampling chain
+    (host native code, ~1 ms for J = 65536); it depends only on (seed, round, k, i), so a
+    background thread makes each upcoming round's N(N-1) permutations with one native
+    call (`rcp_permutations_host`, several threads, one release of the interpreter lock)
+    into a pinned (N, N, J) buffer while the GPU runs the current round; the eager path
+    uploads them asynchronously and recycles the buffer once its copies completed."""
 
-    def __init__(self, seed, J, N, workers=4):
+    def __init__(self, seed, J, N, ahead=2):
         import threading
         from concurrent.futures import ThreadPoolExecutor
         self.seed, self.J, self.N = int(seed), int(J), int(N)
-        self.pool = ThreadPoolExecutor(max_workers=workers)
-        self.futs = {}
-        self.free = []          # recycled pinned buffers
+        self.ahead = int(ahead)   # rounds requested beyond the one being consumed
+        self.pool = ThreadPoolExecutor(max_workers=1)
+        self.futs = {}            # round -> future of its pinned (N, N, J) buffer
+        self.left = {}            # round -> pairs not yet copied out
+        self.free = []            # recycled pinned buffers
         self.lock = threading.Lock()
-        self.inflight = []      # (event, buffer) until the upload is done
+        self.inflight = []        # (event, buffer) until the uploads are done
 
     def _buffer(self):
         with self.lock:
             if self.free:
                 return self.free.pop()
         t = torch()
-        return t.empty(self.J, dtype=t.int64, pin_memory=True)
+        return t.empty((self.N, self.N, self.J), dtype=t.int64, pin_memory=True)
 
-    def _make(self, rnd, k, i, buf):
-        key = np.array(rng.stream_key(self.seed, rng.SHUFFLE, rnd, k, i), dtype=np.uint64)
-        from . import _lib
-        _lib.call("rcp_permutation_host", key.ctypes.data, self.J, buf.data_ptr())
+    def fill(self, rnd, buf):
+        """Write round rnd's permutations into buf[k, i] (k != i)."""
+        pairs = [(k, i) for k in range(self.N) for i in range(self.N) if i != k]
+        keys = [rng.stream_key(self.seed, rng.SHUFFLE, rnd, k, i) for k, i in pairs]
+        rng.permutations_into(keys, self.J, [buf[k, i] for k, i in pairs],
+                              threads=len(pairs))
         return buf
 
-    def _prime(self):
-        """Pinned buffers for three rounds up front (a pinned allocation inside a timed
-        round can stall it for milliseconds)."""
-        if getattr(self, "_primed", False):
-            return
-        t = torch()
-        n = 3 * self.N * (self.N - 1)
-        with self.lock:
-            self.free.extend(t.empty(self.J, dtype=t.int64, pin_memory=True) for _ in range(n))
-        self._primed = True
-
     def _request(self, rnd):
-        self._prime()
-        for k in range(self.N):
-            for i in range(self.N):
-                if i != k and (rnd, k, i) not in self.futs:
-                    self.futs[(rnd, k, i)] = self.pool.submit(self._make, rnd, k, i, self._buffer())
+        for r in range(rnd, rnd + self.ahead + 1):
+            if r not in self.futs:
+                self.futs[r] = self.pool.submit(self.fill, r, self._buffer())
+                self.left[r] = self.N * (self.N - 1)
 
     def copy_to(self, dst, rnd, k, i):
         t = torch()
         self._request(rnd)
-        self._request(rnd + 1)
-        buf = self.futs.pop((rnd, k, i)).result()
-        dst.copy_(buf, non_blocking=True)
-        ev = t.cuda.Event()
-        ev.record()
-        self.inflight.append((ev, buf))
+        buf = self.futs[rnd].result()
+        dst.copy_(buf[k, i], non_blocking=True)
+        self.left[rnd] -= 1
+        if self.left[rnd] == 0:   # every pair uploaded: recycle after the copies finish
+            ev = t.cuda.Event()
+            ev.record()
+            self.inflight.append((ev, buf))
+            self.futs.pop(rnd)
+            self.left.pop(rnd)
         while self.inflight and self.inflight[0][0].query():
             with self.lock:
                 self.free.append(self.inflight.pop(0)[1])
-        for key in [q for q in self.futs if q[0] < rnd]:   # rounds that will not come back
-            self.futs.pop(key)
-
+        for r in [q for q in self.futs if q < rnd]:   # rounds that will not come back
+            self.futs.pop(r)
+            self.left.pop(r, None)
 
 class LocalComm:
     """P virtual ranks in one process (list collectives, rank order)."""
@@ -199,7 +195,8 @@ class RankState:
         self.Mout = t.zeros((max(self.n) if N else 0, R), **f64)
         self.stats = t.zeros(8, dtype=t.int64, device=dev)
         self.mt_cap = {}
-        self.dkeys = None        # (N, N, 2) WALK_UNIFORM keys of the round (graph mode)
+        self.dkeys = None        # (N, N, 2) stream keys of the round's draws (graph mode)
+        self.gperm = None        # (N, N, J) SHUFFLE permutations of the round (graph mode)
         self.block_gram_buf = t.zeros((R, R), **f64)
 
     # -------------------------------------------------------------- set-up
@@ -357,7 +354,10 @@ class RankState:
         q = int(quota[self.rank]) if self.P > 1 else self.J
         if q == 0:
             return 0
-        key = rng.stream_key(self.seed, rng.LOCAL_DRAW, rnd, k, i, self.rank)
+        if self.dkeys is not None:   # graph-replayed round: the key is read on the device
+            key = self.dkeys[k, i]
+        else:
+            key = rng.stream_key(self.seed, rng.LOCAL_DRAW, rnd, k, i, self.rank)
         if self.P > 1:
             ratio = float(self.C_host[i][self.rank]) / W
             tmass = None
@@ -371,10 +371,14 @@ class RankState:
         return q
 
     def arls_fold(self, i, k, rnd, first, rows, probs, urows):
-        if self.shuffles is None:
-            self.shuffles = ShufflePrefetch(self.seed, self.J, self.N)
-        self.shuffles.copy_to(self.perm, rnd, k, i)
-        self.ops.batch_fold(self.perm, rows, probs, self.U[i] if urows is None else None,
+        if self.gperm is not None:   # graph-replayed round: permutations uploaded beforehand
+            perm = self.gperm[k, i]
+        else:
+            if self.shuffles is None:
+                self.shuffles = ShufflePrefetch(self.seed, self.J, self.N)
+            self.shuffles.copy_to(self.perm, rnd, k, i)
+            perm = self.perm
+        self.ops.batch_fold(perm, rows, probs, self.U[i] if urows is None else None,
                             self.lo[i], urows, first, self.X[i], self.pmp[i], self.H)
 
     # --------------------------------------------------------------- solve
@@ -692,17 +696,20 @@ class Cluster:
     # ------------------------------------------------------------ CUDA-graph rounds
     def graph_ok(self):
         """A round is replayable from a CUDA graph when nothing in it depends on the host
-        between launches: one rank, STS (its only per-round host input is the walk keys,
-        which move to device memory), and workspaces sized up front (no bounded-capacity
-        MTTKRP, which checks its entry count on the host)."""
-        return (self.P == 1 and self.sampler == "sts" and
+        between launches: one rank (its per-round host inputs -- the draw keys and, for
+        CP-ARLS-LEV, the SHUFFLE permutations -- move to device memory before the replay)
+        and workspaces sized up front (no bounded-capacity MTTKRP, which checks its entry
+        count on the host)."""
+        return (self.P == 1 and
                 all(st.capacity(self.J) <= CAP_LIMIT for st in self.ranks[0].stores))
 
     def round_graph(self, rnd, on_solved=None, join=(), tag="round"):
         """One ALS round replayed from a CUDA graph (captured on the first call, after at
-        least one eager round has sized every workspace).  The round's WALK_UNIFORM keys
-        are written to device memory before each replay; the replay issues the same
-        kernels with the same arguments as an eager round (tests/test_gpu_graph.py).
+        least one eager round has sized every workspace).  The round's draw keys (and
+        CP-ARLS-LEV's SHUFFLE permutations) are uploaded to device memory before each
+        replay, from pinned staging filled while the previous replay runs; the replay
+        issues the same kernels with the same arguments as an eager round
+        (tests/test_gpu_graph.py).
         on_solved/join: as in round(), with the side streams its work forks into (joined
         before the capture ends); one graph is kept per `tag`."""
         t = torch()
@@ -710,22 +717,25 @@ class Cluster:
             raise RuntimeError("this cluster's rounds cannot be replayed from a graph")
         r = self.ranks[0]
         N = self.N
+        arls = self.sampler != "sts"
         if r.dkeys is None:
             r.dkeys = t.zeros((N, N, 2), dtype=t.int64, device=r.dev)
             self._gkeys = [t.zeros((N, N, 2), dtype=t.int64, pin_memory=True) for _ in range(2)]
+            if arls:
+                r.gperm = t.zeros((N, N, self.J), dtype=t.int64, device=r.dev)
+                self._gperm = [t.zeros((N, N, self.J), dtype=t.int64, pin_memory=True)
+                               for _ in range(2)]
+                if r.shuffles is None:
+                    r.shuffles = ShufflePrefetch(self.seed, self.J, N)
             self._gkey_ev = [None, None]
-            self._gslot = 0
-        slot = self._gslot
-        self._gslot ^= 1
-        if self._gkey_ev[slot] is not None:
-            self._gkey_ev[slot].synchronize()   # its previous upload has been consumed
-        host = np.zeros((N, N, 2), dtype=np.uint64)
-        for k in range(N):
-            for i in range(N):
-                if i != k:
-                    host[k, i] = rng.stream_key(self.seed, rng.WALK_UNIFORM, rnd, k, i)
-        self._gkeys[slot].numpy()[...] = host.view(np.int64)
+            self._gready = {}   # round -> staging slot holding its inputs
+        slot = self._gready.pop(rnd, None)
+        self._gready.clear()   # inputs staged for any other round are stale
+        if slot is None:
+            slot = self._graph_stage(rnd, 0)
         r.dkeys.copy_(self._gkeys[slot], non_blocking=True)
+        if arls:
+            r.gperm.copy_(self._gperm[slot], non_blocking=True)
         ev = t.cuda.Event()
         ev.record()
         self._gkey_ev[slot] = ev
@@ -745,6 +755,28 @@ class Cluster:
             self.graph_kernels = lib.rcp_launch_count() - n0
             self._graphs[tag] = g
         g.replay()
+        # the next round's inputs are staged in the other slot while the GPU runs this one
+        self._gready[rnd + 1] = self._graph_stage(rnd + 1, 1 - slot)
+
+    def _graph_stage(self, rnd, slot):
+        """Write round rnd's draw keys (and permutations) into pinned staging slot `slot`."""
+        r = self.ranks[0]
+        N = self.N
+        if self._gkey_ev[slot] is not None:
+            self._gkey_ev[slot].synchronize()   # the slot's previous upload is done
+        host = np.zeros((N, N, 2), dtype=np.uint64)
+        for k in range(N):
+            for i in range(N):
+                if i == k:
+                    continue
+                if self.sampler == "sts":
+                    host[k, i] = rng.stream_key(self.seed, rng.WALK_UNIFORM, rnd, k, i)
+                else:
+                    host[k, i] = rng.stream_key(self.seed, rng.LOCAL_DRAW, rnd, k, i, r.rank)
+        if self.sampler != "sts":   # native threads, straight into the pinned slot
+            r.shuffles.fill(rnd, self._gperm[slot])
+        self._gkeys[slot].numpy()[...] = host.view(np.int64)
+        return slot
 
 
 def _lib_capacity():

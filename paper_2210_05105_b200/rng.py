@@ -57,3 +57,12 @@ def stream(seed, purpose, *context) -> np.random.Generator:
     key = np.random.SeedSequence(entropy=int(seed) & ((1 << 64) - 1),
                                  spawn_key=(int(purpose),) + tuple(int(c) for c in context))
     return np.random.Generator(np.random.Philox(key))
+
+
+def permutations_into(keys, n, outs, threads=8):
+    """Generator.permutation(n) of several streams at once (native threads), written into
+    the int64 buffers `outs` (numpy arrays or CPU tensors, n elements each)."""
+    k = np.ascontiguousarray(np.asarray(keys, dtype=np.uint64).reshape(-1, 2))
+    ptrs = (C.c_void_p * len(outs))(*[C.c_void_p(o.data_ptr() if hasattr(o, "data_ptr")
+                                                 else o.ctypes.data) for o in outs])
+    _lib.call("rcp_permutations_host", k.ctypes.data, len(outs), int(n), ptrs, int(threads))
