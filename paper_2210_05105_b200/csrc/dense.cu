@@ -4,6 +4,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "gram_mma.cuh"
 
 using namespace rcp;
 
@@ -674,6 +675,69 @@ __global__ void hadamard_rows_kernel(double *__restrict__ H, const double *__res
     H[e] = init ? urow[e] : H[e] * urow[e];
 }
 
+// R <= 64: the same Gram on the fp64 tensor cores.  For a 4-row step of Z = diag(s) U,
+// thread t of a warp holds Z[r0 + t%4][8 tile + t/4] for every 8-column tile -- at once
+// the A fragment (Z^T, row-major 8x4) and the B fragment (Z, col-major 4x8) of
+// mma.m8n8k4 -- and accumulates every upper tile pair (a <= b) of G from registers.
+// Steps go to (CTA, warp) in a fixed order; warps are combined in a fixed order (the CTA
+// partials then by sum_partials): deterministic.
+template <int T>
+__global__ void __launch_bounds__(256)
+gram_mma_kernel(const double *__restrict__ U, const double *__restrict__ scale, int64_t n, int R,
+                double *__restrict__ part) {
+  constexpr int NP = T * (T + 1) / 2;
+  __shared__ double red[NP * 64];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double acc[NP][2];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) acc[p][0] = acc[p][1] = 0.0;
+  const int64_t steps = (n + 3) >> 2;
+  const int64_t stride = (int64_t)gridDim.x * nw;
+  const int kk = lane & 3, col = lane >> 2;
+  // three 4-row steps in flight per warp (loads of the next ones overlap the MMAs)
+  double f0[T], f1[T], f2[T];
+  int64_t s = (int64_t)blockIdx.x * nw + wid;
+  gram_load<T>(U, scale, 4 * s + kk, n, R, col, f0);
+  gram_load<T>(U, scale, 4 * (s + stride) + kk, n, R, col, f1);
+  gram_load<T>(U, scale, 4 * (s + 2 * stride) + kk, n, R, col, f2);
+  for (; s < steps; s += 3 * stride) {
+    gram_accum<T>(f0, acc);
+    gram_load<T>(U, scale, 4 * (s + 3 * stride) + kk, n, R, col, f0);
+    if (s + stride >= steps) break;
+    gram_accum<T>(f1, acc);
+    gram_load<T>(U, scale, 4 * (s + 4 * stride) + kk, n, R, col, f1);
+    if (s + 2 * stride >= steps) break;
+    gram_accum<T>(f2, acc);
+    gram_load<T>(U, scale, 4 * (s + 5 * stride) + kk, n, R, col, f2);
+  }
+  for (int w = 0; w < nw; ++w) {   // fixed-order combination of the warps
+    if (wid == w) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        double *q = red + p * 64 + 2 * lane;
+        q[0] = w ? q[0] + acc[p][0] : acc[p][0];
+        q[1] = w ? q[1] + acc[p][1] : acc[p][1];
+      }
+    }
+    __syncthreads();
+  }
+  double *out = part + (int64_t)blockIdx.x * R * R;
+  for (int e = threadIdx.x; e < NP * 64; e += blockDim.x) {
+    int p = e >> 6, a = 0;
+    while (p >= T - a) {
+      p -= T - a;
+      ++a;
+    }
+    const int b = a + p;
+    const int ln = (e & 63) >> 1, u = e & 1;
+    const int ga = 8 * a + (ln >> 2), gb = 8 * b + 2 * (ln & 3) + u;
+    if (ga < R && gb < R) {
+      out[ga * R + gb] = red[e];
+      out[gb * R + ga] = red[e];
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -706,7 +770,18 @@ int rcp_gram(const double *d_U, const double *d_scale, int64_t n, int R, double 
   const int al = ((uintptr_t)d_U & 15) == 0 ? 1 : 0;
   const int nT = (R + 3) / 4, npairs = nT * (nT + 1) / 2;
   double *part = (double *)d_ws;
-  if (npairs <= kGramThreads)
+  if (R <= 64) {   // fp64 tensor cores
+    switch ((R + 7) / 8) {
+      case 1: gram_mma_kernel<1><<<grid, 256, 0, st>>>(d_U, d_scale, n, R, part); break;
+      case 2: gram_mma_kernel<2><<<grid, 256, 0, st>>>(d_U, d_scale, n, R, part); break;
+      case 3: gram_mma_kernel<3><<<grid, 256, 0, st>>>(d_U, d_scale, n, R, part); break;
+      case 4: gram_mma_kernel<4><<<grid, 256, 0, st>>>(d_U, d_scale, n, R, part); break;
+      case 5: gram_mma_kernel<5><<<grid, 256, 0, st>>>(d_U, d_scale, n, R, part); break;
+      case 6: gram_mma_kernel<6><<<grid, 256, 0, st>>>(d_U, d_scale, n, R, part); break;
+      case 7: gram_mma_kernel<7><<<grid, 256, 0, st>>>(d_U, d_scale, n, R, part); break;
+      default: gram_mma_kernel<8><<<grid, 256, 0, st>>>(d_U, d_scale, n, R, part); break;
+    }
+  } else if (npairs <= kGramThreads)
     gram_partial_kernel<1><<<grid, kGramThreads, smem, st>>>(d_U, d_scale, n, R, al, part);
   else if (npairs <= 2 * kGramThreads)
     gram_partial_kernel<2><<<grid, kGramThreads, smem, st>>>(d_U, d_scale, n, R, al, part);

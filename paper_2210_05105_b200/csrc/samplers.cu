@@ -10,6 +10,7 @@
 #include <float.h>
 
 #include "common.cuh"
+#include "gram_mma.cuh"
 #include "scan.cuh"
 
 using namespace rcp;
@@ -186,9 +187,14 @@ __global__ void batch_fold_kernel(const int64_t *__restrict__ perm, const int64_
 // --------------------------------------------------------------------- STS build
 __global__ void sts_leaf_kernel(const double *__restrict__ U, int64_t n, int R, int leaf,
                                 int64_t nleaves, double *__restrict__ level) {
-  extern __shared__ double rows[];  // leaf x R
+  extern __shared__ double rows[];  // leaf x R, then the packed (a, b) table
   const int Rt = R * (R + 1) / 2;
   const int Rs = tri_stride(R);
+  uint16_t *ab = reinterpret_cast<uint16_t *>(rows + (size_t)leaf * R);
+  for (int a = threadIdx.x; a < R; a += blockDim.x) {   // row a of the packed triangle
+    const int e0 = a * R - (a * (a - 1)) / 2;
+    for (int b = a; b < R; ++b) ab[e0 + b - a] = (uint16_t)(a | (b << 8));
+  }
   for (int64_t v = blockIdx.x; v < nleaves; v += gridDim.x) {
     const int64_t r0 = v * leaf;
     const int nr = (int)min((int64_t)leaf, n - r0);
@@ -198,17 +204,58 @@ __global__ void sts_leaf_kernel(const double *__restrict__ U, int64_t n, int R, 
     double *out = level + v * Rs;
     if (Rs > Rt && threadIdx.x == 0) out[Rt] = 0.0;
     for (int e = threadIdx.x; e < Rt; e += blockDim.x) {
-      // decode packed (a, b)
-      int a = 0, rem = e;
-      while (rem >= R - a) {
-        rem -= R - a;
-        ++a;
-      }
-      const int b = a + rem;
+      const int a = ab[e] & 0xff, b = ab[e] >> 8;
       double s = 0.0;
       for (int q = 0; q < nr; ++q) s = fma(rows[q * R + a], rows[q * R + b], s);
       out[e] = s;
     }
+  }
+}
+
+// R <= 64: leaf Grams on the fp64 tensor cores, one warp per leaf (gram_mma.cuh), written
+// as the packed upper triangle.
+template <int T>
+__global__ void __launch_bounds__(256)
+sts_leaf_mma_kernel(const double *__restrict__ U, int64_t n, int R, int leaf, int64_t nleaves,
+                    double *__restrict__ level) {
+  extern __shared__ double sh[];   // one packed node per warp
+  constexpr int NP = T * (T + 1) / 2;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int Rt = R * (R + 1) / 2, Rs = tri_stride(R);
+  const int kk = lane & 3, col = lane >> 2;
+  for (int64_t v = (int64_t)blockIdx.x * nw + wid; v < nleaves; v += (int64_t)gridDim.x * nw) {
+    const int64_t r0 = v * leaf, rend = min(r0 + leaf, n);
+    double acc[NP][2];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) acc[p][0] = acc[p][1] = 0.0;
+    for (int k0 = 0; k0 < leaf; k0 += 16) {   // 4 row steps' loads in flight at once
+      double f[4][T];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) gram_load<T>(U, nullptr, r0 + k0 + 4 * g + kk, rend, R, col, f[g]);
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        if (k0 + 4 * g < leaf) gram_accum<T>(f[g], acc);
+    }
+    // packed triangle staged in shared memory, then written with coalesced stores
+    double *stage = sh + (size_t)wid * Rs;
+    int p = 0;
+#pragma unroll
+    for (int a = 0; a < T; ++a)
+#pragma unroll
+      for (int b = a; b < T; ++b) {
+        const int ga = 8 * a + col;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int gb = 8 * b + 2 * kk + u;
+          if (ga <= gb && gb < R) stage[tri_index(ga, gb, R)] = acc[p][u];
+        }
+        ++p;
+      }
+    if (Rs > Rt && lane == 0) stage[Rt] = 0.0;
+    __syncwarp();
+    double *out = level + v * Rs;
+    for (int e = lane; e < Rs; e += 32) out[e] = stage[e];
+    __syncwarp();
   }
 }
 
@@ -432,9 +479,37 @@ int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
   const int64_t width = 1LL << depth;
   double *lvl = d_tree + (width - 1) * (int64_t)Rt;
   int64_t g = nleaves < 16LL * sm_count() ? nleaves : 16LL * sm_count();
-  sts_leaf_kernel<<<(unsigned)g, 128, sizeof(double) * leaf * R, st>>>(d_U, n, R, leaf, nleaves,
-                                                                      lvl);
+  if (R <= 64) {
+    int64_t gm = ceil_div(nleaves, 8);
+    if (gm > 8LL * sm_count()) gm = 8LL * sm_count();
+    const size_t msm = sizeof(double) * 8 * (size_t)Rt;
+    static bool leaf_attr[9] = {};
+#define RCP_LEAF(K)                                                                             \
+  case K:                                                                                       \
+    if (!leaf_attr[K]) {                                                                        \
+      RCP_CUDA_TRY(cudaFuncSetAttribute(sts_leaf_mma_kernel<K>,                                 \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
+      leaf_attr[K] = true;                                                                      \
+    }                                                                                           \
+    sts_leaf_mma_kernel<K><<<(unsigned)gm, 256, msm, st>>>(d_U, n, R, leaf, nleaves, lvl);      \
+    break
+    switch ((R + 7) / 8) {
+      RCP_LEAF(1); RCP_LEAF(2); RCP_LEAF(3); RCP_LEAF(4); RCP_LEAF(5); RCP_LEAF(6); RCP_LEAF(7);
+      default: RCP_LEAF(8);
+    }
+#undef RCP_LEAF
+    RCP_LAUNCH_CHECK("sts_leaf_mma");
+  } else {
+  const size_t lsm = sizeof(double) * leaf * R + sizeof(uint16_t) * (size_t)R * (R + 1) / 2;
+  static bool attr = false;
+  if (!attr) {
+    RCP_CUDA_TRY(cudaFuncSetAttribute(sts_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      100 * 1024));
+    attr = true;
+  }
+  sts_leaf_kernel<<<(unsigned)g, 128, lsm, st>>>(d_U, n, R, leaf, nleaves, lvl);
   RCP_LAUNCH_CHECK("sts_leaf");
+  }
   if (width > nleaves) {
     int64_t len = (width - nleaves) * Rt;
     int64_t b = ceil_div(len, 256);
