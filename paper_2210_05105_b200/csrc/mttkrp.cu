@@ -37,9 +37,19 @@ int sm_count() {
 
 constexpr int kMaxModes = 8;
 constexpr int kPrivRows = 49152;   // CTA-private row histogram limit (int32 in smem)
-constexpr int kSpmmChunk = 256;    // entries per warp in the segmented reduction
+// (overridable at compile time for parameter sweeps: tools/lab/sweep_spmm.py)
+#ifndef RCP_SPMM_CHUNK
+#define RCP_SPMM_CHUNK 256
+#endif
+#ifndef RCP_SPMM_U
+#define RCP_SPMM_U 4
+#endif
+#ifndef RCP_SPMM_BLOCKS_PER_SM
+#define RCP_SPMM_BLOCKS_PER_SM 8
+#endif
+constexpr int kSpmmChunk = RCP_SPMM_CHUNK;   // entries per warp in the segmented reduction
 constexpr int64_t kItemE = 512;    // entries per traversal item (a fiber chunk)
-constexpr int kSpmmU = 4;          // Hs-row loads in flight per lane
+constexpr int kSpmmU = RCP_SPMM_U;           // Hs-row loads in flight per lane
 
 // Row stride of the scaled KRP rows Hs: a multiple of 16 doubles, so every row starts on a
 // 128-byte line and a warp's double2 row load touches ceil(R/16) lines, not one more.
@@ -1319,7 +1329,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     RCP_LAUNCH_CHECK("rows_hit");
   }
   // 6. segmented reduction
-  const unsigned sb = (unsigned)(8 * sm_count());
+  const unsigned sb = (unsigned)(RCP_SPMM_BLOCKS_PER_SM * sm_count());
   if (R <= 64) spmm_packed_kernel<1><<<sb, 256, 0, st>>>(rptr, n_rows, nnz, ent, Hs, R, d_out);
   else spmm_packed_kernel<2><<<sb, 256, 0, st>>>(rptr, n_rows, nnz, ent, Hs, R, d_out);
   RCP_LAUNCH_CHECK("spmm_packed");
