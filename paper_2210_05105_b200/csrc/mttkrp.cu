@@ -552,7 +552,10 @@ cta_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__
 constexpr int kBucketMax = 512;        // buckets of the small-row (CTA-histogram) path
 constexpr int kBigBucketMax = 2048;    // buckets of the large-row path (<= 2^14 rows each)
 constexpr int kBigMaxShift = 14;
-constexpr int64_t kBucketMinRows = 4096;   // below: the single-pass scatter is faster
+#ifndef RCP_BUCKET_MIN_ROWS
+#define RCP_BUCKET_MIN_ROWS 4096
+#endif
+constexpr int64_t kBucketMinRows = RCP_BUCKET_MIN_ROWS;   // below: the single-pass scatter is faster
 
 // bofs[cta][b] = start of the CTA's slice of bucket b = rptr[b << sh] + sum over the
 // bucket's rows of the CTA-exclusive prefix cmat[cta][row]

@@ -50,11 +50,15 @@ print(json.dumps({"mttkrp_ms": sum(a.elapsed_time(b) for a, b in ev) / len(ev)})
 
 def main():
     variants = {}
-    for chunk in (128, 256, 512):
-        for u in (2, 4):
-            for bps in (4, 8):
-                variants["c%d_u%d_b%d" % (chunk, u, bps)] = {
-                    "RCP_SPMM_CHUNK": chunk, "RCP_SPMM_U": u, "RCP_SPMM_BLOCKS_PER_SM": bps}
+    if len(sys.argv) > 1 and sys.argv[1] == "transpose":
+        variants["two_pass"] = {"RCP_BUCKET_MIN_ROWS": 4096}
+        variants["single_pass"] = {"RCP_BUCKET_MIN_ROWS": 1 << 20}
+    else:
+        for chunk in (128, 256, 512):
+            for u in (2, 4):
+                for bps in (4, 8):
+                    variants["c%d_u%d_b%d" % (chunk, u, bps)] = {
+                        "RCP_SPMM_CHUNK": chunk, "RCP_SPMM_U": u, "RCP_SPMM_BLOCKS_PER_SM": bps}
     res = {}
     for tag, defs in variants.items():
         so = build(tag, defs)
@@ -63,7 +67,8 @@ def main():
         line = [l for l in out.stdout.splitlines() if l.startswith("{")]
         res[tag] = json.loads(line[-1])["mttkrp_ms"] if line else out.stderr[-300:]
         print(tag, res[tag], flush=True)
-    with open(os.path.join(ROOT, "gpurun_out", "sweep_spmm.json"), "w") as f:
+    name = "sweep_%s.json" % (sys.argv[1] if len(sys.argv) > 1 else "spmm")
+    with open(os.path.join(ROOT, "gpurun_out", name), "w") as f:
         json.dump(res, f, indent=1)
 
 
