@@ -53,7 +53,15 @@ constexpr int kMaxDepth = 30;   // local tree depth limit (2^30 leaves)
 // [kGenBase + g] runs pushed during generation g (each generation has its own counter, so
 // the extent of generation g + 1 is stable once every CTA has passed the barrier)
 constexpr int kGenBase = 8;
-constexpr size_t kProfBytes = 16 * (kMaxDepth + 2);
+// per level: [start time, runs] at 2 l, then [last warp finish, ~first warp finish] at
+// 2 (kMaxDepth + 2) + 2 l (global timer, ns).  With -DRCP_WALK_TRACE also, per level, the
+// longest time any warp spent in each phase of one run (claim -> run record, -> h row,
+// -> child mass, -> partition + push) at 4 (kMaxDepth + 2) + 4 l (diagnostics only).
+#ifdef RCP_WALK_TRACE
+constexpr size_t kProfBytes = 64 * (kMaxDepth + 2);
+#else
+constexpr size_t kProfBytes = 32 * (kMaxDepth + 2);
+#endif
 constexpr size_t kCtlBytes = sizeof(int) * (kGenBase + kMaxDepth + 8);
 
 struct Run {
@@ -357,13 +365,29 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
   // l + 1 through that level's own counter, whose value is stable after the grid barrier.
   __shared__ int claim;
   __shared__ Stage stg;
+  __shared__ unsigned long long fin_last, fin_first_inv;   // this CTA's warps, this level
+#ifdef RCP_WALK_TRACE
+  __shared__ unsigned long long ph_max[4];
+  auto gtime = []() {
+    unsigned long long x;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(x));
+    return x;
+  };
+#endif
   if (threadIdx.x == 0) stg.count = 0;
   int64_t begin = 0, end = min((int64_t)ld_volatile(&ctl[0]), cap_runs);
   for (int lvl = 0; lvl <= depth && end > begin; ++lvl) {
     int *gen_cnt = &ctl[kGenBase + lvl];
     // this CTA's runs begin + blockIdx.x + k gridDim.x (spread over the level), claimed one
     // by one by its warps
-    if (threadIdx.x == 0) claim = 0;
+    if (threadIdx.x == 0) {
+      claim = 0;
+      fin_last = 0ull;
+      fin_first_inv = 0ull;
+#ifdef RCP_WALK_TRACE
+      ph_max[0] = ph_max[1] = ph_max[2] = ph_max[3] = 0ull;
+#endif
+    }
     if (threadIdx.x == 0 && blockIdx.x == 0) {   // level start time and run count
       unsigned long long tnow;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
@@ -375,14 +399,31 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
       int tc = 0;
       if (lane == 0) tc = atomicAdd(&claim, 1);
       const int64_t t = begin + blockIdx.x + (int64_t)__shfl_sync(0xffffffffu, tc, 0) * gridDim.x;
-      if (t >= end) break;
+      if (t >= end) {
+        if (lane == 0) {   // this warp's finish time for the per-level record
+          unsigned long long tnow;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+          atomicMax(&fin_last, tnow);
+          atomicMax(&fin_first_inv, ~tnow);
+        }
+        break;
+      }
+#ifdef RCP_WALK_TRACE
+      const unsigned long long tr0 = gtime();
+#endif
       const Run run = runs[t];
       const int32_t lo = run.lo, hi = run.hi, level = run.level;
       const double *rs = (level & 1) ? rB : rA;
       const int32_t *is = (level & 1) ? iB : iA;
       const int32_t s0 = is[lo];
+#ifdef RCP_WALK_TRACE
+      const unsigned long long tr1 = gtime();
+#endif
       for (int c = lane; c < R; c += 32) hv[c] = H ? H[(int64_t)s0 * R + c] : 1.0;
       __syncwarp();
+#ifdef RCP_WALK_TRACE
+      const unsigned long long tr2 = gtime();
+#endif
       if (level < depth) {
         // child masses <GM_child, h h^T> over the packed triangle, two positions per step
         // T = max(q_left, 0) / q_node (ref samplers.py:423-451).  q_node is inherited from
@@ -422,6 +463,9 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
           }
         }
         qL = warp_sum(qL + qL2);
+#ifdef RCP_WALK_TRACE
+        const unsigned long long tr3 = gtime();
+#endif
         const double qnode = known ? run.qv : warp_sum(qV + qV2);
         if (!(qnode > 0.0)) {
           fail_run(lo, hi, is, Xi, status, ctl, lane);
@@ -469,6 +513,15 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         if (nr > 0)
           push_child(runs, gen_cnt, end, cap_runs, status, stg, run, lo + nl, hi, T, true, unknown,
                      depth, lane);
+#ifdef RCP_WALK_TRACE
+        if (lane == 0) {
+          const unsigned long long tr4 = gtime();
+          atomicMax(&ph_max[0], tr1 - tr0);
+          atomicMax(&ph_max[1], tr2 - tr1);
+          atomicMax(&ph_max[2], tr3 - tr2);
+          atomicMax(&ph_max[3], tr4 - tr3);
+        }
+#endif
         continue;
       }
       // ---- leaf block: masses z^T M' z of its rows z = u (.) h, then each sample's
@@ -552,6 +605,13 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
       if (lane == 0) atomicAdd(&ctl[2], hi - lo);
     }
     publish_children(runs, gen_cnt, end, cap_runs, status, stg);
+    if (threadIdx.x == 0) {   // (publish_children synchronised the CTA)
+      atomicMax(&prof[2 * (kMaxDepth + 2) + 2 * lvl], fin_last);
+      atomicMax(&prof[2 * (kMaxDepth + 2) + 2 * lvl + 1], fin_first_inv);
+#ifdef RCP_WALK_TRACE
+      for (int q = 0; q < 4; ++q) atomicMax(&prof[4 * (kMaxDepth + 2) + 4 * lvl + q], ph_max[q]);
+#endif
+    }
     grid.sync();
     const int64_t pushed_n = ld_volatile(gen_cnt);
     begin = end;

@@ -89,7 +89,7 @@ def main():
             e.record()
             torch.cuda.synchronize()
             J = a[3]
-            buf = (ctypes.c_ulonglong * 64)()
+            buf = (ctypes.c_ulonglong * 128)()
             lab.lab_walk_prof(ctypes.c_void_p(ops._ws["sts_walk"].data_ptr()), ctypes.c_int64(J),
                               ctypes.c_int64(U.shape[0]), int(leaf), U.shape[1], buf)
             t = list(buf)
@@ -99,7 +99,10 @@ def main():
                     break
                 lv.append((t[2 * l + 1], t[2 * l]))
             end = t[2 * 31]
-            per = [{"runs": r, "us": round(((lv[i + 1][1] if i + 1 < len(lv) else end) - t0) / 1e3, 1)}
+            fb = 2 * 32
+            per = [{"runs": r, "us": round(((lv[i + 1][1] if i + 1 < len(lv) else end) - t0) / 1e3, 1),
+                    "first_warp_done_us": round(((~t[fb + 2 * i + 1]) & (2 ** 64 - 1) - t0) / 1e3, 1),
+                    "last_warp_done_us": round((t[fb + 2 * i] - t0) / 1e3, 1)}
                    for i, (r, t0) in enumerate(lv)]
             row = {"walk_n": U.shape[0], "leaf": int(leaf), "walk_ms": s.elapsed_time(e),
                    "kernel_us": round((end - lv[0][1]) / 1e3, 1), "levels": per}
