@@ -47,6 +47,13 @@ constexpr int kMaxLeaf = 64;
 // partitions more than kMaxRun samples.
 constexpr int32_t kLeafChunk = 256;
 constexpr int32_t kMaxRun = 256;
+#ifndef RCP_WALK_UNROLL
+#define RCP_WALK_UNROLL 8   // child-mass loop: node loads in flight per lane (swept: 4/8/10)
+#endif
+#ifndef RCP_WALK_MIN_BLOCKS
+#define RCP_WALK_MIN_BLOCKS 2
+#endif
+constexpr int kWalkUnroll = RCP_WALK_UNROLL;
 constexpr int kWalkWarps = 16;
 constexpr int kMaxDepth = 30;   // local tree depth limit (2^30 leaves)
 // control words: [0] seeded runs, [2] samples finished, [3] participants,
@@ -334,7 +341,7 @@ __device__ __forceinline__ void fail_run(int32_t lo, int32_t hi, const int32_t *
   }
 }
 
-__global__ void __launch_bounds__(kWalkWarps * 32, 2)
+__global__ void __launch_bounds__(kWalkWarps * 32, RCP_WALK_MIN_BLOCKS)
 walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, int64_t n, int R,
                  int leaf, int depth, int64_t row_lo,
                  const double *__restrict__ Mfull,
@@ -439,7 +446,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         double qL = 0.0, qV = 0.0, qL2 = 0.0, qV2 = 0.0;
         const int n2 = Rs / 2;
         if (known) {
-#pragma unroll 4
+#pragma unroll (kWalkUnroll)
           for (int e = lane; e < n2; e += 32) {
             const double2 gl = __ldg(GL + e);
             const uint2 ab = PR[e];
@@ -449,7 +456,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
             qL2 = fma(gl.y, h1, qL2);
           }
         } else {
-#pragma unroll 4
+#pragma unroll (kWalkUnroll)
           for (int e = lane; e < n2; e += 32) {
             const double2 gl = __ldg(GL + e);
             const double2 gv = __ldg(GV + e);

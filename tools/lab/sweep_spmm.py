@@ -44,13 +44,23 @@ me.mttkrp = timed
 for r in range(4, 9):
     cl.round(r)
 torch.cuda.synchronize()
-print(json.dumps({"mttkrp_ms": sum(a.elapsed_time(b) for a, b in ev) / len(ev)}))
+me.mttkrp = orig
+rt = []
+for r in range(9, 14):
+    a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+    a.record(); cl.round(r, check=False); b.record(); b.synchronize(); rt.append(a.elapsed_time(b))
+print(json.dumps({"mttkrp_ms": sum(a.elapsed_time(b) for a, b in ev) / len(ev),
+                  "round_ms": sorted(rt)[len(rt) // 2]}))
 """
 
 
 def main():
     variants = {}
-    if len(sys.argv) > 1 and sys.argv[1] == "transpose":
+    if len(sys.argv) > 1 and sys.argv[1] == "walk":
+        for u in (4, 8, 10):
+            for mb in (1, 2):
+                variants["u%d_mb%d" % (u, mb)] = {"RCP_WALK_UNROLL": u, "RCP_WALK_MIN_BLOCKS": mb}
+    elif len(sys.argv) > 1 and sys.argv[1] == "transpose":
         variants["two_pass"] = {"RCP_BUCKET_MIN_ROWS": 4096}
         variants["single_pass"] = {"RCP_BUCKET_MIN_ROWS": 1 << 20}
     else:
@@ -65,7 +75,7 @@ def main():
         out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, so)], capture_output=True,
                              text=True, cwd=ROOT)
         line = [l for l in out.stdout.splitlines() if l.startswith("{")]
-        res[tag] = json.loads(line[-1])["mttkrp_ms"] if line else out.stderr[-300:]
+        res[tag] = json.loads(line[-1]) if line else out.stderr[-300:]
         print(tag, res[tag], flush=True)
     name = "sweep_%s.json" % (sys.argv[1] if len(sys.argv) > 1 else "spmm")
     with open(os.path.join(ROOT, "gpurun_out", name), "w") as f:
