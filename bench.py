@@ -208,6 +208,10 @@ def run_ours(args):
             cl.round(rnd)
     torch.cuda.synchronize()
     mt_events.clear()
+    # factor state entering the first timed round: the e2e leg replays the same rounds
+    from paper_2210_05105_b200.als import AlsSession
+    snap = AlsSession(cl).pinned_factors()
+    first_timed = rnd + 1
     stats0 = me.stats.clone()
     if spmd:
         import torch.distributed as dist
@@ -279,7 +283,7 @@ def run_ours(args):
     #   12 nnz_d + 16 S_d + 8R S_ne + 8R rows_hit  per solve, summed over the timed solves
     B = 12.0 * st_mt[2] + 16.0 * st_mt[0] + 8.0 * R * st_mt[1] + 8.0 * R * st_mt[4]
     achieved = (B / (mt_ms / 1e3)) / 1e9 if mt_ms > 0 else 0.0
-    e2e = measure_e2e(cl, args, rnd)
+    e2e = measure_e2e(cl, args, first_timed, snap, float(st[3]))
     if spmd:
         import torch.distributed as dist
         tt = torch.tensor([e2e.pop("_dt"), e2e.pop("_nnz")], dtype=torch.float64, device=dev)
@@ -346,33 +350,40 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def measure_e2e(cl, args, rnd, steps=None):
-    """Same metric through the public host-buffer API: each step uploads the factor
-    matrices from pinned host memory, rebuilds the sampler state, runs the round and
-    reads the updated factors and sigma back (AlsSession.step_host)."""
+def measure_e2e(cl, args, first, snap, timed_nnz):
+    """Same metric through the public host-buffer API, over the SAME rounds as the timed
+    region: step 0 uploads the factor state that entered the first timed round (pinned
+    host snapshot), each later step uploads the factors the previous step downloaded
+    (ping-pong between two pinned sets), so every step rebuilds the sampler state from
+    host memory, runs the round with the timed region's round id and reads the updated
+    factors and sigma back (AlsSession.step_host).  The rounds are deterministic, so the
+    sampled-nonzero count equals the timed region's (`same_rounds` says whether it did)."""
     import torch
     from paper_2210_05105_b200.als import AlsSession
     sess = AlsSession(cl)
-    host_in = sess.pinned_factors()
-    host_out = sess.pinned_factors()
-    steps = steps or max(2, args.steps)
+    bufs = [sess.pinned_factors(), sess.pinned_factors()]
+    steps = args.steps
     me = cl.ranks[0]
     graph = not args.eager
-    sess.step_host(host_in, host_out, rnd + 1)   # eager: sizes every workspace
-    sess.step_host(host_in, host_out, rnd + 2, graph=graph)
+    sess.step_host(snap, bufs[0], first)   # eager: sizes every workspace
+    for b in bufs:                         # one graph per output set
+        sess.step_host(snap, b, first, graph=graph)
     torch.cuda.synchronize()
     st0 = me.stats.clone()
     t0 = time.perf_counter()
     for s in range(steps):
-        sess.step_host(host_in, host_out, rnd + 3 + s, graph=graph)
+        src = snap if s == 0 else bufs[(s - 1) % 2]
+        sess.step_host(src, bufs[s % 2], first + s, graph=graph)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     st = (me.stats - st0).cpu().numpy()
     return {"value": float(st[3]) / dt, "unit": UNIT,
-            "h2d_bytes_per_step": int(sum(h.numel() * 8 for h in host_in)),
-            "d2h_bytes_per_step": int(sum(h.numel() * 8 for h in host_out) + 8 * me.R),
+            "h2d_bytes_per_step": int(sum(h.numel() * 8 for h in snap)),
+            "d2h_bytes_per_step": int(sum(h.numel() * 8 for h in bufs[0]) + 8 * me.R),
             "steps": steps, "ms_per_step": dt / steps * 1e3, "_dt": dt, "_nnz": float(st[3]),
-            "api": "AlsSession.step_host (pinned host factors in, factors + sigma out)" +
+            "same_rounds": bool(float(st[3]) == timed_nnz),
+            "api": "AlsSession.step_host (pinned host factors in, factors + sigma out; the "
+                   "timed region's rounds replayed from its entry state)" +
                    (", round replayed from a CUDA graph" if graph and cl.graph_ok() else "")}
 
 

@@ -203,8 +203,9 @@ class AlsSession:
         download the updated factors and sigma.  Transfers run on a copy stream: mode j's
         upload overlaps the rebuild of the modes before it, and factor k's download
         overlaps the solves after k.  graph=True replays the round (with its downloads)
-        from a CUDA graph when the cluster allows it (Cluster.graph_ok); the buffers in
-        `factors_out` must then be the same on every call."""
+        from a CUDA graph when the cluster allows it (Cluster.graph_ok); one graph is
+        captured per `factors_out` buffer set (the downloads are part of the graph), so a
+        caller may ping-pong between two sets."""
         t = torch()
         r0 = self.cl.ranks[0]
         if len(self.cl.ranks) != 1:
@@ -232,7 +233,8 @@ class AlsSession:
                 factors_out[k].copy_(r0.U[k], non_blocking=True)
 
         if graph and self.cl.graph_ok():
-            self.cl.round_graph(rnd, on_solved=download, join=(self.copy,), tag="step_host")
+            self.cl.round_graph(rnd, on_solved=download, join=(self.copy,),
+                               tag="step_host:%x" % factors_out[0].data_ptr())
         else:
             self.cl.round(rnd, check=False, on_solved=download)
         self.sigma = r0.sigma.to("cpu", non_blocking=True)
