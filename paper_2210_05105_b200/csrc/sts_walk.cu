@@ -676,6 +676,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   if (key_bits > 64 || !d_hkey) key_bits = 64;
   if (J == 0) return RCP_OK;
   if (n == 0 || !d_tree || !d_U || !d_M || !d_Xi || !d_pmp_i || !d_ws) return RCP_ERR_ARG;
+  if (d_H_out && d_H_out == d_H_in) return RCP_ERR_ARG;   // groups read a shared row of H_in
   const int depth = rcp_sts_depth(n, leaf);
   if (depth > kMaxDepth) return RCP_ERR_ARG;
   WalkWs L(J, depth, R);
