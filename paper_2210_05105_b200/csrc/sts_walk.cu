@@ -121,7 +121,11 @@ struct WalkWs {
 constexpr int kMmaMaxR = 128;
 static_assert(kMmaMaxR >= RCP_MAX_RANK, "leaf masses run on the tensor cores for every rank");
 __host__ __device__ __forceinline__ int mma_rn(int R) { return (R + 7) & ~7; }
-__host__ __device__ __forceinline__ int mma_zs(int R) { return mma_rn(R) + 2; }   // Z row stride
+// Row strides of the leaf tile Z and of M in shared memory: Rn + 4 is 4 or 12 mod 16 doubles,
+// so the mma fragment reads (8 rows x 4 k of Z, 4 k x 8 columns of M) hit 16 distinct
+// double-banks per half-warp (Rn + 2 and Rn were 2-way conflicted: 4 wavefronts per load).
+__host__ __device__ __forceinline__ int mma_zs(int R) { return mma_rn(R) + 4; }
+__host__ __device__ __forceinline__ int mma_ms(int R) { return mma_rn(R) + 4; }
 
 // Shared doubles per walker warp: h, leaf rows z = u (.) h (a batch, or an 8-row mma
 // tile), leaf masses, path.
@@ -133,7 +137,7 @@ __host__ __device__ __forceinline__ size_t walk_per_warp(int R) {
 
 // Block-shared doubles: the full padded M (mma path) or packed M' (fallback).
 __host__ __device__ __forceinline__ size_t walk_block_doubles(int R) {
-  return (size_t)mma_rn(R) * mma_rn(R);
+  return (size_t)mma_rn(R) * mma_ms(R);
 }
 
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
@@ -279,7 +283,7 @@ __global__ void walk_gm_kernel(const double *__restrict__ tree, const double2 *_
 // reservation per CTA and level (a global counter taking one atomic per child run
 // serialised ~2*10^4 same-address atomics per level); a full buffer falls back to the
 // global counter.
-constexpr int kStage = 288;
+constexpr int kStage = 224;   // two CTAs of 16 walker warps per SM at R = 50
 
 struct Stage {
   Run buf[kStage];
@@ -354,16 +358,16 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
   extern __shared__ double sh[];
   const int Rs = tri_stride(R);                    // even node stride (zero pad)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int Rn = mma_rn(R), Zs = mma_zs(R);
+  const int Rn = mma_rn(R), Zs = mma_zs(R), Ms = mma_ms(R);
   const size_t bd = walk_block_doubles(R);
-  double *Mp = sh;                                 // full M, zero-padded to Rn x Rn
+  double *Mp = sh;                                 // full M, zero-padded to Rn x Ms
   double *hv = sh + bd + (size_t)wid * walk_per_warp(R);   // R: the run's Hadamard row
   double *zb = hv + R;                             // leaf rows (.) h
   double *mass = zb + 8 * Zs;                      // leaf
   uint32_t *pairs = reinterpret_cast<uint32_t *>(sh + bd + (size_t)nw * walk_per_warp(R));
   for (int e = threadIdx.x; e < Rs; e += blockDim.x) pairs[e] = pairs_g[e];
-  for (int e = threadIdx.x; e < Rn * Rn; e += blockDim.x) {
-    const int k = e / Rn, c = e - k * Rn;
+  for (int e = threadIdx.x; e < Rn * Ms; e += blockDim.x) {
+    const int k = e / Ms, c = e - k * Ms;
     Mp[e] = (k < R && c < R) ? Mfull[k * R + c] : 0.0;
   }
   __syncthreads();
@@ -553,7 +557,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
           for (int nt = 0; nt < Rn; nt += 8) {
             double c0 = 0.0, c1 = 0.0;
             for (int ks = 0; ks < Rn; ks += 4)
-              dmma_8x8x4(c0, c1, zr[ks + quad], Mp[(ks + quad) * Rn + nt + row]);
+              dmma_8x8x4(c0, c1, zr[ks + quad], Mp[(ks + quad) * Ms + nt + row]);
             msum = fma(c0, zr[nt + 2 * quad], msum);
             msum = fma(c1, zr[nt + 2 * quad + 1], msum);
           }
