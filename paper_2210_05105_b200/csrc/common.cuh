@@ -102,6 +102,33 @@ __host__ __device__ __forceinline__ int tri_index(int a, int b, int R) {
   return a * R - (a * (a - 1)) / 2 + (b - a);
 }
 
+// ---- asynchronous staging of 8-row tiles (cp.async), shared by the tall-skinny mma kernels
+__device__ __forceinline__ void cpa8_zfill(double *smem, const double *gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 8 : 0;   // src-size 0: the 8 destination bytes are zero-filled
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+// wait until at most nbuf - 1 groups are pending (nbuf in 1..4)
+__device__ __forceinline__ void cpa_wait_stages(int nbuf) {
+  if (nbuf >= 4) cpa_wait<3>();
+  else if (nbuf == 3) cpa_wait<2>();
+  else if (nbuf == 2) cpa_wait<1>();
+  else cpa_wait<0>();
+}
+// Rows r0 .. r0+7 of a row-major (n x R) matrix into a warp's tile with row stride zs:
+// rows >= nb are zero-filled, columns >= R are left untouched (zero them once).
+__device__ __forceinline__ void stage_tile8(double *tile, const double *__restrict__ src,
+                                            int64_t r0, int nb, int R, int zs, int lane) {
+  for (int c = lane; c < 8 * R; c += 32) {
+    const int j = c / R, col = c - j * R;
+    const bool ok = j < nb;
+    cpa8_zfill(tile + j * zs + col, ok ? src + (r0 + j) * R + col : src, ok);
+  }
+}
+
 }  // namespace rcp
 
 #define RCP_CUDA_TRY(expr)                                   \

@@ -28,9 +28,16 @@ constexpr int kGramRows = 64;      // rows per staged chunk
 constexpr int kGramThreads = 256;
 // tile pairs per thread: (R/4)(R/4+1)/2 <= 3*256 for R <= 128 (template parameter)
 
+#ifndef RCP_GRAM_CTAS
+#define RCP_GRAM_CTAS 2   // CTAs per SM of the Gram kernels (swept 1/2/3: tools/lab/dense_lab.py)
+#endif
+#ifndef RCP_GRAM_MINB
+#define RCP_GRAM_MINB 2   // __launch_bounds__ min blocks of gram_mma_kernel (<= 128 registers)
+#endif
 int gram_grid(int64_t n) {
   int64_t tiles = ceil_div(n, kGramRows);
-  int64_t g = sm_count();
+  // large factors: more CTAs hide the load latency; small ones keep fewer partials
+  int64_t g = (int64_t)(n >= (1LL << 20) ? RCP_GRAM_CTAS : 1) * sm_count();
   if (tiles < g) g = tiles;
   return (int)(g < 1 ? 1 : g);
 }
@@ -562,41 +569,50 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
 template <int KS>   // k-steps = Rn / 4
 __global__ void __launch_bounds__(kUpdThreads)
 update_mma_kernel(const double *__restrict__ M, int64_t n, int R, const double *__restrict__ B,
-                  double *__restrict__ U, double *__restrict__ part, int *status) {
+                  double *__restrict__ U, double *__restrict__ part, int *status, int nbuf) {
   extern __shared__ double sh[];
   const int Rn = KS * 4;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int row = lane >> 2, quad = lane & 3;
-  double *Bs = sh;                                   // Rn x Rn
-  double *Ms = sh + Rn * Rn + (size_t)wid * 8 * Rn;  // per warp: 8 x Rn
-  for (int e = threadIdx.x; e < Rn * Rn; e += blockDim.x) {
-    const int k = e / Rn, c = e - k * Rn;
+  // row strides Rn + 4 (4 or 12 mod 16 doubles): conflict-free fragment reads
+  const int Ss = Rn + 4;
+  double *Bs = sh;                                   // Rn x Ss
+  double *Mbase = sh + Rn * Ss + (size_t)wid * nbuf * 8 * Ss;   // per warp: nbuf x 8 x Ss
+  for (int e = threadIdx.x; e < Rn * Ss; e += blockDim.x) {
+    const int k = e / Ss, c = e - k * Ss;
     Bs[e] = (k < R && c < R) ? B[k * R + c] : 0.0;
   }
+  for (int c = lane; c < nbuf * 8 * Ss; c += 32) Mbase[c] = 0.0;   // padding columns stay 0
   __syncthreads();
   double sq[KS / 2][2];   // this lane's columns nt*8 + 2 quad + {0,1}, nt < Rn/8
 #pragma unroll
   for (int t = 0; t < KS / 2; ++t) sq[t][0] = sq[t][1] = 0.0;
   bool bad = false;
   const int64_t ntiles = ceil_div(n, (int64_t)8);
-  for (int64_t tile = (int64_t)blockIdx.x * nw + wid; tile < ntiles;
-       tile += (int64_t)gridDim.x * nw) {
+  const int64_t stride = (int64_t)gridDim.x * nw, t0 = (int64_t)blockIdx.x * nw + wid;
+  // nbuf-stage cp.async pipeline: the tiles nbuf - 1 ahead load while this one computes
+  auto stage = [&](int64_t tl, int slot) {
+    if (tl < ntiles)
+      stage_tile8(Mbase + slot * 8 * Ss, M, tl * 8, (int)min((int64_t)8, n - tl * 8), R, Ss, lane);
+    cpa_commit();
+  };
+  for (int s = 0; s < nbuf - 1; ++s) stage(t0 + s * stride, s);
+  int slot = 0;
+  for (int64_t tile = t0; tile < ntiles; tile += stride) {
+    stage(tile + (nbuf - 1) * stride, slot == 0 ? nbuf - 1 : slot - 1);
+    cpa_wait_stages(nbuf);
+    __syncwarp();
     const int64_t r0 = tile * 8;
     const int nr = (int)min((int64_t)8, n - r0);
-    __syncwarp();
-    for (int e = lane; e < 8 * Rn; e += 32) {
-      const int q = e / Rn, c = e - q * Rn;
-      Ms[e] = (q < nr && c < R) ? M[(r0 + q) * R + c] : 0.0;
-    }
-    __syncwarp();
+    const double *Ms = Mbase + slot * 8 * Ss;
     double a[KS];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) a[ks] = Ms[row * Rn + ks * 4 + quad];
+    for (int ks = 0; ks < KS; ++ks) a[ks] = Ms[row * Ss + ks * 4 + quad];
 #pragma unroll
     for (int nt = 0; nt < KS / 2; ++nt) {
       double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) dmma_8x8x4(c0, c1, a[ks], Bs[(ks * 4 + quad) * Rn + nt * 8 + row]);
+      for (int ks = 0; ks < KS; ++ks) dmma_8x8x4(c0, c1, a[ks], Bs[(ks * 4 + quad) * Ss + nt * 8 + row]);
       const int col = nt * 8 + 2 * quad;
       if (row < nr) {
         if (col < R) {
@@ -611,7 +627,10 @@ update_mma_kernel(const double *__restrict__ M, int64_t n, int R, const double *
         }
       }
     }
+    __syncwarp();   // every lane is done with this slot before it is refilled
+    slot = slot + 1 == nbuf ? 0 : slot + 1;
   }
+  cpa_wait<0>();
   if (bad) raise_status(status, RCP_ST_NONFINITE);
   // lanes with equal quad hold the same columns: reduce over the 8 rows, then warps
 #pragma unroll
@@ -682,7 +701,7 @@ __global__ void hadamard_rows_kernel(double *__restrict__ H, const double *__res
 // Steps go to (CTA, warp) in a fixed order; warps are combined in a fixed order (the CTA
 // partials then by sum_partials): deterministic.
 template <int T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, RCP_GRAM_MINB)
 gram_mma_kernel(const double *__restrict__ U, const double *__restrict__ scale, int64_t n, int R,
                 double *__restrict__ part) {
   constexpr int NP = T * (T + 1) / 2;
@@ -846,24 +865,35 @@ int rcp_update(const double *d_M, int64_t n, int R, const double *d_B, double *d
     const int ks = Rn / 4;
     int64_t tiles = ceil_div(n, (int64_t)8);
     int g = (int)std::min<int64_t>(ceil_div(tiles, (int64_t)nw), 4LL * sm_count());
-    const size_t sm2 = sizeof(double) * ((size_t)Rn * Rn + (size_t)nw * 8 * Rn);
+#ifndef RCP_UPD_NBUF
+#define RCP_UPD_NBUF 2
+#endif
+#ifndef RCP_UPD_SMEM_KB
+#define RCP_UPD_SMEM_KB 110   // two CTAs per SM
+#endif
+    int nbuf = RCP_UPD_NBUF;
+    auto upd_smem = [&](int nb) {
+      return sizeof(double) * ((size_t)Rn * (Rn + 4) + (size_t)nw * nb * 8 * (Rn + 4));
+    };
+    while (nbuf > 1 && upd_smem(nbuf) > RCP_UPD_SMEM_KB * 1024) --nbuf;
+    const size_t sm2 = upd_smem(nbuf);
     switch (ks) {
-      case 2: update_mma_kernel<2><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 4: update_mma_kernel<4><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 6: update_mma_kernel<6><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 8: update_mma_kernel<8><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 10: update_mma_kernel<10><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 12: update_mma_kernel<12><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 14: update_mma_kernel<14><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 16: update_mma_kernel<16><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 18: update_mma_kernel<18><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 20: update_mma_kernel<20><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 22: update_mma_kernel<22><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 24: update_mma_kernel<24><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 26: update_mma_kernel<26><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 28: update_mma_kernel<28><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      case 30: update_mma_kernel<30><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
-      default: update_mma_kernel<32><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status); break;
+      case 2: update_mma_kernel<2><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 4: update_mma_kernel<4><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 6: update_mma_kernel<6><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 8: update_mma_kernel<8><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 10: update_mma_kernel<10><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 12: update_mma_kernel<12><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 14: update_mma_kernel<14><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 16: update_mma_kernel<16><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 18: update_mma_kernel<18><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 20: update_mma_kernel<20><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 22: update_mma_kernel<22><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 24: update_mma_kernel<24><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 26: update_mma_kernel<26><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 28: update_mma_kernel<28><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      case 30: update_mma_kernel<30><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
+      default: update_mma_kernel<32><<<g, kUpdThreads, sm2, st>>>(d_M, n, R, d_B, d_U_out, part, d_status, nbuf); break;
     }
     RCP_LAUNCH_CHECK("update_mma");
     sum_partials_kernel<<<(unsigned)ceil_div(R, 32), 256, 0, st>>>(part, g, R, d_colsq);

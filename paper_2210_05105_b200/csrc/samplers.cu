@@ -34,7 +34,9 @@ int sm_count() {
 constexpr int kLevMmaMaxR = 128;
 static_assert(kLevMmaMaxR >= RCP_MAX_RANK, "leverage scores run on the tensor cores for every rank");
 __host__ __device__ __forceinline__ int lev_rn(int R) { return (R + 7) & ~7; }
-__host__ __device__ __forceinline__ int lev_zs(int R) { return lev_rn(R) + 2; }
+// Row stride of the staged U tile and of G+ in shared memory: Rn + 4 (4 or 12 mod 16
+// doubles) makes the mma fragment reads conflict-free.
+__host__ __device__ __forceinline__ int lev_zs(int R) { return lev_rn(R) + 4; }
 
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -42,33 +44,45 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
                : "d"(a), "d"(b));
 }
 
+#ifndef RCP_LEV_MINB
+#define RCP_LEV_MINB 1   // __launch_bounds__ min blocks of leverage_mma_kernel
+#endif
 template <int KS>   // k-steps = Rn / 4
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, RCP_LEV_MINB)
 leverage_mma_kernel(const double *__restrict__ U, int64_t n, int R, const double *__restrict__ Gp,
-                    double *__restrict__ lev, double *__restrict__ part) {
+                    double *__restrict__ lev, double *__restrict__ part, int nbuf) {
   extern __shared__ double sh[];
   constexpr int Rn = KS * 4;
   const int Zs = lev_zs(R);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double *G = sh;                                   // Rn x Rn
-  double *zb = sh + Rn * Rn + (size_t)wid * 8 * Zs;  // this warp's 8 x Zs tile
-  for (int e = threadIdx.x; e < Rn * Rn; e += blockDim.x) {
-    const int a = e / Rn, b = e - a * Rn;
+  double *G = sh;                                          // Rn x Zs
+  double *zbase = sh + Rn * Zs + (size_t)wid * nbuf * 8 * Zs;   // this warp's nbuf tiles
+  for (int e = threadIdx.x; e < Rn * Zs; e += blockDim.x) {
+    const int a = e / Zs, b = e - a * Zs;
     G[e] = (a < R && b < R) ? Gp[a * R + b] : 0.0;
   }
+  for (int c = lane; c < nbuf * 8 * Zs; c += 32) zbase[c] = 0.0;   // padding columns stay 0
   __syncthreads();
   const int row = lane >> 2, quad = lane & 3;
   double local = 0.0;
   const int64_t tiles = (n + 7) >> 3;
-  for (int64_t tl = (int64_t)blockIdx.x * nw + wid; tl < tiles; tl += (int64_t)gridDim.x * nw) {
+  const int64_t stride = (int64_t)gridDim.x * nw, t0 = (int64_t)blockIdx.x * nw + wid;
+  // nbuf-stage cp.async pipeline: the tiles nbuf - 1 ahead load while this one computes
+  auto stage = [&](int64_t tl, int slot) {
+    if (tl < tiles)
+      stage_tile8(zbase + slot * 8 * Zs, U, tl << 3, (int)min((int64_t)8, n - (tl << 3)), R, Zs,
+                  lane);
+    cpa_commit();
+  };
+  for (int s = 0; s < nbuf - 1; ++s) stage(t0 + s * stride, s);
+  int slot = 0;
+  for (int64_t tl = t0; tl < tiles; tl += stride) {
+    stage(tl + (nbuf - 1) * stride, slot == 0 ? nbuf - 1 : slot - 1);
+    cpa_wait_stages(nbuf);
+    __syncwarp();
     const int64_t r0 = tl << 3;
     const int nb = (int)min((int64_t)8, n - r0);
-    for (int c = lane; c < 8 * Zs; c += 32) {
-      const int j = c / Zs, col = c - j * Zs;
-      zb[c] = (j < nb && col < R) ? U[(r0 + j) * R + col] : 0.0;
-    }
-    __syncwarp();
-    const double *zr = zb + row * Zs;
+    const double *zr = zbase + slot * 8 * Zs + row * Zs;
     double a[KS];   // A fragments of the tile, reused by every n-tile
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) a[ks] = zr[ks * 4 + quad];
@@ -78,7 +92,7 @@ leverage_mma_kernel(const double *__restrict__ U, int64_t n, int R, const double
       double c0 = 0.0, c1 = 0.0;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks)
-        dmma_8x8x4(c0, c1, a[ks], G[(ks * 4 + quad) * Rn + nt + row]);
+        dmma_8x8x4(c0, c1, a[ks], G[(ks * 4 + quad) * Zs + nt + row]);
       msum = fma(c0, zr[nt + 2 * quad], msum);
       msum = fma(c1, zr[nt + 2 * quad + 1], msum);
     }
@@ -91,8 +105,10 @@ leverage_mma_kernel(const double *__restrict__ U, int64_t n, int R, const double
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
     local += t;
-    __syncwarp();
+    __syncwarp();   // every lane is done with this slot before it is refilled
+    slot = slot + 1 == nbuf ? 0 : slot + 1;
   }
+  cpa_wait<0>();
   __syncthreads();
   if (lane == 0) sh[wid] = local;   // reuse (G no longer needed)
   __syncthreads();
@@ -214,8 +230,10 @@ __global__ void sts_leaf_kernel(const double *__restrict__ U, int64_t n, int R, 
 
 // R <= 64: leaf Grams on the fp64 tensor cores, one warp per leaf (gram_mma.cuh), written
 // as the packed upper triangle.
+// CTAs per SM (register cap): swept 1/2/3 with tools/lab/dense_lab.py at 4.8M rows —
+// R = 50 (T = 7): 3.35 / 2.62 / 4.04 ms per tree build; R = 25 (T = 4): 0.82 / 0.74 / 0.60.
 template <int T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, (T <= 4 ? 3 : 2))
 sts_leaf_mma_kernel(const double *__restrict__ U, int64_t n, int R, int leaf, int64_t nleaves,
                     double *__restrict__ level) {
   extern __shared__ double sh[];   // one packed node per warp
@@ -381,7 +399,19 @@ int rcp_arls_build(const double *d_U, int64_t n, int R, const double *d_Gp, doub
   int grid = (int)(want < 4LL * sm_count() ? want : 4LL * sm_count());
   double *part = (double *)d_ws;
   void *scan_ws = (char *)d_ws + (size_t)4 * sm_count() * sizeof(double);
-  const size_t sm = sizeof(double) * ((size_t)lev_rn(R) * lev_rn(R) + 8 * 8 * (size_t)lev_zs(R));
+#ifndef RCP_LEV_NBUF
+#define RCP_LEV_NBUF 2   // with RCP_LEV_SMEM_KB 110: two CTAs per SM (swept: tools/lab/dense_lab.py)
+#endif
+#ifndef RCP_LEV_SMEM_KB
+#define RCP_LEV_SMEM_KB 110
+#endif
+  // up to RCP_LEV_NBUF staged tiles per warp within the shared-memory budget
+  int nbuf = RCP_LEV_NBUF;
+  auto lev_smem = [&](int nb) {
+    return sizeof(double) * ((size_t)lev_rn(R) * lev_zs(R) + 8 * (size_t)nb * 8 * lev_zs(R));
+  };
+  while (nbuf > 1 && lev_smem(nbuf) > RCP_LEV_SMEM_KB * 1024) --nbuf;
+  const size_t sm = lev_smem(nbuf);
   static bool attr_set[17] = {};
 #define RCP_LEV(K)                                                                              \
   case K:                                                                                       \
@@ -390,7 +420,7 @@ int rcp_arls_build(const double *d_U, int64_t n, int R, const double *d_Gp, doub
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
       attr_set[K / 2] = true;                                                                   \
     }                                                                                           \
-    leverage_mma_kernel<K><<<grid, 256, sm, st>>>(d_U, n, R, d_Gp, d_dist, part);               \
+    leverage_mma_kernel<K><<<grid, 256, sm, st>>>(d_U, n, R, d_Gp, d_dist, part, nbuf);         \
     break
   switch (lev_rn(R) / 4) {
     RCP_LEV(2); RCP_LEV(4); RCP_LEV(6); RCP_LEV(8); RCP_LEV(10); RCP_LEV(12); RCP_LEV(14);
