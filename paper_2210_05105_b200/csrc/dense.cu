@@ -37,7 +37,10 @@ constexpr int kGramThreads = 256;
 int gram_grid(int64_t n) {
   int64_t tiles = ceil_div(n, kGramRows);
   // large factors: more CTAs hide the load latency; small ones keep fewer partials
-  int64_t g = (int64_t)(n >= (1LL << 20) ? RCP_GRAM_CTAS : 1) * sm_count();
+#ifndef RCP_GRAM_BIG_ROWS
+#define RCP_GRAM_BIG_ROWS (1LL << 20)
+#endif
+  int64_t g = (int64_t)(n >= RCP_GRAM_BIG_ROWS ? RCP_GRAM_CTAS : 1) * sm_count();
   if (tiles < g) g = tiles;
   return (int)(g < 1 ? 1 : g);
 }
