@@ -49,6 +49,8 @@ def run(so, n, R):
                      device="cuda")
     out["gram_ms"] = timeit(lambda: lib.rcp_gram(P(U.data_ptr()), None, i64(n), i32(R),
                                                  P(G.data_ptr()), P(ws.data_ptr()), None))
+    ref = U.T @ U
+    out["gram_rel_err"] = float(((G - ref).abs().max() / ref.abs().max()).item())
     dist = torch.empty(n, dtype=torch.float64, device="cuda")
     cdf = torch.empty(n, dtype=torch.float64, device="cuda")
     mass = torch.empty(1, dtype=torch.float64, device="cuda")
