@@ -54,6 +54,16 @@ constexpr int32_t kMaxRun = 256;
 #define RCP_WALK_MIN_BLOCKS 2
 #endif
 constexpr int kWalkUnroll = RCP_WALK_UNROLL;
+// Diagnostics (per-level finish times, sample counters): off in the product build, where
+// they cost same-address global atomics per sample, run and CTA; tools/lab/walk_trace.py
+// builds with -DRCP_WALK_PROF=1.
+#ifndef RCP_WALK_PROF
+#ifdef RCP_WALK_TRACE
+#define RCP_WALK_PROF 1
+#else
+#define RCP_WALK_PROF 0
+#endif
+#endif
 constexpr int kWalkWarps = 16;
 constexpr int kMaxDepth = 30;   // local tree depth limit (2^30 leaves)
 // control words: [0] seeded runs, [2] samples finished, [3] participants,
@@ -197,7 +207,9 @@ __global__ void walk_seed_kernel(const int64_t *__restrict__ key, const int32_t 
   if (s >= J) return;
   const int64_t k = key[s];
   if (k == INT64_MAX) return;
+#if RCP_WALK_PROF
   atomicAdd(&ctl[3], 1);
+#endif
   if (s > 0 && key[s - 1] == k) return;
   int64_t lo = s + 1, hi = J;   // first position with a larger key
   while (lo < hi) {
@@ -376,7 +388,9 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
   // l + 1 through that level's own counter, whose value is stable after the grid barrier.
   __shared__ int claim;
   __shared__ Stage stg;
+#if RCP_WALK_PROF
   __shared__ unsigned long long fin_last, fin_first_inv;   // this CTA's warps, this level
+#endif
 #ifdef RCP_WALK_TRACE
   __shared__ unsigned long long ph_max[4];
   auto gtime = []() {
@@ -393,8 +407,10 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
     // by one by its warps
     if (threadIdx.x == 0) {
       claim = 0;
+#if RCP_WALK_PROF
       fin_last = 0ull;
       fin_first_inv = 0ull;
+#endif
 #ifdef RCP_WALK_TRACE
       ph_max[0] = ph_max[1] = ph_max[2] = ph_max[3] = 0ull;
 #endif
@@ -411,12 +427,14 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
       if (lane == 0) tc = atomicAdd(&claim, 1);
       const int64_t t = begin + blockIdx.x + (int64_t)__shfl_sync(0xffffffffu, tc, 0) * gridDim.x;
       if (t >= end) {
+#if RCP_WALK_PROF
         if (lane == 0) {   // this warp's finish time for the per-level record
           unsigned long long tnow;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
           atomicMax(&fin_last, tnow);
           atomicMax(&fin_first_inv, ~tnow);
         }
+#endif
         break;
       }
 #ifdef RCP_WALK_TRACE
@@ -613,9 +631,12 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         }
         __syncwarp();
       }
+#if RCP_WALK_PROF
       if (lane == 0) atomicAdd(&ctl[2], hi - lo);
+#endif
     }
     publish_children(runs, gen_cnt, end, cap_runs, status, stg);
+#if RCP_WALK_PROF
     if (threadIdx.x == 0) {   // (publish_children synchronised the CTA)
       atomicMax(&prof[2 * (kMaxDepth + 2) + 2 * lvl], fin_last);
       atomicMax(&prof[2 * (kMaxDepth + 2) + 2 * lvl + 1], fin_first_inv);
@@ -623,6 +644,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
       for (int q = 0; q < 4; ++q) atomicMax(&prof[4 * (kMaxDepth + 2) + 4 * lvl + q], ph_max[q]);
 #endif
     }
+#endif
     grid.sync();
     const int64_t pushed_n = ld_volatile(gen_cnt);
     begin = end;

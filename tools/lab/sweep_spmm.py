@@ -61,7 +61,10 @@ def main():
     build_only = "--build-only" in sys.argv
     if build_only:
         sys.argv.remove("--build-only")
-    if len(sys.argv) > 1 and sys.argv[1] == "walk":
+    if len(sys.argv) > 1 and sys.argv[1] == "prof":
+        variants["prof0"] = {"RCP_WALK_PROF": 0}
+        variants["prof1"] = {"RCP_WALK_PROF": 1}
+    elif len(sys.argv) > 1 and sys.argv[1] == "walk":
         for u in (4, 8, 10):
             for mb in (1, 2):
                 variants["u%d_mb%d" % (u, mb)] = {"RCP_WALK_UNROLL": u, "RCP_WALK_MIN_BLOCKS": mb}

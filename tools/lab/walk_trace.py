@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tools", "lab"))
 import sweep_spmm  # noqa: E402
 
-so = sweep_spmm.build("trace", {"RCP_WALK_TRACE": 1})
+so = sweep_spmm.build("trace", {"RCP_WALK_TRACE": 1, "RCP_WALK_PROF": 1})
 from paper_2210_05105_b200 import _lib  # noqa: E402
 _lib.load(so)
 import bench  # noqa: E402
