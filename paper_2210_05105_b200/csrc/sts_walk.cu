@@ -64,7 +64,10 @@ constexpr int kWalkUnroll = RCP_WALK_UNROLL;
 #define RCP_WALK_PROF 0
 #endif
 #endif
-constexpr int kWalkWarps = 16;
+#ifndef RCP_WALK_WARPS
+#define RCP_WALK_WARPS 16
+#endif
+constexpr int kWalkWarps = RCP_WALK_WARPS;
 constexpr int kMaxDepth = 30;   // local tree depth limit (2^30 leaves)
 // control words: [0] seeded runs, [2] samples finished, [3] participants,
 // [kGenBase + g] runs pushed during generation g (each generation has its own counter, so

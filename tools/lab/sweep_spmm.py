@@ -61,7 +61,10 @@ def main():
     build_only = "--build-only" in sys.argv
     if build_only:
         sys.argv.remove("--build-only")
-    if len(sys.argv) > 1 and sys.argv[1] == "prof":
+    if len(sys.argv) > 1 and sys.argv[1] == "warps":
+        for w, mb in ((16, 2), (12, 2), (8, 3), (8, 2)):
+            variants["w%d_mb%d" % (w, mb)] = {"RCP_WALK_WARPS": w, "RCP_WALK_MIN_BLOCKS": mb}
+    elif len(sys.argv) > 1 and sys.argv[1] == "prof":
         variants["prof0"] = {"RCP_WALK_PROF": 0}
         variants["prof1"] = {"RCP_WALK_PROF": 1}
     elif len(sys.argv) > 1 and sys.argv[1] == "walk":
