@@ -549,7 +549,10 @@ cta_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__
 //     instead of one per row — as {row, fiber, value};
 //  B. one CTA per bucket orders its range by row in place of the final array (the range,
 //     ~1/256 of the entries, stays L2-resident while its rows' cursors advance).
-constexpr int kBucketMax = 512;        // buckets of the small-row (CTA-histogram) path
+#ifndef RCP_BUCKET_MAX
+#define RCP_BUCKET_MAX 512   // <= kBigBucketMax (bucket_scatter's shared cursors, bofs)
+#endif
+constexpr int kBucketMax = RCP_BUCKET_MAX;   // buckets of the small-row (CTA-histogram) path
 constexpr int kBigBucketMax = 2048;    // buckets of the large-row path (<= 2^14 rows each)
 constexpr int kBigMaxShift = 14;
 #ifndef RCP_BUCKET_MIN_ROWS

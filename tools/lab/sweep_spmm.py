@@ -61,7 +61,10 @@ def main():
     build_only = "--build-only" in sys.argv
     if build_only:
         sys.argv.remove("--build-only")
-    if len(sys.argv) > 1 and sys.argv[1] == "warps":
+    if len(sys.argv) > 1 and sys.argv[1] == "buckets":
+        for nb in (128, 256, 512, 1024, 2048):
+            variants["b%d" % nb] = {"RCP_BUCKET_MAX": nb}
+    elif len(sys.argv) > 1 and sys.argv[1] == "warps":
         for w, mb in ((16, 2), (12, 2), (8, 3), (8, 2)):
             variants["w%d_mb%d" % (w, mb)] = {"RCP_WALK_WARPS": w, "RCP_WALK_MIN_BLOCKS": mb}
     elif len(sys.argv) > 1 and sys.argv[1] == "prof":
