@@ -142,7 +142,7 @@ def run_als(cfg: AlsConfig, tensor=None, perms=None, grid=None, partition=None,
     sigma = sigma0
     for rnd in range(1, cfg.rounds + 1):
         for k in range(N):
-            cl.solve(k, rnd)
+            cl.solve(k, rnd, check=True)
             cl.check("after round %d mode %d solve" % (rnd, k))
             if cfg.record_samples:
                 sample_log.append(to_host(cl.ranks[0].X.T.contiguous()))

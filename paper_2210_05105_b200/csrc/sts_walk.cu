@@ -349,9 +349,18 @@ __device__ __forceinline__ void publish_children(Run *runs, int *gen_cnt, int64_
   if (threadIdx.x == 0) stg.count = 0;
 }
 
+// A degenerate run (zero node or leaf mass: ref DegenerateWalkError samplers.py:428-430)
+// marks its samples' indices -1 and zeroes their Hadamard output rows, so nothing after
+// it in the solve reads unset memory; the status flag is raised for the host.
 __device__ __forceinline__ void fail_run(int32_t lo, int32_t hi, const int32_t *__restrict__ idx,
-                                         int64_t *__restrict__ Xi, int *status, int *ctl, int lane) {
+                                         int64_t *__restrict__ Xi, double *__restrict__ Hout,
+                                         int R, int *status, int *ctl, int lane) {
   for (int32_t s = lo + lane; s < hi; s += 32) Xi[idx[s]] = -1;
+  if (Hout)
+    for (int32_t s = lo; s < hi; ++s) {
+      double *dst = Hout + (int64_t)idx[s] * R;
+      for (int c = lane; c < R; c += 32) dst[c] = 0.0;
+    }
   __syncwarp();
   if (lane == 0) {
     raise_status(status, RCP_ST_DEGENERATE);
@@ -500,7 +509,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
 #endif
         const double qnode = known ? run.qv : warp_sum(qV + qV2);
         if (!(qnode > 0.0)) {
-          fail_run(lo, hi, is, Xi, status, ctl, lane);
+          fail_run(lo, hi, is, Xi, Hout, R, status, ctl, lane);
           continue;
         }
         double T = (qL > 0.0 ? qL : 0.0) / qnode;
@@ -595,7 +604,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         bad = !(total_m > 0.0);
       }
       if (bad) {
-        fail_run(lo, hi, is, Xi, status, ctl, lane);
+        fail_run(lo, hi, is, Xi, Hout, R, status, ctl, lane);
         continue;
       }
       // blocks of kLeafChunk samples: lanes pick rows, then (optionally) the warp writes the

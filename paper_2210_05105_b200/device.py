@@ -7,9 +7,17 @@ no CUDA device is visible.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
+
+# Debug: RCP_POISON=1 fills every uninitialised device allocation of the package (and the
+# allocator's cached blocks, see poison_allocator) with 0xFF bytes -- NaN as fp64, -1 as
+# integers -- so a kernel that reads memory it never wrote fails deterministically instead
+# of depending on what the previous user of that memory left there.
+POISON = os.environ.get("RCP_POISON", "") == "1"
 
 _torch = None
 
@@ -47,10 +55,34 @@ def stream_handle():
     return torch().cuda.current_stream().cuda_stream
 
 
+def empty(shape, dtype, dev):
+    """Uninitialised device tensor (0xFF-filled under RCP_POISON=1)."""
+    t = torch()
+    x = t.empty(shape, dtype=dtype, device=dev)
+    if POISON:
+        x.view(t.uint8).fill_(0xFF) if x.numel() else None
+    return x
+
+
+def poison_allocator(dev, large_gb=8, small_mb=512):
+    """Fill a large block and many small blocks of the caching allocator with 0xFF and
+    release them: later torch.empty() calls are carved from poisoned memory."""
+    t = torch()
+    big = t.empty(int(large_gb * (1 << 30)), dtype=t.uint8, device=dev)
+    big.fill_(0xFF)
+    smalls = []
+    for _ in range(max(1, (small_mb << 20) >> 19)):   # 512 KB blocks: the small pool
+        x = t.empty(1 << 19, dtype=t.uint8, device=dev)
+        x.fill_(0xFF)
+        smalls.append(x)
+    t.cuda.synchronize()
+    del big, smalls
+
+
 def f64(shape, dev, fill=None):
     t = torch()
     if fill is None:
-        return t.empty(shape, dtype=t.float64, device=dev)
+        return empty(shape, t.float64, dev)
     return t.full(shape, float(fill), dtype=t.float64, device=dev)
 
 
@@ -87,23 +119,30 @@ class Status:
     def clear_flag(self, flag):
         self.buf.bitwise_and_(~int(flag))
 
+    # Causal order: a flag raised upstream (sampler, workspace) explains everything the
+    # same solve computed after it, so it is reported before the downstream ones (a
+    # degenerate walk leaves its samples' rows unset, which the update then sees as
+    # non-finite factors).  The raw word is part of every message.
+    _ORDER = (
+        ("ST_CAPACITY", RuntimeError, "sampled-MTTKRP workspace too small"),
+        ("ST_TIMEOUT", RuntimeError, "device work queue watchdog expired"),
+        ("ST_ASYMMETRIC", ValueError, "matrix is not symmetric"),
+        ("ST_ZERO_MASS", ValueError, "zero total leverage mass; nothing to sample from"),
+        ("ST_DEGENERATE", DegenerateWalkError, "zero-mass node in leverage tree walk"),
+        ("ST_ZERO_PROB", ValueError, "sample with zero probability cannot have been drawn"),
+        ("ST_NONFINITE", FloatingPointError, "non-finite factor entries"),
+    )
+
+    def peek(self):
+        return int(self.buf.item())
+
     def check(self, where=""):
         v = int(self.buf.item())
         if not v:
             return
         self.buf.zero_()
-        if v & _lib.ST_NONFINITE:
-            raise FloatingPointError("non-finite factor entries %s" % where)
-        if v & _lib.ST_DEGENERATE:
-            raise DegenerateWalkError("zero-mass node in leverage tree walk %s" % where)
-        if v & _lib.ST_ASYMMETRIC:
-            raise ValueError("matrix is not symmetric %s" % where)
-        if v & _lib.ST_ZERO_MASS:
-            raise ValueError("zero total leverage mass; nothing to sample from %s" % where)
-        if v & _lib.ST_ZERO_PROB:
-            raise ValueError("sample with zero probability cannot have been drawn %s" % where)
-        if v & _lib.ST_TIMEOUT:
-            raise RuntimeError("device work queue watchdog expired %s" % where)
-        if v & _lib.ST_CAPACITY:
-            raise RuntimeError("sampled-MTTKRP workspace too small %s" % where)
+        flags = [name for name, _, _ in self._ORDER if v & getattr(_lib, name)]
+        for name, exc, msg in self._ORDER:
+            if v & getattr(_lib, name):
+                raise exc("%s %s (device status 0x%x: %s)" % (msg, where, v, "|".join(flags)))
         raise RuntimeError("device status 0x%x %s" % (v, where))

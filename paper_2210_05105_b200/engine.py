@@ -174,7 +174,7 @@ class RankState:
         self.w = t.ones(J, **f64)
         self.resid = t.zeros(J, **f64)
         self.H = t.ones((J, R), **f64)
-        self.H_alt = t.empty((J, R), **f64)      # walk output buffer (swapped with H)
+        self.H_alt = t.zeros((J, R), **f64)      # walk output buffer (swapped with H)
         self.urow = t.zeros((J, R), **f64)
         self.owner = t.zeros(J, dtype=t.int32, device=dev)
         self.rtop = t.zeros(J, **f64)
@@ -576,7 +576,10 @@ class Cluster:
         e.record()
         self.phase_events.append((phase, e))
 
-    def solve(self, k, rnd, override=None, injected=None):
+    def solve(self, k, rnd, override=None, injected=None, check=False):
+        """One mode-k solve.  check=True synchronises after the sampler and raises its
+        errors there, where the reference raises them (ref samplers.py:34-35,93-94,
+        142-143): not usable inside a CUDA-graph capture."""
         t0 = time.perf_counter()
         self._ev("sampling")
         if injected is None:
@@ -584,6 +587,8 @@ class Cluster:
         else:
             for r in self.ranks:
                 injected(r)
+        if check:
+            self.check("after round %d mode %d sampling" % (rnd, k))
         t0 = self._tick("sampling", t0)
         # Gs = (H w)^T (H w) and its pseudo-inverse depend only on the batch: they run on a
         # side stream, overlapped with the sampled MTTKRP, and join before the update

@@ -6,7 +6,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from .device import Status, ptr, stream_handle, torch
+from .device import Status, empty, ptr, stream_handle, torch
 
 CUTOFF = 1e-10   # ref linalg.py:16
 
@@ -32,7 +32,7 @@ class Ops:
         nbytes = max(int(nbytes), 256)
         buf = self._ws.get(name)
         if buf is None or buf.numel() < nbytes:
-            buf = t.empty(nbytes, dtype=t.uint8, device=self.dev)
+            buf = empty(nbytes, t.uint8, self.dev)
             self._ws[name] = buf
         return buf
 
@@ -46,7 +46,7 @@ class Ops:
         t = torch()
         n, R = U.shape
         if out is None:
-            out = t.empty((R, R), dtype=t.float64, device=self.dev)
+            out = empty((R, R), t.float64, self.dev)
         w = self.ws("gram", self.lib.rcp_gram_ws_bytes(n, R))
         self._c("rcp_gram", ptr(U), ptr(scale), n, R, ptr(out), ptr(w), stream_handle())
         return out
@@ -55,7 +55,7 @@ class Ops:
         t = torch()
         R = G.shape[-1]
         if out is None:
-            out = t.empty((R, R), dtype=t.float64, device=self.dev)
+            out = empty((R, R), t.float64, self.dev)
         self._c("rcp_pinv", ptr(G), int(n_chain), int(skip), int(R), float(cutoff),
                 ptr(chain_out), ptr(out), self.status.ptr, stream_handle())
         return out
@@ -109,7 +109,7 @@ class Ops:
         n, R = U.shape
         nd = int(self.lib.rcp_sts_tree_doubles(n, int(leaf), R))
         if tree is None or tree.numel() < nd:
-            tree = t.empty(max(nd, 1), dtype=t.float64, device=self.dev)
+            tree = empty(max(nd, 1), t.float64, self.dev)
         self._c("rcp_sts_build", ptr(U), n, R, int(leaf), ptr(tree), stream_handle())
         return tree
 

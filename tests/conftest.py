@@ -29,3 +29,14 @@ def cuda_ok():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _poisoned_device_memory():
+    """RCP_POISON=1: start the session with the caching allocator's blocks full of 0xFF
+    (NaN as fp64), so reads of never-written device memory fail every time."""
+    if os.environ.get("RCP_POISON", "") == "1" and cuda_ok():
+        import torch
+        from paper_2210_05105_b200.device import poison_allocator
+        poison_allocator(torch.device("cuda", 0))
+    yield
