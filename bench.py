@@ -443,14 +443,70 @@ def oracle_store_from_device(st):
     return s
 
 
+def host_info():
+    """CPU model, cores, RAM, numpy and BLAS versions of this host."""
+    info = {"cpu_count": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        with open("/proc/meminfo") as f:
+            kb = int(f.readline().split()[1])
+        info["ram_gb"] = round(kb / 2 ** 20, 1)
+    except (OSError, ValueError, IndexError):
+        pass
+    info["numpy"] = np.__version__
+    try:
+        from threadpoolctl import threadpool_info
+        info["blas"] = ["%s %s (%s threads)" % (p.get("internal_api"), p.get("version"),
+                                                p.get("num_threads"))
+                        for p in threadpool_info() if p.get("user_api") == "blas"]
+    except Exception:   # pragma: no cover - informational only
+        pass
+    info["threads_env"] = {k: os.environ[k] for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS")
+                           if k in os.environ}
+    return info
+
+
+def reference_tensor(args, c):
+    """The workload's tensor for the reference arm, without this repo's CUDA library:
+    the same seeded Zipf draws (torch, on the GPU when present, else the host) and the
+    reference's own permutation streams (numpy Philox, ref rng.py:26-32, tensor.py:207-210)
+    through the oracle."""
+    import torch
+    from oracle import randcp_oracle as O
+    from paper_2210_05105_b200 import synth
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    if c["kind"] == "planted":
+        idx, vals = synth.planted_c1(seed=args.seed)
+        return np.asarray(idx), np.asarray(vals)
+    idx, vals = synth.zipf_tensor(c["dims"], c["nnz"], c["s"], seed=args.seed, values=c["values"],
+                                  sigma=c.get("sigma", 1.0), device=dev)
+    idx = idx.cpu().numpy()
+    vals = vals.cpu().numpy()
+    for j, d in enumerate(c["dims"]):
+        perm = O.stream(args.seed, O.P_TENSOR_PERM, j).permutation(d)
+        idx[:, j] = perm[idx[:, j]]
+    return idx, vals
+
+
 def run_reference(args):
-    """`--impl reference`: the reference's own algorithm on host cores (oracle port,
-    numpy), same config/metric; each step = one bounded solve sample."""
+    """`--impl reference`: the reference's own algorithm (the oracle port, numpy on all
+    host cores; the reference is pure Python, so nothing compiles into oracle/_ref) on the
+    same config and metric.  Each step is one ALS round over all N modes restricted to a
+    bounded number of samples per solve: sampler + gather + downsampled MTTKRP + sketched
+    solve timed (ref schedules.py:227-258), factor update + sampler-state rebuild untimed.
+    It never loads this repo's CUDA library: state comes from the reference's init_factors
+    on the host."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch
     from oracle import randcp_oracle as O
     from paper_2210_05105_b200 import synth
     c = synth.CONFIGS[args.config]
@@ -460,76 +516,75 @@ def run_reference(args):
                           "per mode, >300 GB) exceeds the host; SURVEY.md 8(d)" % args.config}),
               flush=True)
         return
-    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
-    c, idx_d, vals_d = make_tensor(args.config, args.seed, dev)   # input generation only
     dims = c["dims"]
     R = args.rank or c["R"]
     J = args.samples or c["J"]
     N = len(dims)
-    k = N - 1
-    # Input state: the factors our timed rounds start from (after `warmup` ALS rounds),
-    # prepared on the GPU only to keep setup within minutes (the reference needs minutes
-    # per round at this size).  The timed path below is the reference algorithm alone.
-    state = "reference init_factors (no GPU for state preparation)"
-    factors = None
-    if dev.type == "cuda":
-        from paper_2210_05105_b200.als import gather_factors
-        from paper_2210_05105_b200.engine import make_local_cluster
-        cl = make_local_cluster(dims, idx_d, vals_d, R, J, args.sampler, args.seed, leaf=args.leaf)
-        for rnd in range(1, args.warmup + 1):
-            cl.round(rnd)
-        factors = gather_factors(cl)
-        state = "factors after %d ALS rounds (state prepared on the GPU, untimed)" % args.warmup
-        del cl
-    idx = idx_d.cpu().numpy()
-    vals = vals_d.cpu().numpy()
-    del idx_d, vals_d
-    samples = args.cpu_samples or min(J, 2048)
+    samples = args.cpu_samples or min(J, 1024)
     workers = os.cpu_count() or 1
     t0 = time.perf_counter()
-    store = O.Store(dims, idx, vals, k)
-    if factors is None:
-        factors, _ = O.init_factors(dims, R, args.seed)
-    blocks = [[U] for U in factors]
-    grams = [O.gram_blocks(b) for b in blocks]
-    if args.sampler == "sts":
-        trees = [O.tree_build(blocks[j], [0]) for j in range(N)]
-    else:
-        levs = [O.lev_build(blocks[j], [0]) for j in range(N)]
+    idx, vals = reference_tensor(args, c)
+    gen_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    stores = [O.Store(dims, idx, vals, k) for k in range(N)]
+    factors, _ = O.init_factors(dims, R, args.seed)
+    factors = [np.array(U) for U in factors]
+
+    def rebuild(j):
+        blocks = [[factors[j]]]
+        grams[j] = O.gram_blocks(blocks[0])
+        if args.sampler == "sts":
+            state[j] = O.tree_build(blocks[0], [0])
+        else:
+            state[j] = O.lev_build(blocks[0], [0])
+
+    grams = [None] * N
+    state = [None] * N
+    for j in range(N):
+        rebuild(j)
     setup = time.perf_counter() - t0
     total_nnz, total_t = 0, 0.0
     for step in range(args.warmup + args.steps):
-        ts = time.perf_counter()
-        if args.sampler == "sts":
-            cp = O.sym_pinv(O.hadamard_chain(grams, skip=k))
-            b = O.tree_sample(trees, k, samples, cp, grams, blocks, args.seed,
-                                args.warmup + 1 + step)
-        else:
-            b = O.lev_sample(levs, k, samples, factors, args.seed, args.warmup + 1 + step)
-        w = O.weights_for(b.prob, samples)
-        csr = O.sampled_csr(store, b.X, k)
-        out = O.sketched_mttkrp(csr, b.H, w, workers=workers)
-        Hw = b.H * w[:, None]
-        newU = out @ O.sym_pinv(Hw.T @ Hw)
-        dt = time.perf_counter() - ts
-        if step >= args.warmup:
-            total_nnz += csr.nnz
-            total_t += dt
-        del newU
+        rnd = 1 + step
+        for k in range(N):
+            ts = time.perf_counter()
+            if args.sampler == "sts":
+                cp = O.sym_pinv(O.hadamard_chain(grams, skip=k))
+                b = O.tree_sample(state, k, samples, cp, grams, [[U] for U in factors], args.seed, rnd)
+            else:
+                b = O.lev_sample(state, k, samples, factors, args.seed, rnd)
+            w = O.weights_for(b.prob, samples)
+            csr = O.sampled_csr(stores[k], b.X, k)
+            out = O.sketched_mttkrp(csr, b.H, w, workers=workers)
+            Hw = b.H * w[:, None]
+            newU = out @ O.sym_pinv(Hw.T @ Hw)
+            dt = time.perf_counter() - ts
+            if step >= args.warmup:
+                total_nnz += csr.nnz
+                total_t += dt
+            norms = np.sqrt((newU * newU).sum(axis=0))     # ref als.py:129-138 (untimed)
+            norms[norms == 0] = 1.0
+            factors[k] = newU / norms
+            rebuild(k)
     value = total_nnz / total_t
+    hi = host_info()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "%s %s R=%d J=%d dims=%s" % (args.config, args.sampler, R, J,
-                                                               "x".join(map(str, dims))),
-                       "sampler": args.sampler, "rank": R, "samples_J": J,
+            "config": {"workload": "%s %s R=%d J=%d dims=%s nnz=%d" % (
+                           args.config, args.sampler, R, J, "x".join(map(str, dims)), len(vals)),
+                       "sampler": args.sampler, "rank": R, "samples_J": J, "modes": N,
                        "parallelism": "host"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                             "sample": "one mode-%d solve per step restricted to the first %d of "
-                                       "J=%d samples (sampler + gather + downsampled MTTKRP + "
-                                       "solve) from %s; oracle setup %.0f s untimed"
-                                       % (k, samples, J, state, setup)},
+                             "sample": "each step = one round over all %d modes with %d of J=%d "
+                                       "samples per solve (sampler + gather + downsampled MTTKRP + "
+                                       "sketched solve timed; factor update and sampler rebuild "
+                                       "untimed), from the reference's init_factors; tensor "
+                                       "generation %.0f s and the reference's per-mode store build "
+                                       "%.0f s untimed" % (N, samples, J, gen_s, setup),
+                             "host": hi},
+            "host": hi,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

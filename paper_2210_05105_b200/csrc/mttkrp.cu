@@ -16,6 +16,8 @@
 //  6. warp-per-chunk segmented reduction out[i,:] = sum val * Hs_d, plain stores for rows
 //     owned by one warp, fp64 red.add only for rows split across chunks.   [spmm]
 #include <limits.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -164,54 +166,6 @@ __global__ void hash_insert_kernel(const int64_t *__restrict__ X, int N, int64_t
       return;
     }
     h = (h + 1) & (uint64_t)tmask;
-  }
-}
-
-__global__ void compact_count_kernel(const int32_t *__restrict__ tcnt, int64_t T,
-                                     int64_t *__restrict__ bcnt) {
-  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
-  int f = (i < T && tcnt[i] > 0) ? 1 : 0;
-  f = __syncthreads_count(f);
-  if (threadIdx.x == 0) bcnt[blockIdx.x] = f;
-}
-
-__global__ void compact_write_kernel(const unsigned long long *__restrict__ tkey,
-                                     const int32_t *__restrict__ tcnt,
-                                     const int32_t *__restrict__ trep,
-                                     const unsigned long long *__restrict__ twmin,
-                                     const unsigned long long *__restrict__ twmax,
-                                     const double *__restrict__ twsum, int64_t T,
-                                     const int64_t *__restrict__ bcnt, int nb,
-                                     int64_t *__restrict__ dkey, int32_t *__restrict__ dcnt,
-                                     int32_t *__restrict__ drep, double *__restrict__ dsc,
-                                     int64_t *__restrict__ S) {
-  __shared__ int64_t base;
-  __shared__ int wsum[32];
-  if (threadIdx.x == 0) {
-    int64_t b = 0, tot = 0;
-    for (int j = 0; j < nb; ++j) {
-      if (j < (int)blockIdx.x) b += bcnt[j];
-      tot += bcnt[j];
-    }
-    base = b;
-    if (blockIdx.x == 0) S[0] = tot;
-  }
-  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
-  const int f = (i < T && tcnt[i] > 0) ? 1 : 0;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const unsigned bal = __ballot_sync(0xffffffffu, f);
-  const int pre = __popc(bal & ((1u << lane) - 1u));
-  if (lane == 0) wsum[wid] = __popc(bal);
-  __syncthreads();
-  int woff = 0;
-  for (int w = 0; w < wid; ++w) woff += wsum[w];
-  if (f) {
-    const int64_t o = base + woff + pre;
-    dkey[o] = (int64_t)tkey[i];
-    dcnt[o] = tcnt[i];
-    drep[o] = trep[i];
-    dsc[o] = twmin[i] == twmax[i] ? (double)tcnt[i] * __longlong_as_double((long long)twmin[i])
-                                  : twsum[i];
   }
 }
 
@@ -1076,6 +1030,8 @@ __global__ void fiber_expand_kernel(const int64_t *__restrict__ lo, const int64_
   }
 }
 
+#include "mttkrp_tiles.cuh"
+
 // ------------------------------------------------------------ workspace layout
 struct Ws {
   size_t off[32];
@@ -1094,7 +1050,7 @@ struct MttkrpLayout {
   size_t o_tkey, o_tcnt, o_trep, o_twmin, o_twmax, o_twsum, o_dsc, o_bcnt, o_dkey, o_dcnt,
       o_drep, o_dlo, o_dlen, o_doff, o_ioff, o_ifib, o_Hs, o_scan, o_rcnt, o_rptr, o_cmat,
       o_ent, o_tmp, o_bofs, o_S,
-      o_nnz;
+      o_nnz, o_flag, o_fpos, o_sslot, o_uoff, o_sbase, o_tdone, o_tmask;
   size_t total;
   MttkrpLayout(int64_t J, int64_t cap, int64_t n_rows, int R) {
     T = 1024;
@@ -1128,6 +1084,13 @@ struct MttkrpLayout {
     o_bofs = w.add(sizeof(int64_t) * ((size_t)sm_count() + 1) * (kBigBucketMax + 1));
     o_S = w.add(sizeof(int64_t) * 4);
     o_nnz = w.add(sizeof(int64_t) * 4);
+    o_flag = w.add(sizeof(int64_t) * (J + 1));
+    o_fpos = w.add(sizeof(int64_t) * (J + 2));
+    o_sslot = w.add(sizeof(int32_t) * (J + 1));
+    o_uoff = w.add(sizeof(int32_t) * (kTileMaxTiles + 2));
+    o_sbase = w.add(sizeof(int32_t) * (kTileMaxTiles + 1));
+    o_tdone = w.add(sizeof(int32_t) * kTileMaxTiles);
+    o_tmask = w.add(sizeof(uint32_t) * kTileMaxTiles);
     total = w.total + 256;
   }
 };
@@ -1205,22 +1168,39 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   for (int m = 0; m < kMaxModes; ++m) sd.s[m] = m < N ? h_strides[m] : 0;
 
   // 1. dedup
+  // The row-tile path (row tiles fit one scan, < 2^22 samples) writes every output row
+  // itself; the row-transpose path (large row counts, or RCP_MTTKRP_PATH=rows) zeroes first.
+  static const int force_rows = [] {
+    const char *e = getenv("RCP_MTTKRP_PATH");
+    return e && !strcmp(e, "tiles") ? 0 : 1;
+  }();
+  const int tile_np = R <= 64 ? 1 : 2;
+  const int tile_ts = tile_np == 1 ? 4 : 3;
+  const int64_t n_tiles = ceil_div(n_rows, (int64_t)1 << tile_ts);
+  const bool tiles = !force_rows && n_tiles <= kTileMaxTiles && J < (1LL << 22) &&
+                     cap < (1LL << 31) && sm_count() <= kPrefixSeg * kPrefixMaxPer;
 
   unsigned long long *twmin = (unsigned long long *)P(L.o_twmin);
   unsigned long long *twmax = (unsigned long long *)P(L.o_twmax);
   double *twsum = (double *)P(L.o_twsum), *dsc = (double *)P(L.o_dsc);
-  mttkrp_init_kernel<<<4 * sm_count(), 256, 0, st>>>(d_out, n_rows * (int64_t)R, L.T, tkey, tcnt,
-                                                      trep, twmin, twmax, twsum);
+  mttkrp_init_kernel<<<4 * sm_count(), 256, 0, st>>>(d_out, tiles ? 0 : n_rows * (int64_t)R, L.T, tkey,
+                                                      tcnt, trep, twmin, twmax, twsum);
   RCP_LAUNCH_CHECK("mttkrp_init");
   hash_insert_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(
       d_X, N, J, k, sd, L.T - 1, d_w, tkey, tcnt, trep, twmin, twmax, twsum);
   RCP_LAUNCH_CHECK("hash_insert");
-  const int nb = (int)(L.T / 1024);
-  compact_count_kernel<<<nb, 1024, 0, st>>>(tcnt, L.T, bcnt);
-  RCP_LAUNCH_CHECK("compact_count");
-  compact_write_kernel<<<nb, 1024, 0, st>>>(tkey, tcnt, trep, twmin, twmax, twsum, L.T, bcnt, nb,
-                                            dkey, dcnt, drep, dsc, S);
-  RCP_LAUNCH_CHECK("compact_write");
+  {   // distinct fibers numbered in representative-sample order (deterministic)
+    int64_t *flag = (int64_t *)P(L.o_flag), *fpos = (int64_t *)P(L.o_fpos);
+    int32_t *sslot = (int32_t *)P(L.o_sslot);
+    rep_flag_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(d_X, N, J, k, sd, L.T - 1, tkey, trep,
+                                                                flag, sslot);
+    RCP_LAUNCH_CHECK("rep_flag");
+    int rc0 = scan_i64_exclusive(flag, fpos, J, nullptr, P(L.o_scan), st);
+    if (rc0) return rc0;
+    rep_compact_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(flag, fpos, J, sslot, tkey, tcnt, twmin,
+                                                                   twmax, twsum, dkey, dcnt, drep, dsc, S);
+    RCP_LAUNCH_CHECK("rep_compact");
+  }
   // 2. lookup + scaled KRP rows
   lookup_kernel<<<(unsigned)std::min<int64_t>(ceil_div(J * 32, 256), 8LL * sm_count()), 256, 0, st>>>(
       d_keys, n_cols, d_colptr, dkey, dcnt, drep, S, d_H, dsc, R, hs_stride(R), dlo, dlen, Hs,
@@ -1239,6 +1219,54 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   int32_t *ifib = (int32_t *)P(L.o_ifib);
   item_fill_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(ioff, S, ifib);
   RCP_LAUNCH_CHECK("item_fill");
+  if (tiles) {
+    const int grid = sm_count();
+    const int nt = (int)n_tiles;
+    int32_t *cmat = (int32_t *)P(L.o_cmat);            // grid x n_tiles
+    int64_t *tcntp = rcnt, *tptr = rptr;                // pairs per tile, tile pointers
+    uint64_t *pairs = (uint64_t *)P(L.o_ent);           // <= entries <= cap pairs
+    double2 *scratch = (double2 *)P(L.o_tmp);           // <= 2 cap / kTilePart parts of 8 KB
+    int32_t *uoff = (int32_t *)P(L.o_uoff), *sbase = (int32_t *)P(L.o_sbase);
+    int32_t *tdone = (int32_t *)P(L.o_tdone);
+    uint32_t *tmask = (uint32_t *)P(L.o_tmask);
+    static bool tattr = false;
+    if (!tattr) {
+      const int scat = (int)pair_scatter_smem(kTileMaxTiles);
+      RCP_CUDA_TRY(cudaFuncSetAttribute(pair_scatter_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, scat));
+      RCP_CUDA_TRY(cudaFuncSetAttribute(pair_scatter_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, scat));
+      RCP_CUDA_TRY(cudaFuncSetAttribute(tile_spmm_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)tile_spmm_smem<4, 1>()));
+      RCP_CUDA_TRY(cudaFuncSetAttribute(tile_spmm_kernel<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)tile_spmm_smem<3, 2>()));
+      tattr = true;
+    }
+    RCP_CUDA_TRY(cudaMemsetAsync(tdone, 0, sizeof(int32_t) * kTileMaxTiles, st));
+    RCP_CUDA_TRY(cudaMemsetAsync(tmask, 0, sizeof(uint32_t) * kTileMaxTiles, st));
+    const size_t hsm = sizeof(int32_t) * nt;
+    if (tile_ts == 4) tile_hist_kernel<4><<<grid, kTraverseThreads, hsm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, cmat);
+    else tile_hist_kernel<3><<<grid, kTraverseThreads, hsm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, cmat);
+    RCP_LAUNCH_CHECK("tile_hist");
+    cta_prefix_kernel<<<(unsigned)ceil_div(nt, kPrefixRows), kPrefixRows * kPrefixSeg, 0, st>>>(
+        cmat, grid, nt, tcntp);
+    RCP_LAUNCH_CHECK("cta_prefix");
+    rc = scan_i64_exclusive(tcntp, tptr, nt, nullptr, scan_ws, st);
+    if (rc) return rc;
+    const size_t ssm = pair_scatter_smem(nt);
+    if (tile_ts == 4) pair_scatter_kernel<4><<<grid, kTraverseThreads, ssm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, tptr, cmat, pairs);
+    else pair_scatter_kernel<3><<<grid, kTraverseThreads, ssm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, tptr, cmat, pairs);
+    RCP_LAUNCH_CHECK("pair_scatter");
+    tile_units_kernel<<<1, 1024, 0, st>>>(tcntp, nt, uoff, sbase);
+    RCP_LAUNCH_CHECK("tile_units");
+    const unsigned sg = (unsigned)(2 * sm_count());
+    if (tile_np == 1)
+      tile_spmm_kernel<4, 1><<<sg, kTileWarps * 32, tile_spmm_smem<4, 1>(), st>>>(tptr, nt, n_rows, uoff, sbase, pairs, d_rows, d_vals,
+                                                              Hs, R, d_out, scratch, tdone, tmask, d_stats);
+    else
+      tile_spmm_kernel<3, 2><<<sg, kTileWarps * 32, tile_spmm_smem<3, 2>(), st>>>(tptr, nt, n_rows, uoff, sbase, pairs, d_rows, d_vals,
+                                                              Hs, R, d_out, scratch, tdone, tmask, d_stats);
+    RCP_LAUNCH_CHECK("tile_spmm");
+    return RCP_OK;
+  }
   // 4. row histogram -> row pointers; 5. scatter into row order (packed entries)
   const int priv =
       (n_rows <= kPrivRows && cap < (1LL << 31) && sm_count() <= kPrefixSeg * kPrefixMaxPer) ? 1 : 0;

@@ -1,0 +1,525 @@
+// Row-tile x fiber sampled MTTKRP (included by mttkrp.cu inside its anonymous namespace).
+//
+// The mode-k store is column-major (CSC analogue, ref matricization.py:67-128): the entries
+// of one fiber are contiguous and their rows ascend.  Cutting the output rows into tiles of
+// TR = 2^TS rows, the entries of a sampled fiber that fall in one tile are therefore one
+// contiguous run of at most TR entries — a "pair" (tile, fiber).  Instead of transposing
+// every gathered entry into row order (the reference's sparse transpose,
+// mttkrp.py:131-155), this path moves only the pairs (8 bytes each, ~2-3 entries per pair at
+// C3), and reads the entries straight from the store:
+//
+//   pass 1  tile_hist      per CTA, pairs per tile (CTA-private shared-memory histogram)
+//   prefix  cta_prefix     per tile, exclusive prefix over CTAs + tile totals -> tptr
+//   pass 2  pair_scatter   pairs written to their tile's range in a deterministic order
+//   units   tile_units     tiles cut into parts of <= kTilePart pairs
+//   spmm    tile_spmm      per part: 8 warps split its pairs; each warp keeps the tile's TR
+//                          output rows in registers, loads the fiber's scaled KRP row Hs_d
+//                          ONCE per pair and applies every entry of the pair to it
+//                          (row selected by a warp-uniform switch); warps and parts are
+//                          combined in a fixed order (no atomics on the output)
+//
+// Every order is a function of the input only, so results are bit-reproducible run to run
+// (ref tests/test_mttkrp.py:60-67,163-172 require bit-identity across worker counts).
+// Pair record: store position (36 bits) | count - 1 (6 bits) | distinct fiber id (22 bits).
+
+constexpr int kTilePart = 2048;         // pairs per spmm part (8 warps x 256)
+constexpr int kTileWarps = 8;
+constexpr int kScatterItems = 1024;     // items per pair_scatter chunk (spans cached in smem)
+constexpr int kTileMaxRowsShift = 5;    // TR <= 32: a pair's end is always inside the next window
+constexpr int kTileMaxTiles = 4096;     // tiles per mode (tile_units scans them in one CTA)
+
+__device__ __forceinline__ uint64_t pack_pair(int64_t pos, int cnt, int64_t d) {
+  return ((uint64_t)pos << 28) | ((uint64_t)(cnt - 1) << 22) | (uint64_t)d;
+}
+__device__ __forceinline__ int64_t pair_pos(uint64_t p) { return (int64_t)(p >> 28); }
+__device__ __forceinline__ int pair_cnt(uint64_t p) { return (int)((p >> 22) & 63u) + 1; }
+__device__ __forceinline__ int pair_fib(uint64_t p) { return (int)(p & 0x3FFFFFu); }
+
+// ---------------------------------------------------------------- deterministic dedup order
+// Distinct fibers are numbered in the order of their representative (smallest) sample id,
+// not in hash-slot order (which depends on the order of the CAS races in hash_insert).
+__global__ void rep_flag_kernel(const int64_t *__restrict__ X, int N, int64_t J, int k, Strides st,
+                                int64_t tmask, const unsigned long long *__restrict__ tkey,
+                                const int32_t *__restrict__ trep, int64_t *__restrict__ flag,
+                                int32_t *__restrict__ sslot) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= J) return;
+  const unsigned long long key = (unsigned long long)sample_key(X, N, J, k, st, s);
+  uint64_t h = mix64((uint64_t)key) & (uint64_t)tmask;
+  while (tkey[h] != key) h = (h + 1) & (uint64_t)tmask;
+  flag[s] = trep[h] == (int32_t)s ? 1 : 0;
+  sslot[s] = (int32_t)h;
+}
+
+__global__ void rep_compact_kernel(const int64_t *__restrict__ flag, const int64_t *__restrict__ fpos,
+                                   int64_t J, const int32_t *__restrict__ sslot,
+                                   const unsigned long long *__restrict__ tkey,
+                                   const int32_t *__restrict__ tcnt,
+                                   const unsigned long long *__restrict__ twmin,
+                                   const unsigned long long *__restrict__ twmax,
+                                   const double *__restrict__ twsum, int64_t *__restrict__ dkey,
+                                   int32_t *__restrict__ dcnt, int32_t *__restrict__ drep,
+                                   double *__restrict__ dsc, int64_t *__restrict__ S) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s == 0) S[0] = fpos[J];
+  if (s >= J || !flag[s]) return;
+  const int64_t d = fpos[s];
+  const int32_t h = sslot[s];
+  dkey[d] = (int64_t)tkey[h];
+  dcnt[d] = tcnt[h];
+  drep[d] = (int32_t)s;
+  dsc[d] = twmin[h] == twmax[h] ? (double)tcnt[h] * __longlong_as_double((long long)twmin[h]) : twsum[h];
+}
+
+// ---------------------------------------------------------------- pass 1: pairs per tile
+// A warp loads all (<= kItemE / 32) windows of its item at once, then flags run starts.
+constexpr int kItemWin = (int)(kItemE / 32);
+
+template <int TS>
+__global__ void __launch_bounds__(kTraverseThreads)
+tile_hist_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                 const int32_t *__restrict__ ifib, const int64_t *__restrict__ dlo,
+                 const int64_t *__restrict__ dlen, const int32_t *__restrict__ rows, int n_tiles,
+                 int32_t *__restrict__ cmat) {
+  extern __shared__ int32_t hist[];
+  const int64_t S = Sp[0];
+  int64_t i0, i1;
+  cta_items(ioff[S], i0, i1);
+  for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t it = i0 + wid; it < i1; it += nw) {
+    const ItemSpan sp = item_span(it, ioff, ifib, dlo, dlen);
+    const int64_t fs = dlo[sp.d];
+    int32_t t[kItemWin];
+#pragma unroll
+    for (int q = 0; q < kItemWin; ++q) {
+      const int64_t pos = sp.a + 32 * q + lane;
+      t[q] = pos < sp.b ? (rows[pos] >> TS) : -1;
+    }
+    const int32_t t0 = (lane == 0 && sp.a > fs) ? (rows[sp.a - 1] >> TS) : -1;
+#pragma unroll
+    for (int q = 0; q < kItemWin; ++q) {
+      int32_t pt = __shfl_up_sync(0xffffffffu, t[q], 1);
+      const int32_t last = q ? __shfl_sync(0xffffffffu, t[q ? q - 1 : 0], 31) : t0;
+      if (lane == 0) pt = last;
+      if (t[q] >= 0 && t[q] != pt) atomicAdd(&hist[t[q]], 1);
+    }
+  }
+  __syncthreads();
+  int32_t *mine = cmat + (int64_t)blockIdx.x * n_tiles;
+  for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) mine[i] = hist[i];
+}
+
+// Block-wide exclusive scan of n <= 4 * blockDim.x int32 values in shared memory (in place);
+// returns the total.  blockDim.x == 1024.
+__device__ int block_scan_excl(int32_t *a, int n) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t total;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  int32_t v[4], s = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = 4 * t + q;
+    v[q] = i < n ? a[i] : 0;
+    s += v[q];
+  }
+  int32_t x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int32_t w = wsum[lane];
+    int32_t z = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    wsum[lane] = z - w;
+    if (lane == 31) total = z;
+  }
+  __syncthreads();
+  int32_t run = wsum[wid] + x - s;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = 4 * t + q;
+    if (i < n) a[i] = run;
+    run += v[q];
+  }
+  __syncthreads();
+  return total;
+}
+
+// ---------------------------------------------------------------- pass 2: pair scatter
+// The CTA's items are cut into units of up to kUnitWin consecutive 32-entry windows of one
+// item; 32 units (one per warp) form a batch.  Within a batch a tile receives at most one
+// pair per unit (a fiber has one pair per tile), ranked by warp index through a per-tile
+// bit mask; the batch order and the unit -> warp assignment are fixed, so every pair's slot
+// is a function of the input only.  Item spans are cached in shared memory per chunk.
+constexpr int kUnitWin = 4;
+
+template <int TS>
+__global__ void __launch_bounds__(kTraverseThreads)
+pair_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                    const int32_t *__restrict__ ifib, const int64_t *__restrict__ dlo,
+                    const int64_t *__restrict__ dlen, const int32_t *__restrict__ rows,
+                    int n_tiles, const int64_t *__restrict__ tptr,
+                    const int32_t *__restrict__ cmat, uint64_t *__restrict__ pairs) {
+  extern __shared__ int64_t smem_i64[];
+  int64_t *cur = smem_i64;                                 // n_tiles
+  int64_t *ia = cur + n_tiles;                             // item start   [kScatterItems]
+  int64_t *ib = ia + kScatterItems;                        // item end
+  int64_t *ifs = ib + kScatterItems;                       // fiber start
+  int64_t *ife = ifs + kScatterItems;                      // fiber end
+  uint32_t *mask = reinterpret_cast<uint32_t *>(ife + kScatterItems);   // n_tiles
+  int32_t *idd = reinterpret_cast<int32_t *>(mask + n_tiles);          // fiber id
+  int32_t *upre = idd + kScatterItems;                                  // kScatterItems + 1
+  const int64_t S = Sp[0];
+  int64_t i0, i1;
+  cta_items(ioff[S], i0, i1);
+  const int32_t *mine = cmat + (int64_t)blockIdx.x * n_tiles;
+  for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
+    cur[i] = tptr[i] + mine[i];
+    mask[i] = 0u;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned below = (1u << wid) - 1u;
+  constexpr int UE = 32 * kUnitWin;
+  for (int64_t ci = i0; ci < i1; ci += kScatterItems) {
+    const int ni = (int)min((int64_t)kScatterItems, i1 - ci);
+    __syncthreads();
+    for (int i = threadIdx.x; i < ni; i += blockDim.x) {
+      const ItemSpan sp = item_span(ci + i, ioff, ifib, dlo, dlen);
+      ia[i] = sp.a;
+      ib[i] = sp.b;
+      ifs[i] = dlo[sp.d];
+      ife[i] = dlo[sp.d] + dlen[sp.d];
+      idd[i] = (int32_t)sp.d;
+      upre[i] = (int32_t)ceil_div(sp.b - sp.a, (int64_t)UE);
+    }
+    __syncthreads();
+    const int nu = block_scan_excl(upre, ni);
+    if (threadIdx.x == 0) upre[ni] = nu;
+    __syncthreads();
+    for (int ub = 0; ub < nu; ub += 32) {
+      const int u = ub + wid;
+      unsigned own = 0u;        // bit v: this lane owns the pair starting in window v
+      int32_t tl[kUnitWin];
+      int cnt[kUnitWin];
+      int64_t base = 0;
+      int32_t d = 0;
+      if (u < nu) {   // warp-uniform
+        int lo = 0, hi = ni;   // largest i with upre[i] <= u
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (upre[mid] <= u) lo = mid; else hi = mid;
+        }
+        const int64_t a = ia[lo], b = ib[lo], fs = ifs[lo], fe = ife[lo];
+        d = idd[lo];
+        base = a + (int64_t)UE * (u - upre[lo]);
+        // windows 0..kUnitWin-1 of the unit and one more (a run ends <= TR <= 32 later),
+        // read to the fiber's end (past the item's end when needed)
+        int32_t t[kUnitWin + 1];
+#pragma unroll
+        for (int v = 0; v <= kUnitWin; ++v) {
+          const int64_t pos = base + 32 * v + lane;
+          t[v] = pos < fe ? (rows[pos] >> TS) : INT_MAX;
+        }
+        const int32_t tp = (lane == 0 && base > fs) ? (rows[base - 1] >> TS) : -1;
+        unsigned bnd[kUnitWin + 1], st[kUnitWin + 1];
+#pragma unroll
+        for (int v = 0; v <= kUnitWin; ++v) {
+          const int64_t pos = base + 32 * v + lane;
+          int32_t pt = __shfl_up_sync(0xffffffffu, t[v], 1);
+          const int32_t last = v ? __shfl_sync(0xffffffffu, t[v ? v - 1 : 0], 31) : tp;
+          if (lane == 0) pt = last;
+          const bool s_ = pos < fe && t[v] != pt;
+          st[v] = s_ ? 1u : 0u;
+          bnd[v] = __ballot_sync(0xffffffffu, s_ || pos >= fe);
+        }
+#pragma unroll
+        for (int v = 0; v < kUnitWin; ++v) {
+          const int64_t pos = base + 32 * v + lane;
+          tl[v] = t[v];
+          cnt[v] = 0;
+          if (st[v] && pos < b) {
+            const unsigned above = bnd[v] & ~((2u << lane) - 1u);
+            const int64_t end = above ? base + 32 * v + (__ffs(above) - 1)
+                                      : base + 32 * (v + 1) + (__ffs(bnd[v + 1]) - 1);
+            cnt[v] = (int)(end - pos);
+            own |= 1u << v;
+            atomicOr(&mask[t[v]], 1u << wid);
+          }
+        }
+      }
+      __syncthreads();
+      unsigned m[kUnitWin];
+#pragma unroll
+      for (int v = 0; v < kUnitWin; ++v) {
+        m[v] = 0u;
+        if (own >> v & 1u) {
+          m[v] = mask[tl[v]];
+          pairs[cur[tl[v]] + __popc(m[v] & below)] = pack_pair(base + 32 * v + lane, cnt[v], d);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int v = 0; v < kUnitWin; ++v)
+        if ((own >> v & 1u) && (m[v] & below) == 0u) {   // the tile's lowest warp advances
+          cur[tl[v]] += __popc(m[v]);
+          mask[tl[v]] = 0u;
+        }
+    }
+  }
+}
+
+inline size_t pair_scatter_smem(int n_tiles) {
+  return 12 * (size_t)n_tiles + (size_t)kScatterItems * (4 * 8 + 4) + 4 * (kScatterItems + 1);
+}
+
+// ---------------------------------------------------------------- work units
+// Tile t is cut into ceil(n_t / kTilePart) parts (at least one: empty tiles still write
+// their zero rows).  uoff[t] = first unit of tile t; sbase[t] = first scratch slot of a
+// multi-part tile.  One CTA of 1024 threads, n_tiles <= 4096.
+__global__ void __launch_bounds__(1024)
+tile_units_kernel(const int64_t *__restrict__ tcnt, int n_tiles, int32_t *__restrict__ uoff,
+                  int32_t *__restrict__ sbase) {
+  __shared__ int32_t a[4096 + 1], b[4096 + 1];
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const int32_t np = (int32_t)max((int64_t)1, ceil_div(tcnt[t], (int64_t)kTilePart));
+    a[t] = np;
+    b[t] = np > 1 ? np : 0;
+  }
+  __syncthreads();
+  const int nu = block_scan_excl(a, n_tiles);
+  const int ns = block_scan_excl(b, n_tiles);
+  (void)ns;
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    uoff[t] = a[t];
+    sbase[t] = b[t];
+  }
+  if (threadIdx.x == 0) uoff[n_tiles] = nu;
+}
+
+// ---------------------------------------------------------------- per-tile SpMM
+// Accumulator row g of the warp's tile: acc[g] += v * h (g warp-uniform).
+template <int TR, int NP>
+__device__ __forceinline__ void tile_apply(double2 (&acc)[TR][NP], int g, double v,
+                                           const double2 (&h)[NP]) {
+#define RCP_TAPPLY(G)                                         \
+  case G:                                                     \
+    if (G < TR) {                                             \
+      _Pragma("unroll") for (int j = 0; j < NP; ++j) {        \
+        acc[G < TR ? G : 0][j].x = fma(v, h[j].x, acc[G < TR ? G : 0][j].x); \
+        acc[G < TR ? G : 0][j].y = fma(v, h[j].y, acc[G < TR ? G : 0][j].y); \
+      }                                                       \
+    }                                                         \
+    break;
+  switch (g) {
+    RCP_TAPPLY(0) RCP_TAPPLY(1) RCP_TAPPLY(2) RCP_TAPPLY(3) RCP_TAPPLY(4) RCP_TAPPLY(5)
+    RCP_TAPPLY(6) RCP_TAPPLY(7) RCP_TAPPLY(8) RCP_TAPPLY(9) RCP_TAPPLY(10) RCP_TAPPLY(11)
+    RCP_TAPPLY(12) RCP_TAPPLY(13) RCP_TAPPLY(14) RCP_TAPPLY(15) RCP_TAPPLY(16)
+    RCP_TAPPLY(17) RCP_TAPPLY(18) RCP_TAPPLY(19) RCP_TAPPLY(20) RCP_TAPPLY(21)
+    RCP_TAPPLY(22) RCP_TAPPLY(23) RCP_TAPPLY(24) RCP_TAPPLY(25) RCP_TAPPLY(26)
+    RCP_TAPPLY(27) RCP_TAPPLY(28) RCP_TAPPLY(29) RCP_TAPPLY(30) RCP_TAPPLY(31)
+    default: break;
+  }
+#undef RCP_TAPPLY
+}
+
+// Per-warp ring of kTileRing pair slots filled by cp.async: the fiber's scaled KRP row (the
+// lane's column pairs) and the pair's rows and values.  Pair i + kTileRing is requested while
+// pair i is applied, so every warp keeps kTileRing pairs' loads in flight.
+template <int TR, int NP>
+struct TileSlot {
+  double2 h[32 * NP];
+  double v[TR];
+  int32_t r[TR];
+  int32_t cnt;
+  int32_t pad[3];
+};
+
+__device__ __forceinline__ void cpa_16(void *smem, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g));
+}
+__device__ __forceinline__ void cpa_8(void *smem, const void *g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g));
+}
+__device__ __forceinline__ void cpa_4(void *smem, const void *g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g));
+}
+
+template <int TS, int NP>
+constexpr int tile_ring() { return NP == 1 ? 16 : 8; }
+
+template <int TS, int NP>
+constexpr size_t tile_spmm_smem() {
+  constexpr size_t ring = (size_t)kTileWarps * tile_ring<TS, NP>() * sizeof(TileSlot<(1 << TS), NP>);
+  constexpr size_t red = (size_t)kTileWarps * (1 << TS) * 32 * NP * sizeof(double2);
+  return ring > red ? ring : red;
+}
+
+template <int TS, int NP>
+__global__ void __launch_bounds__(kTileWarps * 32, 2)
+tile_spmm_kernel(const int64_t *__restrict__ tptr, int n_tiles, int64_t n_rows,
+                 const int32_t *__restrict__ uoff, const int32_t *__restrict__ sbase,
+                 const uint64_t *__restrict__ pairs, const int32_t *__restrict__ rows,
+                 const double *__restrict__ vals, const double *__restrict__ Hs, int R,
+                 double *__restrict__ out, double2 *__restrict__ scratch,
+                 int32_t *__restrict__ tile_done, uint32_t *__restrict__ tile_mask,
+                 int64_t *__restrict__ stats) {
+  constexpr int TR = 1 << TS;
+  constexpr int W = 32 * NP;   // double2 columns per row
+  constexpr int D = tile_ring<TS, NP>();
+  using Slot = TileSlot<TR, NP>;
+  extern __shared__ __align__(16) unsigned char tsm[];
+  double2 *red = reinterpret_cast<double2 *>(tsm);                 // [kTileWarps][TR][W]
+  __shared__ uint32_t s_mask;
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Slot *ring = reinterpret_cast<Slot *>(tsm) + wid * D;
+  const int Rp2 = hs_stride(R) >> 1;
+  const double2 *H2 = reinterpret_cast<const double2 *>(Hs);
+  const int U = uoff[n_tiles];
+  unsigned long long hit_total = 0;
+  if (threadIdx.x == 0) s_mask = 0u;
+  __syncthreads();
+  for (int u = blockIdx.x; u < U; u += gridDim.x) {
+    int lo = 0, hi = n_tiles;   // tile: largest t with uoff[t] <= u
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (uoff[mid] <= u) lo = mid; else hi = mid;
+    }
+    const int t = lo;
+    const int part = u - uoff[t], nparts = uoff[t + 1] - uoff[t];
+    const int64_t p0 = tptr[t], p1 = tptr[t + 1];
+    const int64_t per = ceil_div(p1 - p0, (int64_t)nparts);
+    const int64_t a = p0 + part * per, b = min(a + per, p1);
+    const int64_t wper = ceil_div(b - a, (int64_t)kTileWarps);
+    const int64_t wa = min(a + wid * wper, b), wb = min(wa + wper, b);
+    const int n = (int)(wb - wa);
+    double2 acc[TR][NP];
+#pragma unroll
+    for (int r = 0; r < TR; ++r)
+#pragma unroll
+      for (int j = 0; j < NP; ++j) acc[r][j] = make_double2(0.0, 0.0);
+    uint32_t hmask = 0u;
+    // pair records: rc holds pairs [wa + 32c, +32) of the issue pointer's batch c, rn the next
+    uint64_t rc = lane < n ? pairs[wa + lane] : 0ull;
+    uint64_t rn = 32 + lane < n ? pairs[wa + 32 + lane] : 0ull;
+    auto issue = [&](int i) {   // request pair i into slot i % D (one commit group per call)
+      if (i < n) {
+        if (i && (i & 31) == 0) {
+          rc = rn;
+          rn = i + 32 + lane < n ? pairs[wa + i + 32 + lane] : 0ull;
+        }
+        const uint64_t pr = __shfl_sync(0xffffffffu, rc, i & 31);
+        Slot &sl = ring[i % D];
+        const int64_t dj = pair_fib(pr);
+#pragma unroll
+        for (int jj = 0; jj < NP; ++jj) {
+          const int c2 = lane + 32 * jj;
+          if (2 * c2 < R) cpa_16(&sl.h[c2], H2 + dj * Rp2 + c2);
+        }
+        const int c = pair_cnt(pr);
+        const int64_t pe = pair_pos(pr) + lane;
+        if (lane < c) {
+          cpa_4(&sl.r[lane], rows + pe);
+          cpa_8(&sl.v[lane], vals + pe);
+        }
+        if (lane == 0) sl.cnt = c;
+      }
+      cpa_commit();
+    };
+#pragma unroll
+    for (int i = 0; i < D; ++i) issue(i);
+    for (int i = 0; i < n; ++i) {
+      cpa_wait<D - 1>();
+      __syncwarp();
+      const Slot &sl = ring[i % D];
+      double2 h[NP];
+#pragma unroll
+      for (int jj = 0; jj < NP; ++jj) h[jj] = sl.h[lane + 32 * jj];
+      const int c = sl.cnt;
+      for (int e = 0; e < c; ++e) {
+        const int g = sl.r[e] & (TR - 1);
+        hmask |= 1u << g;
+        tile_apply<TR, NP>(acc, g, sl.v[e], h);
+      }
+      __syncwarp();
+      issue(i + D);
+    }
+    cpa_wait<0>();
+    __syncthreads();   // every warp is done with its ring: the area becomes the reduction buffer
+    // fixed-order combine of the warps' partial tiles
+    double2 *mine = red + (size_t)wid * TR * W;
+#pragma unroll
+    for (int r = 0; r < TR; ++r)
+#pragma unroll
+      for (int j = 0; j < NP; ++j) mine[r * W + lane + 32 * j] = acc[r][j];
+    if (lane == 0 && hmask) atomicOr(&s_mask, hmask);
+    __syncthreads();
+    const int64_t row0 = (int64_t)t * TR;
+    double2 *slot = nparts > 1 ? scratch + ((size_t)sbase[t] + part) * TR * W : nullptr;
+    for (int i = threadIdx.x; i < TR * W; i += blockDim.x) {
+      double2 s = red[i];
+#pragma unroll
+      for (int w = 1; w < kTileWarps; ++w) {
+        const double2 x = red[(size_t)w * TR * W + i];
+        s.x += x.x;
+        s.y += x.y;
+      }
+      if (slot) {
+        __stcg(slot + i, s);
+      } else {
+        const int64_t row = row0 + i / W;
+        const int c = 2 * (i % W);
+        if (row < n_rows && c < R) {
+          out[row * R + c] = s.x;
+          if (c + 1 < R) out[row * R + c + 1] = s.y;
+        }
+      }
+    }
+    if (nparts == 1) {
+      if (threadIdx.x == 0) hit_total += __popc(s_mask);
+    } else {
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        atomicOr(&tile_mask[t], s_mask);
+        s_last = atomicAdd(&tile_done[t], 1) == nparts - 1;
+      }
+      __syncthreads();
+      if (s_last) {   // the last part to finish sums every part in part order
+        __threadfence();
+        const double2 *base = scratch + (size_t)sbase[t] * TR * W;
+        for (int i = threadIdx.x; i < TR * W; i += blockDim.x) {
+          double2 s = __ldcg(base + i);
+          for (int q = 1; q < nparts; ++q) {
+            const double2 x = __ldcg(base + (size_t)q * TR * W + i);
+            s.x += x.x;
+            s.y += x.y;
+          }
+          const int64_t row = row0 + i / W;
+          const int c = 2 * (i % W);
+          if (row < n_rows && c < R) {
+            out[row * R + c] = s.x;
+            if (c + 1 < R) out[row * R + c + 1] = s.y;
+          }
+        }
+        if (threadIdx.x == 0) {
+          hit_total += __popc(atomicExch(&tile_mask[t], 0u));
+          tile_done[t] = 0;
+        }
+      }
+    }
+    if (threadIdx.x == 0) s_mask = 0u;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && hit_total) atomicAdd((unsigned long long *)&stats[4], hit_total);
+}

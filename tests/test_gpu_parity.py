@@ -331,6 +331,21 @@ def test_c1_als_matches_reference(pkg, c1, sampler, P):
         assert h is not None and min(mism) >= h, \
             "sample batches differ at solves %s (reference sensitivity horizon %s)" % (mism, h)
         assert all(a == b for a, b in zip(hashes[:h], ref_hashes[:h]))
+        # factors, sigma and fits are still held to the bars at the last whole round
+        # before the horizon (the reference's own trajectory is well-defined up to there)
+        rh = h // 3
+        assert rh >= 1, "horizon %d leaves no whole round to compare" % h
+        cfg_h = pkg.AlsConfig(rank=8, rounds=rh, sampler=sampler, samples=4096,
+                              schedule="accumulator-stationary", procs=P, seed=3, fit_every=1,
+                              record_samples=True, permute=False)
+        res_h = pkg.run_als(cfg_h, tensor=t)
+        st, fits_o = O.run_as((2000, 1500, 1000), idx, vals, 8, sampler, 4096, rh, seed=3, P=P)
+        assert [sha(X) for X in res_h.sample_log] == ref_hashes[:3 * rh]
+        for j in range(3):
+            assert rel_err(res_h.factors[j], st.full(j)) < REL, j
+        assert rel_err(res_h.sigma, st.sigma) < REL
+        fits = np.array([f for _, f in res_h.fit_history])
+        assert np.abs(fits - np.array(fits_o)).max() < 1e-6
         return
     for j in range(3):
         assert rel_err(res.factors[j], g0[tag + "_U%d" % j]) < REL, j

@@ -59,6 +59,32 @@ def hook(k):
         nt = (st.n_rows + T - 1) // T
         pairs[str(T)] = int(torch.unique(fid * nt + rows // T).numel())
     d["tile_fiber_pairs"] = pairs
+    for T in (8, 16, 32):
+        nt = (st.n_rows + T - 1) // T
+        pairs[str(T)] = int(torch.unique(fid * nt + rows // T).numel())
+    # rows relabelled by descending entry count: how dense are row tiles of the head?
+    order = torch.argsort(rh, descending=True)
+    rank = torch.empty_like(order)
+    rank[order] = torch.arange(order.numel(), device=dev)
+    rr = rank[rows]
+    ranked = {}
+    for T in (8, 16):
+        nt = (st.n_rows + T - 1) // T
+        tile = rr // T
+        pk = torch.unique(fid * nt + tile)
+        ptile = torch.bincount(pk % nt, minlength=nt)      # fibers touching each ranked tile
+        etile = torch.bincount(tile, minlength=nt)         # entries in each ranked tile
+        cum_e = torch.cumsum(etile, 0).double() / max(nnz_d, 1)
+        cum_p = torch.cumsum(ptile, 0).double()
+        pts = []
+        for frac in (0.25, 0.5, 0.75, 0.9, 1.0):
+            t_ = int(torch.searchsorted(cum_e, torch.tensor([frac - 1e-12], dtype=torch.float64, device=dev)))
+            t_ = min(t_, nt - 1)
+            # dense-block density of the first t_+1 ranked tiles: entries / (T * fibers)
+            pts.append({"entry_frac": frac, "tiles": t_ + 1, "pairs": int(cum_p[t_]),
+                        "density": float(cum_e[t_] * nnz_d / (T * cum_p[t_]))})
+        ranked[str(T)] = pts
+    d["ranked_tiles"] = ranked
     res.append(d)
     return orig(k)
 
