@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=0)
     ap.add_argument("--leaf", type=int, default=None, help="STS tree leaf rows (default: engine)")
+    ap.add_argument("--balance", default="auto", choices=["auto", "rows", "nnz"],
+                    help="row blocks: reference equal-row cuts, or nnz-balanced cuts "
+                         "(auto: nnz when more than one GPU)")
     ap.add_argument("--rank", type=int, default=None, help="CP rank (default: the config's)")
     ap.add_argument("--eager", action="store_true",
                     help="launch every kernel from the host (default: replay STS rounds from a "
@@ -167,11 +170,14 @@ def run_ours(args):
     N = len(dims)
     nnz = sum(int(ch[0].shape[0]) for ch in idx) if isinstance(idx, list) else int(idx.shape[0])
     t_gen = time.perf_counter() - t_setup
+    balance = args.balance if args.balance != "auto" else ("nnz" if world > 1 else "rows")
     if spmd:
         from paper_2210_05105_b200.dist import make_spmd_cluster
-        cl = make_spmd_cluster(dims, idx, vals, R, J, args.sampler, args.seed, leaf=args.leaf)
+        cl = make_spmd_cluster(dims, idx, vals, R, J, args.sampler, args.seed, leaf=args.leaf,
+                               balance=balance)
     else:
-        cl = make_local_cluster(dims, idx, vals, R, J, args.sampler, args.seed, leaf=args.leaf)
+        cl = make_local_cluster(dims, idx, vals, R, J, args.sampler, args.seed, leaf=args.leaf,
+                                balance=balance)
     del idx, vals
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
@@ -302,7 +308,7 @@ def run_ours(args):
         "config": {"workload": "%s %s R=%d J=%d dims=%s nnz=%d" % (args.config, args.sampler, R, J,
                                                                  "x".join(map(str, dims)), nnz),
                    "sampler": args.sampler, "rank": R, "samples_J": J, "modes": N,
-                   "parallelism": "as%d" % world, "l2": "256 MB flush between timed rounds "
+                   "parallelism": "as%d" % world, "row_blocks": balance, "l2": "256 MB flush between timed rounds "
                    "(outside the round events); stores %.1f GB > L2" % (
                        sum(s.bytes() for s in me.stores) / 1e9),
                    "setup_s": round(setup_s, 1), "generate_s": round(t_gen, 1),

@@ -22,8 +22,10 @@
 // (ref tests/test_mttkrp.py:60-67,163-172 require bit-identity across worker counts).
 // Pair record: store position (36 bits) | count - 1 (6 bits) | distinct fiber id (22 bits).
 
-constexpr int kTilePart = 2048;         // pairs per spmm part (8 warps x 256)
-constexpr int kTileWarps = 8;
+#include "tile_apply_ptx.cuh"
+
+constexpr int kTilePart = 2048;         // pairs per spmm part (4 warps x 512)
+constexpr int kTileWarps = 4;
 constexpr int kScatterItems = 1024;     // items per pair_scatter chunk (spans cached in smem)
 constexpr int kTileMaxRowsShift = 5;    // TR <= 32: a pair's end is always inside the next window
 constexpr int kTileMaxTiles = 4096;     // tiles per mode (tile_units scans them in one CTA)
@@ -206,57 +208,83 @@ pair_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict_
     const int nu = block_scan_excl(upre, ni);
     if (threadIdx.x == 0) upre[ni] = nu;
     __syncthreads();
-    for (int ub = 0; ub < nu; ub += 32) {
-      const int u = ub + wid;
-      unsigned own = 0u;        // bit v: this lane owns the pair starting in window v
-      int32_t tl[kUnitWin];
-      int cnt[kUnitWin];
-      int64_t base = 0;
-      int32_t d = 0;
-      if (u < nu) {   // warp-uniform
+    // unit loads for batch ub are issued before the barriers of batch ub - 32
+    struct UnitLoad {
+      int32_t t[kUnitWin + 1];
+      int32_t tp;
+      int64_t base, b, fs, fe;
+      int32_t d;
+      bool ok;
+    };
+    auto load_unit = [&](int u) {
+      UnitLoad L;
+      L.ok = u < nu;
+      L.base = L.b = L.fs = L.fe = 0;
+      L.d = 0;
+      L.tp = -1;
+#pragma unroll
+      for (int v = 0; v <= kUnitWin; ++v) L.t[v] = INT_MAX;
+      if (L.ok) {   // warp-uniform
         int lo = 0, hi = ni;   // largest i with upre[i] <= u
         while (hi - lo > 1) {
           const int mid = (lo + hi) >> 1;
           if (upre[mid] <= u) lo = mid; else hi = mid;
         }
-        const int64_t a = ia[lo], b = ib[lo], fs = ifs[lo], fe = ife[lo];
-        d = idd[lo];
-        base = a + (int64_t)UE * (u - upre[lo]);
+        L.b = ib[lo];
+        L.fs = ifs[lo];
+        L.fe = ife[lo];
+        L.d = idd[lo];
+        L.base = ia[lo] + (int64_t)UE * (u - upre[lo]);
         // windows 0..kUnitWin-1 of the unit and one more (a run ends <= TR <= 32 later),
         // read to the fiber's end (past the item's end when needed)
-        int32_t t[kUnitWin + 1];
 #pragma unroll
         for (int v = 0; v <= kUnitWin; ++v) {
-          const int64_t pos = base + 32 * v + lane;
-          t[v] = pos < fe ? (rows[pos] >> TS) : INT_MAX;
+          const int64_t pos = L.base + 32 * v + lane;
+          if (pos < L.fe) L.t[v] = rows[pos];
         }
-        const int32_t tp = (lane == 0 && base > fs) ? (rows[base - 1] >> TS) : -1;
+        if (lane == 0 && L.base > L.fs) L.tp = rows[L.base - 1];
+      }
+      return L;
+    };
+    UnitLoad cu = load_unit(wid);
+    for (int ub = 0; ub < nu; ub += 32) {
+      unsigned own = 0u;        // bit v: this lane owns the pair starting in window v
+      int32_t tl[kUnitWin];
+      int cnt[kUnitWin];
+      if (cu.ok) {   // warp-uniform
+        int32_t t[kUnitWin + 1];
+#pragma unroll
+        for (int v = 0; v <= kUnitWin; ++v) t[v] = cu.t[v] == INT_MAX ? INT_MAX : (cu.t[v] >> TS);
+        const int32_t tp = cu.tp < 0 ? -1 : (cu.tp >> TS);
         unsigned bnd[kUnitWin + 1], st[kUnitWin + 1];
 #pragma unroll
         for (int v = 0; v <= kUnitWin; ++v) {
-          const int64_t pos = base + 32 * v + lane;
+          const int64_t pos = cu.base + 32 * v + lane;
           int32_t pt = __shfl_up_sync(0xffffffffu, t[v], 1);
           const int32_t last = v ? __shfl_sync(0xffffffffu, t[v ? v - 1 : 0], 31) : tp;
           if (lane == 0) pt = last;
-          const bool s_ = pos < fe && t[v] != pt;
+          const bool s_ = pos < cu.fe && t[v] != pt;
           st[v] = s_ ? 1u : 0u;
-          bnd[v] = __ballot_sync(0xffffffffu, s_ || pos >= fe);
+          bnd[v] = __ballot_sync(0xffffffffu, s_ || pos >= cu.fe);
         }
 #pragma unroll
         for (int v = 0; v < kUnitWin; ++v) {
-          const int64_t pos = base + 32 * v + lane;
+          const int64_t pos = cu.base + 32 * v + lane;
           tl[v] = t[v];
           cnt[v] = 0;
-          if (st[v] && pos < b) {
+          if (st[v] && pos < cu.b) {
             const unsigned above = bnd[v] & ~((2u << lane) - 1u);
-            const int64_t end = above ? base + 32 * v + (__ffs(above) - 1)
-                                      : base + 32 * (v + 1) + (__ffs(bnd[v + 1]) - 1);
+            const int64_t end = above ? cu.base + 32 * v + (__ffs(above) - 1)
+                                      : cu.base + 32 * (v + 1) + (__ffs(bnd[v + 1]) - 1);
             cnt[v] = (int)(end - pos);
             own |= 1u << v;
             atomicOr(&mask[t[v]], 1u << wid);
           }
         }
       }
+      const int64_t base = cu.base;
+      const int32_t d = cu.d;
+      cu = load_unit(ub + 32 + wid);   // next batch's loads fly during the barriers
       __syncthreads();
       unsigned m[kUnitWin];
 #pragma unroll
@@ -274,6 +302,7 @@ pair_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict_
           cur[tl[v]] += __popc(m[v]);
           mask[tl[v]] = 0u;
         }
+      __syncthreads();
     }
   }
 }
@@ -307,59 +336,77 @@ tile_units_kernel(const int64_t *__restrict__ tcnt, int n_tiles, int32_t *__rest
 }
 
 // ---------------------------------------------------------------- per-tile SpMM
-// Accumulator row g of the warp's tile: acc[g] += v * h (g warp-uniform).
+// Accumulator row g of the warp's tile: acc[g] += v * h (g warp-uniform), through the
+// generated brx.idx jump table (tile_apply_ptx.cuh).
 template <int TR, int NP>
-__device__ __forceinline__ void tile_apply(double2 (&acc)[TR][NP], int g, double v,
-                                           const double2 (&h)[NP]) {
-#define RCP_TAPPLY(G)                                         \
-  case G:                                                     \
-    if (G < TR) {                                             \
-      _Pragma("unroll") for (int j = 0; j < NP; ++j) {        \
-        acc[G < TR ? G : 0][j].x = fma(v, h[j].x, acc[G < TR ? G : 0][j].x); \
-        acc[G < TR ? G : 0][j].y = fma(v, h[j].y, acc[G < TR ? G : 0][j].y); \
-      }                                                       \
-    }                                                         \
-    break;
-  switch (g) {
-    RCP_TAPPLY(0) RCP_TAPPLY(1) RCP_TAPPLY(2) RCP_TAPPLY(3) RCP_TAPPLY(4) RCP_TAPPLY(5)
-    RCP_TAPPLY(6) RCP_TAPPLY(7) RCP_TAPPLY(8) RCP_TAPPLY(9) RCP_TAPPLY(10) RCP_TAPPLY(11)
-    RCP_TAPPLY(12) RCP_TAPPLY(13) RCP_TAPPLY(14) RCP_TAPPLY(15) RCP_TAPPLY(16)
-    RCP_TAPPLY(17) RCP_TAPPLY(18) RCP_TAPPLY(19) RCP_TAPPLY(20) RCP_TAPPLY(21)
-    RCP_TAPPLY(22) RCP_TAPPLY(23) RCP_TAPPLY(24) RCP_TAPPLY(25) RCP_TAPPLY(26)
-    RCP_TAPPLY(27) RCP_TAPPLY(28) RCP_TAPPLY(29) RCP_TAPPLY(30) RCP_TAPPLY(31)
-    default: break;
-  }
-#undef RCP_TAPPLY
+__device__ __forceinline__ void tile_apply(double2 (&a)[TR][NP], int g, double v, const double2 (&h)[NP]);
+
+template <>
+__device__ __forceinline__ void tile_apply<16, 1>(double2 (&a)[16][1], int g, double v, const double2 (&h)[1]) {
+  tile_apply_ptx_16_1(a[0][0].x, a[0][0].y, a[1][0].x, a[1][0].y, a[2][0].x, a[2][0].y, a[3][0].x, a[3][0].y,
+                      a[4][0].x, a[4][0].y, a[5][0].x, a[5][0].y, a[6][0].x, a[6][0].y, a[7][0].x, a[7][0].y,
+                      a[8][0].x, a[8][0].y, a[9][0].x, a[9][0].y, a[10][0].x, a[10][0].y, a[11][0].x, a[11][0].y,
+                      a[12][0].x, a[12][0].y, a[13][0].x, a[13][0].y, a[14][0].x, a[14][0].y, a[15][0].x, a[15][0].y,
+                      g, v, h[0].x, h[0].y);
+}
+
+template <>
+__device__ __forceinline__ void tile_apply<8, 2>(double2 (&a)[8][2], int g, double v, const double2 (&h)[2]) {
+  tile_apply_ptx_8_2(a[0][0].x, a[0][0].y, a[0][1].x, a[0][1].y, a[1][0].x, a[1][0].y, a[1][1].x, a[1][1].y,
+                     a[2][0].x, a[2][0].y, a[2][1].x, a[2][1].y, a[3][0].x, a[3][0].y, a[3][1].x, a[3][1].y,
+                     a[4][0].x, a[4][0].y, a[4][1].x, a[4][1].y, a[5][0].x, a[5][0].y, a[5][1].x, a[5][1].y,
+                     a[6][0].x, a[6][0].y, a[6][1].x, a[6][1].y, a[7][0].x, a[7][0].y, a[7][1].x, a[7][1].y,
+                     g, v, h[0].x, h[0].y, h[1].x, h[1].y);
 }
 
 // Per-warp ring of kTileRing pair slots filled by cp.async: the fiber's scaled KRP row (the
 // lane's column pairs) and the pair's rows and values.  Pair i + kTileRing is requested while
 // pair i is applied, so every warp keeps kTileRing pairs' loads in flight.
+// Per-warp ring of 2 x BS pair slots filled by cp.async, BS pairs per batch: batch b + 1 is
+// requested while batch b is applied.  Each pair is requested by 32 / BS lanes of its own
+// (the lanes split its Hs row's 16-byte chunks and its entries), so issuing a batch costs a
+// few instructions per pair.  Slot: the fiber's scaled KRP row (512 NP bytes), then one
+// 16-byte record {value, row} per entry.
 template <int TR, int NP>
-struct TileSlot {
-  double2 h[32 * NP];
-  double v[TR];
-  int32_t r[TR];
-  int32_t cnt;
-  int32_t pad[3];
+struct TileSlotLayout {
+  static constexpr int BS = NP == 1 ? 16 : 8;       // pairs per batch
+  static constexpr int LPP = 32 / BS;               // lanes per pair
+  static constexpr uint32_t E = 512u * NP;          // entry records
+  static constexpr uint32_t bytes = E + 16u * TR;
 };
 
-__device__ __forceinline__ void cpa_16(void *smem, const void *g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g));
+__device__ __forceinline__ void cpa16_u32(uint32_t s, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g));
 }
-__device__ __forceinline__ void cpa_8(void *smem, const void *g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g));
+__device__ __forceinline__ void cpa8_u32(uint32_t s, const void *g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(g));
 }
-__device__ __forceinline__ void cpa_4(void *smem, const void *g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g));
+__device__ __forceinline__ void cpa4_u32(uint32_t s, const void *g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(g));
 }
-
-template <int TS, int NP>
-constexpr int tile_ring() { return NP == 1 ? 16 : 8; }
+__device__ __forceinline__ void sts_u32(uint32_t s, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(s), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t s) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(s) : "memory");
+  return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t s) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(s) : "memory");
+  return v;
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t s) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(s) : "memory");
+  return v;
+}
 
 template <int TS, int NP>
 constexpr size_t tile_spmm_smem() {
-  constexpr size_t ring = (size_t)kTileWarps * tile_ring<TS, NP>() * sizeof(TileSlot<(1 << TS), NP>);
+  using SL = TileSlotLayout<(1 << TS), NP>;
+  constexpr size_t ring = (size_t)kTileWarps * 2 * SL::BS * SL::bytes;
   constexpr size_t red = (size_t)kTileWarps * (1 << TS) * 32 * NP * sizeof(double2);
   return ring > red ? ring : red;
 }
@@ -375,14 +422,15 @@ tile_spmm_kernel(const int64_t *__restrict__ tptr, int n_tiles, int64_t n_rows,
                  int64_t *__restrict__ stats) {
   constexpr int TR = 1 << TS;
   constexpr int W = 32 * NP;   // double2 columns per row
-  constexpr int D = tile_ring<TS, NP>();
-  using Slot = TileSlot<TR, NP>;
+  using SL = TileSlotLayout<TR, NP>;
+  constexpr int BS = SL::BS, LPP = SL::LPP;
+  constexpr uint32_t kSlot = SL::bytes, kSlotE = SL::E;
   extern __shared__ __align__(16) unsigned char tsm[];
   double2 *red = reinterpret_cast<double2 *>(tsm);                 // [kTileWarps][TR][W]
   __shared__ uint32_t s_mask;
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  Slot *ring = reinterpret_cast<Slot *>(tsm) + wid * D;
+  const uint32_t ring_u32 = (uint32_t)__cvta_generic_to_shared(tsm) + (uint32_t)(wid * 2 * BS) * kSlot;
   const int Rp2 = hs_stride(R) >> 1;
   const double2 *H2 = reinterpret_cast<const double2 *>(Hs);
   const int U = uoff[n_tiles];
@@ -409,50 +457,57 @@ tile_spmm_kernel(const int64_t *__restrict__ tptr, int n_tiles, int64_t n_rows,
 #pragma unroll
       for (int j = 0; j < NP; ++j) acc[r][j] = make_double2(0.0, 0.0);
     uint32_t hmask = 0u;
-    // pair records: rc holds pairs [wa + 32c, +32) of the issue pointer's batch c, rn the next
-    uint64_t rc = lane < n ? pairs[wa + lane] : 0ull;
-    uint64_t rn = 32 + lane < n ? pairs[wa + 32 + lane] : 0ull;
-    auto issue = [&](int i) {   // request pair i into slot i % D (one commit group per call)
-      if (i < n) {
-        if (i && (i & 31) == 0) {
-          rc = rn;
-          rn = i + 32 + lane < n ? pairs[wa + i + 32 + lane] : 0ull;
-        }
-        const uint64_t pr = __shfl_sync(0xffffffffu, rc, i & 31);
-        Slot &sl = ring[i % D];
-        const int64_t dj = pair_fib(pr);
+    // lane -> (pair jp of the batch, sub-lane sub): the lane requests the pair's 16-byte
+    // Hs chunks sub, sub + LPP, ... and its entries sub, sub + LPP, ...
+    const int jp = lane / LPP, sub = lane % LPP;
+    const int nch = (R + 1) >> 1;                                   // 16-byte chunks per row
+    const int nb = (int)ceil_div((int64_t)n, (int64_t)BS);
+    int cnt_nx = 0, cnt_cu = 0;   // this lane's pair count in the requested / applied batch
+    auto issue = [&](int bi) {
+      const int ip = bi * BS + jp;
+      const uint64_t pr = ip < n ? pairs[wa + ip] : 0ull;
+      const uint32_t sl = ring_u32 + (uint32_t)((bi & 1) * BS + jp) * kSlot;
+      int c = 0;
+      if (ip < n) {
+        c = pair_cnt(pr);
+        const double2 *hs = H2 + (int64_t)pair_fib(pr) * Rp2;
 #pragma unroll
-        for (int jj = 0; jj < NP; ++jj) {
-          const int c2 = lane + 32 * jj;
-          if (2 * c2 < R) cpa_16(&sl.h[c2], H2 + dj * Rp2 + c2);
+        for (int q = 0; q < 32 * NP / LPP; ++q) {
+          const int ch = q * LPP + sub;
+          if (ch < nch) cpa16_u32(sl + 16u * ch, hs + ch);
         }
-        const int c = pair_cnt(pr);
-        const int64_t pe = pair_pos(pr) + lane;
-        if (lane < c) {
-          cpa_4(&sl.r[lane], rows + pe);
-          cpa_8(&sl.v[lane], vals + pe);
+        const int64_t pe = pair_pos(pr);
+        for (int e = sub; e < c; e += LPP) {
+          cpa8_u32(sl + kSlotE + 16u * e, vals + pe + e);
+          cpa4_u32(sl + kSlotE + 16u * e + 8u, rows + pe + e);
         }
-        if (lane == 0) sl.cnt = c;
       }
       cpa_commit();
+      return c;
     };
-#pragma unroll
-    for (int i = 0; i < D; ++i) issue(i);
-    for (int i = 0; i < n; ++i) {
-      cpa_wait<D - 1>();
+    if (nb > 0) cnt_nx = issue(0);
+    for (int bi = 0; bi < nb; ++bi) {
+      cnt_cu = cnt_nx;
+      cnt_nx = bi + 1 < nb ? issue(bi + 1) : (cpa_commit(), 0);
+      cpa_wait<1>();
       __syncwarp();
-      const Slot &sl = ring[i % D];
-      double2 h[NP];
+      const uint32_t base = ring_u32 + (uint32_t)((bi & 1) * BS) * kSlot;
+      const int np_ = min(BS, n - bi * BS);
+      for (int j = 0; j < np_; ++j) {
+        const uint32_t sl = base + (uint32_t)j * kSlot;
+        double2 h[NP];
 #pragma unroll
-      for (int jj = 0; jj < NP; ++jj) h[jj] = sl.h[lane + 32 * jj];
-      const int c = sl.cnt;
-      for (int e = 0; e < c; ++e) {
-        const int g = sl.r[e] & (TR - 1);
-        hmask |= 1u << g;
-        tile_apply<TR, NP>(acc, g, sl.v[e], h);
+        for (int jj = 0; jj < NP; ++jj) h[jj] = lds_f64x2(sl + 16u * lane + 512u * jj);
+        const int c = __shfl_sync(0xffffffffu, cnt_cu, j * LPP);
+        uint32_t ea = sl + kSlotE;
+        for (int e = 0; e < c; ++e, ea += 16u) {
+          const double2 rec = lds_f64x2(ea);
+          const int g = __double2loint(rec.y) & (TR - 1);
+          hmask |= 1u << g;
+          tile_apply<TR, NP>(acc, g, rec.x, h);
+        }
       }
       __syncwarp();
-      issue(i + D);
     }
     cpa_wait<0>();
     __syncthreads();   // every warp is done with its ring: the area becomes the reduction buffer

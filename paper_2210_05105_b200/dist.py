@@ -5,9 +5,10 @@ The engine's bulk-synchronous round (engine.Cluster) is written against a commun
 with list semantics; `TorchComm` implements it for SPMD processes, each holding exactly
 one rank state.  Collectives on the hot path (ref schedules.py:227-258 and SURVEY.md 8(e)):
 
-* sampled rows: all-gather-v of (row, step probability, residual, factor row) per STS
-  constant mode, or of (row, probability, factor row) per CP-ARLS-LEV mode in rank order
-  -- J (N-1) (R+2) / R words per solve, independent of the tensor size;
+* sampled rows: per STS constant mode, (row, step probability, residual, factor row) of
+  every sample, as one fixed-size sum all-reduce of disjoint owner contributions (no
+  host-side counts); per CP-ARLS-LEV mode, an all-gather-v of (row, probability, factor row)
+  in rank order -- O(J (N-1) R) words per solve, independent of the tensor size;
 * R x R block Grams (all-gather, summed in rank order -- also yields the STS rank tree);
 * R column sums of squares for renormalisation; P rank masses for CP-ARLS-LEV.
 
@@ -31,6 +32,7 @@ class TorchComm:
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.ranks = [self.rank]
+        self.words = 0      # 8-byte words this rank handed to sum all-reduces (exchange volume)
 
     def all_gather(self, local):
         """local: [tensor] (this rank's) -> list of P tensors, rank order."""
@@ -54,6 +56,13 @@ class TorchComm:
         self.dist.all_gather(out, buf, group=self.group)
         return [o[:int(counts[p])] for p, o in enumerate(out)]
 
+    def all_reduce_sum(self, local):
+        """In-place sum all-reduce of this rank's tensor; returns [tensor]."""
+        (x,) = local
+        self.words += x.numel()
+        self.dist.all_reduce(x, op=self.dist.ReduceOp.SUM, group=self.group)
+        return [x]
+
     def all_gather_obj(self, local):
         (x,) = local
         out = [None] * self.P
@@ -72,7 +81,7 @@ def comm_words_per_solve(J, R, N, P, sampler):
 
 
 def make_spmd_cluster(dims, idx, vals, R, J, sampler, seed, grid_dims=None, leaf=None,
-                      factors=None, trial=0):
+                      factors=None, trial=0, balance="rows"):
     """This process's rank of a P-GPU accumulator-stationary cluster.  idx/vals: the
     tensor's COO on this GPU (every rank may hold all of it; only the rows of its blocks
     are kept in its stores).  Ownership follows the reference processor grid."""
@@ -84,7 +93,8 @@ def make_spmd_cluster(dims, idx, vals, R, J, sampler, seed, grid_dims=None, leaf
     dev = require_cuda()
     P = dist.get_world_size()
     rank = dist.get_rank()
-    grid = ProcessorGrid(dims, grid_dims) if grid_dims is not None else optimal_grid(dims, P)
+    from .engine import make_grid
+    grid = make_grid(dims, P, grid_dims, idx, balance)
     if grid.P != P:
         raise ValueError("grid %s has %d ranks, world size is %d" % (grid.grid_dims, grid.P, P))
     if factors is None:

@@ -133,6 +133,13 @@ class LocalComm:
     def all_gather_obj(self, local):
         return list(local)
 
+    def all_reduce_sum(self, local):
+        """Sum over the virtual ranks in rank order; every rank gets the total."""
+        tot = local[0].clone()
+        for x in local[1:]:
+            tot.add_(x)
+        return [tot if p == 0 else tot.clone() for p in range(len(local))]
+
     def barrier(self):
         pass
 
@@ -542,30 +549,33 @@ class Cluster:
         return gen.multinomial(self.J, C / W), W
 
     def _exchange_walk(self, i):
-        """After the local walks, every rank holds the finished samples it owns; gather
-        (row, step probability, residual, factor row) to all ranks in rank order
-        (ref schedules.py:239-247: R+2 words per sample per constant mode)."""
+        """After the local walks, every rank holds the finished samples it owns; move
+        (row, step probability, residual, factor row) of every sample to all ranks
+        (ref schedules.py:239-247: R+2 words per sample per constant mode, plus the
+        residual here).  Every rank knows every sample's owner (the rank-level walk is
+        replicated), so the exchange is one fixed-size J x (R+3) sum all-reduce of disjoint
+        contributions: each slot has exactly one nonzero contributor, the sum is exact,
+        and nothing depends on host-side counts (no host synchronisation; capturable in a
+        CUDA graph)."""
         t = torch()
-        P = self.P
-        owner = self.ranks[0].owner
-        counts = t.bincount(owner.long(), minlength=P).cpu().tolist()
-        packs = []
+        bufs = []
         for r in self.ranks:
-            mine = (r.owner == r.rank).nonzero().squeeze(1)
-            pk = t.cat([r.X[i][mine].to(t.float64).unsqueeze(1), r.pmp[i][mine].unsqueeze(1),
-                        r.resid[mine].unsqueeze(1), r.urow[mine]], dim=1).contiguous()
-            packs.append(pk)
-        got = self.comm.all_gather_v(packs, counts)
-        for r in self.ranks:
-            for q in range(P):
-                sel = (r.owner == q).nonzero().squeeze(1)
-                if sel.numel() == 0:
-                    continue
-                blk = got[q][:counts[q]].to(r.dev)
-                r.X[i][sel] = blk[:, 0].to(t.int64)
-                r.pmp[i][sel] = blk[:, 1]
-                r.resid[sel] = blk[:, 2]
-                r.urow[sel] = blk[:, 3:]
+            buf = getattr(r, "xbuf", None)
+            if buf is None or buf.shape != (r.J, r.R + 3):
+                buf = r.xbuf = t.empty((r.J, r.R + 3), dtype=t.float64, device=r.dev)
+            others = (r.owner != r.rank).unsqueeze(1)
+            buf[:, 0] = r.X[i].to(t.float64)
+            buf[:, 1] = r.pmp[i]
+            buf[:, 2] = r.resid
+            buf[:, 3:] = r.urow
+            buf.masked_fill_(others, 0.0)
+            bufs.append(buf)
+        got = self.comm.all_reduce_sum(bufs)
+        for r, g in zip(self.ranks, got):
+            r.X[i].copy_(g[:, 0].to(t.int64))
+            r.pmp[i].copy_(g[:, 1])
+            r.resid.copy_(g[:, 2])
+            r.urow.copy_(g[:, 3:])
 
     # -------------------------------------------------------------- solve
     def _ev(self, phase):
@@ -789,13 +799,26 @@ def _lib_capacity():
     return _lib.ST_CAPACITY
 
 
+def make_grid(dims, P, grid_dims, idx, balance="rows"):
+    """The AS processor grid: reference equal-row blocks, or nnz-balanced blocks."""
+    from .grid import nnz_row_weights
+    if balance not in ("rows", "nnz"):
+        raise ValueError("balance must be 'rows' or 'nnz'")
+    rw = nnz_row_weights(dims, idx) if balance == "nnz" else None
+    if grid_dims is not None:
+        return ProcessorGrid(dims, grid_dims, row_weights=rw)
+    return optimal_grid(dims, P, row_weights=rw)
+
+
 def make_local_cluster(dims, idx, vals, R, J, sampler, seed, P=1, grid_dims=None, leaf=None,
-                       factors=None, trial=0):
+                       factors=None, trial=0, balance="rows"):
     """Single-process cluster (P virtual ranks on the current device).  idx/vals are CUDA
-    tensors; factors default to the reference initialisation (ref als.py:99-105)."""
+    tensors; factors default to the reference initialisation (ref als.py:99-105).
+    balance="rows": the reference's equal-row blocks (parity); "nnz": nnz-balanced blocks
+    (grid.ProcessorGrid row_weights; performance runs)."""
     from .device import require_cuda
     dev = require_cuda()
-    grid = ProcessorGrid(dims, grid_dims) if grid_dims is not None else optimal_grid(dims, P)
+    grid = make_grid(dims, P, grid_dims, idx, balance)
     if factors is None:
         from .linalg import init_factors
         factors, _ = init_factors(dims, R, seed, trial)

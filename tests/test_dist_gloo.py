@@ -111,3 +111,34 @@ def test_grid_ownership_matches_oracle(dims, P):
         assert np.array_equal(g.row_order(j), o.order[j])
         rows = np.arange(dims[j])
         assert np.array_equal(g.row_owner(j, rows), o.owner(j, rows))
+
+
+def test_nnz_balanced_blocks():
+    """ProcessorGrid(row_weights=...) cuts every mode into contiguous blocks minimising the
+    largest block's nonzeros: never worse than the reference's equal-row cuts, within one
+    row's weight of the ideal share, and the default (no weights) stays the reference map."""
+    dims = (3000, 2000, 1500)
+    rng = np.random.default_rng(1)
+    idx = np.stack([np.minimum(rng.zipf(1.2, 300000) - 1, d - 1) for d in dims], axis=1)
+    idx = np.stack([rng.permutation(d)[idx[:, j]] for j, d in enumerate(dims)], axis=1)
+    w = G.nnz_row_weights(dims, idx)
+    for P in (2, 4, 8):
+        ref = G.optimal_grid(dims, P)
+        bal = G.optimal_grid(dims, P, row_weights=w)
+        assert bal.grid_dims == ref.grid_dims
+        for j in range(3):
+            lr = [w[j][slice(*ref.block_range(j, p))].sum() for p in range(P)]
+            lb = [w[j][slice(*bal.block_range(j, p))].sum() for p in range(P)]
+            assert sum(lb) == sum(lr) == len(idx)
+            assert max(lb) <= max(lr)
+            # blocks are contiguous, cover the mode, and ownership is consistent
+            rows = np.arange(dims[j])
+            own = bal.row_owner(j, rows)
+            for p in range(P):
+                lo, hi = bal.block_range(j, p)
+                assert np.all(own[lo:hi] == p)
+    # weighted cuts of one sequence: the optimum of the min-max contiguous partition
+    ww = np.array([5, 1, 1, 1, 1, 1, 5, 1], dtype=float)
+    off = G.weighted_offsets(ww, 3)
+    assert off[0] == 0 and off[-1] == ww.size
+    assert max(ww[off[i]:off[i + 1]].sum() for i in range(3)) == 6.0
