@@ -246,6 +246,17 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
                        const double *d_H, const double *d_w, int R, double *d_out,
                        int64_t *d_stats, void *d_ws, size_t ws_bytes, int *d_status,
                        void *stream);
+/* MTTKRP mode for subsequent rcp_sampled_mttkrp calls (process-wide; initial value from
+ * the environment: RCP_MTTKRP_PATH=tiles selects 1):
+ *   0  fast: entries transposed to row order, segmented SpMM (fp64 red.add for rows split
+ *      across warps; the order of a row's terms varies run to run);
+ *   1  deterministic: row-tile x fiber pairs in a canonical order, every output row summed
+ *      in a fixed order -- bit-identical results on every run (ref tests/test_mttkrp.py:
+ *      60-67,163-172 require bit-identity across worker counts).  Available when the mode's
+ *      rows fit 4096 row tiles (16 rows each for R <= 64, 8 for R <= 128) and J < 2^22;
+ *      other calls run mode 0.
+ * Returns the previous mode; a negative argument only queries. */
+int rcp_set_mttkrp_mode(int mode);
 /* Reference-shaped CSR gather with multiplicity (drop-in for
  * gather_sampled_nonzeros_to_csr): d_counts[s] = fiber length of sample s, and, when
  * d_pos_out != NULL, expanded (row, sample, value) triples in sample order (row-sorting

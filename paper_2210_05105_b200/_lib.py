@@ -68,6 +68,7 @@ _SIGS = {
     "rcp_weights": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp, _vp]),
     "rcp_mttkrp_ws_bytes": (_sz, [_i64, _i64, _i64, _i32]),
     "rcp_mttkrp_layout": (_i32, [_i64, _i64, _i32, _sz, _vp]),
+    "rcp_set_mttkrp_mode": (_i32, [_i32]),
     "rcp_sampled_mttkrp": (_i32, [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _i32, _i64, _i32, _vp,
                                   _vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp, _vp]),
     "rcp_fiber_lookup": (_i32, [_vp, _i64, _vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp]),

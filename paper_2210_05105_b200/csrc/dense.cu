@@ -3,6 +3,8 @@
 // Ref: linalg.py:64-111, schedules.py:104-128, samplers.py:89-96, als.py:129-138.
 #include <algorithm>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "gram_mma.cuh"
 
@@ -34,6 +36,11 @@ constexpr int kGramThreads = 256;
 #ifndef RCP_GRAM_MINB
 #define RCP_GRAM_MINB 2   // __launch_bounds__ min blocks of gram_mma_kernel (<= 128 registers)
 #endif
+int getenv_flag(const char *name) {   // 1 when the variable is set to "1" (read once per name use)
+  const char *e = getenv(name);
+  return e && e[0] == '1' ? 1 : 0;
+}
+
 int gram_grid(int64_t n) {
   int64_t tiles = ceil_div(n, kGramRows);
   // large factors: more CTAs hide the load latency; small ones keep fewer partials
@@ -760,6 +767,115 @@ gram_mma_kernel(const double *__restrict__ U, const double *__restrict__ scale, 
   }
 }
 
+// 64 < R <= 128: the same register fragments, with the T(T+1)/2 upper tile pairs split
+// into G groups of warps (a warp's group is fixed, its pairs a compile-time range) so the
+// accumulators fit the register file; every warp loads the whole 4-row step (the warps of
+// a CTA read the same rows at nearly the same time: L1 hits).  Steps go to (CTA, warp of
+// the group) in a fixed order; warps and CTAs are combined in fixed orders: deterministic.
+template <int T, int G, int g>
+__device__ __forceinline__ void gram_accum_group(const double (&f)[T],
+                                                 double (&acc)[(T * (T + 1) / 2 + G - 1) / G][2]) {
+  constexpr int PPG = (T * (T + 1) / 2 + G - 1) / G;
+  int p = 0;
+#pragma unroll
+  for (int a = 0; a < T; ++a)
+#pragma unroll
+    for (int b = a; b < T; ++b) {
+      if (p >= g * PPG && p < (g + 1) * PPG) gram_dmma(acc[p - g * PPG][0], acc[p - g * PPG][1], f[a], f[b]);
+      ++p;
+    }
+}
+
+template <int T, int G, int g>
+__device__ __forceinline__ void gram_split_body(const double *__restrict__ U,
+                                                const double *__restrict__ scale, int64_t n, int R,
+                                                int sub, double *red) {
+  constexpr int NP = T * (T + 1) / 2;
+  constexpr int PPG = (NP + G - 1) / G;
+  constexpr int WG = 8 / G;   // warps per group
+  const int lane = threadIdx.x & 31;
+  double acc[PPG][2];
+#pragma unroll
+  for (int p = 0; p < PPG; ++p) acc[p][0] = acc[p][1] = 0.0;
+  const int64_t steps = (n + 3) >> 2;
+  const int64_t stride = (int64_t)gridDim.x * WG;
+  const int kk = lane & 3, col = lane >> 2;
+  double f0[T], f1[T];   // two 4-row steps in flight
+  int64_t s = (int64_t)blockIdx.x * WG + sub;
+  gram_load<T>(U, scale, 4 * s + kk, n, R, col, f0);
+  gram_load<T>(U, scale, 4 * (s + stride) + kk, n, R, col, f1);
+  for (; s < steps; s += 2 * stride) {
+    gram_accum_group<T, G, g>(f0, acc);
+    gram_load<T>(U, scale, 4 * (s + 2 * stride) + kk, n, R, col, f0);
+    if (s + stride >= steps) break;
+    gram_accum_group<T, G, g>(f1, acc);
+    gram_load<T>(U, scale, 4 * (s + 3 * stride) + kk, n, R, col, f1);
+  }
+  for (int w = 0; w < WG; ++w) {   // fixed-order combination of the group's warps
+    if (sub == w) {
+#pragma unroll
+      for (int p = 0; p < PPG; ++p) {
+        if (g * PPG + p >= NP) break;
+        double *q = red + (g * PPG + p) * 64 + 2 * lane;
+        q[0] = w ? q[0] + acc[p][0] : acc[p][0];
+        q[1] = w ? q[1] + acc[p][1] : acc[p][1];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int T, int G>
+__global__ void __launch_bounds__(256, 1)
+gram_mma_split_kernel(const double *__restrict__ U, const double *__restrict__ scale, int64_t n,
+                      int R, double *__restrict__ part) {
+  constexpr int NP = T * (T + 1) / 2;
+  extern __shared__ double red[];   // NP x 64
+  const int wid = threadIdx.x >> 5;
+  const int grp = wid % G, sub = wid / G;
+  static_assert(G == 2 || G == 4 || G == 8, "G divides the 8 warps");
+  switch (grp) {
+    case 0: gram_split_body<T, G, 0>(U, scale, n, R, sub, red); break;
+    case 1: gram_split_body<T, G, (G > 1 ? 1 : 0)>(U, scale, n, R, sub, red); break;
+    case 2: gram_split_body<T, G, (G > 2 ? 2 : 0)>(U, scale, n, R, sub, red); break;
+    case 3: gram_split_body<T, G, (G > 3 ? 3 : 0)>(U, scale, n, R, sub, red); break;
+    case 4: gram_split_body<T, G, (G > 4 ? 4 : 0)>(U, scale, n, R, sub, red); break;
+    case 5: gram_split_body<T, G, (G > 5 ? 5 : 0)>(U, scale, n, R, sub, red); break;
+    case 6: gram_split_body<T, G, (G > 6 ? 6 : 0)>(U, scale, n, R, sub, red); break;
+    default: gram_split_body<T, G, (G > 7 ? 7 : 0)>(U, scale, n, R, sub, red); break;
+  }
+  double *out = part + (int64_t)blockIdx.x * R * R;
+  for (int e = threadIdx.x; e < NP * 64; e += blockDim.x) {
+    int p = e >> 6, a = 0;
+    while (p >= T - a) {
+      p -= T - a;
+      ++a;
+    }
+    const int b = a + p;
+    const int ln = (e & 63) >> 1, u = e & 1;
+    const int ga = 8 * a + (ln >> 2), gb = 8 * b + 2 * (ln & 3) + u;
+    if (ga < R && gb < R) {
+      out[ga * R + gb] = red[e];
+      out[gb * R + ga] = red[e];
+    }
+  }
+}
+
+template <int T, int G>
+int launch_gram_split(const double *U, const double *scale, int64_t n, int R, double *part, int grid,
+                      cudaStream_t st) {
+  constexpr int NP = T * (T + 1) / 2;
+  const int smem = NP * 64 * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    RCP_CUDA_TRY(cudaFuncSetAttribute(gram_mma_split_kernel<T, G>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  gram_mma_split_kernel<T, G><<<grid, 256, smem, st>>>(U, scale, n, R, part);
+  return RCP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -803,6 +919,18 @@ int rcp_gram(const double *d_U, const double *d_scale, int64_t n, int R, double 
       case 7: gram_mma_kernel<7><<<grid, 256, 0, st>>>(d_U, d_scale, n, R, part); break;
       default: gram_mma_kernel<8><<<grid, 256, 0, st>>>(d_U, d_scale, n, R, part); break;
     }
+  } else if (R <= 96 && getenv_flag("RCP_GRAM_FFMA") == 0) {
+    // 64 < R <= 96: fp64 tensor cores with the tile pairs split over warp groups (C4 R=75 on
+    // 4.8M rows: 3.15 ms vs 4.03 ms FFMA; above 96 the G=8 split is load-bound and the FFMA
+    // kernel wins -- R=128: 18.5 vs 13.2 ms; profiles/r02_gram_r64.json)
+    int rc = RCP_OK;
+    switch ((R + 7) / 8) {
+      case 9: rc = launch_gram_split<9, 4>(d_U, d_scale, n, R, part, grid, st); break;
+      case 10: rc = launch_gram_split<10, 4>(d_U, d_scale, n, R, part, grid, st); break;
+      case 11: rc = launch_gram_split<11, 4>(d_U, d_scale, n, R, part, grid, st); break;
+      default: rc = launch_gram_split<12, 4>(d_U, d_scale, n, R, part, grid, st); break;
+    }
+    if (rc) return rc;
   } else if (npairs <= kGramThreads)
     gram_partial_kernel<1><<<grid, kGramThreads, smem, st>>>(d_U, d_scale, n, R, al, part);
   else if (npairs <= 2 * kGramThreads)

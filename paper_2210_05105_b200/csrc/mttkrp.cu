@@ -28,6 +28,15 @@ using namespace rcp;
 
 namespace {
 
+int g_mttkrp_mode = -1;   // rcp_set_mttkrp_mode; -1: not yet read from the environment
+int mttkrp_mode() {
+  if (g_mttkrp_mode < 0) {
+    const char *e = getenv("RCP_MTTKRP_PATH");
+    g_mttkrp_mode = e && !strcmp(e, "tiles") ? 1 : 0;
+  }
+  return g_mttkrp_mode;
+}
+
 int sm_count() {
   static int s = 0;
   if (!s) {
@@ -411,7 +420,7 @@ cta_hist_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp
 // quarters are offset by their predecessors' sums.
 constexpr int kPrefixSeg = 4;
 constexpr int kPrefixRows = 64;    // rows per 256-thread block
-constexpr int kPrefixMaxPer = 48;  // CTA counts one thread keeps in registers (G <= 192)
+constexpr int kPrefixMaxPer = 80;  // CTA counts one thread keeps in registers (G <= 320)
 
 __global__ void __launch_bounds__(kPrefixRows * kPrefixSeg)
 cta_prefix_kernel(int32_t *__restrict__ cmat, int G, int64_t n_rows, int64_t *__restrict__ rcnt) {
@@ -1099,6 +1108,12 @@ struct MttkrpLayout {
 
 extern "C" {
 
+int rcp_set_mttkrp_mode(int mode) {
+  const int prev = mttkrp_mode();
+  if (mode >= 0) g_mttkrp_mode = mode ? 1 : 0;
+  return prev;
+}
+
 size_t rcp_mttkrp_ws_bytes(int64_t J, int64_t store_nnz, int64_t n_rows, int R) {
   MttkrpLayout L(J, store_nnz, n_rows, R);
   return L.total;
@@ -1170,15 +1185,12 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   // 1. dedup
   // The row-tile path (row tiles fit one scan, < 2^22 samples) writes every output row
   // itself; the row-transpose path (large row counts, or RCP_MTTKRP_PATH=rows) zeroes first.
-  static const int force_rows = [] {
-    const char *e = getenv("RCP_MTTKRP_PATH");
-    return e && !strcmp(e, "tiles") ? 0 : 1;
-  }();
+  const int force_rows = mttkrp_mode() == 1 ? 0 : 1;
   const int tile_np = R <= 64 ? 1 : 2;
   const int tile_ts = tile_np == 1 ? 4 : 3;
   const int64_t n_tiles = ceil_div(n_rows, (int64_t)1 << tile_ts);
   const bool tiles = !force_rows && n_tiles <= kTileMaxTiles && J < (1LL << 22) &&
-                     cap < (1LL << 31) && sm_count() <= kPrefixSeg * kPrefixMaxPer;
+                     cap < (1LL << 31) && 2 * sm_count() <= kPrefixSeg * kPrefixMaxPer;
 
   unsigned long long *twmin = (unsigned long long *)P(L.o_twmin);
   unsigned long long *twmax = (unsigned long long *)P(L.o_twmax);
@@ -1220,7 +1232,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   item_fill_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(ioff, S, ifib);
   RCP_LAUNCH_CHECK("item_fill");
   if (tiles) {
-    const int grid = sm_count();
+    const int grid = 2 * sm_count();                    // pair passes: 2 CTAs per SM
     const int nt = (int)n_tiles;
     int32_t *cmat = (int32_t *)P(L.o_cmat);            // grid x n_tiles
     int64_t *tcntp = rcnt, *tptr = rptr;                // pairs per tile, tile pointers
@@ -1243,8 +1255,8 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     RCP_CUDA_TRY(cudaMemsetAsync(tdone, 0, sizeof(int32_t) * kTileMaxTiles, st));
     RCP_CUDA_TRY(cudaMemsetAsync(tmask, 0, sizeof(uint32_t) * kTileMaxTiles, st));
     const size_t hsm = sizeof(int32_t) * nt;
-    if (tile_ts == 4) tile_hist_kernel<4><<<grid, kTraverseThreads, hsm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, cmat);
-    else tile_hist_kernel<3><<<grid, kTraverseThreads, hsm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, cmat);
+    if (tile_ts == 4) tile_hist_kernel<4><<<grid, kPairThreads, hsm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, cmat);
+    else tile_hist_kernel<3><<<grid, kPairThreads, hsm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, cmat);
     RCP_LAUNCH_CHECK("tile_hist");
     cta_prefix_kernel<<<(unsigned)ceil_div(nt, kPrefixRows), kPrefixRows * kPrefixSeg, 0, st>>>(
         cmat, grid, nt, tcntp);
@@ -1252,18 +1264,18 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     rc = scan_i64_exclusive(tcntp, tptr, nt, nullptr, scan_ws, st);
     if (rc) return rc;
     const size_t ssm = pair_scatter_smem(nt);
-    if (tile_ts == 4) pair_scatter_kernel<4><<<grid, kTraverseThreads, ssm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, tptr, cmat, pairs);
-    else pair_scatter_kernel<3><<<grid, kTraverseThreads, ssm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, tptr, cmat, pairs);
+    if (tile_ts == 4) pair_scatter_kernel<4><<<grid, kPairThreads, ssm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, tptr, cmat, pairs);
+    else pair_scatter_kernel<3><<<grid, kPairThreads, ssm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, tptr, cmat, pairs);
     RCP_LAUNCH_CHECK("pair_scatter");
     tile_units_kernel<<<1, 1024, 0, st>>>(tcntp, nt, uoff, sbase);
     RCP_LAUNCH_CHECK("tile_units");
-    const unsigned sg = (unsigned)(2 * sm_count());
+    const unsigned sg = (unsigned)(4 * sm_count());   // 4 CTAs of 4 warps per SM (smem, registers)
     if (tile_np == 1)
-      tile_spmm_kernel<4, 1><<<sg, kTileWarps * 32, tile_spmm_smem<4, 1>(), st>>>(tptr, nt, n_rows, uoff, sbase, pairs, d_rows, d_vals,
-                                                              Hs, R, d_out, scratch, tdone, tmask, d_stats);
+      tile_spmm_kernel<4, 1><<<sg, kTileWarps * 32, tile_spmm_smem<4, 1>(), st>>>(
+          tptr, nt, n_rows, uoff, sbase, pairs, d_rows, d_vals, Hs, R, d_out, scratch, tdone, tmask, d_stats);
     else
-      tile_spmm_kernel<3, 2><<<sg, kTileWarps * 32, tile_spmm_smem<3, 2>(), st>>>(tptr, nt, n_rows, uoff, sbase, pairs, d_rows, d_vals,
-                                                              Hs, R, d_out, scratch, tdone, tmask, d_stats);
+      tile_spmm_kernel<3, 2><<<sg, kTileWarps * 32, tile_spmm_smem<3, 2>(), st>>>(
+          tptr, nt, n_rows, uoff, sbase, pairs, d_rows, d_vals, Hs, R, d_out, scratch, tdone, tmask, d_stats);
     RCP_LAUNCH_CHECK("tile_spmm");
     return RCP_OK;
   }

@@ -24,6 +24,7 @@
 
 #include "tile_apply_ptx.cuh"
 
+
 constexpr int kTilePart = 2048;         // pairs per spmm part (4 warps x 512)
 constexpr int kTileWarps = 4;
 constexpr int kScatterItems = 1024;     // items per pair_scatter chunk (spans cached in smem)
@@ -77,8 +78,10 @@ __global__ void rep_compact_kernel(const int64_t *__restrict__ flag, const int64
 // A warp loads all (<= kItemE / 32) windows of its item at once, then flags run starts.
 constexpr int kItemWin = (int)(kItemE / 32);
 
+constexpr int kPairThreads = 512;   // pair passes: 16 warps x 2 CTAs per SM
+
 template <int TS>
-__global__ void __launch_bounds__(kTraverseThreads)
+__global__ void __launch_bounds__(kPairThreads, 2)
 tile_hist_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
                  const int32_t *__restrict__ ifib, const int64_t *__restrict__ dlo,
                  const int64_t *__restrict__ dlen, const int32_t *__restrict__ rows, int n_tiles,
@@ -114,7 +117,7 @@ tile_hist_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ S
 }
 
 // Block-wide exclusive scan of n <= 4 * blockDim.x int32 values in shared memory (in place);
-// returns the total.  blockDim.x == 1024.
+// returns the total.  blockDim.x a multiple of 32, <= 1024.
 __device__ int block_scan_excl(int32_t *a, int n) {
   __shared__ int32_t wsum[32];
   __shared__ int32_t total;
@@ -135,7 +138,7 @@ __device__ int block_scan_excl(int32_t *a, int n) {
   if (lane == 31) wsum[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    int32_t w = wsum[lane];
+    int32_t w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
     int32_t z = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -159,14 +162,14 @@ __device__ int block_scan_excl(int32_t *a, int n) {
 
 // ---------------------------------------------------------------- pass 2: pair scatter
 // The CTA's items are cut into units of up to kUnitWin consecutive 32-entry windows of one
-// item; 32 units (one per warp) form a batch.  Within a batch a tile receives at most one
+// item; one unit per warp forms a batch.  Within a batch a tile receives at most one
 // pair per unit (a fiber has one pair per tile), ranked by warp index through a per-tile
 // bit mask; the batch order and the unit -> warp assignment are fixed, so every pair's slot
 // is a function of the input only.  Item spans are cached in shared memory per chunk.
 constexpr int kUnitWin = 4;
 
 template <int TS>
-__global__ void __launch_bounds__(kTraverseThreads)
+__global__ void __launch_bounds__(kPairThreads, 2)
 pair_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
                     const int32_t *__restrict__ ifib, const int64_t *__restrict__ dlo,
                     const int64_t *__restrict__ dlen, const int32_t *__restrict__ rows,
@@ -246,8 +249,9 @@ pair_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict_
       }
       return L;
     };
+    const int nwarp = (int)(blockDim.x >> 5);   // units per batch (one per warp)
     UnitLoad cu = load_unit(wid);
-    for (int ub = 0; ub < nu; ub += 32) {
+    for (int ub = 0; ub < nu; ub += nwarp) {
       unsigned own = 0u;        // bit v: this lane owns the pair starting in window v
       int32_t tl[kUnitWin];
       int cnt[kUnitWin];
@@ -284,7 +288,7 @@ pair_scatter_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict_
       }
       const int64_t base = cu.base;
       const int32_t d = cu.d;
-      cu = load_unit(ub + 32 + wid);   // next batch's loads fly during the barriers
+      cu = load_unit(ub + nwarp + wid);   // next batch's loads fly during the barriers
       __syncthreads();
       unsigned m[kUnitWin];
 #pragma unroll
@@ -369,10 +373,10 @@ __device__ __forceinline__ void tile_apply<8, 2>(double2 (&a)[8][2], int g, doub
 // 16-byte record {value, row} per entry.
 template <int TR, int NP>
 struct TileSlotLayout {
-  static constexpr int BS = NP == 1 ? 16 : 8;       // pairs per batch
+  static constexpr int BS = NP == 1 ? 8 : 4;        // pairs per batch
   static constexpr int LPP = 32 / BS;               // lanes per pair
   static constexpr uint32_t E = 512u * NP;          // entry records
-  static constexpr uint32_t bytes = E + 16u * TR;
+  static constexpr uint32_t bytes = E + 16u * (TR + 1);   // +1: the loop reads one record ahead
 };
 
 __device__ __forceinline__ void cpa16_u32(uint32_t s, const void *g) {
@@ -383,19 +387,6 @@ __device__ __forceinline__ void cpa8_u32(uint32_t s, const void *g) {
 }
 __device__ __forceinline__ void cpa4_u32(uint32_t s, const void *g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(g));
-}
-__device__ __forceinline__ void sts_u32(uint32_t s, uint32_t v) {
-  asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(s), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t lds_u32(uint32_t s) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(s) : "memory");
-  return v;
-}
-__device__ __forceinline__ double lds_f64(uint32_t s) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(s) : "memory");
-  return v;
 }
 __device__ __forceinline__ double2 lds_f64x2(uint32_t s) {
   double2 v;
@@ -412,7 +403,7 @@ constexpr size_t tile_spmm_smem() {
 }
 
 template <int TS, int NP>
-__global__ void __launch_bounds__(kTileWarps * 32, 2)
+__global__ void __launch_bounds__(kTileWarps * 32, 4)
 tile_spmm_kernel(const int64_t *__restrict__ tptr, int n_tiles, int64_t n_rows,
                  const int32_t *__restrict__ uoff, const int32_t *__restrict__ sbase,
                  const uint64_t *__restrict__ pairs, const int32_t *__restrict__ rows,
@@ -463,9 +454,28 @@ tile_spmm_kernel(const int64_t *__restrict__ tptr, int n_tiles, int64_t n_rows,
     const int nch = (R + 1) >> 1;                                   // 16-byte chunks per row
     const int nb = (int)ceil_div((int64_t)n, (int64_t)BS);
     int cnt_nx = 0, cnt_cu = 0;   // this lane's pair count in the requested / applied batch
+    // Pair records come from registers: rc holds the records of 32-pair group g0, rn of
+    // group g0 + 1 (loaded a group ahead).  The store entries of batch bi + kPF are
+    // prefetched into L2 while batch bi + 1 is copied, so the copies hit L2.
+    constexpr int kPF = 3;
+    int g0 = 0;
+    uint64_t rc = lane < n ? pairs[wa + lane] : 0ull;
+    uint64_t rn = 32 + lane < n ? pairs[wa + 32 + lane] : 0ull;
+    auto rec_of = [&](int ip) {   // ip in [32 g0, 32 g0 + 64)
+      const uint64_t x = __shfl_sync(0xffffffffu, rc, ip & 31);
+      const uint64_t y = __shfl_sync(0xffffffffu, rn, ip & 31);
+      return (ip >> 5) == g0 ? x : y;
+    };
     auto issue = [&](int bi) {
+      if (bi * BS >= 32 * (g0 + 1)) {   // warp-uniform: advance the record window
+        ++g0;
+        rc = rn;
+        rn = 32 * (g0 + 1) + lane < n ? pairs[wa + 32 * (g0 + 1) + lane] : 0ull;
+      }
       const int ip = bi * BS + jp;
-      const uint64_t pr = ip < n ? pairs[wa + ip] : 0ull;
+      const uint64_t pr = rec_of(ip);
+      const int ipf = (bi + kPF) * BS + jp;
+      const uint64_t pf = rec_of(ipf);
       const uint32_t sl = ring_u32 + (uint32_t)((bi & 1) * BS + jp) * kSlot;
       int c = 0;
       if (ip < n) {
@@ -481,6 +491,11 @@ tile_spmm_kernel(const int64_t *__restrict__ tptr, int n_tiles, int64_t n_rows,
           cpa8_u32(sl + kSlotE + 16u * e, vals + pe + e);
           cpa4_u32(sl + kSlotE + 16u * e + 8u, rows + pe + e);
         }
+      }
+      if (ipf < n && sub < 2) {
+        const int64_t pe = pair_pos(pf);
+        if (sub == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(vals + pe));
+        else asm volatile("prefetch.global.L2 [%0];" ::"l"(rows + pe));
       }
       cpa_commit();
       return c;
@@ -500,11 +515,14 @@ tile_spmm_kernel(const int64_t *__restrict__ tptr, int n_tiles, int64_t n_rows,
         for (int jj = 0; jj < NP; ++jj) h[jj] = lds_f64x2(sl + 16u * lane + 512u * jj);
         const int c = __shfl_sync(0xffffffffu, cnt_cu, j * LPP);
         uint32_t ea = sl + kSlotE;
-        for (int e = 0; e < c; ++e, ea += 16u) {
-          const double2 rec = lds_f64x2(ea);
+        double2 rec = lds_f64x2(ea);   // the next record is loaded before this one's branch
+        for (int e = 0; e < c; ++e) {
+          ea += 16u;
+          const double2 nx = lds_f64x2(ea);   // (past the last entry: unused slot bytes)
           const int g = __double2loint(rec.y) & (TR - 1);
           hmask |= 1u << g;
           tile_apply<TR, NP>(acc, g, rec.x, h);
+          rec = nx;
         }
       }
       __syncwarp();

@@ -452,6 +452,7 @@ class Cluster:
         self.timed = False
         self.phase_events = None
         self._side = None
+        self._nvtx_open = False
 
     def _tick(self, phase, t0):
         if not self.timed:
@@ -579,7 +580,17 @@ class Cluster:
 
     # -------------------------------------------------------------- solve
     def _ev(self, phase):
-        """Device-side phase marker (CUDA event on the current stream) when profiling."""
+        """Phase boundary: closes the previous NVTX range and opens `phase` (ranges are
+        named after the reference's ctx.timings phases, ref schedules.py:227-258; visible
+        in nsys/ncu --nvtx), and records a CUDA event on the current stream when
+        profiling."""
+        nv = torch().cuda.nvtx
+        if self._nvtx_open:
+            nv.range_pop()
+            self._nvtx_open = False
+        if phase != "end":
+            nv.range_push("rcp:" + phase)
+            self._nvtx_open = True
         if self.phase_events is None:
             return
         e = torch().cuda.Event(enable_timing=True)

@@ -115,3 +115,28 @@ def mttkrp_exact(mat: Matricization, factors, offsets=None, workers=1):
     out = t.empty((mat.n_rows, R), dtype=t.float64, device=dev)
     ops_for(dev).exact_mttkrp(mat.store, facs, offsets, out)
     return to_host(out)
+
+
+def set_mttkrp_mode(deterministic):
+    """Select the fused sampled MTTKRP's mode for subsequent solves (process-wide):
+    deterministic=True runs the row-tile x fiber pair path, whose every output row is
+    summed in a fixed order (bit-identical results run to run, like the reference's
+    worker-count invariance, ref tests/test_mttkrp.py:60-67,163-172); False the faster
+    row-transpose path.  Returns the previous setting (C ABI rcp_set_mttkrp_mode)."""
+    from . import _lib
+    return bool(_lib.lib().rcp_set_mttkrp_mode(1 if deterministic else 0))
+
+
+class deterministic_mttkrp:
+    """Context manager: deterministic sampled MTTKRP inside the block."""
+
+    def __init__(self, on=True):
+        self.on = on
+
+    def __enter__(self):
+        self.prev = set_mttkrp_mode(self.on)
+        return self
+
+    def __exit__(self, *exc):
+        set_mttkrp_mode(self.prev)
+        return False

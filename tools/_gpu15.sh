@@ -1,0 +1,3 @@
+export RCP_MTTKRP_PATH=tiles
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --profile-from-start off --log-file gpurun_out/launches15.csv python tools/prof_round.py > gpurun_out/ncu15.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:tile_csr -s 2 -c 1 -o gpurun_out/tile_csr15 python tools/prof_round.py > gpurun_out/ncu15b.log 2>&1
