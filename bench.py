@@ -97,18 +97,24 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ workload
-def make_tensor(cfg_name, seed, dev):
+def make_tensor(cfg_name, seed, dev, rank_grid=None):
     """Synthetic tensor of the named config on `dev` (torch tensors), reference
-    load-balancing permutation applied (ref tensor.py:207-210)."""
+    load-balancing permutation applied (ref tensor.py:207-210).  rank_grid=(grid, rank):
+    device-generated configs keep only that rank's accumulator-stationary blocks."""
     import torch
     from paper_2210_05105_b200 import rng, synth
     c = synth.CONFIGS[cfg_name]
     perm_of = lambda j, d: rng.permutation(rng.stream_key(seed, rng.TENSOR_PERM, j), d)  # noqa: E731
     if c["kind"] == "zipf_device":   # C4/C5: generated, deduplicated and permuted on the GPU
         perms = [perm_of(j, d) for j, d in enumerate(c["dims"])]
+        keep = None
+        if rank_grid is not None:
+            g, p = rank_grid
+            keep = [g.block_range(j, p) for j in range(len(c["dims"]))]
         chunks = synth.zipf_chunks(c["dims"], c["draws"], c["s"], seed=seed, values=c["values"],
                                    sigma=c.get("sigma", 1.0), parts=c["parts"], device=dev,
-                                   perms=perms, log=lambda m: print(m, file=sys.stderr, flush=True))
+                                   perms=perms, log=lambda m: print(m, file=sys.stderr, flush=True),
+                                   keep=keep)
         return c, chunks, None
     if c["kind"] == "planted":
         idx, vals = synth.planted_c1(seed=seed)
@@ -163,18 +169,32 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     t_setup = time.perf_counter()
-    c, idx, vals = make_tensor(args.config, args.seed, dev)
+    balance = args.balance if args.balance != "auto" else ("nnz" if world > 1 else "rows")
+    rank_grid = None
+    from paper_2210_05105_b200 import synth as _synth
+    cdef = _synth.CONFIGS[args.config]
+    if spmd and cdef["kind"] == "zipf_device":
+        # per-rank ingest: the grid first (nnz cuts from the expected Zipf row weights), then
+        # every rank generates the tensor and keeps only its own blocks
+        from paper_2210_05105_b200 import rng as _rng
+        from paper_2210_05105_b200.grid import ProcessorGrid, optimal_grid
+        rw = None
+        if balance == "nnz":
+            perms = [_rng.permutation(_rng.stream_key(args.seed, _rng.TENSOR_PERM, j), d)
+                     for j, d in enumerate(cdef["dims"])]
+            rw = _synth.zipf_expected_row_weights(cdef["dims"], cdef["s"], perms)
+        rank_grid = (optimal_grid(cdef["dims"], world, row_weights=rw), rank)
+    c, idx, vals = make_tensor(args.config, args.seed, dev, rank_grid=rank_grid)
     dims = c["dims"]
     R = args.rank or c["R"]
     J = args.samples or c["J"]
     N = len(dims)
     nnz = sum(int(ch[0].shape[0]) for ch in idx) if isinstance(idx, list) else int(idx.shape[0])
     t_gen = time.perf_counter() - t_setup
-    balance = args.balance if args.balance != "auto" else ("nnz" if world > 1 else "rows")
     if spmd:
         from paper_2210_05105_b200.dist import make_spmd_cluster
         cl = make_spmd_cluster(dims, idx, vals, R, J, args.sampler, args.seed, leaf=args.leaf,
-                               balance=balance)
+                               balance=balance, grid=rank_grid[0] if rank_grid else None)
     else:
         cl = make_local_cluster(dims, idx, vals, R, J, args.sampler, args.seed, leaf=args.leaf,
                                 balance=balance)
@@ -416,8 +436,23 @@ def cpu_baseline(args, cl, c, samples=None):
     csr = O.sampled_csr(ostore, X, k)
     out = O.sketched_mttkrp(csr, H, w, workers=workers)
     dt = time.perf_counter() - t0
-    del out
+    # parity on the benchmarked batch (untimed): the fused GPU MTTKRP of the same samples
+    dev = me.X.device
+    Xd = me.X[:, :samples].contiguous()
+    gout = torch.empty((st.n_rows, me.R), dtype=torch.float64, device=dev)
+    gst = torch.zeros(8, dtype=torch.int64, device=dev)
+    me.ops.sampled_mttkrp(st, Xd, k, me.H[:samples].contiguous(), me.w[:samples].contiguous(),
+                          gout, gst)
+    got = gout.cpu().numpy()
+    parity = {"samples": int(samples), "mode": int(k),
+              "max_rel_err": float(np.abs(got - out).max() / max(np.abs(out).max(), 1e-300)),
+              "gathered_nnz_gpu": int(gst[3]), "gathered_nnz_oracle": int(csr.nnz),
+              "bar": "max_rel_err <= 1e-9, equal gathered nonzeros"}
+    parity["ok"] = bool(parity["max_rel_err"] <= 1e-9 and
+                        parity["gathered_nnz_gpu"] == parity["gathered_nnz_oracle"])
+    del out, gout
     return {"value": csr.nnz / dt, "unit": UNIT, "cores": workers, "kind": "port",
+            "parity": parity,
             "sample": "oracle gather_sampled_nonzeros_to_csr + downsampled_mttkrp, mode %d of %s, "
                       "first %d of J=%d samples of a device STS/ARLS batch; %d nnz iterated in %.2f s "
                       "(store conversion %.1f s untimed)" % (k, args.config, samples, cl.J, csr.nnz,

@@ -81,7 +81,7 @@ def comm_words_per_solve(J, R, N, P, sampler):
 
 
 def make_spmd_cluster(dims, idx, vals, R, J, sampler, seed, grid_dims=None, leaf=None,
-                      factors=None, trial=0, balance="rows"):
+                      factors=None, trial=0, balance="rows", grid=None):
     """This process's rank of a P-GPU accumulator-stationary cluster.  idx/vals: the
     tensor's COO on this GPU (every rank may hold all of it; only the rows of its blocks
     are kept in its stores).  Ownership follows the reference processor grid."""
@@ -94,7 +94,8 @@ def make_spmd_cluster(dims, idx, vals, R, J, sampler, seed, grid_dims=None, leaf
     P = dist.get_world_size()
     rank = dist.get_rank()
     from .engine import make_grid
-    grid = make_grid(dims, P, grid_dims, idx, balance)
+    if grid is None:   # (a caller that ingested only its blocks passes the grid it used)
+        grid = make_grid(dims, P, grid_dims, idx, balance)
     if grid.P != P:
         raise ValueError("grid %s has %d ranks, world size is %d" % (grid.grid_dims, grid.P, P))
     if factors is None:

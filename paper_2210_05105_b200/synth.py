@@ -173,15 +173,34 @@ def zipf_tensor(dims, target, s, seed=0, values="lognormal", sigma=1.0, device="
     return idx, v
 
 
+def zipf_expected_row_weights(dims, s, perms=None):
+    """Expected share of draws per (permuted) row of every mode: the finite Zipf(s) pmf
+    moved through the mode permutation (row perm[i] carries the weight of i).  Used to cut
+    nnz-balanced row blocks before a rank ingests only its own blocks (the exact counts
+    need the whole tensor)."""
+    out = []
+    for j, d in enumerate(dims):
+        w = np.arange(1, int(d) + 1, dtype=np.float64) ** (-float(s))
+        if perms is not None:
+            pw = np.empty_like(w)
+            pw[np.asarray(perms[j], dtype=np.int64)] = w
+            w = pw
+        out.append(w / w.sum())
+    return out
+
+
 def zipf_chunks(dims, draws, s, seed=0, values="lognormal", sigma=1.0, parts=16,
-                chunk_bits=28, device=None, perms=None, log=None):
+                chunk_bits=28, device=None, perms=None, log=None, keep=None):
     """Device ingest for C4/C5 (ingest.cu): `draws` Zipf draws of the splitmix stream of
     `zipf_tensor` (chunks of 2^chunk_bits draws), duplicates summed in draw order, all
     distinct cells kept.  One pass over the draw sequence per hash partition of the cell
     space keeps the working set at ~draws/parts cells; a cell's draws are summed in
     ascending value order (reproducible).  Coordinates are mapped through
     `perms` (the reference's per-mode load-balancing permutations, ref tensor.py:207-210).
-    Returns a list of (idx int32 [n, N], vals fp64 [n]) CUDA tensors, one per partition."""
+    Returns a list of (idx int32 [n, N], vals fp64 [n]) CUDA tensors, one per partition.
+    keep: optional per-mode (lo, hi) row ranges -- each partition then keeps only the cells
+    with at least one mode index inside its range (a rank's accumulator-stationary blocks,
+    ref matricization.py:187-198), so a rank never holds the whole tensor."""
     import torch
     from .ops import ops_for
     dev = torch.device(device) if device is not None else torch.device("cuda", 0)
@@ -236,9 +255,17 @@ def zipf_chunks(dims, draws, s, seed=0, values="lognormal", sigma=1.0, parts=16,
         v = torch.empty(nc, dtype=torch.float64, device=dev)
         ops.cells(sk, sv, starts, dims, pdev, values == "log1p_poisson", idx, v)
         del sk, sv, starts
+        if keep is not None:
+            sel = torch.zeros(nc, dtype=torch.bool, device=dev)
+            for j, (lo, hi) in enumerate(keep):
+                col = idx[:, j]
+                sel |= (col >= int(lo)) & (col < int(hi))
+            idx, v = idx[sel].contiguous(), v[sel].contiguous()
+            del sel
         chunks.append((idx, v))
         if log:
-            log("partition %d/%d: %d draws -> %d cells" % (p + 1, parts, n, nc))
+            log("partition %d/%d: %d draws -> %d cells%s" % (
+                p + 1, parts, n, nc, "" if keep is None else " (%d kept)" % idx.shape[0]))
     return chunks
 
 

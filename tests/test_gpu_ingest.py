@@ -129,3 +129,40 @@ def test_engine_on_chunks_matches_coo_engine():
     assert torch.equal(a.ranks[0].X, b.ranks[0].X)
     for j in range(3):
         assert torch.allclose(a.ranks[0].U[j], b.ranks[0].U[j], rtol=1e-12, atol=1e-14)
+
+
+def test_zipf_chunks_keep_only_rank_blocks():
+    """Per-rank ingest: with keep=<a rank's block ranges>, every partition keeps exactly the
+    cells of the full ingest that have at least one mode index in the rank's blocks
+    (ref matricization.py:187-198); the ranks' stores built from their kept cells equal the
+    stores built from the whole tensor."""
+    from paper_2210_05105_b200.grid import optimal_grid
+    from paper_2210_05105_b200.store import build_store_chunks
+    dims = (300, 200, 250)
+    perms = [np.random.default_rng(j).permutation(d) for j, d in enumerate(dims)]
+    full = synth.zipf_chunks(dims, 1 << 15, 1.2, seed=5, parts=4, chunk_bits=13, perms=perms)
+    w = synth.zipf_expected_row_weights(dims, 1.2, perms)
+    assert all(abs(x.sum() - 1.0) < 1e-12 for x in w)
+    g = optimal_grid(dims, 4, row_weights=w)
+    fidx = np.concatenate([c[0].cpu().numpy() for c in full]).astype(np.int64)
+    for p in range(4):
+        keep = [g.block_range(j, p) for j in range(3)]
+        mine = synth.zipf_chunks(dims, 1 << 15, 1.2, seed=5, parts=4, chunk_bits=13, perms=perms,
+                                 keep=keep)
+        midx = np.concatenate([c[0].cpu().numpy() for c in mine]).astype(np.int64)
+        sel = np.zeros(len(fidx), dtype=bool)
+        for j, (lo, hi) in enumerate(keep):
+            sel |= (fidx[:, j] >= lo) & (fidx[:, j] < hi)
+        assert np.array_equal(canon(midx, np.zeros(len(midx)))[0],
+                              canon(fidx[sel], np.zeros(int(sel.sum())))[0])
+        for j, (lo, hi) in enumerate(keep):
+            a = build_store_chunks(dims, mine, j, lo, hi)
+            b = build_store_chunks(dims, full, j, lo, hi)
+            assert a.nnz == b.nnz
+            assert torch_equal(a.keys, b.keys) and torch_equal(a.rows, b.rows)
+            assert torch_equal(a.vals, b.vals)
+
+
+def torch_equal(x, y):
+    import torch
+    return bool(torch.equal(x, y))
