@@ -73,10 +73,6 @@ constexpr int kMaxDepth = 30;   // local tree depth limit (2^30 leaves)
 // [kGenBase + g] runs pushed during generation g (each generation has its own counter, so
 // the extent of generation g + 1 is stable once every CTA has passed the barrier)
 constexpr int kGenBase = 8;
-constexpr int kCtlFinished = 2;       // samples whose walk ended (leaf or degenerate)
-constexpr int kCtlParticipants = 4;   // samples walked (set by the seed kernel)
-constexpr int kCtlHead = 5;           // next run to claim
-constexpr int kCtlTail = 6;           // runs pushed after the seeds
 // per level: [start time, runs] at 2 l, then [last warp finish, ~first warp finish] at
 // 2 (kMaxDepth + 2) + 2 l (global timer, ns).  With -DRCP_WALK_TRACE also, per level, the
 // longest time any warp spent in each phase of one run (claim -> run record, -> h row,
@@ -98,7 +94,7 @@ struct Run {
 
 struct WalkWs {
   size_t o_key, o_key2, o_r, o_r2, o_idx, o_idx2, o_idx3, o_runs, o_ctl, o_mp, o_pairs, o_gm,
-      o_cub, o_prof, o_ready, total;
+      o_cub, o_prof, total;
   size_t cub_bytes;
   int64_t nruns;
   WalkWs(int64_t J, int depth, int R) {
@@ -129,7 +125,6 @@ struct WalkWs {
     o_gm = add(8 * Rs * (size_t)((2LL << depth) - 1));   // G (.) M' for every tree node
     o_cub = add(cub_bytes + 256);
     o_prof = add(kProfBytes);   // per level: global timer at the level start, runs
-    o_ready = add(sizeof(int) * nruns);   // publication flags of the task queue
     total = t + 256;
   }
 };
@@ -212,10 +207,12 @@ __global__ void walk_seed_kernel(const int64_t *__restrict__ key, const int32_t 
                                  int64_t J, const double *__restrict__ pmp_in, Run *runs,
                                  int *ctl) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t k = s < J ? key[s] : INT64_MAX;
-  const int part = __syncthreads_count(k != INT64_MAX);
-  if (threadIdx.x == 0 && part) atomicAdd(&ctl[kCtlParticipants], part);
+  if (s >= J) return;
+  const int64_t k = key[s];
   if (k == INT64_MAX) return;
+#if RCP_WALK_PROF
+  atomicAdd(&ctl[3], 1);
+#endif
   if (s > 0 && key[s - 1] == k) return;
   int64_t lo = s + 1, hi = J;   // first position with a larger key
   while (lo < hi) {
@@ -292,19 +289,64 @@ __global__ void walk_gm_kernel(const double *__restrict__ tree, const double2 *_
   }
 }
 
-// A run as published by another warp: read through L2 (the slot may hold an earlier
-// walk's run in this SM's L1).
-__device__ __forceinline__ Run load_run(const Run *p) {
-  const int4 a = __ldcg(reinterpret_cast<const int4 *>(p));
-  const int4 b = __ldcg(reinterpret_cast<const int4 *>(p) + 1);
-  Run r;
-  r.lo = a.x;
-  r.hi = a.y;
-  r.level = a.z;
-  r.node = a.w;
-  r.prob = __hiloint2double(b.y, b.x);
-  r.qv = __hiloint2double(b.w, b.z);
-  return r;
+// Warp-cooperative push of a child run (path of the parent + one step) into the next
+// level's generation.  Runs entering the leaf level are cut into chunks so that the
+// per-sample leaf work spreads over warps.
+
+
+// Child runs are staged in a per-CTA shared buffer and published with one global
+// reservation per CTA and level (a global counter taking one atomic per child run
+// serialised ~2*10^4 same-address atomics per level); a full buffer falls back to the
+// global counter.
+constexpr int kStage = 224;   // two CTAs of 16 walker warps per SM at R = 50
+
+struct Stage {
+  Run buf[kStage];
+  int count;
+  int base;
+};
+
+__device__ __forceinline__ void push_child(Run *runs, int *gen_cnt, int64_t base, int64_t cap,
+                                           int *status, Stage &stg, const Run &par, int32_t lo,
+                                           int32_t hi, double T, bool right, double qv, int depth,
+                                           int lane) {
+  const int lev = par.level;
+  const int32_t chunk = (lev + 1 == depth) ? kLeafChunk : kMaxRun;
+  for (int32_t c0 = lo; c0 < hi; c0 += chunk) {
+    if (lane == 0) {
+      Run c;
+      c.lo = c0;
+      c.hi = min(hi, c0 + chunk);
+      c.level = lev + 1;
+      c.node = 2 * par.node + (right ? 1 : 0);
+      c.prob = par.prob * (right ? (1.0 - T) : T);
+      c.qv = qv;
+      const int t = atomicAdd(&stg.count, 1);
+      if (t < kStage) {
+        stg.buf[t] = c;
+      } else {
+        const int g = atomicAdd(gen_cnt, 1);
+        if (base + g >= cap) raise_status(status, RCP_ST_CAPACITY);   // cannot happen: one
+        else runs[base + g] = c;   // level holds at most J disjoint runs
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// End of a level: the CTA's staged children go to the next level's array.
+__device__ __forceinline__ void publish_children(Run *runs, int *gen_cnt, int64_t base,
+                                                 int64_t cap, int *status, Stage &stg) {
+  __syncthreads();
+  const int n = min(stg.count, kStage);
+  if (threadIdx.x == 0) stg.base = n ? atomicAdd(gen_cnt, n) : 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t o = base + stg.base + i;
+    if (o >= cap) raise_status(status, RCP_ST_CAPACITY);
+    else runs[o] = stg.buf[i];
+  }
+  if (threadIdx.x == 0) stg.count = 0;
 }
 
 // A degenerate run (zero node or leaf mass: ref DegenerateWalkError samplers.py:428-430)
@@ -336,7 +378,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
                  int32_t *__restrict__ iB, Run *runs,
                  int *ctl, int64_t cap_runs, int64_t *__restrict__ Xi, double *__restrict__ pmp,
                  double *__restrict__ resid, double *__restrict__ Hout, int *status,
-                 int *ready) {
+                 unsigned long long *prof) {
   extern __shared__ double sh[];
   const int Rs = tri_stride(R);                    // even node stride (zero pad)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -353,252 +395,277 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
     Mp[e] = (k < R && c < R) ? Mfull[k * R + c] : 0.0;
   }
   __syncthreads();
-  // Task queue, no grid barrier: a task is a run (samples with one Hadamard row at one
-  // node, a range [lo, hi) of its level's buffer).  A run partitions its range into its
-  // children's ranges of the other buffer, so runs at different levels never touch the
-  // same entries unless one descends from the other -- which runs only after its parent
-  // finished.  A warp keeps descending into its first child and pushes the others;
-  // idle warps claim pushed runs in push order.  Each sample's path depends only on its
-  // own residual and row: the schedule cannot change any result.
-  const int seeded = ld_volatile(&ctl[0]);
-  const int total = ld_volatile(&ctl[kCtlParticipants]);
-  Run run;
-  bool have = false;
-  while (true) {
-    if (!have) {
-      int t = 0;
-      if (lane == 0) t = atomicAdd(&ctl[kCtlHead], 1);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      if (t >= seeded) {   // wait until run t is published, or every sample is done
-        bool done = false;
-        while (true) {
-          int rdy = 0, fin = 0;
-          if (lane == 0) {
-            rdy = t < cap_runs ? ld_volatile(&ready[t]) : 0;
-            fin = ld_volatile(&ctl[kCtlFinished]);
-          }
-          rdy = __shfl_sync(0xffffffffu, rdy, 0);
-          fin = __shfl_sync(0xffffffffu, fin, 0);
-          if (rdy) break;
-          if (fin >= total) {
-            done = true;
-            break;
-          }
-          __nanosleep(128);
-        }
-        if (done) break;
-        __threadfence();
-      }
-      run = load_run(runs + t);
+  cg::grid_group grid = cg::this_grid();
+  // Level-synchronous: the runs of level l are [begin, end); their children go to level
+  // l + 1 through that level's own counter, whose value is stable after the grid barrier.
+  __shared__ int claim;
+  __shared__ Stage stg;
+#if RCP_WALK_PROF
+  __shared__ unsigned long long fin_last, fin_first_inv;   // this CTA's warps, this level
+#endif
+#ifdef RCP_WALK_TRACE
+  __shared__ unsigned long long ph_max[4];
+  auto gtime = []() {
+    unsigned long long x;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(x));
+    return x;
+  };
+#endif
+  if (threadIdx.x == 0) stg.count = 0;
+  int64_t begin = 0, end = min((int64_t)ld_volatile(&ctl[0]), cap_runs);
+  for (int lvl = 0; lvl <= depth && end > begin; ++lvl) {
+    int *gen_cnt = &ctl[kGenBase + lvl];
+    // this CTA's runs begin + blockIdx.x + k gridDim.x (spread over the level), claimed one
+    // by one by its warps
+    if (threadIdx.x == 0) {
+      claim = 0;
+#if RCP_WALK_PROF
+      fin_last = 0ull;
+      fin_first_inv = 0ull;
+#endif
+#ifdef RCP_WALK_TRACE
+      ph_max[0] = ph_max[1] = ph_max[2] = ph_max[3] = 0ull;
+#endif
     }
-    have = false;
-    const int32_t lo = run.lo, hi = run.hi, level = run.level;
-    const double *rs = (level & 1) ? rB : rA;
-    const int32_t *is = (level & 1) ? iB : iA;
-    const int32_t s0 = __ldcg(is + lo);
-    for (int c = lane; c < R; c += 32) hv[c] = H ? H[(int64_t)s0 * R + c] : 1.0;
-    __syncwarp();
-    if (level < depth) {
-      // child masses <GM_child, h h^T> over the packed triangle, two positions per step
-      // T = max(q_left, 0) / q_node (ref samplers.py:423-451).  q_node is inherited from
-      // the parent by left children; right children and seeds compute it here, in the
-      // same pass as q_left.
-      const int64_t v = run.node;
-      const double2 *GL = reinterpret_cast<const double2 *>(
-          gm + ((1LL << (level + 1)) - 1 + 2 * v) * (int64_t)Rs);
-      const double2 *GV = reinterpret_cast<const double2 *>(
-          gm + ((1LL << level) - 1 + v) * (int64_t)Rs);
-      const uint2 *PR = reinterpret_cast<const uint2 *>(pairs);
-      const bool known = !isnan(run.qv);
-      double qL = 0.0, qV = 0.0, qL2 = 0.0, qV2 = 0.0;
-      const int n2 = Rs / 2;
-      if (known) {
-#pragma unroll (kWalkUnroll)
-        for (int e = lane; e < n2; e += 32) {
-          const double2 gl = __ldg(GL + e);
-          const uint2 ab = PR[e];
-          const double h0 = hv[ab.x & 0xffffu] * hv[ab.x >> 16];
-          const double h1 = hv[ab.y & 0xffffu] * hv[ab.y >> 16];
-          qL = fma(gl.x, h0, qL);
-          qL2 = fma(gl.y, h1, qL2);
+    if (threadIdx.x == 0 && blockIdx.x == 0) {   // level start time and run count
+      unsigned long long tnow;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+      prof[2 * lvl] = tnow;
+      prof[2 * lvl + 1] = (unsigned long long)(end - begin);
+    }
+    __syncthreads();
+    while (true) {
+      int tc = 0;
+      if (lane == 0) tc = atomicAdd(&claim, 1);
+      const int64_t t = begin + blockIdx.x + (int64_t)__shfl_sync(0xffffffffu, tc, 0) * gridDim.x;
+      if (t >= end) {
+#if RCP_WALK_PROF
+        if (lane == 0) {   // this warp's finish time for the per-level record
+          unsigned long long tnow;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+          atomicMax(&fin_last, tnow);
+          atomicMax(&fin_first_inv, ~tnow);
         }
-      } else {
+#endif
+        break;
+      }
+#ifdef RCP_WALK_TRACE
+      const unsigned long long tr0 = gtime();
+#endif
+      const Run run = runs[t];
+      const int32_t lo = run.lo, hi = run.hi, level = run.level;
+      const double *rs = (level & 1) ? rB : rA;
+      const int32_t *is = (level & 1) ? iB : iA;
+      const int32_t s0 = is[lo];
+#ifdef RCP_WALK_TRACE
+      const unsigned long long tr1 = gtime();
+#endif
+      for (int c = lane; c < R; c += 32) hv[c] = H ? H[(int64_t)s0 * R + c] : 1.0;
+      __syncwarp();
+#ifdef RCP_WALK_TRACE
+      const unsigned long long tr2 = gtime();
+#endif
+      if (level < depth) {
+        // child masses <GM_child, h h^T> over the packed triangle, two positions per step
+        // T = max(q_left, 0) / q_node (ref samplers.py:423-451).  q_node is inherited from
+        // the parent by left children; right children and seeds compute it here, in the
+        // same pass as q_left.
+        const int64_t v = run.node;
+        const double2 *GL = reinterpret_cast<const double2 *>(
+            gm + ((1LL << (level + 1)) - 1 + 2 * v) * (int64_t)Rs);
+        const double2 *GV = reinterpret_cast<const double2 *>(
+            gm + ((1LL << level) - 1 + v) * (int64_t)Rs);
+        const uint2 *PR = reinterpret_cast<const uint2 *>(pairs);
+        const bool known = !isnan(run.qv);
+        double qL = 0.0, qV = 0.0, qL2 = 0.0, qV2 = 0.0;
+        const int n2 = Rs / 2;
+        if (known) {
 #pragma unroll (kWalkUnroll)
-        for (int e = lane; e < n2; e += 32) {
-          const double2 gl = __ldg(GL + e);
-          const double2 gv = __ldg(GV + e);
-          const uint2 ab = PR[e];
-          const double h0 = hv[ab.x & 0xffffu] * hv[ab.x >> 16];
-          const double h1 = hv[ab.y & 0xffffu] * hv[ab.y >> 16];
-          qL = fma(gl.x, h0, qL);
-          qL2 = fma(gl.y, h1, qL2);
-          qV = fma(gv.x, h0, qV);
-          qV2 = fma(gv.y, h1, qV2);
+          for (int e = lane; e < n2; e += 32) {
+            const double2 gl = __ldg(GL + e);
+            const uint2 ab = PR[e];
+            const double h0 = hv[ab.x & 0xffffu] * hv[ab.x >> 16];
+            const double h1 = hv[ab.y & 0xffffu] * hv[ab.y >> 16];
+            qL = fma(gl.x, h0, qL);
+            qL2 = fma(gl.y, h1, qL2);
+          }
+        } else {
+#pragma unroll (kWalkUnroll)
+          for (int e = lane; e < n2; e += 32) {
+            const double2 gl = __ldg(GL + e);
+            const double2 gv = __ldg(GV + e);
+            const uint2 ab = PR[e];
+            const double h0 = hv[ab.x & 0xffffu] * hv[ab.x >> 16];
+            const double h1 = hv[ab.y & 0xffffu] * hv[ab.y >> 16];
+            qL = fma(gl.x, h0, qL);
+            qL2 = fma(gl.y, h1, qL2);
+            qV = fma(gv.x, h0, qV);
+            qV2 = fma(gv.y, h1, qV2);
+          }
+        }
+        qL = warp_sum(qL + qL2);
+#ifdef RCP_WALK_TRACE
+        const unsigned long long tr3 = gtime();
+#endif
+        const double qnode = known ? run.qv : warp_sum(qV + qV2);
+        if (!(qnode > 0.0)) {
+          fail_run(lo, hi, is, Xi, Hout, R, status, ctl, lane);
+          continue;
+        }
+        double T = (qL > 0.0 ? qL : 0.0) / qnode;
+        T = fmin(fmax(T, 0.0), 1.0);
+        // partition the run's samples into the children's ranges of the next level's
+        // buffer (left from the front, right from the back), rescaling each residual
+        double *rd = (level & 1) ? rA : rB;
+        int32_t *id = (level & 1) ? iA : iB;
+        int32_t nl = 0, nr = 0;
+        const unsigned below = (1u << lane) - 1u;
+        constexpr int kPU = 4;   // 32-sample groups with loads in flight per step
+        for (int32_t q0 = lo; q0 < hi; q0 += 32 * kPU) {
+          double rv[kPU];
+          int32_t sv[kPU];
+#pragma unroll
+          for (int u = 0; u < kPU; ++u) {
+            const int32_t q = q0 + 32 * u + lane;
+            rv[u] = q < hi ? rs[q] : 0.0;
+            sv[u] = q < hi ? is[q] : 0;
+          }
+#pragma unroll
+          for (int u = 0; u < kPU; ++u) {
+            const int32_t q = q0 + 32 * u + lane;
+            const bool valid = q < hi;
+            const bool right = rv[u] >= T;
+            const unsigned ml = __ballot_sync(0xffffffffu, valid && !right);
+            const unsigned mr = __ballot_sync(0xffffffffu, valid && right);
+            if (valid) {
+              const int32_t o =
+                  right ? hi - 1 - (nr + __popc(mr & below)) : lo + nl + __popc(ml & below);
+              rd[o] = rescale(rv[u], T, right);
+              id[o] = sv[u];
+            }
+            nl += __popc(ml);
+            nr += __popc(mr);
+          }
+        }
+        const double unknown = __longlong_as_double(0x7ff8000000000000LL);
+        if (nl > 0)
+          push_child(runs, gen_cnt, end, cap_runs, status, stg, run, lo, lo + nl, T, false, qL, depth,
+                     lane);
+        if (nr > 0)
+          push_child(runs, gen_cnt, end, cap_runs, status, stg, run, lo + nl, hi, T, true, unknown,
+                     depth, lane);
+#ifdef RCP_WALK_TRACE
+        if (lane == 0) {
+          const unsigned long long tr4 = gtime();
+          atomicMax(&ph_max[0], tr1 - tr0);
+          atomicMax(&ph_max[1], tr2 - tr1);
+          atomicMax(&ph_max[2], tr3 - tr2);
+          atomicMax(&ph_max[3], tr4 - tr3);
+        }
+#endif
+        continue;
+      }
+      // ---- leaf block: masses z^T M' z of its rows z = u (.) h, then each sample's
+      // inverse CDF
+      const int64_t r0 = (int64_t)run.node * leaf;
+      const int nrow = (int)min((int64_t)leaf, n - r0);
+      const double rprob = run.prob;
+      bool bad = nrow <= 0;
+      double total_m = 0.0;
+      if (!bad) {
+        // 8-row tiles: Y = Z M on the fp64 tensor cores, mass_q = <Y_q, Z_q>
+        const int row = lane >> 2, quad = lane & 3;
+        for (int q0 = 0; q0 < nrow; q0 += 8) {
+          const int nb = min(8, nrow - q0);
+          for (int c = lane; c < 8 * Zs; c += 32) {
+            const int j = c / Zs, col = c - j * Zs;
+            zb[c] = (j < nb && col < R) ? U[(r0 + q0 + j) * R + col] * hv[col] : 0.0;
+          }
+          __syncwarp();
+          const double *zr = zb + row * Zs;
+          double msum = 0.0;
+          for (int nt = 0; nt < Rn; nt += 8) {
+            double c0 = 0.0, c1 = 0.0;
+            for (int ks = 0; ks < Rn; ks += 4)
+              dmma_8x8x4(c0, c1, zr[ks + quad], Mp[(ks + quad) * Ms + nt + row]);
+            msum = fma(c0, zr[nt + 2 * quad], msum);
+            msum = fma(c1, zr[nt + 2 * quad + 1], msum);
+          }
+          msum += __shfl_xor_sync(0xffffffffu, msum, 1);
+          msum += __shfl_xor_sync(0xffffffffu, msum, 2);
+          if (quad == 0 && row < nb) mass[q0 + row] = msum > 0.0 ? msum : 0.0;
+          __syncwarp();
         }
       }
-      qL = warp_sum(qL + qL2);
-      const double qnode = known ? run.qv : warp_sum(qV + qV2);
-      if (!(qnode > 0.0)) {
+      if (!bad) {
+        if (lane == 0)
+          for (int q = 0; q < nrow; ++q) total_m += mass[q];
+        total_m = __shfl_sync(0xffffffffu, total_m, 0);
+        bad = !(total_m > 0.0);
+      }
+      if (bad) {
         fail_run(lo, hi, is, Xi, Hout, R, status, ctl, lane);
         continue;
       }
-      double T = (qL > 0.0 ? qL : 0.0) / qnode;
-      T = fmin(fmax(T, 0.0), 1.0);
-      // partition the run's samples into the children's ranges of the other buffer (left
-      // from the front, right from the back), rescaling each residual
-      double *rd = (level & 1) ? rA : rB;
-      int32_t *id = (level & 1) ? iA : iB;
-      int32_t nl = 0, nr = 0;
-      const unsigned below = (1u << lane) - 1u;
-      constexpr int kPU = 4;   // 32-sample groups with loads in flight per step
-      for (int32_t q0 = lo; q0 < hi; q0 += 32 * kPU) {
-        double rv[kPU];
-        int32_t sv[kPU];
-#pragma unroll
-        for (int u = 0; u < kPU; ++u) {
-          const int32_t q = q0 + 32 * u + lane;
-          rv[u] = q < hi ? __ldcg(rs + q) : 0.0;
-          sv[u] = q < hi ? __ldcg(is + q) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < kPU; ++u) {
-          const int32_t q = q0 + 32 * u + lane;
-          const bool valid = q < hi;
-          const bool right = rv[u] >= T;
-          const unsigned ml = __ballot_sync(0xffffffffu, valid && !right);
-          const unsigned mr = __ballot_sync(0xffffffffu, valid && right);
-          if (valid) {
-            const int32_t o =
-                right ? hi - 1 - (nr + __popc(mr & below)) : lo + nl + __popc(ml & below);
-            rd[o] = rescale(rv[u], T, right);
-            id[o] = sv[u];
+      // blocks of kLeafChunk samples: lanes pick rows, then (optionally) the warp writes the
+      // folded Hadamard rows from the staged leaf rows z = u (.) h
+      const bool zrows = nrow <= 8;   // zb holds every row of this leaf
+      for (int32_t b0 = lo; b0 < hi; b0 += kLeafChunk) {
+        const int32_t b1 = min(hi, b0 + kLeafChunk);
+        for (int32_t s = b0 + lane; s < b1; s += 32) {
+          const double target = rs[s] * total_m;
+          double cdf = 0.0;
+          int cnt = 0;
+          for (int q = 0; q < nrow; ++q) {
+            cdf += mass[q];
+            if (cdf <= target) ++cnt;
           }
-          nl += __popc(ml);
-          nr += __popc(mr);
-        }
-      }
-      // children, cut into pieces (leaf level: kLeafChunk samples, else kMaxRun); the
-      // warp continues with the first piece and publishes the others
-      const int32_t chunk = (level + 1 == depth) ? kLeafChunk : kMaxRun;
-      const int np_l = (nl + chunk - 1) / chunk, np_r = (nr + chunk - 1) / chunk;
-      const int npush = np_l + np_r - 1;
-      __threadfence();   // the children's (r, sample) entries before their publication
-      int base = 0;
-      if (lane == 0 && npush > 0) base = seeded + atomicAdd(&ctl[kCtlTail], npush);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      const double unknown = __longlong_as_double(0x7ff8000000000000LL);
-      Run next;
-      int q = 0;
-      for (int side = 0; side < 2; ++side) {
-        const int32_t c_lo = side ? lo + nl : lo, c_hi = side ? hi : lo + nl;
-        for (int32_t c0 = c_lo; c0 < c_hi; c0 += chunk) {
-          Run c;
-          c.lo = c0;
-          c.hi = min(c_hi, c0 + chunk);
-          c.level = level + 1;
-          c.node = 2 * run.node + side;
-          c.prob = run.prob * (side ? (1.0 - T) : T);
-          c.qv = side ? unknown : qL;
-          if (q == 0) {
-            next = c;
-          } else if (lane == 0) {
-            const int g = base + q - 1;
-            if (g >= cap_runs) {
-              raise_status(status, RCP_ST_CAPACITY);   // cannot happen: a level holds at
-            } else {                                   // most J disjoint runs
-              runs[g] = c;
-              __threadfence();
-              *(volatile int *)&ready[g] = 1;
+          const int choice = cnt < nrow - 1 ? cnt : nrow - 1;
+          double cdf_at = 0.0;
+          for (int q = 0; q <= choice; ++q) cdf_at += mass[q];
+          const double picked = mass[choice];
+          double ro = picked > 0.0 ? (target - (cdf_at - picked)) / picked : 0.0;
+          ro = fmin(fmax(ro, 0.0), one_below());
+          const int32_t o = is[s];
+          Xi[o] = row_lo + r0 + choice;
+          pmp[o] = rprob * (picked / total_m);
+          if (resid) resid[o] = ro;
+          if (Hout) {   // fold the chosen factor row into the sample's Hadamard row
+            double *dst = Hout + (int64_t)o * R;
+            if (zrows) {
+              const double *z = zb + choice * Zs;
+              for (int c = 0; c < R; ++c) dst[c] = z[c];
+            } else {
+              const double *u = U + (r0 + choice) * R;
+              for (int c = 0; c < R; ++c) dst[c] = u[c] * hv[c];
             }
           }
-          ++q;
-        }
-      }
-      if (q > 0) {
-        run = next;
-        have = true;
-      }
-      continue;
-    }
-    // ---- leaf block: masses z^T M' z of its rows z = u (.) h, then each sample's
-    // inverse CDF
-    const int64_t r0 = (int64_t)run.node * leaf;
-    const int nrow = (int)min((int64_t)leaf, n - r0);
-    const double rprob = run.prob;
-    bool bad = nrow <= 0;
-    double total_m = 0.0;
-    if (!bad) {
-      // 8-row tiles: Y = Z M on the fp64 tensor cores, mass_q = <Y_q, Z_q>
-      const int row = lane >> 2, quad = lane & 3;
-      for (int q0 = 0; q0 < nrow; q0 += 8) {
-        const int nb = min(8, nrow - q0);
-        for (int c = lane; c < 8 * Zs; c += 32) {
-          const int j = c / Zs, col = c - j * Zs;
-          zb[c] = (j < nb && col < R) ? U[(r0 + q0 + j) * R + col] * hv[col] : 0.0;
         }
         __syncwarp();
-        const double *zr = zb + row * Zs;
-        double msum = 0.0;
-        for (int nt = 0; nt < Rn; nt += 8) {
-          double c0 = 0.0, c1 = 0.0;
-          for (int ks = 0; ks < Rn; ks += 4)
-            dmma_8x8x4(c0, c1, zr[ks + quad], Mp[(ks + quad) * Ms + nt + row]);
-          msum = fma(c0, zr[nt + 2 * quad], msum);
-          msum = fma(c1, zr[nt + 2 * quad + 1], msum);
-        }
-        msum += __shfl_xor_sync(0xffffffffu, msum, 1);
-        msum += __shfl_xor_sync(0xffffffffu, msum, 2);
-        if (quad == 0 && row < nb) mass[q0 + row] = msum > 0.0 ? msum : 0.0;
-        __syncwarp();
       }
+#if RCP_WALK_PROF
+      if (lane == 0) atomicAdd(&ctl[2], hi - lo);
+#endif
     }
-    if (!bad) {
-      if (lane == 0)
-        for (int q = 0; q < nrow; ++q) total_m += mass[q];
-      total_m = __shfl_sync(0xffffffffu, total_m, 0);
-      bad = !(total_m > 0.0);
+    publish_children(runs, gen_cnt, end, cap_runs, status, stg);
+#if RCP_WALK_PROF
+    if (threadIdx.x == 0) {   // (publish_children synchronised the CTA)
+      atomicMax(&prof[2 * (kMaxDepth + 2) + 2 * lvl], fin_last);
+      atomicMax(&prof[2 * (kMaxDepth + 2) + 2 * lvl + 1], fin_first_inv);
+#ifdef RCP_WALK_TRACE
+      for (int q = 0; q < 4; ++q) atomicMax(&prof[4 * (kMaxDepth + 2) + 4 * lvl + q], ph_max[q]);
+#endif
     }
-    if (bad) {
-      fail_run(lo, hi, is, Xi, Hout, R, status, ctl, lane);
-      continue;
-    }
-    // lanes pick rows, then (optionally) the warp writes the folded Hadamard rows from the
-    // staged leaf rows z = u (.) h
-    const bool zrows = nrow <= 8;   // zb holds every row of this leaf
-    for (int32_t s = lo + lane; s < hi; s += 32) {
-      const double target = __ldcg(rs + s) * total_m;
-      double cdf = 0.0;
-      int cnt = 0;
-      for (int q = 0; q < nrow; ++q) {
-        cdf += mass[q];
-        if (cdf <= target) ++cnt;
-      }
-      const int choice = cnt < nrow - 1 ? cnt : nrow - 1;
-      double cdf_at = 0.0;
-      for (int q = 0; q <= choice; ++q) cdf_at += mass[q];
-      const double picked = mass[choice];
-      double ro = picked > 0.0 ? (target - (cdf_at - picked)) / picked : 0.0;
-      ro = fmin(fmax(ro, 0.0), one_below());
-      const int32_t o = __ldcg(is + s);
-      Xi[o] = row_lo + r0 + choice;
-      pmp[o] = rprob * (picked / total_m);
-      if (resid) resid[o] = ro;
-      if (Hout) {   // fold the chosen factor row into the sample's Hadamard row
-        double *dst = Hout + (int64_t)o * R;
-        if (zrows) {
-          const double *z = zb + choice * Zs;
-          for (int c = 0; c < R; ++c) dst[c] = z[c];
-        } else {
-          const double *u = U + (r0 + choice) * R;
-          for (int c = 0; c < R; ++c) dst[c] = u[c] * hv[c];
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {   // after this run's outputs: count its samples finished
-      __threadfence();
-      atomicAdd(&ctl[kCtlFinished], hi - lo);
-    }
+#endif
+    grid.sync();
+    const int64_t pushed_n = ld_volatile(gen_cnt);
+    begin = end;
+    end = min(end + pushed_n, cap_runs);
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long tnow;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+    prof[2 * (kMaxDepth + 1)] = tnow;
   }
 }
 
@@ -705,13 +772,12 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   if (per_sm < 1) return RCP_ERR_ARG;
   // persistent: every CTA resident at once (workers wait on the shared queue)
   const int grid = per_sm * sm_count();
-  // cooperative launch: every CTA co-resident (workers wait on the shared task queue)
+  // cooperative launch: every CTA co-resident, grid-wide barrier between tree levels
   const double *a_gm = gm, *a_U = d_U, *a_H = d_H_in, *a_Mf = d_M;
   const uint32_t *a_pairs = pairs;
   double *a_rA = r, *a_rB = r2;
   int32_t *a_iA = idx2, *a_iB = idx3;
-  int *a_ready = (int *)(w + L.o_ready);
-  RCP_CUDA_TRY(cudaMemsetAsync(a_ready, 0, sizeof(int) * L.nruns, st));
+  unsigned long long *a_prof = (unsigned long long *)(w + L.o_prof);
   int64_t a_n = n, a_row_lo = row_lo, a_cap = L.nruns;
   int a_R = R, a_leaf = leaf, a_depth = depth;
   void *args[] = {(void *)&a_gm, (void *)&a_U, (void *)&a_n, (void *)&a_R, (void *)&a_leaf,
@@ -720,7 +786,7 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
                   (void *)&a_H, (void *)&a_rA, (void *)&a_rB, (void *)&a_iA, (void *)&a_iB,
                   (void *)&runs, (void *)&ctl,
                   (void *)&a_cap, (void *)&d_Xi, (void *)&d_pmp_i, (void *)&d_resid, (void *)&d_H_out,
-                  (void *)&d_status, (void *)&a_ready};
+                  (void *)&d_status, (void *)&a_prof};
   RCP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)walk_runs_kernel, dim3(grid),
                                            dim3(warps * 32), args, smem, st));
   RCP_LAUNCH_CHECK("walk_runs");
