@@ -21,6 +21,8 @@
 
 #include <algorithm>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -1041,9 +1043,19 @@ __global__ void fiber_expand_kernel(const int64_t *__restrict__ lo, const int64_
 
 #include "mttkrp_tiles.cuh"
 
+// radix sort temporary storage (double-buffer mode) for up to n pairs keyed by tile
+size_t sort_tmp_bytes(int64_t n) {
+  size_t b = 0;
+  const int nn = (int)(n < (1LL << 31) - 1 ? n : (1LL << 31) - 1);
+  cub::DoubleBuffer<uint32_t> k(nullptr, nullptr);
+  cub::DoubleBuffer<uint64_t> v(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, b, k, v, nn > 0 ? nn : 1);
+  return b + 256;
+}
+
 // ------------------------------------------------------------ workspace layout
 struct Ws {
-  size_t off[32];
+  size_t off[48];
   int n = 0;
   size_t total = 0;
   size_t add(size_t bytes) {
@@ -1059,7 +1071,8 @@ struct MttkrpLayout {
   size_t o_tkey, o_tcnt, o_trep, o_twmin, o_twmax, o_twsum, o_dsc, o_bcnt, o_dkey, o_dcnt,
       o_drep, o_dlo, o_dlen, o_doff, o_ioff, o_ifib, o_Hs, o_scan, o_rcnt, o_rptr, o_cmat,
       o_ent, o_tmp, o_bofs, o_S,
-      o_nnz, o_flag, o_fpos, o_sslot, o_uoff, o_sbase, o_tdone, o_tmask;
+      o_nnz, o_flag, o_fpos, o_sslot, o_uoff, o_sbase, o_tdone, o_tmask, o_icnt, o_ipos,
+      o_t64, o_t32, o_sort, o_np;
   size_t total;
   MttkrpLayout(int64_t J, int64_t cap, int64_t n_rows, int R) {
     T = 1024;
@@ -1083,6 +1096,7 @@ struct MttkrpLayout {
     o_ifib = w.add(sizeof(int32_t) * (J + cap / kItemE + 2));     // items <= S + nnz / kItemE
     o_Hs = w.add(sizeof(double) * (size_t)(J + 1) * hs_stride(R));
     int64_t sc = J + 1 > n_rows + 1 ? J + 1 : n_rows + 1;
+    if (J + cap / kItemE + 2 > sc) sc = J + cap / kItemE + 2;   // per-item pair offsets
     o_scan = w.add(scan_ws_bytes(sc));
     o_rcnt = w.add(sizeof(int64_t) * (n_rows + 1));
     o_rptr = w.add(sizeof(int64_t) * (n_rows + 2));
@@ -1100,6 +1114,17 @@ struct MttkrpLayout {
     o_sbase = w.add(sizeof(int32_t) * (kTileMaxTiles + 1));
     o_tdone = w.add(sizeof(int32_t) * kTileMaxTiles);
     o_tmask = w.add(sizeof(uint32_t) * kTileMaxTiles);
+    // deterministic mode with many row tiles: per-item pair counts and offsets, per-tile
+    // arrays (parts, scans as int64; unit offsets, scratch bases, counters as int32), the
+    // radix sort's temporary storage and the pair count
+    const int64_t nitems = J + cap / kItemE + 2;
+    o_icnt = w.add(sizeof(int64_t) * nitems);
+    o_ipos = w.add(sizeof(int64_t) * (nitems + 1));
+    const int64_t nt = n_rows / 8 + 2;
+    o_t64 = w.add(sizeof(int64_t) * 4 * nt);
+    o_t32 = w.add(sizeof(int32_t) * 4 * nt);
+    o_sort = w.add(sort_tmp_bytes(cap));
+    o_np = w.add(sizeof(int64_t) * 2);
     total = w.total + 256;
   }
 };
@@ -1189,13 +1214,21 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   const int tile_np = R <= 64 ? 1 : 2;
   const int tile_ts = tile_np == 1 ? 4 : 3;
   const int64_t n_tiles = ceil_div(n_rows, (int64_t)1 << tile_ts);
-  const bool tiles = !force_rows && n_tiles <= kTileMaxTiles && J < (1LL << 22) &&
-                     cap < (1LL << 31) && 2 * sm_count() <= kPrefixSeg * kPrefixMaxPer;
+  bool tiles = !force_rows && n_tiles <= kTileMaxTiles && J < (1LL << 22) &&
+               cap < (1LL << 31) && 2 * sm_count() <= kPrefixSeg * kPrefixMaxPer;
+  // many row tiles: sorted pairs (reads the pair count on the host, so not inside a graph)
+  bool tiles_big = false;
+  if (!force_rows && !tiles && J < (1LL << 22) && cap < (1LL << 31)) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    RCP_CUDA_TRY(cudaStreamIsCapturing(st, &cs));
+    tiles_big = cs == cudaStreamCaptureStatusNone;
+  }
+  if (tiles_big) tiles = false;
 
   unsigned long long *twmin = (unsigned long long *)P(L.o_twmin);
   unsigned long long *twmax = (unsigned long long *)P(L.o_twmax);
   double *twsum = (double *)P(L.o_twsum), *dsc = (double *)P(L.o_dsc);
-  mttkrp_init_kernel<<<4 * sm_count(), 256, 0, st>>>(d_out, tiles ? 0 : n_rows * (int64_t)R, L.T, tkey,
+  mttkrp_init_kernel<<<4 * sm_count(), 256, 0, st>>>(d_out, (tiles || tiles_big) ? 0 : n_rows * (int64_t)R, L.T, tkey,
                                                       tcnt, trep, twmin, twmax, twsum);
   RCP_LAUNCH_CHECK("mttkrp_init");
   hash_insert_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(
@@ -1276,6 +1309,77 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     else
       tile_spmm_kernel<3, 2><<<sg, kTileWarps * 32, tile_spmm_smem<3, 2>(), st>>>(
           tptr, nt, n_rows, uoff, sbase, pairs, d_rows, d_vals, Hs, R, d_out, scratch, tdone, tmask, d_stats);
+    RCP_LAUNCH_CHECK("tile_spmm");
+    return RCP_OK;
+  }
+  if (tiles_big) {
+    const int64_t nt = n_tiles;
+    uint32_t *kA = (uint32_t *)((char *)P(L.o_ent) + sizeof(uint64_t) * (size_t)cap);
+    uint64_t *vA = (uint64_t *)P(L.o_ent);
+    uint32_t *kB = (uint32_t *)((char *)P(L.o_tmp) + sizeof(uint64_t) * (size_t)cap);
+    uint64_t *vB = (uint64_t *)P(L.o_tmp);
+    int64_t *icnt2 = (int64_t *)P(L.o_icnt), *ipos = (int64_t *)P(L.o_ipos);
+    int64_t *np = (int64_t *)P(L.o_np);
+    int64_t *t64 = (int64_t *)P(L.o_t64);
+    int64_t *up = t64, *spp = t64 + (nt + 2), *uo = t64 + 2 * (nt + 2), *so = t64 + 3 * (nt + 2);
+    int32_t *t32 = (int32_t *)P(L.o_t32);
+    int32_t *uoff = t32, *sbase = t32 + (nt + 2), *tdone = t32 + 2 * (nt + 2);
+    uint32_t *tmask = (uint32_t *)(t32 + 3 * (nt + 2));
+    int64_t *tptr = rptr;   // n_rows + 2 >= n_tiles + 1
+    const int ts = tile_ts;
+    const unsigned gw = (unsigned)(8 * sm_count());
+    if (ts == 4) pair_count_kernel<4><<<gw, 256, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, icnt2, np + 1);
+    else pair_count_kernel<3><<<gw, 256, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, icnt2, np + 1);
+    RCP_LAUNCH_CHECK("pair_count");
+    rc = scan_i64_exclusive(icnt2, ipos, J + cap / kItemE + 1, np + 1, scan_ws, st);
+    if (rc) return rc;
+    if (ts == 4) pair_emit_kernel<4><<<gw, 256, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, ipos, kA, vA);
+    else pair_emit_kernel<3><<<gw, 256, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, ipos, kA, vA);
+    RCP_LAUNCH_CHECK("pair_emit");
+    // the pair count: ipos[n_items]
+    int64_t h_nit = 0, h_np = 0;
+    RCP_CUDA_TRY(cudaMemcpyAsync(&h_nit, np + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    RCP_CUDA_TRY(cudaStreamSynchronize(st));
+    RCP_CUDA_TRY(cudaMemcpyAsync(&h_np, ipos + h_nit, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    RCP_CUDA_TRY(cudaStreamSynchronize(st));
+    RCP_CUDA_TRY(cudaMemcpyAsync(np, &h_np, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    cub::DoubleBuffer<uint32_t> kb(kA, kB);
+    cub::DoubleBuffer<uint64_t> vb(vA, vB);
+    int bits = 1;
+    while (bits < 32 && ((int64_t)1 << bits) < nt) ++bits;
+    size_t tb = sort_tmp_bytes(cap);
+    if (h_np > 0)
+      RCP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(P(L.o_sort), tb, kb, vb, (int)h_np, 0, bits, st));
+    const uint32_t *tk = kb.Current();
+    const uint64_t *pairs = vb.Current();
+    double2 *scratch = (double2 *)(vb.Current() == vA ? (void *)vB : (void *)vA);
+    tile_bounds_kernel<<<(unsigned)ceil_div(nt + 1, 256), 256, 0, st>>>(tk, np, nt, tptr);
+    RCP_LAUNCH_CHECK("tile_bounds");
+    tile_parts_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, st>>>(tptr, nt, up, spp);
+    RCP_LAUNCH_CHECK("tile_parts");
+    rc = scan_i64_exclusive(up, uo, nt, nullptr, scan_ws, st);
+    if (rc) return rc;
+    rc = scan_i64_exclusive(spp, so, nt, nullptr, scan_ws, st);
+    if (rc) return rc;
+    tile_parts_i32_kernel<<<(unsigned)ceil_div(nt + 1, 256), 256, 0, st>>>(uo, so, nt, uoff, sbase);
+    RCP_LAUNCH_CHECK("tile_parts_i32");
+    RCP_CUDA_TRY(cudaMemsetAsync(tdone, 0, sizeof(int32_t) * nt, st));
+    RCP_CUDA_TRY(cudaMemsetAsync(tmask, 0, sizeof(uint32_t) * nt, st));
+    static bool battr = false;
+    if (!battr) {
+      RCP_CUDA_TRY(cudaFuncSetAttribute(tile_spmm_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)tile_spmm_smem<4, 1>()));
+      RCP_CUDA_TRY(cudaFuncSetAttribute(tile_spmm_kernel<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)tile_spmm_smem<3, 2>()));
+      battr = true;
+    }
+    const unsigned sg = (unsigned)(4 * sm_count());
+    if (tile_np == 1)
+      tile_spmm_kernel<4, 1><<<sg, kTileWarps * 32, tile_spmm_smem<4, 1>(), st>>>(
+          tptr, (int)nt, n_rows, uoff, sbase, pairs, d_rows, d_vals, Hs, R, d_out, scratch, tdone, tmask, d_stats);
+    else
+      tile_spmm_kernel<3, 2><<<sg, kTileWarps * 32, tile_spmm_smem<3, 2>(), st>>>(
+          tptr, (int)nt, n_rows, uoff, sbase, pairs, d_rows, d_vals, Hs, R, d_out, scratch, tdone, tmask, d_stats);
     RCP_LAUNCH_CHECK("tile_spmm");
     return RCP_OK;
   }

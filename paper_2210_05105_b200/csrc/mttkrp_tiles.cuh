@@ -596,3 +596,107 @@ tile_spmm_kernel(const int64_t *__restrict__ tptr, int n_tiles, int64_t n_rows,
   }
   if (threadIdx.x == 0 && hit_total) atomicAdd((unsigned long long *)&stats[4], hit_total);
 }
+
+// ---------------------------------------------------------------- many row tiles
+// Modes with more than kTileMaxTiles row tiles (C4/C5 factor modes: 10^5..10^6 tiles): the
+// pairs are emitted per item in item order (count, scan, emit: fiber order, ascending tile
+// inside a fiber), then stably radix-sorted by tile -- inside a tile they stay in fiber
+// order, the same canonical order as the CTA-histogram passes produce -- and the tile
+// pointers are found by binary search in the sorted tiles.
+template <int TS>
+__global__ void pair_count_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                                  const int32_t *__restrict__ ifib, const int64_t *__restrict__ dlo,
+                                  const int64_t *__restrict__ dlen, const int32_t *__restrict__ rows,
+                                  int64_t *__restrict__ icnt, int64_t *__restrict__ nit) {
+  const int64_t n_items = ioff[Sp[0]];
+  if (blockIdx.x == 0 && threadIdx.x == 0) nit[0] = n_items;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; it < n_items; it += nw) {
+    const ItemSpan sp = item_span(it, ioff, ifib, dlo, dlen);
+    const int64_t fs = dlo[sp.d];
+    int64_t c = 0;
+    for (int64_t base = sp.a; base < sp.b; base += 32) {
+      const int64_t pos = base + lane;
+      const int32_t t = pos < sp.b ? (rows[pos] >> TS) : -1;
+      int32_t pt = __shfl_up_sync(0xffffffffu, t, 1);
+      if (lane == 0) pt = pos > fs ? (rows[pos - 1] >> TS) : -1;
+      c += __popc(__ballot_sync(0xffffffffu, pos < sp.b && (pos == fs || t != pt)));
+    }
+    if (lane == 0) icnt[it] = c;
+  }
+}
+
+template <int TS>
+__global__ void pair_emit_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp,
+                                 const int32_t *__restrict__ ifib, const int64_t *__restrict__ dlo,
+                                 const int64_t *__restrict__ dlen, const int32_t *__restrict__ rows,
+                                 const int64_t *__restrict__ ipos, uint32_t *__restrict__ tkeys,
+                                 uint64_t *__restrict__ pairs) {
+  const int64_t n_items = ioff[Sp[0]];
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned below = (1u << lane) - 1u;
+  for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; it < n_items; it += nw) {
+    const ItemSpan sp = item_span(it, ioff, ifib, dlo, dlen);
+    const int64_t fs = dlo[sp.d], fe = fs + dlen[sp.d];
+    int64_t o = ipos[it];
+    for (int64_t base = sp.a; base < sp.b; base += 32) {
+      const int64_t pos = base + lane;
+      // this window and the next (a run ends at most TR <= 32 entries later), to the fiber end
+      const int32_t t1 = pos < fe ? (rows[pos] >> TS) : INT_MAX;
+      const int32_t t2 = pos + 32 < fe ? (rows[pos + 32] >> TS) : INT_MAX;
+      int32_t p1 = __shfl_up_sync(0xffffffffu, t1, 1);
+      if (lane == 0) p1 = pos > fs ? (rows[pos - 1] >> TS) : -1;
+      int32_t p2 = __shfl_up_sync(0xffffffffu, t2, 1);
+      const int32_t last1 = __shfl_sync(0xffffffffu, t1, 31);
+      if (lane == 0) p2 = last1;
+      const bool s1 = pos < fe && t1 != p1;
+      const bool s2 = pos + 32 < fe && t2 != p2;
+      const unsigned b1 = __ballot_sync(0xffffffffu, s1 || pos >= fe);
+      const unsigned b2 = __ballot_sync(0xffffffffu, s2 || pos + 32 >= fe);
+      const bool own = s1 && pos < sp.b;
+      const unsigned m = __ballot_sync(0xffffffffu, own);
+      if (own) {
+        const unsigned above = b1 & ~((2u << lane) - 1u);
+        const int64_t end = above ? base + (__ffs(above) - 1) : base + 32 + (__ffs(b2) - 1);
+        const int64_t q = o + __popc(m & below);
+        tkeys[q] = (uint32_t)t1;
+        pairs[q] = pack_pair(pos, (int)(end - pos), sp.d);
+      }
+      o += __popc(m);
+    }
+  }
+}
+
+// tptr[t] = first pair of tile t in the tile-sorted pairs (t = 0..n_tiles)
+__global__ void tile_bounds_kernel(const uint32_t *__restrict__ tkeys, const int64_t *__restrict__ np,
+                                   int64_t n_tiles, int64_t *__restrict__ tptr) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > n_tiles) return;
+  int64_t lo = 0, hi = np[0];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)tkeys[mid] < t) lo = mid + 1; else hi = mid;
+  }
+  tptr[t] = lo;
+}
+
+// Per tile: parts (>= 1) and multi-part parts, as int64 counts for the scans.
+__global__ void tile_parts_kernel(const int64_t *__restrict__ tptr, int64_t n_tiles,
+                                  int64_t *__restrict__ up, int64_t *__restrict__ sp) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_tiles) return;
+  const int64_t np = max((int64_t)1, ceil_div(tptr[t + 1] - tptr[t], (int64_t)kTilePart));
+  up[t] = np;
+  sp[t] = np > 1 ? np : 0;
+}
+
+__global__ void tile_parts_i32_kernel(const int64_t *__restrict__ uo, const int64_t *__restrict__ so,
+                                      int64_t n_tiles, int32_t *__restrict__ uoff,
+                                      int32_t *__restrict__ sbase) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > n_tiles) return;
+  uoff[t] = (int32_t)uo[t];
+  if (t < n_tiles) sbase[t] = (int32_t)so[t];
+}

@@ -103,13 +103,15 @@ def test_c3_batch_mttkrp_matches_oracle(c3_round, samples):
     assert rel_err(outs[0][0].cpu().numpy(), ref) < 1e-9
 
 
-def test_deterministic_mode_bit_identical_runs_over_49152_rows():
+@pytest.mark.parametrize("rows", [60000, 100000])
+def test_deterministic_mode_bit_identical_runs_over_49152_rows(rows):
     """Deterministic MTTKRP mode: two full ALS runs on a tensor whose first mode has more
     than 49,152 rows give bit-identical samples, factors, sigma and fits, and stay within
-    the parity bars of the oracle."""
+    the parity bars of the oracle.  60,000 rows: 3,750 row tiles (CTA-histogram pair
+    passes); 100,000 rows: 6,250 tiles (pairs radix-sorted by tile)."""
     import paper_2210_05105_b200 as P
     from paper_2210_05105_b200 import synth
-    dims = (60000, 300, 200)
+    dims = (rows, 300, 200)
     idx, vals = synth.small_random(dims, 400000, seed=21)
     t = P.SparseTensorCOO(dims, idx, vals)
     cfg = P.AlsConfig(rank=16, rounds=2, sampler="sts", samples=8192,

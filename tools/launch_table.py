@@ -7,11 +7,12 @@ import collections
 import csv
 import sys
 
-MTTKRP = ("hash_insert", "compact_count", "compact_write", "lookup_kernel", "finalize_counts",
+MTTKRP = ("hash_insert", "rep_flag", "rep_compact", "lookup_kernel", "finalize_counts",
           "item_count", "item_fill", "cta_hist", "cta_prefix", "rows_hit", "cta_scatter",
           "bucket_offsets", "bucket_scatter", "bucket_rows", "spmm_packed", "row_count",
           "scatter_kernel", "big_hist", "big_colprefix", "big_offsets", "big_rows",
-          "mttkrp_init")
+          "mttkrp_init", "tile_hist", "pair_scatter", "tile_units", "tile_spmm", "pair_count",
+          "pair_emit", "tile_bounds", "tile_parts")
 
 
 def short(name):
@@ -44,7 +45,7 @@ def main(path):
     mt_t = sum(a[1] for _, a in mt)
     mt_b = sum(a[2] for _, a in mt)
     walks = agg.get("walk_runs_kernel", [0])[0]
-    solves = max(agg.get("cta_hist_kernel", [0])[0], agg.get("spmm_packed_kernel<1>", [0])[0], 1)
+    solves = max(agg.get("lookup_kernel", [0])[0], 1)
     print("\nSampled-MTTKRP pipeline kernels (%s): %.1f µs, %.1f MB DRAM over %d solves -> "
           "%.1f MB DRAM traffic per rcp_sampled_mttkrp call." %
           (", ".join(sorted(set(n.split("<")[0] for n, _ in mt))), mt_t, mt_b / 1e6, solves,
