@@ -452,7 +452,7 @@ def cpu_baseline(args, cl, c, samples=None):
                         parity["gathered_nnz_gpu"] == parity["gathered_nnz_oracle"])
     del out, gout
     return {"value": csr.nnz / dt, "unit": UNIT, "cores": workers, "kind": "port",
-            "parity": parity,
+            "parity": parity, "host": host_info(),
             "sample": "oracle gather_sampled_nonzeros_to_csr + downsampled_mttkrp, mode %d of %s, "
                       "first %d of J=%d samples of a device STS/ARLS batch; %d nnz iterated in %.2f s "
                       "(store conversion %.1f s untimed)" % (k, args.config, samples, cl.J, csr.nnz,

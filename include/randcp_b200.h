@@ -252,9 +252,10 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
  *      across warps; the order of a row's terms varies run to run);
  *   1  deterministic: row-tile x fiber pairs in a canonical order, every output row summed
  *      in a fixed order -- bit-identical results on every run (ref tests/test_mttkrp.py:
- *      60-67,163-172 require bit-identity across worker counts).  Available when the mode's
- *      rows fit 4096 row tiles (16 rows each for R <= 64, 8 for R <= 128) and J < 2^22;
- *      other calls run mode 0.
+ *      60-67,163-172 require bit-identity across worker counts).  Row tiles of 16 rows
+ *      (R <= 64) or 8 (R <= 128); above 4096 tiles the pairs are radix-sorted by tile,
+ *      which reads their count on the host: such calls inside a CUDA-graph capture run
+ *      mode 0.  Requires J < 2^22.
  * Returns the previous mode; a negative argument only queries. */
 int rcp_set_mttkrp_mode(int mode);
 /* Reference-shaped CSR gather with multiplicity (drop-in for

@@ -1053,9 +1053,16 @@ size_t sort_tmp_bytes(int64_t n) {
   return b + 256;
 }
 
+size_t wsort_tmp_bytes(int64_t J) {
+  size_t b = 0;
+  cub::DoubleBuffer<uint32_t> k(nullptr, nullptr), v(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, b, k, v, (int)(J > 0 ? J : 1));
+  return b + 256;
+}
+
 // ------------------------------------------------------------ workspace layout
 struct Ws {
-  size_t off[48];
+  size_t off[64];
   int n = 0;
   size_t total = 0;
   size_t add(size_t bytes) {
@@ -1072,7 +1079,7 @@ struct MttkrpLayout {
       o_drep, o_dlo, o_dlen, o_doff, o_ioff, o_ifib, o_Hs, o_scan, o_rcnt, o_rptr, o_cmat,
       o_ent, o_tmp, o_bofs, o_S,
       o_nnz, o_flag, o_fpos, o_sslot, o_uoff, o_sbase, o_tdone, o_tmask, o_icnt, o_ipos,
-      o_t64, o_t32, o_sort, o_np;
+      o_t64, o_t32, o_sort, o_np, o_wk, o_wv, o_wk2, o_wv2, o_wst, o_wsort;
   size_t total;
   MttkrpLayout(int64_t J, int64_t cap, int64_t n_rows, int R) {
     T = 1024;
@@ -1125,6 +1132,13 @@ struct MttkrpLayout {
     o_t32 = w.add(sizeof(int32_t) * 4 * nt);
     o_sort = w.add(sort_tmp_bytes(cap));
     o_np = w.add(sizeof(int64_t) * 2);
+    // deterministic mode: samples sorted by distinct fiber for ordered weight sums
+    o_wk = w.add(sizeof(uint32_t) * (J + 1));
+    o_wv = w.add(sizeof(uint32_t) * (J + 1));
+    o_wk2 = w.add(sizeof(uint32_t) * (J + 1));
+    o_wv2 = w.add(sizeof(uint32_t) * (J + 1));
+    o_wst = w.add(sizeof(int32_t) * (J + 1));
+    o_wsort = w.add(wsort_tmp_bytes(J));
     total = w.total + 256;
   }
 };
@@ -1245,6 +1259,23 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     rep_compact_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(flag, fpos, J, sslot, tkey, tcnt, twmin,
                                                                    twmax, twsum, dkey, dcnt, drep, dsc, S);
     RCP_LAUNCH_CHECK("rep_compact");
+    if (tiles || tiles_big) {   // unequal weights of one fiber: their w^2 summed in sample order
+      uint32_t *wk = (uint32_t *)P(L.o_wk), *wv = (uint32_t *)P(L.o_wv);
+      uint32_t *wk2 = (uint32_t *)P(L.o_wk2), *wv2 = (uint32_t *)P(L.o_wv2);
+      int32_t *wst = (int32_t *)P(L.o_wst);
+      sample_fiber_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(sslot, trep, fpos, J, wk, wv);
+      RCP_LAUNCH_CHECK("sample_fiber");
+      cub::DoubleBuffer<uint32_t> kb(wk, wk2), vb(wv, wv2);
+      int bits = 1;
+      while (bits < 31 && ((int64_t)1 << bits) < J) ++bits;
+      size_t tb = wsort_tmp_bytes(J);
+      RCP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(P(L.o_wsort), tb, kb, vb, (int)J, 0, bits, st));
+      fiber_start_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(kb.Current(), J, wst);
+      RCP_LAUNCH_CHECK("fiber_start");
+      ordered_w2_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(S, wst, dcnt, vb.Current(), d_w, drep,
+                                                                    sslot, twmin, twmax, dsc);
+      RCP_LAUNCH_CHECK("ordered_w2");
+    }
   }
   // 2. lookup + scaled KRP rows
   lookup_kernel<<<(unsigned)std::min<int64_t>(ceil_div(J * 32, 256), 8LL * sm_count()), 256, 0, st>>>(

@@ -700,3 +700,43 @@ __global__ void tile_parts_i32_kernel(const int64_t *__restrict__ uo, const int6
   uoff[t] = (int32_t)uo[t];
   if (t < n_tiles) sbase[t] = (int32_t)so[t];
 }
+
+// ---------------------------------------------------------------- ordered sample weights
+// Deterministic mode: a distinct fiber whose samples carry unequal weights (an injected batch;
+// sampler output has equal weights, whose merged weight count * w^2 is exact) gets its sum
+// of w^2 in sample order instead of the hash table's atomic sum.
+__global__ void sample_fiber_kernel(const int32_t *__restrict__ sslot, const int32_t *__restrict__ trep,
+                                    const int64_t *__restrict__ fpos, int64_t J,
+                                    uint32_t *__restrict__ key, uint32_t *__restrict__ val) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= J) return;
+  key[s] = (uint32_t)fpos[trep[sslot[s]]];
+  val[s] = (uint32_t)s;
+}
+
+__global__ void fiber_start_kernel(const uint32_t *__restrict__ key, int64_t J,
+                                   int32_t *__restrict__ start) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= J) return;
+  if (i == 0 || key[i] != key[i - 1]) start[key[i]] = (int32_t)i;
+}
+
+__global__ void ordered_w2_kernel(const int64_t *__restrict__ Sp, const int32_t *__restrict__ start,
+                                  const int32_t *__restrict__ dcnt, const uint32_t *__restrict__ val,
+                                  const double *__restrict__ w, const int32_t *__restrict__ drep,
+                                  const int32_t *__restrict__ sslot,
+                                  const unsigned long long *__restrict__ twmin,
+                                  const unsigned long long *__restrict__ twmax,
+                                  double *__restrict__ dsc) {
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= Sp[0]) return;
+  const int32_t h = sslot[drep[d]];
+  if (twmin[h] == twmax[h]) return;   // equal weights: count * w^2 already exact
+  double s = 0.0;
+  const int32_t b = start[d], e = b + dcnt[d];
+  for (int32_t i = b; i < e; ++i) {
+    const double x = w[val[i]];
+    s = fma(x, x, s);
+  }
+  dsc[d] = s;
+}

@@ -191,19 +191,31 @@ def test_gather_csr_and_downsampled_match_reference(pkg):
         assert rel_err(out, g0["out%d" % k]) < 1e-13
 
 
-@pytest.mark.parametrize("dims,nnz", [
-    ((40, 35, 30), 6000),        # CTA-private histograms, single-pass scatter
-    ((6000, 35, 30), 60000),     # >= 4096 rows in mode 0: bucketed two-pass transpose
-    ((60000, 12, 10), 50000),    # > 49152 rows in mode 0: large-row bucketed transpose
-    ((300000, 6, 5), 40000),     # 2^8-row buckets
+@pytest.mark.parametrize("deterministic", [False, True])
+@pytest.mark.parametrize("dims,nnz,R", [
+    ((40, 35, 30), 6000, 37),        # CTA-private histograms, single-pass scatter
+    ((6000, 35, 30), 60000, 37),     # >= 4096 rows in mode 0: bucketed two-pass transpose
+    ((60000, 12, 10), 50000, 37),    # > 49152 rows in mode 0: large-row bucketed transpose
+    ((300000, 6, 5), 40000, 37),     # 2^8-row buckets (deterministic: sorted pairs)
+    ((6000, 35, 30), 60000, 90),     # R > 64: two column pairs per lane, 8-row tiles
 ])
-def test_fused_sampled_mttkrp_matches_oracle(pkg, dims, nnz):
+def test_fused_sampled_mttkrp_matches_oracle(pkg, dims, nnz, R, deterministic):
+    """Both MTTKRP modes against the oracle (ref mttkrp.py:131-189), every row-count
+    regime of each; the deterministic mode is also bit-identical on a repeated call."""
+    from paper_2210_05105_b200 import set_mttkrp_mode
+    prev = set_mttkrp_mode(deterministic)
+    try:
+        _fused_case(dims, nnz, R, deterministic)
+    finally:
+        set_mttkrp_mode(prev)
+
+
+def _fused_case(dims, nnz, R, deterministic):
     import torch
     from paper_2210_05105_b200.ops import ops_for
     from paper_2210_05105_b200.store import build_store
     idx, vals = synth.small_random(dims, nnz, seed=2)
     gen = np.random.default_rng(4)
-    R = 37
     factors = [gen.standard_normal((d, R)) for d in dims]
     dev = torch.device("cuda")
     ops = ops_for(dev)
@@ -228,6 +240,13 @@ def test_fused_sampled_mttkrp_matches_oracle(pkg, dims, nnz):
         ops.status.check()
         got = out.cpu().numpy()
         assert rel_err(got, ref) < 1e-12, k
+        if deterministic:
+            out2 = torch.empty_like(out)
+            stats2 = torch.zeros_like(stats)
+            ops.sampled_mttkrp(st, torch.as_tensor(np.ascontiguousarray(X.T), device=dev), k,
+                               torch.as_tensor(H, device=dev), torch.as_tensor(w, device=dev),
+                               out2, stats2, cap=st.capacity(J))
+            assert torch.equal(out, out2) and torch.equal(stats, stats2), k
         csr = O.sampled_csr(O.Store(dims, idx, vals, k), X, k)
         s = stats.cpu().numpy()
         assert s[3] == csr.nnz                       # gathered nnz with multiplicity
