@@ -97,11 +97,13 @@ class LibraryMissing(RuntimeError):
     pass
 
 
-def load(path=LIB_PATH):
-    """Load and bind the library (no GPU needed to load)."""
+def load(path=None):
+    """Load and bind the library (no GPU needed to load).  RCP_LIB overrides the in-tree
+    path (A/B runs of library variants, tools/lab/ab_bench.py)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("RCP_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise LibraryMissing("librandcp_b200.so not built (run __graft_entry__.build() or "
                              "python paper_2210_05105_b200/build.py): %s" % path)

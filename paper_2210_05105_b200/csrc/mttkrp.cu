@@ -423,7 +423,9 @@ cta_hist_kernel(const int64_t *__restrict__ ioff, const int64_t *__restrict__ Sp
 constexpr int kPrefixSeg = 4;
 constexpr int kPrefixRows = 64;    // rows per 256-thread block
 constexpr int kPrefixMaxPer = 80;  // CTA counts one thread keeps in registers (G <= 320)
+constexpr int kPrefixMaxPerFast = 48;   // the row-transpose path's grid (one CTA per SM)
 
+template <int MP>
 __global__ void __launch_bounds__(kPrefixRows * kPrefixSeg)
 cta_prefix_kernel(int32_t *__restrict__ cmat, int G, int64_t n_rows, int64_t *__restrict__ rcnt) {
   __shared__ int32_t seg_sum[kPrefixSeg][kPrefixRows];
@@ -431,10 +433,10 @@ cta_prefix_kernel(int32_t *__restrict__ cmat, int G, int64_t n_rows, int64_t *__
   const int64_t r = blockIdx.x * (int64_t)kPrefixRows + rl;
   const int per = (G + kPrefixSeg - 1) / kPrefixSeg;
   const int c0 = sg * per, c1 = min(G, c0 + per);
-  int32_t v[kPrefixMaxPer];
+  int32_t v[MP];
   int32_t sum = 0;
 #pragma unroll
-  for (int q = 0; q < kPrefixMaxPer; ++q) {
+  for (int q = 0; q < MP; ++q) {
     const int c = c0 + q;
     v[q] = (r < n_rows && c < c1) ? cmat[(int64_t)c * n_rows + r] : 0;
     sum += v[q];
@@ -445,7 +447,7 @@ cta_prefix_kernel(int32_t *__restrict__ cmat, int G, int64_t n_rows, int64_t *__
   for (int q = 0; q < sg; ++q) run += seg_sum[q][rl];
   if (r < n_rows) {
 #pragma unroll
-    for (int q = 0; q < kPrefixMaxPer; ++q) {
+    for (int q = 0; q < MP; ++q) {
       const int c = c0 + q;
       if (c < c1) {
         cmat[(int64_t)c * n_rows + r] = run;
@@ -1322,7 +1324,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     if (tile_ts == 4) tile_hist_kernel<4><<<grid, kPairThreads, hsm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, cmat);
     else tile_hist_kernel<3><<<grid, kPairThreads, hsm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, cmat);
     RCP_LAUNCH_CHECK("tile_hist");
-    cta_prefix_kernel<<<(unsigned)ceil_div(nt, kPrefixRows), kPrefixRows * kPrefixSeg, 0, st>>>(
+    cta_prefix_kernel<kPrefixMaxPer><<<(unsigned)ceil_div(nt, kPrefixRows), kPrefixRows * kPrefixSeg, 0, st>>>(
         cmat, grid, nt, tcntp);
     RCP_LAUNCH_CHECK("cta_prefix");
     rc = scan_i64_exclusive(tcntp, tptr, nt, nullptr, scan_ws, st);
@@ -1416,7 +1418,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   }
   // 4. row histogram -> row pointers; 5. scatter into row order (packed entries)
   const int priv =
-      (n_rows <= kPrivRows && cap < (1LL << 31) && sm_count() <= kPrefixSeg * kPrefixMaxPer) ? 1 : 0;
+      (n_rows <= kPrivRows && cap < (1LL << 31) && sm_count() <= kPrefixSeg * kPrefixMaxPerFast) ? 1 : 0;
   static bool attr = false;
   if (!attr) {
     RCP_CUDA_TRY(cudaFuncSetAttribute(cta_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1429,7 +1431,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     const size_t smem = sizeof(int32_t) * n_rows;
     cta_hist_kernel<<<grid, kTraverseThreads, smem, st>>>(ioff, S, ifib, dlo, dlen, d_rows, n_rows, cmat);
     RCP_LAUNCH_CHECK("cta_hist");
-    cta_prefix_kernel<<<(unsigned)ceil_div(n_rows, kPrefixRows), kPrefixRows * kPrefixSeg, 0, st>>>(
+    cta_prefix_kernel<kPrefixMaxPerFast><<<(unsigned)ceil_div(n_rows, kPrefixRows), kPrefixRows * kPrefixSeg, 0, st>>>(
         cmat, grid, n_rows, rcnt);
     RCP_LAUNCH_CHECK("cta_prefix");
     rc = scan_i64_exclusive(rcnt, rptr, n_rows, nullptr, scan_ws, st);
