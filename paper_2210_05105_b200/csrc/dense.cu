@@ -773,20 +773,6 @@ gram_mma_kernel(const double *__restrict__ U, const double *__restrict__ scale, 
 // a CTA read the same rows at nearly the same time: L1 hits).  Steps go to (CTA, warp of
 // the group) in a fixed order; warps and CTAs are combined in fixed orders: deterministic.
 template <int T, int G, int g>
-__device__ __forceinline__ void gram_accum_group(const double (&f)[T],
-                                                 double (&acc)[(T * (T + 1) / 2 + G - 1) / G][2]) {
-  constexpr int PPG = (T * (T + 1) / 2 + G - 1) / G;
-  int p = 0;
-#pragma unroll
-  for (int a = 0; a < T; ++a)
-#pragma unroll
-    for (int b = a; b < T; ++b) {
-      if (p >= g * PPG && p < (g + 1) * PPG) gram_dmma(acc[p - g * PPG][0], acc[p - g * PPG][1], f[a], f[b]);
-      ++p;
-    }
-}
-
-template <int T, int G, int g>
 __device__ __forceinline__ void gram_split_body(const double *__restrict__ U,
                                                 const double *__restrict__ scale, int64_t n, int R,
                                                 int sub, double *red) {

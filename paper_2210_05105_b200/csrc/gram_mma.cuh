@@ -41,4 +41,20 @@ __device__ __forceinline__ void gram_accum(const double (&f)[T], double (&acc)[T
 }
 
 
+// The pairs of group g of G (a compile-time range of the T(T+1)/2 upper tile pairs): R > 64,
+// where one warp cannot hold every pair's accumulators.
+template <int T, int G, int g>
+__device__ __forceinline__ void gram_accum_group(const double (&f)[T],
+                                                 double (&acc)[(T * (T + 1) / 2 + G - 1) / G][2]) {
+  constexpr int PPG = (T * (T + 1) / 2 + G - 1) / G;
+  int p = 0;
+#pragma unroll
+  for (int a = 0; a < T; ++a)
+#pragma unroll
+    for (int b = a; b < T; ++b) {
+      if (p >= g * PPG && p < (g + 1) * PPG) gram_dmma(acc[p - g * PPG][0], acc[p - g * PPG][1], f[a], f[b]);
+      ++p;
+    }
+}
+
 }  // namespace rcp

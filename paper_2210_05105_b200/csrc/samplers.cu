@@ -9,6 +9,8 @@
 //    global order (the reference itself is leaf-size and rank-count invariant).
 #include <float.h>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "gram_mma.cuh"
 #include "scan.cuh"
@@ -201,6 +203,11 @@ __global__ void batch_fold_kernel(const int64_t *__restrict__ perm, const int64_
 }
 
 // --------------------------------------------------------------------- STS build
+int getenv_leaf_ffma() {   // RCP_LEAF_FFMA=1: the FFMA leaf Grams for every R > 64 (A/B)
+  const char *e = getenv("RCP_LEAF_FFMA");
+  return e && e[0] == '1' ? 1 : 0;
+}
+
 __global__ void sts_leaf_kernel(const double *__restrict__ U, int64_t n, int R, int leaf,
                                 int64_t nleaves, double *__restrict__ level) {
   extern __shared__ double rows[];  // leaf x R, then the packed (a, b) table
@@ -274,6 +281,73 @@ sts_leaf_mma_kernel(const double *__restrict__ U, int64_t n, int R, int leaf, in
     double *out = level + v * Rs;
     for (int e = lane; e < Rs; e += 32) out[e] = stage[e];
     __syncwarp();
+  }
+}
+
+// 64 < R <= 128: leaf Grams on the fp64 tensor cores with the tile pairs split over G warps
+// per leaf (gram_accum_group); the CTA's 8 warps serve 8 / G leaves at a time, each leaf's
+// warps meeting at their own named barrier before the packed triangle is written.
+template <int T, int G, int g>
+__device__ __forceinline__ void leaf_split_body(const double *__restrict__ U, int64_t r0, int64_t rend,
+                                                int R, int leaf, double *stage) {
+  constexpr int NP = T * (T + 1) / 2;
+  constexpr int PPG = (NP + G - 1) / G;
+  const int lane = threadIdx.x & 31, kk = lane & 3, col = lane >> 2;
+  double acc[PPG][2];
+#pragma unroll
+  for (int p = 0; p < PPG; ++p) acc[p][0] = acc[p][1] = 0.0;
+  for (int k0 = 0; k0 < leaf; k0 += 8) {   // two row steps' loads in flight
+    double f0[T], f1[T];
+    gram_load<T>(U, nullptr, r0 + k0 + kk, rend, R, col, f0);
+    gram_load<T>(U, nullptr, r0 + k0 + 4 + kk, rend, R, col, f1);
+    gram_accum_group<T, G, g>(f0, acc);
+    if (k0 + 4 < leaf) gram_accum_group<T, G, g>(f1, acc);
+  }
+  int p = 0;
+#pragma unroll
+  for (int a = 0; a < T; ++a)
+#pragma unroll
+    for (int b = a; b < T; ++b) {
+      if (p >= g * PPG && p < (g + 1) * PPG) {
+        const int ga = 8 * a + col;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int gb = 8 * b + 2 * kk + u;
+          if (ga <= gb && gb < R) stage[tri_index(ga, gb, R)] = acc[p - g * PPG][u];
+        }
+      }
+      ++p;
+    }
+}
+
+template <int T, int G>
+__global__ void __launch_bounds__(256, 1)
+sts_leaf_split_kernel(const double *__restrict__ U, int64_t n, int R, int leaf, int64_t nleaves,
+                      double *__restrict__ level) {
+  extern __shared__ double sh[];   // one packed node per leaf slot
+  constexpr int SLOTS = 8 / G;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int grp = wid % G, slot = wid / G;
+  const int Rt = R * (R + 1) / 2, Rs = tri_stride(R);
+  double *stage = sh + (size_t)slot * Rs;
+  for (int64_t v = (int64_t)blockIdx.x * SLOTS + slot; v < nleaves; v += (int64_t)gridDim.x * SLOTS) {
+    const int64_t r0 = v * leaf, rend = min(r0 + leaf, n);
+    switch (grp) {
+      case 0: leaf_split_body<T, G, 0>(U, r0, rend, R, leaf, stage); break;
+      case 1: leaf_split_body<T, G, (G > 1 ? 1 : 0)>(U, r0, rend, R, leaf, stage); break;
+      case 2: leaf_split_body<T, G, (G > 2 ? 2 : 0)>(U, r0, rend, R, leaf, stage); break;
+      case 3: leaf_split_body<T, G, (G > 3 ? 3 : 0)>(U, r0, rend, R, leaf, stage); break;
+      case 4: leaf_split_body<T, G, (G > 4 ? 4 : 0)>(U, r0, rend, R, leaf, stage); break;
+      case 5: leaf_split_body<T, G, (G > 5 ? 5 : 0)>(U, r0, rend, R, leaf, stage); break;
+      case 6: leaf_split_body<T, G, (G > 6 ? 6 : 0)>(U, r0, rend, R, leaf, stage); break;
+      default: leaf_split_body<T, G, (G > 7 ? 7 : 0)>(U, r0, rend, R, leaf, stage); break;
+    }
+    if (Rs > Rt && grp == 0 && lane == 0) stage[Rt] = 0.0;
+    // the leaf's G warps (named barrier 1 + slot), then its packed triangle out
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * G) : "memory");
+    double *out = level + v * Rs;
+    for (int e = grp * 32 + lane; e < Rs; e += 32 * G) out[e] = stage[e];
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * G) : "memory");
   }
 }
 
@@ -529,6 +603,30 @@ int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
     }
 #undef RCP_LEAF
     RCP_LAUNCH_CHECK("sts_leaf_mma");
+  } else if (R <= 96 && !getenv_leaf_ffma()) {   // fp64 tensor cores, tile pairs split over warps
+    const int T = (R + 7) / 8;
+    const int G = 4, slots = 8 / G;
+    int64_t gs = ceil_div(nleaves, (int64_t)slots);
+    if (gs > 4LL * sm_count()) gs = 4LL * sm_count();
+    const size_t ssm = sizeof(double) * (size_t)slots * Rt;
+#define RCP_LEAFS(K)                                                                              \
+  case K: {                                                                                       \
+    static bool a_ = false;                                                                       \
+    if (!a_) {                                                                                    \
+      RCP_CUDA_TRY(cudaFuncSetAttribute(sts_leaf_split_kernel<K, 4>,                              \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));  \
+      a_ = true;                                                                                  \
+    }                                                                                             \
+    sts_leaf_split_kernel<K, 4><<<(unsigned)gs, 256, ssm, st>>>(d_U, n, R, leaf, nleaves, lvl);   \
+    break;                                                                                        \
+  }
+    switch (T) {
+      RCP_LEAFS(9) RCP_LEAFS(10) RCP_LEAFS(11)
+      default: RCP_LEAFS(12)
+    }
+#undef RCP_LEAFS
+    RCP_LAUNCH_CHECK("sts_leaf_split");
+    (void)G;
   } else {
   const size_t lsm = sizeof(double) * leaf * R + sizeof(uint16_t) * (size_t)R * (R + 1) / 2;
   static bool attr = false;
