@@ -250,8 +250,9 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
  * the environment: RCP_MTTKRP_PATH=tiles selects 1):
  *   0  fast: entries transposed to row order, segmented SpMM (fp64 red.add for rows split
  *      across warps; the order of a row's terms varies run to run);
- *   1  deterministic: row-tile x fiber pairs in a canonical order, every output row summed
- *      in a fixed order -- bit-identical results on every run (ref tests/test_mttkrp.py:
+ *   1  deterministic: the sampled fibers' runs per row tile ("pairs") in a canonical order,
+ *      expanded stably into row-sorted entries, rows split across the SpMM's chunks summed
+ *      in chunk order -- bit-identical results on every run (ref tests/test_mttkrp.py:
  *      60-67,163-172 require bit-identity across worker counts).  Row tiles of 16 rows
  *      (R <= 64) or 8 (R <= 128); above 4096 tiles the pairs are radix-sorted by tile,
  *      which reads their count on the host: such calls inside a CUDA-graph capture run

@@ -887,11 +887,12 @@ spmm_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__r
 // warp loads 32 entries at once (one per lane) and broadcasts them with shuffles: a
 // broadcast load would cost the L1 as many register-writeback cycles as an Hs row
 // (measured: writeback was the limiter at ~75% busy).
-template <int NP>
+template <int NP, bool DET = false>
 __global__ void __launch_bounds__(256)
 spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__restrict__ nnzp,
                    const double2 *__restrict__ ent, const double *__restrict__ Hs, int R,
-                   double *__restrict__ out) {
+                   double *__restrict__ out, double2 *__restrict__ slotF = nullptr,
+                   double2 *__restrict__ slotL = nullptr) {
   const int lane = threadIdx.x & 31;
   const int Rp = hs_stride(R);
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -919,6 +920,8 @@ spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64
             if (whole) {
               o[0] = acc[j].x;
               if (c + 1 < R) o[1] = acc[j].y;
+            } else if (DET) {   // a split row: this chunk's partial, combined in chunk order
+              (rs < c0 ? slotF : slotL)[ch * (32 * NP) + lane + 32 * j] = acc[j];
             } else {
               atomicAdd(o, acc[j].x);
               if (c + 1 < R) atomicAdd(o + 1, acc[j].y);
@@ -1080,8 +1083,8 @@ struct MttkrpLayout {
   size_t o_tkey, o_tcnt, o_trep, o_twmin, o_twmax, o_twsum, o_dsc, o_bcnt, o_dkey, o_dcnt,
       o_drep, o_dlo, o_dlen, o_doff, o_ioff, o_ifib, o_Hs, o_scan, o_rcnt, o_rptr, o_cmat,
       o_ent, o_tmp, o_bofs, o_S,
-      o_nnz, o_flag, o_fpos, o_sslot, o_uoff, o_sbase, o_tdone, o_tmask, o_icnt, o_ipos,
-      o_t64, o_t32, o_sort, o_np, o_wk, o_wv, o_wk2, o_wv2, o_wst, o_wsort;
+      o_nnz, o_flag, o_fpos, o_sslot, o_icnt, o_ipos,
+      o_t64, o_sort, o_np, o_wk, o_wv, o_wk2, o_wv2, o_wst, o_wsort, o_slots, o_slots2;
   size_t total;
   MttkrpLayout(int64_t J, int64_t cap, int64_t n_rows, int R) {
     T = 1024;
@@ -1119,19 +1122,14 @@ struct MttkrpLayout {
     o_flag = w.add(sizeof(int64_t) * (J + 1));
     o_fpos = w.add(sizeof(int64_t) * (J + 2));
     o_sslot = w.add(sizeof(int32_t) * (J + 1));
-    o_uoff = w.add(sizeof(int32_t) * (kTileMaxTiles + 2));
-    o_sbase = w.add(sizeof(int32_t) * (kTileMaxTiles + 1));
-    o_tdone = w.add(sizeof(int32_t) * kTileMaxTiles);
-    o_tmask = w.add(sizeof(uint32_t) * kTileMaxTiles);
-    // deterministic mode with many row tiles: per-item pair counts and offsets, per-tile
-    // arrays (parts, scans as int64; unit offsets, scratch bases, counters as int32), the
-    // radix sort's temporary storage and the pair count
+    // deterministic mode: per-item pair counts and offsets (many row tiles), per-tile int64
+    // arrays (tile pointers, entry counts and offsets, chunk counts and offsets), the radix
+    // sort's temporary storage and the pair count
     const int64_t nitems = J + cap / kItemE + 2;
     o_icnt = w.add(sizeof(int64_t) * nitems);
     o_ipos = w.add(sizeof(int64_t) * (nitems + 1));
-    const int64_t nt = n_rows / 8 + 2;
-    o_t64 = w.add(sizeof(int64_t) * 4 * nt);
-    o_t32 = w.add(sizeof(int32_t) * 4 * nt);
+    const int64_t nt = n_rows / 8 + 4;
+    o_t64 = w.add(sizeof(int64_t) * 5 * nt);
     o_sort = w.add(sort_tmp_bytes(cap));
     o_np = w.add(sizeof(int64_t) * 2);
     // deterministic mode: samples sorted by distinct fiber for ordered weight sums
@@ -1141,6 +1139,10 @@ struct MttkrpLayout {
     o_wv2 = w.add(sizeof(uint32_t) * (J + 1));
     o_wst = w.add(sizeof(int32_t) * (J + 1));
     o_wsort = w.add(wsort_tmp_bytes(J));
+    // deterministic mode: the SpMM's per-chunk partials of rows split across chunks
+    o_slots2 = w.add(sizeof(double2) * 2 * (size_t)(cap / kSpmmChunk + 2) * 32 * (R <= 64 ? 1 : 2));
+    // per (32-pair chunk, tile row) entry counts, then slots: chunks <= cap / 32 + tiles
+    o_slots = w.add(sizeof(int64_t) * (size_t)(cap / 32 + n_rows / 8 + 2) * 16);
     total = w.total + 256;
   }
 };
@@ -1244,7 +1246,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   unsigned long long *twmin = (unsigned long long *)P(L.o_twmin);
   unsigned long long *twmax = (unsigned long long *)P(L.o_twmax);
   double *twsum = (double *)P(L.o_twsum), *dsc = (double *)P(L.o_dsc);
-  mttkrp_init_kernel<<<4 * sm_count(), 256, 0, st>>>(d_out, (tiles || tiles_big) ? 0 : n_rows * (int64_t)R, L.T, tkey,
+  mttkrp_init_kernel<<<4 * sm_count(), 256, 0, st>>>(d_out, n_rows * (int64_t)R, L.T, tkey,
                                                       tcnt, trep, twmin, twmax, twsum);
   RCP_LAUNCH_CHECK("mttkrp_init");
   hash_insert_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(
@@ -1297,29 +1299,63 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   int32_t *ifib = (int32_t *)P(L.o_ifib);
   item_fill_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, st>>>(ioff, S, ifib);
   RCP_LAUNCH_CHECK("item_fill");
+  // deterministic mode, after the pairs: row-sorted entries per tile (stable), then the
+  // segmented SpMM with split rows combined in chunk order
+  auto det_csr = [&](const uint64_t *pairs_, const int64_t *tptr_, int64_t nt_, double2 *ent_) -> int {
+    int64_t *t64_ = (int64_t *)P(L.o_t64);
+    int64_t *te = t64_ + (nt_ + 2), *eoff = t64_ + 2 * (nt_ + 2);
+    const unsigned gw = (unsigned)(8 * sm_count());
+    tile_entries_kernel<<<gw, 256, 0, st>>>(tptr_, nt_, pairs_, te);
+    RCP_LAUNCH_CHECK("tile_entries");
+    int rcx = scan_i64_exclusive(te, eoff, nt_, nullptr, scan_ws, st);
+    if (rcx) return rcx;
+    // 32-pair chunks per tile: per-chunk row counts -> stable slots -> entries
+    int64_t *nchk = t64_ + 3 * (nt_ + 2), *choff = nchk + (nt_ + 2);
+    tile_chunks_kernel<<<(unsigned)ceil_div(nt_, 256), 256, 0, st>>>(tptr_, nt_, nchk);
+    RCP_LAUNCH_CHECK("tile_chunks");
+    rcx = scan_i64_exclusive(nchk, choff, nt_, nullptr, scan_ws, st);
+    if (rcx) return rcx;
+    int64_t *cc = (int64_t *)P(L.o_slots);   // <= pairs / 32 + n_tiles chunks x TR rows
+    if (tile_ts == 4) {
+      chunk_rows_kernel<4><<<gw, 256, 0, st>>>(tptr_, choff, nt_, pairs_, d_rows, cc);
+      tile_rowscan_kernel<4><<<gw, 256, 0, st>>>(choff, nt_, n_rows, eoff, cc, rptr, d_stats);
+      chunk_write_kernel<4><<<gw, 256, 0, st>>>(tptr_, choff, nt_, pairs_, d_rows, d_vals, cc, ent_);
+    } else {
+      chunk_rows_kernel<3><<<gw, 256, 0, st>>>(tptr_, choff, nt_, pairs_, d_rows, cc);
+      tile_rowscan_kernel<3><<<gw, 256, 0, st>>>(choff, nt_, n_rows, eoff, cc, rptr, d_stats);
+      chunk_write_kernel<3><<<gw, 256, 0, st>>>(tptr_, choff, nt_, pairs_, d_rows, d_vals, cc, ent_);
+    }
+    RCP_LAUNCH_CHECK("tile_expand");
+    double2 *slotF = (double2 *)P(L.o_slots2);
+    double2 *slotL = slotF + (size_t)(cap / kSpmmChunk + 2) * 32 * tile_np;
+    const unsigned sb2 = (unsigned)(RCP_SPMM_BLOCKS_PER_SM * sm_count());
+    const int64_t *nnzp = eoff + nt_;
+    if (tile_np == 1) {
+      spmm_packed_kernel<1, true><<<sb2, 256, 0, st>>>(rptr, n_rows, nnzp, ent_, Hs, R, d_out, slotF, slotL);
+      RCP_LAUNCH_CHECK("spmm_det");
+      spmm_fix_kernel<1><<<gw, 256, 0, st>>>(rptr, n_rows, slotF, slotL, R, d_out);
+    } else {
+      spmm_packed_kernel<2, true><<<sb2, 256, 0, st>>>(rptr, n_rows, nnzp, ent_, Hs, R, d_out, slotF, slotL);
+      RCP_LAUNCH_CHECK("spmm_det");
+      spmm_fix_kernel<2><<<gw, 256, 0, st>>>(rptr, n_rows, slotF, slotL, R, d_out);
+    }
+    RCP_LAUNCH_CHECK("spmm_fix");
+    return RCP_OK;
+  };
   if (tiles) {
     const int grid = 2 * sm_count();                    // pair passes: 2 CTAs per SM
     const int nt = (int)n_tiles;
     int32_t *cmat = (int32_t *)P(L.o_cmat);            // grid x n_tiles
-    int64_t *tcntp = rcnt, *tptr = rptr;                // pairs per tile, tile pointers
-    uint64_t *pairs = (uint64_t *)P(L.o_ent);           // <= entries <= cap pairs
-    double2 *scratch = (double2 *)P(L.o_tmp);           // <= 2 cap / kTilePart parts of 8 KB
-    int32_t *uoff = (int32_t *)P(L.o_uoff), *sbase = (int32_t *)P(L.o_sbase);
-    int32_t *tdone = (int32_t *)P(L.o_tdone);
-    uint32_t *tmask = (uint32_t *)P(L.o_tmask);
+    int64_t *tcntp = rcnt;                              // pairs per tile
+    int64_t *tptr = (int64_t *)P(L.o_t64);              // tile pointers (n_tiles + 1)
+    uint64_t *pairs = (uint64_t *)P(L.o_tmp);           // <= entries <= cap pairs
     static bool tattr = false;
     if (!tattr) {
       const int scat = (int)pair_scatter_smem(kTileMaxTiles);
       RCP_CUDA_TRY(cudaFuncSetAttribute(pair_scatter_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, scat));
       RCP_CUDA_TRY(cudaFuncSetAttribute(pair_scatter_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, scat));
-      RCP_CUDA_TRY(cudaFuncSetAttribute(tile_spmm_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)tile_spmm_smem<4, 1>()));
-      RCP_CUDA_TRY(cudaFuncSetAttribute(tile_spmm_kernel<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)tile_spmm_smem<3, 2>()));
       tattr = true;
     }
-    RCP_CUDA_TRY(cudaMemsetAsync(tdone, 0, sizeof(int32_t) * kTileMaxTiles, st));
-    RCP_CUDA_TRY(cudaMemsetAsync(tmask, 0, sizeof(uint32_t) * kTileMaxTiles, st));
     const size_t hsm = sizeof(int32_t) * nt;
     if (tile_ts == 4) tile_hist_kernel<4><<<grid, kPairThreads, hsm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, cmat);
     else tile_hist_kernel<3><<<grid, kPairThreads, hsm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, cmat);
@@ -1333,16 +1369,8 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     if (tile_ts == 4) pair_scatter_kernel<4><<<grid, kPairThreads, ssm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, tptr, cmat, pairs);
     else pair_scatter_kernel<3><<<grid, kPairThreads, ssm, st>>>(ioff, S, ifib, dlo, dlen, d_rows, nt, tptr, cmat, pairs);
     RCP_LAUNCH_CHECK("pair_scatter");
-    tile_units_kernel<<<1, 1024, 0, st>>>(tcntp, nt, uoff, sbase);
-    RCP_LAUNCH_CHECK("tile_units");
-    const unsigned sg = (unsigned)(4 * sm_count());   // 4 CTAs of 4 warps per SM (smem, registers)
-    if (tile_np == 1)
-      tile_spmm_kernel<4, 1><<<sg, kTileWarps * 32, tile_spmm_smem<4, 1>(), st>>>(
-          tptr, nt, n_rows, uoff, sbase, pairs, d_rows, d_vals, Hs, R, d_out, scratch, tdone, tmask, d_stats);
-    else
-      tile_spmm_kernel<3, 2><<<sg, kTileWarps * 32, tile_spmm_smem<3, 2>(), st>>>(
-          tptr, nt, n_rows, uoff, sbase, pairs, d_rows, d_vals, Hs, R, d_out, scratch, tdone, tmask, d_stats);
-    RCP_LAUNCH_CHECK("tile_spmm");
+    rc = det_csr(pairs, tptr, nt, ent);
+    if (rc) return rc;
     return RCP_OK;
   }
   if (tiles_big) {
@@ -1353,12 +1381,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     uint64_t *vB = (uint64_t *)P(L.o_tmp);
     int64_t *icnt2 = (int64_t *)P(L.o_icnt), *ipos = (int64_t *)P(L.o_ipos);
     int64_t *np = (int64_t *)P(L.o_np);
-    int64_t *t64 = (int64_t *)P(L.o_t64);
-    int64_t *up = t64, *spp = t64 + (nt + 2), *uo = t64 + 2 * (nt + 2), *so = t64 + 3 * (nt + 2);
-    int32_t *t32 = (int32_t *)P(L.o_t32);
-    int32_t *uoff = t32, *sbase = t32 + (nt + 2), *tdone = t32 + 2 * (nt + 2);
-    uint32_t *tmask = (uint32_t *)(t32 + 3 * (nt + 2));
-    int64_t *tptr = rptr;   // n_rows + 2 >= n_tiles + 1
+    int64_t *tptr = (int64_t *)P(L.o_t64);   // tile pointers (n_tiles + 1)
     const int ts = tile_ts;
     const unsigned gw = (unsigned)(8 * sm_count());
     if (ts == 4) pair_count_kernel<4><<<gw, 256, 0, st>>>(ioff, S, ifib, dlo, dlen, d_rows, icnt2, np + 1);
@@ -1385,35 +1408,11 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
       RCP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(P(L.o_sort), tb, kb, vb, (int)h_np, 0, bits, st));
     const uint32_t *tk = kb.Current();
     const uint64_t *pairs = vb.Current();
-    double2 *scratch = (double2 *)(vb.Current() == vA ? (void *)vB : (void *)vA);
+    double2 *entries = (double2 *)(vb.Current() == vA ? (void *)vB : (void *)vA);
     tile_bounds_kernel<<<(unsigned)ceil_div(nt + 1, 256), 256, 0, st>>>(tk, np, nt, tptr);
     RCP_LAUNCH_CHECK("tile_bounds");
-    tile_parts_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, st>>>(tptr, nt, up, spp);
-    RCP_LAUNCH_CHECK("tile_parts");
-    rc = scan_i64_exclusive(up, uo, nt, nullptr, scan_ws, st);
+    rc = det_csr(pairs, tptr, nt, entries);
     if (rc) return rc;
-    rc = scan_i64_exclusive(spp, so, nt, nullptr, scan_ws, st);
-    if (rc) return rc;
-    tile_parts_i32_kernel<<<(unsigned)ceil_div(nt + 1, 256), 256, 0, st>>>(uo, so, nt, uoff, sbase);
-    RCP_LAUNCH_CHECK("tile_parts_i32");
-    RCP_CUDA_TRY(cudaMemsetAsync(tdone, 0, sizeof(int32_t) * nt, st));
-    RCP_CUDA_TRY(cudaMemsetAsync(tmask, 0, sizeof(uint32_t) * nt, st));
-    static bool battr = false;
-    if (!battr) {
-      RCP_CUDA_TRY(cudaFuncSetAttribute(tile_spmm_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)tile_spmm_smem<4, 1>()));
-      RCP_CUDA_TRY(cudaFuncSetAttribute(tile_spmm_kernel<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)tile_spmm_smem<3, 2>()));
-      battr = true;
-    }
-    const unsigned sg = (unsigned)(4 * sm_count());
-    if (tile_np == 1)
-      tile_spmm_kernel<4, 1><<<sg, kTileWarps * 32, tile_spmm_smem<4, 1>(), st>>>(
-          tptr, (int)nt, n_rows, uoff, sbase, pairs, d_rows, d_vals, Hs, R, d_out, scratch, tdone, tmask, d_stats);
-    else
-      tile_spmm_kernel<3, 2><<<sg, kTileWarps * 32, tile_spmm_smem<3, 2>(), st>>>(
-          tptr, (int)nt, n_rows, uoff, sbase, pairs, d_rows, d_vals, Hs, R, d_out, scratch, tdone, tmask, d_stats);
-    RCP_LAUNCH_CHECK("tile_spmm");
     return RCP_OK;
   }
   // 4. row histogram -> row pointers; 5. scatter into row order (packed entries)

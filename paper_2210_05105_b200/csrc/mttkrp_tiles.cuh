@@ -1,35 +1,26 @@
-// Row-tile x fiber sampled MTTKRP (included by mttkrp.cu inside its anonymous namespace).
+// Deterministic sampled MTTKRP (included by mttkrp.cu inside its anonymous namespace).
 //
 // The mode-k store is column-major (CSC analogue, ref matricization.py:67-128): the entries
 // of one fiber are contiguous and their rows ascend.  Cutting the output rows into tiles of
-// TR = 2^TS rows, the entries of a sampled fiber that fall in one tile are therefore one
-// contiguous run of at most TR entries — a "pair" (tile, fiber).  Instead of transposing
-// every gathered entry into row order (the reference's sparse transpose,
-// mttkrp.py:131-155), this path moves only the pairs (8 bytes each, ~2-3 entries per pair at
-// C3), and reads the entries straight from the store:
+// TR = 2^TS rows, the entries of a sampled fiber that fall in one tile are one contiguous
+// run of at most TR entries -- a "pair" (tile, fiber).  The deterministic mode orders the
+// pairs canonically (by tile, then by fiber) and derives every later order from that one:
 //
-//   pass 1  tile_hist      per CTA, pairs per tile (CTA-private shared-memory histogram)
-//   prefix  cta_prefix     per tile, exclusive prefix over CTAs + tile totals -> tptr
-//   pass 2  pair_scatter   pairs written to their tile's range in a deterministic order
-//   units   tile_units     tiles cut into parts of <= kTilePart pairs
-//   spmm    tile_spmm      per part: 8 warps split its pairs; each warp keeps the tile's TR
-//                          output rows in registers, loads the fiber's scaled KRP row Hs_d
-//                          ONCE per pair and applies every entry of the pair to it
-//                          (row selected by a warp-uniform switch); warps and parts are
-//                          combined in a fixed order (no atomics on the output)
+//   pairs   <= 4096 tiles: tile_hist (pairs per (CTA, tile)) -> cta_prefix -> pair_scatter
+//           (slots from per-tile warp masks in fixed batches);  more tiles: pair_count ->
+//           scan -> pair_emit (item order) -> stable radix sort by tile
+//   entries tile_entries + scan (entry offset of every tile); 32-pair chunks: chunk_rows
+//           (entries per row) -> tile_rowscan (each chunk's slot per row, stable) ->
+//           chunk_write: row-sorted entries, pair order inside a row
+//   spmm    the fast path's segmented SpMM, except that rows split across its chunks leave
+//           per-chunk partials which spmm_fix sums in chunk order (no red.add)
 //
 // Every order is a function of the input only, so results are bit-reproducible run to run
 // (ref tests/test_mttkrp.py:60-67,163-172 require bit-identity across worker counts).
 // Pair record: store position (36 bits) | count - 1 (6 bits) | distinct fiber id (22 bits).
 
-#include "tile_apply_ptx.cuh"
-
-
-constexpr int kTilePart = 2048;         // pairs per spmm part (4 warps x 512)
-constexpr int kTileWarps = 4;
 constexpr int kScatterItems = 1024;     // items per pair_scatter chunk (spans cached in smem)
-constexpr int kTileMaxRowsShift = 5;    // TR <= 32: a pair's end is always inside the next window
-constexpr int kTileMaxTiles = 4096;     // tiles per mode (tile_units scans them in one CTA)
+constexpr int kTileMaxTiles = 4096;     // CTA-private tile histograms up to this many tiles
 
 __device__ __forceinline__ uint64_t pack_pair(int64_t pos, int cnt, int64_t d) {
   return ((uint64_t)pos << 28) | ((uint64_t)(cnt - 1) << 22) | (uint64_t)d;
@@ -315,288 +306,6 @@ inline size_t pair_scatter_smem(int n_tiles) {
   return 12 * (size_t)n_tiles + (size_t)kScatterItems * (4 * 8 + 4) + 4 * (kScatterItems + 1);
 }
 
-// ---------------------------------------------------------------- work units
-// Tile t is cut into ceil(n_t / kTilePart) parts (at least one: empty tiles still write
-// their zero rows).  uoff[t] = first unit of tile t; sbase[t] = first scratch slot of a
-// multi-part tile.  One CTA of 1024 threads, n_tiles <= 4096.
-__global__ void __launch_bounds__(1024)
-tile_units_kernel(const int64_t *__restrict__ tcnt, int n_tiles, int32_t *__restrict__ uoff,
-                  int32_t *__restrict__ sbase) {
-  __shared__ int32_t a[4096 + 1], b[4096 + 1];
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-    const int32_t np = (int32_t)max((int64_t)1, ceil_div(tcnt[t], (int64_t)kTilePart));
-    a[t] = np;
-    b[t] = np > 1 ? np : 0;
-  }
-  __syncthreads();
-  const int nu = block_scan_excl(a, n_tiles);
-  const int ns = block_scan_excl(b, n_tiles);
-  (void)ns;
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-    uoff[t] = a[t];
-    sbase[t] = b[t];
-  }
-  if (threadIdx.x == 0) uoff[n_tiles] = nu;
-}
-
-// ---------------------------------------------------------------- per-tile SpMM
-// Accumulator row g of the warp's tile: acc[g] += v * h (g warp-uniform), through the
-// generated brx.idx jump table (tile_apply_ptx.cuh).
-template <int TR, int NP>
-__device__ __forceinline__ void tile_apply(double2 (&a)[TR][NP], int g, double v, const double2 (&h)[NP]);
-
-template <>
-__device__ __forceinline__ void tile_apply<16, 1>(double2 (&a)[16][1], int g, double v, const double2 (&h)[1]) {
-  tile_apply_ptx_16_1(a[0][0].x, a[0][0].y, a[1][0].x, a[1][0].y, a[2][0].x, a[2][0].y, a[3][0].x, a[3][0].y,
-                      a[4][0].x, a[4][0].y, a[5][0].x, a[5][0].y, a[6][0].x, a[6][0].y, a[7][0].x, a[7][0].y,
-                      a[8][0].x, a[8][0].y, a[9][0].x, a[9][0].y, a[10][0].x, a[10][0].y, a[11][0].x, a[11][0].y,
-                      a[12][0].x, a[12][0].y, a[13][0].x, a[13][0].y, a[14][0].x, a[14][0].y, a[15][0].x, a[15][0].y,
-                      g, v, h[0].x, h[0].y);
-}
-
-template <>
-__device__ __forceinline__ void tile_apply<8, 2>(double2 (&a)[8][2], int g, double v, const double2 (&h)[2]) {
-  tile_apply_ptx_8_2(a[0][0].x, a[0][0].y, a[0][1].x, a[0][1].y, a[1][0].x, a[1][0].y, a[1][1].x, a[1][1].y,
-                     a[2][0].x, a[2][0].y, a[2][1].x, a[2][1].y, a[3][0].x, a[3][0].y, a[3][1].x, a[3][1].y,
-                     a[4][0].x, a[4][0].y, a[4][1].x, a[4][1].y, a[5][0].x, a[5][0].y, a[5][1].x, a[5][1].y,
-                     a[6][0].x, a[6][0].y, a[6][1].x, a[6][1].y, a[7][0].x, a[7][0].y, a[7][1].x, a[7][1].y,
-                     g, v, h[0].x, h[0].y, h[1].x, h[1].y);
-}
-
-// Per-warp ring of kTileRing pair slots filled by cp.async: the fiber's scaled KRP row (the
-// lane's column pairs) and the pair's rows and values.  Pair i + kTileRing is requested while
-// pair i is applied, so every warp keeps kTileRing pairs' loads in flight.
-// Per-warp ring of 2 x BS pair slots filled by cp.async, BS pairs per batch: batch b + 1 is
-// requested while batch b is applied.  Each pair is requested by 32 / BS lanes of its own
-// (the lanes split its Hs row's 16-byte chunks and its entries), so issuing a batch costs a
-// few instructions per pair.  Slot: the fiber's scaled KRP row (512 NP bytes), then one
-// 16-byte record {value, row} per entry.
-template <int TR, int NP>
-struct TileSlotLayout {
-  static constexpr int BS = NP == 1 ? 8 : 4;        // pairs per batch
-  static constexpr int LPP = 32 / BS;               // lanes per pair
-  static constexpr uint32_t E = 512u * NP;          // entry records
-  static constexpr uint32_t bytes = E + 16u * (TR + 1);   // +1: the loop reads one record ahead
-};
-
-__device__ __forceinline__ void cpa16_u32(uint32_t s, const void *g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g));
-}
-__device__ __forceinline__ void cpa8_u32(uint32_t s, const void *g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(g));
-}
-__device__ __forceinline__ void cpa4_u32(uint32_t s, const void *g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(g));
-}
-__device__ __forceinline__ double2 lds_f64x2(uint32_t s) {
-  double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(s) : "memory");
-  return v;
-}
-
-template <int TS, int NP>
-constexpr size_t tile_spmm_smem() {
-  using SL = TileSlotLayout<(1 << TS), NP>;
-  constexpr size_t ring = (size_t)kTileWarps * 2 * SL::BS * SL::bytes;
-  constexpr size_t red = (size_t)kTileWarps * (1 << TS) * 32 * NP * sizeof(double2);
-  return ring > red ? ring : red;
-}
-
-template <int TS, int NP>
-__global__ void __launch_bounds__(kTileWarps * 32, 4)
-tile_spmm_kernel(const int64_t *__restrict__ tptr, int n_tiles, int64_t n_rows,
-                 const int32_t *__restrict__ uoff, const int32_t *__restrict__ sbase,
-                 const uint64_t *__restrict__ pairs, const int32_t *__restrict__ rows,
-                 const double *__restrict__ vals, const double *__restrict__ Hs, int R,
-                 double *__restrict__ out, double2 *__restrict__ scratch,
-                 int32_t *__restrict__ tile_done, uint32_t *__restrict__ tile_mask,
-                 int64_t *__restrict__ stats) {
-  constexpr int TR = 1 << TS;
-  constexpr int W = 32 * NP;   // double2 columns per row
-  using SL = TileSlotLayout<TR, NP>;
-  constexpr int BS = SL::BS, LPP = SL::LPP;
-  constexpr uint32_t kSlot = SL::bytes, kSlotE = SL::E;
-  extern __shared__ __align__(16) unsigned char tsm[];
-  double2 *red = reinterpret_cast<double2 *>(tsm);                 // [kTileWarps][TR][W]
-  __shared__ uint32_t s_mask;
-  __shared__ int s_last;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t ring_u32 = (uint32_t)__cvta_generic_to_shared(tsm) + (uint32_t)(wid * 2 * BS) * kSlot;
-  const int Rp2 = hs_stride(R) >> 1;
-  const double2 *H2 = reinterpret_cast<const double2 *>(Hs);
-  const int U = uoff[n_tiles];
-  unsigned long long hit_total = 0;
-  if (threadIdx.x == 0) s_mask = 0u;
-  __syncthreads();
-  for (int u = blockIdx.x; u < U; u += gridDim.x) {
-    int lo = 0, hi = n_tiles;   // tile: largest t with uoff[t] <= u
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (uoff[mid] <= u) lo = mid; else hi = mid;
-    }
-    const int t = lo;
-    const int part = u - uoff[t], nparts = uoff[t + 1] - uoff[t];
-    const int64_t p0 = tptr[t], p1 = tptr[t + 1];
-    const int64_t per = ceil_div(p1 - p0, (int64_t)nparts);
-    const int64_t a = p0 + part * per, b = min(a + per, p1);
-    const int64_t wper = ceil_div(b - a, (int64_t)kTileWarps);
-    const int64_t wa = min(a + wid * wper, b), wb = min(wa + wper, b);
-    const int n = (int)(wb - wa);
-    double2 acc[TR][NP];
-#pragma unroll
-    for (int r = 0; r < TR; ++r)
-#pragma unroll
-      for (int j = 0; j < NP; ++j) acc[r][j] = make_double2(0.0, 0.0);
-    uint32_t hmask = 0u;
-    // lane -> (pair jp of the batch, sub-lane sub): the lane requests the pair's 16-byte
-    // Hs chunks sub, sub + LPP, ... and its entries sub, sub + LPP, ...
-    const int jp = lane / LPP, sub = lane % LPP;
-    const int nch = (R + 1) >> 1;                                   // 16-byte chunks per row
-    const int nb = (int)ceil_div((int64_t)n, (int64_t)BS);
-    int cnt_nx = 0, cnt_cu = 0;   // this lane's pair count in the requested / applied batch
-    // Pair records come from registers: rc holds the records of 32-pair group g0, rn of
-    // group g0 + 1 (loaded a group ahead).  The store entries of batch bi + kPF are
-    // prefetched into L2 while batch bi + 1 is copied, so the copies hit L2.
-    constexpr int kPF = 3;
-    int g0 = 0;
-    uint64_t rc = lane < n ? pairs[wa + lane] : 0ull;
-    uint64_t rn = 32 + lane < n ? pairs[wa + 32 + lane] : 0ull;
-    auto rec_of = [&](int ip) {   // ip in [32 g0, 32 g0 + 64)
-      const uint64_t x = __shfl_sync(0xffffffffu, rc, ip & 31);
-      const uint64_t y = __shfl_sync(0xffffffffu, rn, ip & 31);
-      return (ip >> 5) == g0 ? x : y;
-    };
-    auto issue = [&](int bi) {
-      if (bi * BS >= 32 * (g0 + 1)) {   // warp-uniform: advance the record window
-        ++g0;
-        rc = rn;
-        rn = 32 * (g0 + 1) + lane < n ? pairs[wa + 32 * (g0 + 1) + lane] : 0ull;
-      }
-      const int ip = bi * BS + jp;
-      const uint64_t pr = rec_of(ip);
-      const int ipf = (bi + kPF) * BS + jp;
-      const uint64_t pf = rec_of(ipf);
-      const uint32_t sl = ring_u32 + (uint32_t)((bi & 1) * BS + jp) * kSlot;
-      int c = 0;
-      if (ip < n) {
-        c = pair_cnt(pr);
-        const double2 *hs = H2 + (int64_t)pair_fib(pr) * Rp2;
-#pragma unroll
-        for (int q = 0; q < 32 * NP / LPP; ++q) {
-          const int ch = q * LPP + sub;
-          if (ch < nch) cpa16_u32(sl + 16u * ch, hs + ch);
-        }
-        const int64_t pe = pair_pos(pr);
-        for (int e = sub; e < c; e += LPP) {
-          cpa8_u32(sl + kSlotE + 16u * e, vals + pe + e);
-          cpa4_u32(sl + kSlotE + 16u * e + 8u, rows + pe + e);
-        }
-      }
-      if (ipf < n && sub < 2) {
-        const int64_t pe = pair_pos(pf);
-        if (sub == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(vals + pe));
-        else asm volatile("prefetch.global.L2 [%0];" ::"l"(rows + pe));
-      }
-      cpa_commit();
-      return c;
-    };
-    if (nb > 0) cnt_nx = issue(0);
-    for (int bi = 0; bi < nb; ++bi) {
-      cnt_cu = cnt_nx;
-      cnt_nx = bi + 1 < nb ? issue(bi + 1) : (cpa_commit(), 0);
-      cpa_wait<1>();
-      __syncwarp();
-      const uint32_t base = ring_u32 + (uint32_t)((bi & 1) * BS) * kSlot;
-      const int np_ = min(BS, n - bi * BS);
-      for (int j = 0; j < np_; ++j) {
-        const uint32_t sl = base + (uint32_t)j * kSlot;
-        double2 h[NP];
-#pragma unroll
-        for (int jj = 0; jj < NP; ++jj) h[jj] = lds_f64x2(sl + 16u * lane + 512u * jj);
-        const int c = __shfl_sync(0xffffffffu, cnt_cu, j * LPP);
-        uint32_t ea = sl + kSlotE;
-        double2 rec = lds_f64x2(ea);   // the next record is loaded before this one's branch
-        for (int e = 0; e < c; ++e) {
-          ea += 16u;
-          const double2 nx = lds_f64x2(ea);   // (past the last entry: unused slot bytes)
-          const int g = __double2loint(rec.y) & (TR - 1);
-          hmask |= 1u << g;
-          tile_apply<TR, NP>(acc, g, rec.x, h);
-          rec = nx;
-        }
-      }
-      __syncwarp();
-    }
-    cpa_wait<0>();
-    __syncthreads();   // every warp is done with its ring: the area becomes the reduction buffer
-    // fixed-order combine of the warps' partial tiles
-    double2 *mine = red + (size_t)wid * TR * W;
-#pragma unroll
-    for (int r = 0; r < TR; ++r)
-#pragma unroll
-      for (int j = 0; j < NP; ++j) mine[r * W + lane + 32 * j] = acc[r][j];
-    if (lane == 0 && hmask) atomicOr(&s_mask, hmask);
-    __syncthreads();
-    const int64_t row0 = (int64_t)t * TR;
-    double2 *slot = nparts > 1 ? scratch + ((size_t)sbase[t] + part) * TR * W : nullptr;
-    for (int i = threadIdx.x; i < TR * W; i += blockDim.x) {
-      double2 s = red[i];
-#pragma unroll
-      for (int w = 1; w < kTileWarps; ++w) {
-        const double2 x = red[(size_t)w * TR * W + i];
-        s.x += x.x;
-        s.y += x.y;
-      }
-      if (slot) {
-        __stcg(slot + i, s);
-      } else {
-        const int64_t row = row0 + i / W;
-        const int c = 2 * (i % W);
-        if (row < n_rows && c < R) {
-          out[row * R + c] = s.x;
-          if (c + 1 < R) out[row * R + c + 1] = s.y;
-        }
-      }
-    }
-    if (nparts == 1) {
-      if (threadIdx.x == 0) hit_total += __popc(s_mask);
-    } else {
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        atomicOr(&tile_mask[t], s_mask);
-        s_last = atomicAdd(&tile_done[t], 1) == nparts - 1;
-      }
-      __syncthreads();
-      if (s_last) {   // the last part to finish sums every part in part order
-        __threadfence();
-        const double2 *base = scratch + (size_t)sbase[t] * TR * W;
-        for (int i = threadIdx.x; i < TR * W; i += blockDim.x) {
-          double2 s = __ldcg(base + i);
-          for (int q = 1; q < nparts; ++q) {
-            const double2 x = __ldcg(base + (size_t)q * TR * W + i);
-            s.x += x.x;
-            s.y += x.y;
-          }
-          const int64_t row = row0 + i / W;
-          const int c = 2 * (i % W);
-          if (row < n_rows && c < R) {
-            out[row * R + c] = s.x;
-            if (c + 1 < R) out[row * R + c + 1] = s.y;
-          }
-        }
-        if (threadIdx.x == 0) {
-          hit_total += __popc(atomicExch(&tile_mask[t], 0u));
-          tile_done[t] = 0;
-        }
-      }
-    }
-    if (threadIdx.x == 0) s_mask = 0u;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0 && hit_total) atomicAdd((unsigned long long *)&stats[4], hit_total);
-}
-
 // ---------------------------------------------------------------- many row tiles
 // Modes with more than kTileMaxTiles row tiles (C4/C5 factor modes: 10^5..10^6 tiles): the
 // pairs are emitted per item in item order (count, scan, emit: fiber order, ascending tile
@@ -682,25 +391,6 @@ __global__ void tile_bounds_kernel(const uint32_t *__restrict__ tkeys, const int
   tptr[t] = lo;
 }
 
-// Per tile: parts (>= 1) and multi-part parts, as int64 counts for the scans.
-__global__ void tile_parts_kernel(const int64_t *__restrict__ tptr, int64_t n_tiles,
-                                  int64_t *__restrict__ up, int64_t *__restrict__ sp) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= n_tiles) return;
-  const int64_t np = max((int64_t)1, ceil_div(tptr[t + 1] - tptr[t], (int64_t)kTilePart));
-  up[t] = np;
-  sp[t] = np > 1 ? np : 0;
-}
-
-__global__ void tile_parts_i32_kernel(const int64_t *__restrict__ uo, const int64_t *__restrict__ so,
-                                      int64_t n_tiles, int32_t *__restrict__ uoff,
-                                      int32_t *__restrict__ sbase) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t > n_tiles) return;
-  uoff[t] = (int32_t)uo[t];
-  if (t < n_tiles) sbase[t] = (int32_t)so[t];
-}
-
 // ---------------------------------------------------------------- ordered sample weights
 // Deterministic mode: a distinct fiber whose samples carry unequal weights (an injected batch;
 // sampler output has equal weights, whose merged weight count * w^2 is exact) gets its sum
@@ -739,4 +429,177 @@ __global__ void ordered_w2_kernel(const int64_t *__restrict__ Sp, const int32_t 
     s = fma(x, x, s);
   }
   dsc[d] = s;
+}
+
+// ---------------------------------------------------------------- canonical row order
+// The deterministic mode's pairs (tile order, fiber order inside a tile) expanded into the
+// row-sorted entries of the segmented SpMM: per tile a stable counting sort by row, so the
+// entries of a row keep pair order.  The SpMM then combines rows split across its chunks
+// in chunk order (spmm_packed_kernel<NP, true> + spmm_fix_kernel) instead of red.add.
+__global__ void tile_entries_kernel(const int64_t *__restrict__ tptr, int64_t n_tiles,
+                                    const uint64_t *__restrict__ pairs, int64_t *__restrict__ te) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n_tiles; t += nw) {
+    int64_t c = 0;
+    for (int64_t p = tptr[t] + lane; p < tptr[t + 1]; p += 32) c += pair_cnt(pairs[p]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) te[t] = c;
+  }
+}
+
+// Rows the deterministic SpMM split across chunks: their chunk partials summed in chunk order.
+template <int NP>
+__global__ void spmm_fix_kernel(const int64_t *__restrict__ rptr, int64_t n_rows,
+                                const double2 *__restrict__ slotF, const double2 *__restrict__ slotL,
+                                int R, double *__restrict__ out) {
+  constexpr int CH = kSpmmChunk;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n_rows; r += nw) {
+    const int64_t rs = rptr[r], re = rptr[r + 1];
+    if (re <= rs) continue;
+    const int64_t c0 = rs / CH, c1 = (re - 1) / CH;
+    if (c0 == c1) continue;   // whole in one chunk: stored by the SpMM
+    double2 s[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) s[j] = make_double2(0.0, 0.0);
+    for (int64_t c = c0; c <= c1; ++c) {
+      const double2 *sl = (rs < c * CH ? slotF : slotL) + c * (32 * NP);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        const double2 v = sl[lane + 32 * j];
+        s[j].x += v.x;
+        s[j].y += v.y;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const int c = 2 * (lane + 32 * j);
+      if (c < R) {
+        out[r * R + c] = s[j].x;
+        if (c + 1 < R) out[r * R + c + 1] = s[j].y;
+      }
+    }
+  }
+}
+
+// Parallel form of the expansion: 32-pair chunks of each tile (one warp each) count their
+// entries per row, a per-tile pass turns the counts into each chunk's slot per row (chunk
+// order = pair order: stable), and the chunks write their entries.
+__global__ void tile_chunks_kernel(const int64_t *__restrict__ tptr, int64_t n_tiles,
+                                   int64_t *__restrict__ nch) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n_tiles) nch[t] = ceil_div(tptr[t + 1] - tptr[t], (int64_t)32);
+}
+
+__device__ __forceinline__ int64_t chunk_tile(const int64_t *__restrict__ choff, int64_t n_tiles,
+                                              int64_t c) {
+  int64_t lo = 0, hi = n_tiles;   // largest t with choff[t] <= c
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (choff[mid] <= c) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <int TS>
+__global__ void chunk_rows_kernel(const int64_t *__restrict__ tptr, const int64_t *__restrict__ choff,
+                                  int64_t n_tiles, const uint64_t *__restrict__ pairs,
+                                  const int32_t *__restrict__ rows, int64_t *__restrict__ cc) {
+  constexpr int TR = 1 << TS;
+  const int lane = threadIdx.x & 31;
+  const int64_t n_ch = choff[n_tiles];
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < n_ch; c += nw) {
+    const int64_t t = chunk_tile(choff, n_tiles, c);
+    const int64_t p = tptr[t] + 32 * (c - choff[t]) + lane;
+    uint32_t m = 0;
+    if (p < tptr[t + 1]) {
+      const uint64_t pr = pairs[p];
+      const int64_t pos = pair_pos(pr);
+      const int cn = pair_cnt(pr);
+      for (int e = 0; e < cn; ++e) m |= 1u << (rows[pos + e] & (TR - 1));
+    }
+    int mine = 0;
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      const int n = __popc(__ballot_sync(0xffffffffu, (m >> r) & 1u));
+      if (lane == r) mine = n;
+    }
+    if (lane < TR) cc[c * TR + lane] = mine;
+  }
+}
+
+// Per tile (warp): row r's chunks' counts -> their absolute first slots; row pointers.
+template <int TS>
+__global__ void tile_rowscan_kernel(const int64_t *__restrict__ choff, int64_t n_tiles, int64_t n_rows,
+                                    const int64_t *__restrict__ eoff, int64_t *__restrict__ cc,
+                                    int64_t *__restrict__ rptr, int64_t *__restrict__ stats) {
+  constexpr int TR = 1 << TS;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long hit = 0;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n_tiles; t += nw) {
+    const int64_t c0 = choff[t], c1 = choff[t + 1];
+    int64_t tot = 0;   // lane r: entries of row r in the tile
+    if (lane < TR)
+      for (int64_t c = c0; c < c1; ++c) tot += cc[c * TR + lane];
+    int64_t x = lane < TR ? tot : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    int64_t run = eoff[t] + x - (lane < TR ? tot : 0);
+    const int64_t row = t * TR + lane;
+    if (lane < TR && row < n_rows) rptr[row] = run;
+    if (lane < TR && row == n_rows - 1) rptr[n_rows] = run + tot;
+    hit += __popc(__ballot_sync(0xffffffffu, lane < TR && tot > 0));
+    if (lane < TR)
+      for (int64_t c = c0; c < c1; ++c) {
+        const int64_t v = cc[c * TR + lane];
+        cc[c * TR + lane] = run;
+        run += v;
+      }
+  }
+  if (lane == 0 && hit) atomicAdd((unsigned long long *)&stats[4], hit);
+}
+
+template <int TS>
+__global__ void chunk_write_kernel(const int64_t *__restrict__ tptr, const int64_t *__restrict__ choff,
+                                   int64_t n_tiles, const uint64_t *__restrict__ pairs,
+                                   const int32_t *__restrict__ rows, const double *__restrict__ vals,
+                                   const int64_t *__restrict__ cc, double2 *__restrict__ ent) {
+  constexpr int TR = 1 << TS;
+  const int lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
+  const int64_t n_ch = choff[n_tiles];
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < n_ch; c += nw) {
+    const int64_t t = chunk_tile(choff, n_tiles, c);
+    const int64_t p = tptr[t] + 32 * (c - choff[t]) + lane;
+    uint32_t m = 0;
+    int64_t pos = 0;
+    int d = 0;
+    if (p < tptr[t + 1]) {
+      const uint64_t pr = pairs[p];
+      pos = pair_pos(pr);
+      d = pair_fib(pr);
+      const int cn = pair_cnt(pr);
+      for (int e = 0; e < cn; ++e) m |= 1u << (rows[pos + e] & (TR - 1));
+    }
+    const int64_t mybase = lane < TR ? cc[c * TR + lane] : 0;
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      const bool has = (m >> r) & 1u;
+      const unsigned b = __ballot_sync(0xffffffffu, has);
+      const int64_t base = __shfl_sync(0xffffffffu, mybase, r);
+      if (has) {
+        const int e = __popc(m & ((1u << r) - 1u));
+        ent[base + __popc(b & below)] = make_double2(__longlong_as_double((long long)d), vals[pos + e]);
+      }
+    }
+  }
 }
