@@ -475,7 +475,9 @@ class Cluster:
             masses = [r.arls_local(k) for r in self.ranks]
             if self.P > 1:
                 allm = self.comm.all_gather(masses)
-                C = np.array([float(m.item()) for m in allm])
+                # the P rank masses feed the host multinomial (numpy's binomial chain is part
+                # of the reference's random-stream contract): one device-to-host read
+                C = torch().cat([m.reshape(-1)[:1] for m in allm]).cpu().numpy().astype(np.float64)
                 for r in self.ranks:
                     r.C_host[k] = C
 
