@@ -160,10 +160,12 @@ int rcp_sts_cond(const double *d_chain_pinv, const double *d_grams, int N, int i
  * of the padded rank tree, full R x R each, level-major (level l at offset (2^l-1)*R*R);
  * leaf_rank[2^depth] maps tree leaves to ranks (-1 = padding).  Writes owner rank, the
  * rescaled residual and the product of step probabilities; RCP_ST_DEGENERATE on a
- * zero-mass node or a branch into an empty padded subtree. */
+ * zero-mass node or a branch into an empty padded subtree.  d_key: as rcp_sts_walk's
+ * (non-null: the two key words are read from device memory, for graph-replayed rounds). */
 int rcp_sts_rank_walk(const double *d_node_grams, int depth, int P, const int32_t *d_leaf_rank,
                       const double *d_M, const double *d_H, int64_t J, int R, uint64_t key0,
-                      uint64_t key1, const double *d_override, int32_t *d_owner,
+                      uint64_t key1, const uint64_t *d_key, const double *d_override,
+                      int32_t *d_owner,
                       double *d_r_out, double *d_pmp_i, int *d_status, void *stream);
 int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
                   void *stream);

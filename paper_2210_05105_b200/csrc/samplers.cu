@@ -402,12 +402,17 @@ __global__ void sts_rank_walk_kernel(const double *__restrict__ ng, int depth, i
                                      const int32_t *__restrict__ leaf_rank,
                                      const double *__restrict__ M, const double *__restrict__ H,
                                      int64_t J, int R, uint64_t k0, uint64_t k1,
+                                     const uint64_t *__restrict__ dk,
                                      const double *__restrict__ ov, int32_t *__restrict__ owner,
                                      double *__restrict__ rout, double *__restrict__ pmp,
                                      int *status) {
   const int lane = threadIdx.x & 31;
   const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (s >= J) return;
+  if (dk) {   // graph-replayed round: the key lives in device memory
+    k0 = dk[0];
+    k1 = dk[1];
+  }
   double r = ov ? ov[s] : u64_to_unit(philox_word(k0, k1, (uint64_t)s));
   const double tiny = DBL_MIN;
   double prob = 1.0;
@@ -668,14 +673,15 @@ int rcp_sts_cond(const double *d_chain_pinv, const double *d_grams, int N, int i
 
 int rcp_sts_rank_walk(const double *d_node_grams, int depth, int P, const int32_t *d_leaf_rank,
                       const double *d_M, const double *d_H, int64_t J, int R, uint64_t key0,
-                      uint64_t key1, const double *d_override, int32_t *d_owner, double *d_r_out,
-                      double *d_pmp_i, int *d_status, void *stream) {
+                      uint64_t key1, const uint64_t *d_key, const double *d_override,
+                      int32_t *d_owner, double *d_r_out, double *d_pmp_i, int *d_status,
+                      void *stream) {
   if (J < 0 || R < 1 || depth < 0 || P < 1 || !d_leaf_rank || !d_owner || !d_r_out || !d_pmp_i)
     return RCP_ERR_ARG;
   if (J == 0) return RCP_OK;
   if (depth > 0 && (!d_node_grams || !d_M || !d_H)) return RCP_ERR_ARG;
   sts_rank_walk_kernel<<<(unsigned)ceil_div(J * 32, 256), 256, 0, RCP_STREAM(stream)>>>(
-      d_node_grams, depth, P, d_leaf_rank, d_M, d_H, J, R, key0, key1, d_override, d_owner,
+      d_node_grams, depth, P, d_leaf_rank, d_M, d_H, J, R, key0, key1, d_key, d_override, d_owner,
       d_r_out, d_pmp_i, d_status);
   RCP_LAUNCH_CHECK("sts_rank_walk");
   return RCP_OK;

@@ -22,6 +22,7 @@ Schedule of one mode-k solve (ref schedules.py:227-258, als.py:196-208):
 from __future__ import annotations
 
 import math
+import os
 import time
 
 import numpy as np
@@ -203,6 +204,7 @@ class RankState:
         self.stats = t.zeros(8, dtype=t.int64, device=dev)
         self.mt_cap = {}
         self.dkeys = None        # (N, N, 2) stream keys of the round's draws (graph mode)
+        self._rank_order = {}    # mode -> (rank row order, padded leaf ranks) on the device
         self.gperm = None        # (N, N, J) SHUFFLE permutations of the round (graph mode)
         self.block_gram_buf = t.zeros((R, R), **f64)
 
@@ -250,8 +252,13 @@ class RankState:
         for b in blocks[1:]:
             g += b
         self.grams[k].copy_(g)
-        if self.P > 1:
-            self.block_grams[k] = torch().stack([b for b in blocks])
+        if self.P > 1:   # persistent per mode: a graph replay reads the captured addresses
+            bg = self.block_grams[k]
+            if bg is None:
+                bg = self.block_grams[k] = self.t.empty((self.P, self.R, self.R),
+                                                        dtype=self.t.float64, device=self.dev)
+            for p, b in enumerate(blocks):
+                bg[p].copy_(b)
 
     def build_tree(self, k):
         """Mark the local tree of mode k stale (it is rebuilt on its first walk: at P = 1 the
@@ -273,17 +280,25 @@ class RankState:
         P, R = self.P, self.R
         depth = int(math.ceil(math.log2(P))) if P > 1 else 0
         width = 1 << depth
-        order = self.grid.row_order(k)
-        leaf_rank = np.full(width, -1, dtype=np.int32)
-        leaf_rank[:P] = order
-        leaves = t.zeros((width, R, R), dtype=t.float64, device=self.dev)
-        leaves[:P] = self.block_grams[k][t.as_tensor(order, device=self.dev)]
-        levels = [None] * (depth + 1)
-        levels[depth] = leaves
+        idx = self._rank_order.get(k)
+        if idx is None:   # fixed by the grid: uploaded once (no host copies inside a capture)
+            order = self.grid.row_order(k)
+            leaf_rank = np.full(width, -1, dtype=np.int32)
+            leaf_rank[:P] = order
+            idx = self._rank_order[k] = (t.as_tensor(order, device=self.dev),
+                                         t.as_tensor(leaf_rank, device=self.dev))
+        RR = R * R
+        old = self.rank_tree[k]
+        if old is None:   # one buffer per mode, rewritten in place (graph replays reuse it)
+            node_grams = t.zeros(((2 * width - 1) * RR,), dtype=t.float64, device=self.dev)
+        else:
+            node_grams = old[0]
+        level = [node_grams[((1 << l) - 1) * RR:((2 << l) - 1) * RR].view(1 << l, R, R)
+                 for l in range(depth + 1)]
+        level[depth][:P].copy_(self.block_grams[k].index_select(0, idx[0]))   # padding stays 0
         for lev in range(depth - 1, -1, -1):
-            levels[lev] = levels[lev + 1].reshape(-1, 2, R, R).sum(dim=1)
-        node_grams = t.cat([lv.reshape(-1) for lv in levels]).contiguous()
-        self.rank_tree[k] = (node_grams, t.as_tensor(leaf_rank, device=self.dev), depth)
+            t.sum(level[lev + 1].view(-1, 2, R, R), dim=1, out=level[lev])
+        self.rank_tree[k] = (node_grams, idx[1], depth)
 
     def arls_local(self, k):
         """Local leverage distribution of mode k given the replicated Gram (ref
@@ -724,12 +739,20 @@ class Cluster:
     # ------------------------------------------------------------ CUDA-graph rounds
     def graph_ok(self):
         """A round is replayable from a CUDA graph when nothing in it depends on the host
-        between launches: one rank (its per-round host inputs -- the draw keys and, for
-        CP-ARLS-LEV, the SHUFFLE permutations -- move to device memory before the replay)
-        and workspaces sized up front (no bounded-capacity MTTKRP, which checks its entry
-        count on the host)."""
-        return (self.P == 1 and
-                all(st.capacity(self.J) <= CAP_LIMIT for st in self.ranks[0].stores))
+        between launches: its per-round host inputs (the draw keys and, for CP-ARLS-LEV,
+        the SHUFFLE permutations) move to device memory before the replay, and workspaces
+        are sized up front (no bounded-capacity MTTKRP, which checks its entry count on
+        the host).  P > 1: STS-CP rounds only (CP-ARLS-LEV splits J over the rank masses
+        with a host multinomial, ref samplers.py:138-145), with the virtual ranks of one
+        process (LocalComm); SPMD rounds (NCCL collectives inside the capture) only with
+        RCP_GRAPH_SPMD=1."""
+        if not all(st.capacity(self.J) <= CAP_LIMIT for r in self.ranks for st in r.stores):
+            return False
+        if self.P == 1:
+            return True
+        if self.sampler != "sts":
+            return False
+        return isinstance(self.comm, LocalComm) or os.environ.get("RCP_GRAPH_SPMD") == "1"
 
     def round_graph(self, rnd, on_solved=None, join=(), tag="round"):
         """One ALS round replayed from a CUDA graph (captured on the first call, after at
@@ -747,7 +770,8 @@ class Cluster:
         N = self.N
         arls = self.sampler != "sts"
         if r.dkeys is None:
-            r.dkeys = t.zeros((N, N, 2), dtype=t.int64, device=r.dev)
+            for q in self.ranks:   # STS keys are rank-independent; ARLS graphs are P = 1
+                q.dkeys = t.zeros((N, N, 2), dtype=t.int64, device=q.dev)
             self._gkeys = [t.zeros((N, N, 2), dtype=t.int64, pin_memory=True) for _ in range(2)]
             if arls:
                 r.gperm = t.zeros((N, N, self.J), dtype=t.int64, device=r.dev)
@@ -761,7 +785,8 @@ class Cluster:
         self._gready.clear()   # inputs staged for any other round are stale
         if slot is None:
             slot = self._graph_stage(rnd, 0)
-        r.dkeys.copy_(self._gkeys[slot], non_blocking=True)
+        for q in self.ranks:
+            q.dkeys.copy_(self._gkeys[slot], non_blocking=True)
         if arls:
             r.gperm.copy_(self._gperm[slot], non_blocking=True)
         ev = t.cuda.Event()

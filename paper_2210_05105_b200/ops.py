@@ -166,8 +166,9 @@ class Ops:
     def sts_rank_walk(self, node_grams, depth, P, leaf_rank, M, H, J, key, override, owner,
                       r_out, pmp_i):
         R = M.shape[0]
+        k0, k1, dk = _key_args(key)
         self._c("rcp_sts_rank_walk", ptr(node_grams), int(depth), int(P), ptr(leaf_rank),
-                ptr(M), ptr(H), int(J), R, key[0], key[1], ptr(override), ptr(owner),
+                ptr(M), ptr(H), int(J), R, k0, k1, dk, ptr(override), ptr(owner),
                 ptr(r_out), ptr(pmp_i), self.status.ptr, stream_handle())
 
     # ------------------------------------------------------------------ MTTKRP
