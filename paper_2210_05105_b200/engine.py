@@ -170,6 +170,8 @@ class RankState:
         self.block_grams = [None] * N          # (P, R, R) per mode (P > 1)
         self.trees = [None] * N
         self.tree_stale = [True] * N
+        self.tree_ev = [None] * N              # pending side-stream tree build per mode
+        self._tree_stream = None
         self.rank_tree = [None] * N            # (node_grams, leaf_rank, depth) per mode
         self.dist = [None] * N
         self.cdf = [None] * N
@@ -268,7 +270,31 @@ class RankState:
         if self.P > 1:
             self._build_rank_tree(k)
 
+    def prefetch_trees(self, modes):
+        """Build the stale trees of `modes` on a side stream: they depend only on the
+        factors, so they overlap the chain pseudo-inverse, the conditioning and the first
+        constant mode's flat draw; the walk that reads a tree waits for its event."""
+        t = self.t
+        pend = [i for i in modes if self.tree_stale[i] and self.n[i] > 0]
+        if not pend:
+            return
+        main = t.cuda.current_stream()
+        if self._tree_stream is None:
+            self._tree_stream = t.cuda.Stream(device=main.device)
+        s = self._tree_stream
+        s.wait_stream(main)
+        with t.cuda.stream(s):
+            for i in pend:
+                self.trees[i] = self.ops.sts_build(self.U[i], self.leaf_of(i), self.trees[i])
+                self.tree_stale[i] = False
+                ev = t.cuda.Event()
+                ev.record()
+                self.tree_ev[i] = ev
+
     def local_tree(self, k):
+        if self.tree_ev[k] is not None:
+            self.t.cuda.current_stream().wait_event(self.tree_ev[k])
+            self.tree_ev[k] = None
         if self.tree_stale[k] and self.n[k] > 0:
             self.trees[k] = self.ops.sts_build(self.U[k], self.leaf_of(k), self.trees[k])
         self.tree_stale[k] = False
@@ -503,7 +529,11 @@ class Cluster:
             r.X[k].fill_(-1)
             r.pmp[k].fill_(1.0)
         if self.sampler == "sts":
+            walked = [i for i in range(N) if i != k]
+            if self.P == 1 and override is None:
+                walked = walked[1:]   # the first constant mode is a flat draw at P = 1
             for r in self.ranks:
+                r.prefetch_trees(walked)
                 r.chain(k)
             first = True
             for i in range(N):
