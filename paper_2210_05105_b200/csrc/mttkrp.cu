@@ -57,6 +57,12 @@ constexpr int kPrivRows = 49152;   // CTA-private row histogram limit (int32 in 
 #ifndef RCP_SPMM_U
 #define RCP_SPMM_U 4
 #endif
+#ifndef RCP_SPMM_GROUP
+#define RCP_SPMM_GROUP 1   // 0: spmm_packed_kernel (entries broadcast by shuffles)
+#endif
+#ifndef RCP_SPMM_GU
+#define RCP_SPMM_GU 2   // spmm_group_kernel, R in 33..64: batch steps with Hs loads in flight
+#endif
 #ifndef RCP_SPMM_BLOCKS_PER_SM
 #define RCP_SPMM_BLOCKS_PER_SM 8
 #endif
@@ -992,6 +998,138 @@ spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64
   }
 }
 
+// Grouped variant (the product path): the warp's lanes form 4 groups of 8; group g takes
+// the entries e = g (mod 4) of a row and its 8 lanes split each Hs row (column pairs
+// li + 8k, k < NL).  A row's entries are loaded 32 at a time (lane 8g + t holds entry
+// 4t + g of the batch, the next batch prefetched) and one shuffle per word hands each
+// group its own entry, so a shuffle serves 4 entries: the L1's register writeback, which
+// limits spmm_packed_kernel (3 shuffles = 384 B per entry beside the 400-byte Hs row at
+// R = 50), carries ~112 B per entry here.  The 4 groups' partial row sums are combined by
+// a 2-step butterfly when the row (or the chunk's part of it) ends; outputs and the
+// deterministic mode's split-row slots keep spmm_packed_kernel's layout (column pair c2
+// of chunk ch at ch * 32 NP + c2).
+template <int NL, bool DET = false>
+__global__ void __launch_bounds__(256)
+spmm_group_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__restrict__ nnzp,
+                  const double2 *__restrict__ ent, const double *__restrict__ Hs, int R,
+                  double *__restrict__ out, double2 *__restrict__ slotF = nullptr,
+                  double2 *__restrict__ slotL = nullptr) {
+  constexpr int NP = NL <= 4 ? 1 : 2;   // slot stride of the deterministic mode (32 NP pairs)
+  constexpr int U = NL <= 2 ? 4 : (NL <= 4 ? RCP_SPMM_GU : 1);   // batch steps in flight
+  const int lane = threadIdx.x & 31, g = lane >> 3, li = lane & 7;
+  const int R2 = (R + 1) >> 1;
+  const int Rp2 = hs_stride(R) >> 1;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nnz = nnzp[0];
+  const int64_t nchunks = ceil_div(nnz, kSpmmChunk);
+  const double2 *H2 = reinterpret_cast<const double2 *>(Hs);
+  const int mine_off = g + 4 * li;   // this lane's entry within a batch of 32
+  for (int64_t ch = warp0; ch < nchunks; ch += nwarps) {
+    const int64_t c0 = ch * kSpmmChunk;
+    const int64_t c1 = min(c0 + kSpmmChunk, nnz);
+    int64_t row = floor_index(rptr, n_rows + 1, c0);
+    int64_t rs = rptr[row], re = rptr[row + 1];
+    while (true) {
+      const int64_t e0 = max(rs, c0), e1 = min(re, c1);
+      if (e1 > e0) {
+        double2 acc[NL];
+#pragma unroll
+        for (int k = 0; k < NL; ++k) acc[k] = make_double2(0.0, 0.0);
+        double2 nxt = e0 + mine_off < e1 ? ent[e0 + mine_off] : make_double2(0.0, 0.0);
+        for (int64_t base = e0; base < e1; base += 32) {
+          const double2 cur = nxt;
+          if (base + 32 < e1)
+            nxt = base + 32 + mine_off < e1 ? ent[base + 32 + mine_off] : make_double2(0.0, 0.0);
+          const int md = (int)(int32_t)__double_as_longlong(cur.x);
+          const double mv = cur.y;
+          const int nsteps = (int)min((int64_t)8, (e1 - base + 3) >> 2);   // warp-uniform
+          for (int t0 = 0; t0 < nsteps; t0 += U) {
+            int64_t d[U];
+            double v[U];
+            bool ok[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int src = (lane & 24) | (t0 + u);
+              d[u] = __shfl_sync(0xffffffffu, md, src);
+              v[u] = __shfl_sync(0xffffffffu, mv, src);
+              ok[u] = base + g + 4 * (t0 + u) < e1;
+            }
+            double2 h[U][NL];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+              for (int k = 0; k < NL; ++k) {
+                const int c2 = li + 8 * k;
+                h[u][k] = (ok[u] && c2 < R2) ? H2[d[u] * Rp2 + c2] : make_double2(0.0, 0.0);
+              }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+              for (int k = 0; k < NL; ++k) {
+                acc[k].x = fma(v[u], h[u][k].x, acc[k].x);
+                acc[k].y = fma(v[u], h[u][k].y, acc[k].y);
+              }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+          acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, 8);
+          acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, 8);
+          acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, 16);
+          acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, 16);
+        }
+        const bool whole = (rs >= c0) && (re <= c1);
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+          const int c2 = li + 8 * k;
+          if ((k & 3) != g || c2 >= R2) continue;   // the 4 groups share the stores
+          if (whole) {
+            double *o = out + row * R + 2 * c2;
+            o[0] = acc[k].x;
+            if (2 * c2 + 1 < R) o[1] = acc[k].y;
+          } else if (DET) {
+            (rs < c0 ? slotF : slotL)[ch * (32 * NP) + c2] = acc[k];
+          } else {
+            double *o = out + row * R + 2 * c2;
+            atomicAdd(o, acc[k].x);
+            if (2 * c2 + 1 < R) atomicAdd(o + 1, acc[k].y);
+          }
+        }
+      }
+      if (re >= c1) break;
+      ++row;
+      rs = re;
+      re = rptr[row + 1];
+    }
+  }
+}
+
+// Segmented reduction of the packed row-sorted entries (rptr over n_rows, entry count at
+// nnzp on the device); slotF/slotL: the deterministic mode's split-row partials.
+template <bool DET>
+void launch_spmm_packed(unsigned blocks, const int64_t *rptr, int64_t n_rows, const int64_t *nnzp,
+                        const double2 *ent, const double *Hs, int R, double *out, double2 *slotF,
+                        double2 *slotL, cudaStream_t st) {
+#if RCP_SPMM_GROUP
+  switch ((R + 15) / 16) {
+#define RCP_SG(K)                                                                            \
+  case K:                                                                                    \
+    spmm_group_kernel<K, DET><<<blocks, 256, 0, st>>>(rptr, n_rows, nnzp, ent, Hs, R, out,   \
+                                                      slotF, slotL);                         \
+    break;
+    RCP_SG(1) RCP_SG(2) RCP_SG(3) RCP_SG(4) RCP_SG(5) RCP_SG(6) RCP_SG(7)
+    default: RCP_SG(8)
+#undef RCP_SG
+  }
+#else
+  if (R <= 64)
+    spmm_packed_kernel<1, DET><<<blocks, 256, 0, st>>>(rptr, n_rows, nnzp, ent, Hs, R, out, slotF, slotL);
+  else
+    spmm_packed_kernel<2, DET><<<blocks, 256, 0, st>>>(rptr, n_rows, nnzp, ent, Hs, R, out, slotF, slotL);
+#endif
+}
+
 template <typename Acc>
 int launch_spmm(const int64_t *rptr, int64_t n_rows, const int64_t *nnzp, int64_t nnz_host,
                 Acc acc, const double *Hs, int R, double *out, cudaStream_t st) {
@@ -1330,15 +1468,10 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
     double2 *slotL = slotF + (size_t)(cap / kSpmmChunk + 2) * 32 * tile_np;
     const unsigned sb2 = (unsigned)(RCP_SPMM_BLOCKS_PER_SM * sm_count());
     const int64_t *nnzp = eoff + nt_;
-    if (tile_np == 1) {
-      spmm_packed_kernel<1, true><<<sb2, 256, 0, st>>>(rptr, n_rows, nnzp, ent_, Hs, R, d_out, slotF, slotL);
-      RCP_LAUNCH_CHECK("spmm_det");
-      spmm_fix_kernel<1><<<gw, 256, 0, st>>>(rptr, n_rows, slotF, slotL, R, d_out);
-    } else {
-      spmm_packed_kernel<2, true><<<sb2, 256, 0, st>>>(rptr, n_rows, nnzp, ent_, Hs, R, d_out, slotF, slotL);
-      RCP_LAUNCH_CHECK("spmm_det");
-      spmm_fix_kernel<2><<<gw, 256, 0, st>>>(rptr, n_rows, slotF, slotL, R, d_out);
-    }
+    launch_spmm_packed<true>(sb2, rptr, n_rows, nnzp, ent_, Hs, R, d_out, slotF, slotL, st);
+    RCP_LAUNCH_CHECK("spmm_det");
+    if (tile_np == 1) spmm_fix_kernel<1><<<gw, 256, 0, st>>>(rptr, n_rows, slotF, slotL, R, d_out);
+    else spmm_fix_kernel<2><<<gw, 256, 0, st>>>(rptr, n_rows, slotF, slotL, R, d_out);
     RCP_LAUNCH_CHECK("spmm_fix");
     return RCP_OK;
   };
@@ -1512,8 +1645,7 @@ int rcp_sampled_mttkrp(const int64_t *d_keys, const int64_t *d_colptr, int64_t n
   }
   // 6. segmented reduction
   const unsigned sb = (unsigned)(RCP_SPMM_BLOCKS_PER_SM * sm_count());
-  if (R <= 64) spmm_packed_kernel<1><<<sb, 256, 0, st>>>(rptr, n_rows, nnz, ent, Hs, R, d_out);
-  else spmm_packed_kernel<2><<<sb, 256, 0, st>>>(rptr, n_rows, nnz, ent, Hs, R, d_out);
+  launch_spmm_packed<false>(sb, rptr, n_rows, nnz, ent, Hs, R, d_out, nullptr, nullptr, st);
   RCP_LAUNCH_CHECK("spmm_packed");
   return RCP_OK;
 }

@@ -9,7 +9,7 @@ import sys
 
 MTTKRP = ("hash_insert", "rep_flag", "rep_compact", "lookup_kernel", "finalize_counts",
           "item_count", "item_fill", "cta_hist", "cta_prefix", "rows_hit", "cta_scatter",
-          "bucket_offsets", "bucket_scatter", "bucket_rows", "spmm_packed", "row_count",
+          "bucket_offsets", "bucket_scatter", "bucket_rows", "spmm_packed", "spmm_group", "row_count",
           "scatter_kernel", "big_hist", "big_colprefix", "big_offsets", "big_rows",
           "mttkrp_init", "tile_hist", "pair_scatter", "pair_count", "pair_emit", "tile_bounds",
           "tile_entries", "tile_chunks", "chunk_rows", "tile_rowscan", "chunk_write", "spmm_fix",
