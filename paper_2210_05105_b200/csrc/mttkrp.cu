@@ -63,12 +63,15 @@ constexpr int kPrivRows = 49152;   // CTA-private row histogram limit (int32 in 
 #ifndef RCP_SPMM_GU
 #define RCP_SPMM_GU 2   // spmm_group_kernel, R in 33..64: batch steps with Hs loads in flight
 #endif
+#ifndef RCP_SPMM_GU5
+#define RCP_SPMM_GU5 2   // spmm_group_kernel, R > 64
+#endif
 #ifndef RCP_SPMM_BLOCKS_PER_SM
 #define RCP_SPMM_BLOCKS_PER_SM 8
 #endif
 constexpr int kSpmmChunk = RCP_SPMM_CHUNK;   // entries per warp in the segmented reduction
 constexpr int64_t kItemE = 512;    // entries per traversal item (a fiber chunk)
-constexpr int kSpmmU = RCP_SPMM_U;           // Hs-row loads in flight per lane
+[[maybe_unused]] constexpr int kSpmmU = RCP_SPMM_U;           // Hs-row loads in flight per lane
 
 // Row stride of the scaled KRP rows Hs: a multiple of 16 doubles, so every row starts on a
 // 128-byte line and a warp's double2 row load touches ceil(R/16) lines, not one more.
@@ -1008,14 +1011,17 @@ spmm_packed_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64
 // a 2-step butterfly when the row (or the chunk's part of it) ends; outputs and the
 // deterministic mode's split-row slots keep spmm_packed_kernel's layout (column pair c2
 // of chunk ch at ch * 32 NP + c2).
+#ifndef RCP_SPMM_GMIN
+#define RCP_SPMM_GMIN 4   // spmm_group_kernel: minimum resident CTAs per SM (64 registers; swept 1/3/4/5)
+#endif
 template <int NL, bool DET = false>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, NL <= 4 ? RCP_SPMM_GMIN : 2)
 spmm_group_kernel(const int64_t *__restrict__ rptr, int64_t n_rows, const int64_t *__restrict__ nnzp,
                   const double2 *__restrict__ ent, const double *__restrict__ Hs, int R,
                   double *__restrict__ out, double2 *__restrict__ slotF = nullptr,
                   double2 *__restrict__ slotL = nullptr) {
   constexpr int NP = NL <= 4 ? 1 : 2;   // slot stride of the deterministic mode (32 NP pairs)
-  constexpr int U = NL <= 2 ? 4 : (NL <= 4 ? RCP_SPMM_GU : 1);   // batch steps in flight
+  constexpr int U = NL <= 2 ? 4 : (NL <= 4 ? RCP_SPMM_GU : RCP_SPMM_GU5);   // steps in flight
   const int lane = threadIdx.x & 31, g = lane >> 3, li = lane & 7;
   const int R2 = (R + 1) >> 1;
   const int Rp2 = hs_stride(R) >> 1;

@@ -2,7 +2,7 @@
 variants interleaved, each run loading its library through RCP_LIB.  Prints one JSON line
 per run (variant, config, ms_per_step, phases).
 
-usage: python tools/lab/ab_bench.py CONFIG REPEATS name=path.so [name=path.so ...]
+usage: [AB_ARGS='--rank 75'] python tools/lab/ab_bench.py CONFIG REPEATS name=path.so [...]
 """
 import json
 import os
@@ -16,7 +16,8 @@ for r in range(reps):
     for name, so in variants:
         env = dict(os.environ, RCP_LIB=os.path.abspath(so))
         out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg,
-                              "--steps", "10", "--warmup", "3", "--no-cpu-baseline"],
+                              "--steps", "10", "--warmup", "3", "--no-cpu-baseline"]
+                             + os.environ.get("AB_ARGS", "").split(),
                              capture_output=True, text=True, env=env, cwd=ROOT)
         line = [x for x in out.stdout.splitlines() if x.startswith("{")]
         if not line:
