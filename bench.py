@@ -162,12 +162,21 @@ def run_ours(args):
     # RCP_SPMD=1 runs the torch.distributed (NCCL) code path even at world size 1 (a check
     # of the multi-GPU plumbing on a single GPU)
     spmd = world > 1 or os.environ.get("RCP_SPMD") == "1"
+    # RCP_BENCH_BACKEND=gloo with RCP_BENCH_ONE_GPU=1: a functional check of the multi-rank
+    # flow on a one-GPU box (every rank on cuda:0, collectives staged through the host; no
+    # kernel waits on another process).  Its timings are not bench values.
+    backend = os.environ.get("RCP_BENCH_BACKEND", "nccl")
+    if os.environ.get("RCP_BENCH_ONE_GPU") == "1":
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     _lib.load()
     if spmd:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     t_setup = time.perf_counter()
     balance = args.balance if args.balance != "auto" else ("nnz" if world > 1 else "rows")
     rank_grid = None
@@ -332,7 +341,9 @@ def run_ours(args):
                    "(outside the round events); stores %.1f GB > L2" % (
                        sum(s.bytes() for s in me.stores) / 1e9),
                    "setup_s": round(setup_s, 1), "generate_s": round(t_gen, 1),
-                   "launch": "cuda-graph replay of the round" if use_graph else "eager"},
+                   "launch": "cuda-graph replay of the round" if use_graph else "eager",
+                   **({"functional_check": "backend %s, every rank on cuda:0: not a bench value" % backend}
+                      if backend != "nccl" else {})},
         "rounds_per_s": K / t_total,
         "distinct_nnz_per_s": nnz_d / t_total,
         "sampled_nnz_per_round": nnz_m / K,

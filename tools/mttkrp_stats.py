@@ -85,6 +85,31 @@ def hook(k):
                         "density": float(cum_e[t_] * nnz_d / (T * cum_p[t_]))})
         ranked[str(T)] = pts
     d["ranked_tiles"] = ranked
+    # a dense head block: the nh most-hit rows x every sampled fiber
+    srt = torch.sort(rh, descending=True).values.double()
+    cs = torch.cumsum(srt, 0)
+    d["dense_head"] = [{"rows": nh, "entry_frac": float(cs[min(nh, cs.numel()) - 1]) / max(nnz_d, 1),
+                        "density": float(cs[min(nh, cs.numel()) - 1]) / (nh * max(int(hit.sum()), 1))}
+                       for nh in (128, 256, 512, 1024, 2048, 4096)]
+    # 2-D dense block: the nh most-hit rows (ranked by the STORE's row counts, a static
+    # choice) x the nf longest sampled fibers
+    srh = torch.bincount(st.rows.long(), minlength=st.n_rows)
+    sorder = torch.argsort(srh, descending=True)
+    srank = torch.empty_like(sorder)
+    srank[sorder] = torch.arange(sorder.numel(), device=dev)
+    er = srank[rows]
+    forder = torch.argsort(ln, descending=True)
+    frank = torch.empty_like(forder)
+    frank[forder] = torch.arange(forder.numel(), device=dev)
+    ef = frank[fid]
+    blk = []
+    for nh in (256, 512, 1024, 2048, 4096, 8192):
+        for nf in (1024, 2048, 4096, 8192, 1 << 30):
+            inb = int(((er < nh) & (ef < nf)).sum())
+            nfe = min(nf, int(hit.sum()))
+            blk.append({"rows": nh, "fibers": nfe, "entry_frac": inb / max(nnz_d, 1),
+                        "density": inb / (min(nh, st.n_rows) * max(nfe, 1))})
+    d["dense_block_static_rows"] = blk
     res.append(d)
     return orig(k)
 
