@@ -333,7 +333,7 @@ def run_ours(args):
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": sum(step_ms) / K, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "%s %s R=%d J=%d dims=%s nnz=%d" % (args.config, args.sampler, R, J,
                                                                  "x".join(map(str, dims)), nnz),
                    "sampler": args.sampler, "rank": R, "samples_J": J, "modes": N,
@@ -622,7 +622,7 @@ def run_reference(args):
     hi = host_info()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": total_t / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "%s %s R=%d J=%d dims=%s nnz=%d" % (
                            args.config, args.sampler, R, J, "x".join(map(str, dims)), len(vals)),

@@ -167,6 +167,42 @@ int rcp_sts_rank_walk(const double *d_node_grams, int depth, int P, const int32_
                       uint64_t key1, const uint64_t *d_key, const double *d_override,
                       int32_t *d_owner,
                       double *d_r_out, double *d_pmp_i, int *d_status, void *stream);
+/* The rank tree in the local trees' packed layout (complete tree over 2^ceil(log2 P) leaves;
+ * leaf v = packed upper triangle of block Gram d_order[v] (d_order NULL: v), zero padding;
+ * inner nodes = sums of their children, ref samplers.py:239-275), and the rank-level walk
+ * over it grouped by the key of the modes already sampled, like rcp_sts_walk: node masses
+ * are evaluated once per distinct (H row, node) instead of once per sample.  Outputs per
+ * sample: owner rank (-1 for a degenerate run), rescaled residual, product of the step
+ * probabilities.  d_leaf_rank[2^depth] maps tree leaves to ranks (-1 = padding). */
+size_t rcp_sts_rank_tree_doubles(int P, int R);
+int rcp_sts_rank_tree(const double *d_block_grams, const int64_t *d_order, int P, int R,
+                      double *d_tree, void *stream);
+size_t rcp_sts_rank_walk_ws_bytes(int64_t J, int P, int R);
+int rcp_sts_rank_walk_grouped(const double *d_rank_tree, int P, const int32_t *d_leaf_rank,
+                              int R, const double *d_M, const double *d_H_in,
+                              const int64_t *d_hkey, int key_bits, int64_t J, uint64_t key0,
+                              uint64_t key1, const uint64_t *d_key, const double *d_override,
+                              int32_t *d_owner, double *d_r_out, double *d_pmp_i, void *d_ws,
+                              size_t ws_bytes, int *d_status, void *stream);
+/* Local search of the first constant mode at P > 1 (all samples share H = ones): samples
+ * with d_sel[s] == sel_value invert the CDF of this rank's row masses (rcp_arls_build of
+ * the block with the conditioning matrix) at their residual d_rin[s]
+ * (ref _leaf_search_batch samplers.py:313-345): d_Xi[s] = row, d_pmp_i[s] *= dist[row],
+ * d_resid[s] (nullable) = the residual inside the row's segment.  RCP_ST_DEGENERATE when
+ * a sample is routed to a rank without mass. */
+int rcp_sts_flat_local(const double *d_cdf, const double *d_dist, int64_t n, int64_t row_lo,
+                       const double *d_total_mass, const double *d_rin, const int32_t *d_sel,
+                       int32_t sel_value, int64_t J, int64_t *d_Xi, double *d_pmp_i,
+                       double *d_resid, int *d_status, void *stream);
+/* STS exchange buffers (ref schedules.py:239-247; J x (R + 3) doubles per rank, summed by
+ * one all-reduce): pack = [row, step probability, residual, factor row] of the samples
+ * this rank owns and zeros elsewhere; unpack = every sample's row, probability and
+ * residual, and H[s,:] = row (init) or H[s,:] (.) row. */
+int rcp_exchange_pack(const int64_t *d_Xi, const double *d_pmp_i, const double *d_resid,
+                      const double *d_U, int64_t n, int64_t row_lo, const int32_t *d_owner,
+                      int32_t rank, int64_t J, int R, double *d_buf, void *stream);
+int rcp_exchange_unpack(const double *d_buf, int64_t J, int R, int init, int64_t *d_Xi,
+                        double *d_pmp_i, double *d_resid, double *d_H, void *stream);
 int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
                   void *stream);
 /* Walk J samples down the tree of one factor block (rows global [row_lo, row_lo+n)).

@@ -56,6 +56,15 @@ _SIGS = {
     "rcp_sts_cond": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "rcp_sts_rank_walk": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _i64, _i32, _u64, _u64, _vp,
                                  _vp, _vp, _vp, _vp, _vp, _vp]),
+    "rcp_sts_rank_tree_doubles": (_sz, [_i32, _i32]),
+    "rcp_sts_rank_tree": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp]),
+    "rcp_sts_rank_walk_ws_bytes": (_sz, [_i64, _i32, _i32]),
+    "rcp_sts_rank_walk_grouped": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _i64, _u64,
+                                         _u64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
+    "rcp_sts_flat_local": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp,
+                                  _vp, _vp]),
+    "rcp_exchange_pack": (_i32, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _i32, _i64, _i32, _vp, _vp]),
+    "rcp_exchange_unpack": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "rcp_sts_build": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp]),
     "rcp_sts_walk_ws_bytes": (_sz, [_i64, _i64, _i32, _i32]),
     "rcp_sts_walk": (_i32, [_vp, _vp, _i64, _i32, _i32, _i64, _vp, _vp, _vp, _i32, _i64, _u64, _u64,

@@ -456,6 +456,115 @@ __global__ void sts_rank_walk_kernel(const double *__restrict__ ng, int depth, i
   }
 }
 
+// Packed rank tree (ref samplers.py:239-275): leaf v of a complete tree over `width` leaves
+// holds the packed upper triangle of block Gram order[v] (zero padding past P), every inner
+// node the sum of its two children; the node layout is the local trees' (level order,
+// stride tri_stride(R)), so the run-grouped walk reads it unchanged.
+__global__ void sts_rank_tree_kernel(const double *__restrict__ blocks,
+                                     const int64_t *__restrict__ order, int P, int R, int depth,
+                                     double *__restrict__ tree) {
+  const int Rt = R * (R + 1) / 2, Rs = tri_stride(R);
+  const int64_t width = 1LL << depth;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < Rs; e += gridDim.x * blockDim.x) {
+    int a = 0, rem = e;
+    if (e < Rt)
+      while (rem >= R - a) {
+        rem -= R - a;
+        ++a;
+      }
+    const int b = a + rem;
+    double *leafs = tree + (width - 1) * (int64_t)Rs;
+    for (int64_t v = 0; v < width; ++v) {
+      double g = 0.0;
+      if (e < Rt && v < P) {
+        const int64_t src = order ? order[v] : v;
+        g = blocks[(src * R + a) * R + b];
+      }
+      leafs[v * Rs + e] = g;
+    }
+    for (int lev = depth - 1; lev >= 0; --lev) {
+      double *up = tree + ((1LL << lev) - 1) * (int64_t)Rs;
+      const double *dn = tree + ((1LL << (lev + 1)) - 1) * (int64_t)Rs;
+      for (int64_t v = 0; v < (1LL << lev); ++v)
+        up[v * Rs + e] = dn[(2 * v) * Rs + e] + dn[(2 * v + 1) * Rs + e];
+    }
+  }
+}
+
+// Local search of the first constant mode at P > 1 (every sample shares H = ones): the
+// samples routed to this rank invert the CDF of its rows' masses with their residual
+// (ref _leaf_search_batch samplers.py:313-345), multiplying the path probability.
+__global__ void sts_flat_local_kernel(const double *__restrict__ cdf,
+                                      const double *__restrict__ dist, int64_t n, int64_t row_lo,
+                                      const double *__restrict__ tmass,
+                                      const double *__restrict__ rin,
+                                      const int32_t *__restrict__ sel, int32_t selv, int64_t J,
+                                      int64_t *__restrict__ Xi, double *__restrict__ pmp,
+                                      double *__restrict__ resid, int *status) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= J || sel[s] != selv) return;
+  if (n < 1 || !(tmass[0] > 0.0)) {   // routed to a rank without mass
+    raise_status(status, RCP_ST_DEGENERATE);
+    Xi[s] = -1;
+    return;
+  }
+  const double u = rin[s];
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (cdf[mid] <= u) lo = mid + 1; else hi = mid;
+  }
+  if (lo > n - 1) lo = n - 1;
+  const double p = dist[lo];
+  Xi[s] = row_lo + lo;
+  pmp[s] *= p;
+  if (resid) {
+    const double below = lo > 0 ? cdf[lo - 1] : 0.0;
+    double ro = p > 0.0 ? (u - below) / p : 0.0;
+    resid[s] = fmin(fmax(ro, 0.0), one_below());
+  }
+}
+
+// STS exchange (ref schedules.py:239-247): a rank's contribution to the J x (R + 3) sum
+// all-reduce -- row, step probability, residual and factor row of the samples it owns,
+// zeros elsewhere -- and, after the reduction, the fold of every sample's row into the
+// running Hadamard rows.  One warp per sample.
+__global__ void exchange_pack_kernel(const int64_t *__restrict__ Xi, const double *__restrict__ pmp,
+                                     const double *__restrict__ resid,
+                                     const double *__restrict__ U, int64_t n, int64_t row_lo,
+                                     const int32_t *__restrict__ owner, int32_t rank, int64_t J,
+                                     int R, double *__restrict__ buf) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (s >= J) return;
+  double *dst = buf + s * (int64_t)(R + 3);
+  const int64_t row = Xi[s] - row_lo;
+  const bool mine = owner[s] == rank && row >= 0 && row < n;
+  if (lane == 0) {
+    dst[0] = mine ? (double)Xi[s] : 0.0;
+    dst[1] = mine ? pmp[s] : 0.0;
+    dst[2] = mine ? resid[s] : 0.0;
+  }
+  const double *src = U + (mine ? row : 0) * R;
+  for (int c = lane; c < R; c += 32) dst[3 + c] = mine ? src[c] : 0.0;
+}
+
+__global__ void exchange_unpack_kernel(const double *__restrict__ buf, int64_t J, int R, int init,
+                                       int64_t *__restrict__ Xi, double *__restrict__ pmp,
+                                       double *__restrict__ resid, double *__restrict__ H) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (s >= J) return;
+  const double *src = buf + s * (int64_t)(R + 3);
+  if (lane == 0) {
+    Xi[s] = (int64_t)src[0];
+    pmp[s] = src[1];
+    resid[s] = src[2];
+  }
+  double *h = H + s * (int64_t)R;
+  for (int c = lane; c < R; c += 32) h[c] = init ? src[3 + c] : h[c] * src[3 + c];
+}
+
 }  // namespace
 
 extern "C" {
@@ -668,6 +777,58 @@ int rcp_sts_cond(const double *d_chain_pinv, const double *d_grams, int N, int i
   sts_cond_kernel<<<(unsigned)ceil_div(R * R, 256), 256, 0, RCP_STREAM(stream)>>>(
       d_chain_pinv, d_grams, N, i, k, R, d_M);
   RCP_LAUNCH_CHECK("sts_cond");
+  return RCP_OK;
+}
+
+size_t rcp_sts_rank_tree_doubles(int P, int R) {
+  if (P < 1 || R < 1) return 0;
+  return (size_t)((2LL << rcp_sts_depth(P, 1)) - 1) * (size_t)tri_stride(R);
+}
+
+int rcp_sts_rank_tree(const double *d_block_grams, const int64_t *d_order, int P, int R,
+                      double *d_tree, void *stream) {
+  if (P < 1 || R < 1 || R > RCP_MAX_RANK || !d_block_grams || !d_tree) return RCP_ERR_ARG;
+  const int depth = rcp_sts_depth(P, 1);
+  sts_rank_tree_kernel<<<(unsigned)ceil_div(tri_stride(R), 128), 128, 0, RCP_STREAM(stream)>>>(
+      d_block_grams, d_order, P, R, depth, d_tree);
+  RCP_LAUNCH_CHECK("sts_rank_tree");
+  return RCP_OK;
+}
+
+int rcp_sts_flat_local(const double *d_cdf, const double *d_dist, int64_t n, int64_t row_lo,
+                       const double *d_total_mass, const double *d_rin, const int32_t *d_sel,
+                       int32_t sel_value, int64_t J, int64_t *d_Xi, double *d_pmp_i,
+                       double *d_resid, int *d_status, void *stream) {
+  if (J < 0 || n < 0 || !d_total_mass || !d_rin || !d_sel || !d_Xi || !d_pmp_i) return RCP_ERR_ARG;
+  if (n > 0 && (!d_cdf || !d_dist)) return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  sts_flat_local_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, RCP_STREAM(stream)>>>(
+      d_cdf, d_dist, n, row_lo, d_total_mass, d_rin, d_sel, sel_value, J, d_Xi, d_pmp_i, d_resid,
+      d_status);
+  RCP_LAUNCH_CHECK("sts_flat_local");
+  return RCP_OK;
+}
+
+int rcp_exchange_pack(const int64_t *d_Xi, const double *d_pmp_i, const double *d_resid,
+                      const double *d_U, int64_t n, int64_t row_lo, const int32_t *d_owner,
+                      int32_t rank, int64_t J, int R, double *d_buf, void *stream) {
+  if (J < 0 || R < 1 || n < 0) return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  if (!d_Xi || !d_pmp_i || !d_resid || !d_owner || !d_buf || (n > 0 && !d_U)) return RCP_ERR_ARG;
+  exchange_pack_kernel<<<(unsigned)ceil_div(J * 32, 256), 256, 0, RCP_STREAM(stream)>>>(
+      d_Xi, d_pmp_i, d_resid, d_U, n, row_lo, d_owner, rank, J, R, d_buf);
+  RCP_LAUNCH_CHECK("exchange_pack");
+  return RCP_OK;
+}
+
+int rcp_exchange_unpack(const double *d_buf, int64_t J, int R, int init, int64_t *d_Xi,
+                        double *d_pmp_i, double *d_resid, double *d_H, void *stream) {
+  if (J < 0 || R < 1) return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  if (!d_buf || !d_Xi || !d_pmp_i || !d_resid || !d_H) return RCP_ERR_ARG;
+  exchange_unpack_kernel<<<(unsigned)ceil_div(J * 32, 256), 256, 0, RCP_STREAM(stream)>>>(
+      d_buf, J, R, init, d_Xi, d_pmp_i, d_resid, d_H);
+  RCP_LAUNCH_CHECK("exchange_unpack");
   return RCP_OK;
 }
 

@@ -354,8 +354,12 @@ __device__ __forceinline__ void publish_children(Run *runs, int *gen_cnt, int64_
 // it in the solve reads unset memory; the status flag is raised for the host.
 __device__ __forceinline__ void fail_run(int32_t lo, int32_t hi, const int32_t *__restrict__ idx,
                                          int64_t *__restrict__ Xi, double *__restrict__ Hout,
-                                         int R, int *status, int *ctl, int lane) {
-  for (int32_t s = lo + lane; s < hi; s += 32) Xi[idx[s]] = -1;
+                                         int R, int *status, int *ctl, int lane,
+                                         int32_t *__restrict__ owner = nullptr) {
+  for (int32_t s = lo + lane; s < hi; s += 32) {
+    if (Xi) Xi[idx[s]] = -1;
+    if (owner) owner[idx[s]] = -1;   // rank mode: no rank finishes these samples
+  }
   if (Hout)
     for (int32_t s = lo; s < hi; ++s) {
       double *dst = Hout + (int64_t)idx[s] * R;
@@ -378,7 +382,8 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
                  int32_t *__restrict__ iB, Run *runs,
                  int *ctl, int64_t cap_runs, int64_t *__restrict__ Xi, double *__restrict__ pmp,
                  double *__restrict__ resid, double *__restrict__ Hout, int *status,
-                 unsigned long long *prof) {
+                 unsigned long long *prof, const int32_t *__restrict__ leaf_rank,
+                 int32_t *__restrict__ owner) {
   extern __shared__ double sh[];
   const int Rs = tri_stride(R);                    // even node stride (zero pad)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -509,7 +514,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
 #endif
         const double qnode = known ? run.qv : warp_sum(qV + qV2);
         if (!(qnode > 0.0)) {
-          fail_run(lo, hi, is, Xi, Hout, R, status, ctl, lane);
+          fail_run(lo, hi, is, Xi, Hout, R, status, ctl, lane, owner);
           continue;
         }
         double T = (qL > 0.0 ? qL : 0.0) / qnode;
@@ -565,6 +570,23 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
 #endif
         continue;
       }
+      if (leaf_rank) {
+        // ---- rank mode (the tree's leaves are ranks, ref samplers.py:423-451): every
+        // sample of the run is finished by the rank owning the leaf; its residual and the
+        // probability of its path go on to that rank's local search
+        const int32_t p = leaf_rank[run.node];
+        if (p < 0) {   // "walk branched into an empty padded subtree"
+          fail_run(lo, hi, is, Xi, Hout, R, status, ctl, lane, owner);
+          continue;
+        }
+        for (int32_t s = lo + lane; s < hi; s += 32) {
+          const int32_t o = is[s];
+          owner[o] = p;
+          resid[o] = rs[s];
+          pmp[o] = run.prob;
+        }
+        continue;
+      }
       // ---- leaf block: masses z^T M' z of its rows z = u (.) h, then each sample's
       // inverse CDF
       const int64_t r0 = (int64_t)run.node * leaf;
@@ -604,7 +626,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         bad = !(total_m > 0.0);
       }
       if (bad) {
-        fail_run(lo, hi, is, Xi, Hout, R, status, ctl, lane);
+        fail_run(lo, hi, is, Xi, Hout, R, status, ctl, lane, owner);
         continue;
       }
       // blocks of kLeafChunk samples: lanes pick rows, then (optionally) the warp writes the
@@ -700,20 +722,32 @@ size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf, int R) {
   return w.total;
 }
 
-int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
-                 int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
-                 int key_bits, int64_t J, uint64_t key0, uint64_t key1, const uint64_t *d_key,
-                 const double *d_override,
-                 const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
-                 double *d_pmp_i, double *d_resid, double *d_H_out, void *d_ws, size_t ws_bytes,
-                 int *d_status,
-                 void *stream) {
+}  // extern "C"
+
+namespace {
+
+// The run-grouped walk.  d_leaf_rank != nullptr selects the rank mode: the tree's leaves are
+// ranks (leaf = 1, n = P, no factor rows); every sample gets its owner, its residual and the
+// probability of its path instead of a row.
+int walk_impl(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
+              int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
+              int key_bits, int64_t J, uint64_t key0, uint64_t key1, const uint64_t *d_key,
+              const double *d_override,
+              const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
+              double *d_pmp_i, double *d_resid, double *d_H_out, void *d_ws, size_t ws_bytes,
+              int *d_status, const int32_t *d_leaf_rank, int32_t *d_owner,
+              void *stream) {
   if (R < 1 || R > RCP_MAX_RANK || leaf < 1 || leaf > kMaxLeaf || J < 0 || n < 0 ||
       J >= (1LL << 31) || key_bits < 1)
     return RCP_ERR_ARG;
   if (key_bits > 64 || !d_hkey) key_bits = 64;
   if (J == 0) return RCP_OK;
-  if (n == 0 || !d_tree || !d_U || !d_M || !d_Xi || !d_pmp_i || !d_ws) return RCP_ERR_ARG;
+  if (n == 0 || !d_tree || !d_M || !d_pmp_i || !d_ws) return RCP_ERR_ARG;
+  if (d_leaf_rank) {
+    if (!d_owner || !d_resid || leaf != 1) return RCP_ERR_ARG;
+  } else if (!d_U || !d_Xi) {
+    return RCP_ERR_ARG;
+  }
   if (d_H_out && d_H_out == d_H_in) return RCP_ERR_ARG;   // groups read a shared row of H_in
   const int depth = rcp_sts_depth(n, leaf);
   if (depth > kMaxDepth) return RCP_ERR_ARG;
@@ -786,11 +820,49 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
                   (void *)&a_H, (void *)&a_rA, (void *)&a_rB, (void *)&a_iA, (void *)&a_iB,
                   (void *)&runs, (void *)&ctl,
                   (void *)&a_cap, (void *)&d_Xi, (void *)&d_pmp_i, (void *)&d_resid, (void *)&d_H_out,
-                  (void *)&d_status, (void *)&a_prof};
+                  (void *)&d_status, (void *)&a_prof, (void *)&d_leaf_rank, (void *)&d_owner};
   RCP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)walk_runs_kernel, dim3(grid),
                                            dim3(warps * 32), args, smem, st));
   RCP_LAUNCH_CHECK("walk_runs");
   return RCP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
+                 int64_t row_lo, const double *d_M, const double *d_H_in, const int64_t *d_hkey,
+                 int key_bits, int64_t J, uint64_t key0, uint64_t key1, const uint64_t *d_key,
+                 const double *d_override,
+                 const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
+                 double *d_pmp_i, double *d_resid, double *d_H_out, void *d_ws, size_t ws_bytes,
+                 int *d_status,
+                 void *stream) {
+  return walk_impl(d_tree, d_U, n, R, leaf, row_lo, d_M, d_H_in, d_hkey, key_bits, J, key0, key1,
+                   d_key, d_override, d_rin, d_sel, sel_value, d_Xi, d_pmp_i, d_resid, d_H_out, d_ws,
+                   ws_bytes, d_status, nullptr, nullptr, stream);
+}
+
+size_t rcp_sts_rank_walk_ws_bytes(int64_t J, int P, int R) {
+  if (R < 1 || R > RCP_MAX_RANK || P < 1) return 0;
+  WalkWs w(J > 0 ? J : 1, rcp_sts_depth(P, 1), R);
+  return w.total;
+}
+
+// Rank-level walk of every sample over the packed rank tree (rcp_sts_rank_tree), grouped
+// by the key of the modes already sampled like the local walk (ref samplers.py:423-451):
+// owner, residual and path probability per sample.
+int rcp_sts_rank_walk_grouped(const double *d_rank_tree, int P, const int32_t *d_leaf_rank,
+                              int R, const double *d_M, const double *d_H_in,
+                              const int64_t *d_hkey, int key_bits, int64_t J, uint64_t key0,
+                              uint64_t key1, const uint64_t *d_key, const double *d_override,
+                              int32_t *d_owner, double *d_r_out, double *d_pmp_i, void *d_ws,
+                              size_t ws_bytes, int *d_status, void *stream) {
+  if (P < 1 || !d_leaf_rank || !d_owner || !d_r_out) return RCP_ERR_ARG;
+  return walk_impl(d_rank_tree, nullptr, P, R, 1, 0, d_M, d_H_in, d_hkey, key_bits, J, key0, key1,
+                   d_key, d_override, nullptr, nullptr, 0, nullptr, d_pmp_i, d_r_out, nullptr, d_ws,
+                   ws_bytes, d_status, d_leaf_rank, d_owner, stream);
 }
 
 int rcp_fold_rows(double *d_out, const double *d_U, int64_t n, int R, int64_t row_lo,

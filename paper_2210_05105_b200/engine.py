@@ -185,7 +185,6 @@ class RankState:
         self.resid = t.zeros(J, **f64)
         self.H = t.ones((J, R), **f64)
         self.H_alt = t.zeros((J, R), **f64)      # walk output buffer (swapped with H)
-        self.urow = t.zeros((J, R), **f64)
         self.owner = t.zeros(J, dtype=t.int32, device=dev)
         self.rtop = t.zeros(J, **f64)
         self.rows_tmp = t.zeros(J, dtype=t.int64, device=dev)
@@ -311,20 +310,12 @@ class RankState:
             order = self.grid.row_order(k)
             leaf_rank = np.full(width, -1, dtype=np.int32)
             leaf_rank[:P] = order
-            idx = self._rank_order[k] = (t.as_tensor(order, device=self.dev),
-                                         t.as_tensor(leaf_rank, device=self.dev))
-        RR = R * R
-        old = self.rank_tree[k]
-        if old is None:   # one buffer per mode, rewritten in place (graph replays reuse it)
-            node_grams = t.zeros(((2 * width - 1) * RR,), dtype=t.float64, device=self.dev)
-        else:
-            node_grams = old[0]
-        level = [node_grams[((1 << l) - 1) * RR:((2 << l) - 1) * RR].view(1 << l, R, R)
-                 for l in range(depth + 1)]
-        level[depth][:P].copy_(self.block_grams[k].index_select(0, idx[0]))   # padding stays 0
-        for lev in range(depth - 1, -1, -1):
-            t.sum(level[lev + 1].view(-1, 2, R, R), dim=1, out=level[lev])
-        self.rank_tree[k] = (node_grams, idx[1], depth)
+            idx = self._rank_order[k] = (
+                t.as_tensor(np.asarray(order, dtype=np.int64), device=self.dev),
+                t.as_tensor(leaf_rank, device=self.dev))
+        old = self.rank_tree[k]   # one buffer per mode, rewritten in place (graph replays)
+        tree = self.ops.sts_rank_tree(self.block_grams[k], idx[0], old[0] if old else None)
+        self.rank_tree[k] = (tree, idx[1], depth)
 
     def arls_local(self, k):
         """Local leverage distribution of mode k given the replicated Gram (ref
@@ -355,28 +346,40 @@ class RankState:
         else:
             key = rng.stream_key(self.seed, rng.WALK_UNIFORM, rnd, k, i)
         H_in = None if first else self.H
+        hk, kb = ops.walk_key(self.X, self.dims, k, i, self.hkey)
         if self.P > 1:
-            node_grams, leaf_rank, depth = self.rank_tree[i]
-            ops.sts_rank_walk(node_grams, depth, self.P, leaf_rank, self.M, self.H if not first else self._ones_H(),
-                              self.J, key, override, self.owner, self.rtop, self.pmp[i])
+            # the rank-level levels, replicated: every rank learns every sample's owner
+            rtree, leaf_rank, _ = self.rank_tree[i]
+            ops.sts_rank_walk_grouped(rtree, self.P, leaf_rank, self.M, H_in, self.J, key, override,
+                                      self.owner, self.rtop, self.pmp[i], hkey=hk, key_bits=kb)
             sel, rin = self.owner, self.rtop
         else:   # the walk / flat draw sets every sample's probability (no rank-level factor)
             sel, rin = None, None
-        if self.P == 1 and first and override is None and self.n[i] > 0:
-            # every sample shares H = ones: one inverse CDF over all rows' masses u M u^T
+        if first and (self.P > 1 or (override is None and self.n[i] > 0)):
+            # every sample shares H = ones: one inverse CDF over the local rows' masses
+            # u M u^T -- all J draws at P = 1, the residuals of the samples routed to this
+            # rank at P > 1 (ref _leaf_search_batch samplers.py:313-345)
             t = self.t
             n = self.n[i]
             if self.flat_dist is None or self.flat_dist.shape[0] < n:
                 self.flat_dist = t.zeros(max(self.n), dtype=t.float64, device=self.dev)
                 self.flat_cdf = t.zeros(max(self.n), dtype=t.float64, device=self.dev)
                 self.flat_mass = t.zeros(1, dtype=t.float64, device=self.dev)
-            ops.arls_build(self.U[i], self.M, self.flat_dist[:n], self.flat_cdf[:n], self.flat_mass)
+            if n > 0:
+                ops.arls_build(self.U[i], self.M, self.flat_dist[:n], self.flat_cdf[:n],
+                               self.flat_mass)
+            else:
+                self.flat_mass.zero_()
+            if self.P > 1:
+                ops.sts_flat_local(self.flat_cdf[:n], self.flat_dist[:n], self.lo[i],
+                                   self.flat_mass, rin, sel, self.rank, self.J, self.X[i],
+                                   self.pmp[i], self.resid)
+                return
             ops.sts_flat_draw(self.flat_cdf[:n], self.flat_dist[:n], self.lo[i], self.flat_mass,
                               key, self.J, self.X[i], self.pmp[i])
             ops.fold_rows(self.H, self.U[i], self.lo[i], self.X[i], init=True)
             return
         if self.n[i] > 0:
-            hk, kb = ops.walk_key(self.X, self.dims, k, i, self.hkey)
             fused = self.P == 1   # the walk folds U rows into the Hadamard rows itself
             ops.sts_walk(self.local_tree(i), self.U[i], self.leaf_of(i), self.lo[i], self.M, H_in,
                          self.J, key, override if self.P == 1 else None, rin, sel, self.rank,
@@ -384,17 +387,11 @@ class RankState:
                          H_out=self.H_alt if fused else None)
             if fused:
                 self.H, self.H_alt = self.H_alt, self.H
-            else:               # this rank's finished rows, exchanged afterwards
-                ops.fold_rows(self.urow, self.U[i], self.lo[i], self.X[i], init=True,
-                              sel=self.owner, sel_value=self.rank)
 
     def _ones_H(self):
         if not hasattr(self, "_H1"):
             self._H1 = self.t.ones((self.J, self.R), dtype=self.t.float64, device=self.dev)
         return self._H1
-
-    def fold_urow(self, first):
-        self.ops.hadamard_rows(self.H, self.urow, init=first)
 
     def arls_draw(self, i, k, rnd, quota, W):
         """This rank's quota of draws for constant mode i (ref samplers.py:169-181);
@@ -545,9 +542,7 @@ class Cluster:
                 for r in self.ranks:
                     r.sts_mode(i, k, rnd, first, override=ov)
                 if self.P > 1:
-                    self._exchange_walk(i)
-                    for r in self.ranks:
-                        r.fold_urow(first)
+                    self._exchange_walk(i, first)
                 first = False
         else:
             first = True
@@ -596,7 +591,7 @@ class Cluster:
         gen = rng.stream(self.seed, rng.MULTINOMIAL, rnd, k, i)
         return gen.multinomial(self.J, C / W), W
 
-    def _exchange_walk(self, i):
+    def _exchange_walk(self, i, first):
         """After the local walks, every rank holds the finished samples it owns; move
         (row, step probability, residual, factor row) of every sample to all ranks
         (ref schedules.py:239-247: R+2 words per sample per constant mode, plus the
@@ -611,19 +606,11 @@ class Cluster:
             buf = getattr(r, "xbuf", None)
             if buf is None or buf.shape != (r.J, r.R + 3):
                 buf = r.xbuf = t.empty((r.J, r.R + 3), dtype=t.float64, device=r.dev)
-            others = (r.owner != r.rank).unsqueeze(1)
-            buf[:, 0] = r.X[i].to(t.float64)
-            buf[:, 1] = r.pmp[i]
-            buf[:, 2] = r.resid
-            buf[:, 3:] = r.urow
-            buf.masked_fill_(others, 0.0)
+            r.ops.exchange_pack(r.X[i], r.pmp[i], r.resid, r.U[i], r.lo[i], r.owner, r.rank, buf)
             bufs.append(buf)
         got = self.comm.all_reduce_sum(bufs)
         for r, g in zip(self.ranks, got):
-            r.X[i].copy_(g[:, 0].to(t.int64))
-            r.pmp[i].copy_(g[:, 1])
-            r.resid.copy_(g[:, 2])
-            r.urow.copy_(g[:, 3:])
+            r.ops.exchange_unpack(g, first, r.X[i], r.pmp[i], r.resid, r.H)
 
     # -------------------------------------------------------------- solve
     def _ev(self, phase):

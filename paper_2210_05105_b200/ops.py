@@ -171,6 +171,42 @@ class Ops:
                 ptr(M), ptr(H), int(J), R, k0, k1, dk, ptr(override), ptr(owner),
                 ptr(r_out), ptr(pmp_i), self.status.ptr, stream_handle())
 
+    def sts_rank_tree(self, block_grams, order, tree=None):
+        """Packed rank tree of P block Grams (P x R x R, summed pairwise up the levels)."""
+        t = torch()
+        P, R = block_grams.shape[0], block_grams.shape[1]
+        nd = int(self.lib.rcp_sts_rank_tree_doubles(P, R))
+        if tree is None or tree.numel() < nd:
+            tree = t.zeros(nd, dtype=t.float64, device=self.dev)
+        self._c("rcp_sts_rank_tree", ptr(block_grams), ptr(order), P, R, ptr(tree), stream_handle())
+        return tree
+
+    def sts_rank_walk_grouped(self, rank_tree, P, leaf_rank, M, H_in, J, key, override, owner,
+                              r_out, pmp_i, hkey=None, key_bits=64):
+        R = M.shape[0]
+        w = self.ws("sts_rank_walk", self.lib.rcp_sts_rank_walk_ws_bytes(int(J), int(P), R))
+        k0, k1, dk = _key_args(key)
+        self._c("rcp_sts_rank_walk_grouped", ptr(rank_tree), int(P), ptr(leaf_rank), R, ptr(M),
+                ptr(H_in), ptr(hkey), int(key_bits), int(J), k0, k1, dk, ptr(override), ptr(owner),
+                ptr(r_out), ptr(pmp_i), ptr(w), w.numel(), self.status.ptr, stream_handle())
+
+    def sts_flat_local(self, cdf, dist, row_lo, mass, rin, sel, sel_value, J, Xi, pmp_i, resid):
+        n = cdf.shape[0]
+        self._c("rcp_sts_flat_local", ptr(cdf), ptr(dist), n, int(row_lo), ptr(mass), ptr(rin),
+                ptr(sel), int(sel_value), int(J), ptr(Xi), ptr(pmp_i), ptr(resid), self.status.ptr,
+                stream_handle())
+
+    def exchange_pack(self, Xi, pmp_i, resid, U, row_lo, owner, rank, buf):
+        n, R = U.shape
+        J = Xi.shape[0]
+        self._c("rcp_exchange_pack", ptr(Xi), ptr(pmp_i), ptr(resid), ptr(U), n, int(row_lo),
+                ptr(owner), int(rank), J, R, ptr(buf), stream_handle())
+
+    def exchange_unpack(self, buf, init, Xi, pmp_i, resid, H):
+        J, R = H.shape
+        self._c("rcp_exchange_unpack", ptr(buf), J, R, 1 if init else 0, ptr(Xi), ptr(pmp_i),
+                ptr(resid), ptr(H), stream_handle())
+
     # ------------------------------------------------------------------ MTTKRP
     def mttkrp_ws(self, J, cap, n_rows, R):
         return self.ws("mttkrp", self.lib.rcp_mttkrp_ws_bytes(int(J), int(cap), int(n_rows), int(R)))

@@ -255,6 +255,7 @@ def sts_build(blocks: FactorBlocks, grid=None, ledger=None, round_id=0,
         levels[lev] = levels[lev + 1].reshape(-1, 2, R, R).sum(dim=1)
     node_dev = t.cat([x.reshape(-1) for x in levels]).contiguous()
     devstate = dict(U=Us, trees=trees, leaves=leaves, node_grams=node_dev,
+                    rank_tree=ops.sts_rank_tree(rank_g, t.as_tensor(order, device=dev)),
                     leaf_rank=t.as_tensor(leaf_rank.astype(np.int32), device=dev))
     return LeverageTree(blocks.mode, [to_host(x) for x in levels], leaf_rank, blocks.lows.copy(),
                         blocks.his.copy(), offsets, None, leaf_block_size, dev=devstate)
@@ -300,12 +301,22 @@ def sts_sample(trees, k, J, gram_chain_pinv, grams, blocks_per_mode, seed, round
         hk, kb = ops.walk_key(X, dims, k, i, hkey)
         depth = trees[i].depth
         if P > 1 and depth > 0:
-            ops.sts_rank_walk(tr["node_grams"], depth, P, tr["leaf_rank"], M,
-                              ones if first else H, J, key, ov, owner, rtop, pmp[i])
+            ops.sts_rank_walk_grouped(tr["rank_tree"], P, tr["leaf_rank"], M, H_in, J, key, ov,
+                                      owner, rtop, pmp[i], hkey=hk, key_bits=kb)
             for p in range(P):
                 if tr["trees"][p] is None:
                     continue
-                ops.sts_walk(tr["trees"][p], tr["U"][p], tr["leaves"][p], int(trees[i].block_lo[p]),
+                Up = tr["U"][p]
+                if first:   # H = ones for every sample: a flat inverse CDF per rank
+                    n = Up.shape[0]
+                    dist = t.zeros(n, dtype=t.float64, device=dev)
+                    cdf = t.zeros(n, dtype=t.float64, device=dev)
+                    mass = t.zeros(1, dtype=t.float64, device=dev)
+                    ops.arls_build(Up, M, dist, cdf, mass)
+                    ops.sts_flat_local(cdf, dist, int(trees[i].block_lo[p]), mass, rtop, owner, p,
+                                       J, X[i], pmp[i], resid)
+                    continue
+                ops.sts_walk(tr["trees"][p], Up, tr["leaves"][p], int(trees[i].block_lo[p]),
                              M, H_in, J, key, None, rtop, owner, p, X[i], pmp[i], resid, hkey=hk,
                              key_bits=kb)
             # samples routed to a rank without rows (ref samplers.py:341-342)

@@ -28,13 +28,41 @@ def _port():
     return p
 
 
+class _HostOps:
+    """Test double for the two exchange kernels (rcp_exchange_pack / rcp_exchange_unpack,
+    include/randcp_b200.h) so that the Cluster's exchange logic runs on CPU tensors; the
+    kernels themselves are checked against the same semantics in tests/test_gpu_engine.py."""
+
+    @staticmethod
+    def exchange_pack(Xi, pmp_i, resid, U, row_lo, owner, rank, buf):
+        row = Xi - row_lo
+        mine = (owner == rank) & (row >= 0) & (row < U.shape[0])
+        buf.zero_()
+        buf[mine, 0] = Xi[mine].to(torch.float64)
+        buf[mine, 1] = pmp_i[mine]
+        buf[mine, 2] = resid[mine]
+        buf[mine, 3:] = U[row[mine]]
+
+    @staticmethod
+    def exchange_unpack(buf, init, Xi, pmp_i, resid, H):
+        Xi.copy_(buf[:, 0].to(torch.int64))
+        pmp_i.copy_(buf[:, 1])
+        resid.copy_(buf[:, 2])
+        if init:
+            H.copy_(buf[:, 3:])
+        else:
+            H.mul_(buf[:, 3:])
+
+
 def _fake_rank(rank, P, N, J, R):
     t = torch
     return types.SimpleNamespace(
-        rank=rank, P=P, N=N, J=J, R=R, dev=t.device("cpu"),
+        rank=rank, P=P, N=N, J=J, R=R, dev=t.device("cpu"), ops=_HostOps(),
         owner=t.tensor([s % P for s in range(J)], dtype=t.int32),
         X=t.full((N, J), -1, dtype=t.int64), pmp=t.ones((N, J), dtype=t.float64),
-        resid=t.zeros(J, dtype=t.float64), urow=t.zeros((J, R), dtype=t.float64),
+        resid=t.zeros(J, dtype=t.float64), H=t.full((J, R), 2.0, dtype=t.float64),
+        lo=[1000 * rank] * N,
+        U=[(t.arange(J, dtype=t.float64) + 0.1 * rank).unsqueeze(1).repeat(1, R) for _ in range(N)],
         rows_tmp=t.zeros(J, dtype=t.int64), prob_tmp=t.zeros(J, dtype=t.float64),
         urow_tmp=t.zeros((J, R), dtype=t.float64))
 
@@ -64,14 +92,19 @@ def _worker(rank, world, port):
         r.X[i][mine] = 1000 * rank + mine
         r.pmp[i][mine] = 0.5 + rank
         r.resid[mine] = 0.25 * rank
-        r.urow[mine] = (mine.to(torch.float64) + 0.1 * rank).unsqueeze(1).repeat(1, R)
         cl = Cluster([r], comm, "sts", J, 0)
-        cl._exchange_walk(i)
+        cl._exchange_walk(i, True)          # first constant mode: H = the sampled rows
         s = torch.arange(J)
         own = s % world
+        rowv = s.to(torch.float64) + 0.1 * own.to(torch.float64)
         assert torch.equal(r.X[i], 1000 * own + s)
         assert torch.equal(r.pmp[i], 0.5 + own.to(torch.float64))
-        assert torch.equal(r.urow[:, 0], s.to(torch.float64) + 0.1 * own.to(torch.float64))
+        assert torch.equal(r.resid, 0.25 * own.to(torch.float64))
+        assert torch.equal(r.H[:, 0], rowv) and torch.equal(r.H[:, R - 1], rowv)
+        r.X[i].fill_(-1)
+        r.X[i][mine] = 1000 * rank + mine
+        cl._exchange_walk(i, False)         # later modes multiply the running rows
+        assert torch.equal(r.H[:, 0], rowv * rowv)
         # CP-ARLS-LEV: rank-order concatenation of local draws
         quota = np.array([3, 4][:world] if world == 2 else [2] * world)
         q = int(quota[rank])
