@@ -184,6 +184,13 @@ int rcp_sts_rank_walk_grouped(const double *d_rank_tree, int P, const int32_t *d
                               uint64_t key1, const uint64_t *d_key, const double *d_override,
                               int32_t *d_owner, double *d_r_out, double *d_pmp_i, void *d_ws,
                               size_t ws_bytes, int *d_status, void *stream);
+/* The rank-level walk of the first constant mode (every sample's Hadamard row is ones): the
+ * 2^(depth+1)-1 node masses are evaluated once per CTA, then every sample descends alone.
+ * Same outputs and errors as rcp_sts_rank_walk_grouped; P <= 1024. */
+int rcp_sts_rank_walk_ones(const double *d_rank_tree, int P, const int32_t *d_leaf_rank, int R,
+                           const double *d_M, int64_t J, uint64_t key0, uint64_t key1,
+                           const uint64_t *d_key, const double *d_override, int32_t *d_owner,
+                           double *d_r_out, double *d_pmp_i, int *d_status, void *stream);
 /* Local search of the first constant mode at P > 1 (all samples share H = ones): samples
  * with d_sel[s] == sel_value invert the CDF of this rank's row masses (rcp_arls_build of
  * the block with the conditioning matrix) at their residual d_rin[s]
@@ -251,6 +258,10 @@ int rcp_sts_flat_draw(const double *d_cdf, const double *d_dist, int64_t n, int6
  * column key, and the STS walk's grouping key). */
 int rcp_row_keys(const int64_t *d_X, int N, int64_t J, const int64_t *h_strides,
                  int64_t *d_out, void *stream);
+/* d_out[e] = ((p_0[e] + p_1[e]) + p_2[e]) + ... over nparts stacked arrays of len doubles:
+ * the rank-ordered sum of replicated contributions (block Grams, column sums of squares;
+ * ref grid.py:295-297). */
+int rcp_ordered_sum(const double *d_parts, int nparts, int64_t len, double *d_out, void *stream);
 /* H[s,:] *= d_urow[s,:] for all s (fold walked rows into the running Hadamard rows). */
 int rcp_hadamard_rows(double *d_H, const double *d_urow, int64_t J, int R, int init_ones,
                       void *stream);

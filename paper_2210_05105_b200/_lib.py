@@ -61,6 +61,8 @@ _SIGS = {
     "rcp_sts_rank_walk_ws_bytes": (_sz, [_i64, _i32, _i32]),
     "rcp_sts_rank_walk_grouped": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _i64, _u64,
                                          _u64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
+    "rcp_sts_rank_walk_ones": (_i32, [_vp, _i32, _vp, _i32, _vp, _i64, _u64, _u64, _vp, _vp, _vp, _vp,
+                                      _vp, _vp, _vp]),
     "rcp_sts_flat_local": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp,
                                   _vp, _vp]),
     "rcp_exchange_pack": (_i32, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _i32, _i64, _i32, _vp, _vp]),
@@ -74,6 +76,7 @@ _SIGS = {
     "rcp_sts_flat_draw": (_i32, [_vp, _vp, _i64, _i64, _vp, _u64, _u64, _vp, _i64, _vp, _vp, _vp,
                                  _vp]),
     "rcp_hadamard_rows": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp]),
+    "rcp_ordered_sum": (_i32, [_vp, _i32, _i64, _vp, _vp]),
     "rcp_weights": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp, _vp]),
     "rcp_mttkrp_ws_bytes": (_sz, [_i64, _i64, _i64, _i32]),
     "rcp_mttkrp_layout": (_i32, [_i64, _i64, _i32, _sz, _vp]),

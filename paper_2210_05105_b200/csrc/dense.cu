@@ -697,6 +697,18 @@ __global__ void weights_kernel(const double *__restrict__ pmp, int N, int64_t J,
   w[s] = 1.0 / sqrt((double)J * p);
 }
 
+// out[e] = ((p_0[e] + p_1[e]) + p_2[e]) + ... : the rank-ordered sum of P replicated
+// contributions (block Grams, column norms; ref grid.py:295-297).
+__global__ void ordered_sum_kernel(const double *__restrict__ parts, int nparts, int64_t len,
+                                   double *__restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double s = parts[e];
+    for (int p = 1; p < nparts; ++p) s += parts[(int64_t)p * len + e];
+    out[e] = s;
+  }
+}
+
 __global__ void hadamard_rows_kernel(double *__restrict__ H, const double *__restrict__ urow,
                                      int64_t tot, int init) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
@@ -1038,6 +1050,17 @@ int rcp_weights(const double *d_pmp, int N, int64_t J, double *d_prob, double *d
   weights_kernel<<<(unsigned)ceil_div(J, 256), 256, 0, RCP_STREAM(stream)>>>(d_pmp, N, J, d_prob,
                                                                              d_w, d_status);
   RCP_LAUNCH_CHECK("weights");
+  return RCP_OK;
+}
+
+int rcp_ordered_sum(const double *d_parts, int nparts, int64_t len, double *d_out, void *stream) {
+  if (nparts < 1 || len < 0) return RCP_ERR_ARG;
+  if (len == 0) return RCP_OK;
+  if (!d_parts || !d_out) return RCP_ERR_ARG;
+  int64_t blocks = ceil_div(len, 256);
+  if (blocks > 8LL * sm_count()) blocks = 8LL * sm_count();
+  ordered_sum_kernel<<<(unsigned)blocks, 256, 0, RCP_STREAM(stream)>>>(d_parts, nparts, len, d_out);
+  RCP_LAUNCH_CHECK("ordered_sum");
   return RCP_OK;
 }
 

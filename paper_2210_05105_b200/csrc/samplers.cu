@@ -491,6 +491,82 @@ __global__ void sts_rank_tree_kernel(const double *__restrict__ blocks,
   }
 }
 
+// Rank-level walk when every sample shares H = ones (the first constant mode): each CTA
+// evaluates the mass <G_v (.) M', 1 1^T> of every rank-tree node once (warp per node over
+// the packed triangle), then its threads descend one sample each with
+// T = max(q_left, 0) / q_node (ref samplers.py:423-451).
+constexpr int kOneGroupMaxNodes = 2047;
+__global__ void __launch_bounds__(1024)
+rank_walk_ones_kernel(const double *__restrict__ tree, int depth, const int32_t *__restrict__ leaf_rank,
+                      const double *__restrict__ M, int R, int64_t J, uint64_t k0, uint64_t k1,
+                      const uint64_t *__restrict__ dk, const double *__restrict__ ov,
+                      int32_t *__restrict__ owner, double *__restrict__ rout,
+                      double *__restrict__ pmp, int *status) {
+  __shared__ double q[kOneGroupMaxNodes];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int Rt = R * (R + 1) / 2, Rs = tri_stride(R);
+  const int nnodes = (2 << depth) - 1;
+  for (int v = wid; v < nnodes; v += nw) {
+    const double *g = tree + (int64_t)v * Rs;
+    double acc = 0.0;
+    // lane's first element and its (a, b); then step 32 elements along the packed rows
+    int e = lane, a = 0, rem = lane;
+    while (e < Rt && rem >= R - a) {
+      rem -= R - a;
+      ++a;
+    }
+    while (e < Rt) {
+      const int b = a + rem;
+      const double m = M[a * R + b];
+      acc = fma(g[e], a == b ? m : 2.0 * m, acc);
+      e += 32;
+      rem += 32;
+      while (e < Rt && rem >= R - a) {
+        rem -= R - a;
+        ++a;
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) q[v] = acc;
+  }
+  __syncthreads();
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= J) return;
+  if (dk) {
+    k0 = dk[0];
+    k1 = dk[1];
+  }
+  double r = ov ? ov[s] : u64_to_unit(philox_word(k0, k1, (uint64_t)s));
+  const double tiny = DBL_MIN;
+  double prob = 1.0;
+  int v = 0;
+  for (int lev = 0; lev < depth; ++lev) {
+    const double den = q[(1 << lev) - 1 + v];
+    const double num = q[(1 << (lev + 1)) - 1 + 2 * v];
+    if (!(den > 0.0)) {
+      raise_status(status, RCP_ST_DEGENERATE);
+      owner[s] = -1;
+      return;
+    }
+    double T = (num > 0.0 ? num : 0.0) / den;
+    T = fmin(fmax(T, 0.0), 1.0);
+    const bool right = r >= T;
+    prob *= right ? (1.0 - T) : T;
+    r = right ? (r - T) / fmax(1.0 - T, tiny) : r / fmax(T, tiny);
+    r = fmin(fmax(r, 0.0), one_below());
+    v = 2 * v + (right ? 1 : 0);
+  }
+  const int32_t p = leaf_rank[v];
+  if (p < 0) {   // "walk branched into an empty padded subtree"
+    raise_status(status, RCP_ST_DEGENERATE);
+    owner[s] = -1;
+    return;
+  }
+  owner[s] = p;
+  rout[s] = r;
+  pmp[s] = prob;
+}
+
 // Local search of the first constant mode at P > 1 (every sample shares H = ones): the
 // samples routed to this rank invert the CDF of its rows' masses with their residual
 // (ref _leaf_search_batch samplers.py:313-345), multiplying the path probability.
@@ -792,6 +868,25 @@ int rcp_sts_rank_tree(const double *d_block_grams, const int64_t *d_order, int P
   sts_rank_tree_kernel<<<(unsigned)ceil_div(tri_stride(R), 128), 128, 0, RCP_STREAM(stream)>>>(
       d_block_grams, d_order, P, R, depth, d_tree);
   RCP_LAUNCH_CHECK("sts_rank_tree");
+  return RCP_OK;
+}
+
+int rcp_sts_rank_walk_ones(const double *d_rank_tree, int P, const int32_t *d_leaf_rank, int R,
+                           const double *d_M, int64_t J, uint64_t key0, uint64_t key1,
+                           const uint64_t *d_key, const double *d_override, int32_t *d_owner,
+                           double *d_r_out, double *d_pmp_i, int *d_status, void *stream) {
+  if (P < 1 || R < 1 || R > RCP_MAX_RANK || J < 0 || !d_rank_tree || !d_leaf_rank || !d_M ||
+      !d_owner || !d_r_out || !d_pmp_i)
+    return RCP_ERR_ARG;
+  const int depth = rcp_sts_depth(P, 1);
+  if ((2 << depth) - 1 > kOneGroupMaxNodes) return RCP_ERR_ARG;
+  if (J == 0) return RCP_OK;
+  // few nodes: small CTAs (each CTA evaluates every node once); many: fewer, larger CTAs
+  const int threads = depth <= 4 ? 256 : 1024;
+  rank_walk_ones_kernel<<<(unsigned)ceil_div(J, threads), threads, 0, RCP_STREAM(stream)>>>(
+      d_rank_tree, depth, d_leaf_rank, d_M, R, J, key0, key1, d_key, d_override, d_owner, d_r_out,
+      d_pmp_i, d_status);
+  RCP_LAUNCH_CHECK("sts_rank_walk_ones");
   return RCP_OK;
 }
 

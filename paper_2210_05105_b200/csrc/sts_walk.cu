@@ -769,15 +769,20 @@ int walk_impl(const double *d_tree, const double *d_U, int64_t n, int R, int lea
   double *gm = (double *)(w + L.o_gm);
   void *cub_tmp = w + L.o_cub;
   const unsigned gb = (unsigned)ceil_div(J, 256);
-  walk_prepare_kernel<<<gb, 256, 0, st>>>(d_hkey, J, d_sel, sel_value, key, idx, ctl,
+  // no key and no selection: every sample is in one group, already "sorted"
+  const bool one_group = !d_hkey && !d_sel;
+  walk_prepare_kernel<<<gb, 256, 0, st>>>(d_hkey, J, d_sel, sel_value, one_group ? key2 : key,
+                                          one_group ? idx2 : idx, ctl,
                                           (unsigned long long *)(w + L.o_prof));
   RCP_LAUNCH_CHECK("walk_prepare");
   // group samples by key (only the key's bits); level 0 holds their uniforms in that order
   int32_t *idx3 = (int32_t *)(w + L.o_idx3);
   size_t tb = L.cub_bytes;
-  RCP_CUDA_TRY(
-      cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key, key2, idx, idx2, (int)J, 0, key_bits, st));
-  RCP_LAUNCH_CHECK("walk_sort_key");
+  if (!one_group) {
+    RCP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key, key2, idx, idx2, (int)J, 0,
+                                                 key_bits, st));
+    RCP_LAUNCH_CHECK("walk_sort_key");
+  }
   walk_fill_r_kernel<<<gb, 256, 0, st>>>(idx2, J, key0, key1, d_key, d_override, d_rin, r);
   RCP_LAUNCH_CHECK("walk_fill_r");
   walk_seed_kernel<<<gb, 256, 0, st>>>(key2, idx2, J, d_sel ? d_pmp_i : nullptr, runs, ctl);

@@ -41,17 +41,20 @@ CAP_LIMIT = 1 << 28
 PHASES = ("sampling", "gather", "mttkrp", "reduction", "postprocess", "rebuild")
 
 
-def default_leaf(n, R, budget_bytes=4 << 30):
-    """Rows per tree leaf: 8, doubled until the padded tree fits the budget (<= 64).  A leaf
-    costs L row masses (L R^2/2 each) per walking run, a level one pair of node masses, so
-    small leaves win until the per-walk G (.) M tree pass and the rebuild grow (measured
-    on C3: L = 8 beats 16 and 4)."""
+def default_leaf(n, R, budget_bytes=4 << 30, walkers=None):
+    """Rows per tree leaf: 8, doubled (<= 64) until the padded tree fits the budget and has
+    at most 8 nodes per walking sample.  A leaf costs L row masses (L R^2/2 each) per
+    walking run, a level one pair of node masses, so small leaves win (measured on C3:
+    L = 8 beats 16 and 4) until the per-walk G (.) M pass over every node and the rebuild
+    grow: with P ranks a rank walks about J / P samples, and a tree with many more nodes
+    than walkers spends its time conditioning nodes nobody visits (C4 at P = 8: 0.46 ms
+    per walk for the 1.5 GB tree of L = 8, 0.06 ms at L = 64)."""
     Rt = R * (R + 1) // 2
     L = 8
     while L < 64:
         nl = max(1, math.ceil(n / L))
         nodes = 2 * (1 << max(0, math.ceil(math.log2(nl)))) - 1
-        if nodes * Rt * 8 <= budget_bytes:
+        if nodes * Rt * 8 <= budget_bytes and (walkers is None or nodes <= 8 * max(walkers, 1)):
             break
         L *= 2
     return L
@@ -240,7 +243,8 @@ class RankState:
             if self.leaf_cfg is not None:
                 self.leaf[j] = int(max(1, min(64, int(self.leaf_cfg))))
             else:
-                self.leaf[j] = default_leaf(max(self.n[j], 1), self.R)
+                self.leaf[j] = default_leaf(max(self.n[j], 1), self.R,
+                                            walkers=max(1, self.J // self.P))
         return self.leaf[j]
 
     # ------------------------------------------------------------- rebuild
@@ -249,17 +253,15 @@ class RankState:
 
     def set_gram(self, k, blocks):
         """blocks: list of P (R x R) tensors in rank order -> ordered sum (ref grid.py:295-297)."""
-        g = blocks[0].clone()
-        for b in blocks[1:]:
-            g += b
-        self.grams[k].copy_(g)
-        if self.P > 1:   # persistent per mode: a graph replay reads the captured addresses
-            bg = self.block_grams[k]
-            if bg is None:
-                bg = self.block_grams[k] = self.t.empty((self.P, self.R, self.R),
-                                                        dtype=self.t.float64, device=self.dev)
-            for p, b in enumerate(blocks):
-                bg[p].copy_(b)
+        if self.P == 1:
+            self.grams[k].copy_(blocks[0])
+            return
+        bg = self.block_grams[k]   # persistent per mode: a graph replay reads its address
+        if bg is None:
+            bg = self.block_grams[k] = self.t.empty((self.P, self.R, self.R),
+                                                    dtype=self.t.float64, device=self.dev)
+        self.t.stack(list(blocks), out=bg)
+        self.ops.ordered_sum(bg, self.grams[k])
 
     def build_tree(self, k):
         """Mark the local tree of mode k stale (it is rebuilt on its first walk: at P = 1 the
@@ -467,8 +469,16 @@ class RankState:
             self.colsq.zero_()
         return self.colsq
 
-    def renormalize(self, k, colsq_total):
-        self.colsq.copy_(colsq_total)
+    def stage_colsq(self, parts):
+        """parts: the P ranks' column sums of squares in rank order (P > 1)."""
+        if getattr(self, "colsq_parts", None) is None:
+            self.colsq_parts = self.t.empty((self.P, self.R), dtype=self.t.float64, device=self.dev)
+        self.t.stack(list(parts), out=self.colsq_parts)
+
+    def renormalize(self, k):
+        """colsq: this rank's sums (P = 1) or the rank-ordered total of the staged parts."""
+        if self.P > 1:
+            self.ops.ordered_sum(self.colsq_parts, self.colsq)
         if self.n[k] > 0:
             self.ops.renormalize(self.U[k], self.colsq, self.sigma)
         else:
@@ -663,11 +673,11 @@ class Cluster:
         t0 = self._tick("mttkrp", t0)
         self._ev("update")
         parts = self.comm.all_gather([r.update(k) for r in self.ranks])
-        tot = parts[0].clone()
-        for p in parts[1:]:
-            tot += p.to(tot.device)
+        if self.P > 1:   # every rank reads all parts before any rank overwrites its own
+            for r in self.ranks:
+                r.stage_colsq(parts)
         for r in self.ranks:
-            r.renormalize(k, tot.to(r.dev))
+            r.renormalize(k)
         t0 = self._tick("postprocess", t0)
         self._ev("rebuild")
         self.rebuild(k)

@@ -75,6 +75,12 @@ class Ops:
         self._c("rcp_weights", ptr(pmp), N, J, ptr(prob), ptr(w), self.status.ptr,
                 stream_handle())
 
+    def ordered_sum(self, parts, out):
+        """out = parts[0] + parts[1] + ... (left to right) for a stacked (P, ...) tensor."""
+        P = parts.shape[0]
+        self._c("rcp_ordered_sum", ptr(parts), P, parts[0].numel(), ptr(out), stream_handle())
+        return out
+
     def hadamard_rows(self, H, urow, init):
         J, R = H.shape
         self._c("rcp_hadamard_rows", ptr(H), ptr(urow), J, R, 1 if init else 0, stream_handle())
@@ -184,8 +190,13 @@ class Ops:
     def sts_rank_walk_grouped(self, rank_tree, P, leaf_rank, M, H_in, J, key, override, owner,
                               r_out, pmp_i, hkey=None, key_bits=64):
         R = M.shape[0]
-        w = self.ws("sts_rank_walk", self.lib.rcp_sts_rank_walk_ws_bytes(int(J), int(P), R))
         k0, k1, dk = _key_args(key)
+        if H_in is None and hkey is None and P <= 1024:   # one group: H = ones for every sample
+            self._c("rcp_sts_rank_walk_ones", ptr(rank_tree), int(P), ptr(leaf_rank), R, ptr(M),
+                    int(J), k0, k1, dk, ptr(override), ptr(owner), ptr(r_out), ptr(pmp_i),
+                    self.status.ptr, stream_handle())
+            return
+        w = self.ws("sts_rank_walk", self.lib.rcp_sts_rank_walk_ws_bytes(int(J), int(P), R))
         self._c("rcp_sts_rank_walk_grouped", ptr(rank_tree), int(P), ptr(leaf_rank), R, ptr(M),
                 ptr(H_in), ptr(hkey), int(key_bits), int(J), k0, k1, dk, ptr(override), ptr(owner),
                 ptr(r_out), ptr(pmp_i), ptr(w), w.numel(), self.status.ptr, stream_handle())

@@ -38,7 +38,7 @@ def _full_rank_tree(blocks, order, width):
 
 
 @pytest.mark.parametrize("P,R,groups", [(2, 5, 1), (3, 8, 7), (4, 50, 300), (8, 25, 2000),
-                                        (5, 70, 50)])
+                                        (5, 70, 50), (8, 50, 1), (37, 100, 1)])
 def test_grouped_rank_walk_matches_per_sample_walk(env, P, R, groups):
     t, dev, ops = env
     rng = np.random.default_rng(P * 100 + R)
@@ -70,14 +70,19 @@ def test_grouped_rank_walk_matches_per_sample_walk(env, P, R, groups):
     r_b = t.zeros(J, dtype=t.float64, device=dev)
     p_b = t.ones(J, dtype=t.float64, device=dev)
     kb = max(1, int(groups - 1).bit_length() + 1)
-    ops.sts_rank_walk_grouped(tree, P, d(leaf_rank), Md, Hd if groups > 1 else None, J, key, None,
-                              own_b, r_b, p_b, hkey=hkey if groups > 1 else None, key_bits=kb)
-    ops.status.check("rank walks")
-    a, b = own_a.cpu().numpy(), own_b.cpu().numpy()
-    assert np.array_equal(a, b)
-    assert set(np.unique(b)) <= set(order.tolist())
-    assert np.allclose(p_a.cpu().numpy(), p_b.cpu().numpy(), rtol=1e-11, atol=0)
-    assert np.allclose(r_a.cpu().numpy(), r_b.cpu().numpy(), rtol=0, atol=1e-9)
+    # one group: H_in = None takes the node-masses-once kernel (rcp_sts_rank_walk_ones), an
+    # explicit all-ones H_in the run-grouped walk with its single-group shortcut (no sort)
+    variants = [(Hd, hkey)] if groups > 1 else [(None, None), (Hd, None)]
+    for Hv, kv in variants:
+        own_b.fill_(-7)
+        ops.sts_rank_walk_grouped(tree, P, d(leaf_rank), Md, Hv, J, key, None, own_b, r_b, p_b,
+                                  hkey=kv, key_bits=kb)
+        ops.status.check("rank walks")
+        a, b = own_a.cpu().numpy(), own_b.cpu().numpy()
+        assert np.array_equal(a, b)
+        assert set(np.unique(b)) <= set(order.tolist())
+        assert np.allclose(p_a.cpu().numpy(), p_b.cpu().numpy(), rtol=1e-11, atol=0)
+        assert np.allclose(r_a.cpu().numpy(), r_b.cpu().numpy(), rtol=0, atol=1e-9)
 
 
 def test_rank_tree_levels_are_pairwise_sums(env):

@@ -7,7 +7,9 @@ import bench
 from paper_2210_05105_b200.engine import make_local_cluster
 dev = torch.device("cuda", 0)
 c, idx, vals = bench.make_tensor(os.environ.get("CFG", "c3"), 0, dev)
-cl = make_local_cluster(c["dims"], idx, vals, c["R"], c["J"], os.environ.get("SAMPLER", "sts"), 0)
+P = int(os.environ.get("P", "1"))   # virtual ranks (LocalComm): every rank's kernels, one after another
+cl = make_local_cluster(c["dims"], idx, vals, c["R"], c["J"], os.environ.get("SAMPLER", "sts"), 0,
+                        P=P, balance="nnz" if P > 1 else "rows")
 for rnd in range(1, 4): cl.round(rnd)
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()

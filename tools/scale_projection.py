@@ -176,12 +176,15 @@ def main():
     plist = [int(x) for x in os.environ.get("PLIST", "1,2,4,8").split(",")]
     rounds = int(os.environ.get("ROUNDS", "3"))
     rank_override = os.environ.get("RANK_R")
+    # LEAF: STS leaf rows for every rank (P virtual ranks share one GPU's memory: C4's
+    # default trees, sized for a GPU per rank, do not fit eight times)
+    leaf = int(os.environ["LEAF"]) if os.environ.get("LEAF") else None
     dev = torch.device("cuda", 0)
     _lib.load()
     c, idx, vals = bench.make_tensor(cfg, 0, dev)
     R = int(rank_override) if rank_override else c["R"]
     out = {"config": cfg, "sampler": sampler, "rank": R, "samples_J": c["J"],
-           "dims": list(c["dims"]), "row_blocks": "nnz-balanced (P > 1)",
+           "dims": list(c["dims"]), "row_blocks": "nnz-balanced (P > 1)", "sts_leaf_rows": leaf,
            "model": {"bus_GBps": BUS_GBS, "latency_us_per_collective": LAT_US,
                      "note": "collective time is modelled, not measured (one GPU available)"},
            "method": "P virtual ranks (LocalComm) on one B200, eager launches; per-rank device "
@@ -192,15 +195,42 @@ def main():
     for P in plist:
         t0 = time.perf_counter()
         cl = make_local_cluster(c["dims"], idx, vals, R, c["J"], sampler, 0, P=P,
-                                balance="nnz" if P > 1 else "rows")
+                                balance="nnz" if P > 1 else "rows", leaf=leaf)
+        if P == plist[-1]:
+            idx = vals = None   # the COO is not needed once the last cluster holds its stores
+            torch.cuda.empty_cache()
         torch.cuda.synchronize()
         setup = time.perf_counter() - t0
+        for rnd in range(1, 4):
+            cl.round(rnd)
+        torch.cuda.synchronize()
+        # the same P ranks' rounds replayed from a CUDA graph (no host launch gaps): the
+        # ratio to the eager wall time says how much of the event-bracketed times below is
+        # launch latency that a replayed N-GPU round does not pay
+        graph_ms = None
+        rnd0 = 4
+        if os.environ.get("GRAPH", "1") == "1" and cl.graph_ok():
+            cl.round_graph(rnd0)
+            torch.cuda.synchronize()
+            g0 = torch.cuda.Event(enable_timing=True)
+            g1 = torch.cuda.Event(enable_timing=True)
+            g0.record()
+            for rnd in range(rnd0 + 1, rnd0 + 1 + rounds):
+                cl.round_graph(rnd)
+            g1.record()
+            torch.cuda.synchronize()
+            cl.check("graph rounds")
+            graph_ms = g0.elapsed_time(g1) / rounds
+            rnd0 += 1 + rounds
+            for r in cl.ranks:   # back to host-side keys for the eager rounds below
+                r.dkeys = None
+                r.gperm = None
         # serialise the side streams: clean per-call timings, overlap credited in analyse()
         cl._side = torch.cuda.current_stream()
         for r in cl.ranks:
             r._tree_stream = torch.cuda.current_stream()
-        for rnd in range(1, 4):
-            cl.round(rnd)
+        cl.round(rnd0)
+        rnd0 += 1
         torch.cuda.synchronize()
         rec = Recorder()
         for r in cl.ranks:
@@ -212,7 +242,7 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        for rnd in range(4, 4 + rounds):
+        for rnd in range(rnd0, rnd0 + rounds):
             cl.round(rnd, check=False)
         e1.record()
         torch.cuda.synchronize()
@@ -228,6 +258,7 @@ def main():
         a.update({
             "P": P, "setup_s": round(setup, 1),
             "one_gpu_wall_ms_per_round_all_ranks_serial": e0.elapsed_time(e1) / rounds,
+            "one_gpu_graph_replay_ms_per_round_all_ranks": graph_ms,
             "distinct_nnz_per_round_per_rank": nnz_d,
             "sampled_nnz_per_round_total": sum(nnz_m),
             "mttkrp_ms_per_round_per_rank": [round(x, 4) for x in mt],
@@ -243,8 +274,10 @@ def main():
             a["projected_parallel_efficiency"] = t1 / (P * a["projected_ms_per_round"])
             a["projected_sampled_nnz_per_s"] = sum(nnz_m) / (a["projected_ms_per_round"] / 1e3)
         out["points"].append(a)
-        print("P=%d projected %.3f ms/round (compute %.3f + comm %.3f), mttkrp imbalance %.2f, eff %s"
-              % (P, a["projected_ms_per_round"], a["compute_ms_per_round"],
+        print("P=%d eager wall %.2f graph wall %s | projected %.3f ms/round (compute %.3f + comm %.3f), mttkrp imbalance %.2f, eff %s"
+              % (P, a["one_gpu_wall_ms_per_round_all_ranks_serial"],
+                 "%.2f" % graph_ms if graph_ms else "n/a",
+                 a["projected_ms_per_round"], a["compute_ms_per_round"],
                  a["modelled_comm_ms_per_round"], a["imbalance_mttkrp_time_max_over_mean"] or 0,
                  "%.2f" % a["projected_parallel_efficiency"] if t1 else "n/a"), flush=True)
         del cl, rec
