@@ -237,6 +237,19 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
                  double *d_pmp_i, double *d_resid, double *d_H_out, void *d_ws, size_t ws_bytes,
                  int *d_status,
                  void *stream);
+/* The conditioning pass of rcp_sts_walk alone (packed M' tables and G (.) M' for every tree
+ * node, written into the walk workspace): it depends only on the tree and M, so it can run
+ * on another stream while earlier modes are sampled; rcp_sts_walk_prepared is rcp_sts_walk
+ * on a workspace prepared this way (same tree, M, J, n, leaf, R). */
+int rcp_sts_walk_gm(const double *d_tree, int64_t n, int R, int leaf, const double *d_M, int64_t J,
+                    void *d_ws, size_t ws_bytes, void *stream);
+int rcp_sts_walk_prepared(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
+                          int64_t row_lo, const double *d_M, const double *d_H_in,
+                          const int64_t *d_hkey, int key_bits, int64_t J, uint64_t key0,
+                          uint64_t key1, const uint64_t *d_key, const double *d_override,
+                          const double *d_rin, const int32_t *d_sel, int32_t sel_value,
+                          int64_t *d_Xi, double *d_pmp_i, double *d_resid, double *d_H_out,
+                          void *d_ws, size_t ws_bytes, int *d_status, void *stream);
 /* Fold the walked rows: d_out[s,:] = U[X_i[s]-row_lo, :] (init != 0) or
  * d_out[s,:] *= U[X_i[s]-row_lo, :], for samples with d_sel[s] == sel_value (all when
  * d_sel is NULL) whose row lies in this block (ref samplers.py:464, H *= U_i[X_i]). */

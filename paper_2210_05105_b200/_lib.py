@@ -71,6 +71,10 @@ _SIGS = {
     "rcp_sts_walk_ws_bytes": (_sz, [_i64, _i64, _i32, _i32]),
     "rcp_sts_walk": (_i32, [_vp, _vp, _i64, _i32, _i32, _i64, _vp, _vp, _vp, _i32, _i64, _u64, _u64,
                             _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
+    "rcp_sts_walk_prepared": (_i32, [_vp, _vp, _i64, _i32, _i32, _i64, _vp, _vp, _vp, _i32, _i64,
+                                     _u64, _u64, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp,
+                                     _sz, _vp, _vp]),
+    "rcp_sts_walk_gm": (_i32, [_vp, _i64, _i32, _i32, _vp, _i64, _vp, _sz, _vp]),
     "rcp_fold_rows": (_i32, [_vp, _vp, _i64, _i32, _i64, _vp, _i64, _i32, _vp, _i32, _vp]),
     "rcp_row_keys": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp]),
     "rcp_sts_flat_draw": (_i32, [_vp, _vp, _i64, _i64, _vp, _u64, _u64, _vp, _i64, _vp, _vp, _vp,

@@ -726,6 +726,20 @@ size_t rcp_sts_walk_ws_bytes(int64_t J, int64_t n, int leaf, int R) {
 
 namespace {
 
+int walk_gm_tables(const double *d_tree, const double *d_M, int R, int depth, double *Mp,
+                   uint32_t *pairs, double *gm, cudaStream_t st) {
+  walk_tables_kernel<<<(unsigned)ceil_div(tri_stride(R), 128), 128, 0, st>>>(d_M, R, Mp, pairs);
+  RCP_LAUNCH_CHECK("walk_tables");
+  const int Rs = tri_stride(R);
+  const int64_t n2 = ((2LL << depth) - 1) * (int64_t)(Rs / 2);
+  int64_t g = ceil_div(n2, 256);
+  if (g > 8LL * sm_count()) g = 8LL * sm_count();
+  walk_gm_kernel<<<(unsigned)g, 256, 0, st>>>(d_tree, (const double2 *)Mp, n2, Rs / 2,
+                                               (double2 *)gm);
+  RCP_LAUNCH_CHECK("walk_gm");
+  return RCP_OK;
+}
+
 // The run-grouped walk.  d_leaf_rank != nullptr selects the rank mode: the tree's leaves are
 // ranks (leaf = 1, n = P, no factor rows); every sample gets its owner, its residual and the
 // probability of its path instead of a row.
@@ -736,7 +750,7 @@ int walk_impl(const double *d_tree, const double *d_U, int64_t n, int R, int lea
               const double *d_rin, const int32_t *d_sel, int32_t sel_value, int64_t *d_Xi,
               double *d_pmp_i, double *d_resid, double *d_H_out, void *d_ws, size_t ws_bytes,
               int *d_status, const int32_t *d_leaf_rank, int32_t *d_owner,
-              void *stream) {
+              void *stream, bool gm_ready = false) {
   if (R < 1 || R > RCP_MAX_RANK || leaf < 1 || leaf > kMaxLeaf || J < 0 || n < 0 ||
       J >= (1LL << 31) || key_bits < 1)
     return RCP_ERR_ARG;
@@ -787,17 +801,10 @@ int walk_impl(const double *d_tree, const double *d_U, int64_t n, int R, int lea
   RCP_LAUNCH_CHECK("walk_fill_r");
   walk_seed_kernel<<<gb, 256, 0, st>>>(key2, idx2, J, d_sel ? d_pmp_i : nullptr, runs, ctl);
   RCP_LAUNCH_CHECK("walk_seed");
-  // this walk's M' tables and G (.) M' for every node
-  walk_tables_kernel<<<(unsigned)ceil_div(tri_stride(R), 128), 128, 0, st>>>(d_M, R, Mp, pairs);
-  RCP_LAUNCH_CHECK("walk_tables");
-  {
-    const int Rs = tri_stride(R);
-    const int64_t n2 = ((2LL << depth) - 1) * (int64_t)(Rs / 2);
-    int64_t g = ceil_div(n2, 256);
-    if (g > 8LL * sm_count()) g = 8LL * sm_count();
-    walk_gm_kernel<<<(unsigned)g, 256, 0, st>>>(d_tree, (const double2 *)Mp, n2,
-                                                 Rs / 2, (double2 *)gm);
-    RCP_LAUNCH_CHECK("walk_gm");
+  // this walk's M' tables and G (.) M' for every node (unless rcp_sts_walk_gm made them)
+  if (!gm_ready) {
+    const int rc = walk_gm_tables(d_tree, d_M, R, depth, Mp, pairs, gm, st);
+    if (rc != RCP_OK) return rc;
   }
   static bool attr = false;
   if (!attr) {
@@ -847,6 +854,37 @@ int rcp_sts_walk(const double *d_tree, const double *d_U, int64_t n, int R, int 
   return walk_impl(d_tree, d_U, n, R, leaf, row_lo, d_M, d_H_in, d_hkey, key_bits, J, key0, key1,
                    d_key, d_override, d_rin, d_sel, sel_value, d_Xi, d_pmp_i, d_resid, d_H_out, d_ws,
                    ws_bytes, d_status, nullptr, nullptr, stream);
+}
+
+// The walk's conditioning pass alone (M' tables and G (.) M' for every node, written into
+// the walk workspace): depends only on the tree and M, so a caller can run it on another
+// stream ahead of the walk (rcp_sts_walk_prepared) while earlier modes are still sampled.
+int rcp_sts_walk_gm(const double *d_tree, int64_t n, int R, int leaf, const double *d_M, int64_t J,
+                    void *d_ws, size_t ws_bytes, void *stream) {
+  if (R < 1 || R > RCP_MAX_RANK || leaf < 1 || leaf > kMaxLeaf || J < 1 || n < 1 || !d_tree ||
+      !d_M || !d_ws)
+    return RCP_ERR_ARG;
+  const int depth = rcp_sts_depth(n, leaf);
+  if (depth > kMaxDepth) return RCP_ERR_ARG;
+  WalkWs L(J, depth, R);
+  if (ws_bytes < L.total) return RCP_ERR_ARG;
+  char *w = (char *)d_ws;
+  return walk_gm_tables(d_tree, d_M, R, depth, (double *)(w + L.o_mp), (uint32_t *)(w + L.o_pairs),
+                        (double *)(w + L.o_gm), RCP_STREAM(stream));
+}
+
+// rcp_sts_walk on a workspace whose conditioning pass rcp_sts_walk_gm already made (same
+// tree, M, J, n, leaf, R).
+int rcp_sts_walk_prepared(const double *d_tree, const double *d_U, int64_t n, int R, int leaf,
+                          int64_t row_lo, const double *d_M, const double *d_H_in,
+                          const int64_t *d_hkey, int key_bits, int64_t J, uint64_t key0,
+                          uint64_t key1, const uint64_t *d_key, const double *d_override,
+                          const double *d_rin, const int32_t *d_sel, int32_t sel_value,
+                          int64_t *d_Xi, double *d_pmp_i, double *d_resid, double *d_H_out,
+                          void *d_ws, size_t ws_bytes, int *d_status, void *stream) {
+  return walk_impl(d_tree, d_U, n, R, leaf, row_lo, d_M, d_H_in, d_hkey, key_bits, J, key0, key1,
+                   d_key, d_override, d_rin, d_sel, sel_value, d_Xi, d_pmp_i, d_resid, d_H_out, d_ws,
+                   ws_bytes, d_status, nullptr, nullptr, stream, true);
 }
 
 size_t rcp_sts_rank_walk_ws_bytes(int64_t J, int P, int R) {

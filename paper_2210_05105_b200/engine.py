@@ -199,6 +199,9 @@ class RankState:
         self.flat_dist = self.flat_cdf = self.flat_mass = None
         self.chain_pinv = t.zeros((R, R), **f64)
         self.M = t.zeros((R, R), **f64)
+        self.M_pre = t.zeros((R, R), **f64)    # conditioning matrix of the prefetched walk
+        self.walk_ws = None                    # this rank's walk workspace (holds G (.) M')
+        self.gm_ev = None                      # (mode, event) of a prefetched conditioning pass
         self.Gs = t.zeros((R, R), **f64)
         self.Gsp = t.zeros((R, R), **f64)
         self.Gp = t.zeros((R, R), **f64)
@@ -292,6 +295,28 @@ class RankState:
                 ev.record()
                 self.tree_ev[i] = ev
 
+    def prefetch_gm(self, i, k):
+        """The conditioning pass of the first walked mode (G (.) M' for every node of its
+        tree) on the tree stream: it needs only the chain pseudo-inverse and the tree, so
+        it overlaps the first constant mode's draw; the walk waits for its event."""
+        if self.n[i] == 0:
+            return
+        t = self.t
+        main = t.cuda.current_stream()
+        if self._tree_stream is None:
+            self._tree_stream = t.cuda.Stream(device=main.device)
+        s = self._tree_stream
+        n, leaf = self.n[i], self.leaf_of(i)
+        self.walk_ws = self.ops.sts_walk_ws(self.J, n, leaf, self.R, self.walk_ws, owned=True)
+        s.wait_stream(main)   # the chain pseudo-inverse; the previous solve's walk
+        with t.cuda.stream(s):
+            tree = self.local_tree(i)
+            self.ops.sts_cond(self.chain_pinv, self.grams, i, k, self.M_pre)
+            self.ops.sts_walk_gm(tree, n, leaf, self.M_pre, self.J, self.walk_ws)
+            ev = t.cuda.Event()
+            ev.record()
+        self.gm_ev = (i, ev)
+
     def local_tree(self, k):
         if self.tree_ev[k] is not None:
             self.t.cuda.current_stream().wait_event(self.tree_ev[k])
@@ -342,7 +367,14 @@ class RankState:
         """Walk all samples for constant mode i; this rank completes the samples whose
         leaf lies in its block (all of them when P == 1)."""
         ops = self.ops
-        ops.sts_cond(self.chain_pinv, self.grams, i, k, self.M)
+        gm_ready = self.gm_ev is not None and self.gm_ev[0] == i
+        if gm_ready:   # conditioning matrix and G (.) M' made ahead on the tree stream
+            self.t.cuda.current_stream().wait_event(self.gm_ev[1])
+            self.gm_ev = None
+            M = self.M_pre
+        else:
+            M = self.M
+            ops.sts_cond(self.chain_pinv, self.grams, i, k, M)
         if self.dkeys is not None:   # graph-replayed round: the key is read on the device
             key = self.dkeys[k, i]
         else:
@@ -352,7 +384,7 @@ class RankState:
         if self.P > 1:
             # the rank-level levels, replicated: every rank learns every sample's owner
             rtree, leaf_rank, _ = self.rank_tree[i]
-            ops.sts_rank_walk_grouped(rtree, self.P, leaf_rank, self.M, H_in, self.J, key, override,
+            ops.sts_rank_walk_grouped(rtree, self.P, leaf_rank, M, H_in, self.J, key, override,
                                       self.owner, self.rtop, self.pmp[i], hkey=hk, key_bits=kb)
             sel, rin = self.owner, self.rtop
         else:   # the walk / flat draw sets every sample's probability (no rank-level factor)
@@ -368,7 +400,7 @@ class RankState:
                 self.flat_cdf = t.zeros(max(self.n), dtype=t.float64, device=self.dev)
                 self.flat_mass = t.zeros(1, dtype=t.float64, device=self.dev)
             if n > 0:
-                ops.arls_build(self.U[i], self.M, self.flat_dist[:n], self.flat_cdf[:n],
+                ops.arls_build(self.U[i], M, self.flat_dist[:n], self.flat_cdf[:n],
                                self.flat_mass)
             else:
                 self.flat_mass.zero_()
@@ -383,10 +415,12 @@ class RankState:
             return
         if self.n[i] > 0:
             fused = self.P == 1   # the walk folds U rows into the Hadamard rows itself
-            ops.sts_walk(self.local_tree(i), self.U[i], self.leaf_of(i), self.lo[i], self.M, H_in,
+            self.walk_ws = ops.sts_walk_ws(self.J, self.n[i], self.leaf_of(i), self.R, self.walk_ws,
+                                            owned=True)
+            ops.sts_walk(self.local_tree(i), self.U[i], self.leaf_of(i), self.lo[i], M, H_in,
                          self.J, key, override if self.P == 1 else None, rin, sel, self.rank,
                          self.X[i], self.pmp[i], self.resid, hkey=hk, key_bits=kb,
-                         H_out=self.H_alt if fused else None)
+                         H_out=self.H_alt if fused else None, ws=self.walk_ws, gm_ready=gm_ready)
             if fused:
                 self.H, self.H_alt = self.H_alt, self.H
 
@@ -537,11 +571,13 @@ class Cluster:
             r.pmp[k].fill_(1.0)
         if self.sampler == "sts":
             walked = [i for i in range(N) if i != k]
-            if self.P == 1 and override is None:
-                walked = walked[1:]   # the first constant mode is a flat draw at P = 1
+            if self.P > 1 or override is None:
+                walked = walked[1:]   # the first constant mode is a flat draw / flat local search
             for r in self.ranks:
                 r.prefetch_trees(walked)
                 r.chain(k)
+                if walked:
+                    r.prefetch_gm(walked[0], k)
             first = True
             for i in range(N):
                 if i == k:

@@ -124,12 +124,31 @@ class Ops:
         self._c("rcp_sts_cond", ptr(chain_pinv), ptr(grams), N, int(i), int(k), R, ptr(out),
                 stream_handle())
 
+    def sts_walk_ws(self, J, n, leaf, R, ws=None, owned=False):
+        """The walk workspace: the device-wide one, or with owned=True a caller-owned buffer
+        (`ws`, allocated when None and grown when too small; several rank states share one
+        device object, and a prefetched conditioning pass must not be overwritten by
+        another rank's)."""
+        need = int(self.lib.rcp_sts_walk_ws_bytes(int(J), int(n), int(leaf), int(R)))
+        if not owned:
+            return self.ws("sts_walk", need)
+        if ws is None or ws.numel() < need:
+            ws = empty(need, torch().uint8, self.dev)
+        return ws
+
+    def sts_walk_gm(self, tree, n, leaf, M, J, ws):
+        """The walk's conditioning pass into `ws` (see rcp_sts_walk_gm)."""
+        R = M.shape[0]
+        self._c("rcp_sts_walk_gm", ptr(tree), int(n), R, int(leaf), ptr(M), int(J), ptr(ws),
+                ws.numel(), stream_handle())
+
     def sts_walk(self, tree, U, leaf, row_lo, M, H_in, J, key, override, rin, sel, sel_value,
-                 Xi, pmp_i, resid, hkey=None, key_bits=64, H_out=None):
+                 Xi, pmp_i, resid, hkey=None, key_bits=64, H_out=None, ws=None, gm_ready=False):
         n, R = U.shape
-        w = self.ws("sts_walk", self.lib.rcp_sts_walk_ws_bytes(int(J), n, int(leaf), R))
+        w = ws if ws is not None else self.sts_walk_ws(J, n, leaf, R)
         k0, k1, dk = _key_args(key)
-        self._c("rcp_sts_walk", ptr(tree), ptr(U), n, R, int(leaf), int(row_lo), ptr(M),
+        self._c("rcp_sts_walk_prepared" if gm_ready else "rcp_sts_walk", ptr(tree), ptr(U), n, R,
+                int(leaf), int(row_lo), ptr(M),
                 ptr(H_in), ptr(hkey), int(key_bits), int(J), k0, k1, dk, ptr(override), ptr(rin),
                 ptr(sel),
                 int(sel_value), ptr(Xi), ptr(pmp_i), ptr(resid), ptr(H_out), ptr(w), w.numel(),

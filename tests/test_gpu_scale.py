@@ -2,7 +2,7 @@
 oracle (oracle/, pinned to the reference by tests/test_oracle_golden.py):
 
 * C2 (4-mode 183x24x1140x1717, 3.3M Zipf nonzeros, STS-CP R=25, J=65536): two full ALS
-  rounds through run_als — every sampled batch bit-exact, factors within 1e-9, fit within
+  rounds through run_als (and one round on four ranks) — every sampled batch bit-exact, factors within 1e-9, fit within
   1e-6 (ref als.py:141-218, schedules.py:227-258);
 * C3 (77M nonzeros, R=50, J=65536): the fused sampled MTTKRP of a real device batch against
   the oracle's gather + downsampled MTTKRP (ref mttkrp.py:131-189) on the same samples —
@@ -31,7 +31,11 @@ def rel_err(a, b):
     return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
 
 
-def test_c2_two_rounds_match_oracle():
+@pytest.mark.parametrize("procs,rounds", [(1, 2), (4, 1)])
+def test_c2_rounds_match_oracle(procs, rounds):
+    """procs = 4: the multi-rank path at scale (grouped rank-level walk over ~10^4 groups,
+    local flat search of the first constant mode, fused exchange) against the oracle run
+    on the same processor grid."""
     import torch
     import bench
     import paper_2210_05105_b200 as P
@@ -41,12 +45,13 @@ def test_c2_two_rounds_match_oracle():
     del idx_d, vals_d
     dims, R, J = c["dims"], c["R"], c["J"]
     t = P.SparseTensorCOO(dims, idx, vals)
-    cfg = P.AlsConfig(rank=R, rounds=2, sampler="sts", samples=J,
-                      schedule="accumulator-stationary", seed=11, fit_every=2,
+    cfg = P.AlsConfig(rank=R, rounds=rounds, sampler="sts", samples=J,
+                      schedule="accumulator-stationary", procs=procs, seed=11, fit_every=rounds,
                       record_samples=True, permute=False)
     res = P.run_als(cfg, tensor=t)
-    st, fits = O.run_as(dims, idx, vals, R, "sts", J, 2, seed=11, workers=os.cpu_count() or 1)
-    assert len(res.sample_log) == len(st.sample_log) == 8
+    st, fits = O.run_as(dims, idx, vals, R, "sts", J, rounds, seed=11, P=procs,
+                        workers=os.cpu_count() or 1)
+    assert len(res.sample_log) == len(st.sample_log) == 4 * rounds
     for i, (a, b) in enumerate(zip(res.sample_log, st.sample_log)):
         assert np.array_equal(a, b), "solve %d" % i
     for j in range(len(dims)):

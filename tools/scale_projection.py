@@ -39,10 +39,10 @@ from paper_2210_05105_b200.engine import make_local_cluster  # noqa: E402
 BUS_GBS = float(os.environ.get("BUS_GBS", "350"))     # all-reduce / all-gather bus bandwidth
 LAT_US = float(os.environ.get("LAT_US", "15"))        # per-collective launch + sync latency
 
-RANK_METHODS = ("prefetch_trees", "chain", "sts_mode", "fold_urow", "arls_draw", "arls_fold",
+RANK_METHODS = ("prefetch_trees", "prefetch_gm", "chain", "sts_mode", "fold_urow", "arls_draw", "arls_fold",
                 "weights", "sketched_system", "mttkrp", "update", "renormalize", "block_gram",
                 "set_gram", "build_tree", "arls_local")
-SIDE = ("sketched_system", "prefetch_trees")   # overlapped work at P = 1 (side streams)
+SIDE = ("sketched_system", "prefetch_trees", "prefetch_gm")   # overlapped work at P = 1 (side streams)
 
 
 class Recorder:
