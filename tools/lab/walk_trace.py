@@ -19,7 +19,7 @@ import bench  # noqa: E402
 from paper_2210_05105_b200.engine import make_local_cluster  # noqa: E402
 
 dev = torch.device("cuda", 0)
-c, idx, vals = bench.make_tensor("c3", 0, dev)
+c, idx, vals = bench.make_tensor(os.environ.get("CFG", "c3"), 0, dev)
 cl = make_local_cluster(c["dims"], idx, vals, c["R"], c["J"], "sts", 0)
 me = cl.ranks[0]
 for r in range(1, 4):
@@ -36,7 +36,10 @@ def hook(tree, U, leaf, *a, **kw):
     J = a[3]
     total = lib.rcp_sts_walk_ws_bytes(int(J), U.shape[0], int(leaf), U.shape[1])
     o = total - 256 - 64 * (KMAX + 2)
-    t = ops._ws["sts_walk"][o:o + 64 * (KMAX + 2)].view(torch.int64).cpu().tolist()
+    ws = kw.get("ws")
+    if ws is None:
+        ws = ops._ws["sts_walk"]
+    t = ws[o:o + 64 * (KMAX + 2)].view(torch.int64).cpu().tolist()
     print("walk n=%d" % U.shape[0])
     for l in range(KMAX):
         if t[2 * l] == 0:
