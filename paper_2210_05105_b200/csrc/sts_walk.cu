@@ -86,8 +86,9 @@ constexpr size_t kCtlBytes = sizeof(int) * (kGenBase + kMaxDepth + 8);
 
 struct Run {
   int32_t lo, hi;      // positions [lo, hi) in the level's (r, sample) buffer
-  int32_t level;       // tree level of `node`
-  int32_t node;        // node index within its level
+  int32_t hrow;        // a sample of the run's group: the row of H all its samples share
+  int32_t node;        // node index within its level (the level is the pass's: runs are
+                       // processed level-synchronously)
   double prob;         // product of the step probabilities so far
   double qv;           // h'(G_node (.) M)h when known (left children inherit it), else NaN
 };
@@ -227,7 +228,7 @@ __global__ void walk_seed_kernel(const int64_t *__restrict__ key, const int32_t 
     Run rr;
     rr.lo = (int32_t)(s + (int64_t)q * kMaxRun);
     rr.hi = (int32_t)min(lo, s + (int64_t)(q + 1) * kMaxRun);
-    rr.level = 0;
+    rr.hrow = idx[s];
     rr.node = 0;
     rr.prob = prob;
     rr.qv = __longlong_as_double(0x7ff8000000000000LL);   // unknown
@@ -309,15 +310,14 @@ struct Stage {
 __device__ __forceinline__ void push_child(Run *runs, int *gen_cnt, int64_t base, int64_t cap,
                                            int *status, Stage &stg, const Run &par, int32_t lo,
                                            int32_t hi, double T, bool right, double qv, int depth,
-                                           int lane) {
-  const int lev = par.level;
+                                           int lev, int lane) {
   const int32_t chunk = (lev + 1 == depth) ? kLeafChunk : kMaxRun;
   for (int32_t c0 = lo; c0 < hi; c0 += chunk) {
     if (lane == 0) {
       Run c;
       c.lo = c0;
       c.hi = min(hi, c0 + chunk);
-      c.level = lev + 1;
+      c.hrow = par.hrow;
       c.node = 2 * par.node + (right ? 1 : 0);
       c.prob = par.prob * (right ? (1.0 - T) : T);
       c.qv = qv;
@@ -458,10 +458,10 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
       const unsigned long long tr0 = gtime();
 #endif
       const Run run = runs[t];
-      const int32_t lo = run.lo, hi = run.hi, level = run.level;
+      const int32_t lo = run.lo, hi = run.hi, level = lvl;
       const double *rs = (level & 1) ? rB : rA;
       const int32_t *is = (level & 1) ? iB : iA;
-      const int32_t s0 = is[lo];
+      const int32_t s0 = run.hrow;   // no dependent load of the run's first sample
 #ifdef RCP_WALK_TRACE
       const unsigned long long tr1 = gtime();
 #endif
@@ -555,10 +555,10 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         const double unknown = __longlong_as_double(0x7ff8000000000000LL);
         if (nl > 0)
           push_child(runs, gen_cnt, end, cap_runs, status, stg, run, lo, lo + nl, T, false, qL, depth,
-                     lane);
+                     level, lane);
         if (nr > 0)
           push_child(runs, gen_cnt, end, cap_runs, status, stg, run, lo + nl, hi, T, true, unknown,
-                     depth, lane);
+                     depth, level, lane);
 #ifdef RCP_WALK_TRACE
         if (lane == 0) {
           const unsigned long long tr4 = gtime();
