@@ -41,6 +41,12 @@ CONFIGS = {
     "c5": dict(dims=(8_200_000, 177_000, 8_100_000), nnz=4_700_000_000, R=100, J=131072,
                rounds=1, samplers=("sts",), kind="zipf_device", s=1.1, values="log1p_poisson",
                draws=9_120_000_000, parts=32),
+    # C5's shape, rank and sample count at one eighth of its draws: the share of the tensor
+    # one of eight GPUs holds, sized for a single B200 (C5 itself needs 169 GB of stores);
+    # exercises the R = 100, J = 131072, 8M-row paths at scale
+    "c5s": dict(dims=(8_200_000, 177_000, 8_100_000), nnz=780_000_000, R=100, J=131072,
+                rounds=1, samplers=("sts",), kind="zipf_device", s=1.1, values="log1p_poisson",
+                draws=1_140_000_000, parts=8),
 }
 
 
