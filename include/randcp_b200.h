@@ -385,6 +385,15 @@ int rcp_zipf_draws(int N, const int64_t *h_dims, const double *const *h_cdf,
                    int chunk_bits, int64_t d0, int64_t d1, int value_kind, double sigma,
                    int part_bits, int64_t part, int64_t *d_key, double *d_val, int64_t *d_count,
                    int64_t cap, int *d_status, void *stream);
+/* Stable (key, row) ordering for the per-mode sorted store and the drop-in CSR transpose:
+ * d_order = the permutation numpy's lexsort((row, key)) returns (ref matricization.py:56-77),
+ * by two LSD radix sorts that carry positions; d_key == NULL orders by d_row alone (the
+ * counting-sort transpose of ref mttkrp.py:131-155).  Values must lie in [0, key_max] and
+ * [0, row_max].  Workspace: rcp_sort_ws_bytes(n). */
+size_t rcp_sort_ws_bytes(int64_t n);
+int rcp_order_by_key_row(const int64_t *d_key, const int64_t *d_row, int64_t n, int64_t key_max,
+                         int64_t row_max, int64_t *d_order, void *d_ws, size_t ws_bytes,
+                         void *stream);
 /* d_flag[i] = 1 where sorted cell ids start a new cell. */
 int rcp_run_flags(const int64_t *d_sorted, int64_t n, int32_t *d_flag, void *stream);
 /* Distinct cells from stably sorted draws: values summed in draw order (ln(1 + sum) when

@@ -98,6 +98,8 @@ _SIGS = {
     "rcp_zipf_guide": (_i32, [_vp, _i64, _i64, _vp, _vp]),
     "rcp_zipf_draws": (_i32, [_i32, _vp, _vp, _vp, _vp, _u64, _i32, _i64, _i64, _i32, _f64, _i32,
                               _i64, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "rcp_sort_ws_bytes": (_sz, [_i64]),
+    "rcp_order_by_key_row": (_i32, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _sz, _vp]),
     "rcp_run_flags": (_i32, [_vp, _i64, _vp, _vp]),
     "rcp_cells": (_i32, [_vp, _vp, _vp, _i64, _i64, _i32, _vp, _vp, _i32, _vp, _vp, _vp]),
     "rcp_exact_mttkrp": (_i32, [_vp, _vp, _i64, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp, _vp,

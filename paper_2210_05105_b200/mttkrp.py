@@ -65,7 +65,7 @@ def gather_sampled_nonzeros_to_csr(mat: Matricization, X, k) -> SampledCsr:
     co = t.empty(nnz, dtype=t.int64, device=dev)
     vo = t.empty(nnz, dtype=t.float64, device=dev)
     ops.fiber_expand(lo, off, st, ro, co, vo)
-    order = t.sort(ro, stable=True).indices          # the counting-sort "sparse transpose"
+    order = ops.order_by_key_row(None, ro, 0, n_rows - 1)   # the counting-sort "sparse transpose"
     ro = ro[order]
     rp = t.zeros(n_rows + 1, dtype=t.int64, device=dev)
     t.cumsum(t.bincount(ro, minlength=n_rows), 0, out=rp[1:])

@@ -340,6 +340,20 @@ class Ops:
                 int(part), ptr(keys), ptr(vals), ptr(count), keys.numel(), self.status.ptr,
                 stream_handle())
 
+    def order_by_key_row(self, key, row, key_max, row_max):
+        """Positions in (key, row) order, stable (key None: by row alone).  The workspace is
+        released after the call: store builds order up to 10^8 entries at a time."""
+        t = torch()
+        n = row.numel()
+        order = empty(n, t.int64, self.dev)
+        if n == 0:
+            return order
+        nb = self.lib.rcp_sort_ws_bytes(n)
+        w = empty(nb, t.uint8, self.dev)
+        self._c("rcp_order_by_key_row", ptr(key) if key is not None else None, ptr(row), n,
+                int(key_max), int(row_max), ptr(order), ptr(w), nb, stream_handle())
+        return order
+
     def run_flags(self, sorted_keys, flag):
         self._c("rcp_run_flags", ptr(sorted_keys), sorted_keys.numel(), ptr(flag),
                 stream_handle())

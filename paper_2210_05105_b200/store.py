@@ -96,11 +96,14 @@ def build_store(dims, idx, vals, mode, row_lo=0, row_hi=None):
     if int(rows.min()) < row_lo or int(rows.max()) >= row_hi:
         raise ValueError("entry rows outside block [%d, %d)" % (row_lo, row_hi))
     key = column_keys_dev(idx, dims, mode)
-    # (key, row) order: stable sort by row, then stable sort by key
-    o1 = t.sort(rows, stable=True).indices
-    o2 = t.sort(key[o1], stable=True).indices
-    order = o1[o2]
-    del o1, o2
+    # (key, row) order: stable radix sort by row, then by key (csrc/sort.cu)
+    span = 1
+    for m, d in enumerate(dims):
+        if m != mode:
+            span *= d
+    rows = rows.contiguous()
+    from .ops import ops_for
+    order = ops_for(dev).order_by_key_row(key, rows, span - 1, dims[mode] - 1)
     skeys = key[order]
     del key
     ukeys, counts = t.unique_consecutive(skeys, return_counts=True)
@@ -133,6 +136,8 @@ def build_store_chunks(dims, chunks, mode, row_lo=0, row_hi=None, buckets=16):
             span *= dims[m]
     dev = chunks[0][0].device if chunks else t.device("cuda", 0)
     B = max(1, int(buckets))
+    from .ops import ops_for
+    _ops = ops_for(dev)
 
     def keyed(idx, vals):
         rows = idx[:, mode].long()
@@ -168,10 +173,7 @@ def build_store_chunks(dims, chunks, mode, row_lo=0, row_hi=None, buckets=16):
         n = fk.numel()
         if n == 0:
             continue
-        o1 = t.sort(rows, stable=True).indices
-        o2 = t.sort(fk[o1], stable=True).indices
-        order = o1[o2]
-        del o1, o2
+        order = _ops.order_by_key_row(fk, rows.contiguous(), span - 1, dims[mode] - 1)
         out_rows[off:off + n] = (rows[order] - row_lo).to(t.int32)
         out_vals[off:off + n] = vals[order]
         uk, c = t.unique_consecutive(fk[order], return_counts=True)
