@@ -874,6 +874,147 @@ int launch_gram_split(const double *U, const double *scale, int64_t n, int R, do
   return RCP_OK;
 }
 
+// 64 < R <= 128, staged: slabs of 32 rows go through a 3-stage cp.async ring in shared
+// memory (row stride 8T + 4 doubles: conflict-free fragment reads); warp w of the 8 owns the
+// tile pairs [w PPW, (w + 1) PPW) for every row of the CTA's slabs, so its accumulators stay
+// in registers and no partial is combined across warps.  Per 4-row step a warp reads the T
+// fragments from shared memory (T LDS per ~T(T+1)/16 mma) instead of every warp of a group
+// re-reading the rows from L1/L2.  Slabs go to CTAs round-robin, CTA partials are combined
+// by sum_partials: deterministic.
+constexpr int kGsRows = 32;
+constexpr int kGsStages = 3;
+
+template <int T>
+__host__ __device__ constexpr int gs_stride() { return 8 * T + 4; }
+
+template <int T>
+size_t gram_staged_smem() {
+  const size_t ring = (size_t)kGsStages * (kGsRows * gs_stride<T>() + kGsRows);
+  const size_t red = (size_t)(T * (T + 1) / 2) * 64;
+  return sizeof(double) * (ring > red ? ring : red);
+}
+
+template <int T, int g>
+__device__ __forceinline__ void gram_staged_body(const double *ring, const double *sc, bool scaled,
+                                                 int lane, double (&acc)[(T * (T + 1) / 2 + 7) / 8][2]) {
+  constexpr int ST = gs_stride<T>();
+  const int kk = lane & 3, col = lane >> 2;
+#pragma unroll 2
+  for (int j = 0; j < kGsRows / 4; ++j) {
+    const double *row = ring + (4 * j + kk) * ST + col;
+    const double w = scaled ? sc[4 * j + kk] : 1.0;
+    double f[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) f[t] = row[8 * t] * w;
+    gram_accum_group<T, 8, g>(f, acc);
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(256, 1)
+gram_mma_staged_kernel(const double *__restrict__ U, const double *__restrict__ scale, int64_t n, int R,
+                       double *__restrict__ part) {
+  constexpr int NP = T * (T + 1) / 2;
+  constexpr int PPW = (NP + 7) / 8;
+  constexpr int ST = gs_stride<T>();
+  constexpr int SLAB = kGsRows * ST + kGsRows;   // rows, then the 32 row scales
+  extern __shared__ double sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool scaled = scale != nullptr;
+  double acc[PPW][2];
+#pragma unroll
+  for (int p = 0; p < PPW; ++p) acc[p][0] = acc[p][1] = 0.0;
+  // pad columns are never written by the copies
+  for (int e = threadIdx.x; e < kGsStages * kGsRows * (ST - R); e += blockDim.x) {
+    const int st = e / (kGsRows * (ST - R)), q = e - st * (kGsRows * (ST - R));
+    const int r = q / (ST - R), c = R + (q - r * (ST - R));
+    sm[st * SLAB + r * ST + c] = 0.0;
+  }
+  const int64_t slabs = (n + kGsRows - 1) / kGsRows;
+  const int crow = threadIdx.x >> 3, c0 = threadIdx.x & 7;   // 8 threads per row
+  auto issue = [&](int64_t sl, int st) {
+    if (sl < slabs) {
+      const int64_t r = sl * kGsRows + crow;
+      const bool ok = r < n;
+      const double *src = U + (ok ? r : 0) * (int64_t)R;
+      double *dst = sm + st * SLAB + crow * ST;
+      for (int c = c0; c < R; c += 8) cpa8_zfill(dst + c, src + c, ok);
+      if (scaled && c0 == 0) cpa8_zfill(sm + st * SLAB + kGsRows * ST + crow, scale + (ok ? r : 0), ok);
+    }
+    cpa_commit();
+  };
+  int64_t sl = blockIdx.x;
+  issue(sl, 0);
+  issue(sl + gridDim.x, 1);
+  int st = 0;
+  for (; sl < slabs; sl += gridDim.x) {
+    cpa_wait<1>();
+    __syncthreads();   // the slab is visible; every warp is done with the stage refilled next
+    issue(sl + 2 * (int64_t)gridDim.x, st == 0 ? 2 : st - 1);
+    const double *ring = sm + st * SLAB;
+    const double *sc = ring + kGsRows * ST;
+    switch (wid) {
+      case 0: gram_staged_body<T, 0>(ring, sc, scaled, lane, acc); break;
+      case 1: gram_staged_body<T, 1>(ring, sc, scaled, lane, acc); break;
+      case 2: gram_staged_body<T, 2>(ring, sc, scaled, lane, acc); break;
+      case 3: gram_staged_body<T, 3>(ring, sc, scaled, lane, acc); break;
+      case 4: gram_staged_body<T, 4>(ring, sc, scaled, lane, acc); break;
+      case 5: gram_staged_body<T, 5>(ring, sc, scaled, lane, acc); break;
+      case 6: gram_staged_body<T, 6>(ring, sc, scaled, lane, acc); break;
+      default: gram_staged_body<T, 7>(ring, sc, scaled, lane, acc); break;
+    }
+    st = st == kGsStages - 1 ? 0 : st + 1;
+  }
+  cpa_wait<0>();
+  __syncthreads();
+  double *red = sm;   // NP x 64, each pair written by its one owner
+#pragma unroll
+  for (int p = 0; p < PPW; ++p) {
+    const int gp = wid * PPW + p;
+    if (gp < NP) {
+      red[gp * 64 + 2 * lane] = acc[p][0];
+      red[gp * 64 + 2 * lane + 1] = acc[p][1];
+    }
+  }
+  __syncthreads();
+  double *out = part + (int64_t)blockIdx.x * R * R;
+  for (int e = threadIdx.x; e < NP * 64; e += blockDim.x) {
+    int p = e >> 6, a = 0;
+    while (p >= T - a) {
+      p -= T - a;
+      ++a;
+    }
+    const int b = a + p;
+    const int ln = (e & 63) >> 1, u = e & 1;
+    const int ga = 8 * a + (ln >> 2), gb = 8 * b + 2 * (ln & 3) + u;
+    if (ga < R && gb < R) {
+      out[ga * R + gb] = red[e];
+      out[gb * R + ga] = red[e];
+    }
+  }
+}
+
+template <int T>
+int launch_gram_staged(const double *U, const double *scale, int64_t n, int R, double *part, int &grid,
+                       cudaStream_t st) {
+  const int smem = (int)gram_staged_smem<T>();
+  static int per_sm = 0;
+  if (!per_sm) {
+    RCP_CUDA_TRY(cudaFuncSetAttribute(gram_mma_staged_kernel<T>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    RCP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gram_mma_staged_kernel<T>, 256,
+                                                               smem));
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t slabs = (n + kGsRows - 1) / kGsRows;
+  int g = per_sm * sm_count();
+  if (g > grid) g = grid;   // the partial buffer holds gram_grid(n) matrices
+  if (slabs < g) g = (int)slabs;
+  grid = g < 1 ? 1 : g;
+  gram_mma_staged_kernel<T><<<grid, 256, smem, st>>>(U, scale, n, R, part);
+  return RCP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -891,7 +1032,7 @@ int rcp_gram(const double *d_U, const double *d_scale, int64_t n, int R, double 
     RCP_CUDA_TRY(cudaMemsetAsync(d_G, 0, sizeof(double) * R * R, st));
     return RCP_OK;
   }
-  const int grid = gram_grid(n);
+  int grid = gram_grid(n);
   const size_t smem = gram_smem(R);
   static bool attr = false;
   if (!attr) {
@@ -917,6 +1058,20 @@ int rcp_gram(const double *d_U, const double *d_scale, int64_t n, int R, double 
       case 7: gram_mma_kernel<7><<<grid, 256, 0, st>>>(d_U, d_scale, n, R, part); break;
       default: gram_mma_kernel<8><<<grid, 256, 0, st>>>(d_U, d_scale, n, R, part); break;
     }
+  } else if (getenv_flag("RCP_GRAM_SPLIT") == 0 && getenv_flag("RCP_GRAM_FFMA") == 0) {
+    // 64 < R <= 128: fp64 tensor cores over shared-memory staged slabs
+    int rc = RCP_OK;
+    switch ((R + 7) / 8) {
+      case 9: rc = launch_gram_staged<9>(d_U, d_scale, n, R, part, grid, st); break;
+      case 10: rc = launch_gram_staged<10>(d_U, d_scale, n, R, part, grid, st); break;
+      case 11: rc = launch_gram_staged<11>(d_U, d_scale, n, R, part, grid, st); break;
+      case 12: rc = launch_gram_staged<12>(d_U, d_scale, n, R, part, grid, st); break;
+      case 13: rc = launch_gram_staged<13>(d_U, d_scale, n, R, part, grid, st); break;
+      case 14: rc = launch_gram_staged<14>(d_U, d_scale, n, R, part, grid, st); break;
+      case 15: rc = launch_gram_staged<15>(d_U, d_scale, n, R, part, grid, st); break;
+      default: rc = launch_gram_staged<16>(d_U, d_scale, n, R, part, grid, st); break;
+    }
+    if (rc) return rc;
   } else if (R <= 96 && getenv_flag("RCP_GRAM_FFMA") == 0) {
     // 64 < R <= 96: fp64 tensor cores with the tile pairs split over warp groups (C4 R=75 on
     // 4.8M rows: 3.15 ms vs 4.03 ms FFMA; above 96 the G=8 split is load-bound and the FFMA

@@ -54,6 +54,10 @@ constexpr int32_t kMaxRun = 256;
 #define RCP_WALK_MIN_BLOCKS 2
 #endif
 constexpr int kWalkUnroll = RCP_WALK_UNROLL;
+#ifndef RCP_WALK_UNROLL_BIG
+#define RCP_WALK_UNROLL_BIG 16
+#endif
+constexpr int kWalkUnrollBig = RCP_WALK_UNROLL_BIG;
 // Diagnostics (per-level finish times, sample counters): off in the product build, where
 // they cost same-address global atomics per sample, run and CTA; tools/lab/walk_trace.py
 // builds with -DRCP_WALK_PROF=1.
@@ -147,6 +151,11 @@ __host__ __device__ __forceinline__ size_t walk_per_warp(int R) {
   const size_t zb = (size_t)8 * mma_zs(R);
   const size_t w = (size_t)R + zb + kMaxLeaf;
   return (w + 1) & ~(size_t)1;
+}
+
+// The inner levels alone need the run's Hadamard row only.
+__host__ __device__ __forceinline__ size_t walk_per_warp_inner(int R) {
+  return ((size_t)R + 1) & ~(size_t)1;
 }
 
 // Block-shared doubles: the full padded M (mma path) or packed M' (fallback).
@@ -373,7 +382,17 @@ __device__ __forceinline__ void fail_run(int32_t lo, int32_t hi, const int32_t *
   }
 }
 
-__global__ void __launch_bounds__(kWalkWarps * 32, RCP_WALK_MIN_BLOCKS)
+// kMinB / kUn: resident CTAs per SM the register budget is set for, and node loads in flight
+// per lane in the child-mass loop.  <RCP_WALK_MIN_BLOCKS, kWalkUnroll> where shared memory lets
+// two CTAs share an SM (R <= 64: node tables mostly L2-resident); <1, kWalkUnrollBig> above,
+// where one CTA fits anyway and the 10^1 KB node tables of million-row trees stream from HBM:
+// twice the registers buy twice the loads in flight (same FMA order, same results).
+// kPhase: 0 = every level in one launch; 1 = the inner levels only, with the slim shared
+// layout (h rows and the pair table: no M, no leaf tile), so that at R > 64 two CTAs still
+// share an SM while the walk is bound by the latency chain of each run; 2 = the leaf level
+// alone (full layout), started from the level extents phase 1 left in the control words.
+template <int kMinB, int kUn, int kPhase>
+__global__ void __launch_bounds__(kWalkWarps * 32, kMinB)
 walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, int64_t n, int R,
                  int leaf, int depth, int64_t row_lo,
                  const double *__restrict__ Mfull,
@@ -388,17 +407,21 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
   const int Rs = tri_stride(R);                    // even node stride (zero pad)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int Rn = mma_rn(R), Zs = mma_zs(R), Ms = mma_ms(R);
-  const size_t bd = walk_block_doubles(R);
+  const size_t bd = kPhase == 1 ? 0 : walk_block_doubles(R);
   double *Mp = sh;                                 // full M, zero-padded to Rn x Ms
-  double *hv = sh + bd + (size_t)wid * walk_per_warp(R);   // R: the run's Hadamard row
+  // R: the run's Hadamard row
+  double *hv = sh + bd + (size_t)wid * (kPhase == 1 ? walk_per_warp_inner(R) : walk_per_warp(R));
   double *zb = hv + R;                             // leaf rows (.) h
   double *mass = zb + 8 * Zs;                      // leaf
-  uint32_t *pairs = reinterpret_cast<uint32_t *>(sh + bd + (size_t)nw * walk_per_warp(R));
-  for (int e = threadIdx.x; e < Rs; e += blockDim.x) pairs[e] = pairs_g[e];
-  for (int e = threadIdx.x; e < Rn * Ms; e += blockDim.x) {
-    const int k = e / Ms, c = e - k * Ms;
-    Mp[e] = (k < R && c < R) ? Mfull[k * R + c] : 0.0;
-  }
+  uint32_t *pairs = reinterpret_cast<uint32_t *>(
+      sh + bd + (size_t)nw * (kPhase == 1 ? walk_per_warp_inner(R) : walk_per_warp(R)));
+  if (kPhase != 2)
+    for (int e = threadIdx.x; e < Rs; e += blockDim.x) pairs[e] = pairs_g[e];
+  if (kPhase != 1)
+    for (int e = threadIdx.x; e < Rn * Ms; e += blockDim.x) {
+      const int k = e / Ms, c = e - k * Ms;
+      Mp[e] = (k < R && c < R) ? Mfull[k * R + c] : 0.0;
+    }
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
   // Level-synchronous: the runs of level l are [begin, end); their children go to level
@@ -418,7 +441,17 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
 #endif
   if (threadIdx.x == 0) stg.count = 0;
   int64_t begin = 0, end = min((int64_t)ld_volatile(&ctl[0]), cap_runs);
-  for (int lvl = 0; lvl <= depth && end > begin; ++lvl) {
+  int lvl0 = 0;
+  if (kPhase == 2) {   // the leaf level's extent, as the inner levels' launch left it
+    while (lvl0 < depth && end > begin) {
+      const int64_t pushed_n = ld_volatile(&ctl[kGenBase + lvl0]);
+      begin = end;
+      end = min(end + pushed_n, cap_runs);
+      ++lvl0;
+    }
+    if (lvl0 < depth) return;   // an inner level ended without runs (grid-uniform)
+  }
+  for (int lvl = lvl0; lvl <= (kPhase == 1 ? depth - 1 : depth) && end > begin; ++lvl) {
     int *gen_cnt = &ctl[kGenBase + lvl];
     // this CTA's runs begin + blockIdx.x + k gridDim.x (spread over the level), claimed one
     // by one by its warps
@@ -470,7 +503,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
 #ifdef RCP_WALK_TRACE
       const unsigned long long tr2 = gtime();
 #endif
-      if (level < depth) {
+      if (kPhase != 2 && (kPhase == 1 || level < depth)) {
         // child masses <GM_child, h h^T> over the packed triangle, two positions per step
         // T = max(q_left, 0) / q_node (ref samplers.py:423-451).  q_node is inherited from
         // the parent by left children; right children and seeds compute it here, in the
@@ -485,7 +518,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
         double qL = 0.0, qV = 0.0, qL2 = 0.0, qV2 = 0.0;
         const int n2 = Rs / 2;
         if (known) {
-#pragma unroll (kWalkUnroll)
+#pragma unroll (kUn)
           for (int e = lane; e < n2; e += 32) {
             const double2 gl = __ldg(GL + e);
             const uint2 ab = PR[e];
@@ -495,7 +528,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
             qL2 = fma(gl.y, h1, qL2);
           }
         } else {
-#pragma unroll (kWalkUnroll)
+#pragma unroll (kUn)
           for (int e = lane; e < n2; e += 32) {
             const double2 gl = __ldg(GL + e);
             const double2 gv = __ldg(GV + e);
@@ -570,6 +603,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
 #endif
         continue;
       }
+      if (kPhase == 1) continue;   // (not reached: phase 1 ends above the leaf level)
       if (leaf_rank) {
         // ---- rank mode (the tree's leaves are ranks, ref samplers.py:423-451): every
         // sample of the run is finished by the rank owning the leaf; its residual and the
@@ -707,6 +741,11 @@ __global__ void fold_rows_kernel(double *__restrict__ out, const double *__restr
   for (int c = lane; c < R; c += 32) dst[c] = init ? src[c] : dst[c] * src[c];
 }
 
+size_t walk_smem_inner(int R, int warps) {
+  return sizeof(double) * ((size_t)warps * walk_per_warp_inner(R)) +
+         sizeof(uint32_t) * (size_t)tri_stride(R) + 64;
+}
+
 size_t walk_smem(int R, int warps) {
   return sizeof(double) * (walk_block_doubles(R) + (size_t)warps * walk_per_warp(R)) +
          sizeof(uint32_t) * (size_t)tri_stride(R) + 64;
@@ -806,15 +845,43 @@ int walk_impl(const double *d_tree, const double *d_U, int64_t n, int R, int lea
     const int rc = walk_gm_tables(d_tree, d_M, R, depth, Mp, pairs, gm, st);
     if (rc != RCP_OK) return rc;
   }
+  using WalkFn = void (*)(const double *, const double *, int64_t, int, int, int, int64_t, const double *,
+                          const uint32_t *, const double *, double *, double *, int32_t *, int32_t *,
+                          Run *, int *, int64_t, int64_t *, double *, double *, double *, int *,
+                          unsigned long long *, const int32_t *, int32_t *);
+  const WalkFn fn_all = walk_runs_kernel<RCP_WALK_MIN_BLOCKS, kWalkUnroll, 0>;
+  const WalkFn fn_all_big = walk_runs_kernel<1, kWalkUnrollBig, 0>;
+  const WalkFn fn_inner = walk_runs_kernel<RCP_WALK_MIN_BLOCKS, kWalkUnroll, 1>;
+  const WalkFn fn_leaf = walk_runs_kernel<1, kWalkUnrollBig, 2>;
   static bool attr = false;
   if (!attr) {
-    RCP_CUDA_TRY(cudaFuncSetAttribute(walk_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
+    for (WalkFn f : {fn_all, fn_all_big, fn_inner, fn_leaf})
+      RCP_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
+  // RCP_WALK_WIDE=0: never the wide-register / split variants (A/B runs)
+  static const int wide_ok = [] {
+    const char *e = getenv("RCP_WALK_WIDE");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
   int per_sm = 0;
-  RCP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_runs_kernel,
-                                                             warps * 32, smem));
+  RCP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn_all, warps * 32, smem));
+  // Shared memory admits one CTA of the full layout per SM (R > 64): the inner levels run
+  // as their own launch with the slim layout (two CTAs of 16 warps per SM again), the leaf
+  // level after it with the full one.
+  const bool split = wide_ok && per_sm <= 1 && depth >= 2;
+  WalkFn fn = fn_all, fn2 = nullptr;
+  int warps1 = warps;
+  size_t smem1 = smem;
+  if (split) {
+    fn = fn_inner;
+    fn2 = fn_leaf;
+    warps1 = kWalkWarps;
+    smem1 = walk_smem_inner(R, warps1);
+  } else if (wide_ok && per_sm <= 1) {
+    fn = fn_all_big;
+  }
+  RCP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, warps1 * 32, smem1));
   if (per_sm < 1) return RCP_ERR_ARG;
   // persistent: every CTA resident at once (workers wait on the shared queue)
   const int grid = per_sm * sm_count();
@@ -833,9 +900,17 @@ int walk_impl(const double *d_tree, const double *d_U, int64_t n, int R, int lea
                   (void *)&runs, (void *)&ctl,
                   (void *)&a_cap, (void *)&d_Xi, (void *)&d_pmp_i, (void *)&d_resid, (void *)&d_H_out,
                   (void *)&d_status, (void *)&a_prof, (void *)&d_leaf_rank, (void *)&d_owner};
-  RCP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)walk_runs_kernel, dim3(grid),
-                                           dim3(warps * 32), args, smem, st));
+  RCP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)fn, dim3(grid),
+                                           dim3(warps1 * 32), args, smem1, st));
   RCP_LAUNCH_CHECK("walk_runs");
+  if (fn2) {
+    int per_sm2 = 0;
+    RCP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, fn2, warps * 32, smem));
+    if (per_sm2 < 1) return RCP_ERR_ARG;
+    RCP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)fn2, dim3(per_sm2 * sm_count()),
+                                             dim3(warps * 32), args, smem, st));
+    RCP_LAUNCH_CHECK("walk_leaf");
+  }
   return RCP_OK;
 }
 

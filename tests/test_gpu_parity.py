@@ -60,6 +60,29 @@ def test_gram_and_pinv_full_rank(pkg, R):
     assert rel_err(Gp, O.sym_pinv(U.T @ U)) < 1e-9
 
 
+@pytest.mark.parametrize("R", [65, 72, 75, 97, 100, 127, 128])
+@pytest.mark.parametrize("n", [1, 31, 33, 40001])
+def test_gram_above_64_staged_slabs(pkg, R, n):
+    """64 < R <= 128: the shared-memory staged tensor-core Gram (dense.cu) over ragged slab
+    tails, several slabs per CTA, with and without row scales; deterministic run to run."""
+    import torch
+    from paper_2210_05105_b200.ops import ops_for
+    dev = torch.device("cuda", 0)
+    ops = ops_for(dev)
+    gen = np.random.default_rng(1000 * R + n)
+    U = gen.standard_normal((n, R))
+    sc = gen.uniform(0.5, 2.0, size=n)
+    Ud = torch.as_tensor(U, device=dev)
+    sd = torch.as_tensor(sc, device=dev)
+    G = ops.gram(Ud).cpu().numpy()
+    assert rel_err(G, U.T @ U) < 1e-13
+    assert np.array_equal(G, G.T)
+    Z = U * sc[:, None]
+    Gs = ops.gram(Ud, scale=sd).cpu().numpy()
+    assert rel_err(Gs, Z.T @ Z) < 1e-13
+    assert np.array_equal(ops.gram(Ud).cpu().numpy(), G)
+
+
 @pytest.mark.parametrize("R,rank", [(6, 3), (25, 10), (50, 49), (3, 0)])
 def test_pinv_rank_deficient_uses_cutoff(pkg, R, rank):
     gen = np.random.default_rng(7)
