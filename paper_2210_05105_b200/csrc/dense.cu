@@ -881,33 +881,11 @@ int launch_gram_split(const double *U, const double *scale, int64_t n, int R, do
 // fragments from shared memory (T LDS per ~T(T+1)/16 mma) instead of every warp of a group
 // re-reading the rows from L1/L2.  Slabs go to CTAs round-robin, CTA partials are combined
 // by sum_partials: deterministic.
-constexpr int kGsRows = 32;
-constexpr int kGsStages = 3;
-
-template <int T>
-__host__ __device__ constexpr int gs_stride() { return 8 * T + 4; }
-
 template <int T>
 size_t gram_staged_smem() {
   const size_t ring = (size_t)kGsStages * (kGsRows * gs_stride<T>() + kGsRows);
   const size_t red = (size_t)(T * (T + 1) / 2) * 64;
   return sizeof(double) * (ring > red ? ring : red);
-}
-
-template <int T, int g>
-__device__ __forceinline__ void gram_staged_body(const double *ring, const double *sc, bool scaled,
-                                                 int lane, double (&acc)[(T * (T + 1) / 2 + 7) / 8][2]) {
-  constexpr int ST = gs_stride<T>();
-  const int kk = lane & 3, col = lane >> 2;
-#pragma unroll 2
-  for (int j = 0; j < kGsRows / 4; ++j) {
-    const double *row = ring + (4 * j + kk) * ST + col;
-    const double w = scaled ? sc[4 * j + kk] : 1.0;
-    double f[T];
-#pragma unroll
-    for (int t = 0; t < T; ++t) f[t] = row[8 * t] * w;
-    gram_accum_group<T, 8, g>(f, acc);
-  }
 }
 
 template <int T>

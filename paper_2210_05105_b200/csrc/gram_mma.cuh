@@ -57,4 +57,29 @@ __device__ __forceinline__ void gram_accum_group(const double (&f)[T],
     }
 }
 
+// ---- shared-memory staged slabs (64 < R <= 128): 32 rows per slab, row stride 8T + 4
+// doubles (4 or 12 mod 16: the fragment reads of a half-warp hit 16 distinct double-banks);
+// warp g of 8 owns the tile pairs of group g (gram_accum_group<T, 8, g>).
+constexpr int kGsRows = 32;
+constexpr int kGsStages = 3;
+
+template <int T>
+__host__ __device__ constexpr int gs_stride() { return 8 * T + 4; }
+
+template <int T, int g>
+__device__ __forceinline__ void gram_staged_body(const double *ring, const double *sc, bool scaled,
+                                                 int lane, double (&acc)[(T * (T + 1) / 2 + 7) / 8][2]) {
+  constexpr int ST = gs_stride<T>();
+  const int kk = lane & 3, col = lane >> 2;
+#pragma unroll 2
+  for (int j = 0; j < kGsRows / 4; ++j) {
+    const double *row = ring + (4 * j + kk) * ST + col;
+    const double w = scaled ? sc[4 * j + kk] : 1.0;
+    double f[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) f[t] = row[8 * t] * w;
+    gram_accum_group<T, 8, g>(f, acc);
+  }
+}
+
 }  // namespace rcp

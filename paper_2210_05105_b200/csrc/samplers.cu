@@ -208,6 +208,11 @@ int getenv_leaf_ffma() {   // RCP_LEAF_FFMA=1: the FFMA leaf Grams for every R >
   return e && e[0] == '1' ? 1 : 0;
 }
 
+int getenv_leaf_split() {   // RCP_LEAF_SPLIT=1: not the staged leaf Grams (A/B)
+  const char *e = getenv("RCP_LEAF_SPLIT");
+  return e && e[0] == '1' ? 1 : 0;
+}
+
 __global__ void sts_leaf_kernel(const double *__restrict__ U, int64_t n, int R, int leaf,
                                 int64_t nleaves, double *__restrict__ level) {
   extern __shared__ double rows[];  // leaf x R, then the packed (a, b) table
@@ -349,6 +354,117 @@ sts_leaf_split_kernel(const double *__restrict__ U, int64_t n, int R, int leaf, 
     for (int e = grp * 32 + lane; e < Rs; e += 32 * G) out[e] = stage[e];
     asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * G) : "memory");
   }
+}
+
+// 64 < R <= 128, leaves of 32 or 64 rows: the staged form of the factor Gram (dense.cu).
+// A CTA takes whole leaves; their 32-row slabs go through a 3-stage cp.async ring, warp w of
+// the 8 owns the tile pairs of group w in registers and, after a leaf's last slab, writes
+// them into the leaf's packed node.  Same products in the same order as the register-split
+// and FFMA kernels: identical trees.
+template <int T, int g>
+__device__ __forceinline__ void leaf_staged_flush(double (&acc)[(T * (T + 1) / 2 + 7) / 8][2], int R,
+                                                  int lane, double *__restrict__ out) {
+  constexpr int NP = T * (T + 1) / 2;
+  constexpr int PPW = (NP + 7) / 8;
+  const int kk = lane & 3, col = lane >> 2;
+  int p = 0;
+#pragma unroll
+  for (int a = 0; a < T; ++a)
+#pragma unroll
+    for (int b = a; b < T; ++b) {
+      if (p >= g * PPW && p < (g + 1) * PPW) {
+        const int ga = 8 * a + col;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int gb = 8 * b + 2 * kk + u;
+          if (ga <= gb && gb < R) out[tri_index(ga, gb, R)] = acc[p - g * PPW][u];
+          acc[p - g * PPW][u] = 0.0;
+        }
+      }
+      ++p;
+    }
+}
+
+template <int T>
+__global__ void __launch_bounds__(256, 2)
+sts_leaf_staged_kernel(const double *__restrict__ U, int64_t n, int R, int leaf, int64_t nleaves,
+                       double *__restrict__ level) {
+  constexpr int NP = T * (T + 1) / 2;
+  constexpr int PPW = (NP + 7) / 8;
+  constexpr int ST = gs_stride<T>();
+  constexpr int SLAB = kGsRows * ST;
+  extern __shared__ double sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int Rt = R * (R + 1) / 2, Rs = tri_stride(R);
+  const int spl = leaf / kGsRows;   // slabs per leaf (1 or 2)
+  double acc[PPW][2];
+#pragma unroll
+  for (int p = 0; p < PPW; ++p) acc[p][0] = acc[p][1] = 0.0;
+  for (int e = threadIdx.x; e < kGsStages * kGsRows * (ST - R); e += blockDim.x) {
+    const int st = e / (kGsRows * (ST - R)), q = e - st * (kGsRows * (ST - R));
+    const int r = q / (ST - R), c = R + (q - r * (ST - R));
+    sm[st * SLAB + r * ST + c] = 0.0;
+  }
+  // this CTA's slabs, in order: leaf blockIdx.x + (q / spl) gridDim.x, part q % spl
+  const int64_t my_leaves = blockIdx.x < nleaves ? (nleaves - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t my_slabs = my_leaves * spl;
+  const int crow = threadIdx.x >> 3, c0 = threadIdx.x & 7;
+  auto issue = [&](int64_t q, int st) {
+    if (q < my_slabs) {
+      const int64_t v = blockIdx.x + (q / spl) * gridDim.x;
+      const int64_t r = v * leaf + (q % spl) * kGsRows + crow;
+      const bool ok = r < n;
+      const double *src = U + (ok ? r : 0) * (int64_t)R;
+      double *dst = sm + st * SLAB + crow * ST;
+      for (int c = c0; c < R; c += 8) cpa8_zfill(dst + c, src + c, ok);
+    }
+    cpa_commit();
+  };
+  issue(0, 0);
+  issue(1, 1);
+  int st = 0;
+  for (int64_t q = 0; q < my_slabs; ++q) {
+    cpa_wait<1>();
+    __syncthreads();
+    issue(q + 2, st == 0 ? 2 : st - 1);
+    const double *ring = sm + st * SLAB;
+    const bool last = (q % spl) == spl - 1;
+    double *out = level + (blockIdx.x + (q / spl) * gridDim.x) * (int64_t)Rs;
+    switch (wid) {
+#define RCP_LS(G_)                                                      \
+  case G_:                                                              \
+    gram_staged_body<T, G_>(ring, nullptr, false, lane, acc);           \
+    if (last) leaf_staged_flush<T, G_>(acc, R, lane, out);              \
+    break;
+      RCP_LS(0) RCP_LS(1) RCP_LS(2) RCP_LS(3) RCP_LS(4) RCP_LS(5) RCP_LS(6)
+      default:
+        gram_staged_body<T, 7>(ring, nullptr, false, lane, acc);
+        if (last) leaf_staged_flush<T, 7>(acc, R, lane, out);
+        break;
+#undef RCP_LS
+    }
+    if (last && Rs > Rt && threadIdx.x == 0) out[Rt] = 0.0;
+    st = st == kGsStages - 1 ? 0 : st + 1;
+  }
+  cpa_wait<0>();
+}
+
+template <int T>
+int launch_leaf_staged(const double *U, int64_t n, int R, int leaf, int64_t nleaves, double *lvl,
+                       cudaStream_t st) {
+  const int smem = (int)(sizeof(double) * kGsStages * kGsRows * gs_stride<T>());
+  static int per_sm = 0;
+  if (!per_sm) {
+    RCP_CUDA_TRY(cudaFuncSetAttribute(sts_leaf_staged_kernel<T>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    RCP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sts_leaf_staged_kernel<T>, 256,
+                                                               smem));
+    if (per_sm < 1) per_sm = 1;
+  }
+  int64_t g = (int64_t)per_sm * sm_count();
+  if (nleaves < g) g = nleaves;
+  sts_leaf_staged_kernel<T><<<(unsigned)g, 256, smem, st>>>(U, n, R, leaf, nleaves, lvl);
+  return RCP_OK;
 }
 
 __global__ void sts_zero_kernel(double *__restrict__ p, int64_t len) {
@@ -793,6 +909,21 @@ int rcp_sts_build(const double *d_U, int64_t n, int R, int leaf, double *d_tree,
     }
 #undef RCP_LEAF
     RCP_LAUNCH_CHECK("sts_leaf_mma");
+  } else if ((leaf == kGsRows || leaf == 2 * kGsRows) && !getenv_leaf_ffma() && !getenv_leaf_split()) {
+    // fp64 tensor cores over shared-memory staged slabs
+    int rc = RCP_OK;
+    switch ((R + 7) / 8) {
+      case 9: rc = launch_leaf_staged<9>(d_U, n, R, leaf, nleaves, lvl, st); break;
+      case 10: rc = launch_leaf_staged<10>(d_U, n, R, leaf, nleaves, lvl, st); break;
+      case 11: rc = launch_leaf_staged<11>(d_U, n, R, leaf, nleaves, lvl, st); break;
+      case 12: rc = launch_leaf_staged<12>(d_U, n, R, leaf, nleaves, lvl, st); break;
+      case 13: rc = launch_leaf_staged<13>(d_U, n, R, leaf, nleaves, lvl, st); break;
+      case 14: rc = launch_leaf_staged<14>(d_U, n, R, leaf, nleaves, lvl, st); break;
+      case 15: rc = launch_leaf_staged<15>(d_U, n, R, leaf, nleaves, lvl, st); break;
+      default: rc = launch_leaf_staged<16>(d_U, n, R, leaf, nleaves, lvl, st); break;
+    }
+    if (rc) return rc;
+    RCP_LAUNCH_CHECK("sts_leaf_staged");
   } else if (R <= 96 && !getenv_leaf_ffma()) {   // fp64 tensor cores, tile pairs split over warps
     const int T = (R + 7) / 8;
     const int G = 4, slots = 8 / G;

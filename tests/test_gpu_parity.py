@@ -83,6 +83,33 @@ def test_gram_above_64_staged_slabs(pkg, R, n):
     assert np.array_equal(ops.gram(Ud).cpu().numpy(), G)
 
 
+@pytest.mark.parametrize("R", [65, 75, 100, 104, 128])
+@pytest.mark.parametrize("n,leaf", [(1000, 64), (4097, 64), (96, 32), (4500, 32), (63, 64)])
+def test_sts_leaf_grams_above_64_staged(pkg, R, n, leaf, monkeypatch):
+    """64 < R <= 128, leaves of 32/64 rows: the staged tensor-core leaf Grams (samplers.cu)
+    write the packed tree of numpy's per-leaf U^T U (ragged last leaf, zero padding leaves),
+    bit-identical to the FFMA tree build (same products, same order)."""
+    import torch
+    from paper_2210_05105_b200.ops import ops_for
+    from paper_2210_05105_b200 import _lib
+    dev = torch.device("cuda", 0)
+    ops = ops_for(dev)
+    gen = np.random.default_rng(7 * R + n)
+    U = gen.standard_normal((n, R))
+    Ud = torch.as_tensor(U, device=dev)
+    tree = ops.sts_build(Ud, leaf).clone()
+    monkeypatch.setenv("RCP_LEAF_FFMA", "1")
+    ref = ops.sts_build(Ud, leaf).clone()
+    monkeypatch.delenv("RCP_LEAF_FFMA")
+    nd = int(_lib.lib().rcp_sts_tree_doubles(n, leaf, R))
+    assert torch.equal(tree[:nd], ref[:nd])
+    # the root is the packed upper triangle of U^T U
+    G = U.T @ U
+    iu = np.triu_indices(R)
+    root = tree[:R * (R + 1) // 2].cpu().numpy()
+    assert rel_err(root, G[iu]) < 1e-12
+
+
 @pytest.mark.parametrize("R,rank", [(6, 3), (25, 10), (50, 49), (3, 0)])
 def test_pinv_rank_deficient_uses_cutoff(pkg, R, rank):
     gen = np.random.default_rng(7)
