@@ -420,7 +420,9 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
   if (kPhase != 1)
     for (int e = threadIdx.x; e < Rn * Ms; e += blockDim.x) {
       const int k = e / Ms, c = e - k * Ms;
-      Mp[e] = (k < R && c < R) ? Mfull[k * R + c] : 0.0;
+      // leaf masses sum only the k-tiles at or above an n-tile's diagonal block: blocks
+      // above the diagonal carry 2 M (M is symmetric, like the nodes' packed M')
+      Mp[e] = (k < R && c < R) ? ((k >> 3) < (c >> 3) ? 2.0 * Mfull[k * R + c] : Mfull[k * R + c]) : 0.0;
     }
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
@@ -629,7 +631,9 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
       bool bad = nrow <= 0;
       double total_m = 0.0;
       if (!bad) {
-        // 8-row tiles: Y = Z M on the fp64 tensor cores, mass_q = <Y_q, Z_q>
+        // 8-row tiles: Y = Z M' on the fp64 tensor cores (M' = the block upper triangle of M
+        // with the off-diagonal blocks doubled: z'Mz over half the tile products),
+        // mass_q = <Y_q, Z_q>
         const int row = lane >> 2, quad = lane & 3;
         for (int q0 = 0; q0 < nrow; q0 += 8) {
           const int nb = min(8, nrow - q0);
@@ -642,7 +646,7 @@ walk_runs_kernel(const double *__restrict__ gm, const double *__restrict__ U, in
           double msum = 0.0;
           for (int nt = 0; nt < Rn; nt += 8) {
             double c0 = 0.0, c1 = 0.0;
-            for (int ks = 0; ks < Rn; ks += 4)
+            for (int ks = 0; ks < nt + 8; ks += 4)   // k-tiles <= this n-tile (upper blocks of M')
               dmma_8x8x4(c0, c1, zr[ks + quad], Mp[(ks + quad) * Ms + nt + row]);
             msum = fma(c0, zr[nt + 2 * quad], msum);
             msum = fma(c1, zr[nt + 2 * quad + 1], msum);
