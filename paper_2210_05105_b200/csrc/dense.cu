@@ -618,11 +618,7 @@ update_mma_kernel(const double *__restrict__ M, int64_t n, int R, const double *
     double a[KS];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) a[ks] = Ms[row * Ss + ks * 4 + quad];
-#pragma unroll
-    for (int nt = 0; nt < KS / 2; ++nt) {
-      double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) dmma_8x8x4(c0, c1, a[ks], Bs[(ks * 4 + quad) * Ss + nt * 8 + row]);
+    auto emit = [&](int nt, double c0, double c1) {
       const int col = nt * 8 + 2 * quad;
       if (row < nr) {
         if (col < R) {
@@ -636,6 +632,18 @@ update_mma_kernel(const double *__restrict__ M, int64_t n, int R, const double *
           if (!isfinite(c1)) bad = true;
         }
       }
+    };
+    // two n-tiles at a time: two independent accumulator chains per warp
+#pragma unroll
+    for (int nt = 0; nt < KS / 2; nt += 2) {
+      double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        dmma_8x8x4(c0, c1, a[ks], Bs[(ks * 4 + quad) * Ss + nt * 8 + row]);
+        if (nt + 1 < KS / 2) dmma_8x8x4(d0, d1, a[ks], Bs[(ks * 4 + quad) * Ss + (nt + 1) * 8 + row]);
+      }
+      emit(nt, c0, c1);
+      if (nt + 1 < KS / 2) emit(nt + 1, d0, d1);
     }
     __syncwarp();   // every lane is done with this slot before it is refilled
     slot = slot + 1 == nbuf ? 0 : slot + 1;

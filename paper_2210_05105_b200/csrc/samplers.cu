@@ -61,7 +61,10 @@ leverage_mma_kernel(const double *__restrict__ U, int64_t n, int R, const double
   double *zbase = sh + Rn * Zs + (size_t)wid * nbuf * 8 * Zs;   // this warp's nbuf tiles
   for (int e = threadIdx.x; e < Rn * Zs; e += blockDim.x) {
     const int a = e / Zs, b = e - a * Zs;
-    G[e] = (a < R && b < R) ? Gp[a * R + b] : 0.0;
+    // u'Gu over the 8x8 blocks at or above the diagonal only: the blocks above it carry 2 G
+    // (G symmetric: a pseudo-inverse or the walk's conditioning matrix), the ones below are
+    // never read
+    G[e] = (a < R && b < R) ? ((a >> 3) < (b >> 3) ? 2.0 * Gp[a * R + b] : Gp[a * R + b]) : 0.0;
   }
   for (int c = lane; c < nbuf * 8 * Zs; c += 32) zbase[c] = 0.0;   // padding columns stay 0
   __syncthreads();
@@ -89,14 +92,23 @@ leverage_mma_kernel(const double *__restrict__ U, int64_t n, int R, const double
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) a[ks] = zr[ks * 4 + quad];
     double msum = 0.0;
+    // two n-tiles at a time: two independent accumulator chains per warp (the mma of one
+    // chain issues while the other's result is in flight)
 #pragma unroll
-    for (int nt = 0; nt < Rn; nt += 8) {
-      double c0 = 0.0, c1 = 0.0;
+    for (int nt = 0; nt < Rn; nt += 16) {
+      double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks)
-        dmma_8x8x4(c0, c1, a[ks], G[(ks * 4 + quad) * Zs + nt + row]);
+      for (int ks = 0; ks < KS; ++ks) {   // (conditions resolved at compile time: unrolled)
+        if (ks * 4 < nt + 8) dmma_8x8x4(c0, c1, a[ks], G[(ks * 4 + quad) * Zs + nt + row]);
+        if (nt + 8 < Rn && ks * 4 < nt + 16)
+          dmma_8x8x4(d0, d1, a[ks], G[(ks * 4 + quad) * Zs + nt + 8 + row]);
+      }
       msum = fma(c0, zr[nt + 2 * quad], msum);
       msum = fma(c1, zr[nt + 2 * quad + 1], msum);
+      if (nt + 8 < Rn) {
+        msum = fma(d0, zr[nt + 8 + 2 * quad], msum);
+        msum = fma(d1, zr[nt + 8 + 2 * quad + 1], msum);
+      }
     }
     msum += __shfl_xor_sync(0xffffffffu, msum, 1);
     msum += __shfl_xor_sync(0xffffffffu, msum, 2);
