@@ -45,7 +45,8 @@ def main(path):
     mt = [(n, a) for n, a in agg.items() if any(n.startswith(m) or m in n for m in MTTKRP)]
     mt_t = sum(a[1] for _, a in mt)
     mt_b = sum(a[2] for _, a in mt)
-    walks = agg.get("walk_runs_kernel", [0])[0]
+    # (one launch per walk at R <= 64; above, an inner-levels launch and a leaf-level launch)
+    walks = sum(v[0] for k, v in agg.items() if k.startswith("walk_runs_kernel") and not k.endswith(", 2>"))
     solves = max(agg.get("lookup_kernel", [0])[0], 1)
     print("\nSampled-MTTKRP pipeline kernels (%s): %.1f µs, %.1f MB DRAM over %d solves -> "
           "%.1f MB DRAM traffic per rcp_sampled_mttkrp call." %
